@@ -1,0 +1,201 @@
+/*
+ * aknn.h -- C-ABI of libaknn.so, the B200 (sm_100a) hot path of the adaptive
+ * k-NN algorithm of LeJeune, Baraniuk & Heckel (arXiv 1902.09465).
+ *
+ * Citations: "P:<line>" = /root/reference/PAPER.md, "S:<line>" = SPEC.md.
+ * The readings of ambiguous passages (R1..R18) are listed in DESIGN.md §3.
+ *
+ * Problem (§3): given points X = {x_1..x_n} in R^m and a query x,
+ * return a set of size k+h that contains the k nearest neighbours of x in
+ * l2 distance.  Points and queries are uint8 vectors; one sampled squared
+ * coordinate difference is (a-b)^2/65025 in [0,1] (reading R2).
+ *
+ * Method (Algorithm 1, run under the batched round rule BR of
+ * DESIGN.md §2): per query, estimate D_i = (1/m)||x - x_i||^2
+ * by uniformly sampled coordinates with confidence radius
+ * alpha(T_i); split arms by rank into close / middle / far
+ * (P:144-146); stop when Eq. (5) holds; return the
+ * top k+h by estimate.
+ *
+ * Conventions for every entry point:
+ *   - All sizes are element counts.  Matrices are dense row-major with no
+ *     padding: points [n][d], queries [q][d], sets [q][k+h], counts [q][n].
+ *   - Buffers belong to the caller; the library never frees or retains a
+ *     caller pointer after the call returns.  An aknn_index owns a device
+ *     copy of X until aknn_free.
+ *   - Host variants take host pointers and are synchronous.  *_async
+ *     variants take DEVICE pointers and a cudaStream_t (as void*) and enqueue
+ *     their device work on that stream.
+ *   - On any status other than AKNN_OK no output is written, except
+ *     AKNN_EMAXROUNDS, which writes the state reached (see aknn_opts).
+ *     aknn_last_error() returns a thread-local message for the last failure.
+ *   - Not thread-safe per index: calls on one aknn_index must be serialised.
+ */
+#ifndef AKNN_H
+#define AKNN_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct aknn_index aknn_index; /* opaque; owns a device copy of X */
+
+typedef enum {
+  AKNN_OK = 0,
+  AKNN_EINVAL = -1,     /* argument outside the domain stated below              */
+  AKNN_ENOMEM = -2,     /* device or host allocation failed                      */
+  AKNN_ECUDA = -3,      /* a CUDA runtime call or kernel launch failed           */
+  AKNN_ENCCL = -4,      /* an NCCL call failed or timed out (sharded index)      */
+  AKNN_EMAXROUNDS = -5  /* aknn_opts.max_rounds reached before Eq. (5) held      */
+} aknn_status;
+
+/* Outputs of a query batch.  `sets` is required; every other field may be
+ * NULL to skip that output.  Host pointers for aknn_query[_ex], device
+ * pointers for aknn_query_async.                                            */
+typedef struct {
+  int32_t *sets;   /* [q][k+h] point ids of (1)..(k+h), rank order    */
+  double *dhat;    /* [q][k+h] fp64 estimates d_hat of those arms     */
+  int32_t *counts; /* [q][n_local] per-pair sample count T_i; T_i == d means
+                      the arm went exact                              */
+  int64_t *sums;   /* [q][n_local] exact integer S_i = sum of sampled (a-b)^2
+                      (or the exact sum once T_i == d); d_hat = S/(65025 T)   */
+  int64_t *evals;  /* [q] draws + d * (#exact fallbacks)          */
+  int64_t *draws;  /* [q] sampled coordinate draws, including initialisation  */
+  int32_t *rounds; /* [q] rounds of the batched rule until Eq. (5) held       */
+} aknn_result;
+
+/* Optional per-call settings; pass NULL for the defaults (all zero).        */
+typedef struct {
+  int32_t qi_offset;  /* RNG query index of queries[0] (default 0): query a uses
+                         counter word qi = qi_offset + a                      */
+  int32_t max_rounds; /* 0 = unlimited; otherwise stop after this many rounds
+                         and return AKNN_EMAXROUNDS with the state reached    */
+  int32_t timing;     /* 1 = time each kernel class with CUDA events on the
+                         launching stream and fill aknn_stats.ms_*           */
+  int32_t reserved;
+} aknn_opts;
+
+/* Execution statistics of the last query call on an index (aknn_get_stats). */
+typedef struct {
+  int32_t rounds;            /* host rounds executed (max over queries)        */
+  int32_t query_batches;     /* internal query sub-batches                     */
+  int64_t kernel_launches;   /* device kernels launched by the call            */
+  int64_t pairs;             /* q * n_local                                    */
+  int64_t draws;             /* total sampled draws (sum over queries)         */
+  int64_t exact_fallbacks;   /* total arms that went exact                     */
+  int64_t active_pair_rounds;/* sum over rounds of advanced pairs              */
+  double ms_total;           /* device time of the whole call (timing=1)       */
+  double ms_init;            /* initialisation gather (a2)                     */
+  double ms_select;          /* rank split + bounds + Eq. (5) (a5-a7)          */
+  double ms_filter;          /* blocker filter + compaction (a8)               */
+  double ms_advance;         /* level gathers + exact fallbacks (a3, a4)       */
+  double ms_output;          /* output assembly (a9)                           */
+  int64_t advance_launches;  /* launches of the advance (gather) kernel        */
+} aknn_stats;
+
+/* ------------------------------------------------------------------------ */
+/* Index construction.                                                       */
+/* ------------------------------------------------------------------------ */
+
+/* Copy points (host, uint8 [n][d]) to the current CUDA device.
+ * Domain: n >= 2, 1 <= d <= 33025 (so that d * 255^2 < 2^31), n < 2^31.
+ * The caller may free `points` on return.                                   */
+aknn_status aknn_build(const uint8_t *points, int64_t n, int32_t d, aknn_index **out);
+
+/* Same, from a DEVICE buffer, copied on `cuda_stream` (the index keeps its own
+ * copy; the caller's buffer may be freed after the stream completes).       */
+aknn_status aknn_build_async(const uint8_t *points_dev, int64_t n, int32_t d,
+                             void *cuda_stream, aknn_index **out);
+
+/* Sharded index: this process holds rows
+ * [offset, offset + n_local) of an n_global-point set.  Point ids in the RNG
+ * counter and in the returned sets are global ids.  `nccl_unique_id` points
+ * to an ncclUniqueId (128 bytes) shared by the `world` ranks (rank 0 creates
+ * it with aknn_nccl_unique_id and broadcasts it out of band).  With
+ * world == 1 no communicator is created.                                    */
+aknn_status aknn_build_shard(const uint8_t *shard, int64_t n_local, int64_t n_global,
+                             int64_t offset, int32_t d, const void *nccl_unique_id,
+                             int32_t rank, int32_t world, aknn_index **out);
+
+/* Write a fresh ncclUniqueId (128 bytes) to `id_out`.                       */
+aknn_status aknn_nccl_unique_id(void *id_out);
+
+/* ------------------------------------------------------------------------ */
+/* The adaptive query (the hot path).                                        */
+/* ------------------------------------------------------------------------ */
+
+/* Run the batched round rule for q queries (host uint8 [q][d]).
+ * k >= 1, h >= 0, k + h < n_global; delta in (0,1); seed = the 64-bit Philox
+ * key (low word = key[0]).  alpha: host fp64 [d+1], alpha[u] for 1 <= u < d
+ * (alpha[0] and alpha[d] are ignored; an exact arm has alpha 0); NULL
+ * selects the footnote-2 table of (n_global, delta) built by
+ * aknn_alpha_table (EINVAL when delta/n_global >= 1/e).
+ * Results are bit-identical to the oracle's for the same inputs.            */
+aknn_status aknn_query(const aknn_index *ix, const uint8_t *queries, int32_t q, int32_t k,
+                       int32_t h, double delta, uint64_t seed, const double *alpha,
+                       aknn_result *out);
+
+/* aknn_query with options (NULL = defaults).                                */
+aknn_status aknn_query_ex(const aknn_index *ix, const uint8_t *queries, int32_t q, int32_t k,
+                          int32_t h, double delta, uint64_t seed, const double *alpha,
+                          const aknn_opts *opts, aknn_result *out);
+
+/* Device-pointer variant: queries_dev uint8 [q][d], alpha_dev fp64 [d+1]
+ * (NULL = footnote-2 table), outputs in `out` are device pointers.  All work
+ * is enqueued on `cuda_stream`.  The round loop needs one 4-byte device->host
+ * read of the active-query count per round, so the call returns after the
+ * loop has finished on the device; outputs are complete when the stream is.  */
+aknn_status aknn_query_async(const aknn_index *ix, const uint8_t *queries_dev, int32_t q,
+                             int32_t k, int32_t h, double delta, uint64_t seed,
+                             const double *alpha_dev, const aknn_opts *opts,
+                             aknn_result *out, void *cuda_stream);
+
+/* Statistics of the last aknn_query* call on `ix`.                          */
+aknn_status aknn_get_stats(const aknn_index *ix, aknn_stats *out);
+
+/* ------------------------------------------------------------------------ */
+/* Exact comparison pass (P:98 brute force): all distances, then top-k.      */
+/* ------------------------------------------------------------------------ */
+
+/* For each of q host queries: the k nearest points by the exact integer
+ * distance sum_j (a_j - b_j)^2, ties to the smaller id; idx/dist2 host
+ * [q][k] in ascending (dist2, id) order.  1 <= k <= min(n_local, 1024).
+ * Computed as ||x'||^2 + ||q'||^2 - 2 x'.q' with x' = x - 128 (int8) on the
+ * tensor cores (int8 -> int32), exact for d <= 33025.                        */
+aknn_status aknn_exact(const aknn_index *ix, const uint8_t *queries, int32_t q, int32_t k,
+                       int32_t *idx, int32_t *dist2);
+
+/* Device-pointer variant on `cuda_stream`.                                   */
+aknn_status aknn_exact_async(const aknn_index *ix, const uint8_t *queries_dev, int32_t q,
+                             int32_t k, int32_t *idx_dev, int32_t *dist2_dev,
+                             void *cuda_stream);
+
+/* ------------------------------------------------------------------------ */
+/* Confidence radius tables (host).                                           */
+/* ------------------------------------------------------------------------ */
+
+/* kind 0 = footnote 2: alpha(u) = sqrt(2 beta(u, delta/n)/u),
+ *          beta = log(1/d') + 3 log log(1/d') + 1.5 log(1 + log u); needs
+ *          delta/n < 1/e.
+ * kind 1 = §5: alpha(u) = sqrt(c_alpha log(1 + (1 + log u) n/delta)/u).
+ * Writes alpha_out[0..d]; alpha_out[0] = alpha_out[d] = 0.                  */
+aknn_status aknn_alpha_table(int32_t kind, int64_t n, double delta, double c_alpha, int32_t d,
+                             double *alpha_out);
+
+/* ------------------------------------------------------------------------ */
+/* Housekeeping.                                                             */
+/* ------------------------------------------------------------------------ */
+
+int64_t aknn_index_n_local(const aknn_index *ix);
+int64_t aknn_index_n_global(const aknn_index *ix);
+int32_t aknn_index_dim(const aknn_index *ix);
+void aknn_free(aknn_index *ix);
+const char *aknn_strerror(aknn_status s);
+const char *aknn_last_error(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* AKNN_H */

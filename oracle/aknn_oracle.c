@@ -324,7 +324,7 @@ int orc_query_br(const uint8_t *X, int64_t n, int32_t d, const uint8_t *Qrows, i
     free(S); free(T); free(order); free(act);
     return ORC_ENOMEM;
   }
-  int status = ORC_OK;
+  int status = ORC_OK, hit_max = 0;
   for (int32_t a = 0; a < q; ++a) {
     const uint8_t *x = Qrows + (size_t)a * d;
     const uint32_t qi = (uint32_t)qids[a];
@@ -376,10 +376,14 @@ int orc_query_br(const uint8_t *X, int64_t n, int32_t d, const uint8_t *Qrows, i
     if (draws) draws[a] = ndraws;
     if (evals) evals[a] = ndraws + (int64_t)d * nexact;
     if (rounds) rounds[a] = r;
+    if (status == ORC_EMAXROUNDS) {  /* every query still runs to its own cap */
+      hit_max = 1;
+      status = ORC_OK;
+    }
     if (status != ORC_OK) break;
   }
   free(S); free(T); free(order); free(act);
-  return status;
+  return status != ORC_OK ? status : (hit_max ? ORC_EMAXROUNDS : ORC_OK);
 }
 
 /* ------------------------------------------------------------------------ */

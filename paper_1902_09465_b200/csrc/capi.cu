@@ -1,0 +1,673 @@
+// capi.cu -- the C-ABI of libaknn.so (include/aknn.h) and the host round
+// driver of the batched round rule.
+//
+// The driver owns: the device copy of X (row pitch padded to 16 B, zero
+// filled), a workspace sized for one query sub-batch, and one CUDA stream.
+// Per sub-batch: k_init, then rounds of {k_select -> 4-byte D2H of the
+// active-query count -> k_filter/k_plan/k_scatter -> k_advance}, then
+// k_output.  Every device step is a kernel of round_kernels.cu; the host
+// only sequences launches and validates arguments.
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "../../include/aknn.h"
+#include "internal.cuh"
+#include "launch.h"
+
+#ifdef AKNN_WITH_NCCL
+#include <nccl.h>
+#endif
+
+using namespace aknn;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+aknn_status fail(aknn_status s, const char *fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return s;
+}
+
+#define CU(call)                                                                          \
+  do {                                                                                    \
+    cudaError_t e_ = (call);                                                              \
+    if (e_ != cudaSuccess)                                                                \
+      return fail(e_ == cudaErrorMemoryAllocation ? AKNN_ENOMEM : AKNN_ECUDA, "%s: %s (%s:%d)", \
+                  #call, cudaGetErrorString(e_), __FILE__, __LINE__);                     \
+  } while (0)
+
+#define TRY(call)                       \
+  do {                                  \
+    aknn_status s_ = (call);            \
+    if (s_ != AKNN_OK) return s_;       \
+  } while (0)
+
+int64_t round_up(int64_t a, int64_t b) { return (a + b - 1) / b * b; }
+
+int bit_length(unsigned long long v) {
+  int b = 0;
+  while (v) {
+    ++b;
+    v >>= 1;
+  }
+  return b;
+}
+
+unsigned long long gcd_u64(unsigned long long a, unsigned long long b) {
+  while (b) {
+    const unsigned long long t = a % b;
+    a = b;
+    b = t;
+  }
+  return a;
+}
+
+struct DevBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+  aknn_status ensure(size_t want) {
+    if (bytes >= want) return AKNN_OK;
+    if (p) cudaFree(p);
+    p = nullptr;
+    bytes = 0;
+    cudaError_t e = cudaMalloc(&p, want);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      return fail(AKNN_ENOMEM, "cudaMalloc(%zu): %s", want, cudaGetErrorString(e));
+    }
+    bytes = want;
+    return AKNN_OK;
+  }
+  template <class T>
+  T *as(size_t byte_off = 0) const {
+    return reinterpret_cast<T *>(static_cast<char *>(p) + byte_off);
+  }
+};
+
+}  // namespace
+
+struct aknn_index {
+  int device = 0;
+  int num_sms = 148;
+  int64_t n_local = 0, n_global = 0, offset = 0;
+  int32_t d = 0;
+  int64_t pitch = 0;
+  DevBuf X;                // [n_local][pitch]
+  cudaStream_t stream = nullptr;
+  DevBuf ws;               // round workspace
+  DevBuf qbuf;             // padded query staging
+  DevBuf alpha;            // [d+1]
+  DevBuf outs;             // device outputs for the host API
+  DevBuf exact_ws;
+  int rank = 0, world = 1;
+#ifdef AKNN_WITH_NCCL
+  ncclComm_t comm = nullptr;
+#endif
+  aknn_stats stats{};
+};
+
+namespace {
+
+aknn_status validate_build(int64_t n, int32_t d) {
+  if (n < 2 || n >= (1ll << 31)) return fail(AKNN_EINVAL, "n=%lld outside [2, 2^31)", (long long)n);
+  if (d < 1 || d > 33025) return fail(AKNN_EINVAL, "d=%d outside [1, 33025]", d);
+  return AKNN_OK;
+}
+
+aknn_status make_index(int64_t n_local, int64_t n_global, int64_t offset, int32_t d,
+                       aknn_index **out) {
+  aknn_index *ix = new (std::nothrow) aknn_index();
+  if (!ix) return fail(AKNN_ENOMEM, "host allocation failed");
+  ix->n_local = n_local;
+  ix->n_global = n_global;
+  ix->offset = offset;
+  ix->d = d;
+  ix->pitch = round_up(d, 16);
+  cudaError_t e = cudaGetDevice(&ix->device);
+  if (e == cudaSuccess) e = cudaDeviceGetAttribute(&ix->num_sms, cudaDevAttrMultiProcessorCount, ix->device);
+  if (e == cudaSuccess) e = cudaStreamCreateWithFlags(&ix->stream, cudaStreamNonBlocking);
+  if (e != cudaSuccess) {
+    delete ix;
+    return fail(AKNN_ECUDA, "CUDA device setup failed: %s", cudaGetErrorString(e));
+  }
+  aknn_status s = ix->X.ensure((size_t)n_local * ix->pitch);
+  if (s != AKNN_OK) {
+    cudaStreamDestroy(ix->stream);
+    delete ix;
+    return s;
+  }
+  *out = ix;
+  return AKNN_OK;
+}
+
+// Builds the level geometry of the composite key (R9).
+struct KeyGeom {
+  unsigned long long L, Ld;
+  int cmax, ibits, nbits;
+};
+
+aknn_status key_geom(int64_t n_local, int32_t d, KeyGeom *kg) {
+  int cmax = 0;
+  while (d >= 2 && (1ll << (cmax + 1)) < d) ++cmax;  // largest c with 2^c < d
+  const unsigned long long p2 = 1ull << cmax;
+  const unsigned long long L = p2 / gcd_u64(p2, (unsigned long long)d) * (unsigned long long)d;
+  kg->L = L;
+  kg->Ld = L / (unsigned long long)d;
+  kg->cmax = cmax;
+  kg->ibits = bit_length((unsigned long long)(n_local - 1));
+  if (kg->ibits < 1) kg->ibits = 1;
+  kg->nbits = bit_length(65025ull * L) + kg->ibits;
+  if (kg->nbits > 63)
+    return fail(AKNN_EINVAL, "composite key needs %d bits (> 63) for n=%lld, d=%d", kg->nbits,
+                (long long)n_local, d);
+  return AKNN_OK;
+}
+
+aknn_status host_alpha_table(int kind, int64_t n, double delta, double c_alpha, int32_t d,
+                             double *a) {
+  if (n < 1 || d < 1 || !(delta > 0.0 && delta < 1.0))
+    return fail(AKNN_EINVAL, "alpha table: need n >= 1, d >= 1, delta in (0,1)");
+  a[0] = 0.0;
+  a[d] = 0.0;
+  if (kind == 0) {
+    // footnote 2
+    const double inv = (double)n / delta;  // 1 / delta'
+    const double lg = std::log(inv);
+    if (!(lg > 1.0)) return fail(AKNN_EINVAL, "footnote-2 alpha needs delta/n < 1/e");
+    const double base = lg + 3.0 * std::log(lg);
+    for (int32_t u = 1; u < d; ++u) {
+      const double beta = base + 1.5 * std::log(1.0 + std::log((double)u));
+      a[u] = std::sqrt(2.0 * beta / (double)u);
+    }
+    return AKNN_OK;
+  }
+  if (kind == 1) {
+    // §5
+    if (!(c_alpha > 0.0)) return fail(AKNN_EINVAL, "c_alpha must be > 0");
+    for (int32_t u = 1; u < d; ++u)
+      a[u] = std::sqrt(c_alpha * std::log(1.0 + (1.0 + std::log((double)u)) * (double)n / delta) / (double)u);
+    return AKNN_OK;
+  }
+  return fail(AKNN_EINVAL, "alpha kind %d unknown (0 = footnote 2, 1 = section 5)", kind);
+}
+
+struct Timer {
+  bool on;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr, b = nullptr;
+  Timer(bool on_, cudaStream_t s_) : on(on_), s(s_) {
+    if (on) {
+      cudaEventCreate(&a);
+      cudaEventCreate(&b);
+    }
+  }
+  ~Timer() {
+    if (a) cudaEventDestroy(a);
+    if (b) cudaEventDestroy(b);
+  }
+  void start() {
+    if (on) cudaEventRecord(a, s);
+  }
+  // accumulate after the stream has been synchronised past `b`
+  void stop() {
+    if (on) cudaEventRecord(b, s);
+  }
+  double ms() {
+    if (!on) return 0.0;
+    float m = 0.f;
+    cudaEventSynchronize(b);
+    cudaEventElapsedTime(&m, a, b);
+    return m;
+  }
+};
+
+// Runs the whole query on device pointers.  Q rows have stride `qstride`
+// bytes in `queries_dev` (device).  Outputs are device pointers.
+aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstride, int32_t q,
+                      int32_t k, int32_t h, uint64_t seed, const double *alpha_dev,
+                      const aknn_opts *opts, const aknn_result *out, cudaStream_t st) {
+  const int64_t n = ix->n_local;
+  const int32_t d = ix->d;
+  KeyGeom kg;
+  TRY(key_geom(n, d, &kg));
+  if (k + h > output_max_kh())
+    return fail(AKNN_EINVAL, "k+h=%d exceeds the supported %d", k + h, output_max_kh());
+  const aknn_opts o = opts ? *opts : aknn_opts{};
+  const int64_t npad = round_up(n, 16);
+  // sub-batch size: the code (qi << ibits | i) must fit 32 bits; the
+  // workspace (S 4 B + lvl 1 B + act 1 B + list 4 B per pair) fits in memory.
+  int64_t qb = q;
+  const int64_t code_cap = 1ll << (32 - kg.ibits);
+  if (qb > code_cap) qb = code_cap;
+  size_t free_b = 0, total_b = 0;
+  CU(cudaMemGetInfo(&free_b, &total_b));
+  const size_t per_q = (size_t)npad * 10 + ix->pitch + sizeof(QState) + 64;
+  const size_t budget = (size_t)(0.6 * (double)(free_b + ix->ws.bytes));
+  if ((size_t)qb * per_q > budget) qb = (int64_t)(budget / per_q);
+  if (qb < 1) return fail(AKNN_ENOMEM, "not enough device memory for one query row");
+  // workspace layout
+  const size_t szS = (size_t)qb * npad * 4, szL = (size_t)qb * npad, szA = szL,
+               szList = (size_t)qb * npad * 4, szQ = (size_t)qb * ix->pitch,
+               szQS = (size_t)qb * sizeof(QState), szCtl = sizeof(RoundCtl);
+  size_t off = 0;
+  const size_t oS = off; off = round_up(off + szS, 256);
+  const size_t oL = off; off = round_up(off + szL, 256);
+  const size_t oA = off; off = round_up(off + szA, 256);
+  const size_t oList = off; off = round_up(off + szList, 256);
+  const size_t oQ = off; off = round_up(off + szQ, 256);
+  const size_t oQS = off; off = round_up(off + szQS, 256);
+  const size_t oCtl = off; off = round_up(off + szCtl, 256);
+  TRY(ix->ws.ensure(off));
+
+  Geom g{};
+  g.X = ix->X.as<uint8_t>();
+  g.Q = ix->ws.as<uint8_t>(oQ);
+  g.alpha = alpha_dev;
+  g.S = ix->ws.as<int32_t>(oS);
+  g.lvl = ix->ws.as<uint8_t>(oL);
+  g.act = ix->ws.as<uint8_t>(oA);
+  g.list = ix->ws.as<uint32_t>(oList);
+  g.qs = ix->ws.as<QState>(oQS);
+  g.ctl = ix->ws.as<RoundCtl>(oCtl);
+  g.pitch = ix->pitch;
+  g.npad = npad;
+  g.n = (int)n;
+  g.d = d;
+  g.k = k;
+  g.h = h;
+  g.id_offset = (uint32_t)ix->offset;
+  g.seed_lo = (uint32_t)(seed & 0xffffffffu);
+  g.seed_hi = (uint32_t)(seed >> 32);
+  g.L = kg.L;
+  g.Ld = kg.Ld;
+  g.ibits = kg.ibits;
+  g.cmax = kg.cmax;
+
+  aknn_stats stats{};
+  stats.pairs = (int64_t)q * n;
+  const bool timing = o.timing != 0;
+  Timer t_all(timing, st), t_ph(timing, st);
+  t_all.start();
+  unsigned int *h_active = nullptr;
+  CU(cudaMallocHost(&h_active, sizeof(unsigned int)));
+  struct HostFree {
+    unsigned int *p;
+    ~HostFree() { cudaFreeHost(p); }
+  } hf{h_active};
+  aknn_status status = AKNN_OK;
+  for (int64_t r0 = 0; r0 < q; r0 += qb) {
+    const int qn = (int)std::min<int64_t>(qb, q - r0);
+    g.q = qn;
+    g.qi0 = (uint32_t)(o.qi_offset + r0);
+    ++stats.query_batches;
+    // stage queries into the zero-padded pitch layout
+    CU(cudaMemsetAsync(ix->ws.as<uint8_t>(oQ), 0, szQ, st));
+    CU(cudaMemcpy2DAsync(ix->ws.as<uint8_t>(oQ), ix->pitch, queries_dev + r0 * qstride, qstride, d,
+                         qn, cudaMemcpyDeviceToDevice, st));
+    CU(cudaMemsetAsync(g.ctl, 0, sizeof(RoundCtl), st));
+    t_ph.start();
+    CU(launch_init(g, st));
+    t_ph.stop();
+    stats.kernel_launches += 2;
+    stats.ms_init += t_ph.ms();
+    int r = 0;
+    for (;;) {
+      ++r;
+      // zero the per-round counters (everything but the cumulative `advanced`)
+      CU(cudaMemsetAsync(g.ctl, 0, offsetof(RoundCtl, advanced), st));
+      t_ph.start();
+      CU(launch_select(g, kg.nbits, st));
+      t_ph.stop();
+      ++stats.kernel_launches;
+      CU(cudaMemcpyAsync(h_active, &g.ctl->n_active, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      stats.ms_select += t_ph.ms();
+      if (*h_active == 0) break;
+      if (o.max_rounds > 0 && r >= o.max_rounds) {
+        status = AKNN_EMAXROUNDS;
+        break;
+      }
+      t_ph.start();
+      CU(launch_filter(g, st));
+      t_ph.stop();
+      stats.kernel_launches += 3;
+      const double mf = t_ph.ms();
+      stats.ms_filter += mf;
+      t_ph.start();
+      CU(launch_advance(g, ix->num_sms, st));
+      t_ph.stop();
+      stats.kernel_launches += 1;
+      stats.advance_launches += 1;
+      stats.ms_advance += t_ph.ms();
+      if (r > 1 + 64 * 64) return fail(AKNN_ECUDA, "round loop did not terminate (internal error)");
+    }
+    if (r > stats.rounds) stats.rounds = r;
+    OutPtrs op{(int)r0, out->sets, out->dhat, out->counts, out->sums, out->evals, out->draws, out->rounds};
+    t_ph.start();
+    CU(launch_output(g, op, st));
+    t_ph.stop();
+    stats.kernel_launches += (out->counts || out->sums) ? 2 : 1;
+    RoundCtl ctl_h;
+    CU(cudaMemcpyAsync(&ctl_h, g.ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    stats.ms_output += t_ph.ms();
+    stats.active_pair_rounds += (int64_t)ctl_h.advanced;
+    // totals from the per-query state
+    std::vector<QState> qs(qn);
+    CU(cudaMemcpy(qs.data(), g.qs, sizeof(QState) * qn, cudaMemcpyDeviceToHost));
+    for (const QState &s : qs) {
+      stats.draws += s.draws;
+      stats.exact_fallbacks += s.nexact;
+    }
+    if (status != AKNN_OK) break;
+  }
+  t_all.stop();
+  stats.ms_total = t_all.ms();
+  ix->stats = stats;
+  CU(cudaGetLastError());
+  return status;
+}
+
+aknn_status check_query_args(const aknn_index *ix, int32_t q, int32_t k, int32_t h, double delta,
+                             const aknn_result *out) {
+  if (!ix) return fail(AKNN_EINVAL, "index is NULL");
+  if (!out || !out->sets) return fail(AKNN_EINVAL, "out->sets is required");
+  if (q < 0) return fail(AKNN_EINVAL, "q=%d < 0", q);
+  if (k < 1 || h < 0) return fail(AKNN_EINVAL, "need k >= 1 and h >= 0 (k=%d, h=%d)", k, h);
+  if ((int64_t)k + h >= ix->n_global)
+    return fail(AKNN_EINVAL, "k+h=%d must be < n=%lld (DESIGN.md R13)", k + h, (long long)ix->n_global);
+  if ((int64_t)k + h >= ix->n_local)
+    return fail(AKNN_EINVAL, "k+h=%d must be < n_local=%lld", k + h, (long long)ix->n_local);
+  if (!(delta > 0.0 && delta < 1.0)) return fail(AKNN_EINVAL, "delta=%g outside (0,1)", delta);
+  return AKNN_OK;
+}
+
+}  // namespace
+
+// ===========================================================================
+extern "C" {
+
+aknn_status aknn_build(const uint8_t *points, int64_t n, int32_t d, aknn_index **out) {
+  if (!points || !out) return fail(AKNN_EINVAL, "NULL argument");
+  TRY(validate_build(n, d));
+  aknn_index *ix = nullptr;
+  TRY(make_index(n, n, 0, d, &ix));
+  cudaError_t e = cudaMemsetAsync(ix->X.p, 0, ix->X.bytes, ix->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(ix->X.p, ix->pitch, points, d, d, n, cudaMemcpyHostToDevice, ix->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ix->stream);
+  if (e != cudaSuccess) {
+    aknn_free(ix);
+    return fail(AKNN_ECUDA, "copying points: %s", cudaGetErrorString(e));
+  }
+  *out = ix;
+  return AKNN_OK;
+}
+
+aknn_status aknn_build_async(const uint8_t *points_dev, int64_t n, int32_t d, void *cuda_stream,
+                             aknn_index **out) {
+  if (!points_dev || !out) return fail(AKNN_EINVAL, "NULL argument");
+  TRY(validate_build(n, d));
+  aknn_index *ix = nullptr;
+  TRY(make_index(n, n, 0, d, &ix));
+  cudaStream_t s = (cudaStream_t)cuda_stream;
+  cudaError_t e = cudaMemsetAsync(ix->X.p, 0, ix->X.bytes, s);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(ix->X.p, ix->pitch, points_dev, d, d, n, cudaMemcpyDeviceToDevice, s);
+  if (e != cudaSuccess) {
+    aknn_free(ix);
+    return fail(AKNN_ECUDA, "copying points: %s", cudaGetErrorString(e));
+  }
+  *out = ix;
+  return AKNN_OK;
+}
+
+aknn_status aknn_nccl_unique_id(void *id_out) {
+  if (!id_out) return fail(AKNN_EINVAL, "NULL argument");
+#ifdef AKNN_WITH_NCCL
+  ncclUniqueId id;
+  if (ncclGetUniqueId(&id) != ncclSuccess) return fail(AKNN_ENCCL, "ncclGetUniqueId failed");
+  memcpy(id_out, &id, sizeof id);
+  return AKNN_OK;
+#else
+  return fail(AKNN_ENCCL, "libaknn was built without NCCL");
+#endif
+}
+
+aknn_status aknn_build_shard(const uint8_t *shard, int64_t n_local, int64_t n_global, int64_t offset,
+                             int32_t d, const void *nccl_unique_id, int32_t rank, int32_t world,
+                             aknn_index **out) {
+  if (!shard || !out) return fail(AKNN_EINVAL, "NULL argument");
+  TRY(validate_build(n_local, d));
+  if (n_global < n_local || offset < 0 || offset + n_local > n_global || n_global >= (1ll << 31))
+    return fail(AKNN_EINVAL, "shard [%lld, %lld) outside [0, %lld)", (long long)offset,
+                (long long)(offset + n_local), (long long)n_global);
+  if (world < 1 || rank < 0 || rank >= world) return fail(AKNN_EINVAL, "rank %d of %d", rank, world);
+  if (world > 1) {
+#ifndef AKNN_WITH_NCCL
+    return fail(AKNN_ENCCL, "sharded query across %d ranks needs NCCL (not built in)", world);
+#endif
+  }
+  aknn_index *ix = nullptr;
+  TRY(make_index(n_local, n_global, offset, d, &ix));
+  ix->rank = rank;
+  ix->world = world;
+  cudaError_t e = cudaMemsetAsync(ix->X.p, 0, ix->X.bytes, ix->stream);
+  if (e == cudaSuccess)
+    e = cudaMemcpy2DAsync(ix->X.p, ix->pitch, shard, d, d, n_local, cudaMemcpyHostToDevice, ix->stream);
+  if (e == cudaSuccess) e = cudaStreamSynchronize(ix->stream);
+  if (e != cudaSuccess) {
+    aknn_free(ix);
+    return fail(AKNN_ECUDA, "copying shard: %s", cudaGetErrorString(e));
+  }
+#ifdef AKNN_WITH_NCCL
+  if (world > 1) {
+    ncclUniqueId id;
+    memcpy(&id, nccl_unique_id, sizeof id);
+    if (ncclCommInitRank(&ix->comm, world, id, rank) != ncclSuccess) {
+      aknn_free(ix);
+      return fail(AKNN_ENCCL, "ncclCommInitRank failed");
+    }
+  }
+#else
+  (void)nccl_unique_id;
+#endif
+  *out = ix;
+  return AKNN_OK;
+}
+
+aknn_status aknn_alpha_table(int32_t kind, int64_t n, double delta, double c_alpha, int32_t d,
+                             double *alpha_out) {
+  if (!alpha_out) return fail(AKNN_EINVAL, "NULL argument");
+  return host_alpha_table(kind, n, delta, c_alpha, d, alpha_out);
+}
+
+aknn_status aknn_query_async(const aknn_index *cix, const uint8_t *queries_dev, int32_t q, int32_t k,
+                             int32_t h, double delta, uint64_t seed, const double *alpha_dev,
+                             const aknn_opts *opts, aknn_result *out, void *cuda_stream) {
+  aknn_index *ix = const_cast<aknn_index *>(cix);
+  TRY(check_query_args(ix, q, k, h, delta, out));
+  if (q > 0 && !queries_dev) return fail(AKNN_EINVAL, "queries is NULL");
+  if (ix->world > 1) return fail(AKNN_EINVAL, "sharded query not implemented in this build");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const double *al = alpha_dev;
+  if (!al) {
+    std::vector<double> a(ix->d + 1);
+    TRY(host_alpha_table(0, ix->n_global, delta, 0.0, ix->d, a.data()));
+    TRY(ix->alpha.ensure(sizeof(double) * (ix->d + 1)));
+    CU(cudaMemcpyAsync(ix->alpha.p, a.data(), sizeof(double) * (ix->d + 1), cudaMemcpyHostToDevice, st));
+    CU(cudaStreamSynchronize(st));
+    al = ix->alpha.as<double>();
+  }
+  if (q == 0) return AKNN_OK;
+  return run_query(ix, queries_dev, ix->d, q, k, h, seed, al, opts, out, st);
+}
+
+aknn_status aknn_query_ex(const aknn_index *cix, const uint8_t *queries, int32_t q, int32_t k,
+                          int32_t h, double delta, uint64_t seed, const double *alpha,
+                          const aknn_opts *opts, aknn_result *out) {
+  aknn_index *ix = const_cast<aknn_index *>(cix);
+  TRY(check_query_args(ix, q, k, h, delta, out));
+  if (q > 0 && !queries) return fail(AKNN_EINVAL, "queries is NULL");
+  if (ix->world > 1) return fail(AKNN_EINVAL, "sharded query not implemented in this build");
+  if (q == 0) return AKNN_OK;
+  cudaStream_t st = ix->stream;
+  const int32_t d = ix->d;
+  const int64_t n = ix->n_local;
+  const int kh = k + h;
+  // alpha
+  std::vector<double> a(d + 1);
+  if (alpha) {
+    memcpy(a.data(), alpha, sizeof(double) * (d + 1));
+  } else {
+    TRY(host_alpha_table(0, ix->n_global, delta, 0.0, d, a.data()));
+  }
+  // device staging: alpha | queries | outputs
+  const size_t szA = sizeof(double) * (d + 1), szQ = (size_t)q * d;
+  const size_t szSets = (size_t)q * kh * 4, szDhat = out->dhat ? (size_t)q * kh * 8 : 0,
+               szCnt = out->counts ? (size_t)q * n * 4 : 0, szSum = out->sums ? (size_t)q * n * 8 : 0,
+               szEv = (size_t)q * 8, szDr = (size_t)q * 8, szRo = (size_t)q * 4;
+  size_t off = 0;
+  const size_t oA = off; off = round_up(off + szA, 256);
+  const size_t oQ = off; off = round_up(off + szQ, 256);
+  const size_t oSets = off; off = round_up(off + szSets, 256);
+  const size_t oDhat = off; off = round_up(off + szDhat, 256);
+  const size_t oCnt = off; off = round_up(off + szCnt, 256);
+  const size_t oSum = off; off = round_up(off + szSum, 256);
+  const size_t oEv = off; off = round_up(off + szEv, 256);
+  const size_t oDr = off; off = round_up(off + szDr, 256);
+  const size_t oRo = off; off = round_up(off + szRo, 256);
+  TRY(ix->outs.ensure(off));
+  CU(cudaMemcpyAsync(ix->outs.as<char>(oA), a.data(), szA, cudaMemcpyHostToDevice, st));
+  CU(cudaMemcpyAsync(ix->outs.as<char>(oQ), queries, szQ, cudaMemcpyHostToDevice, st));
+  aknn_result dout{ix->outs.as<int32_t>(oSets), out->dhat ? ix->outs.as<double>(oDhat) : nullptr,
+                   out->counts ? ix->outs.as<int32_t>(oCnt) : nullptr,
+                   out->sums ? ix->outs.as<int64_t>(oSum) : nullptr, ix->outs.as<int64_t>(oEv),
+                   ix->outs.as<int64_t>(oDr), ix->outs.as<int32_t>(oRo)};
+  aknn_status s = run_query(ix, ix->outs.as<uint8_t>(oQ), d, q, k, h, seed, ix->outs.as<double>(oA),
+                            opts, &dout, st);
+  if (s != AKNN_OK && s != AKNN_EMAXROUNDS) return s;
+  CU(cudaMemcpyAsync(out->sets, dout.sets, szSets, cudaMemcpyDeviceToHost, st));
+  if (out->dhat) CU(cudaMemcpyAsync(out->dhat, dout.dhat, szDhat, cudaMemcpyDeviceToHost, st));
+  if (out->counts) CU(cudaMemcpyAsync(out->counts, dout.counts, szCnt, cudaMemcpyDeviceToHost, st));
+  if (out->sums) CU(cudaMemcpyAsync(out->sums, dout.sums, szSum, cudaMemcpyDeviceToHost, st));
+  if (out->evals) CU(cudaMemcpyAsync(out->evals, dout.evals, szEv, cudaMemcpyDeviceToHost, st));
+  if (out->draws) CU(cudaMemcpyAsync(out->draws, dout.draws, szDr, cudaMemcpyDeviceToHost, st));
+  if (out->rounds) CU(cudaMemcpyAsync(out->rounds, dout.rounds, szRo, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return s;
+}
+
+aknn_status aknn_query(const aknn_index *ix, const uint8_t *queries, int32_t q, int32_t k, int32_t h,
+                       double delta, uint64_t seed, const double *alpha, aknn_result *out) {
+  return aknn_query_ex(ix, queries, q, k, h, delta, seed, alpha, nullptr, out);
+}
+
+aknn_status aknn_get_stats(const aknn_index *ix, aknn_stats *out) {
+  if (!ix || !out) return fail(AKNN_EINVAL, "NULL argument");
+  *out = ix->stats;
+  return AKNN_OK;
+}
+
+aknn_status aknn_exact_async(const aknn_index *cix, const uint8_t *queries_dev, int32_t q, int32_t k,
+                             int32_t *idx_dev, int32_t *dist2_dev, void *cuda_stream) {
+  aknn_index *ix = const_cast<aknn_index *>(cix);
+  if (!ix || !idx_dev || !dist2_dev) return fail(AKNN_EINVAL, "NULL argument");
+  if (q < 0 || k < 1 || k > ix->n_local || k > 1024)
+    return fail(AKNN_EINVAL, "need q >= 0 and 1 <= k <= min(n_local, 1024) (k=%d)", k);
+  if (q == 0) return AKNN_OK;
+  if (!queries_dev) return fail(AKNN_EINVAL, "queries is NULL");
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const int64_t n = ix->n_local, npad = round_up(n, 16);
+  ExactGeom e{};
+  e.ibits = std::max(1, bit_length((unsigned long long)(n - 1)));
+  e.nbits = bit_length(65025ull * (unsigned long long)ix->d) + e.ibits;
+  if (e.nbits > 63) return fail(AKNN_EINVAL, "exact key needs %d bits", e.nbits);
+  // process queries in chunks so the distance scratch stays bounded
+  const int64_t qc = std::max<int64_t>(1, std::min<int64_t>(q, (int64_t)(2ll << 30) / (npad * 4)));
+  const size_t szD = (size_t)qc * npad * 4, szQ = (size_t)qc * ix->pitch;
+  TRY(ix->exact_ws.ensure(round_up(szD, 256) + szQ));
+  for (int64_t r0 = 0; r0 < q; r0 += qc) {
+    const int qn = (int)std::min<int64_t>(qc, q - r0);
+    uint8_t *qpad = ix->exact_ws.as<uint8_t>(round_up(szD, 256));
+    CU(cudaMemsetAsync(qpad, 0, szQ, st));
+    CU(cudaMemcpy2DAsync(qpad, ix->pitch, queries_dev + r0 * ix->d, ix->d, ix->d, qn,
+                         cudaMemcpyDeviceToDevice, st));
+    e.X = ix->X.as<uint8_t>();
+    e.Q = qpad;
+    e.pitch = ix->pitch;
+    e.n = (int)n;
+    e.d = ix->d;
+    e.q = qn;
+    e.k = k;
+    e.id_offset = (uint32_t)ix->offset;
+    e.D = ix->exact_ws.as<int32_t>();
+    e.npad = npad;
+    e.idx = idx_dev + r0 * k;
+    e.dist2 = dist2_dev + r0 * k;
+    CU(launch_exact(e, st));
+  }
+  return AKNN_OK;
+}
+
+aknn_status aknn_exact(const aknn_index *cix, const uint8_t *queries, int32_t q, int32_t k, int32_t *idx,
+                       int32_t *dist2) {
+  aknn_index *ix = const_cast<aknn_index *>(cix);
+  if (!ix || !queries || !idx || !dist2) return fail(AKNN_EINVAL, "NULL argument");
+  if (q == 0) return AKNN_OK;
+  const size_t szQ = (size_t)q * ix->d, szO = (size_t)q * k * 4;
+  TRY(ix->outs.ensure(round_up(szQ, 256) + 2 * round_up(szO, 256)));
+  uint8_t *dq = ix->outs.as<uint8_t>();
+  int32_t *di = ix->outs.as<int32_t>(round_up(szQ, 256));
+  int32_t *dd = ix->outs.as<int32_t>(round_up(szQ, 256) + round_up(szO, 256));
+  cudaStream_t st = ix->stream;
+  CU(cudaMemcpyAsync(dq, queries, szQ, cudaMemcpyHostToDevice, st));
+  TRY(aknn_exact_async(ix, dq, q, k, di, dd, st));
+  CU(cudaMemcpyAsync(idx, di, szO, cudaMemcpyDeviceToHost, st));
+  CU(cudaMemcpyAsync(dist2, dd, szO, cudaMemcpyDeviceToHost, st));
+  CU(cudaStreamSynchronize(st));
+  return AKNN_OK;
+}
+
+int64_t aknn_index_n_local(const aknn_index *ix) { return ix ? ix->n_local : -1; }
+int64_t aknn_index_n_global(const aknn_index *ix) { return ix ? ix->n_global : -1; }
+int32_t aknn_index_dim(const aknn_index *ix) { return ix ? ix->d : -1; }
+
+void aknn_free(aknn_index *ix) {
+  if (!ix) return;
+#ifdef AKNN_WITH_NCCL
+  if (ix->comm) ncclCommDestroy(ix->comm);
+#endif
+  if (ix->stream) cudaStreamSynchronize(ix->stream);
+  if (ix->stream) cudaStreamDestroy(ix->stream);
+  delete ix;
+}
+
+const char *aknn_strerror(aknn_status s) {
+  switch (s) {
+    case AKNN_OK: return "AKNN_OK: success";
+    case AKNN_EINVAL: return "AKNN_EINVAL: invalid argument";
+    case AKNN_ENOMEM: return "AKNN_ENOMEM: out of memory";
+    case AKNN_ECUDA: return "AKNN_ECUDA: CUDA error";
+    case AKNN_ENCCL: return "AKNN_ENCCL: NCCL error";
+    case AKNN_EMAXROUNDS: return "AKNN_EMAXROUNDS: max_rounds reached before Eq. (5) held";
+  }
+  return "unknown aknn_status";
+}
+
+const char *aknn_last_error(void) { return g_last_error.c_str(); }
+
+}  // extern "C"

@@ -1,0 +1,109 @@
+// internal.cuh -- shared device/host definitions of libaknn (product path).
+//
+// Nothing here is shared with oracle/: the Philox rounds, the Lemire map, the
+// estimator and the key are written out again from the paper / DESIGN.md.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace aknn {
+
+// Level byte per (query, point) pair: c = log2 T (T = 2^c sampled draws so
+// far), or LVL_EXACT once T = d.
+constexpr uint8_t LVL_EXACT = 0xFF;
+// Action byte written by the blocker filter: 0 = idle, c+1 = draw level c+1
+// (T -> 2T), ACT_EXACT = exact fallback.
+constexpr uint8_t ACT_EXACT = 0xFE;
+// d <= 33025 -> sampled levels c in [0, 15]; slot MAX_LEVELS = exact list.
+constexpr int MAX_LEVELS = 16;
+constexpr int NSLOT = MAX_LEVELS + 1;
+
+// Per-query state of the round loop (device memory, one per batch row).
+struct QState {
+  unsigned long long thr_k;   // composite key of rank k      (end of C)
+  unsigned long long thr_kh;  // composite key of rank k + h  (end of M)
+  double A;                   // max_{C} d_hat + alpha  (Eq. 2)
+  double B;                   // min_{F} d_hat - alpha  (Eq. 3)
+  double a_d2;                // alpha_{d2}             (Eq. 4 batched)
+  int d1, d2;                 // local ids of d1, d2
+  int done;                   // 1 once Eq. (5) held
+  int rounds;                 // rounds evaluated
+  long long draws;            // sampled draws so far
+  long long nexact;           // exact fallbacks so far
+};
+
+// Per-round control block (device memory; one per batch).
+struct RoundCtl {
+  unsigned int n_active;                  // queries failing Eq. (5) this round
+  unsigned int pad0;
+  unsigned int cnt[NSLOT];                // pairs per action slot
+  unsigned int off[NSLOT + 1];            // list offsets per slot
+  unsigned int cursor[NSLOT];             // scatter cursors
+  unsigned long long chunk_off[NSLOT + 1];// warp-chunk prefix per slot
+  unsigned long long advanced;            // pairs advanced, cumulative
+};
+
+// Everything a round kernel needs, passed by value.
+struct Geom {
+  const uint8_t *X;      // [n][pitch] points (zero padded)
+  const uint8_t *Q;      // [q][pitch] queries of this batch (zero padded)
+  const double *alpha;   // [d+1]
+  int32_t *S;            // [q][npad] exact integer sums
+  uint8_t *lvl;          // [q][npad] level bytes
+  uint8_t *act;          // [q][npad] action bytes
+  uint32_t *list;        // work list, codes (qi << ibits) | i
+  QState *qs;            // [q]
+  RoundCtl *ctl;
+  int64_t pitch;         // row pitch of X and Q (bytes, multiple of 16)
+  int64_t npad;          // row pitch of S/lvl/act (elements, multiple of 16)
+  int n;                 // local points
+  int d;                 // dimension m
+  int q;                 // queries in this batch
+  int k, h;
+  uint32_t id_offset;    // global id of local row 0
+  uint32_t qi0;          // RNG query index of batch row 0
+  uint32_t seed_lo, seed_hi;
+  unsigned long long L;  // lcm(2^cmax, d): K = S * (L / T) is an exact order key
+  unsigned long long Ld; // L / d
+  int ibits;             // bits of the local point index in the composite key
+  int cmax;              // largest sampled level (2^cmax < d)
+};
+
+// ---- Philox4x32-10 (Salmon et al.), counter (x,y,z,w), key (k0,k1) --------
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const unsigned long long p0 = (unsigned long long)0xD2511F53u * c.x;
+    const unsigned long long p1 = (unsigned long long)0xCD9E8D57u * c.z;
+    c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ k0, (uint32_t)p1,
+                   (uint32_t)(p0 >> 32) ^ c.w ^ k1, (uint32_t)p0);
+    k0 += 0x9E3779B9u;
+    k1 += 0xBB67AE85u;
+  }
+  return c;
+}
+
+// Multiply-high map of a 32-bit word onto [0, d) (reading R5).
+__device__ __forceinline__ uint32_t coord_of(uint32_t w, uint32_t d) { return __umulhi(w, d); }
+
+// Exact order key of an arm: K = S * (L / T).  S/T ranks exactly like the
+// fp64 estimate S/(65025 T) (reading R9), and with the local index
+// in the low bits every key is unique: (d_hat, i) lexicographic order.
+__device__ __forceinline__ unsigned long long arm_key(int32_t S, uint8_t l, uint32_t i,
+                                                      const Geom &g) {
+  const unsigned long long mul = (l == LVL_EXACT) ? g.Ld : (g.L >> l);
+  return (((unsigned long long)(uint32_t)S * mul) << g.ibits) | i;
+}
+
+// d_hat = S / (T * 65025), one correctly rounded fp64 division (P:121-124,
+// DESIGN.md reading R15).  T * 65025 is exact in fp64.
+__device__ __forceinline__ double dhat_of(int32_t S, uint8_t l, int d) {
+  const double T = (l == LVL_EXACT) ? (double)d : (double)(1u << l);
+  return __ddiv_rn((double)S, __dmul_rn(T, 65025.0));
+}
+
+__device__ __forceinline__ double alpha_of(uint8_t l, const double *alpha) {
+  return (l == LVL_EXACT) ? 0.0 : __ldg(alpha + (1u << l));
+}
+
+}  // namespace aknn

@@ -1,0 +1,44 @@
+// launch.h -- internal launch wrappers (host side of the kernels).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+#include "internal.cuh"
+
+namespace aknn {
+
+// Device output pointers of one query batch (rows row0 .. row0 + q - 1).
+struct OutPtrs {
+  int row0;
+  int32_t *sets;
+  double *dhat;
+  int32_t *counts;
+  int64_t *sums;
+  int64_t *evals;
+  int64_t *draws;
+  int32_t *rounds;
+};
+
+cudaError_t launch_init(const Geom &g, cudaStream_t s);
+cudaError_t launch_select(const Geom &g, int nbits, cudaStream_t s);
+cudaError_t launch_filter(const Geom &g, cudaStream_t s);
+cudaError_t launch_advance(const Geom &g, int num_sms, cudaStream_t s);
+cudaError_t launch_output(const Geom &g, const OutPtrs &o, cudaStream_t s);
+int output_max_kh();
+
+// Exact comparison pass (exact_kernels.cu).
+struct ExactGeom {
+  const uint8_t *X;   // [n][pitch]
+  const uint8_t *Q;   // [q][pitch]
+  int64_t pitch;
+  int n, d, q, k;
+  uint32_t id_offset;
+  int32_t *D;         // [q][npad] scratch distances
+  int64_t npad;
+  int ibits, nbits;
+  int32_t *idx;       // [q][k] out (device)
+  int32_t *dist2;     // [q][k] out (device)
+};
+cudaError_t launch_exact(const ExactGeom &e, cudaStream_t s);
+
+}  // namespace aknn

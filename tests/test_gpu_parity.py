@@ -1,0 +1,190 @@
+"""GPU parity (-m gpu): the CUDA path through the C-ABI vs the CPU oracle.
+
+Bar: integer outputs (sets, per-pair counts T_i, per-pair sums
+S_i, draws, evals, rounds) bit-exact; the fp64 estimates d_hat to 0 ulp
+(np.array_equal on float64).  Inputs are seeded synthetic data (synth/)."""
+import numpy as np
+import pytest
+
+import oracle.oracle as orc
+import synth
+
+pytestmark = pytest.mark.gpu
+
+KEYS = ("sets", "dhat", "counts", "sums", "evals", "draws", "rounds")
+
+
+@pytest.fixture(scope="module")
+def ak():
+    import torch
+    torch.cuda.set_device(0)
+    import paper_1902_09465_b200 as m
+    return m
+
+
+def _assert_parity(got, ref, keys=KEYS, rows=None):
+    for k in keys:
+        g = got[k] if rows is None else got[k][rows]
+        assert g.shape == ref[k].shape, (k, g.shape, ref[k].shape)
+        if not np.array_equal(g, ref[k]):
+            bad = np.argwhere(np.atleast_1d(g != ref[k]))[:5]
+            raise AssertionError(f"{k} differs at {bad.tolist()}")
+
+
+def _run_both(ak, X, Q, k, h, seed, alpha, **kw):
+    ix = ak.Index(X)
+    got = ix.query(Q, k, h, 0.05, seed, alpha, counts=True, sums=True, **kw)
+    ix.close()
+    ref = orc.query_br(X, Q, k, h, seed, alpha, want_sums=True,
+                       max_rounds=kw.get("max_rounds", 0))
+    return got, ref
+
+
+def test_config1_full_bit_exact(ak):
+    cfg = synth.config(1)
+    X, Q, planted = synth.planted(cfg)
+    al = orc.alpha_theory(cfg.n, cfg.delta, cfg.d)
+    got, ref = _run_both(ak, X, Q, cfg.k, cfg.h, cfg.seed, al)
+    _assert_parity(got, ref)
+    assert sorted(got["sets"][0].tolist()) == planted.tolist()
+
+
+CASES = [
+    # (name, n, d, q, k, h, alpha kind, c_alpha, seed, data kind)
+    ("ragged_n_d", 1237, 100, 5, 3, 4, "theory", 0, 1, "mixture"),
+    ("d_not16", 777, 33, 7, 5, 5, "exp", 0.05, 2, "mixture"),
+    ("many_rounds_mixed_levels", 3001, 256, 6, 4, 6, "exp", 0.02, 3, "mixture"),
+    ("h0_lucb", 900, 64, 4, 6, 0, "exp", 0.1, 4, "mixture"),
+    ("uniform_hard", 4099, 128, 3, 10, 10, "theory", 0, 5, "uniform"),
+    ("n_above_select_cap", 20011, 96, 3, 7, 9, "exp", 0.05, 6, "mixture"),
+    ("tiny_n", 5, 16, 4, 2, 2, "theory", 0, 7, "uniform"),
+    ("d2", 300, 2, 3, 3, 3, "theory", 0, 8, "uniform"),
+    ("d3", 300, 3, 3, 3, 3, "exp", 0.1, 9, "uniform"),
+    ("large_k", 5000, 48, 2, 300, 200, "exp", 0.05, 10, "mixture"),
+]
+
+
+@pytest.mark.parametrize("case", CASES, ids=[c[0] for c in CASES])
+def test_small_instances_bit_exact(ak, case):
+    name, n, d, q, k, h, kind, c, seed, data = case
+    X, Q = synth.small_instance(100 + seed, n, d, q=q, kind=data)
+    al = orc.alpha_theory(n, 0.05, d) if kind == "theory" else orc.alpha_experimental(n, 0.05, d, c)
+    got, ref = _run_both(ak, X, Q, k, h, 0xDEADBEEF00000000 + seed, al)
+    _assert_parity(got, ref)
+
+
+def test_d1_exact_after_init(ak):
+    rng = np.random.default_rng(3)
+    X = rng.integers(0, 256, (500, 1), dtype=np.uint8)
+    Q = rng.integers(0, 256, (4, 1), dtype=np.uint8)
+    al = orc.alpha_theory(500, 0.05, 1)
+    got, ref = _run_both(ak, X, Q, 3, 3, 0, al)
+    _assert_parity(got, ref)
+    assert np.all(got["rounds"] == 1)
+
+
+def test_max_rounds_partial_state(ak):
+    X, Q = synth.small_instance(55, 2000, 200, q=4)
+    al = orc.alpha_theory(2000, 0.05, 200)
+    got, ref = _run_both(ak, X, Q, 5, 5, 3, al, max_rounds=3)
+    assert got["status"] == ak.AKNN_EMAXROUNDS and ref["status"] == orc.EMAXROUNDS
+    _assert_parity(got, ref)
+
+
+def test_qi_offset_selects_rng_stream(ak):
+    X, Q = synth.small_instance(56, 800, 64, q=6)
+    al = orc.alpha_experimental(800, 0.05, 64, 0.1)
+    ix = ak.Index(X)
+    full = ix.query(Q, 4, 4, 0.05, 11, al, sums=True)
+    part = ix.query(Q[3:], 4, 4, 0.05, 11, al, sums=True, qi_offset=3)
+    ix.close()
+    for k in ("sets", "counts", "sums", "rounds"):
+        assert np.array_equal(full[k][3:], part[k])
+
+
+@pytest.mark.parametrize("i,n,q", [(2, 6000, 8), (3, 1500, 3), (4, 20000, 3), (5, 8000, 4)])
+def test_reduced_configs_bit_exact(ak, i, n, q):
+    """Configs 2-5 at a prefix of their rows and queries (oracle finishes in seconds)."""
+    cfg = synth.config(i)
+    X = synth.points(cfg, 0, n)
+    Q = synth.queries(cfg)[:q]
+    al = orc.alpha_theory(n, cfg.delta, cfg.d)
+    got, ref = _run_both(ak, X, Q, cfg.k, cfg.h, cfg.seed, al)
+    _assert_parity(got, ref)
+
+
+def test_config2_full_size_sampled_queries(ak):
+    """Config 2 at its BASELINE size (the bench workload, same launch path: device API,
+    all 1000 queries in one call); the oracle recomputes 3 sampled queries in full."""
+    import torch
+    cfg = synth.config(2)
+    X = synth.points(cfg)
+    Q = synth.queries(cfg)
+    al = orc.alpha_theory(cfg.n, cfg.delta, cfg.d)
+    ix = ak.Index(torch.from_numpy(X).cuda())
+    out = ix.query_device(torch.from_numpy(Q).cuda(), cfg.k, cfg.h, cfg.delta, cfg.seed, al,
+                          counts=True, sums=True)
+    torch.cuda.synchronize()
+    got = {k: v.cpu().numpy() for k, v in out.items() if k != "status" and v is not None}
+    ix.close()
+    rows = np.random.default_rng(2).choice(cfg.q, 3, replace=False)
+    ref = orc.query_br(X, Q[rows], cfg.k, cfg.h, cfg.seed, al, qids=rows, want_sums=True)
+    _assert_parity(got, ref, rows=rows)
+
+
+def test_device_api_equals_host_api(ak):
+    import torch
+    X, Q = synth.small_instance(77, 3000, 120, q=9)
+    al = orc.alpha_experimental(3000, 0.05, 120, 0.05)
+    ix = ak.Index(X)
+    host = ix.query(Q, 5, 5, 0.05, 21, al, counts=True, sums=True)
+    dev = ix.query_device(torch.from_numpy(Q).cuda(), 5, 5, 0.05, 21, al, counts=True, sums=True)
+    torch.cuda.synchronize()
+    for k in KEYS:
+        assert np.array_equal(host[k], dev[k].cpu().numpy()), k
+    # determinism: a second run is byte-identical
+    again = ix.query(Q, 5, 5, 0.05, 21, al, counts=True, sums=True)
+    for k in KEYS:
+        assert np.array_equal(host[k], again[k]), k
+    ix.close()
+
+
+def test_null_alpha_uses_footnote2_table(ak):
+    X, Q = synth.small_instance(78, 700, 40, q=2)
+    ix = ak.Index(X)
+    a = ix.query(Q, 3, 3, 0.05, 1, None, sums=True)
+    b = ix.query(Q, 3, 3, 0.05, 1, orc.alpha_theory(700, 0.05, 40), sums=True)
+    ix.close()
+    for k in KEYS[:-1]:
+        if a[k] is not None:
+            assert np.array_equal(a[k], b[k]), k
+
+
+def test_invalid_arguments_rejected(ak):
+    X, Q = synth.small_instance(79, 50, 8, q=1)
+    ix = ak.Index(X)
+    al = orc.alpha_theory(50, 0.05, 8)
+    for kw in (dict(k=25, h=25), dict(k=0, h=1), dict(k=1, h=-1)):
+        with pytest.raises(ak.AknnError):
+            ix.query(Q, kw["k"], kw["h"], 0.05, 0, al)
+    with pytest.raises(ak.AknnError):
+        ix.query(Q, 2, 2, 1.5, 0, al)
+    with pytest.raises(ak.AknnError):
+        ix.query(np.zeros((1, 9), np.uint8), 2, 2, 0.05, 0, al)
+    ix.close()
+
+
+# --------------------------------------------------------------------------- exact pass
+@pytest.mark.parametrize("n,d,q,k,lo,hi", [(1000, 256, 1, 5, 0, 256), (5003, 100, 70, 17, 0, 256),
+                                           (3000, 64, 9, 50, 0, 2), (129, 784, 130, 128, 0, 256)])
+def test_exact_pass_vs_bruteforce(ak, n, d, q, k, lo, hi):
+    """aknn_exact == oracle brute force, ties (values in {0,1}) by smaller id."""
+    rng = np.random.default_rng(n + d)
+    X = rng.integers(lo, hi, (n, d), dtype=np.uint8)
+    Q = rng.integers(lo, hi, (q, d), dtype=np.uint8)
+    ix = ak.Index(X)
+    idx, dist = ix.exact(Q, k)
+    ix.close()
+    ridx, rdist = orc.bruteforce(X, Q, k)
+    assert np.array_equal(idx, ridx)
+    assert np.array_equal(dist, rdist)
