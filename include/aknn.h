@@ -77,22 +77,28 @@ typedef struct {
   int32_t reserved;
 } aknn_opts;
 
-/* Execution statistics of the last query call on an index (aknn_get_stats). */
+/* Execution statistics of the last query call on an index (aknn_get_stats).
+ * Kernel classes: init (a2), select (a6-a7: rank split, bounds, Eq. 5),
+ * filter (a8 blocker predicate), compact (a8 list plan + scatter), advance
+ * (a3-a4 level gathers and exact fallbacks), output (a9).  ms_* are device
+ * times from CUDA events recorded on the launching stream around every
+ * launch of that class (timing = 1 only; events are read after the call's
+ * final synchronisation, so timing adds no host round trips).              */
 typedef struct {
-  int32_t rounds;            /* host rounds executed (max over queries)        */
-  int32_t query_batches;     /* internal query sub-batches                     */
-  int64_t kernel_launches;   /* device kernels launched by the call            */
-  int64_t pairs;             /* q * n_local                                    */
-  int64_t draws;             /* total sampled draws (sum over queries)         */
-  int64_t exact_fallbacks;   /* total arms that went exact                     */
-  int64_t active_pair_rounds;/* sum over rounds of advanced pairs              */
-  double ms_total;           /* device time of the whole call (timing=1)       */
-  double ms_init;            /* initialisation gather (a2)                     */
-  double ms_select;          /* rank split + bounds + Eq. (5) (a5-a7)          */
-  double ms_filter;          /* blocker filter + compaction (a8)               */
-  double ms_advance;         /* level gathers + exact fallbacks (a3, a4)       */
-  double ms_output;          /* output assembly (a9)                           */
-  int64_t advance_launches;  /* launches of the advance (gather) kernel        */
+  int32_t rounds;             /* host rounds executed (max over sub-batches)   */
+  int32_t query_batches;      /* internal query sub-batches                    */
+  int64_t kernel_launches;    /* device kernels launched by the call           */
+  int64_t pairs;              /* q * n_local                                   */
+  int64_t draws;              /* total sampled draws incl. init (sum over q)   */
+  int64_t exact_fallbacks;    /* total arms that went exact                    */
+  int64_t active_pair_rounds; /* sum over rounds of advanced (listed) pairs    */
+  int64_t query_rounds;       /* sum over rounds of queries the rank split
+                                 evaluated (not yet stopped)                   */
+  int64_t blocked_query_rounds;/* ... of those, queries that failed Eq. (5)    */
+  double ms_total;            /* device time of the whole call (timing=1)      */
+  double ms_init, ms_select, ms_filter, ms_compact, ms_advance, ms_output;
+  int64_t launches_init, launches_select, launches_filter, launches_compact,
+      launches_advance, launches_output;
 } aknn_stats;
 
 /* ------------------------------------------------------------------------ */

@@ -51,9 +51,13 @@ class Stats(C.Structure):
     _fields_ = [("rounds", C.c_int32), ("query_batches", C.c_int32),
                 ("kernel_launches", C.c_int64), ("pairs", C.c_int64), ("draws", C.c_int64),
                 ("exact_fallbacks", C.c_int64), ("active_pair_rounds", C.c_int64),
+                ("query_rounds", C.c_int64), ("blocked_query_rounds", C.c_int64),
                 ("ms_total", C.c_double), ("ms_init", C.c_double), ("ms_select", C.c_double),
-                ("ms_filter", C.c_double), ("ms_advance", C.c_double), ("ms_output", C.c_double),
-                ("advance_launches", C.c_int64)]
+                ("ms_filter", C.c_double), ("ms_compact", C.c_double),
+                ("ms_advance", C.c_double), ("ms_output", C.c_double),
+                ("launches_init", C.c_int64), ("launches_select", C.c_int64),
+                ("launches_filter", C.c_int64), ("launches_compact", C.c_int64),
+                ("launches_advance", C.c_int64), ("launches_output", C.c_int64)]
 
 
 _P = C.c_void_p
@@ -164,19 +168,35 @@ class Index:
     # ------------------------------------------------------------------ query
     def query(self, queries, k: int, h: int, delta: float, seed: int = 0, alpha=None, *,
               counts: bool = True, sums: bool = False, dhat: bool = True, max_rounds: int = 0,
-              qi_offset: int = 0, timing: bool = False) -> dict:
-        """aknn_query_ex on host arrays; returns numpy arrays."""
+              qi_offset: int = 0, timing: bool = False, out: Optional[dict] = None) -> dict:
+        """aknn_query_ex on host arrays; returns numpy arrays.
+
+        ``out`` may pass preallocated (e.g. pinned) host arrays with the keys of the
+        returned dict; a key mapped to None skips that output."""
         Q = np.ascontiguousarray(np.atleast_2d(queries), np.uint8)
         q, d = Q.shape
         if d != self.d:
             raise AknnError(AKNN_EINVAL, f"query dimension {d} != index dimension {self.d}")
         kh = k + h
-        out = dict(sets=np.zeros((q, kh), np.int32),
-                   dhat=np.zeros((q, kh), np.float64) if dhat else None,
-                   counts=np.zeros((q, self.n_local), np.int32) if counts else None,
-                   sums=np.zeros((q, self.n_local), np.int64) if sums else None,
-                   evals=np.zeros(q, np.int64), draws=np.zeros(q, np.int64),
-                   rounds=np.zeros(q, np.int32))
+        if out is None:
+            out = dict(sets=np.zeros((q, kh), np.int32),
+                       dhat=np.zeros((q, kh), np.float64) if dhat else None,
+                       counts=np.zeros((q, self.n_local), np.int32) if counts else None,
+                       sums=np.zeros((q, self.n_local), np.int64) if sums else None,
+                       evals=np.zeros(q, np.int64), draws=np.zeros(q, np.int64),
+                       rounds=np.zeros(q, np.int32))
+        else:
+            want = dict(sets=((q, kh), np.int32), dhat=((q, kh), np.float64),
+                        counts=((q, self.n_local), np.int32), sums=((q, self.n_local), np.int64),
+                        evals=((q,), np.int64), draws=((q,), np.int64), rounds=((q,), np.int32))
+            for key, (shape, dt) in want.items():
+                a = out.get(key)
+                if a is None:
+                    if key == "sets":
+                        raise AknnError(AKNN_EINVAL, "out['sets'] is required")
+                    out[key] = None
+                elif a.shape != shape or a.dtype != dt or not a.flags.c_contiguous:
+                    raise AknnError(AKNN_EINVAL, f"out[{key!r}] must be C-contiguous {dt.__name__}{shape}")
         res = Result(*[_ptr(out[f]) for f, _ in Result._fields_])
         al = None if alpha is None else np.ascontiguousarray(alpha, np.float64)
         if al is not None and al.shape != (self.d + 1,):

@@ -97,6 +97,22 @@ struct DevBuf {
   }
 };
 
+struct EventPool {
+  std::vector<cudaEvent_t> ev;
+  size_t used = 0;
+  ~EventPool() {
+    for (cudaEvent_t e : ev) cudaEventDestroy(e);
+  }
+  cudaEvent_t get() {
+    if (used == ev.size()) {
+      cudaEvent_t e = nullptr;
+      if (cudaEventCreate(&e) != cudaSuccess) return nullptr;
+      ev.push_back(e);
+    }
+    return ev[used++];
+  }
+};
+
 }  // namespace
 
 struct aknn_index {
@@ -112,6 +128,7 @@ struct aknn_index {
   DevBuf alpha;            // [d+1]
   DevBuf outs;             // device outputs for the host API
   DevBuf exact_ws;
+  EventPool events;
   int rank = 0, world = 1;
 #ifdef AKNN_WITH_NCCL
   ncclComm_t comm = nullptr;
@@ -204,33 +221,43 @@ aknn_status host_alpha_table(int kind, int64_t n, double delta, double c_alpha, 
   return fail(AKNN_EINVAL, "alpha kind %d unknown (0 = footnote 2, 1 = section 5)", kind);
 }
 
-struct Timer {
+// Per-launch CUDA events on the launching stream, read after the call's final
+// synchronisation (no extra host round trips).  Events are pooled per index.
+enum Phase { PH_INIT = 0, PH_SELECT, PH_FILTER, PH_COMPACT, PH_ADVANCE, PH_OUTPUT, PH_ALL, PH_N };
+
+struct PhaseTimer {
   bool on;
   cudaStream_t s;
-  cudaEvent_t a = nullptr, b = nullptr;
-  Timer(bool on_, cudaStream_t s_) : on(on_), s(s_) {
-    if (on) {
-      cudaEventCreate(&a);
-      cudaEventCreate(&b);
-    }
-  }
-  ~Timer() {
-    if (a) cudaEventDestroy(a);
-    if (b) cudaEventDestroy(b);
+  EventPool *pool;
+  struct Rec {
+    int ph;
+    cudaEvent_t a, b;
+  };
+  std::vector<Rec> recs;
+  cudaEvent_t open_a = nullptr;
+  PhaseTimer(bool on_, cudaStream_t s_, EventPool *p) : on(on_), s(s_), pool(p) {
+    if (on) pool->used = 0;
   }
   void start() {
-    if (on) cudaEventRecord(a, s);
+    if (!on) return;
+    open_a = pool->get();
+    if (open_a) cudaEventRecord(open_a, s);
   }
-  // accumulate after the stream has been synchronised past `b`
-  void stop() {
-    if (on) cudaEventRecord(b, s);
+  void stop(int ph) {
+    if (!on || !open_a) return;
+    cudaEvent_t b = pool->get();
+    if (!b) return;
+    cudaEventRecord(b, s);
+    recs.push_back(Rec{ph, open_a, b});
+    open_a = nullptr;
   }
-  double ms() {
-    if (!on) return 0.0;
-    float m = 0.f;
-    cudaEventSynchronize(b);
-    cudaEventElapsedTime(&m, a, b);
-    return m;
+  // call after the stream has been synchronised past every recorded event
+  void resolve(double ms[PH_N]) {
+    for (int i = 0; i < PH_N; ++i) ms[i] = 0.0;
+    for (const Rec &r : recs) {
+      float m = 0.f;
+      if (cudaEventElapsedTime(&m, r.a, r.b) == cudaSuccess) ms[r.ph] += m;
+    }
   }
 };
 
@@ -298,15 +325,16 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
 
   aknn_stats stats{};
   stats.pairs = (int64_t)q * n;
-  const bool timing = o.timing != 0;
-  Timer t_all(timing, st), t_ph(timing, st);
-  t_all.start();
+  PhaseTimer tm(o.timing != 0, st, &ix->events);
+  tm.start();
+  cudaEvent_t all_a = tm.open_a;
   unsigned int *h_active = nullptr;
   CU(cudaMallocHost(&h_active, sizeof(unsigned int)));
   struct HostFree {
     unsigned int *p;
     ~HostFree() { cudaFreeHost(p); }
   } hf{h_active};
+  tm.open_a = nullptr;
   aknn_status status = AKNN_OK;
   for (int64_t r0 = 0; r0 < q; r0 += qb) {
     const int qn = (int)std::min<int64_t>(qb, q - r0);
@@ -318,64 +346,77 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
     CU(cudaMemcpy2DAsync(ix->ws.as<uint8_t>(oQ), ix->pitch, queries_dev + r0 * qstride, qstride, d,
                          qn, cudaMemcpyDeviceToDevice, st));
     CU(cudaMemsetAsync(g.ctl, 0, sizeof(RoundCtl), st));
-    t_ph.start();
+    tm.start();
     CU(launch_init(g, st));
-    t_ph.stop();
-    stats.kernel_launches += 2;
-    stats.ms_init += t_ph.ms();
+    tm.stop(PH_INIT);
+    stats.launches_init += 2;
     int r = 0;
+    unsigned evaluated = (unsigned)qn;  // queries the rank split looks at this round
     for (;;) {
       ++r;
       // zero the per-round counters (everything but the cumulative `advanced`)
       CU(cudaMemsetAsync(g.ctl, 0, offsetof(RoundCtl, advanced), st));
-      t_ph.start();
+      tm.start();
       CU(launch_select(g, kg.nbits, st));
-      t_ph.stop();
-      ++stats.kernel_launches;
+      tm.stop(PH_SELECT);
+      ++stats.launches_select;
+      stats.query_rounds += evaluated;
       CU(cudaMemcpyAsync(h_active, &g.ctl->n_active, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
       CU(cudaStreamSynchronize(st));
-      stats.ms_select += t_ph.ms();
-      if (*h_active == 0) break;
+      const unsigned nact = *h_active;
+      stats.blocked_query_rounds += nact;
+      evaluated = nact;
+      if (nact == 0) break;
       if (o.max_rounds > 0 && r >= o.max_rounds) {
         status = AKNN_EMAXROUNDS;
         break;
       }
-      t_ph.start();
+      tm.start();
       CU(launch_filter(g, st));
-      t_ph.stop();
-      stats.kernel_launches += 3;
-      const double mf = t_ph.ms();
-      stats.ms_filter += mf;
-      t_ph.start();
+      tm.stop(PH_FILTER);
+      ++stats.launches_filter;
+      tm.start();
+      CU(launch_compact(g, st));
+      tm.stop(PH_COMPACT);
+      stats.launches_compact += 2;
+      tm.start();
       CU(launch_advance(g, ix->num_sms, st));
-      t_ph.stop();
-      stats.kernel_launches += 1;
-      stats.advance_launches += 1;
-      stats.ms_advance += t_ph.ms();
+      tm.stop(PH_ADVANCE);
+      ++stats.launches_advance;
       if (r > 1 + 64 * 64) return fail(AKNN_ECUDA, "round loop did not terminate (internal error)");
     }
     if (r > stats.rounds) stats.rounds = r;
     OutPtrs op{(int)r0, out->sets, out->dhat, out->counts, out->sums, out->evals, out->draws, out->rounds};
-    t_ph.start();
+    tm.start();
     CU(launch_output(g, op, st));
-    t_ph.stop();
-    stats.kernel_launches += (out->counts || out->sums) ? 2 : 1;
+    tm.stop(PH_OUTPUT);
+    stats.launches_output += (out->counts || out->sums) ? 2 : 1;
     RoundCtl ctl_h;
     CU(cudaMemcpyAsync(&ctl_h, g.ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
-    stats.ms_output += t_ph.ms();
-    stats.active_pair_rounds += (int64_t)ctl_h.advanced;
-    // totals from the per-query state
     std::vector<QState> qs(qn);
-    CU(cudaMemcpy(qs.data(), g.qs, sizeof(QState) * qn, cudaMemcpyDeviceToHost));
+    CU(cudaMemcpyAsync(qs.data(), g.qs, sizeof(QState) * qn, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    stats.active_pair_rounds += (int64_t)ctl_h.advanced;
     for (const QState &s : qs) {
       stats.draws += s.draws;
       stats.exact_fallbacks += s.nexact;
     }
     if (status != AKNN_OK) break;
   }
-  t_all.stop();
-  stats.ms_total = t_all.ms();
+  tm.open_a = all_a;
+  tm.stop(PH_ALL);
+  CU(cudaStreamSynchronize(st));
+  double ms[PH_N];
+  tm.resolve(ms);
+  stats.ms_init = ms[PH_INIT];
+  stats.ms_select = ms[PH_SELECT];
+  stats.ms_filter = ms[PH_FILTER];
+  stats.ms_compact = ms[PH_COMPACT];
+  stats.ms_advance = ms[PH_ADVANCE];
+  stats.ms_output = ms[PH_OUTPUT];
+  stats.ms_total = ms[PH_ALL];
+  stats.kernel_launches = stats.launches_init + stats.launches_select + stats.launches_filter +
+                          stats.launches_compact + stats.launches_advance + stats.launches_output;
   ix->stats = stats;
   CU(cudaGetLastError());
   return status;

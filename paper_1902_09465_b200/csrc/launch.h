@@ -22,6 +22,7 @@ struct OutPtrs {
 cudaError_t launch_init(const Geom &g, cudaStream_t s);
 cudaError_t launch_select(const Geom &g, int nbits, cudaStream_t s);
 cudaError_t launch_filter(const Geom &g, cudaStream_t s);
+cudaError_t launch_compact(const Geom &g, cudaStream_t s);
 cudaError_t launch_advance(const Geom &g, int num_sms, cudaStream_t s);
 cudaError_t launch_output(const Geom &g, const OutPtrs &o, cudaStream_t s);
 int output_max_kh();

@@ -475,6 +475,10 @@ cudaError_t launch_select(const Geom &g, int nbits, cudaStream_t s) {
 
 cudaError_t launch_filter(const Geom &g, cudaStream_t s) {
   k_filter<<<dim3(cdiv(g.npad, FIL_NT * 4), g.q), FIL_NT, 0, s>>>(g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_compact(const Geom &g, cudaStream_t s) {
   k_plan<<<1, 32, 0, s>>>(g.ctl);
   k_scatter<<<dim3(g.q, cdiv(g.npad, FIL_NT * 4)), FIL_NT, 0, s>>>(g);
   return cudaGetLastError();

@@ -17,8 +17,8 @@ HEADER = os.path.join(ROOT, "include", "aknn.h")
 
 @pytest.fixture(scope="module")
 def ak():
-    from paper_1902_09465_b200 import _build
-    _build.build()
+    import __graft_entry__
+    __graft_entry__._load_builder().build()
     import paper_1902_09465_b200 as m
     return m
 
