@@ -55,6 +55,7 @@ def _args():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-exact", action="store_true")
+    ap.add_argument("--clock-sampler", choices=("nvml", "smi", "none"), default="nvml")
     return ap.parse_args()
 
 
@@ -104,63 +105,97 @@ class Dist:
 
 # ----------------------------------------------------------------------------- clocks
 class ClockSampler:
-    """nvidia-smi clocks + throttle reasons sampled every 200 ms during the timed region."""
+    """SM clock, max clock, power and throttle reasons sampled during the timed region.
+
+    mode "nvml" (default): in-process NVML queries every 200 ms from a thread (the
+    same counters the nvidia-smi recipe line reads); mode "smi": an nvidia-smi
+    -lms 200 subprocess (the recipe line itself); "none": no sampling."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    NAMES = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
 
-    def __init__(self, gpu: int):
-        self.gpu = gpu
+    def __init__(self, gpu: int, mode: str = "nvml", period_s: float = 0.2):
+        self.gpu, self.mode, self.period = gpu, mode, period_s
         self.proc = None
-        self.lines = []
+        self.samples = []  # (sm, smax, power_w, set(reasons))
         self.t = None
+        self.stop_evt = threading.Event()
 
     def start(self):
-        try:
-            self.proc = subprocess.Popen(
-                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
-                 "--format=csv,noheader,nounits", "-lms", "200"],
-                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
-        except Exception:
-            self.proc = None
+        if self.mode == "none":
             return
-        self.t = threading.Thread(target=self._read, daemon=True)
+        if self.mode == "smi":
+            try:
+                self.proc = subprocess.Popen(
+                    ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}",
+                     "--format=csv,noheader,nounits", "-lms", str(int(self.period * 1000))],
+                    stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            except Exception:
+                self.proc = None
+                return
+            self.t = threading.Thread(target=self._read_smi, daemon=True)
+        else:
+            try:
+                import pynvml
+                pynvml.nvmlInit()
+                self.h = pynvml.nvmlDeviceGetHandleByIndex(self.gpu)
+                self.nv = pynvml
+            except Exception:
+                self.mode = "none"
+                return
+            self.t = threading.Thread(target=self._poll_nvml, daemon=True)
         self.t.start()
 
-    def _read(self):
-        for line in self.proc.stdout:
-            self.lines.append(line.strip())
-
-    def stop(self) -> dict:
-        if self.proc is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        time.sleep(0.25)
-        self.proc.terminate()
-        try:
-            self.proc.wait(timeout=5)
-        except Exception:
-            self.proc.kill()
-        if self.t:
-            self.t.join(timeout=2)
-        sm, smax, reasons, power = [], [], set(), []
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for ln in self.lines:
-            f = [x.strip() for x in ln.split(",")]
+    def _read_smi(self):
+        for ln in self.proc.stdout:
+            f = [x.strip() for x in ln.strip().split(",")]
             if len(f) < 9:
                 continue
             try:
-                sm.append(float(f[1]))
-                smax.append(float(f[2]))
-                power.append(float(f[3]))
+                rs = {nm for nm, v in zip(self.NAMES, f[5:9]) if v.lower().startswith("active")}
+                self.samples.append((float(f[1]), float(f[2]), float(f[3]), rs))
             except ValueError:
                 continue
-            for nm, v in zip(names, f[5:9]):
-                if v.lower().startswith("active"):
-                    reasons.add(nm)
+
+    def _poll_nvml(self):
+        nv, h = self.nv, self.h
+        bits = {"hw_slowdown": nv.nvmlClocksEventReasonHwSlowdown,
+                "hw_thermal_slowdown": nv.nvmlClocksEventReasonHwThermalSlowdown,
+                "sw_thermal_slowdown": nv.nvmlClocksEventReasonSwThermalSlowdown,
+                "sw_power_cap": nv.nvmlClocksEventReasonSwPowerCap}
+        while not self.stop_evt.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                smax = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+                pw = nv.nvmlDeviceGetPowerUsage(h) / 1000.0
+                r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                self.samples.append((float(sm), float(smax), pw,
+                                     {k for k, b in bits.items() if r & b}))
+            except Exception:
+                pass
+            self.stop_evt.wait(self.period)
+
+    def stop(self) -> dict:
+        if self.mode == "none":
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "source": "not sampled"}
+        self.stop_evt.set()
+        if self.proc is not None:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        if self.t:
+            self.t.join(timeout=2)
+        sm = [s[0] for s in self.samples]
+        reasons = set().union(*[s[3] for s in self.samples]) if self.samples else set()
         return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(smax) if smax else None,
-                "power_w_max": max(power) if power else None,
-                "samples": len(sm), "reasons": sorted(reasons)}
+                "sm_max_mhz": max(s[1] for s in self.samples) if sm else None,
+                "power_w_max": max(s[2] for s in self.samples) if sm else None,
+                "samples": len(sm), "reasons": sorted(reasons),
+                "source": "NVML every 200 ms" if self.mode == "nvml" else "nvidia-smi -lms 200"}
 
 
 # ----------------------------------------------------------------------------- peaks
@@ -341,7 +376,7 @@ def run_ours(args, dist: Dist):
 
     for _ in range(args.warmup):
         step()
-    clocks = ClockSampler(dist.local)
+    clocks = ClockSampler(dist.local, args.clock_sampler)
     dist.barrier()
     torch.cuda.synchronize()
     clocks.start()
@@ -447,7 +482,7 @@ def run_ours(args, dist: Dist):
             wall.append(time.perf_counter() - t0)
         e2e_s = dist.max(sum(wall))
         h2d = Qh.nbytes + alpha.nbytes
-        d2h = sum(v.nbytes for v in hout.values() if v is not None)
+        d2h = sum(v.nbytes for key, v in hout.items() if key != "status" and v is not None)
         e2e = {"value": dist.sum(qpr * args.steps) / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "api": "aknn_query (host pointers, pinned), wall clock incl. copies"}

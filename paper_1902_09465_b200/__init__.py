@@ -158,7 +158,7 @@ class Index:
         self.d = int(_lib.aknn_index_dim(h))
 
     def close(self):
-        if getattr(self, "_h", None):
+        if getattr(self, "_h", None) and _lib is not None:
             _lib.aknn_free(self._h)
             self._h = None
 
