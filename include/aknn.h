@@ -115,7 +115,7 @@ aknn_status aknn_build(const uint8_t *points, int64_t n, int32_t d, aknn_index *
 aknn_status aknn_build_async(const uint8_t *points_dev, int64_t n, int32_t d,
                              void *cuda_stream, aknn_index **out);
 
-/* Sharded index (DESIGN.md §6): this process holds rows
+/* Sharded index (DESIGN.md §9): this process holds rows
  * [offset, offset + n_local) of an n_global-point set.  Point ids in the RNG
  * counter and in the returned sets are global ids.  `nccl_unique_id` points
  * to an ncclUniqueId (128 bytes) shared by the `world` ranks (rank 0 creates
@@ -124,6 +124,13 @@ aknn_status aknn_build_async(const uint8_t *points_dev, int64_t n, int32_t d,
 aknn_status aknn_build_shard(const uint8_t *shard, int64_t n_local, int64_t n_global,
                              int64_t offset, int32_t d, const void *nccl_unique_id,
                              int32_t rank, int32_t world, aknn_index **out);
+/* aknn_query* on an index built with world > 1 runs the point-sharded round
+ * loop: one ncclAllGather per round of (k+h+1) 16-byte records per query and
+ * rank, a deterministic merge on every rank, and at the end an ncclAllReduce of
+ * draws/evals.  Every rank must call it with the same arguments; sets, d_hat,
+ * evals, draws and rounds are then identical on every rank (global ids), and
+ * counts/sums hold this rank's n_local columns.  Needs world * (k+h) <= 16384
+ * and n_local > k + h on every rank.                                          */
 
 /* Write a fresh ncclUniqueId (128 bytes) to `id_out`.                       */
 aknn_status aknn_nccl_unique_id(void *id_out);
@@ -157,6 +164,21 @@ aknn_status aknn_query_async(const aknn_index *ix, const uint8_t *queries_dev, i
                              int32_t k, int32_t h, double delta, uint64_t seed,
                              const double *alpha_dev, const aknn_opts *opts,
                              aknn_result *out, void *cuda_stream);
+
+/* One query batch over a point set split into `nshards` shard indices that all
+ * live on the CURRENT device (built with aknn_build_shard(..., world = 1)),
+ * driven in lockstep by this process.  Shard s must hold rows
+ * [offset_s, offset_s + n_s) with the shards tiling [0, n_global) in order, and
+ * n_s > k + h.  Each round every shard writes its summary (local top-(k+h)
+ * arms + its minimum-L remainder arm) into one receive buffer and
+ * every shard merges them identically -- the same kernels as the NCCL path,
+ * without the transport.  Outputs as aknn_query, except counts/sums rows have
+ * n_global columns (shard s at columns offset_s ..).  Results are bit-identical
+ * to aknn_query on the unsharded set.  Stats go to shards[0].                */
+aknn_status aknn_query_multi(const aknn_index *const *shards, int32_t nshards,
+                             const uint8_t *queries, int32_t q, int32_t k, int32_t h,
+                             double delta, uint64_t seed, const double *alpha,
+                             const aknn_opts *opts, aknn_result *out);
 
 /* Statistics of the last aknn_query* call on `ix`.                          */
 aknn_status aknn_get_stats(const aknn_index *ix, aknn_stats *out);

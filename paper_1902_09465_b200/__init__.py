@@ -73,6 +73,8 @@ _sig = {
                        C.POINTER(Result)], _I),
     "aknn_query_async": ([_P, _P, _I, _I, _I, C.c_double, C.c_uint64, _P, C.POINTER(Opts),
                           C.POINTER(Result), _P], _I),
+    "aknn_query_multi": ([C.POINTER(_P), _I, _P, _I, _I, _I, C.c_double, C.c_uint64, _P,
+                          C.POINTER(Opts), C.POINTER(Result)], _I),
     "aknn_get_stats": ([_P, C.POINTER(Stats)], _I),
     "aknn_exact": ([_P, _P, _I, _I, _P, _P], _I),
     "aknn_exact_async": ([_P, _P, _I, _I, _P, _P, _P], _I),
@@ -109,6 +111,35 @@ def alpha_table(n: int, delta: float, d: int, kind: str = "theory", c_alpha: flo
     """aknn_alpha_table: kind 'theory' = footnote 2, 'experimental' = §5."""
     out = np.zeros(d + 1, np.float64)
     _check(_lib.aknn_alpha_table(0 if kind == "theory" else 1, n, delta, c_alpha, d, _ptr(out)))
+    return out
+
+
+def query_multi(shards, queries, k: int, h: int, delta: float, seed: int = 0, alpha=None, *,
+                counts: bool = True, sums: bool = False, dhat: bool = True, max_rounds: int = 0,
+                qi_offset: int = 0, timing: bool = False) -> dict:
+    """aknn_query_multi: one query batch over shard indices on the current device.
+
+    ``shards`` are Index objects built with ``Index(rows, n_global=..., offset=...)``
+    tiling [0, n_global) in order; counts/sums come back with n_global columns."""
+    Q = np.ascontiguousarray(np.atleast_2d(queries), np.uint8)
+    q, d = Q.shape
+    n = shards[0].n_global
+    kh = k + h
+    out = dict(sets=np.zeros((q, kh), np.int32),
+               dhat=np.zeros((q, kh), np.float64) if dhat else None,
+               counts=np.zeros((q, n), np.int32) if counts else None,
+               sums=np.zeros((q, n), np.int64) if sums else None,
+               evals=np.zeros(q, np.int64), draws=np.zeros(q, np.int64),
+               rounds=np.zeros(q, np.int32))
+    res = Result(*[_ptr(out[f]) for f, _ in Result._fields_])
+    al = None if alpha is None else np.ascontiguousarray(alpha, np.float64)
+    arr = (_P * len(shards))(*[s._h for s in shards])
+    opts = Opts(qi_offset, max_rounds, 1 if timing else 0, 0)
+    st = _lib.aknn_query_multi(arr, len(shards), _ptr(Q), q, k, h, delta, seed & (2**64 - 1),
+                               _ptr(al), C.byref(opts), C.byref(res))
+    out["status"] = st
+    if st != AKNN_EMAXROUNDS:
+        _check(st)
     return out
 
 

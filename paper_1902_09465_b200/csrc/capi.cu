@@ -173,10 +173,11 @@ aknn_status make_index(int64_t n_local, int64_t n_global, int64_t offset, int32_
 // Builds the level geometry of the composite key (R9).
 struct KeyGeom {
   unsigned long long L, Ld;
-  int cmax, ibits, nbits;
+  int cmax, ibits, kbits, nbits;
 };
 
-aknn_status key_geom(int64_t n_local, int32_t d, KeyGeom *kg) {
+// ibits: local index bits of a work-list code; kbits: GLOBAL id bits of the key.
+aknn_status key_geom(int64_t n_local, int64_t n_global, int32_t d, KeyGeom *kg) {
   int cmax = 0;
   while (d >= 2 && (1ll << (cmax + 1)) < d) ++cmax;  // largest c with 2^c < d
   const unsigned long long p2 = 1ull << cmax;
@@ -186,10 +187,12 @@ aknn_status key_geom(int64_t n_local, int32_t d, KeyGeom *kg) {
   kg->cmax = cmax;
   kg->ibits = bit_length((unsigned long long)(n_local - 1));
   if (kg->ibits < 1) kg->ibits = 1;
-  kg->nbits = bit_length(65025ull * L) + kg->ibits;
+  kg->kbits = bit_length((unsigned long long)(n_global - 1));
+  if (kg->kbits < 1) kg->kbits = 1;
+  kg->nbits = bit_length(65025ull * L) + kg->kbits;
   if (kg->nbits > 63)
     return fail(AKNN_EINVAL, "composite key needs %d bits (> 63) for n=%lld, d=%d", kg->nbits,
-                (long long)n_local, d);
+                (long long)n_global, d);
   return AKNN_OK;
 }
 
@@ -269,7 +272,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   const int64_t n = ix->n_local;
   const int32_t d = ix->d;
   KeyGeom kg;
-  TRY(key_geom(n, d, &kg));
+  TRY(key_geom(n, ix->n_global, d, &kg));
   if (k + h > output_max_kh())
     return fail(AKNN_EINVAL, "k+h=%d exceeds the supported %d", k + h, output_max_kh());
   const aknn_opts o = opts ? *opts : aknn_opts{};
@@ -318,9 +321,15 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   g.id_offset = (uint32_t)ix->offset;
   g.seed_lo = (uint32_t)(seed & 0xffffffffu);
   g.seed_hi = (uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    g.rk0[r] = g.seed_lo + (uint32_t)r * 0x9E3779B9u;
+    g.rk1[r] = g.seed_hi + (uint32_t)r * 0xBB67AE85u;
+  }
   g.L = kg.L;
   g.Ld = kg.Ld;
   g.ibits = kg.ibits;
+  g.kbits = kg.kbits;
+  g.world = 1;
   g.cmax = kg.cmax;
 
   aknn_stats stats{};
@@ -386,7 +395,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
       if (r > 1 + 64 * 64) return fail(AKNN_ECUDA, "round loop did not terminate (internal error)");
     }
     if (r > stats.rounds) stats.rounds = r;
-    OutPtrs op{(int)r0, out->sets, out->dhat, out->counts, out->sums, out->evals, out->draws, out->rounds};
+    OutPtrs op{(int)r0, 0, n, 0, out->sets, out->dhat, out->counts, out->sums, out->evals, out->draws, out->rounds};
     tm.start();
     CU(launch_output(g, op, st));
     tm.stop(PH_OUTPUT);
@@ -418,6 +427,253 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   stats.kernel_launches = stats.launches_init + stats.launches_select + stats.launches_filter +
                           stats.launches_compact + stats.launches_advance + stats.launches_output;
   ix->stats = stats;
+  CU(cudaGetLastError());
+  return status;
+}
+
+// ---------------------------------------------------------------------------
+// The point-sharded round loop.  `shards` are either the one
+// local shard of an NCCL communicator (nccl = true: one process per GPU, one
+// ncclAllGather per round), or several shards of one point set on the current
+// device driven in lockstep by this process (nccl = false: the exchange is
+// that every shard writes its summary straight into the shared receive
+// buffer).  Both run the same kernels and the same merge, so the results are
+// identical to each other, to the unsharded path and to the oracle.
+aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl,
+                              const uint8_t *queries_dev, int32_t q, int32_t k, int32_t h,
+                              uint64_t seed, const double *alpha_dev, const aknn_opts *opts,
+                              const aknn_result *out, int64_t out_ncols, cudaStream_t st) {
+  aknn_index *ix0 = shards[0];
+  const int32_t d = ix0->d;
+  const int W = nccl ? ix0->world : (int)shards.size();
+  const int kh = k + h;
+  if ((int64_t)W * kh > 16384)
+    return fail(AKNN_EINVAL, "world * (k+h) = %lld exceeds 16384 (merge buffer)", (long long)W * kh);
+  const aknn_opts o = opts ? *opts : aknn_opts{};
+  std::vector<KeyGeom> kg(shards.size());
+  for (size_t s = 0; s < shards.size(); ++s) TRY(key_geom(shards[s]->n_local, ix0->n_global, d, &kg[s]));
+  // sub-batch size: list codes fit 32 bits on every shard; memory on this device
+  int64_t qb = q;
+  size_t free_b = 0, total_b = 0;
+  CU(cudaMemGetInfo(&free_b, &total_b));
+  size_t held = 0, per_q = (size_t)W * (kh + 1) * sizeof(ShardRec);
+  for (size_t s = 0; s < shards.size(); ++s) {
+    qb = std::min<int64_t>(qb, 1ll << (32 - kg[s].ibits));
+    held += shards[s]->ws.bytes;
+    per_q += (size_t)round_up(shards[s]->n_local, 16) * 10 + shards[s]->pitch + sizeof(QState) + 64 +
+             (size_t)(kh + 1) * sizeof(ShardRec);
+  }
+  const size_t budget = (size_t)(0.6 * (double)(free_b + held));
+  if ((size_t)qb * per_q > budget) qb = (int64_t)(budget / per_q);
+#ifdef AKNN_WITH_NCCL
+  if (nccl) {  // every rank must use the same sub-batches
+    DevBuf tmp;
+    TRY(tmp.ensure(sizeof(int64_t)));
+    CU(cudaMemcpyAsync(tmp.p, &qb, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    if (ncclAllReduce(tmp.p, tmp.p, 1, ncclInt64, ncclMin, ix0->comm, st) != ncclSuccess)
+      return fail(AKNN_ENCCL, "ncclAllReduce(qb) failed");
+    CU(cudaMemcpyAsync(&qb, tmp.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+  }
+#endif
+  if (qb < 1) return fail(AKNN_ENOMEM, "not enough device memory for one query row");
+  const int64_t recv_stride = qb * (kh + 1);
+  // per-shard workspace: S | lvl | act | list | Q | QState | RoundCtl | send | [recv]
+  std::vector<Geom> G(shards.size());
+  std::vector<size_t> oQv(shards.size()), szQv(shards.size());
+  ShardRec *recv_shared = nullptr;
+  for (size_t si = 0; si < shards.size(); ++si) {
+    aknn_index *ix = shards[si];
+    const int64_t npad = round_up(ix->n_local, 16);
+    const bool has_recv = nccl || si == 0;
+    const size_t szS = (size_t)qb * npad * 4, szL = (size_t)qb * npad,
+                 szList = (size_t)qb * npad * 4, szQ = (size_t)qb * ix->pitch,
+                 szQS = (size_t)qb * sizeof(QState), szCtl = sizeof(RoundCtl),
+                 szSend = nccl ? (size_t)recv_stride * sizeof(ShardRec) : 0,
+                 szRecv = has_recv ? (size_t)W * recv_stride * sizeof(ShardRec) : 0;
+    size_t off = 0;
+    const size_t oS = off; off = round_up(off + szS, 256);
+    const size_t oL = off; off = round_up(off + szL, 256);
+    const size_t oA = off; off = round_up(off + szL, 256);
+    const size_t oList = off; off = round_up(off + szList, 256);
+    const size_t oQ = off; off = round_up(off + szQ, 256);
+    const size_t oQS = off; off = round_up(off + szQS, 256);
+    const size_t oCtl = off; off = round_up(off + szCtl, 256);
+    const size_t oSend = off; off = round_up(off + szSend, 256);
+    const size_t oRecv = off; off = round_up(off + szRecv, 256);
+    TRY(ix->ws.ensure(off));
+    Geom &g = G[si];
+    g = Geom{};
+    g.X = ix->X.as<uint8_t>();
+    g.Q = ix->ws.as<uint8_t>(oQ);
+    g.alpha = alpha_dev;
+    g.S = ix->ws.as<int32_t>(oS);
+    g.lvl = ix->ws.as<uint8_t>(oL);
+    g.act = ix->ws.as<uint8_t>(oA);
+    g.list = ix->ws.as<uint32_t>(oList);
+    g.qs = ix->ws.as<QState>(oQS);
+    g.ctl = ix->ws.as<RoundCtl>(oCtl);
+    g.pitch = ix->pitch;
+    g.npad = npad;
+    g.n = (int)ix->n_local;
+    g.d = d;
+    g.k = k;
+    g.h = h;
+    g.id_offset = (uint32_t)ix->offset;
+    g.seed_lo = (uint32_t)(seed & 0xffffffffu);
+    g.seed_hi = (uint32_t)(seed >> 32);
+    for (int r = 0; r < 10; ++r) {
+      g.rk0[r] = g.seed_lo + (uint32_t)r * 0x9E3779B9u;
+      g.rk1[r] = g.seed_hi + (uint32_t)r * 0xBB67AE85u;
+    }
+    g.L = kg[si].L;
+    g.Ld = kg[si].Ld;
+    g.ibits = kg[si].ibits;
+    g.kbits = kg[si].kbits;
+    g.cmax = kg[si].cmax;
+    g.world = W;
+    g.recv_stride = recv_stride;
+    if (has_recv) g.recv = ix->ws.as<ShardRec>(oRecv);
+    if (si == 0 && !nccl) recv_shared = ix->ws.as<ShardRec>(oRecv);
+    if (nccl) g.send = ix->ws.as<ShardRec>(oSend);
+    oQv[si] = oQ;
+    szQv[si] = szQ;
+  }
+  if (!nccl)
+    for (size_t si = 0; si < shards.size(); ++si) {
+      G[si].recv = recv_shared;
+      G[si].send = recv_shared + (size_t)si * recv_stride;
+    }
+
+  aknn_stats stats{};
+  for (aknn_index *ix : shards) stats.pairs += (int64_t)q * ix->n_local;
+  PhaseTimer tm(o.timing != 0, st, &ix0->events);
+  tm.start();
+  cudaEvent_t all_a = tm.open_a;
+  tm.open_a = nullptr;
+  unsigned int *h_active = nullptr;
+  CU(cudaMallocHost(&h_active, sizeof(unsigned int)));
+  struct HostFree {
+    unsigned int *p;
+    ~HostFree() { cudaFreeHost(p); }
+  } hf{h_active};
+  const size_t nS = shards.size();
+  aknn_status status = AKNN_OK;
+  for (int64_t r0 = 0; r0 < q; r0 += qb) {
+    const int qn = (int)std::min<int64_t>(qb, q - r0);
+    ++stats.query_batches;
+    tm.start();
+    for (size_t si = 0; si < nS; ++si) {
+      Geom &g = G[si];
+      g.q = qn;
+      g.qi0 = (uint32_t)(o.qi_offset + r0);
+      CU(cudaMemsetAsync(shards[si]->ws.as<uint8_t>(oQv[si]), 0, szQv[si], st));
+      CU(cudaMemcpy2DAsync(shards[si]->ws.as<uint8_t>(oQv[si]), g.pitch, queries_dev + r0 * d, d, d,
+                           qn, cudaMemcpyDeviceToDevice, st));
+      CU(cudaMemsetAsync(g.ctl, 0, sizeof(RoundCtl), st));
+      CU(launch_init(g, st));
+      stats.launches_init += 2;
+    }
+    tm.stop(PH_INIT);
+    if (!nccl && nS > 1) {  // shards add their counters into the output rows
+      if (out->draws) CU(cudaMemsetAsync(out->draws + r0, 0, sizeof(int64_t) * qn, st));
+      if (out->evals) CU(cudaMemsetAsync(out->evals + r0, 0, sizeof(int64_t) * qn, st));
+    }
+    int r = 0;
+    unsigned evaluated = (unsigned)qn;
+    for (;;) {
+      ++r;
+      tm.start();
+      for (size_t si = 0; si < nS; ++si) {
+        CU(cudaMemsetAsync(G[si].ctl, 0, offsetof(RoundCtl, advanced), st));
+        CU(launch_select_local(G[si], kg[si].nbits, st));
+        ++stats.launches_select;
+      }
+#ifdef AKNN_WITH_NCCL
+      if (nccl) {
+        if (ncclAllGather(G[0].send, const_cast<ShardRec *>(G[0].recv),
+                          (size_t)recv_stride * sizeof(ShardRec), ncclUint8, ix0->comm, st) != ncclSuccess)
+          return fail(AKNN_ENCCL, "ncclAllGather of the round summaries failed");
+      }
+#endif
+      for (size_t si = 0; si < nS; ++si) {
+        OutPtrs op{(int)r0, 0, 0, 0, (nccl || si == 0) ? out->sets : nullptr,
+                   (nccl || si == 0) ? out->dhat : nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+        CU(launch_merge(G[si], op, st));
+        ++stats.launches_select;
+      }
+      tm.stop(PH_SELECT);
+      stats.query_rounds += evaluated;
+      CU(cudaMemcpyAsync(h_active, &G[0].ctl->n_active, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      const unsigned nact = *h_active;
+      stats.blocked_query_rounds += nact;
+      evaluated = nact;
+      if (nact == 0) break;
+      if (o.max_rounds > 0 && r >= o.max_rounds) {
+        status = AKNN_EMAXROUNDS;
+        break;
+      }
+      tm.start();
+      for (size_t si = 0; si < nS; ++si) CU(launch_filter(G[si], st));
+      tm.stop(PH_FILTER);
+      stats.launches_filter += nS;
+      tm.start();
+      for (size_t si = 0; si < nS; ++si) CU(launch_compact(G[si], st));
+      tm.stop(PH_COMPACT);
+      stats.launches_compact += 2 * nS;
+      tm.start();
+      for (size_t si = 0; si < nS; ++si) CU(launch_advance(G[si], shards[si]->num_sms, st));
+      tm.stop(PH_ADVANCE);
+      stats.launches_advance += nS;
+      if (r > 1 + 64 * 64) return fail(AKNN_ECUDA, "round loop did not terminate (internal error)");
+    }
+    if (r > stats.rounds) stats.rounds = r;
+    tm.start();
+    for (size_t si = 0; si < nS; ++si) {
+      OutPtrs op{(int)r0, nccl ? 0 : shards[si]->offset, out_ncols, (!nccl && nS > 1) ? 1 : 0,
+                 nullptr, nullptr, out->counts, out->sums, out->evals, out->draws, out->rounds};
+      CU(launch_output_sharded(G[si], op, st));
+      stats.launches_output += (out->counts || out->sums) ? 2 : 1;
+    }
+#ifdef AKNN_WITH_NCCL
+    if (nccl) {
+      if (out->draws && ncclAllReduce(out->draws + r0, out->draws + r0, qn, ncclInt64, ncclSum, ix0->comm, st) != ncclSuccess)
+        return fail(AKNN_ENCCL, "ncclAllReduce(draws) failed");
+      if (out->evals && ncclAllReduce(out->evals + r0, out->evals + r0, qn, ncclInt64, ncclSum, ix0->comm, st) != ncclSuccess)
+        return fail(AKNN_ENCCL, "ncclAllReduce(evals) failed");
+    }
+#endif
+    tm.stop(PH_OUTPUT);
+    for (size_t si = 0; si < nS; ++si) {
+      RoundCtl ctl_h;
+      CU(cudaMemcpyAsync(&ctl_h, G[si].ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
+      std::vector<QState> qs(qn);
+      CU(cudaMemcpyAsync(qs.data(), G[si].qs, sizeof(QState) * qn, cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      stats.active_pair_rounds += (int64_t)ctl_h.advanced;
+      for (const QState &x : qs) {
+        stats.draws += x.draws;
+        stats.exact_fallbacks += x.nexact;
+      }
+    }
+    if (status != AKNN_OK) break;
+  }
+  tm.open_a = all_a;
+  tm.stop(PH_ALL);
+  CU(cudaStreamSynchronize(st));
+  double ms[PH_N];
+  tm.resolve(ms);
+  stats.ms_init = ms[PH_INIT];
+  stats.ms_select = ms[PH_SELECT];
+  stats.ms_filter = ms[PH_FILTER];
+  stats.ms_compact = ms[PH_COMPACT];
+  stats.ms_advance = ms[PH_ADVANCE];
+  stats.ms_output = ms[PH_OUTPUT];
+  stats.ms_total = ms[PH_ALL];
+  stats.kernel_launches = stats.launches_init + stats.launches_select + stats.launches_filter +
+                          stats.launches_compact + stats.launches_advance + stats.launches_output;
+  ix0->stats = stats;
   CU(cudaGetLastError());
   return status;
 }
@@ -542,7 +798,6 @@ aknn_status aknn_query_async(const aknn_index *cix, const uint8_t *queries_dev, 
   aknn_index *ix = const_cast<aknn_index *>(cix);
   TRY(check_query_args(ix, q, k, h, delta, out));
   if (q > 0 && !queries_dev) return fail(AKNN_EINVAL, "queries is NULL");
-  if (ix->world > 1) return fail(AKNN_EINVAL, "sharded query not implemented in this build");
   cudaStream_t st = (cudaStream_t)cuda_stream;
   const double *al = alpha_dev;
   if (!al) {
@@ -554,22 +809,27 @@ aknn_status aknn_query_async(const aknn_index *cix, const uint8_t *queries_dev, 
     al = ix->alpha.as<double>();
   }
   if (q == 0) return AKNN_OK;
+  if (ix->world > 1) {
+    std::vector<aknn_index *> one{ix};
+    return run_query_sharded(one, true, queries_dev, q, k, h, seed, al, opts, out, ix->n_local, st);
+  }
   return run_query(ix, queries_dev, ix->d, q, k, h, seed, al, opts, out, st);
 }
 
-aknn_status aknn_query_ex(const aknn_index *cix, const uint8_t *queries, int32_t q, int32_t k,
-                          int32_t h, double delta, uint64_t seed, const double *alpha,
-                          const aknn_opts *opts, aknn_result *out) {
-  aknn_index *ix = const_cast<aknn_index *>(cix);
-  TRY(check_query_args(ix, q, k, h, delta, out));
-  if (q > 0 && !queries) return fail(AKNN_EINVAL, "queries is NULL");
-  if (ix->world > 1) return fail(AKNN_EINVAL, "sharded query not implemented in this build");
+}  // extern "C"
+
+namespace {
+// Host-pointer query over one index (unsharded, or one NCCL shard) or over several
+// shards of one point set on the current device (multi = true).
+aknn_status host_query(const std::vector<aknn_index *> &shards, bool multi, const uint8_t *queries,
+                       int32_t q, int32_t k, int32_t h, double delta, uint64_t seed,
+                       const double *alpha, const aknn_opts *opts, aknn_result *out) {
+  aknn_index *ix = shards[0];
   if (q == 0) return AKNN_OK;
   cudaStream_t st = ix->stream;
   const int32_t d = ix->d;
-  const int64_t n = ix->n_local;
+  const int64_t n = multi ? ix->n_global : ix->n_local;  // row length of counts/sums
   const int kh = k + h;
-  // alpha
   std::vector<double> a(d + 1);
   if (alpha) {
     memcpy(a.data(), alpha, sizeof(double) * (d + 1));
@@ -598,8 +858,13 @@ aknn_status aknn_query_ex(const aknn_index *cix, const uint8_t *queries, int32_t
                    out->counts ? ix->outs.as<int32_t>(oCnt) : nullptr,
                    out->sums ? ix->outs.as<int64_t>(oSum) : nullptr, ix->outs.as<int64_t>(oEv),
                    ix->outs.as<int64_t>(oDr), ix->outs.as<int32_t>(oRo)};
-  aknn_status s = run_query(ix, ix->outs.as<uint8_t>(oQ), d, q, k, h, seed, ix->outs.as<double>(oA),
-                            opts, &dout, st);
+  aknn_status s;
+  if (multi || ix->world > 1)
+    s = run_query_sharded(shards, !multi, ix->outs.as<uint8_t>(oQ), q, k, h, seed,
+                          ix->outs.as<double>(oA), opts, &dout, n, st);
+  else
+    s = run_query(ix, ix->outs.as<uint8_t>(oQ), d, q, k, h, seed, ix->outs.as<double>(oA), opts,
+                  &dout, st);
   if (s != AKNN_OK && s != AKNN_EMAXROUNDS) return s;
   CU(cudaMemcpyAsync(out->sets, dout.sets, szSets, cudaMemcpyDeviceToHost, st));
   if (out->dhat) CU(cudaMemcpyAsync(out->dhat, dout.dhat, szDhat, cudaMemcpyDeviceToHost, st));
@@ -610,6 +875,47 @@ aknn_status aknn_query_ex(const aknn_index *cix, const uint8_t *queries, int32_t
   if (out->rounds) CU(cudaMemcpyAsync(out->rounds, dout.rounds, szRo, cudaMemcpyDeviceToHost, st));
   CU(cudaStreamSynchronize(st));
   return s;
+}
+}  // namespace
+
+extern "C" {
+
+aknn_status aknn_query_ex(const aknn_index *cix, const uint8_t *queries, int32_t q, int32_t k,
+                          int32_t h, double delta, uint64_t seed, const double *alpha,
+                          const aknn_opts *opts, aknn_result *out) {
+  aknn_index *ix = const_cast<aknn_index *>(cix);
+  TRY(check_query_args(ix, q, k, h, delta, out));
+  if (q > 0 && !queries) return fail(AKNN_EINVAL, "queries is NULL");
+  std::vector<aknn_index *> one{ix};
+  return host_query(one, false, queries, q, k, h, delta, seed, alpha, opts, out);
+}
+
+aknn_status aknn_query_multi(const aknn_index *const *shards, int32_t nshards, const uint8_t *queries,
+                             int32_t q, int32_t k, int32_t h, double delta, uint64_t seed,
+                             const double *alpha, const aknn_opts *opts, aknn_result *out) {
+  if (!shards || nshards < 1) return fail(AKNN_EINVAL, "need at least one shard");
+  std::vector<aknn_index *> v(nshards);
+  int64_t covered = 0;
+  int dev = -1;
+  CU(cudaGetDevice(&dev));
+  for (int32_t s = 0; s < nshards; ++s) {
+    v[s] = const_cast<aknn_index *>(shards[s]);
+    if (!v[s]) return fail(AKNN_EINVAL, "shard %d is NULL", s);
+    TRY(check_query_args(v[s], q, k, h, delta, out));
+    if (v[s]->world != 1) return fail(AKNN_EINVAL, "shard %d belongs to an NCCL communicator", s);
+    if (v[s]->device != dev) return fail(AKNN_EINVAL, "shard %d is not on the current device", s);
+    if (v[s]->d != v[0]->d || v[s]->n_global != v[0]->n_global)
+      return fail(AKNN_EINVAL, "shard %d has another dimension or n_global", s);
+    if (v[s]->offset != covered)
+      return fail(AKNN_EINVAL, "shards must tile [0, n_global) in order (shard %d starts at %lld, expected %lld)",
+                  s, (long long)v[s]->offset, (long long)covered);
+    covered += v[s]->n_local;
+  }
+  if (covered != v[0]->n_global)
+    return fail(AKNN_EINVAL, "shards cover %lld of n_global=%lld points", (long long)covered,
+                (long long)v[0]->n_global);
+  if (q > 0 && !queries) return fail(AKNN_EINVAL, "queries is NULL");
+  return host_query(v, true, queries, q, k, h, delta, seed, alpha, opts, out);
 }
 
 aknn_status aknn_query(const aknn_index *ix, const uint8_t *queries, int32_t q, int32_t k, int32_t h,

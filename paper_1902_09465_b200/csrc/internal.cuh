@@ -43,6 +43,15 @@ struct RoundCtl {
   unsigned long long advanced;            // pairs advanced, cumulative
 };
 
+// One arm as exchanged between point shards: its composite key
+// (global id in the low bits), exact integer sum S and level byte.  16 bytes.
+struct ShardRec {
+  unsigned long long key;
+  int32_t S;
+  uint8_t lvl;
+  uint8_t pad[3];
+};
+
 // Everything a round kernel needs, passed by value.
 struct Geom {
   const uint8_t *X;      // [n][pitch] points (zero padded)
@@ -63,9 +72,16 @@ struct Geom {
   uint32_t id_offset;    // global id of local row 0
   uint32_t qi0;          // RNG query index of batch row 0
   uint32_t seed_lo, seed_hi;
+  uint32_t rk0[10], rk1[10]; // Philox round keys of (seed_lo, seed_hi): kernel-param
+                             // constants, so each round's key XOR is one LOP3
   unsigned long long L;  // lcm(2^cmax, d): K = S * (L / T) is an exact order key
   unsigned long long Ld; // L / d
-  int ibits;             // bits of the local point index in the composite key
+  int ibits;             // bits of the local point index in a work-list code
+  int kbits;             // bits of the GLOBAL point id in the composite key
+  ShardRec *send;        // [q][k+h+1] this shard's summary (sharded query only)
+  const ShardRec *recv;  // [world][recv_stride] every shard's summary
+  int64_t recv_stride;   // records per shard slot of recv (qb * (k+h+1))
+  int world;             // shards taking part (1 = unsharded)
   int cmax;              // largest sampled level (2^cmax < d)
 };
 
@@ -83,27 +99,66 @@ __device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1
   return c;
 }
 
+// Same permutation with precomputed round keys rk0[r] = k0 + r*0x9E3779B9,
+// rk1[r] = k1 + r*0xBB67AE85 (kernel-parameter constants).
+__device__ __forceinline__ uint4 philox4x32_10_rk(uint4 c, const uint32_t *rk0, const uint32_t *rk1) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const unsigned long long p0 = (unsigned long long)0xD2511F53u * c.x;
+    const unsigned long long p1 = (unsigned long long)0xCD9E8D57u * c.z;
+    c = make_uint4((uint32_t)(p1 >> 32) ^ c.y ^ rk0[r], (uint32_t)p1,
+                   (uint32_t)(p0 >> 32) ^ c.w ^ rk1[r], (uint32_t)p0);
+  }
+  return c;
+}
+
 // Multiply-high map of a 32-bit word onto [0, d) (reading R5).
 __device__ __forceinline__ uint32_t coord_of(uint32_t w, uint32_t d) { return __umulhi(w, d); }
 
 // Exact order key of an arm: K = S * (L / T).  S/T ranks exactly like the
 // fp64 estimate S/(65025 T) (reading R9), and with the local index
 // in the low bits every key is unique: (d_hat, i) lexicographic order.
+// i is the LOCAL index; the key carries the global id i + id_offset, so keys of
+// different shards are comparable and unique.
 __device__ __forceinline__ unsigned long long arm_key(int32_t S, uint8_t l, uint32_t i,
                                                       const Geom &g) {
   const unsigned long long mul = (l == LVL_EXACT) ? g.Ld : (g.L >> l);
-  return (((unsigned long long)(uint32_t)S * mul) << g.ibits) | i;
+  return (((unsigned long long)(uint32_t)S * mul) << g.kbits) | (i + g.id_offset);
 }
 
 // d_hat = S / (T * 65025), one correctly rounded fp64 division (P:121-124,
 // DESIGN.md reading R15).  T * 65025 is exact in fp64.
-__device__ __forceinline__ double dhat_of(int32_t S, uint8_t l, int d) {
+__host__ __device__ __forceinline__ double dhat_of(int32_t S, uint8_t l, int d) {
   const double T = (l == LVL_EXACT) ? (double)d : (double)(1u << l);
+#ifdef __CUDA_ARCH__
   return __ddiv_rn((double)S, __dmul_rn(T, 65025.0));
+#else
+  return (double)S / (T * 65025.0);  // host: -ffp-contract=off, one rounding each
+#endif
 }
 
-__device__ __forceinline__ double alpha_of(uint8_t l, const double *alpha) {
+__host__ __device__ __forceinline__ double alpha_of(uint8_t l, const double *alpha) {
+#ifdef __CUDA_ARCH__
   return (l == LVL_EXACT) ? 0.0 : __ldg(alpha + (1u << l));
+#else
+  return (l == LVL_EXACT) ? 0.0 : alpha[1u << l];
+#endif
+}
+
+__host__ __device__ __forceinline__ double upper_of(int32_t S, uint8_t l, int d, const double *alpha) {
+#ifdef __CUDA_ARCH__
+  return __dadd_rn(dhat_of(S, l, d), alpha_of(l, alpha));
+#else
+  return dhat_of(S, l, d) + alpha_of(l, alpha);
+#endif
+}
+
+__host__ __device__ __forceinline__ double lower_of(int32_t S, uint8_t l, int d, const double *alpha) {
+#ifdef __CUDA_ARCH__
+  return __dsub_rn(dhat_of(S, l, d), alpha_of(l, alpha));
+#else
+  return dhat_of(S, l, d) - alpha_of(l, alpha);
+#endif
 }
 
 }  // namespace aknn

@@ -10,6 +10,9 @@ namespace aknn {
 // Device output pointers of one query batch (rows row0 .. row0 + q - 1).
 struct OutPtrs {
   int row0;
+  int64_t col0;     // first column of this shard in counts/sums rows
+  int64_t ncols;    // row length of counts/sums
+  int accumulate;   // 1: atomically add draws/evals (several shards, one device)
   int32_t *sets;
   double *dhat;
   int32_t *counts;
@@ -25,6 +28,11 @@ cudaError_t launch_filter(const Geom &g, cudaStream_t s);
 cudaError_t launch_compact(const Geom &g, cudaStream_t s);
 cudaError_t launch_advance(const Geom &g, int num_sms, cudaStream_t s);
 cudaError_t launch_output(const Geom &g, const OutPtrs &o, cudaStream_t s);
+// Sharded rounds (shard_kernels.cu).
+cudaError_t launch_select_local(const Geom &g, int nbits, cudaStream_t s);
+cudaError_t launch_merge(const Geom &g, const OutPtrs &o, cudaStream_t s);
+cudaError_t launch_output_sharded(const Geom &g, const OutPtrs &o, cudaStream_t s);
+size_t merge_smem_bytes(int world, int kh);
 int output_max_kh();
 
 // Exact comparison pass (exact_kernels.cu).

@@ -1,0 +1,48 @@
+// round_common.cuh -- per-arm state access shared by the round kernels.
+#pragma once
+#include "internal.cuh"
+#include "select.cuh"
+
+namespace aknn {
+
+// ---------------------------------------------------------------------------
+// Pair state loading: 4 consecutive arms of query row `qi` starting at i0
+// (i0 % 4 == 0, rows padded to npad % 16 == 0, so the loads are aligned).
+struct Arm4 {
+  int32_t S[4];
+  uint8_t l[4];
+};
+
+__device__ __forceinline__ Arm4 load_arm4(const Geom &g, int qi, int i0) {
+  Arm4 a;
+  const int4 s = *reinterpret_cast<const int4 *>(g.S + (size_t)qi * g.npad + i0);
+  const uint32_t lv = *reinterpret_cast<const uint32_t *>(g.lvl + (size_t)qi * g.npad + i0);
+  a.S[0] = s.x; a.S[1] = s.y; a.S[2] = s.z; a.S[3] = s.w;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) a.l[e] = (uint8_t)(lv >> (8 * e));
+  return a;
+}
+
+struct ArmKeys {
+  const Geom *g;
+  int qi;
+  __device__ __forceinline__ void operator()(int i0, unsigned long long key[4]) const {
+    if (i0 >= g->n) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) key[e] = KEY_INVALID;
+      return;
+    }
+    const Arm4 a = load_arm4(*g, qi, i0);
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      key[e] = (i0 + e < g->n) ? arm_key(a.S[e], a.l[e], (uint32_t)(i0 + e), *g) : KEY_INVALID;
+  }
+};
+
+struct Best {
+  double v;
+  int i;
+  double a;
+};
+
+}  // namespace aknn

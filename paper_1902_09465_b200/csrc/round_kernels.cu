@@ -16,26 +16,9 @@
 #include "internal.cuh"
 #include "launch.h"
 #include "select.cuh"
+#include "round_common.cuh"
 
 namespace aknn {
-
-// ---------------------------------------------------------------------------
-// Pair state loading: 4 consecutive arms of query row `qi` starting at i0
-// (i0 % 4 == 0, rows padded to npad % 16 == 0, so the loads are aligned).
-struct Arm4 {
-  int32_t S[4];
-  uint8_t l[4];
-};
-
-__device__ __forceinline__ Arm4 load_arm4(const Geom &g, int qi, int i0) {
-  Arm4 a;
-  const int4 s = *reinterpret_cast<const int4 *>(g.S + (size_t)qi * g.npad + i0);
-  const uint32_t lv = *reinterpret_cast<const uint32_t *>(g.lvl + (size_t)qi * g.npad + i0);
-  a.S[0] = s.x; a.S[1] = s.y; a.S[2] = s.z; a.S[3] = s.w;
-#pragma unroll
-  for (int e = 0; e < 4; ++e) a.l[e] = (uint8_t)(lv >> (8 * e));
-  return a;
-}
 
 // ---------------------------------------------------------------------------
 // a2: initialisation -- S_i = (X[i][j] - x[j])^2 for j = Draw(i, 0), T_i = 1.
@@ -72,28 +55,6 @@ __global__ void k_init_qstate(Geom g) {
   s.nexact = 0;
   g.qs[qi] = s;
 }
-
-struct ArmKeys {
-  const Geom *g;
-  int qi;
-  __device__ __forceinline__ void operator()(int i0, unsigned long long key[4]) const {
-    if (i0 >= g->n) {
-#pragma unroll
-      for (int e = 0; e < 4; ++e) key[e] = KEY_INVALID;
-      return;
-    }
-    const Arm4 a = load_arm4(*g, qi, i0);
-#pragma unroll
-    for (int e = 0; e < 4; ++e)
-      key[e] = (i0 + e < g->n) ? arm_key(a.S[e], a.l[e], (uint32_t)(i0 + e), *g) : KEY_INVALID;
-  }
-};
-
-struct Best {
-  double v;
-  int i;
-  double a;
-};
 
 // a6 + a7: rank split, d1/d2/A/B, Eq. (5).  One CTA per query.
 __global__ void __launch_bounds__(SEL_NT) k_select(Geom g, int nbits) {
@@ -234,8 +195,23 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
   }
 }
 
-// Pairs per warp-chunk for level c (2^c draws = ceil(2^c / 4) Philox blocks).
+// Work decomposition of one advance level c (s = 2^c draws = nb Philox blocks of 4
+// draws per pair).  Every lane runs ADV_P independent Philox blocks at a time (ILP
+// across the 10 dependent rounds):
+//   nb <= ADV_P        a lane owns ADV_P / nb whole pairs (no cross-lane reduce)
+//   nb <= 32 * ADV_P   nb / ADV_P lanes per pair (shuffle reduce inside the group)
+//   otherwise          a warp per pair, lanes loop over ADV_P-block groups
+// Exact fallbacks (slot MAX_LEVELS): ADV_XP pairs per warp, rows streamed with
+// 16-B loads.  A warp-chunk is one warp's share of a slot.
+constexpr int ADV_P = 4;
+constexpr int ADV_XP = 4;
+
 __host__ __device__ __forceinline__ unsigned nblk_of(int c) { return c < 2 ? 1u : (1u << (c - 2)); }
+__host__ __device__ __forceinline__ unsigned pairs_per_chunk(int slot) {
+  if (slot == MAX_LEVELS) return ADV_XP;
+  const unsigned nb = nblk_of(slot);
+  return nb >= 32u * ADV_P ? 1u : 32u * ADV_P / nb;
+}
 
 __global__ void k_plan(RoundCtl *ctl) {
   if (threadIdx.x != 0) return;
@@ -248,12 +224,8 @@ __global__ void k_plan(RoundCtl *ctl) {
     ctl->cursor[s] = 0;
     off += c;
     adv += c;
-    if (s == MAX_LEVELS) {
-      ch += c;  // one warp per exact pair
-    } else {
-      const unsigned nb = nblk_of(s);
-      ch += nb <= 32 ? (c + (32 / nb) - 1) / (32 / nb) : c;
-    }
+    const unsigned ppc = pairs_per_chunk(s);
+    ch += (c + ppc - 1) / ppc;
   }
   ctl->off[NSLOT] = off;
   ctl->chunk_off[NSLOT] = ch;
@@ -289,44 +261,102 @@ __global__ void __launch_bounds__(FIL_NT) k_scatter(Geom g) {
 // a3 + a4: advance every listed pair.  Grid-stride over warp-chunks.
 constexpr int ADV_NT = 256;
 
-// Sum of the squared differences of the draws u = 4*blk .. 4*blk+3 (< s) of
-// pair (qi, i) at level b = c + 1 (T -> 2T, t = T + u).
-__device__ __forceinline__ uint32_t draw_block(const Geom &g, uint32_t qi, uint32_t i, int c,
-                                               uint32_t blk, uint32_t s) {
-  const uint4 w = philox4x32_10(make_uint4(blk, i + g.id_offset, qi + g.qi0, (uint32_t)(c + 1)),
-                                g.seed_lo, g.seed_hi);
-  const uint8_t *xr = g.X + (size_t)i * g.pitch;
-  const uint8_t *qr = g.Q + (size_t)qi * g.pitch;
-  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-  uint32_t acc = 0;
-  const uint32_t u0 = blk * 4;
+// Sum of the squared differences of the draws u = 4*blk .. 4*blk+3 (< s) of pair
+// (qi, i) at level b = c + 1 (T -> 2T, t = T + u), for ADV_P blocks at once.
+struct BlockTask {
+  const uint8_t *xr, *qr;  // rows of X and of the query
+  uint32_t i, qi, blk;      // global point id, RNG query index, Philox block
+  bool valid;
+};
+
+__device__ __forceinline__ void draw_blocks(const Geom &g, const BlockTask (&t)[ADV_P], int c,
+                                            uint32_t s, uint32_t (&acc)[ADV_P]) {
+  uint4 w[ADV_P];
 #pragma unroll
-  for (int t = 0; t < 4; ++t) {
-    if (u0 + t < s) {
-      const uint32_t j = coord_of(ws[t], (uint32_t)g.d);
-      const int diff = (int)__ldg(xr + j) - (int)__ldg(qr + j);
-      acc += (uint32_t)(diff * diff);
+  for (int k = 0; k < ADV_P; ++k)
+    w[k] = philox4x32_10_rk(make_uint4(t[k].blk, t[k].i, t[k].qi, (uint32_t)(c + 1)), g.rk0, g.rk1);
+#pragma unroll
+  for (int k = 0; k < ADV_P; ++k) {
+    const uint32_t ws[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
+    uint32_t a = 0;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      // s < 4 only at levels 0 and 1 (1 and 2 draws); the word is discarded
+      if (t[k].valid && (s >= 4 || (uint32_t)e < s)) {
+        const uint32_t j = coord_of(ws[e], (uint32_t)g.d);
+        const int diff = (int)__ldg(t[k].xr + j) - (int)__ldg(t[k].qr + j);
+        a += (uint32_t)(diff * diff);
+      }
     }
+    acc[k] = a;
   }
-  return acc;
 }
 
-__device__ __forceinline__ uint32_t exact_row(const Geom &g, uint32_t qi, uint32_t i) {
-  const uint4 *xr = reinterpret_cast<const uint4 *>(g.X + (size_t)i * g.pitch);
-  const uint4 *qr = reinterpret_cast<const uint4 *>(g.Q + (size_t)qi * g.pitch);
+__device__ __forceinline__ void decode(const Geom &g, uint32_t code, uint32_t imask, uint32_t &qi,
+                                       uint32_t &i) {
+  qi = code >> g.ibits;
+  i = code & imask;
+}
+
+__device__ __forceinline__ void commit(const Geom &g, uint32_t qi, uint32_t i, uint32_t add,
+                                       uint8_t lvl) {
+  const size_t o = (size_t)qi * g.npad + i;
+  g.S[o] += (int32_t)add;
+  g.lvl[o] = lvl;
+}
+
+// Exact fallback of up to ADV_XP pairs per warp: S = sum_j (x_j - q_j)^2.
+__device__ __forceinline__ void exact_rows(const Geom &g, const uint32_t *codes, unsigned cnt,
+                                           uint32_t imask) {
+  const int lane = lane_id();
   const int nv = (int)(g.pitch >> 4);
-  uint32_t acc = 0;
-  for (int v = lane_id(); v < nv; v += 32) {
-    const uint4 a = __ldg(xr + v), b = __ldg(qr + v);
-    uint32_t t;
-    t = __vabsdiffu4(a.x, b.x); acc = __dp4a(t, t, acc);
-    t = __vabsdiffu4(a.y, b.y); acc = __dp4a(t, t, acc);
-    t = __vabsdiffu4(a.z, b.z); acc = __dp4a(t, t, acc);
-    t = __vabsdiffu4(a.w, b.w); acc = __dp4a(t, t, acc);
+  const uint4 *xr[ADV_XP], *qr[ADV_XP];
+  uint32_t acc[ADV_XP];
+#pragma unroll
+  for (int p = 0; p < ADV_XP; ++p) {
+    uint32_t qi = 0, i = 0;
+    if ((unsigned)p < cnt) decode(g, codes[p], imask, qi, i);
+    xr[p] = reinterpret_cast<const uint4 *>(g.X + (size_t)i * g.pitch);
+    qr[p] = reinterpret_cast<const uint4 *>(g.Q + (size_t)qi * g.pitch);
+    acc[p] = 0;
+  }
+  for (int v0 = 0; v0 < nv; v0 += 64) {
+    uint4 a[ADV_XP][2], b[ADV_XP][2];
+#pragma unroll
+    for (int p = 0; p < ADV_XP; ++p)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int v = v0 + h * 32 + lane;
+        const bool ok = (unsigned)p < cnt && v < nv;
+        a[p][h] = ok ? __ldg(xr[p] + v) : make_uint4(0, 0, 0, 0);
+        b[p][h] = ok ? __ldg(qr[p] + v) : make_uint4(0, 0, 0, 0);
+      }
+#pragma unroll
+    for (int p = 0; p < ADV_XP; ++p)
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        uint32_t t;
+        t = __vabsdiffu4(a[p][h].x, b[p][h].x); acc[p] = __dp4a(t, t, acc[p]);
+        t = __vabsdiffu4(a[p][h].y, b[p][h].y); acc[p] = __dp4a(t, t, acc[p]);
+        t = __vabsdiffu4(a[p][h].z, b[p][h].z); acc[p] = __dp4a(t, t, acc[p]);
+        t = __vabsdiffu4(a[p][h].w, b[p][h].w); acc[p] = __dp4a(t, t, acc[p]);
+      }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
-  return acc;
+  for (int p = 0; p < ADV_XP; ++p)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc[p] += __shfl_xor_sync(FULL, acc[p], o);
+  if (lane < ADV_XP && (unsigned)lane < cnt) {
+    uint32_t mine = acc[0];
+#pragma unroll
+    for (int p = 1; p < ADV_XP; ++p)
+      if (lane == p) mine = acc[p];
+    uint32_t qi, i;
+    decode(g, codes[lane], imask, qi, i);
+    const size_t o = (size_t)qi * g.npad + i;
+    g.S[o] = (int32_t)mine;
+    g.lvl[o] = LVL_EXACT;
+  }
 }
 
 __global__ void __launch_bounds__(ADV_NT) k_advance(Geom g) {
@@ -350,47 +380,87 @@ __global__ void __launch_bounds__(ADV_NT) k_advance(Geom g) {
     while (coff[slot + 1] <= ch) ++slot;  // chunks are visited in increasing order
     const unsigned long long rel = ch - coff[slot];
     if (slot == MAX_LEVELS) {
-      const uint32_t code = g.list[soff[slot] + rel];
-      const uint32_t qi = code >> g.ibits, i = code & imask;
-      const uint32_t acc = exact_row(g, qi, i);
-      if (lane == 0) {
-        const size_t o = (size_t)qi * g.npad + i;
-        g.S[o] = (int32_t)acc;
-        g.lvl[o] = LVL_EXACT;
-      }
+      const unsigned p0 = (unsigned)rel * ADV_XP;
+      const unsigned cnt = min((unsigned)ADV_XP, scnt[slot] - p0);
+      exact_rows(g, g.list + soff[slot] + p0, cnt, imask);
       continue;
     }
     const int c = slot;
     const uint32_t s = 1u << c;
     const unsigned nb = nblk_of(c);
-    if (nb <= 32) {
-      const unsigned ppw = 32 / nb;
-      const unsigned long long p = rel * ppw + lane / nb;
-      const uint32_t blk = lane % nb;
-      const bool valid = p < scnt[c];
-      uint32_t code = 0, acc = 0;
-      if (valid) {
-        code = g.list[soff[c] + p];
-        acc = draw_block(g, code >> g.ibits, code & imask, c, blk, s);
-      }
-      for (unsigned o = nb >> 1; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
-      if (valid && blk == 0) {
-        const size_t o = (size_t)(code >> g.ibits) * g.npad + (code & imask);
-        g.S[o] += (int32_t)acc;
-        g.lvl[o] = (uint8_t)(c + 1);
-      }
-    } else {
-      const uint32_t code = g.list[soff[c] + rel];
-      const uint32_t qi = code >> g.ibits, i = code & imask;
-      uint32_t acc = 0;
-      for (uint32_t blk = lane; blk < nb; blk += 32) acc += draw_block(g, qi, i, c, blk, s);
+    const uint8_t newlvl = (uint8_t)(c + 1);
+    const unsigned ppc = pairs_per_chunk(c);
+    const unsigned pbase = (unsigned)rel * ppc;  // first pair of this chunk
+    const uint32_t *lst = g.list + soff[c];
+    const unsigned cnt = scnt[c];
+    if (nb <= (unsigned)ADV_P) {
+      // lane owns ppt pairs: pbase + j*32 + lane, each with nb blocks
+      constexpr int dummy = 0;
+      (void)dummy;
+      const unsigned ppt = ADV_P / nb;
+      BlockTask t[ADV_P];
+      uint32_t code[ADV_P];
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(FULL, acc, o);
-      if (lane == 0) {
-        const size_t o = (size_t)qi * g.npad + i;
-        g.S[o] += (int32_t)acc;
-        g.lvl[o] = (uint8_t)(c + 1);
+      for (int k = 0; k < ADV_P; ++k) {
+        const unsigned j = k / nb, blk = k % nb;  // nb is a power of two <= ADV_P
+        const unsigned p = pbase + j * 32 + lane;
+        const bool ok = j < ppt && p < cnt;
+        uint32_t qi = 0, i = 0;
+        code[k] = ok ? lst[p] : 0u;
+        decode(g, code[k], imask, qi, i);
+        t[k] = BlockTask{g.X + (size_t)i * g.pitch, g.Q + (size_t)qi * g.pitch, i + g.id_offset,
+                         qi + g.qi0, blk, ok};
       }
+      uint32_t acc[ADV_P];
+      draw_blocks(g, t, c, s, acc);
+#pragma unroll
+      for (int k = 0; k < ADV_P; ++k) {
+        if (k % nb != 0 || !t[k].valid) continue;
+        uint32_t sum = 0;
+#pragma unroll
+        for (int e = 0; e < ADV_P; ++e)
+          if (e / nb == k / nb) sum += acc[e];
+        uint32_t qi, i;
+        decode(g, code[k], imask, qi, i);
+        commit(g, qi, i, sum, newlvl);
+      }
+    } else if (nb <= 32u * ADV_P) {
+      // tpp lanes per pair; lane group gi handles blocks [sub*ADV_P, sub*ADV_P + ADV_P)
+      const unsigned tpp = nb / ADV_P;
+      const unsigned p = pbase + lane / tpp, sub = lane % tpp;
+      const bool ok = p < cnt;
+      const uint32_t cd = ok ? lst[p] : 0u;
+      uint32_t qi, i;
+      decode(g, cd, imask, qi, i);
+      BlockTask t[ADV_P];
+#pragma unroll
+      for (int k = 0; k < ADV_P; ++k)
+        t[k] = BlockTask{g.X + (size_t)i * g.pitch, g.Q + (size_t)qi * g.pitch, i + g.id_offset,
+                         qi + g.qi0, sub * ADV_P + k, ok};
+      uint32_t acc[ADV_P];
+      draw_blocks(g, t, c, s, acc);
+      uint32_t sum = acc[0] + acc[1] + acc[2] + acc[3];
+      for (unsigned o = tpp >> 1; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+      if (ok && sub == 0) commit(g, qi, i, sum, newlvl);
+    } else {
+      // one warp per pair; lanes loop over groups of ADV_P blocks
+      const uint32_t cd = lst[pbase];
+      uint32_t qi, i;
+      decode(g, cd, imask, qi, i);
+      const uint8_t *xr = g.X + (size_t)i * g.pitch, *qr = g.Q + (size_t)qi * g.pitch;
+      uint32_t sum = 0;
+      for (unsigned b0 = lane * ADV_P; b0 < nb; b0 += 32 * ADV_P) {
+        BlockTask t[ADV_P];
+#pragma unroll
+        for (int k = 0; k < ADV_P; ++k)
+          t[k] = BlockTask{xr, qr, i + g.id_offset, qi + g.qi0, b0 + k, true};
+        uint32_t acc[ADV_P];
+        draw_blocks(g, t, c, s, acc);
+        sum += acc[0] + acc[1] + acc[2] + acc[3];
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+      if (lane == 0) commit(g, qi, i, sum, newlvl);
     }
   }
 }
@@ -452,7 +522,7 @@ __global__ void k_counts(Geom g, OutPtrs o) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= g.n) return;
   const size_t src = (size_t)qi * g.npad + i;
-  const size_t dst = (size_t)(o.row0 + qi) * g.n + i;
+  const size_t dst = (size_t)(o.row0 + qi) * o.ncols + o.col0 + i;
   const uint8_t l = g.lvl[src];
   if (o.counts) o.counts[dst] = (l == LVL_EXACT) ? g.d : (int32_t)(1u << l);
   if (o.sums) o.sums[dst] = (int64_t)(uint32_t)g.S[src];
