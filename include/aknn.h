@@ -201,6 +201,41 @@ aknn_status aknn_exact_async(const aknn_index *ix, const uint8_t *queries_dev, i
                              void *cuda_stream);
 
 /* ------------------------------------------------------------------------ */
+/* Host reference of the shard exchange.  Not on the hot path:  */
+/* the same records, keys and merge the device kernels use, so the N > 1      */
+/* protocol can be tested on CPUs (gloo) without a GPU.                        */
+/* ------------------------------------------------------------------------ */
+
+/* A shard record is 16 bytes: uint64 composite key (exact order key of the
+ * estimate S/(65025 T) in the high bits, GLOBAL id in the low bits), int32 S,
+ * uint8 level (log2 T, 0xFF = exact), 3 pad bytes.                            */
+#define AKNN_SHARD_REC_BYTES 16
+
+/* Summary of one query's arms on one shard: the k+h smallest composite keys
+ * (ascending) then the arm with the smallest L = d_hat - alpha among the rest
+ * (ties: smaller id) -> recs_out[(k+h+1) * 16 bytes].  S, lvl: [n_local] arm
+ * state (lvl = log2 T or 0xFF for exact); ids are offset + i.                 */
+aknn_status aknn_shard_summary_host(const int32_t *S, const uint8_t *lvl, int64_t n_local,
+                                    int64_t offset, int64_t n_global, int32_t d, int32_t k,
+                                    int32_t h, const double *alpha, void *recs_out);
+
+typedef struct {
+  int32_t *sets;         /* [k+h] global ids of ranks 1..k+h (required)          */
+  double *dhat;          /* [k+h] their estimates (nullable)                     */
+  uint64_t thr_k, thr_kh;/* composite keys of ranks k and k+h                    */
+  double A, B;           /* Eq. (2)-(3) bounds                       */
+  int64_t d1, d2;        /* their global ids                                     */
+  double alpha_d2;       /* alpha of d2 (the middle-set rule, Eq. 4 batched)     */
+  int32_t stop;          /* 1 iff A <= B, Eq. (5)                                */
+} aknn_merge_result;
+
+/* Merge `world` summaries (recs: [world][(k+h+1) * 16 bytes], rank order) of
+ * one query into the global round quantities, exactly as k_merge does.       */
+aknn_status aknn_shard_merge_host(const void *recs, int32_t world, int64_t n_global, int32_t d,
+                                  int32_t k, int32_t h, const double *alpha,
+                                  aknn_merge_result *res);
+
+/* ------------------------------------------------------------------------ */
 /* Confidence radius tables (host).                                           */
 /* ------------------------------------------------------------------------ */
 

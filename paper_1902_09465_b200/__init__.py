@@ -60,6 +60,15 @@ class Stats(C.Structure):
                 ("launches_advance", C.c_int64), ("launches_output", C.c_int64)]
 
 
+class MergeResult(C.Structure):
+    _fields_ = [("sets", C.c_void_p), ("dhat", C.c_void_p), ("thr_k", C.c_uint64),
+                ("thr_kh", C.c_uint64), ("A", C.c_double), ("B", C.c_double),
+                ("d1", C.c_int64), ("d2", C.c_int64), ("alpha_d2", C.c_double),
+                ("stop", C.c_int32)]
+
+
+SHARD_REC_BYTES = 16
+
 _P = C.c_void_p
 _I = C.c_int32
 _L = C.c_int64
@@ -76,6 +85,8 @@ _sig = {
     "aknn_query_multi": ([C.POINTER(_P), _I, _P, _I, _I, _I, C.c_double, C.c_uint64, _P,
                           C.POINTER(Opts), C.POINTER(Result)], _I),
     "aknn_get_stats": ([_P, C.POINTER(Stats)], _I),
+    "aknn_shard_summary_host": ([_P, _P, _L, _L, _L, _I, _I, _I, _P, _P], _I),
+    "aknn_shard_merge_host": ([_P, _I, _L, _I, _I, _I, _P, C.POINTER(MergeResult)], _I),
     "aknn_exact": ([_P, _P, _I, _I, _P, _P], _I),
     "aknn_exact_async": ([_P, _P, _I, _I, _P, _P, _P], _I),
     "aknn_alpha_table": ([_I, _L, C.c_double, C.c_double, _I, _P], _I),
@@ -141,6 +152,30 @@ def query_multi(shards, queries, k: int, h: int, delta: float, seed: int = 0, al
     if st != AKNN_EMAXROUNDS:
         _check(st)
     return out
+
+
+def shard_summary_host(S, lvl, offset: int, n_global: int, d: int, k: int, h: int,
+                       alpha) -> np.ndarray:
+    """aknn_shard_summary_host: one query's shard summary as (k+h+1)*16 raw bytes."""
+    S = np.ascontiguousarray(S, np.int32)
+    lvl = np.ascontiguousarray(lvl, np.uint8)
+    al = np.ascontiguousarray(alpha, np.float64)
+    out = np.zeros((k + h + 1) * SHARD_REC_BYTES, np.uint8)
+    _check(_lib.aknn_shard_summary_host(_ptr(S), _ptr(lvl), S.shape[0], offset, n_global, d, k, h,
+                                        _ptr(al), _ptr(out)))
+    return out
+
+
+def shard_merge_host(recs, world: int, n_global: int, d: int, k: int, h: int, alpha) -> dict:
+    """aknn_shard_merge_host on the concatenated summaries of `world` shards."""
+    recs = np.ascontiguousarray(recs, np.uint8)
+    al = np.ascontiguousarray(alpha, np.float64)
+    sets = np.zeros(k + h, np.int32)
+    dh = np.zeros(k + h, np.float64)
+    r = MergeResult(sets.ctypes.data, dh.ctypes.data, 0, 0, 0.0, 0.0, 0, 0, 0.0, 0)
+    _check(_lib.aknn_shard_merge_host(_ptr(recs), world, n_global, d, k, h, _ptr(al), C.byref(r)))
+    return dict(sets=sets, dhat=dh, thr_k=r.thr_k, thr_kh=r.thr_kh, A=r.A, B=r.B, d1=r.d1,
+                d2=r.d2, alpha_d2=r.alpha_d2, stop=bool(r.stop))
 
 
 def nccl_unique_id() -> bytes:

@@ -7,6 +7,7 @@
 // active-query count -> k_filter/k_plan/k_scatter -> k_advance}, then
 // k_output.  Every device step is a kernel of round_kernels.cu; the host
 // only sequences launches and validates arguments.
+#include <algorithm>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -921,6 +922,106 @@ aknn_status aknn_query_multi(const aknn_index *const *shards, int32_t nshards, c
 aknn_status aknn_query(const aknn_index *ix, const uint8_t *queries, int32_t q, int32_t k, int32_t h,
                        double delta, uint64_t seed, const double *alpha, aknn_result *out) {
   return aknn_query_ex(ix, queries, q, k, h, delta, seed, alpha, nullptr, out);
+}
+
+// ---------------------------------------------------------------------------
+// Host reference of the shard protocol (the same records, keys, tie rules and
+// merge as k_select_local / k_merge), for CPU tests of the N > 1 exchange.
+namespace {
+struct HostKey {
+  KeyGeom kg;
+  unsigned long long key(int32_t S, uint8_t l, uint32_t gid) const {
+    const unsigned long long mul = (l == LVL_EXACT) ? kg.Ld : (kg.L >> l);
+    return (((unsigned long long)(uint32_t)S * mul) << kg.kbits) | gid;
+  }
+};
+}  // namespace
+
+aknn_status aknn_shard_summary_host(const int32_t *S, const uint8_t *lvl, int64_t n_local,
+                                    int64_t offset, int64_t n_global, int32_t d, int32_t k,
+                                    int32_t h, const double *alpha, void *recs_out) {
+  if (!S || !lvl || !alpha || !recs_out) return fail(AKNN_EINVAL, "NULL argument");
+  if (k < 1 || h < 0 || (int64_t)k + h >= n_local || d < 1)
+    return fail(AKNN_EINVAL, "need k >= 1, h >= 0, k + h < n_local, d >= 1");
+  HostKey hk;
+  TRY(key_geom(n_local, n_global, d, &hk.kg));
+  const int kh = k + h;
+  std::vector<std::pair<unsigned long long, int64_t>> v((size_t)n_local);
+  for (int64_t i = 0; i < n_local; ++i) v[i] = {hk.key(S[i], lvl[i], (uint32_t)(i + offset)), i};
+  std::nth_element(v.begin(), v.begin() + (kh - 1), v.end());
+  const unsigned long long th = v[kh - 1].first;
+  ShardRec *out = static_cast<ShardRec *>(recs_out);
+  int p = 0;
+  int64_t best = -1;
+  double bl = 0.0;
+  for (int64_t i = 0; i < n_local; ++i) {
+    const unsigned long long kk = hk.key(S[i], lvl[i], (uint32_t)(i + offset));
+    if (kk <= th) {
+      ShardRec r{};
+      r.key = kk;
+      r.S = S[i];
+      r.lvl = lvl[i];
+      out[p++] = r;
+    } else {
+      const double L = lower_of(S[i], lvl[i], d, alpha);
+      if (best < 0 || L < bl) {  // ascending i: ties keep the smaller id
+        best = i;
+        bl = L;
+      }
+    }
+  }
+  std::sort(out, out + kh, [](const ShardRec &a, const ShardRec &b) { return a.key < b.key; });
+  ShardRec r{};
+  r.key = hk.key(S[best], lvl[best], (uint32_t)(best + offset));
+  r.S = S[best];
+  r.lvl = lvl[best];
+  out[kh] = r;
+  return AKNN_OK;
+}
+
+aknn_status aknn_shard_merge_host(const void *recs, int32_t world, int64_t n_global, int32_t d,
+                                  int32_t k, int32_t h, const double *alpha, aknn_merge_result *res) {
+  if (!recs || !alpha || !res || !res->sets) return fail(AKNN_EINVAL, "NULL argument");
+  if (world < 1 || k < 1 || h < 0) return fail(AKNN_EINVAL, "need world >= 1, k >= 1, h >= 0");
+  KeyGeom kg;
+  TRY(key_geom(n_global, n_global, d, &kg));
+  const int kh = k + h;
+  const ShardRec *rc = static_cast<const ShardRec *>(recs);
+  std::vector<const ShardRec *> top;
+  for (int w = 0; w < world; ++w)
+    for (int r = 0; r < kh; ++r) top.push_back(rc + (size_t)w * (kh + 1) + r);
+  std::sort(top.begin(), top.end(), [](const ShardRec *a, const ShardRec *b) { return a->key < b->key; });
+  const unsigned long long gmask = (1ull << kg.kbits) - 1ull;
+  auto gid = [&](const ShardRec *r) { return (int64_t)(r->key & gmask); };
+  // d1 = argmax U over ranks 1..k (Eq. 2), ties to the smaller id
+  const ShardRec *b1 = nullptr;
+  double A = 0.0;
+  for (int t = 0; t < k; ++t) {
+    const double U = upper_of(top[t]->S, top[t]->lvl, d, alpha);
+    if (!b1 || U > A || (U == A && gid(top[t]) < gid(b1))) { b1 = top[t]; A = U; }
+  }
+  // d2 = argmin L over ranks > k+h and every shard's remainder arm (Eq. 3)
+  std::vector<const ShardRec *> far(top.begin() + kh, top.end());
+  for (int w = 0; w < world; ++w) far.push_back(rc + (size_t)w * (kh + 1) + kh);
+  const ShardRec *b2 = nullptr;
+  double B = 0.0;
+  for (const ShardRec *r : far) {
+    const double L = lower_of(r->S, r->lvl, d, alpha);
+    if (!b2 || L < B || (L == B && gid(r) < gid(b2))) { b2 = r; B = L; }
+  }
+  for (int t = 0; t < kh; ++t) {
+    res->sets[t] = (int32_t)gid(top[t]);
+    if (res->dhat) res->dhat[t] = dhat_of(top[t]->S, top[t]->lvl, d);
+  }
+  res->thr_k = top[k - 1]->key;
+  res->thr_kh = top[kh - 1]->key;
+  res->A = A;
+  res->B = B;
+  res->d1 = gid(b1);
+  res->d2 = gid(b2);
+  res->alpha_d2 = alpha_of(b2->lvl, alpha);
+  res->stop = A <= B;  // Eq. (5)
+  return AKNN_OK;
 }
 
 aknn_status aknn_get_stats(const aknn_index *ix, aknn_stats *out) {
