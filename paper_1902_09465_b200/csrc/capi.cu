@@ -11,6 +11,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -129,6 +130,8 @@ struct aknn_index {
   DevBuf alpha;            // [d+1]
   DevBuf outs;             // device outputs for the host API
   DevBuf exact_ws;
+  DevBuf nx;               // [n_local] ||x_i||^2 for the tensor-core exact pass (lazy)
+  bool nx_ready = false;
   EventPool events;
   int rank = 0, world = 1;
 #ifdef AKNN_WITH_NCCL
@@ -1046,11 +1049,19 @@ aknn_status aknn_exact_async(const aknn_index *cix, const uint8_t *queries_dev, 
   if (e.nbits > 63) return fail(AKNN_EINVAL, "exact key needs %d bits", e.nbits);
   // process queries in chunks so the distance scratch stays bounded
   const int64_t qc = std::max<int64_t>(1, std::min<int64_t>(q, (int64_t)(2ll << 30) / (npad * 4)));
-  const size_t szD = (size_t)qc * npad * 4, szQ = (size_t)qc * ix->pitch;
-  TRY(ix->exact_ws.ensure(round_up(szD, 256) + szQ));
+  const size_t szD = (size_t)qc * npad * 4, szQ = (size_t)qc * ix->pitch, szN = (size_t)qc * 4;
+  TRY(ix->exact_ws.ensure(round_up(szD, 256) + round_up(szQ, 256) + szN));
+  static const bool use_dp4a = getenv("AKNN_EXACT_DP4A") && getenv("AKNN_EXACT_DP4A")[0] == '1';
+  if (!use_dp4a && !ix->nx_ready) {
+    TRY(ix->nx.ensure(sizeof(int32_t) * (size_t)npad));
+    CU(cudaMemsetAsync(ix->nx.p, 0, sizeof(int32_t) * (size_t)npad, st));
+    CU(launch_row_norms(ix->X.as<uint8_t>(), ix->pitch, (int)n, ix->nx.as<int32_t>(), st));
+    ix->nx_ready = true;
+  }
   for (int64_t r0 = 0; r0 < q; r0 += qc) {
     const int qn = (int)std::min<int64_t>(qc, q - r0);
     uint8_t *qpad = ix->exact_ws.as<uint8_t>(round_up(szD, 256));
+    int32_t *nq = ix->exact_ws.as<int32_t>(round_up(szD, 256) + round_up(szQ, 256));
     CU(cudaMemsetAsync(qpad, 0, szQ, st));
     CU(cudaMemcpy2DAsync(qpad, ix->pitch, queries_dev + r0 * ix->d, ix->d, ix->d, qn,
                          cudaMemcpyDeviceToDevice, st));
@@ -1066,7 +1077,13 @@ aknn_status aknn_exact_async(const aknn_index *cix, const uint8_t *queries_dev, 
     e.npad = npad;
     e.idx = idx_dev + r0 * k;
     e.dist2 = dist2_dev + r0 * k;
-    CU(launch_exact(e, st));
+    if (use_dp4a) {
+      CU(launch_exact(e, st));
+    } else {
+      CU(launch_row_norms(qpad, ix->pitch, qn, nq, st));
+      CU(launch_exact_mma(e, nq, ix->nx.as<int32_t>(), st));
+      CU(launch_exact_topk(e, st));
+    }
   }
   return AKNN_OK;
 }

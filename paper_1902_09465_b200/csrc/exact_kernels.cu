@@ -107,4 +107,9 @@ cudaError_t launch_exact(const ExactGeom &e, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+cudaError_t launch_exact_topk(const ExactGeom &e, cudaStream_t s) {
+  k_exact_topk<<<e.q, SEL_NT, 0, s>>>(e);
+  return cudaGetLastError();
+}
+
 }  // namespace aknn

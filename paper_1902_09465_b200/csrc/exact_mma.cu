@@ -1,0 +1,263 @@
+// exact_mma.cu -- the exact comparison pass (P:98 brute force) on the 5th-generation
+// tensor cores: D(q, i) = ||x_i||^2 + ||q||^2 - 2 <x_i, q>, with the inner products
+// an unsigned-8-bit contraction accumulated exactly in int32 (tcgen05.mma kind::i8,
+// u8 x u8 -> s32; d * 255^2 < 2^31 for d <= 33025, and so is every D).
+//
+// One CTA per 128-query x 256-point tile, K in 128-byte blocks:
+//   warp 0 lane 0   TMA producer: cp.async.bulk.tensor 2-D loads of the query tile
+//                   (128 x 128 B) and the point tile (256 x 128 B) into a 4-stage
+//                   ring, 128-byte swizzled, completion on mbarriers (expect_tx)
+//   warp 1 lane 0   MMA issuer: 4 x tcgen05.mma (K = 32 bytes each) per stage into a
+//                   128 x 256 int32 accumulator in TMEM (256 columns); tcgen05.commit
+//                   frees the stage, the last one signals the epilogue
+//   warp 2          TMEM allocator (tcgen05.alloc / dealloc, 256 columns)
+//   warps 4-7       epilogue: tcgen05.ld 32x32b.x32 (lane = query row, 32 points per
+//                   load), D = nx + nq - 2 dot, int32 stores
+// The distances then go through the block radix top-k of exact_kernels.cu.
+#include <cuda.h>
+
+#include "internal.cuh"
+#include "launch.h"
+
+namespace aknn {
+
+constexpr int MM_BM = 128, MM_BN = 256, MM_BK = 128, MM_STAGES = 4, MM_NT = 256;
+constexpr uint32_t MM_A_BYTES = MM_BM * MM_BK, MM_B_BYTES = MM_BN * MM_BK;
+constexpr uint32_t MM_STAGE_BYTES = MM_A_BYTES + MM_B_BYTES;
+constexpr size_t MM_SMEM = (size_t)MM_STAGES * MM_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+constexpr uint32_t MM_TMEM_COLS = 256;
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+
+__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int x, int y) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
+          "r"(smem_u32(dst)),
+      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
+      : "memory");
+}
+
+// K-major operand, 128-byte swizzle: rows of 128 B, 8-row atoms of 1024 B (SBO).
+__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
+  uint64_t d = 0;
+  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);        // start address
+  d |= (uint64_t)1u << 16;                         // leading byte offset (unused for SW128 K-major)
+  d |= (uint64_t)(1024u >> 4) << 32;               // stride byte offset: 8 rows x 128 B
+  d |= (uint64_t)1u << 46;                         // descriptor version (sm_100)
+  d |= (uint64_t)2u << 61;                         // layout: SWIZZLE_128B
+  return d;
+}
+
+// kind::i8 instruction descriptor: D s32, A u8, B u8, both K-major, M = 128, N = 256.
+__host__ __device__ constexpr uint32_t umma_idesc_u8(int M, int N) {
+  return (2u << 4)                       // D format: s32
+         | (0u << 7) | (0u << 10)        // A, B format: unsigned 8-bit
+         | (0u << 15) | (0u << 16)       // A, B K-major
+         | ((uint32_t)(N >> 3) << 17)    // N / 8
+         | ((uint32_t)(M >> 4) << 24);   // M / 16
+}
+
+__global__ void __launch_bounds__(MM_NT, 1)
+    k_exact_mma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmX,
+                const int32_t *__restrict__ nq, const int32_t *__restrict__ nx, int q, int n, int d,
+                int32_t *__restrict__ D, int64_t ldd) {
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char *sm = reinterpret_cast<unsigned char *>(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  uint64_t *full = reinterpret_cast<uint64_t *>(sm + MM_STAGES * MM_STAGE_BYTES);
+  uint64_t *empty = full + MM_STAGES;
+  uint64_t *tfull = empty + MM_STAGES;
+  uint32_t *tmem_base = reinterpret_cast<uint32_t *>(tfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * MM_BM, n0 = blockIdx.x * MM_BN;
+  const int nk = (d + MM_BK - 1) / MM_BK;
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < MM_STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmQ)) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base)),
+                 "n"(MM_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % MM_STAGES;
+        if (kb >= MM_STAGES) mbar_wait(empty + s, ((kb / MM_STAGES) - 1) & 1);
+        unsigned char *sa = sm + s * MM_STAGE_BYTES;
+        mbar_expect_tx(full + s, MM_STAGE_BYTES);
+        tma_load_2d(sa, &tmQ, full + s, kb * MM_BK, m0);
+        tma_load_2d(sa + MM_A_BYTES, &tmX, full + s, kb * MM_BK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer
+      constexpr uint32_t idesc = umma_idesc_u8(MM_BM, MM_BN);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % MM_STAGES;
+        mbar_wait(full + s, (kb / MM_STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t sa = smem_u32(sm + s * MM_STAGE_BYTES), sb = sa + MM_A_BYTES;
+#pragma unroll
+        for (int kk = 0; kk < MM_BK / 32; ++kk) {
+          const uint64_t da = umma_desc_sw128(sa + kk * 32), db = umma_desc_sw128(sb + kk * 32);
+          const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+          asm volatile(
+              "{\n\t.reg .pred p;\n\t"
+              "setp.ne.b32 p, %4, 0;\n\t"
+              "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem),
+              "l"(da), "l"(db), "r"(idesc), "r"(acc));
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(empty + s))
+                     : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(tfull))
+                   : "memory");
+    }
+  } else if (warp >= 4) {  // epilogue: TMEM lanes 32*(warp-4) .. +31 = query rows
+    const int quad = warp - 4;
+    mbar_wait(tfull, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    const int row = m0 + quad * 32 + lane;
+    const int32_t nqr = row < q ? __ldg(nq + row) : 0;
+#pragma unroll 1
+    for (int c0 = 0; c0 < MM_BN; c0 += 32) {
+      uint32_t v[32];
+      const uint32_t taddr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0;
+      asm volatile(
+          "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+          "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+          : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+            "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+            "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+            "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+            "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+          : "r"(taddr));
+      asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      if (row < q) {
+        const int col0 = n0 + c0;
+        int32_t *drow = D + (size_t)row * ldd + col0;
+        if (col0 + 32 <= n) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4) {
+            const int4 xn = __ldg(reinterpret_cast<const int4 *>(nx + col0 + j));
+            int4 o;
+            o.x = xn.x + nqr - 2 * (int32_t)v[j + 0];
+            o.y = xn.y + nqr - 2 * (int32_t)v[j + 1];
+            o.z = xn.z + nqr - 2 * (int32_t)v[j + 2];
+            o.w = xn.w + nqr - 2 * (int32_t)v[j + 3];
+            *reinterpret_cast<int4 *>(drow + j) = o;
+          }
+        } else {
+          for (int j = 0; j < 32 && col0 + j < n; ++j) drow[j] = __ldg(nx + col0 + j) + nqr - 2 * (int32_t)v[j];
+        }
+      }
+    }
+  }
+  __syncwarp();
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(MM_TMEM_COLS));
+  }
+}
+
+// ||row||^2 of each of `rows` uint8 rows (pitch bytes, zero padded): warp per row.
+__global__ void k_row_norms(const uint8_t *A, int64_t pitch, int rows, int32_t *out) {
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (w >= rows) return;
+  const uint4 *r = reinterpret_cast<const uint4 *>(A + (size_t)w * pitch);
+  uint32_t acc = 0;
+  for (int v = lane; v < (int)(pitch >> 4); v += 32) {
+    const uint4 a = __ldg(r + v);
+    acc = __dp4a(a.x, a.x, acc);
+    acc = __dp4a(a.y, a.y, acc);
+    acc = __dp4a(a.z, a.z, acc);
+    acc = __dp4a(a.w, a.w, acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+  if (lane == 0) out[w] = (int32_t)acc;
+}
+
+cudaError_t launch_row_norms(const uint8_t *A, int64_t pitch, int rows, int32_t *out, cudaStream_t s) {
+  if (rows <= 0) return cudaSuccess;
+  k_row_norms<<<(rows + 7) / 8, 256, 0, s>>>(A, pitch, rows, out);
+  return cudaGetLastError();
+}
+
+// --- TMA descriptors through the driver entry point (no libcuda link) -------
+typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t, void *, const cuuint64_t *,
+                                  const cuuint64_t *, const cuuint32_t *, const cuuint32_t *,
+                                  CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
+                                  CUtensorMapFloatOOBfill);
+
+static cudaError_t make_map(CUtensorMap *m, const uint8_t *base, int rows, int d, int64_t pitch, int box_rows) {
+  static EncodeTiledFn fn = nullptr;
+  if (!fn) {
+    void *p = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    cudaError_t e = cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &qr);
+    if (e != cudaSuccess || qr != cudaDriverEntryPointSuccess || !p) return cudaErrorNotSupported;
+    fn = reinterpret_cast<EncodeTiledFn>(p);
+  }
+  const cuuint64_t dims[2] = {(cuuint64_t)d, (cuuint64_t)rows};
+  const cuuint64_t strides[1] = {(cuuint64_t)pitch};
+  const cuuint32_t box[2] = {(cuuint32_t)MM_BK, (cuuint32_t)box_rows};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 2, const_cast<uint8_t *>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS ? cudaSuccess : cudaErrorInvalidValue;
+}
+
+cudaError_t launch_exact_mma(const ExactGeom &e, const int32_t *nq, const int32_t *nx, cudaStream_t s) {
+  CUtensorMap tq, tx;
+  cudaError_t err = make_map(&tq, e.Q, e.q, e.d, e.pitch, MM_BM);
+  if (err != cudaSuccess) return err;
+  err = make_map(&tx, e.X, e.n, e.d, e.pitch, MM_BN);
+  if (err != cudaSuccess) return err;
+  err = cudaFuncSetAttribute(k_exact_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MM_SMEM);
+  if (err != cudaSuccess) return err;
+  dim3 grid((e.n + MM_BN - 1) / MM_BN, (e.q + MM_BM - 1) / MM_BM);
+  k_exact_mma<<<grid, MM_NT, MM_SMEM, s>>>(tq, tx, nq, nx, e.q, e.n, e.d, e.D, e.npad);
+  return cudaGetLastError();
+}
+
+}  // namespace aknn

@@ -48,6 +48,10 @@ struct ExactGeom {
   int32_t *idx;       // [q][k] out (device)
   int32_t *dist2;     // [q][k] out (device)
 };
-cudaError_t launch_exact(const ExactGeom &e, cudaStream_t s);
+cudaError_t launch_exact(const ExactGeom &e, cudaStream_t s);        // D via dp4a tiles + top-k
+cudaError_t launch_exact_topk(const ExactGeom &e, cudaStream_t s);   // top-k of e.D only
+// D via tcgen05 kind::i8 (exact_mma.cu); nq [q], nx [n] squared row norms.
+cudaError_t launch_exact_mma(const ExactGeom &e, const int32_t *nq, const int32_t *nx, cudaStream_t s);
+cudaError_t launch_row_norms(const uint8_t *A, int64_t pitch, int rows, int32_t *out, cudaStream_t s);
 
 }  // namespace aknn
