@@ -133,6 +133,10 @@ struct aknn_index {
   DevBuf nx;               // [n_local] ||x_i||^2 for the tensor-core exact pass (lazy)
   bool nx_ready = false;
   EventPool events;
+  // cached graph of the device-driven round loop (one query sub-batch shape)
+  cudaStream_t cap_stream = nullptr;
+  cudaGraphExec_t loop_exec = nullptr;
+  std::vector<unsigned char> loop_key;
   int rank = 0, world = 1;
 #ifdef AKNN_WITH_NCCL
   ncclComm_t comm = nullptr;
@@ -268,6 +272,82 @@ struct PhaseTimer {
   }
 };
 
+// The round loop of one query sub-batch as ONE CUDA graph: reset, init (a2), rank
+// split (a6-a7), then a conditional WHILE node whose body is filter -> plan ->
+// scatter -> advance -> zero -> rank split -> k_round_ctl, the last of which sets the
+// condition on the device.  No host round trip per round.  The instantiated graph is
+// cached on the index and reused while the launch parameters are unchanged.
+aknn_status loop_graph(aknn_index *ix, const Geom &g, int nbits, int max_rounds, cudaGraphExec_t *out) {
+  std::vector<unsigned char> key(sizeof(Geom) + 2 * sizeof(int));
+  memcpy(key.data(), &g, sizeof(Geom));
+  memcpy(key.data() + sizeof(Geom), &nbits, sizeof(int));
+  memcpy(key.data() + sizeof(Geom) + sizeof(int), &max_rounds, sizeof(int));
+  if (ix->loop_exec && key == ix->loop_key) {
+    *out = ix->loop_exec;
+    return AKNN_OK;
+  }
+  if (ix->loop_exec) {
+    cudaGraphExecDestroy(ix->loop_exec);
+    ix->loop_exec = nullptr;
+  }
+  if (!ix->cap_stream) CU(cudaStreamCreateWithFlags(&ix->cap_stream, cudaStreamNonBlocking));
+  cudaStream_t cs = ix->cap_stream;
+  cudaGraph_t graph = nullptr;
+  CU(cudaGraphCreate(&graph, 0));
+  struct GraphFree {
+    cudaGraph_t g;
+    ~GraphFree() {
+      if (g) cudaGraphDestroy(g);
+    }
+  } gf{graph};
+  cudaGraphConditionalHandle h;
+  CU(cudaGraphConditionalHandleCreate(&h, graph, 1, cudaGraphCondAssignDefault));
+  CU(cudaStreamBeginCaptureToGraph(cs, graph, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  cudaError_t e = launch_ctl_reset(g.ctl, (unsigned)g.q, cs);
+  if (e == cudaSuccess) e = launch_init(g, cs);
+  if (e == cudaSuccess) e = launch_select(g, nbits, cs);
+  if (e == cudaSuccess) e = launch_round_ctl(g.ctl, h, max_rounds, cs);
+  cudaStreamCaptureStatus cst;
+  const cudaGraphNode_t *deps = nullptr;
+  size_t ndeps = 0;
+  if (e == cudaSuccess) e = cudaStreamGetCaptureInfo(cs, &cst, nullptr, nullptr, &deps, &ndeps);
+  cudaGraphNodeParams cp{};
+  cp.type = cudaGraphNodeTypeConditional;
+  cp.conditional.handle = h;
+  cp.conditional.type = cudaGraphCondTypeWhile;
+  cp.conditional.size = 1;
+  cudaGraphNode_t cnode = nullptr;
+  if (e == cudaSuccess) e = cudaGraphAddNode(&cnode, graph, deps, ndeps, &cp);
+  if (e == cudaSuccess) e = cudaStreamUpdateCaptureDependencies(cs, &cnode, 1, cudaStreamSetCaptureDependencies);
+  cudaGraph_t captured = nullptr;
+  const cudaError_t e2 = cudaStreamEndCapture(cs, &captured);
+  if (e != cudaSuccess || e2 != cudaSuccess) {
+    cudaGetLastError();
+    return fail(AKNN_ECUDA, "capturing the round-loop graph: %s",
+                cudaGetErrorString(e != cudaSuccess ? e : e2));
+  }
+  cudaGraph_t body = cp.conditional.phGraph_out[0];
+  CU(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+  e = launch_filter(g, cs);
+  if (e == cudaSuccess) e = launch_compact(g, cs);
+  if (e == cudaSuccess) e = launch_advance(g, ix->num_sms, cs);
+  if (e == cudaSuccess) e = launch_zero_round(g.ctl, cs);
+  if (e == cudaSuccess) e = launch_select(g, nbits, cs);
+  if (e == cudaSuccess) e = launch_round_ctl(g.ctl, h, max_rounds, cs);
+  cudaGraph_t body_out = nullptr;
+  const cudaError_t e3 = cudaStreamEndCapture(cs, &body_out);
+  if (e != cudaSuccess || e3 != cudaSuccess) {
+    cudaGetLastError();
+    return fail(AKNN_ECUDA, "capturing the loop body: %s", cudaGetErrorString(e != cudaSuccess ? e : e3));
+  }
+  cudaGraphExec_t exec = nullptr;
+  CU(cudaGraphInstantiate(&exec, graph, 0));
+  ix->loop_exec = exec;
+  ix->loop_key = key;
+  *out = exec;
+  return AKNN_OK;
+}
+
 // Runs the whole query on device pointers.  Q rows have stride `qstride`
 // bytes in `queries_dev` (device).  Outputs are device pointers.
 aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstride, int32_t q,
@@ -338,6 +418,10 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
 
   aknn_stats stats{};
   stats.pairs = (int64_t)q * n;
+  // the device-driven (graph) loop unless per-kernel timing was asked for, which
+  // needs the host loop to bracket each launch with events
+  static const bool no_graph = getenv("AKNN_NO_GRAPH") && getenv("AKNN_NO_GRAPH")[0] == '1';
+  const bool use_graph = o.timing == 0 && !no_graph;
   PhaseTimer tm(o.timing != 0, st, &ix->events);
   tm.start();
   cudaEvent_t all_a = tm.open_a;
@@ -358,12 +442,31 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
     CU(cudaMemsetAsync(ix->ws.as<uint8_t>(oQ), 0, szQ, st));
     CU(cudaMemcpy2DAsync(ix->ws.as<uint8_t>(oQ), ix->pitch, queries_dev + r0 * qstride, qstride, d,
                          qn, cudaMemcpyDeviceToDevice, st));
+    int r = 0;
+    if (use_graph) {
+      // device-driven loop: one graph launch per sub-batch, no host round trips
+      cudaGraphExec_t exec = nullptr;
+      TRY(loop_graph(ix, g, kg.nbits, o.max_rounds, &exec));
+      CU(cudaGraphLaunch(exec, st));
+      RoundCtl c;
+      CU(cudaMemcpyAsync(&c, g.ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
+      CU(cudaStreamSynchronize(st));
+      r = (int)c.round;
+      stats.query_rounds += (int64_t)c.qrounds;
+      stats.blocked_query_rounds += (int64_t)c.brounds;
+      stats.launches_init += 3;
+      stats.launches_select += 2 * r;  // rank split + round control
+      stats.launches_filter += r - 1;
+      stats.launches_compact += 2 * (r - 1);
+      stats.launches_advance += 2 * (r - 1);  // advance + counter reset
+      if (c.n_active > 0) status = AKNN_EMAXROUNDS;
+    }
+    if (!use_graph) {
     CU(cudaMemsetAsync(g.ctl, 0, sizeof(RoundCtl), st));
     tm.start();
     CU(launch_init(g, st));
     tm.stop(PH_INIT);
     stats.launches_init += 2;
-    int r = 0;
     unsigned evaluated = (unsigned)qn;  // queries the rank split looks at this round
     for (;;) {
       ++r;
@@ -398,6 +501,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
       ++stats.launches_advance;
       if (r > 1 + 64 * 64) return fail(AKNN_ECUDA, "round loop did not terminate (internal error)");
     }
+    }  // host-driven loop
     if (r > stats.rounds) stats.rounds = r;
     OutPtrs op{(int)r0, 0, n, 0, out->sets, out->dhat, out->counts, out->sums, out->evals, out->draws, out->rounds};
     tm.start();
@@ -1117,6 +1221,8 @@ void aknn_free(aknn_index *ix) {
   if (ix->comm) ncclCommDestroy(ix->comm);
 #endif
   if (ix->stream) cudaStreamSynchronize(ix->stream);
+  if (ix->loop_exec) cudaGraphExecDestroy(ix->loop_exec);
+  if (ix->cap_stream) cudaStreamDestroy(ix->cap_stream);
   if (ix->stream) cudaStreamDestroy(ix->stream);
   delete ix;
 }

@@ -41,6 +41,10 @@ struct RoundCtl {
   unsigned int cursor[NSLOT];             // scatter cursors
   unsigned long long chunk_off[NSLOT + 1];// warp-chunk prefix per slot
   unsigned long long advanced;            // pairs advanced, cumulative
+  // cumulative, maintained on the device by k_round_ctl (graph-launched loop)
+  unsigned int round;                     // rounds evaluated
+  unsigned int evaluated;                 // queries the next rank split looks at
+  unsigned long long qrounds, brounds;    // sums of evaluated / blocked queries
 };
 
 // One arm as exchanged between point shards: its composite key

@@ -207,10 +207,17 @@ constexpr int ADV_P = 4;
 constexpr int ADV_XP = 4;
 
 __host__ __device__ __forceinline__ unsigned nblk_of(int c) { return c < 2 ? 1u : (1u << (c - 2)); }
+// Lanes per pair at levels with nb > ADV_P blocks: each lane runs >= ADV_BPL blocks
+// (two rounds of ADV_P independent Philox blocks) before the group reduce.
+constexpr unsigned ADV_BPL = 8;
+__host__ __device__ __forceinline__ unsigned lanes_per_pair(unsigned nb) {
+  const unsigned t = nb / ADV_BPL;
+  return t < 1u ? 1u : (t > 32u ? 32u : t);
+}
 __host__ __device__ __forceinline__ unsigned pairs_per_chunk(int slot) {
   if (slot == MAX_LEVELS) return ADV_XP;
   const unsigned nb = nblk_of(slot);
-  return nb >= 32u * ADV_P ? 1u : 32u * ADV_P / nb;
+  return nb <= (unsigned)ADV_P ? 32u * ADV_P / nb : 32u / lanes_per_pair(nb);
 }
 
 __global__ void k_plan(RoundCtl *ctl) {
@@ -233,28 +240,41 @@ __global__ void k_plan(RoundCtl *ctl) {
 }
 
 // a8: compaction of the action bytes into per-slot lists of (qi << ibits | i).
-// blockIdx.x = query, so consecutive CTAs append the same point chunk of
-// different queries (point-major list order, X-row locality in L2).
+// One CTA per (query, 1024-arm chunk); thread t owns arms chunk + t + 256 e, so for
+// each e a warp covers 32 consecutive arms.  Slots are counted in shared memory
+// (warp-aggregated), the CTA reserves one range per slot with ONE global atomic,
+// and writes its entries there: list order within a slot follows the arm order
+// of each warp, so the advance kernel reads S / level nearly sequentially.
 __global__ void __launch_bounds__(FIL_NT) k_scatter(Geom g) {
   const int qi = blockIdx.x;
   if (g.qs[qi].done) return;
-  const int i0 = (blockIdx.y * FIL_NT + threadIdx.x) * 4;
-  uint32_t actw = 0;
-  if (i0 < g.n) actw = *reinterpret_cast<const uint32_t *>(g.act + (size_t)qi * g.npad + i0);
+  __shared__ unsigned scnt[NSLOT], sbase[NSLOT];
+  for (int s = threadIdx.x; s < NSLOT; s += FIL_NT) scnt[s] = 0;
+  __syncthreads();
+  const int base_i = blockIdx.y * FIL_NT * 4 + threadIdx.x;
+  const uint8_t *arow = g.act + (size_t)qi * g.npad;
   const int lane = lane_id();
+  unsigned slot[4], loc[4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const uint8_t act = (uint8_t)(actw >> (8 * e));
-    const unsigned slot = act == 0 ? NONE : (act == ACT_EXACT ? (unsigned)MAX_LEVELS : act - 1u);
-    const unsigned m = __match_any_sync(FULL, slot);
-    if (slot == NONE) continue;
+    const int i = base_i + e * FIL_NT;
+    const uint8_t act = i < g.n ? arow[i] : (uint8_t)0;
+    slot[e] = act == 0 ? NONE : (act == ACT_EXACT ? (unsigned)MAX_LEVELS : act - 1u);
+    const unsigned m = __match_any_sync(FULL, slot[e]);
     const int leader = __ffs(m) - 1;
-    unsigned base = 0;
-    if (lane == leader) base = atomicAdd(&g.ctl->cursor[slot], (unsigned)__popc(m));
-    base = __shfl_sync(m, base, leader);
-    const unsigned r = __popc(m & ((1u << lane) - 1u));
-    g.list[g.ctl->off[slot] + base + r] = ((uint32_t)qi << g.ibits) | (uint32_t)(i0 + e);
+    unsigned b = 0;
+    if (slot[e] != NONE && lane == leader) b = atomicAdd(&scnt[slot[e]], (unsigned)__popc(m));
+    b = __shfl_sync(FULL, b, leader);
+    loc[e] = b + __popc(m & ((1u << lane) - 1u));
   }
+  __syncthreads();
+  if (threadIdx.x < NSLOT && scnt[threadIdx.x])
+    sbase[threadIdx.x] = g.ctl->off[threadIdx.x] + atomicAdd(&g.ctl->cursor[threadIdx.x], scnt[threadIdx.x]);
+  __syncthreads();
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    if (slot[e] != NONE)
+      g.list[sbase[slot[e]] + loc[e]] = ((uint32_t)qi << g.ibits) | (uint32_t)(base_i + e * FIL_NT);
 }
 
 // ---------------------------------------------------------------------------
@@ -290,6 +310,27 @@ __device__ __forceinline__ void draw_blocks(const Geom &g, const BlockTask (&t)[
     }
     acc[k] = a;
   }
+}
+
+// ADV_P consecutive Philox blocks blk0.. of ONE pair (all 4 draws of each used: s >= 4).
+__device__ __forceinline__ uint32_t draw4_pair(const Geom &g, const uint8_t *__restrict__ xr,
+                                               const uint8_t *__restrict__ qr, uint32_t gi, uint32_t gq,
+                                               uint32_t lv, uint32_t blk0) {
+  uint4 w[ADV_P];
+#pragma unroll
+  for (int k = 0; k < ADV_P; ++k) w[k] = philox4x32_10_rk(make_uint4(blk0 + k, gi, gq, lv), g.rk0, g.rk1);
+  uint32_t acc = 0;
+#pragma unroll
+  for (int k = 0; k < ADV_P; ++k) {
+    const uint32_t ws[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t j = coord_of(ws[e], (uint32_t)g.d);
+      const int diff = (int)__ldg(xr + j) - (int)__ldg(qr + j);
+      acc += (uint32_t)(diff * diff);
+    }
+  }
+  return acc;
 }
 
 __device__ __forceinline__ void decode(const Geom &g, uint32_t code, uint32_t imask, uint32_t &qi,
@@ -424,43 +465,21 @@ __global__ void __launch_bounds__(ADV_NT) k_advance(Geom g) {
         decode(g, code[k], imask, qi, i);
         commit(g, qi, i, sum, newlvl);
       }
-    } else if (nb <= 32u * ADV_P) {
-      // tpp lanes per pair; lane group gi handles blocks [sub*ADV_P, sub*ADV_P + ADV_P)
-      const unsigned tpp = nb / ADV_P;
+    } else {
+      // tpp lanes per pair (a warp holds 32/tpp pairs); lane `sub` of a pair runs the
+      // blocks (it*tpp + sub)*ADV_P + k, ADV_P independent Philox chains at a time
+      const unsigned tpp = lanes_per_pair(nb);
       const unsigned p = pbase + lane / tpp, sub = lane % tpp;
       const bool ok = p < cnt;
-      const uint32_t cd = ok ? lst[p] : 0u;
-      uint32_t qi, i;
-      decode(g, cd, imask, qi, i);
-      BlockTask t[ADV_P];
-#pragma unroll
-      for (int k = 0; k < ADV_P; ++k)
-        t[k] = BlockTask{g.X + (size_t)i * g.pitch, g.Q + (size_t)qi * g.pitch, i + g.id_offset,
-                         qi + g.qi0, sub * ADV_P + k, ok};
-      uint32_t acc[ADV_P];
-      draw_blocks(g, t, c, s, acc);
-      uint32_t sum = acc[0] + acc[1] + acc[2] + acc[3];
+      uint32_t qi = 0, i = 0, sum = 0;
+      if (ok) {
+        decode(g, lst[p], imask, qi, i);
+        const uint8_t *xr = g.X + (size_t)i * g.pitch, *qr = g.Q + (size_t)qi * g.pitch;
+        const uint32_t gi = i + g.id_offset, gq = qi + g.qi0, lv = (uint32_t)(c + 1);
+        for (unsigned b0 = sub * ADV_P; b0 < nb; b0 += tpp * ADV_P) sum += draw4_pair(g, xr, qr, gi, gq, lv, b0);
+      }
       for (unsigned o = tpp >> 1; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
       if (ok && sub == 0) commit(g, qi, i, sum, newlvl);
-    } else {
-      // one warp per pair; lanes loop over groups of ADV_P blocks
-      const uint32_t cd = lst[pbase];
-      uint32_t qi, i;
-      decode(g, cd, imask, qi, i);
-      const uint8_t *xr = g.X + (size_t)i * g.pitch, *qr = g.Q + (size_t)qi * g.pitch;
-      uint32_t sum = 0;
-      for (unsigned b0 = lane * ADV_P; b0 < nb; b0 += 32 * ADV_P) {
-        BlockTask t[ADV_P];
-#pragma unroll
-        for (int k = 0; k < ADV_P; ++k)
-          t[k] = BlockTask{xr, qr, i + g.id_offset, qi + g.qi0, b0 + k, true};
-        uint32_t acc[ADV_P];
-        draw_blocks(g, t, c, s, acc);
-        sum += acc[0] + acc[1] + acc[2] + acc[3];
-      }
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
-      if (lane == 0) commit(g, qi, i, sum, newlvl);
     }
   }
 }
@@ -568,5 +587,46 @@ cudaError_t launch_output(const Geom &g, const OutPtrs &o, cudaStream_t s) {
 }
 
 int output_max_kh() { return OUT_MAXKH; }
+
+// ---------------------------------------------------------------------------
+// Device-side round control for the graph-launched loop: the rank split leaves
+// n_active (queries failing Eq. (5)) in the control block; k_round_ctl counts the
+// round and sets the WHILE condition = n_active > 0 and the round cap not reached
+// (the same rule as the host loop: stop at Eq. (5) for all, or EMAXROUNDS).
+__global__ void k_ctl_reset(RoundCtl *ctl, unsigned q) {
+  RoundCtl z{};
+  z.evaluated = q;
+  *ctl = z;
+}
+
+__global__ void k_zero_round(RoundCtl *ctl) {
+  unsigned *p = reinterpret_cast<unsigned *>(ctl);
+  for (int t = threadIdx.x; t < (int)(offsetof(RoundCtl, advanced) / 4); t += blockDim.x) p[t] = 0;
+}
+
+__global__ void k_round_ctl(RoundCtl *ctl, cudaGraphConditionalHandle h, int max_rounds) {
+  const unsigned r = ++ctl->round;
+  const unsigned nact = ctl->n_active;
+  ctl->qrounds += ctl->evaluated;
+  ctl->brounds += nact;
+  ctl->evaluated = nact;
+  const bool cont = nact > 0 && (max_rounds <= 0 || (int)r < max_rounds);
+  cudaGraphSetConditional(h, cont ? 1u : 0u);
+}
+
+cudaError_t launch_ctl_reset(RoundCtl *ctl, unsigned q, cudaStream_t s) {
+  k_ctl_reset<<<1, 1, 0, s>>>(ctl, q);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_zero_round(RoundCtl *ctl, cudaStream_t s) {
+  k_zero_round<<<1, 128, 0, s>>>(ctl);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_round_ctl(RoundCtl *ctl, cudaGraphConditionalHandle h, int max_rounds, cudaStream_t s) {
+  k_round_ctl<<<1, 1, 0, s>>>(ctl, h, max_rounds);
+  return cudaGetLastError();
+}
 
 }  // namespace aknn

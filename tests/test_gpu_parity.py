@@ -188,3 +188,26 @@ def test_exact_pass_vs_bruteforce(ak, n, d, q, k, lo, hi):
     ridx, rdist = orc.bruteforce(X, Q, k)
     assert np.array_equal(idx, ridx)
     assert np.array_equal(dist, rdist)
+
+
+@pytest.mark.parametrize("max_rounds", [0, 3])
+def test_graph_loop_equals_host_loop(ak, max_rounds):
+    """The device-driven loop (CUDA graph with a conditional WHILE node, timing off) and
+    the host-driven loop (timing on: per-launch events) give identical bytes, also when
+    the round cap stops the batch (EMAXROUNDS)."""
+    X, Q = synth.small_instance(91, 2500, 140, q=7)
+    al = orc.alpha_experimental(2500, 0.05, 140, 0.05)
+    ix = ak.Index(X)
+    a = ix.query(Q, 6, 4, 0.05, 5, al, counts=True, sums=True, max_rounds=max_rounds)
+    b = ix.query(Q, 6, 4, 0.05, 5, al, counts=True, sums=True, max_rounds=max_rounds, timing=True)
+    sa = ix.stats()
+    c = ix.query(Q, 6, 4, 0.05, 5, al, counts=True, sums=True, max_rounds=max_rounds)  # cached graph
+    sc = ix.stats()
+    ix.close()
+    assert a["status"] == b["status"] == c["status"]
+    for k in KEYS:
+        assert np.array_equal(a[k], b[k]) and np.array_equal(a[k], c[k]), k
+    assert sa["rounds"] == sc["rounds"] and sa["query_rounds"] == sc["query_rounds"]
+    assert sa["blocked_query_rounds"] == sc["blocked_query_rounds"]
+    ref = orc.query_br(X, Q, 6, 4, 5, al, want_sums=True, max_rounds=max_rounds)
+    _assert_parity(a, ref)
