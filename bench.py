@@ -229,6 +229,20 @@ def _traffic_from_profiles(kernel: str):
 #   advance  per sampled draw: one 32-B sector of X; per exact fallback: d bytes of X;
 #            per advanced pair: list entry 4 + S read 4 + S write 4 + level 1
 SECTOR = 32
+L2_BYTES = 126 << 20
+
+
+def _measure_probes(d: int, x_bytes: int) -> dict:
+    """Roofline denominators measured on this GPU now (tools/probes.cu)."""
+    try:
+        sys.path.insert(0, os.path.join(ROOT, "tools"))
+        import run_probes as rp
+        L = rp.load()
+        pb = rp.philox_blocks_per_s(L, d=d)
+        gl, fb = rp.gather_sectors_per_s(L, x_bytes)
+        return {"philox_blocks_per_s": pb, "gather_loads_per_s": gl, "gather_footprint_bytes": fb}
+    except Exception as e:  # the probes are evidence, never a reason to fail the bench
+        return {"error": repr(e)}
 
 
 def _algorithmic_bytes(st: dict, n: int, d: int, q: int) -> dict:
@@ -416,21 +430,46 @@ def run_ours(args, dist: Dist):
             abytes[c] += b
     dom = max(classes, key=lambda c: ms_cls[c])
     peak, peak_src = _peaks()
-    achieved = abytes.get(dom, 0) / (ms_cls[dom] / 1e3) / 1e9 if ms_cls[dom] > 0 else 0.0
-    traffic = _traffic_from_profiles(KERNEL_OF[dom])
-    roofline = {"bound": "hbm", "kernel": KERNEL_OF[dom], "achieved": achieved, "peak": peak,
-                "unit": "GB/s", "frac": achieved / peak, "traffic": traffic,
-                "peak_source": peak_src,
-                "launches": launches[dom], "avg_launch_ms": ms_cls[dom] / max(1, launches[dom]),
-                "algorithmic_bytes_per_launch": abytes[dom] / max(1, launches[dom]),
-                "share_of_step": ms_cls[dom] / ms_local_instr,
-                "timing": "CUDA events around every launch on the library stream, K instrumented "
-                          "steps (host-driven loop) right after the K graph-launched timed steps",
-                "ms_per_step_instrumented": dist.max(ms_local_instr) / args.steps,
-                "per_class": {c: {"ms": ms_cls[c], "launches": launches[c],
-                                  "GBps_algorithmic": (abytes[c] / (ms_cls[c] / 1e3) / 1e9)
-                                  if c in abytes and ms_cls[c] > 0 else None}
-                              for c in classes}}
+    probes = _measure_probes(d, n * cfg.d)
+    blocks = agg.get("philox_blocks", 0)
+    adv_draws = agg["draws"] - args.steps * qpr * n  # level-gather draws (init excluded)
+    x_in_l2 = n * d <= L2_BYTES * 0.8
+    common = {"kernel": KERNEL_OF[dom], "launches": launches[dom],
+              "avg_launch_ms": ms_cls[dom] / max(1, launches[dom]),
+              "share_of_step": ms_cls[dom] / ms_local_instr,
+              "timing": "CUDA events around every launch on the library stream, K instrumented "
+                        "steps (host-driven loop) right after the K graph-launched timed steps",
+              "ms_per_step_instrumented": dist.max(ms_local_instr) / args.steps,
+              "traffic": _traffic_from_profiles(KERNEL_OF[dom]),
+              "per_class": {c: {"ms": ms_cls[c], "launches": launches[c],
+                                "GBps_algorithmic": (abytes[c] / (ms_cls[c] / 1e3) / 1e9)
+                                if c in abytes and ms_cls[c] > 0 else None}
+                            for c in classes},
+              "probes": probes}
+    adv_s = ms_cls["advance"] / 1e3
+    sector_view = {
+        "draws_per_s": adv_draws / adv_s if adv_s > 0 else None,
+        "sector_GBps": adv_draws * SECTOR / adv_s / 1e9 if adv_s > 0 else None,
+        "frac_of_measured_random_sector_rate": (adv_draws / adv_s) / probes["gather_loads_per_s"]
+        if adv_s > 0 and probes.get("gather_loads_per_s") else None,
+        "x_footprint_bytes": n * d, "x_l2_resident": x_in_l2}
+    if dom == "advance" and x_in_l2 and probes.get("philox_blocks_per_s"):
+        # X fits the 126 MB L2: the sampled levels are bound by the integer pipe running
+        # Philox4x32-10 (ncu: fma-heavy pipe busiest), not by memory
+        ach = blocks / adv_s / 1e9
+        pk = probes["philox_blocks_per_s"] / 1e9
+        roofline = {"bound": "alu", "achieved": ach, "peak": pk, "unit": "G Philox blocks/s",
+                    "frac": ach / pk,
+                    "peak_source": "measured in this run: tools/probes.cu k_probe_philox "
+                                   "(Philox4x32-10 + multiply-high map, no memory)",
+                    "algorithmic_units_per_launch": blocks / max(1, launches[dom]),
+                    "sector_view": sector_view, **common}
+    else:
+        achieved = abytes.get(dom, 0) / (ms_cls[dom] / 1e3) / 1e9 if ms_cls[dom] > 0 else 0.0
+        roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                    "frac": achieved / peak, "peak_source": peak_src,
+                    "algorithmic_bytes_per_launch": abytes[dom] / max(1, launches[dom]),
+                    "sector_view": sector_view, **common}
 
     extra = {
         "draws_per_s": dist.sum(draws) / (ms_max / 1e3),

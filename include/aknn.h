@@ -99,6 +99,8 @@ typedef struct {
   double ms_init, ms_select, ms_filter, ms_compact, ms_advance, ms_output;
   int64_t launches_init, launches_select, launches_filter, launches_compact,
       launches_advance, launches_output;
+  int64_t philox_blocks;      /* Philox4x32-10 blocks the level gathers drew
+                                 (one per 4 draws; levels 1 and 2 use one)      */
 } aknn_stats;
 
 /* ------------------------------------------------------------------------ */

@@ -57,7 +57,8 @@ class Stats(C.Structure):
                 ("ms_advance", C.c_double), ("ms_output", C.c_double),
                 ("launches_init", C.c_int64), ("launches_select", C.c_int64),
                 ("launches_filter", C.c_int64), ("launches_compact", C.c_int64),
-                ("launches_advance", C.c_int64), ("launches_output", C.c_int64)]
+                ("launches_advance", C.c_int64), ("launches_output", C.c_int64),
+                ("philox_blocks", C.c_int64)]
 
 
 class MergeResult(C.Structure):

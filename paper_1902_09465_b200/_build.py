@@ -49,12 +49,28 @@ def sources_newer_than(path):
     return any(os.path.getmtime(p) > t for p in deps)
 
 
+PROBES_SRC = os.path.join(ROOT, "tools", "probes.cu")
+PROBES_LIB = os.path.join(ROOT, "tools", "libprobes.so")
+
+
+def build_probes(force: bool = False, verbose: bool = True) -> str:
+    """tools/libprobes.so: roofline microbenchmarks used by bench.py (not the product)."""
+    if force or not os.path.exists(PROBES_LIB) or os.path.getmtime(PROBES_LIB) < os.path.getmtime(PROBES_SRC):
+        cmd = ["nvcc", *ARCH, "-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-shared",
+               "-o", PROBES_LIB, PROBES_SRC]
+        if verbose:
+            print(" ".join(cmd), file=sys.stderr)
+        subprocess.check_call(cmd)
+    return PROBES_LIB
+
+
 def build(force: bool = False, verbose: bool = True) -> str:
     if force or sources_newer_than(LIB):
         cmd = nvcc_cmd()
         if verbose:
             print(" ".join(cmd), file=sys.stderr)
         subprocess.check_call(cmd)
+    build_probes(force, verbose)
     return LIB
 
 

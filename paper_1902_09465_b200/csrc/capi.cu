@@ -178,6 +178,17 @@ aknn_status make_index(int64_t n_local, int64_t n_global, int64_t offset, int32_
   return AKNN_OK;
 }
 
+// Philox blocks per lane in the advance kernel's lane groups (tuning knob; the
+// results do not depend on it).  AKNN_ADV_BPL overrides for experiments.
+unsigned adv_bpl() {
+  static const unsigned v = [] {
+    const char *e = getenv("AKNN_ADV_BPL");
+    const unsigned x = e ? (unsigned)atoi(e) : 8u;
+    return (x >= 4 && (x & (x - 1)) == 0) ? x : 8u;
+  }();
+  return v;
+}
+
 // Builds the level geometry of the composite key (R9).
 struct KeyGeom {
   unsigned long long L, Ld;
@@ -415,6 +426,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   g.kbits = kg.kbits;
   g.world = 1;
   g.cmax = kg.cmax;
+  g.adv_bpl = adv_bpl();
 
   aknn_stats stats{};
   stats.pairs = (int64_t)q * n;
@@ -517,6 +529,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
     for (const QState &s : qs) {
       stats.draws += s.draws;
       stats.exact_fallbacks += s.nexact;
+      stats.philox_blocks += s.blocks;
     }
     if (status != AKNN_OK) break;
   }
@@ -639,6 +652,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     g.ibits = kg[si].ibits;
     g.kbits = kg[si].kbits;
     g.cmax = kg[si].cmax;
+    g.adv_bpl = adv_bpl();
     g.world = W;
     g.recv_stride = recv_stride;
     if (has_recv) g.recv = ix->ws.as<ShardRec>(oRecv);
@@ -763,6 +777,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
       for (const QState &x : qs) {
         stats.draws += x.draws;
         stats.exact_fallbacks += x.nexact;
+        stats.philox_blocks += x.blocks;
       }
     }
     if (status != AKNN_OK) break;

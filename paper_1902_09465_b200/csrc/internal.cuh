@@ -30,6 +30,7 @@ struct QState {
   int rounds;                 // rounds evaluated
   long long draws;            // sampled draws so far
   long long nexact;           // exact fallbacks so far
+  long long blocks;           // Philox4x32-10 blocks the level gathers used
 };
 
 // Per-round control block (device memory; one per batch).
@@ -87,6 +88,7 @@ struct Geom {
   int64_t recv_stride;   // records per shard slot of recv (qb * (k+h+1))
   int world;             // shards taking part (1 = unsharded)
   int cmax;              // largest sampled level (2^cmax < d)
+  unsigned adv_bpl;      // advance: Philox blocks per lane before a lane-group reduce
 };
 
 // ---- Philox4x32-10 (Salmon et al.), counter (x,y,z,w), key (k0,k1) --------

@@ -53,6 +53,7 @@ __global__ void k_init_qstate(Geom g) {
   s.rounds = 0;
   s.draws = g.n;  // one initial draw per arm
   s.nexact = 0;
+  s.blocks = 0;
   g.qs[qi] = s;
 }
 
@@ -133,11 +134,11 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
   if (st.done) return;
   const int i0 = (blockIdx.x * FIL_NT + threadIdx.x) * 4;
   __shared__ unsigned scnt[NSLOT];
-  __shared__ unsigned long long sdraw, sexact;
+  __shared__ unsigned long long sdraw, sexact, sblk;
   for (int s = threadIdx.x; s < NSLOT; s += FIL_NT) scnt[s] = 0;
-  if (threadIdx.x == 0) sdraw = sexact = 0;
+  if (threadIdx.x == 0) sdraw = sexact = sblk = 0;
   __syncthreads();
-  unsigned long long mydraw = 0, myexact = 0;
+  unsigned long long mydraw = 0, myexact = 0, myblk = 0;
   uint32_t actw = 0;
   if (i0 < g.npad) {
     if (i0 < g.n) {
@@ -164,6 +165,7 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
             } else {
               act = (uint8_t)(a.l[e] + 1);
               mydraw += 1ull << a.l[e];
+              myblk += a.l[e] < 2 ? 1ull : (1ull << (a.l[e] - 2));  // Philox blocks
             }
           }
         }
@@ -181,16 +183,19 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     mydraw += __shfl_xor_sync(FULL, mydraw, o);
+    myblk += __shfl_xor_sync(FULL, myblk, o);
     myexact += __shfl_xor_sync(FULL, myexact, o);
   }
   if (lane_id() == 0 && (mydraw | myexact)) {
     atomicAdd(&sdraw, mydraw);
+    atomicAdd(&sblk, myblk);
     atomicAdd(&sexact, myexact);
   }
   __syncthreads();
   if (threadIdx.x < NSLOT && scnt[threadIdx.x]) atomicAdd(&g.ctl->cnt[threadIdx.x], scnt[threadIdx.x]);
   if (threadIdx.x == 0 && (sdraw | sexact)) {
     atomicAdd(reinterpret_cast<unsigned long long *>(&g.qs[qi].draws), sdraw);
+    atomicAdd(reinterpret_cast<unsigned long long *>(&g.qs[qi].blocks), sblk);
     atomicAdd(reinterpret_cast<unsigned long long *>(&g.qs[qi].nexact), sexact);
   }
 }
@@ -209,18 +214,17 @@ constexpr int ADV_XP = 4;
 __host__ __device__ __forceinline__ unsigned nblk_of(int c) { return c < 2 ? 1u : (1u << (c - 2)); }
 // Lanes per pair at levels with nb > ADV_P blocks: each lane runs >= ADV_BPL blocks
 // (two rounds of ADV_P independent Philox blocks) before the group reduce.
-constexpr unsigned ADV_BPL = 8;
-__host__ __device__ __forceinline__ unsigned lanes_per_pair(unsigned nb) {
-  const unsigned t = nb / ADV_BPL;
+__host__ __device__ __forceinline__ unsigned lanes_per_pair(unsigned nb, unsigned bpl) {
+  const unsigned t = nb / bpl;
   return t < 1u ? 1u : (t > 32u ? 32u : t);
 }
-__host__ __device__ __forceinline__ unsigned pairs_per_chunk(int slot) {
+__host__ __device__ __forceinline__ unsigned pairs_per_chunk(int slot, unsigned bpl) {
   if (slot == MAX_LEVELS) return ADV_XP;
   const unsigned nb = nblk_of(slot);
-  return nb <= (unsigned)ADV_P ? 32u * ADV_P / nb : 32u / lanes_per_pair(nb);
+  return nb <= (unsigned)ADV_P ? 32u * ADV_P / nb : 32u / lanes_per_pair(nb, bpl);
 }
 
-__global__ void k_plan(RoundCtl *ctl) {
+__global__ void k_plan(RoundCtl *ctl, unsigned bpl) {
   if (threadIdx.x != 0) return;
   unsigned off = 0;
   unsigned long long ch = 0, adv = 0;
@@ -231,7 +235,7 @@ __global__ void k_plan(RoundCtl *ctl) {
     ctl->cursor[s] = 0;
     off += c;
     adv += c;
-    const unsigned ppc = pairs_per_chunk(s);
+    const unsigned ppc = pairs_per_chunk(s, bpl);
     ch += (c + ppc - 1) / ppc;
   }
   ctl->off[NSLOT] = off;
@@ -430,7 +434,7 @@ __global__ void __launch_bounds__(ADV_NT) k_advance(Geom g) {
     const uint32_t s = 1u << c;
     const unsigned nb = nblk_of(c);
     const uint8_t newlvl = (uint8_t)(c + 1);
-    const unsigned ppc = pairs_per_chunk(c);
+    const unsigned ppc = pairs_per_chunk(c, g.adv_bpl);
     const unsigned pbase = (unsigned)rel * ppc;  // first pair of this chunk
     const uint32_t *lst = g.list + soff[c];
     const unsigned cnt = scnt[c];
@@ -468,13 +472,20 @@ __global__ void __launch_bounds__(ADV_NT) k_advance(Geom g) {
     } else {
       // tpp lanes per pair (a warp holds 32/tpp pairs); lane `sub` of a pair runs the
       // blocks (it*tpp + sub)*ADV_P + k, ADV_P independent Philox chains at a time
-      const unsigned tpp = lanes_per_pair(nb);
+      const unsigned tpp = lanes_per_pair(nb, g.adv_bpl);
       const unsigned p = pbase + lane / tpp, sub = lane % tpp;
       const bool ok = p < cnt;
       uint32_t qi = 0, i = 0, sum = 0;
+      if (ok) decode(g, lst[p], imask, qi, i);
+      // keep the two row pointers live in registers: otherwise ptxas re-derives
+      // X + i*pitch + j for every draw with an IMAD.WIDE on the fma-heavy pipe, the
+      // pipe Philox saturates (ncu: fmaheavy 73 %).  A shuffle result cannot be
+      // rematerialised, so the pointers stay put.
+      const uint8_t *xr = reinterpret_cast<const uint8_t *>(
+          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(g.X + (size_t)i * g.pitch), lane));
+      const uint8_t *qr = reinterpret_cast<const uint8_t *>(
+          __shfl_sync(FULL, reinterpret_cast<unsigned long long>(g.Q + (size_t)qi * g.pitch), lane));
       if (ok) {
-        decode(g, lst[p], imask, qi, i);
-        const uint8_t *xr = g.X + (size_t)i * g.pitch, *qr = g.Q + (size_t)qi * g.pitch;
         const uint32_t gi = i + g.id_offset, gq = qi + g.qi0, lv = (uint32_t)(c + 1);
         for (unsigned b0 = sub * ADV_P; b0 < nb; b0 += tpp * ADV_P) sum += draw4_pair(g, xr, qr, gi, gq, lv, b0);
       }
@@ -568,7 +579,7 @@ cudaError_t launch_filter(const Geom &g, cudaStream_t s) {
 }
 
 cudaError_t launch_compact(const Geom &g, cudaStream_t s) {
-  k_plan<<<1, 32, 0, s>>>(g.ctl);
+  k_plan<<<1, 32, 0, s>>>(g.ctl, g.adv_bpl);
   k_scatter<<<dim3(g.q, cdiv(g.npad, FIL_NT * 4)), FIL_NT, 0, s>>>(g);
   return cudaGetLastError();
 }
