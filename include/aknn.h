@@ -74,8 +74,12 @@ typedef struct {
                          and return AKNN_EMAXROUNDS with the state reached    */
   int32_t timing;     /* 1 = time each kernel class with CUDA events on the
                          launching stream and fill aknn_stats.ms_*           */
-  int32_t reserved;
+  int32_t flags;      /* bit 0 (AKNN_FLAG_RADIX_SELECT): decide every rank split
+                         with the multi-pass radix select instead of the one-pass
+                         pivot select (diagnostics; results are identical)       */
 } aknn_opts;
+
+#define AKNN_FLAG_RADIX_SELECT 1
 
 /* Execution statistics of the last query call on an index (aknn_get_stats).
  * Kernel classes: init (a2), select (a6-a7: rank split, bounds, Eq. 5),
@@ -101,6 +105,9 @@ typedef struct {
       launches_advance, launches_output;
   int64_t philox_blocks;      /* Philox4x32-10 blocks the level gathers drew
                                  (one per 4 draws; levels 1 and 2 use one)      */
+  int32_t graph_builds;       /* round-loop graphs captured + instantiated by
+                                 this call (0 when the cached graph was reused) */
+  int32_t pad0;
 } aknn_stats;
 
 /* ------------------------------------------------------------------------ */

@@ -44,7 +44,10 @@ class Result(C.Structure):
 
 class Opts(C.Structure):
     _fields_ = [("qi_offset", C.c_int32), ("max_rounds", C.c_int32), ("timing", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("flags", C.c_int32)]
+
+
+FLAG_RADIX_SELECT = 1
 
 
 class Stats(C.Structure):
@@ -58,7 +61,7 @@ class Stats(C.Structure):
                 ("launches_init", C.c_int64), ("launches_select", C.c_int64),
                 ("launches_filter", C.c_int64), ("launches_compact", C.c_int64),
                 ("launches_advance", C.c_int64), ("launches_output", C.c_int64),
-                ("philox_blocks", C.c_int64)]
+                ("philox_blocks", C.c_int64), ("graph_builds", C.c_int32), ("pad0", C.c_int32)]
 
 
 class MergeResult(C.Structure):
@@ -128,7 +131,7 @@ def alpha_table(n: int, delta: float, d: int, kind: str = "theory", c_alpha: flo
 
 def query_multi(shards, queries, k: int, h: int, delta: float, seed: int = 0, alpha=None, *,
                 counts: bool = True, sums: bool = False, dhat: bool = True, max_rounds: int = 0,
-                qi_offset: int = 0, timing: bool = False) -> dict:
+                qi_offset: int = 0, timing: bool = False, flags: int = 0) -> dict:
     """aknn_query_multi: one query batch over shard indices on the current device.
 
     ``shards`` are Index objects built with ``Index(rows, n_global=..., offset=...)``
@@ -146,7 +149,7 @@ def query_multi(shards, queries, k: int, h: int, delta: float, seed: int = 0, al
     res = Result(*[_ptr(out[f]) for f, _ in Result._fields_])
     al = None if alpha is None else np.ascontiguousarray(alpha, np.float64)
     arr = (_P * len(shards))(*[s._h for s in shards])
-    opts = Opts(qi_offset, max_rounds, 1 if timing else 0, 0)
+    opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags)
     st = _lib.aknn_query_multi(arr, len(shards), _ptr(Q), q, k, h, delta, seed & (2**64 - 1),
                                _ptr(al), C.byref(opts), C.byref(res))
     out["status"] = st
@@ -235,7 +238,8 @@ class Index:
     # ------------------------------------------------------------------ query
     def query(self, queries, k: int, h: int, delta: float, seed: int = 0, alpha=None, *,
               counts: bool = True, sums: bool = False, dhat: bool = True, max_rounds: int = 0,
-              qi_offset: int = 0, timing: bool = False, out: Optional[dict] = None) -> dict:
+              qi_offset: int = 0, timing: bool = False, out: Optional[dict] = None,
+              flags: int = 0) -> dict:
         """aknn_query_ex on host arrays; returns numpy arrays.
 
         ``out`` may pass preallocated (e.g. pinned) host arrays with the keys of the
@@ -268,7 +272,7 @@ class Index:
         al = None if alpha is None else np.ascontiguousarray(alpha, np.float64)
         if al is not None and al.shape != (self.d + 1,):
             raise AknnError(AKNN_EINVAL, f"alpha must have d+1={self.d + 1} entries")
-        opts = Opts(qi_offset, max_rounds, 1 if timing else 0, 0)
+        opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags)
         st = _lib.aknn_query_ex(self._h, _ptr(Q), q, k, h, delta, seed & (2**64 - 1), _ptr(al),
                                 C.byref(opts), C.byref(res))
         out["status"] = st
@@ -279,7 +283,7 @@ class Index:
     def query_device(self, queries, k: int, h: int, delta: float, seed: int = 0, alpha=None, *,
                      counts: bool = False, sums: bool = False, dhat: bool = True,
                      max_rounds: int = 0, qi_offset: int = 0, timing: bool = False,
-                     stream=None, out: Optional[dict] = None) -> dict:
+                     stream=None, out: Optional[dict] = None, flags: int = 0) -> dict:
         """aknn_query_async on torch CUDA tensors (current stream); returns device tensors."""
         torch = _torch()
         assert queries.is_cuda and queries.dtype == torch.uint8
@@ -300,7 +304,7 @@ class Index:
         if alpha is not None:
             al = alpha if (hasattr(alpha, "is_cuda") and alpha.is_cuda) else \
                 torch.as_tensor(np.ascontiguousarray(alpha, np.float64)).to(dev)
-        opts = Opts(qi_offset, max_rounds, 1 if timing else 0, 0)
+        opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags)
         st = _lib.aknn_query_async(self._h, _ptr(Q), q, k, h, delta, seed & (2**64 - 1), _ptr(al),
                                    C.byref(opts), C.byref(res), _stream_ptr(stream))
         out["status"] = st

@@ -288,7 +288,8 @@ struct PhaseTimer {
 // scatter -> advance -> zero -> rank split -> k_round_ctl, the last of which sets the
 // condition on the device.  No host round trip per round.  The instantiated graph is
 // cached on the index and reused while the launch parameters are unchanged.
-aknn_status loop_graph(aknn_index *ix, const Geom &g, int nbits, int max_rounds, cudaGraphExec_t *out) {
+aknn_status loop_graph(aknn_index *ix, const Geom &g, int nbits, int max_rounds, cudaGraphExec_t *out,
+                       int32_t *builds) {
   std::vector<unsigned char> key(sizeof(Geom) + 2 * sizeof(int));
   memcpy(key.data(), &g, sizeof(Geom));
   memcpy(key.data() + sizeof(Geom), &nbits, sizeof(int));
@@ -353,6 +354,7 @@ aknn_status loop_graph(aknn_index *ix, const Geom &g, int nbits, int max_rounds,
   }
   cudaGraphExec_t exec = nullptr;
   CU(cudaGraphInstantiate(&exec, graph, 0));
+  ++*builds;
   ix->loop_exec = exec;
   ix->loop_key = key;
   *out = exec;
@@ -427,6 +429,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   g.world = 1;
   g.cmax = kg.cmax;
   g.adv_bpl = adv_bpl();
+  g.force_radix = (o.flags & AKNN_FLAG_RADIX_SELECT) ? 1 : 0;
 
   aknn_stats stats{};
   stats.pairs = (int64_t)q * n;
@@ -456,22 +459,11 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
                          qn, cudaMemcpyDeviceToDevice, st));
     int r = 0;
     if (use_graph) {
-      // device-driven loop: one graph launch per sub-batch, no host round trips
+      // device-driven loop: one graph launch per sub-batch; the outputs are enqueued
+      // behind it and the control block is read back once, at the end
       cudaGraphExec_t exec = nullptr;
-      TRY(loop_graph(ix, g, kg.nbits, o.max_rounds, &exec));
+      TRY(loop_graph(ix, g, kg.nbits, o.max_rounds, &exec, &stats.graph_builds));
       CU(cudaGraphLaunch(exec, st));
-      RoundCtl c;
-      CU(cudaMemcpyAsync(&c, g.ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
-      CU(cudaStreamSynchronize(st));
-      r = (int)c.round;
-      stats.query_rounds += (int64_t)c.qrounds;
-      stats.blocked_query_rounds += (int64_t)c.brounds;
-      stats.launches_init += 3;
-      stats.launches_select += 2 * r;  // rank split + round control
-      stats.launches_filter += r - 1;
-      stats.launches_compact += 2 * (r - 1);
-      stats.launches_advance += 2 * (r - 1);  // advance + counter reset
-      if (c.n_active > 0) status = AKNN_EMAXROUNDS;
     }
     if (!use_graph) {
     CU(cudaMemsetAsync(g.ctl, 0, sizeof(RoundCtl), st));
@@ -487,7 +479,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
       tm.start();
       CU(launch_select(g, kg.nbits, st));
       tm.stop(PH_SELECT);
-      ++stats.launches_select;
+      stats.launches_select += 2;
       stats.query_rounds += evaluated;
       CU(cudaMemcpyAsync(h_active, &g.ctl->n_active, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
       CU(cudaStreamSynchronize(st));
@@ -514,7 +506,6 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
       if (r > 1 + 64 * 64) return fail(AKNN_ECUDA, "round loop did not terminate (internal error)");
     }
     }  // host-driven loop
-    if (r > stats.rounds) stats.rounds = r;
     OutPtrs op{(int)r0, 0, n, 0, out->sets, out->dhat, out->counts, out->sums, out->evals, out->draws, out->rounds};
     tm.start();
     CU(launch_output(g, op, st));
@@ -525,6 +516,18 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
     std::vector<QState> qs(qn);
     CU(cudaMemcpyAsync(qs.data(), g.qs, sizeof(QState) * qn, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    if (use_graph) {
+      r = (int)ctl_h.round;
+      stats.query_rounds += (int64_t)ctl_h.qrounds;
+      stats.blocked_query_rounds += (int64_t)ctl_h.brounds;
+      stats.launches_init += 3;
+      stats.launches_select += 3 * r;  // pivot select + radix fallback + round control
+      stats.launches_filter += r - 1;
+      stats.launches_compact += 2 * (r - 1);
+      stats.launches_advance += 2 * (r - 1);  // advance + counter reset
+      if (ctl_h.n_active > 0) status = AKNN_EMAXROUNDS;
+    }
+    if (r > stats.rounds) stats.rounds = r;
     stats.active_pair_rounds += (int64_t)ctl_h.advanced;
     for (const QState &s : qs) {
       stats.draws += s.draws;
@@ -653,6 +656,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     g.kbits = kg[si].kbits;
     g.cmax = kg[si].cmax;
     g.adv_bpl = adv_bpl();
+    g.force_radix = (o.flags & AKNN_FLAG_RADIX_SELECT) ? 1 : 0;
     g.world = W;
     g.recv_stride = recv_stride;
     if (has_recv) g.recv = ix->ws.as<ShardRec>(oRecv);

@@ -27,6 +27,8 @@ struct QState {
   double a_d2;                // alpha_{d2}             (Eq. 4 batched)
   int d1, d2;                 // local ids of d1, d2
   int done;                   // 1 once Eq. (5) held
+  int fallback;               // 1: the one-pass pivot select could not decide this
+                              //    round; the multi-pass radix select does
   int rounds;                 // rounds evaluated
   long long draws;            // sampled draws so far
   long long nexact;           // exact fallbacks so far
@@ -89,6 +91,7 @@ struct Geom {
   int world;             // shards taking part (1 = unsharded)
   int cmax;              // largest sampled level (2^cmax < d)
   unsigned adv_bpl;      // advance: Philox blocks per lane before a lane-group reduce
+  int force_radix;       // 1: skip the pivot select (aknn_opts.flags bit 0)
 };
 
 // ---- Philox4x32-10 (Salmon et al.), counter (x,y,z,w), key (k0,k1) --------

@@ -34,6 +34,9 @@ cudaError_t launch_round_ctl(RoundCtl *ctl, cudaGraphConditionalHandle h, int ma
 cudaError_t launch_output(const Geom &g, const OutPtrs &o, cudaStream_t s);
 // Sharded rounds (shard_kernels.cu).
 cudaError_t launch_select_local(const Geom &g, int nbits, cudaStream_t s);
+// One-pass pivot selects (select_pivot.cu); flag QState.fallback when undecided.
+cudaError_t launch_select_pivot(const Geom &g, cudaStream_t s);
+cudaError_t launch_select_local_pivot(const Geom &g, cudaStream_t s);
 cudaError_t launch_merge(const Geom &g, const OutPtrs &o, cudaStream_t s);
 cudaError_t launch_output_sharded(const Geom &g, const OutPtrs &o, cudaStream_t s);
 size_t merge_smem_bytes(int world, int kh);

@@ -45,4 +45,45 @@ struct Best {
   double a;
 };
 
+struct RecBest {  // a candidate for d1 (max U) or d2 (min L), ties to the smaller global id
+  double v;
+  uint32_t gid;
+  int32_t S;
+  uint8_t lvl;
+};
+
+__device__ __forceinline__ bool better_min(const RecBest &a, const RecBest &b) {
+  return a.v < b.v || (a.v == b.v && a.gid < b.gid);
+}
+__device__ __forceinline__ bool better_max(const RecBest &a, const RecBest &b) {
+  return a.v > b.v || (a.v == b.v && a.gid < b.gid);
+}
+
+__device__ __forceinline__ RecBest shfl_best(const RecBest &b, int o) {
+  RecBest r;
+  r.v = __shfl_xor_sync(FULL, b.v, o);
+  r.gid = __shfl_xor_sync(FULL, b.gid, o);
+  r.S = __shfl_xor_sync(FULL, b.S, o);
+  r.lvl = (uint8_t)__shfl_xor_sync(FULL, (unsigned)b.lvl, o);
+  return r;
+}
+
+// Block-wide arg-min (want_max = false) or arg-max; result valid in every thread.
+template <bool want_max>
+__device__ RecBest block_best(RecBest b, RecBest *wsm) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const RecBest t = shfl_best(b, o);
+    if (want_max ? better_max(t, b) : better_min(t, b)) b = t;
+  }
+  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (lane_id() == 0) wsm[w] = b;
+  __syncthreads();
+  RecBest r = wsm[0];
+  for (int i = 1; i < nw; ++i)
+    if (want_max ? better_max(wsm[i], r) : better_min(wsm[i], r)) r = wsm[i];
+  return r;
+}
+
 }  // namespace aknn

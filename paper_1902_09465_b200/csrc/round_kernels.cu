@@ -50,6 +50,7 @@ __global__ void k_init_qstate(Geom g) {
   s.A = s.B = s.a_d2 = 0.0;
   s.d1 = s.d2 = -1;
   s.done = 0;
+  s.fallback = 0;
   s.rounds = 0;
   s.draws = g.n;  // one initial draw per arm
   s.nexact = 0;
@@ -58,12 +59,13 @@ __global__ void k_init_qstate(Geom g) {
 }
 
 // a6 + a7: rank split, d1/d2/A/B, Eq. (5).  One CTA per query.
+// Multi-pass radix version; runs only for queries the pivot select flagged.
 __global__ void __launch_bounds__(SEL_NT) k_select(Geom g, int nbits) {
   __shared__ SelSmem sm;
   __shared__ Best wbest[2][SEL_NT / 32];
   const int qi = blockIdx.x;
   QState *st = g.qs + qi;
-  if (st->done) return;
+  if (st->done || !st->fallback) return;
   const int tid = threadIdx.x;
   ArmKeys keys{&g, qi};
   unsigned long long thk, thkh;
@@ -569,6 +571,8 @@ cudaError_t launch_init(const Geom &g, cudaStream_t s) {
 }
 
 cudaError_t launch_select(const Geom &g, int nbits, cudaStream_t s) {
+  const cudaError_t e = launch_select_pivot(g, s);
+  if (e != cudaSuccess) return e;
   k_select<<<g.q, SEL_NT, 0, s>>>(g, nbits);
   return cudaGetLastError();
 }

@@ -21,47 +21,6 @@
 
 namespace aknn {
 
-struct RecBest {  // a candidate for d1 (max U) or d2 (min L), ties to the smaller global id
-  double v;
-  uint32_t gid;
-  int32_t S;
-  uint8_t lvl;
-};
-
-__device__ __forceinline__ bool better_min(const RecBest &a, const RecBest &b) {
-  return a.v < b.v || (a.v == b.v && a.gid < b.gid);
-}
-__device__ __forceinline__ bool better_max(const RecBest &a, const RecBest &b) {
-  return a.v > b.v || (a.v == b.v && a.gid < b.gid);
-}
-
-__device__ __forceinline__ RecBest shfl_best(const RecBest &b, int o) {
-  RecBest r;
-  r.v = __shfl_xor_sync(FULL, b.v, o);
-  r.gid = __shfl_xor_sync(FULL, b.gid, o);
-  r.S = __shfl_xor_sync(FULL, b.S, o);
-  r.lvl = (uint8_t)__shfl_xor_sync(FULL, (unsigned)b.lvl, o);
-  return r;
-}
-
-// Block-wide arg-min (want_max = false) or arg-max; result valid in every thread.
-template <bool want_max>
-__device__ RecBest block_best(RecBest b, RecBest *wsm) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    const RecBest t = shfl_best(b, o);
-    if (want_max ? better_max(t, b) : better_min(t, b)) b = t;
-  }
-  const int w = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  __syncthreads();
-  if (lane_id() == 0) wsm[w] = b;
-  __syncthreads();
-  RecBest r = wsm[0];
-  for (int i = 1; i < nw; ++i)
-    if (want_max ? better_max(wsm[i], r) : better_min(wsm[i], r)) r = wsm[i];
-  return r;
-}
-
 // ---------------------------------------------------------------------------
 // Local summary of one query (one CTA per undecided query).
 __global__ void __launch_bounds__(SEL_NT) k_select_local(Geom g, int nbits) {
@@ -69,7 +28,7 @@ __global__ void __launch_bounds__(SEL_NT) k_select_local(Geom g, int nbits) {
   __shared__ RecBest wsm[SEL_NT / 32];
   __shared__ unsigned cnt;
   const int qi = blockIdx.x;
-  if (g.qs[qi].done) return;
+  if (g.qs[qi].done || !g.qs[qi].fallback) return;  // the pivot select decided it
   const int tid = threadIdx.x;
   const unsigned kh = (unsigned)(g.k + g.h);
   ArmKeys keys{&g, qi};
@@ -244,6 +203,8 @@ __global__ void k_counts_sharded(Geom g, OutPtrs o) {
 static inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 
 cudaError_t launch_select_local(const Geom &g, int nbits, cudaStream_t s) {
+  const cudaError_t e = launch_select_local_pivot(g, s);
+  if (e != cudaSuccess) return e;
   k_select_local<<<g.q, SEL_NT, 0, s>>>(g, nbits);
   return cudaGetLastError();
 }

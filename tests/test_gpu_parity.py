@@ -211,3 +211,30 @@ def test_graph_loop_equals_host_loop(ak, max_rounds):
     assert sa["blocked_query_rounds"] == sc["blocked_query_rounds"]
     ref = orc.query_br(X, Q, 6, 4, 5, al, want_sums=True, max_rounds=max_rounds)
     _assert_parity(a, ref)
+
+
+@pytest.mark.parametrize("n,d,q,k,h", [(20011, 96, 3, 7, 9), (30000, 64, 4, 40, 40), (700, 32, 3, 3, 3)])
+def test_pivot_select_equals_radix_select(ak, n, d, q, k, h):
+    """The one-pass pivot rank split and the multi-pass radix select (forced with
+    AKNN_FLAG_RADIX_SELECT) decide every round identically; both equal the oracle."""
+    X, Q = synth.small_instance(n + 1, n, d, q=q)
+    al = orc.alpha_experimental(n, 0.05, d, 0.05)
+    ix = ak.Index(X)
+    a = ix.query(Q, k, h, 0.05, 9, al, counts=True, sums=True)
+    b = ix.query(Q, k, h, 0.05, 9, al, counts=True, sums=True, flags=ak.FLAG_RADIX_SELECT)
+    ix.close()
+    for key in KEYS:
+        assert np.array_equal(a[key], b[key]), key
+    _assert_parity(a, orc.query_br(X, Q, k, h, 9, al, want_sums=True))
+
+
+def test_sharded_radix_flag_equals_pivot(ak):
+    X, Q = synth.small_instance(5, 12000, 48, q=3)
+    al = orc.alpha_experimental(12000, 0.05, 48, 0.05)
+    sh = [ak.Index(X[a:b], n_global=12000, offset=a) for a, b in ((0, 5000), (5000, 12000))]
+    a = ak.query_multi(sh, Q, 8, 8, 0.05, 4, al, counts=True, sums=True)
+    b = ak.query_multi(sh, Q, 8, 8, 0.05, 4, al, counts=True, sums=True, flags=ak.FLAG_RADIX_SELECT)
+    for s in sh:
+        s.close()
+    for key in KEYS:
+        assert np.array_equal(a[key], b[key]), key
