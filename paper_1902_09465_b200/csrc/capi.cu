@@ -74,6 +74,25 @@ unsigned long long gcd_u64(unsigned long long a, unsigned long long b) {
   return a;
 }
 
+// Pinned host staging (device->host reads of the round control block and query
+// states): a pageable destination would make cudaMemcpyAsync block in the driver.
+struct HostBuf {
+  void *p = nullptr;
+  size_t bytes = 0;
+  ~HostBuf() {
+    if (p) cudaFreeHost(p);
+  }
+  cudaError_t ensure(size_t want) {
+    if (bytes >= want) return cudaSuccess;
+    if (p) cudaFreeHost(p);
+    p = nullptr;
+    bytes = 0;
+    const cudaError_t e = cudaMallocHost(&p, want);
+    if (e == cudaSuccess) bytes = want;
+    return e;
+  }
+};
+
 struct DevBuf {
   void *p = nullptr;
   size_t bytes = 0;
@@ -130,6 +149,7 @@ struct aknn_index {
   DevBuf alpha;            // [d+1]
   DevBuf outs;             // device outputs for the host API
   DevBuf exact_ws;
+  HostBuf host;            // pinned: n_active | RoundCtl | QState[qb]
   DevBuf nx;               // [n_local] ||x_i||^2 for the tensor-core exact pass (lazy)
   bool nx_ready = false;
   EventPool events;
@@ -241,6 +261,24 @@ aknn_status host_alpha_table(int kind, int64_t n, double delta, double c_alpha, 
     return AKNN_OK;
   }
   return fail(AKNN_EINVAL, "alpha kind %d unknown (0 = footnote 2, 1 = section 5)", kind);
+}
+
+// Waits for `st` by polling an event instead of blocking in cudaStreamSynchronize:
+// a blocked host thread can be descheduled (seen on the VM hosts: wake-ups 100+ ms
+// late), and every round trip of the host loop -- and the return of every call --
+// would pay for it.  The spin costs one host core while the device works.
+cudaError_t sync_spin(cudaStream_t st) {
+  thread_local cudaEvent_t ev = nullptr;
+  if (!ev) {
+    const cudaError_t e = cudaEventCreateWithFlags(&ev, cudaEventDisableTiming);
+    if (e != cudaSuccess) return e;
+  }
+  cudaError_t e = cudaEventRecord(ev, st);
+  if (e != cudaSuccess) return e;
+  for (;;) {
+    e = cudaEventQuery(ev);
+    if (e != cudaErrorNotReady) return e;
+  }
 }
 
 // Per-launch CUDA events on the launching stream, read after the call's final
@@ -430,6 +468,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   g.cmax = kg.cmax;
   g.adv_bpl = adv_bpl();
   g.force_radix = (o.flags & AKNN_FLAG_RADIX_SELECT) ? 1 : 0;
+  g.stage_lo = stage_level(g.pitch);
 
   aknn_stats stats{};
   stats.pairs = (int64_t)q * n;
@@ -440,12 +479,10 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   PhaseTimer tm(o.timing != 0, st, &ix->events);
   tm.start();
   cudaEvent_t all_a = tm.open_a;
-  unsigned int *h_active = nullptr;
-  CU(cudaMallocHost(&h_active, sizeof(unsigned int)));
-  struct HostFree {
-    unsigned int *p;
-    ~HostFree() { cudaFreeHost(p); }
-  } hf{h_active};
+  CU(ix->host.ensure(256 + sizeof(RoundCtl) + sizeof(QState) * (size_t)qb));
+  unsigned int *h_active = static_cast<unsigned int *>(ix->host.p);
+  RoundCtl *h_ctl = reinterpret_cast<RoundCtl *>(static_cast<char *>(ix->host.p) + 256);
+  QState *h_qs = reinterpret_cast<QState *>(h_ctl + 1);
   tm.open_a = nullptr;
   aknn_status status = AKNN_OK;
   for (int64_t r0 = 0; r0 < q; r0 += qb) {
@@ -482,7 +519,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
       stats.launches_select += 2;
       stats.query_rounds += evaluated;
       CU(cudaMemcpyAsync(h_active, &g.ctl->n_active, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
-      CU(cudaStreamSynchronize(st));
+      CU(sync_spin(st));
       const unsigned nact = *h_active;
       stats.blocked_query_rounds += nact;
       evaluated = nact;
@@ -511,11 +548,11 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
     CU(launch_output(g, op, st));
     tm.stop(PH_OUTPUT);
     stats.launches_output += (out->counts || out->sums) ? 2 : 1;
-    RoundCtl ctl_h;
-    CU(cudaMemcpyAsync(&ctl_h, g.ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
-    std::vector<QState> qs(qn);
-    CU(cudaMemcpyAsync(qs.data(), g.qs, sizeof(QState) * qn, cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
+    CU(cudaMemcpyAsync(h_ctl, g.ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
+    CU(cudaMemcpyAsync(h_qs, g.qs, sizeof(QState) * qn, cudaMemcpyDeviceToHost, st));
+    CU(sync_spin(st));
+    const RoundCtl &ctl_h = *h_ctl;
+    const QState *qs = h_qs;
     if (use_graph) {
       r = (int)ctl_h.round;
       stats.query_rounds += (int64_t)ctl_h.qrounds;
@@ -529,16 +566,16 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
     }
     if (r > stats.rounds) stats.rounds = r;
     stats.active_pair_rounds += (int64_t)ctl_h.advanced;
-    for (const QState &s : qs) {
-      stats.draws += s.draws;
-      stats.exact_fallbacks += s.nexact;
-      stats.philox_blocks += s.blocks;
+    for (int a = 0; a < qn; ++a) {
+      stats.draws += qs[a].draws;
+      stats.exact_fallbacks += qs[a].nexact;
+      stats.philox_blocks += qs[a].blocks;
     }
     if (status != AKNN_OK) break;
   }
   tm.open_a = all_a;
   tm.stop(PH_ALL);
-  CU(cudaStreamSynchronize(st));
+  CU(sync_spin(st));
   double ms[PH_N];
   tm.resolve(ms);
   stats.ms_init = ms[PH_INIT];
@@ -597,7 +634,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     if (ncclAllReduce(tmp.p, tmp.p, 1, ncclInt64, ncclMin, ix0->comm, st) != ncclSuccess)
       return fail(AKNN_ENCCL, "ncclAllReduce(qb) failed");
     CU(cudaMemcpyAsync(&qb, tmp.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    CU(cudaStreamSynchronize(st));
+    CU(sync_spin(st));
   }
 #endif
   if (qb < 1) return fail(AKNN_ENOMEM, "not enough device memory for one query row");
@@ -657,6 +694,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     g.cmax = kg[si].cmax;
     g.adv_bpl = adv_bpl();
     g.force_radix = (o.flags & AKNN_FLAG_RADIX_SELECT) ? 1 : 0;
+    g.stage_lo = stage_level(g.pitch);
     g.world = W;
     g.recv_stride = recv_stride;
     if (has_recv) g.recv = ix->ws.as<ShardRec>(oRecv);
@@ -677,12 +715,10 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
   tm.start();
   cudaEvent_t all_a = tm.open_a;
   tm.open_a = nullptr;
-  unsigned int *h_active = nullptr;
-  CU(cudaMallocHost(&h_active, sizeof(unsigned int)));
-  struct HostFree {
-    unsigned int *p;
-    ~HostFree() { cudaFreeHost(p); }
-  } hf{h_active};
+  CU(ix0->host.ensure(256 + sizeof(RoundCtl) + sizeof(QState) * (size_t)qb));
+  unsigned int *h_active = static_cast<unsigned int *>(ix0->host.p);
+  RoundCtl *h_ctl = reinterpret_cast<RoundCtl *>(static_cast<char *>(ix0->host.p) + 256);
+  QState *h_qs = reinterpret_cast<QState *>(h_ctl + 1);
   const size_t nS = shards.size();
   aknn_status status = AKNN_OK;
   for (int64_t r0 = 0; r0 < q; r0 += qb) {
@@ -731,7 +767,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
       tm.stop(PH_SELECT);
       stats.query_rounds += evaluated;
       CU(cudaMemcpyAsync(h_active, &G[0].ctl->n_active, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
-      CU(cudaStreamSynchronize(st));
+      CU(sync_spin(st));
       const unsigned nact = *h_active;
       stats.blocked_query_rounds += nact;
       evaluated = nact;
@@ -772,23 +808,23 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
 #endif
     tm.stop(PH_OUTPUT);
     for (size_t si = 0; si < nS; ++si) {
-      RoundCtl ctl_h;
-      CU(cudaMemcpyAsync(&ctl_h, G[si].ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
-      std::vector<QState> qs(qn);
-      CU(cudaMemcpyAsync(qs.data(), G[si].qs, sizeof(QState) * qn, cudaMemcpyDeviceToHost, st));
-      CU(cudaStreamSynchronize(st));
+      CU(cudaMemcpyAsync(h_ctl, G[si].ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
+      CU(cudaMemcpyAsync(h_qs, G[si].qs, sizeof(QState) * qn, cudaMemcpyDeviceToHost, st));
+      CU(sync_spin(st));
+      const RoundCtl &ctl_h = *h_ctl;
+      const QState *qs = h_qs;
       stats.active_pair_rounds += (int64_t)ctl_h.advanced;
-      for (const QState &x : qs) {
-        stats.draws += x.draws;
-        stats.exact_fallbacks += x.nexact;
-        stats.philox_blocks += x.blocks;
+      for (int a = 0; a < qn; ++a) {
+        stats.draws += qs[a].draws;
+        stats.exact_fallbacks += qs[a].nexact;
+        stats.philox_blocks += qs[a].blocks;
       }
     }
     if (status != AKNN_OK) break;
   }
   tm.open_a = all_a;
   tm.stop(PH_ALL);
-  CU(cudaStreamSynchronize(st));
+  CU(sync_spin(st));
   double ms[PH_N];
   tm.resolve(ms);
   stats.ms_init = ms[PH_INIT];
@@ -1000,7 +1036,7 @@ aknn_status host_query(const std::vector<aknn_index *> &shards, bool multi, cons
   if (out->evals) CU(cudaMemcpyAsync(out->evals, dout.evals, szEv, cudaMemcpyDeviceToHost, st));
   if (out->draws) CU(cudaMemcpyAsync(out->draws, dout.draws, szDr, cudaMemcpyDeviceToHost, st));
   if (out->rounds) CU(cudaMemcpyAsync(out->rounds, dout.rounds, szRo, cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
+  CU(sync_spin(st));
   return s;
 }
 }  // namespace
@@ -1226,7 +1262,7 @@ aknn_status aknn_exact(const aknn_index *cix, const uint8_t *queries, int32_t q,
   TRY(aknn_exact_async(ix, dq, q, k, di, dd, st));
   CU(cudaMemcpyAsync(idx, di, szO, cudaMemcpyDeviceToHost, st));
   CU(cudaMemcpyAsync(dist2, dd, szO, cudaMemcpyDeviceToHost, st));
-  CU(cudaStreamSynchronize(st));
+  CU(sync_spin(st));
   return AKNN_OK;
 }
 

@@ -92,6 +92,7 @@ struct Geom {
   int cmax;              // largest sampled level (2^cmax < d)
   unsigned adv_bpl;      // advance: Philox blocks per lane before a lane-group reduce
   int force_radix;       // 1: skip the pivot select (aknn_opts.flags bit 0)
+  int stage_lo;          // first row-staged advance level (MAX_LEVELS = none)
 };
 
 // ---- Philox4x32-10 (Salmon et al.), counter (x,y,z,w), key (k0,k1) --------

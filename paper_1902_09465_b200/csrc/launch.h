@@ -27,6 +27,7 @@ cudaError_t launch_select(const Geom &g, int nbits, cudaStream_t s);
 cudaError_t launch_filter(const Geom &g, cudaStream_t s);
 cudaError_t launch_compact(const Geom &g, cudaStream_t s);
 cudaError_t launch_advance(const Geom &g, int num_sms, cudaStream_t s);
+int stage_level(int64_t pitch);
 // Device-driven round loop (CUDA graph with a conditional WHILE node).
 cudaError_t launch_ctl_reset(RoundCtl *ctl, unsigned q, cudaStream_t s);
 cudaError_t launch_zero_round(RoundCtl *ctl, cudaStream_t s);

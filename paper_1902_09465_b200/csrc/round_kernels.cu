@@ -220,13 +220,14 @@ __host__ __device__ __forceinline__ unsigned lanes_per_pair(unsigned nb, unsigne
   const unsigned t = nb / bpl;
   return t < 1u ? 1u : (t > 32u ? 32u : t);
 }
-__host__ __device__ __forceinline__ unsigned pairs_per_chunk(int slot, unsigned bpl) {
+__host__ __device__ __forceinline__ unsigned pairs_per_chunk(int slot, unsigned bpl, int stage_lo) {
   if (slot == MAX_LEVELS) return ADV_XP;
+  if (slot >= stage_lo) return 1u;  // row-staged levels: one pair per warp
   const unsigned nb = nblk_of(slot);
   return nb <= (unsigned)ADV_P ? 32u * ADV_P / nb : 32u / lanes_per_pair(nb, bpl);
 }
 
-__global__ void k_plan(RoundCtl *ctl, unsigned bpl) {
+__global__ void k_plan(RoundCtl *ctl, unsigned bpl, int stage_lo) {
   if (threadIdx.x != 0) return;
   unsigned off = 0;
   unsigned long long ch = 0, adv = 0;
@@ -237,7 +238,7 @@ __global__ void k_plan(RoundCtl *ctl, unsigned bpl) {
     ctl->cursor[s] = 0;
     off += c;
     adv += c;
-    const unsigned ppc = pairs_per_chunk(s, bpl);
+    const unsigned ppc = pairs_per_chunk(s, bpl, stage_lo);
     ch += (c + ppc - 1) / ppc;
   }
   ctl->off[NSLOT] = off;
@@ -417,13 +418,18 @@ __global__ void __launch_bounds__(ADV_NT) k_advance(Geom g) {
     }
   }
   __syncthreads();
-  const unsigned long long total = coff[NSLOT];
+  // this kernel takes the levels below stage_lo and the exact fallbacks; the
+  // row-staged levels [stage_lo, MAX_LEVELS) belong to k_advance_staged
+  const int slo = g.stage_lo < MAX_LEVELS ? g.stage_lo : MAX_LEVELS;
+  const unsigned long long total_a = coff[slo], skip = coff[MAX_LEVELS] - coff[slo];
+  const unsigned long long total = coff[NSLOT] - skip;
   const unsigned long long nwarps = (unsigned long long)gridDim.x * (ADV_NT / 32);
   const int lane = lane_id();
   const uint32_t imask = (1u << g.ibits) - 1u;
   int slot = 0;
-  for (unsigned long long ch = (unsigned long long)blockIdx.x * (ADV_NT / 32) + (threadIdx.x >> 5);
-       ch < total; ch += nwarps) {
+  for (unsigned long long vch = (unsigned long long)blockIdx.x * (ADV_NT / 32) + (threadIdx.x >> 5);
+       vch < total; vch += nwarps) {
+    const unsigned long long ch = vch < total_a ? vch : vch + skip;
     while (coff[slot + 1] <= ch) ++slot;  // chunks are visited in increasing order
     const unsigned long long rel = ch - coff[slot];
     if (slot == MAX_LEVELS) {
@@ -436,7 +442,7 @@ __global__ void __launch_bounds__(ADV_NT) k_advance(Geom g) {
     const uint32_t s = 1u << c;
     const unsigned nb = nblk_of(c);
     const uint8_t newlvl = (uint8_t)(c + 1);
-    const unsigned ppc = pairs_per_chunk(c, g.adv_bpl);
+    const unsigned ppc = pairs_per_chunk(c, g.adv_bpl, g.stage_lo);
     const unsigned pbase = (unsigned)rel * ppc;  // first pair of this chunk
     const uint32_t *lst = g.list + soff[c];
     const unsigned cnt = scnt[c];
@@ -494,6 +500,68 @@ __global__ void __launch_bounds__(ADV_NT) k_advance(Geom g) {
       for (unsigned o = tpp >> 1; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
       if (ok && sub == 0) commit(g, qi, i, sum, newlvl);
     }
+  }
+}
+
+// Row-staged levels (large d, many draws per pair): the warp copies the point's
+// row into shared memory with 16-byte loads (one streaming read of d bytes instead
+// of one random 32-byte sector per draw), then gathers its draws from there.
+__device__ __forceinline__ uint32_t draw4_pair_srow(const Geom &g, const uint8_t *sx, const uint8_t *__restrict__ qr,
+                                                    uint32_t gi, uint32_t gq, uint32_t lv, uint32_t blk0) {
+  uint4 w[ADV_P];
+#pragma unroll
+  for (int k = 0; k < ADV_P; ++k) w[k] = philox4x32_10_rk(make_uint4(blk0 + k, gi, gq, lv), g.rk0, g.rk1);
+  uint32_t acc = 0;
+#pragma unroll
+  for (int k = 0; k < ADV_P; ++k) {
+    const uint32_t ws[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint32_t j = coord_of(ws[e], (uint32_t)g.d);
+      const int diff = (int)sx[j] - (int)__ldg(qr + j);
+      acc += (uint32_t)(diff * diff);
+    }
+  }
+  return acc;
+}
+
+__global__ void __launch_bounds__(ADV_NT) k_advance_staged(Geom g) {
+  extern __shared__ uint4 srow[];
+  __shared__ unsigned long long coff[NSLOT + 1];
+  __shared__ unsigned soff[NSLOT];
+  for (int s = threadIdx.x; s <= NSLOT; s += ADV_NT) {
+    coff[s] = g.ctl->chunk_off[s];
+    if (s < NSLOT) soff[s] = g.ctl->off[s];
+  }
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = lane_id();
+  const int nv = (int)(g.pitch >> 4);
+  uint4 *sx = srow + (size_t)warp * nv;
+  const uint32_t imask = (1u << g.ibits) - 1u;
+  const unsigned long long c0 = coff[g.stage_lo], total = coff[MAX_LEVELS] - c0;
+  const unsigned long long nwarps = (unsigned long long)gridDim.x * (ADV_NT / 32);
+  int slot = g.stage_lo;
+  for (unsigned long long vch = (unsigned long long)blockIdx.x * (ADV_NT / 32) + warp; vch < total;
+       vch += nwarps) {
+    const unsigned long long ch = c0 + vch;
+    while (coff[slot + 1] <= ch) ++slot;
+    const int c = slot;
+    const unsigned nb = nblk_of(c);
+    const uint32_t code = g.list[soff[c] + (ch - coff[c])];
+    uint32_t qi, i;
+    decode(g, code, imask, qi, i);
+    const uint4 *xg = reinterpret_cast<const uint4 *>(g.X + (size_t)i * g.pitch);
+    __syncwarp();
+    for (int v = lane; v < nv; v += 32) sx[v] = __ldg(xg + v);
+    __syncwarp();
+    const uint8_t *sxb = reinterpret_cast<const uint8_t *>(sx);
+    const uint8_t *qr = g.Q + (size_t)qi * g.pitch;
+    const uint32_t gi = i + g.id_offset, gq = qi + g.qi0, lv = (uint32_t)(c + 1);
+    uint32_t sum = 0;
+    for (unsigned b0 = lane * ADV_P; b0 < nb; b0 += 32 * ADV_P) sum += draw4_pair_srow(g, sxb, qr, gi, gq, lv, b0);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+    if (lane == 0) commit(g, qi, i, sum, (uint8_t)(c + 1));
   }
 }
 
@@ -583,14 +651,32 @@ cudaError_t launch_filter(const Geom &g, cudaStream_t s) {
 }
 
 cudaError_t launch_compact(const Geom &g, cudaStream_t s) {
-  k_plan<<<1, 32, 0, s>>>(g.ctl, g.adv_bpl);
+  k_plan<<<1, 32, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo);
   k_scatter<<<dim3(g.q, cdiv(g.npad, FIL_NT * 4)), FIL_NT, 0, s>>>(g);
   return cudaGetLastError();
 }
 
 cudaError_t launch_advance(const Geom &g, int num_sms, cudaStream_t s) {
   k_advance<<<num_sms * 8, ADV_NT, 0, s>>>(g);
+  if (g.stage_lo < MAX_LEVELS) {
+    const size_t smem = (size_t)(ADV_NT / 32) * (size_t)g.pitch;
+    cudaError_t e = cudaFuncSetAttribute(k_advance_staged, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    const int per_sm = (int)((200u * 1024u) / (smem + 1024));
+    k_advance_staged<<<num_sms * (per_sm < 1 ? 1 : per_sm), ADV_NT, smem, s>>>(g);
+  }
   return cudaGetLastError();
+}
+
+// First level whose advance stages the point row in shared memory, or MAX_LEVELS for
+// none: rows of >= 4 KB (an L1 cannot hold a warp-row per resident warp) and levels
+// drawing at least pitch/64 coordinates (random sectors then cost more than one
+// streaming pass over the row); rows up to 24 KB (8 warps x pitch <= 192 KB).
+int stage_level(int64_t pitch) {
+  if (pitch < 4096 || pitch > 24 * 1024) return MAX_LEVELS;
+  int c = 0;
+  while ((1ll << c) * 64 < pitch) ++c;
+  return c < MAX_LEVELS ? c : MAX_LEVELS;
 }
 
 cudaError_t launch_output(const Geom &g, const OutPtrs &o, cudaStream_t s) {

@@ -61,6 +61,8 @@ CASES = [
     ("d2", 300, 2, 3, 3, 3, "theory", 0, 8, "uniform"),
     ("d3", 300, 3, 3, 3, 3, "exp", 0.1, 9, "uniform"),
     ("large_k", 5000, 48, 2, 300, 200, "exp", 0.05, 10, "mixture"),
+    ("row_staged_d5000", 1500, 5000, 2, 5, 5, "theory", 0, 11, "mixture"),
+    ("row_staged_exp", 3000, 8192, 2, 4, 4, "exp", 0.3, 12, "mixture"),
 ]
 
 

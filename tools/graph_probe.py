@@ -3,7 +3,7 @@ import os, sys, statistics
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 import synth, paper_1902_09465_b200 as ak
-cfg = synth.config(2)
+cfg = synth.config(int(sys.argv[1]) if len(sys.argv) > 1 else 2)
 X = synth.points(cfg); Q = synth.queries(cfg)
 al = torch.from_numpy(ak.alpha_table(cfg.n, cfg.delta, cfg.d, "theory")).cuda()
 ix = ak.Index(torch.from_numpy(X).cuda())
