@@ -134,6 +134,30 @@ def test_config2_full_size_sampled_queries(ak):
     _assert_parity(got, ref, rows=rows)
 
 
+@pytest.mark.parametrize("i,nsample", [(3, 1), (4, 2)])
+def test_full_size_configs_sampled_queries(ak, i, nsample):
+    """Configs 3 and 4 at their BASELINE sizes through the bench launch path (device API,
+    the whole query batch in one call, graph-launched loop); the oracle recomputes
+    `nsample` seeded queries of the batch in full (sets, d_hat, per-pair T and S,
+    draws, evals, rounds)."""
+    import torch
+    cfg = synth.config(i)
+    X = synth.points(cfg)
+    Q = synth.queries(cfg)
+    al = orc.alpha_theory(cfg.n, cfg.delta, cfg.d)
+    ix = ak.Index(torch.from_numpy(X).cuda())
+    rows = np.random.default_rng(i).choice(cfg.q, nsample, replace=False)
+    out = ix.query_device(torch.from_numpy(Q).cuda(), cfg.k, cfg.h, cfg.delta, cfg.seed, al,
+                          counts=True, sums=True)
+    torch.cuda.synchronize()
+    got = {k: v[torch.as_tensor(rows).cuda()].cpu().numpy()
+           for k, v in out.items() if k != "status" and v is not None}
+    ix.close()
+    del out
+    ref = orc.query_br(X, Q[rows], cfg.k, cfg.h, cfg.seed, al, qids=rows, want_sums=True)
+    _assert_parity(got, ref)
+
+
 def test_device_api_equals_host_api(ak):
     import torch
     X, Q = synth.small_instance(77, 3000, 120, q=9)
