@@ -508,7 +508,7 @@ def run_ours(args, dist: Dist):
             ok += strict <= s
         extra.update({"exact_pass_ms": ex_ms, "speedup_vs_exact": ex_ms / ms_per_step,
                       "recall_contains_knn": dist.sum(ok) / (qpr * dist.world),
-                      "exact_pass_kernel": "dp4a CUDA-core tiles (v1)"})
+                      "exact_pass_kernel": "tcgen05 kind::i8 tiles (k_mma_tiles) + block top-k"})
 
     # end to end through the host API (pinned host buffers, H2D + D2H inside the timed region)
     e2e = None
@@ -542,8 +542,9 @@ def run_ours(args, dist: Dist):
 
     cpu = None
     if not args.no_cpu_baseline and dist.rank == 0 and dist.world == 1:
+        # a bounded sample of the same workload: ~10-30 s of oracle work on the host cores
         cores = max(1, min(_cpu_cores(), 16))
-        nq = min(qpr, 16)
+        nq = min(qpr, 8 * cores)
         dt, _ = _oracle_time(X, Qh, cfg, _oracle_alpha(cfg, args.alpha), nq, cores)
         cpu = {"value": nq / dt, "unit": UNIT, "cores": min(cores, nq), "kind": "oracle",
                "sample": f"first {nq} queries of {cfg.name} (full n={n}, d={d}), one "

@@ -76,10 +76,14 @@ typedef struct {
                          launching stream and fill aknn_stats.ms_*           */
   int32_t flags;      /* bit 0 (AKNN_FLAG_RADIX_SELECT): decide every rank split
                          with the multi-pass radix select instead of the one-pass
-                         pivot select (diagnostics; results are identical)       */
+                         pivot select (diagnostics; results are identical);
+                         bit 1 (AKNN_FLAG_EXACT_ROWS): see below                  */
 } aknn_opts;
 
 #define AKNN_FLAG_RADIX_SELECT 1
+/* bit 1: compute the exact fallbacks by streaming each pair's row on the
+   CUDA cores instead of the tensor-core tile pass (diagnostics; identical results) */
+#define AKNN_FLAG_EXACT_ROWS 2
 
 /* Execution statistics of the last query call on an index (aknn_get_stats).
  * Kernel classes: init (a2), select (a6-a7: rank split, bounds, Eq. 5),

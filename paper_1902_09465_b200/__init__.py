@@ -48,6 +48,7 @@ class Opts(C.Structure):
 
 
 FLAG_RADIX_SELECT = 1
+FLAG_EXACT_ROWS = 2  # exact fallbacks as per-pair row streams instead of tensor-core tiles
 
 
 class Stats(C.Structure):

@@ -209,6 +209,32 @@ unsigned adv_bpl() {
   return v;
 }
 
+// Exact fallbacks on the tensor cores (exact_mma.cu) unless AKNN_FLAG_EXACT_ROWS.
+// Workspace: nq [qb] int32 and the tile flags [ceil(qb/128)][ceil(npad/256)].
+size_t exact_mma_ws_bytes(int64_t qb, int64_t npad) {
+  const int64_t rt = (qb + exact_tile_rows() - 1) / exact_tile_rows();
+  const int64_t ct = (npad + exact_tile_cols() - 1) / exact_tile_cols();
+  return round_up((size_t)qb * 4, 256) + round_up((size_t)(rt * ct) * 4, 256);
+}
+
+aknn_status setup_exact_mma(aknn_index *ix, Geom &g, int64_t qb, uint8_t *ws, const aknn_opts &o,
+                            cudaStream_t st) {
+  g.exact_mma = (o.flags & AKNN_FLAG_EXACT_ROWS) ? 0 : 1;
+  if (!g.exact_mma) return AKNN_OK;
+  if (!ix->nx_ready) {
+    const int64_t npad = round_up(ix->n_local, 16);
+    TRY(ix->nx.ensure(sizeof(int32_t) * (size_t)npad));
+    CU(cudaMemsetAsync(ix->nx.p, 0, sizeof(int32_t) * (size_t)npad, st));
+    CU(launch_row_norms(ix->X.as<uint8_t>(), ix->pitch, (int)ix->n_local, ix->nx.as<int32_t>(), st));
+    ix->nx_ready = true;
+  }
+  g.nx = ix->nx.as<int32_t>();
+  g.nq = reinterpret_cast<int32_t *>(ws);
+  g.xflags = reinterpret_cast<uint32_t *>(ws + round_up((size_t)qb * 4, 256));
+  g.xf_cols = (int)((g.npad + exact_tile_cols() - 1) / exact_tile_cols());
+  return AKNN_OK;
+}
+
 // Builds the level geometry of the composite key (R9).
 struct KeyGeom {
   unsigned long long L, Ld;
@@ -435,6 +461,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   const size_t oQ = off; off = round_up(off + szQ, 256);
   const size_t oQS = off; off = round_up(off + szQS, 256);
   const size_t oCtl = off; off = round_up(off + szCtl, 256);
+  const size_t oXm = off; off = round_up(off + exact_mma_ws_bytes(qb, npad), 256);
   TRY(ix->ws.ensure(off));
 
   Geom g{};
@@ -469,6 +496,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   g.adv_bpl = adv_bpl();
   g.force_radix = (o.flags & AKNN_FLAG_RADIX_SELECT) ? 1 : 0;
   g.stage_lo = stage_level(g.pitch);
+  TRY(setup_exact_mma(ix, g, qb, ix->ws.as<uint8_t>(oXm), o, st));
 
   aknn_stats stats{};
   stats.pairs = (int64_t)q * n;
@@ -662,6 +690,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     const size_t oCtl = off; off = round_up(off + szCtl, 256);
     const size_t oSend = off; off = round_up(off + szSend, 256);
     const size_t oRecv = off; off = round_up(off + szRecv, 256);
+    const size_t oXm = off; off = round_up(off + exact_mma_ws_bytes(qb, npad), 256);
     TRY(ix->ws.ensure(off));
     Geom &g = G[si];
     g = Geom{};
@@ -697,6 +726,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     g.stage_lo = stage_level(g.pitch);
     g.world = W;
     g.recv_stride = recv_stride;
+    TRY(setup_exact_mma(ix, g, qb, ix->ws.as<uint8_t>(oXm), o, st));
     if (has_recv) g.recv = ix->ws.as<ShardRec>(oRecv);
     if (si == 0 && !nccl) recv_shared = ix->ws.as<ShardRec>(oRecv);
     if (nccl) g.send = ix->ws.as<ShardRec>(oSend);

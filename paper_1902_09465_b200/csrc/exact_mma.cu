@@ -14,6 +14,11 @@
 //   warps 4-7       epilogue: tcgen05.ld 32x32b.x32 (lane = query row, 32 points per
 //                   load), D = nx + nq - 2 dot, int32 stores
 // The distances then go through the block radix top-k of exact_kernels.cu.
+//
+// The same tile kernel, with another epilogue (EpiFallback), computes the round
+// loop's exact fallbacks (row a4) when they are dense: under the footnote-2
+// radius nearly every arm of a query reaches 2T >= d and goes exact in the same
+// round, which as per-pair row streams re-reads n*d bytes per query from L2.
 #include <cuda.h>
 
 #include "internal.cuh"
@@ -78,10 +83,97 @@ __host__ __device__ constexpr uint32_t umma_idesc_u8(int M, int N) {
          | ((uint32_t)(M >> 4) << 24);   // M / 16
 }
 
+// Epilogue of the exact comparison pass: D = ||x||^2 + ||q||^2 - 2 dot, int32 rows.
+struct EpiDistances {
+  const int32_t *nq, *nx;
+  int32_t *D;
+  int64_t ldd;
+  int q, n;
+  __device__ __forceinline__ bool tile_active(int, int) const { return true; }
+  __device__ __forceinline__ void store(int row, int col0, const uint32_t (&v)[32]) const {
+    if (row >= q) return;
+    const int32_t nqr = __ldg(nq + row);
+    int32_t *drow = D + (size_t)row * ldd + col0;
+    if (col0 + 32 <= n) {
+#pragma unroll
+      for (int j = 0; j < 32; j += 4) {
+        const int4 xn = __ldg(reinterpret_cast<const int4 *>(nx + col0 + j));
+        int4 o;
+        o.x = xn.x + nqr - 2 * (int32_t)v[j + 0];
+        o.y = xn.y + nqr - 2 * (int32_t)v[j + 1];
+        o.z = xn.z + nqr - 2 * (int32_t)v[j + 2];
+        o.w = xn.w + nqr - 2 * (int32_t)v[j + 3];
+        *reinterpret_cast<int4 *>(drow + j) = o;
+      }
+    } else {
+      for (int j = 0; j < 32 && col0 + j < n; ++j) drow[j] = __ldg(nx + col0 + j) + nqr - 2 * (int32_t)v[j];
+    }
+  }
+};
+
+// Epilogue of the round loop's exact fallbacks (row a4): for every pair of
+// the tile whose action byte is ACT_EXACT, S = sum_j (x_j - q_j)^2 = D exactly and
+// the level becomes LVL_EXACT.  Tiles without a fallback (flag 0, set by k_filter)
+// exit before touching TMEM; the CTA clears its flag for the next round.
+struct EpiFallback {
+  Geom g;
+  __device__ __forceinline__ bool tile_active(int m0, int n0) const {
+    __shared__ uint32_t sflag;
+    uint32_t *f = g.xflags + (size_t)(m0 / MM_BM) * g.xf_cols + (n0 / MM_BN);
+    if (threadIdx.x == 0) {
+      sflag = *f;
+      if (sflag) *f = 0u;
+    }
+    __syncthreads();
+    return sflag != 0u;
+  }
+  __device__ __forceinline__ void store(int row, int col0, const uint32_t (&v)[32]) const {
+    if (row >= g.q || col0 >= g.n || g.qs[row].done) return;
+    const int32_t nqr = __ldg(g.nq + row);
+    const size_t o = (size_t)row * g.npad + col0;
+    uint8_t a[32];
+    if (col0 + 32 <= g.npad) {
+      const uint4 a0 = *reinterpret_cast<const uint4 *>(g.act + o);
+      const uint4 a1 = *reinterpret_cast<const uint4 *>(g.act + o + 16);
+      memcpy(a, &a0, 16);
+      memcpy(a + 16, &a1, 16);
+    } else {
+#pragma unroll
+      for (int j = 0; j < 32; ++j) a[j] = (col0 + j < g.npad) ? g.act[o + j] : (uint8_t)0;
+    }
+    int32_t *srow = g.S + o;
+    uint8_t *lrow = g.lvl + o;
+#pragma unroll
+    for (int j0 = 0; j0 < 32; j0 += 4) {
+      const bool all = a[j0] == ACT_EXACT && a[j0 + 1] == ACT_EXACT && a[j0 + 2] == ACT_EXACT &&
+                       a[j0 + 3] == ACT_EXACT && col0 + j0 + 4 <= g.n;
+      if (all) {
+        const int4 xn = __ldg(reinterpret_cast<const int4 *>(g.nx + col0 + j0));
+        int4 s4;
+        s4.x = xn.x + nqr - 2 * (int32_t)v[j0 + 0];
+        s4.y = xn.y + nqr - 2 * (int32_t)v[j0 + 1];
+        s4.z = xn.z + nqr - 2 * (int32_t)v[j0 + 2];
+        s4.w = xn.w + nqr - 2 * (int32_t)v[j0 + 3];
+        *reinterpret_cast<int4 *>(srow + j0) = s4;
+        *reinterpret_cast<uint32_t *>(lrow + j0) = 0xFFFFFFFFu;  // 4 x LVL_EXACT
+      } else {
+#pragma unroll
+        for (int j = j0; j < j0 + 4; ++j)
+          if (a[j] == ACT_EXACT && col0 + j < g.n) {
+            srow[j] = __ldg(g.nx + col0 + j) + nqr - 2 * (int32_t)v[j];
+            lrow[j] = LVL_EXACT;
+          }
+      }
+    }
+  }
+};
+
+template <class Epi>
 __global__ void __launch_bounds__(MM_NT, 1)
-    k_exact_mma(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmX,
-                const int32_t *__restrict__ nq, const int32_t *__restrict__ nx, int q, int n, int d,
-                int32_t *__restrict__ D, int64_t ldd) {
+    k_mma_tiles(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmX, int d,
+                const __grid_constant__ Epi epi) {
+  const int m0 = blockIdx.y * MM_BM, n0 = blockIdx.x * MM_BN;
+  if (!epi.tile_active(m0, n0)) return;  // uniform across the CTA
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char *sm = reinterpret_cast<unsigned char *>(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
   uint64_t *full = reinterpret_cast<uint64_t *>(sm + MM_STAGES * MM_STAGE_BYTES);
@@ -89,7 +181,6 @@ __global__ void __launch_bounds__(MM_NT, 1)
   uint64_t *tfull = empty + MM_STAGES;
   uint32_t *tmem_base = reinterpret_cast<uint32_t *>(tfull + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * MM_BM, n0 = blockIdx.x * MM_BN;
   const int nk = (d + MM_BK - 1) / MM_BK;
 
   if (warp == 0 && lane == 0) {
@@ -154,7 +245,6 @@ __global__ void __launch_bounds__(MM_NT, 1)
     mbar_wait(tfull, 0);
     asm volatile("tcgen05.fence::after_thread_sync;");
     const int row = m0 + quad * 32 + lane;
-    const int32_t nqr = row < q ? __ldg(nq + row) : 0;
 #pragma unroll 1
     for (int c0 = 0; c0 < MM_BN; c0 += 32) {
       uint32_t v[32];
@@ -169,24 +259,7 @@ __global__ void __launch_bounds__(MM_NT, 1)
             "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
           : "r"(taddr));
       asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-      if (row < q) {
-        const int col0 = n0 + c0;
-        int32_t *drow = D + (size_t)row * ldd + col0;
-        if (col0 + 32 <= n) {
-#pragma unroll
-          for (int j = 0; j < 32; j += 4) {
-            const int4 xn = __ldg(reinterpret_cast<const int4 *>(nx + col0 + j));
-            int4 o;
-            o.x = xn.x + nqr - 2 * (int32_t)v[j + 0];
-            o.y = xn.y + nqr - 2 * (int32_t)v[j + 1];
-            o.z = xn.z + nqr - 2 * (int32_t)v[j + 2];
-            o.w = xn.w + nqr - 2 * (int32_t)v[j + 3];
-            *reinterpret_cast<int4 *>(drow + j) = o;
-          }
-        } else {
-          for (int j = 0; j < 32 && col0 + j < n; ++j) drow[j] = __ldg(nx + col0 + j) + nqr - 2 * (int32_t)v[j];
-        }
-      }
+      epi.store(row, n0 + c0, v);
     }
   }
   __syncwarp();
@@ -253,11 +326,32 @@ cudaError_t launch_exact_mma(const ExactGeom &e, const int32_t *nq, const int32_
   if (err != cudaSuccess) return err;
   err = make_map(&tx, e.X, e.n, e.d, e.pitch, MM_BN);
   if (err != cudaSuccess) return err;
-  err = cudaFuncSetAttribute(k_exact_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MM_SMEM);
+  err = cudaFuncSetAttribute(k_mma_tiles<EpiDistances>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MM_SMEM);
   if (err != cudaSuccess) return err;
+  const EpiDistances epi{nq, nx, e.D, e.npad, e.q, e.n};
   dim3 grid((e.n + MM_BN - 1) / MM_BN, (e.q + MM_BM - 1) / MM_BM);
-  k_exact_mma<<<grid, MM_NT, MM_SMEM, s>>>(tq, tx, nq, nx, e.q, e.n, e.d, e.D, e.npad);
+  k_mma_tiles<EpiDistances><<<grid, MM_NT, MM_SMEM, s>>>(tq, tx, e.d, epi);
   return cudaGetLastError();
 }
+
+// Exact fallbacks of one round on the tensor cores (g.exact_mma): every tile of the
+// (batch query x point) grid that k_filter flagged computes its distances and writes
+// them into S for the pairs whose action byte is ACT_EXACT.
+cudaError_t launch_exact_fallback_mma(const Geom &g, cudaStream_t s) {
+  CUtensorMap tq, tx;
+  cudaError_t err = make_map(&tq, g.Q, g.q, g.d, g.pitch, MM_BM);
+  if (err != cudaSuccess) return err;
+  err = make_map(&tx, g.X, g.n, g.d, g.pitch, MM_BN);
+  if (err != cudaSuccess) return err;
+  err = cudaFuncSetAttribute(k_mma_tiles<EpiFallback>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MM_SMEM);
+  if (err != cudaSuccess) return err;
+  const EpiFallback epi{g};
+  dim3 grid((g.n + MM_BN - 1) / MM_BN, (g.q + MM_BM - 1) / MM_BM);
+  k_mma_tiles<EpiFallback><<<grid, MM_NT, MM_SMEM, s>>>(tq, tx, g.d, epi);
+  return cudaGetLastError();
+}
+
+int exact_tile_rows() { return MM_BM; }
+int exact_tile_cols() { return MM_BN; }
 
 }  // namespace aknn

@@ -93,6 +93,12 @@ struct Geom {
   unsigned adv_bpl;      // advance: Philox blocks per lane before a lane-group reduce
   int force_radix;       // 1: skip the pivot select (aknn_opts.flags bit 0)
   int stage_lo;          // first row-staged advance level (MAX_LEVELS = none)
+  // exact fallbacks on the tensor cores (exact_mma.cu, EpiFallback)
+  int exact_mma;         // 1: k_filter flags tiles, k_mma_tiles<EpiFallback> computes them
+  int xf_cols;           // columns of xflags (point tiles of 256)
+  uint32_t *xflags;      // [ceil(q/128)][xf_cols] tile holds an ACT_EXACT pair this round
+  const int32_t *nx;     // [n] ||x_i||^2
+  int32_t *nq;           // [q] ||x_q||^2 of this batch
 };
 
 // ---- Philox4x32-10 (Salmon et al.), counter (x,y,z,w), key (k0,k1) --------

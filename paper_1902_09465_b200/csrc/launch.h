@@ -60,6 +60,10 @@ cudaError_t launch_exact(const ExactGeom &e, cudaStream_t s);        // D via dp
 cudaError_t launch_exact_topk(const ExactGeom &e, cudaStream_t s);   // top-k of e.D only
 // D via tcgen05 kind::i8 (exact_mma.cu); nq [q], nx [n] squared row norms.
 cudaError_t launch_exact_mma(const ExactGeom &e, const int32_t *nq, const int32_t *nx, cudaStream_t s);
+// Exact fallbacks of a round on the tensor cores (flagged tiles only).
+cudaError_t launch_exact_fallback_mma(const Geom &g, cudaStream_t s);
+int exact_tile_rows();
+int exact_tile_cols();
 cudaError_t launch_row_norms(const uint8_t *A, int64_t pitch, int rows, int32_t *out, cudaStream_t s);
 
 }  // namespace aknn

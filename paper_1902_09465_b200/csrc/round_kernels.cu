@@ -176,6 +176,14 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
     }
     *reinterpret_cast<uint32_t *>(g.act + (size_t)qi * g.npad + i0) = actw;
   }
+  if (g.exact_mma) {
+    // a warp's 128 arms lie in one 256-point tile: flag it for the tensor-core pass
+    bool ex = false;
+#pragma unroll
+    for (int e = 0; e < 4; ++e) ex |= (uint8_t)(actw >> (8 * e)) == ACT_EXACT;
+    if (__any_sync(FULL, ex) && lane_id() == 0)
+      g.xflags[(size_t)(qi >> 7) * g.xf_cols + (i0 >> 8)] = 1u;
+  }
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const uint8_t act = (uint8_t)(actw >> (8 * e));
@@ -278,9 +286,10 @@ __global__ void __launch_bounds__(FIL_NT) k_scatter(Geom g) {
   if (threadIdx.x < NSLOT && scnt[threadIdx.x])
     sbase[threadIdx.x] = g.ctl->off[threadIdx.x] + atomicAdd(&g.ctl->cursor[threadIdx.x], scnt[threadIdx.x]);
   __syncthreads();
+  const unsigned skip_slot = g.exact_mma ? (unsigned)MAX_LEVELS : NONE;  // tensor-core exact pass
 #pragma unroll
   for (int e = 0; e < 4; ++e)
-    if (slot[e] != NONE)
+    if (slot[e] != NONE && slot[e] != skip_slot)
       g.list[sbase[slot[e]] + loc[e]] = ((uint32_t)qi << g.ibits) | (uint32_t)(base_i + e * FIL_NT);
 }
 
@@ -422,7 +431,8 @@ __global__ void __launch_bounds__(ADV_NT) k_advance(Geom g) {
   // row-staged levels [stage_lo, MAX_LEVELS) belong to k_advance_staged
   const int slo = g.stage_lo < MAX_LEVELS ? g.stage_lo : MAX_LEVELS;
   const unsigned long long total_a = coff[slo], skip = coff[MAX_LEVELS] - coff[slo];
-  const unsigned long long total = coff[NSLOT] - skip;
+  // exact fallbacks (the last slot) go to the tensor-core tile pass when g.exact_mma
+  const unsigned long long total = (g.exact_mma ? coff[MAX_LEVELS] : coff[NSLOT]) - skip;
   const unsigned long long nwarps = (unsigned long long)gridDim.x * (ADV_NT / 32);
   const int lane = lane_id();
   const uint32_t imask = (1u << g.ibits) - 1u;
@@ -635,6 +645,11 @@ static inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b
 cudaError_t launch_init(const Geom &g, cudaStream_t s) {
   k_init<<<dim3(cdiv(g.npad, 256), g.q), 256, 0, s>>>(g);
   k_init_qstate<<<cdiv(g.q, 128), 128, 0, s>>>(g);
+  if (g.exact_mma) {
+    cudaError_t e = cudaMemsetAsync(g.xflags, 0, sizeof(uint32_t) * (size_t)cdiv(g.q, 128) * g.xf_cols, s);
+    if (e == cudaSuccess) e = launch_row_norms(g.Q, g.pitch, g.q, g.nq, s);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 
@@ -657,6 +672,10 @@ cudaError_t launch_compact(const Geom &g, cudaStream_t s) {
 }
 
 cudaError_t launch_advance(const Geom &g, int num_sms, cudaStream_t s) {
+  if (g.exact_mma) {
+    const cudaError_t e = launch_exact_fallback_mma(g, s);
+    if (e != cudaSuccess) return e;
+  }
   k_advance<<<num_sms * 8, ADV_NT, 0, s>>>(g);
   if (g.stage_lo < MAX_LEVELS) {
     const size_t smem = (size_t)(ADV_NT / 32) * (size_t)g.pitch;

@@ -264,3 +264,24 @@ def test_sharded_radix_flag_equals_pivot(ak):
         s.close()
     for key in KEYS:
         assert np.array_equal(a[key], b[key]), key
+
+
+@pytest.mark.parametrize("n,d,q,k,h,kind", [(3001, 256, 6, 4, 6, "theory"), (1237, 100, 131, 3, 4, "theory"),
+                                            (777, 33, 7, 5, 5, "exp"), (5, 16, 4, 2, 2, "theory"),
+                                            (2000, 784, 3, 10, 10, "theory")])
+def test_exact_fallback_tensor_cores_equals_rows(ak, n, d, q, k, h, kind):
+    """Exact fallbacks computed by the tcgen05 tile pass (default) and by per-pair
+    row streams (AKNN_FLAG_EXACT_ROWS) give identical bytes; both equal the oracle.  q = 131
+    spans two 128-query tiles; n = 1237 and 3001 leave ragged point tiles."""
+    X, Q = synth.small_instance(n + d, n, d, q=q)
+    al = orc.alpha_theory(n, 0.05, d) if kind == "theory" else orc.alpha_experimental(n, 0.05, d, 0.05)
+    ix = ak.Index(X)
+    a = ix.query(Q, k, h, 0.05, 21, al, counts=True, sums=True)
+    sa = ix.stats()
+    b = ix.query(Q, k, h, 0.05, 21, al, counts=True, sums=True, flags=ak.FLAG_EXACT_ROWS)
+    ix.close()
+    for key in KEYS:
+        assert np.array_equal(a[key], b[key]), key
+    if n > 100:
+        assert sa["exact_fallbacks"] > 0  # the tile pass was exercised
+    _assert_parity(a, orc.query_br(X, Q, k, h, 21, al, want_sums=True))
