@@ -561,6 +561,7 @@ def run_ours(args, dist: Dist):
             "config": _config_desc(cfg, args),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": gpu_launches, "gpu_launches_per_step": gpu_launches / args.steps,
+            "step_ms": [round(t, 3) for t in times],
             **extra,
         }
         print(json.dumps(line), flush=True)

@@ -77,13 +77,18 @@ typedef struct {
   int32_t flags;      /* bit 0 (AKNN_FLAG_RADIX_SELECT): decide every rank split
                          with the multi-pass radix select instead of the one-pass
                          pivot select (diagnostics; results are identical);
-                         bit 1 (AKNN_FLAG_EXACT_ROWS): see below                  */
+                         bits 1, 2 (AKNN_FLAG_EXACT_ROWS, AKNN_FLAG_NO_TILES): see
+                         below                                                   */
 } aknn_opts;
 
 #define AKNN_FLAG_RADIX_SELECT 1
 /* bit 1: compute the exact fallbacks by streaming each pair's row on the
    CUDA cores instead of the tensor-core tile pass (diagnostics; identical results) */
 #define AKNN_FLAG_EXACT_ROWS 2
+/* bit 2: advance every pair through the work lists (global-memory gathers) instead
+   of staging dense (query x point) tiles in shared memory (diagnostics; identical
+   results)                                                                   */
+#define AKNN_FLAG_NO_TILES 4
 
 /* Execution statistics of the last query call on an index (aknn_get_stats).
  * Kernel classes: init (a2), select (a6-a7: rank split, bounds, Eq. 5),
@@ -170,9 +175,13 @@ aknn_status aknn_query_ex(const aknn_index *ix, const uint8_t *queries, int32_t 
 
 /* Device-pointer variant: queries_dev uint8 [q][d], alpha_dev fp64 [d+1]
  * (NULL = footnote-2 table), outputs in `out` are device pointers.  All work
- * is enqueued on `cuda_stream`.  The round loop needs one 4-byte device->host
- * read of the active-query count per round, so the call returns after the
- * loop has finished on the device; outputs are complete when the stream is.  */
+ * is enqueued on `cuda_stream`.  With timing = 0 the round loop runs on the
+ * device (one CUDA graph per query sub-batch, a conditional WHILE node decides
+ * the rounds); with max_rounds = 0 as well the call returns WITHOUT waiting for
+ * the device (the status cannot be EMAXROUNDS) and the statistics of the call
+ * are completed by aknn_get_stats or by the next call on this index.  Otherwise
+ * it returns after the loop has finished.  Outputs are complete when the
+ * stream is.  Calls on one index must be ordered (one stream, or synchronised). */
 aknn_status aknn_query_async(const aknn_index *ix, const uint8_t *queries_dev, int32_t q,
                              int32_t k, int32_t h, double delta, uint64_t seed,
                              const double *alpha_dev, const aknn_opts *opts,

@@ -1,0 +1,273 @@
+// advance_tiles.cu -- level gathers (row a3) of DENSE tiles from shared memory.
+//
+// The batch's (query x point) grid is cut into tiles of R = 2^tile_lr queries x
+// P = 2^tile_lp points.  k_filter adds, per tile, the draws its blockers take this
+// round (tilework); a tile whose draws reach tile_min is advanced here instead of
+// through the work lists (k_scatter leaves its pairs out): the CTA copies the R
+// query rows and P point rows into shared memory once with 16-byte loads, then every
+// draw of every listed pair of the tile gathers its two bytes from there.
+//
+// Why: a draw gathered from global memory costs one random 32-byte sector (L2, or HBM
+// when X does not fit L2) and two L1 wavefronts; in a dense tile the R + P rows are
+// read once for R * P pairs, so the sector traffic per pair and level drops from
+// ~min(s, d/32) sectors to (R + P) * d / (R * P) bytes and the gathers become
+// shared-memory loads.  What remains is the Philox4x32-10 integer work (the ALU bound
+// of DESIGN.md §7).  Under the footnote-2 radius every arm of a query walks every
+// level in lockstep, so nearly every tile is dense at every level.
+//
+// Inside a tile the active pairs are grouped by level c (smem compaction); each
+// pair's draws are summed by one thread or one group of consecutive lanes (shuffle
+// reduce), ADV_TP independent Philox blocks in flight per thread.  Integer sums: the
+// result does not depend on the order, so S matches the list path and the oracle bit
+// for bit.
+#include "internal.cuh"
+#include "launch.h"
+#include "select.cuh"
+
+namespace aknn {
+
+constexpr int TILE_NT = 256;
+constexpr int ADV_TP = 4;  // items (Philox blocks) in flight per thread
+
+// Row slots are 2^slot_l bytes (>= pitch) and start at multiples of 2^slot_l, so
+// the shared-memory address of coordinate j of a row is (row base | j): one LOP3 on
+// the ALU pipe.  With a plain add, ptxas folds the row base into the multiply-high of
+// the coordinate map (IMAD.HI with a 64-bit addend, plus IMAD.MOVs to build it) and
+// repeats that multiply for the query row -- all on the fma-heavy pipe, the one the
+// Philox rounds saturate (ncu: fmaheavy 84 % at 256 draws per pair).
+__device__ __forceinline__ uint32_t lds_u8(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ uint32_t sq_diff(uint32_t xa, uint32_t qa, uint32_t j) {
+  const int diff = (int)lds_u8(xa | j) - (int)lds_u8(qa | j);
+  return (uint32_t)(diff * diff);
+}
+
+// Four draws of one Philox block: the bytes are packed four to a word (PRMT, ALU)
+// and summed with one VABSDIFF4 + one IDP.4A, instead of four subtractions and four
+// multiply-adds on the fma-heavy pipe.  Exact: |x - q|^2 summed in uint32.
+__device__ __forceinline__ uint32_t sq_diff4(uint32_t xa, uint32_t qa, uint4 w, uint32_t d, uint32_t acc) {
+  const uint32_t j0 = coord_of(w.x, d), j1 = coord_of(w.y, d), j2 = coord_of(w.z, d), j3 = coord_of(w.w, d);
+  const uint32_t x01 = __byte_perm(lds_u8(xa | j0), lds_u8(xa | j1), 0x1140);
+  const uint32_t x23 = __byte_perm(lds_u8(xa | j2), lds_u8(xa | j3), 0x4011);
+  const uint32_t q01 = __byte_perm(lds_u8(qa | j0), lds_u8(qa | j1), 0x1140);
+  const uint32_t q23 = __byte_perm(lds_u8(qa | j2), lds_u8(qa | j3), 0x4011);
+  const uint32_t t = __vabsdiffu4(__byte_perm(x01, x23, 0x7610), __byte_perm(q01, q23, 0x7610));
+  return __dp4a(t, t, acc);
+}
+
+__global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
+  extern __shared__ __align__(16) unsigned char tsm[];
+  __shared__ unsigned lcnt[MAX_LEVELS], loff[MAX_LEVELS + 1], lfill[MAX_LEVELS];
+  __shared__ int sdone[256];
+  const int R = 1 << g.tile_lr, P = 1 << g.tile_lp, RP = R * P;
+  const int pitch = (int)g.pitch, nv = pitch >> 4;
+  const int sl = g.tile_slot_l;
+  const uint32_t slot = 1u << sl;
+  // rows: [R query rows][P point rows], slot-aligned; then acc [RP] int32, lst [RP] u16
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(tsm);
+  const uint32_t rows_s = (base + slot - 1) & ~(slot - 1);
+  unsigned char *rows_g = tsm + (rows_s - base);
+  int32_t *acc = reinterpret_cast<int32_t *>(rows_g + (size_t)(R + P) * slot);
+  uint16_t *lst = reinterpret_cast<uint16_t *>(acc + RP);
+  uint8_t *sact = reinterpret_cast<uint8_t *>(lst + RP);  // [RP] action bytes of the tile
+  const uint32_t xs = rows_s + ((uint32_t)R << sl);  // first point row
+  const int tid = threadIdx.x;
+  const int rows = (g.q + R - 1) >> g.tile_lr;
+  const uint32_t d = (uint32_t)g.d;
+  const unsigned ntiles = g.ctl->n_tiles;
+
+  for (unsigned ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
+    const uint32_t t = g.tilelist[ti];
+    const int tp = (int)(t / (unsigned)rows), tr = (int)(t % (unsigned)rows);
+    const int r0 = tr << g.tile_lr, p0 = tp << g.tile_lp;
+    __syncthreads();  // the previous tile's shared memory is no longer in use
+    if (tid < MAX_LEVELS) lcnt[tid] = 0;
+    for (int r = tid; r < R; r += TILE_NT) sdone[r] = (r0 + r >= g.q) ? 1 : g.qs[r0 + r].done;
+
+    // stage the rows: asynchronous 16-byte copies (cp.async), all in flight at once;
+    // rows past q / n are never referenced and are left as they are
+    for (int v = tid; v < (R + P) * nv; v += TILE_NT) {
+      const int row = v / nv, c = v - row * nv;
+      const uint8_t *src = nullptr;
+      if (row < R) {
+        if (r0 + row < g.q) src = g.Q + (size_t)(r0 + row) * pitch + 16 * c;
+      } else if (p0 + row - R < g.n) {
+        src = g.X + (size_t)(p0 + row - R) * pitch + 16 * c;
+      }
+      if (src)
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(rows_s + ((uint32_t)row << sl) + 16u * c),
+                     "l"(src)
+                     : "memory");
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+    __syncthreads();  // sdone, lcnt
+    // action bytes of the tile -> per-level counts (pairs of finished queries: none)
+    for (int e = tid; e < RP; e += TILE_NT) {
+      const int r = e >> g.tile_lp, p = e & (P - 1);
+      uint8_t a = 0;
+      if (!sdone[r] && p0 + p < g.n) a = g.act[(size_t)(r0 + r) * g.npad + p0 + p];
+      if (a > MAX_LEVELS) a = 0;  // exact fallbacks are the tensor-core pass's
+      sact[e] = a;
+      if (a) atomicAdd(&lcnt[a - 1], 1u);
+    }
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    __syncthreads();
+    if (tid == 0) {
+      unsigned o = 0;
+      for (int c = 0; c < MAX_LEVELS; ++c) {
+        loff[c] = o;
+        lfill[c] = o;
+        o += lcnt[c];
+      }
+      loff[MAX_LEVELS] = o;
+    }
+    __syncthreads();
+    for (int e = tid; e < RP; e += TILE_NT) {
+      const uint8_t a = sact[e];
+      if (a) lst[atomicAdd(&lfill[a - 1], 1u)] = (uint16_t)e;
+    }
+    __syncthreads();
+
+    // the draws, level by level.  nb <= ADV_TP blocks per pair: a thread owns
+    // ADV_TP / nb whole pairs per pass.  nb > ADV_TP: tpp lanes per pair (consecutive
+    // lanes), each running ADV_TP independent Philox blocks at a time, then a shuffle
+    // reduce inside the lane group; every pair's sum is written by one thread.
+    for (int c = 0; c < MAX_LEVELS; ++c) {
+      const unsigned m = lcnt[c];
+      if (m == 0) continue;
+      const int lb = c < 2 ? 0 : c - 2;  // log2 Philox blocks per pair
+      const unsigned s = 1u << c, nb = 1u << lb;
+      const uint16_t *L = lst + loff[c];
+      const uint32_t lv = (uint32_t)(c + 1);
+      if (nb <= (unsigned)ADV_TP) {
+        const unsigned ppt = ADV_TP / nb;
+        for (unsigned l0 = tid; l0 < m; l0 += TILE_NT * ppt) {
+          uint4 w[ADV_TP];
+          int pr[ADV_TP];
+#pragma unroll
+          for (int k = 0; k < ADV_TP; ++k) {
+            const unsigned li = l0 + (k / nb) * TILE_NT;
+            const bool ok = (unsigned)k / nb < ppt && li < m;
+            pr[k] = ok ? (int)L[li] : -1;
+            const int e = ok ? pr[k] : 0;
+            const uint32_t gi = (uint32_t)(p0 + (e & (P - 1))) + g.id_offset;
+            const uint32_t gq = (uint32_t)(r0 + (e >> g.tile_lp)) + g.qi0;
+            w[k] = philox4x32_10_rk(make_uint4((uint32_t)k & (nb - 1), gi, gq, lv), g.rk0, g.rk1);
+          }
+          uint32_t sum = 0;
+#pragma unroll
+          for (int k = 0; k < ADV_TP; ++k) {
+            if (pr[k] >= 0) {
+              const uint32_t xa = xs + ((uint32_t)(pr[k] & (P - 1)) << sl);
+              const uint32_t qa = rows_s + ((uint32_t)(pr[k] >> g.tile_lp) << sl);
+              if (s >= 4) {
+                sum = sq_diff4(xa, qa, w[k], d, sum);
+              } else {  // levels 0 and 1 use 1 and 2 words of the block
+                sum += sq_diff(xa, qa, coord_of(w[k].x, d));
+                if (s == 2) sum += sq_diff(xa, qa, coord_of(w[k].y, d));
+              }
+            }
+            if ((unsigned)(k + 1) % nb == 0) {  // last block of this pair
+              if (pr[k] >= 0) acc[pr[k]] = (int32_t)sum;
+              sum = 0;
+            }
+          }
+        }
+      } else {
+        unsigned tpp = nb / 16u;  // >= 4 passes of ADV_TP blocks per lane
+        tpp = tpp < 1u ? 1u : (tpp > 32u ? 32u : tpp);
+        const unsigned sub = tid & (tpp - 1), slots = TILE_NT / tpp;
+        // all lanes of a warp run the same number of passes (uniform shuffles)
+        for (unsigned l0 = 0; l0 < m; l0 += slots) {
+          const unsigned li = l0 + tid / tpp;
+          const bool ok = li < m;
+          const int pe = ok ? (int)L[li] : 0;
+          const uint32_t xa = xs + ((uint32_t)(pe & (P - 1)) << sl);
+          const uint32_t qa = rows_s + ((uint32_t)(pe >> g.tile_lp) << sl);
+          const uint32_t gi = (uint32_t)(p0 + (pe & (P - 1))) + g.id_offset;
+          const uint32_t gq = (uint32_t)(r0 + (pe >> g.tile_lp)) + g.qi0;
+          uint32_t sum = 0;
+          if (ok) {
+            for (unsigned b0 = sub * ADV_TP; b0 < nb; b0 += tpp * ADV_TP) {
+              uint4 w[ADV_TP];
+#pragma unroll
+              for (int k = 0; k < ADV_TP; ++k)
+                w[k] = philox4x32_10_rk(make_uint4(b0 + k, gi, gq, lv), g.rk0, g.rk1);
+#pragma unroll
+              for (int k = 0; k < ADV_TP; ++k) sum = sq_diff4(xa, qa, w[k], d, sum);
+            }
+          }
+          for (unsigned o = tpp >> 1; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
+          if (ok && sub == 0) acc[pe] = (int32_t)sum;
+        }
+      }
+    }
+    __syncthreads();
+    // commit: S += the level's sum, T -> 2T
+    for (int e = tid; e < RP; e += TILE_NT) {
+      const uint8_t a = sact[e];
+      if (a) {
+        const size_t o = (size_t)(r0 + (e >> g.tile_lp)) * g.npad + p0 + (e & (P - 1));
+        g.S[o] += acc[e];
+        g.lvl[o] = a;
+      }
+    }
+  }
+}
+
+// The dense tiles of this round (tilework >= tile_min) in point-major numbering
+// t = tp * rows + tr; every counter is reset for the next round.  Runs after k_scatter.
+__global__ void k_tile_list(Geom g) {
+  const int rows = (g.q + (1 << g.tile_lr) - 1) >> g.tile_lr;
+  const int cols = (g.n + (1 << g.tile_lp) - 1) >> g.tile_lp;
+  const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
+  bool dense = false;
+  if (t < (unsigned)rows * (unsigned)cols) {
+    const int tp = (int)(t / (unsigned)rows), tr = (int)(t % (unsigned)rows);
+    uint32_t *w = g.tilework + (size_t)tr * g.tile_cols + tp;
+    dense = *w >= g.tile_min;
+    *w = 0u;
+  }
+  const unsigned m = __ballot_sync(FULL, dense);
+  unsigned b = 0;
+  if (lane_id() == 0 && m) b = atomicAdd(&g.ctl->n_tiles, (unsigned)__popc(m));
+  b = __shfl_sync(FULL, b, 0);
+  if (dense) g.tilelist[b + __popc(m & ((1u << lane_id()) - 1u))] = t;
+}
+
+cudaError_t launch_tile_list(const Geom &g, cudaStream_t s) {
+  const long long rows = (g.q + (1ll << g.tile_lr) - 1) >> g.tile_lr;
+  const long long cols = (g.n + (1ll << g.tile_lp) - 1) >> g.tile_lp;
+  const long long nt = rows * cols;
+  if (nt > 0) k_tile_list<<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(g);
+  return cudaGetLastError();
+}
+
+int tile_slot_log2(int64_t pitch) {
+  int l = 4;
+  while ((1ll << l) < pitch) ++l;
+  return l;
+}
+
+size_t tile_smem_bytes(int lr, int lp, int64_t pitch) {
+  const size_t R = (size_t)1 << lr, P = (size_t)1 << lp, slot = (size_t)1 << tile_slot_log2(pitch);
+  return (R + P + 1) * slot + R * P * (4 + 2 + 1);  // + one slot of alignment slack
+}
+
+cudaError_t launch_advance_tiles(const Geom &g, int num_sms, cudaStream_t s) {
+  const size_t smem = tile_smem_bytes(g.tile_lr, g.tile_lp, g.pitch);
+  cudaError_t e = cudaFuncSetAttribute(k_advance_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_advance_tiles, TILE_NT, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  k_advance_tiles<<<num_sms * per_sm, TILE_NT, smem, s>>>(g);
+  return cudaGetLastError();
+}
+
+}  // namespace aknn

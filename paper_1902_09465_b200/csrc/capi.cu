@@ -162,6 +162,17 @@ struct aknn_index {
   ncclComm_t comm = nullptr;
 #endif
   aknn_stats stats{};
+  // statistics of an aknn_query_async call whose control blocks are still being
+  // copied to `host` (graph loop, no round cap): finished on the next call on this
+  // index or by aknn_get_stats, so the call itself never waits for the device
+  struct Pending {
+    bool on = false;
+    cudaEvent_t ev = nullptr;
+    std::vector<int> qn;  // queries per sub-batch
+    size_t slot = 0;      // bytes per sub-batch in `host`
+  } pending;
+  Geom pending_geom{};
+  int pending_outputs_per_batch = 0;
 };
 
 namespace {
@@ -233,6 +244,66 @@ aknn_status setup_exact_mma(aknn_index *ix, Geom &g, int64_t qb, uint8_t *ws, co
   g.xflags = reinterpret_cast<uint32_t *>(ws + round_up((size_t)qb * 4, 256));
   g.xf_cols = (int)((g.npad + exact_tile_cols() - 1) / exact_tile_cols());
   return AKNN_OK;
+}
+
+// Tile-staged level gathers (advance_tiles.cu) unless AKNN_FLAG_NO_TILES / AKNN_TILE=0.
+// Tile shape: the largest R = P (powers of two, <= 32) whose rows fit a third of the
+// SM's shared memory (3 CTAs per SM), else half, else all of it.  AKNN_TILE_LR /
+// AKNN_TILE_LP override (experiments).  A tile is dense when its draws, at one 32-byte
+// sector each on the list path, cost at least AKNN_TILE_F (default 1) times its
+// staging bytes (R + P) * pitch.
+struct TileShape {
+  int on, lr, lp;
+  uint32_t min_draws;
+};
+
+int env_int(const char *name, int dflt) {
+  const char *e = getenv(name);
+  return e && e[0] ? atoi(e) : dflt;
+}
+
+TileShape tile_shape(int64_t pitch) {
+  TileShape t{0, 0, 0, 0};
+  if (env_int("AKNN_TILE", 1) == 0) return t;
+  int lr = -1;
+  for (size_t cap : {(size_t)75 * 1024, (size_t)112 * 1024, (size_t)220 * 1024}) {
+    for (int l = 5; l >= 2; --l)
+      if (tile_smem_bytes(l, l, pitch) <= cap) {
+        lr = l;
+        break;
+      }
+    if (lr >= 0) break;
+  }
+  if (lr < 0) return t;
+  t.lr = env_int("AKNN_TILE_LR", lr);
+  t.lp = env_int("AKNN_TILE_LP", lr);
+  if (t.lr < 0 || t.lr > 8 || t.lp < 2 || t.lp > 8 || t.lr + t.lp > 16 ||
+      tile_smem_bytes(t.lr, t.lp, pitch) > (size_t)220 * 1024)
+    return TileShape{0, 0, 0, 0};
+  const char *fe = getenv("AKNN_TILE_F");
+  const double f = fe && fe[0] ? atof(fe) : 1.0;
+  const double bytes = (double)(((int64_t)1 << t.lr) + ((int64_t)1 << t.lp)) * (double)pitch;
+  t.min_draws = (uint32_t)std::max(1.0, std::ceil(f * bytes / 32.0));
+  t.on = 1;
+  return t;
+}
+
+size_t tile_ws_bytes(int64_t qb, int64_t npad, const TileShape &t) {
+  if (!t.on) return 0;
+  const int64_t rows = (qb + (1ll << t.lr) - 1) >> t.lr, cols = (npad + (1ll << t.lp) - 1) >> t.lp;
+  return 2 * round_up((size_t)(rows * cols) * 4, 256);  // tilework + tilelist
+}
+
+void setup_tiles(Geom &g, const TileShape &t, int64_t qb, uint8_t *ws, const aknn_opts &o) {
+  g.tile_on = (t.on && !(o.flags & AKNN_FLAG_NO_TILES)) ? 1 : 0;
+  if (!g.tile_on) return;
+  g.tile_lr = t.lr;
+  g.tile_lp = t.lp;
+  g.tile_cols = (int)((g.npad + (1ll << t.lp) - 1) >> t.lp);
+  g.tilework = reinterpret_cast<uint32_t *>(ws);
+  g.tilelist = reinterpret_cast<uint32_t *>(ws + tile_ws_bytes(qb, g.npad, t) / 2);
+  g.tile_min = t.min_draws;
+  g.tile_slot_l = tile_slot_log2(g.pitch);
 }
 
 // Builds the level geometry of the composite key (R9).
@@ -425,11 +496,71 @@ aknn_status loop_graph(aknn_index *ix, const Geom &g, int nbits, int max_rounds,
   return AKNN_OK;
 }
 
+// Kernel launches per class (for aknn_stats; memset nodes excluded).
+int launches_init_of(const Geom &g) { return 2 + (g.exact_mma ? 1 : 0); }  // init, qstate, norms
+int launches_compact_of(const Geom &g) { return 2 + (g.tile_on ? 2 : 0); }  // plan, scatter (+ lists)
+int launches_advance_of(const Geom &g) {
+  return 1 + (g.tile_on ? 1 : 0) + (g.exact_mma ? 1 : 0) + (g.stage_lo < MAX_LEVELS ? 1 : 0);
+}
+
+// Folds one sub-batch's control block and query states (copied to the host) into
+// the statistics; graph = the device-driven loop counted the rounds itself.
+void fold_batch_stats(aknn_stats &stats, const RoundCtl &ctl_h, const QState *qs, int qn, bool graph,
+                      const Geom &g, int r, aknn_status *status) {
+  if (graph) {
+    r = (int)ctl_h.round;
+    stats.query_rounds += (int64_t)ctl_h.qrounds;
+    stats.blocked_query_rounds += (int64_t)ctl_h.brounds;
+    stats.launches_init += 1 + launches_init_of(g);  // + loop reset
+    stats.launches_select += 3 * r;                  // pivot, radix fallback, round control
+    stats.launches_filter += r - 1;
+    stats.launches_compact += launches_compact_of(g) * (r - 1);
+    stats.launches_advance += (launches_advance_of(g) + 1) * (r - 1);  // + counter reset
+    if (ctl_h.n_active > 0 && status) *status = AKNN_EMAXROUNDS;
+  }
+  if (r > stats.rounds) stats.rounds = r;
+  stats.active_pair_rounds += (int64_t)ctl_h.advanced;
+  for (int a = 0; a < qn; ++a) {
+    stats.draws += qs[a].draws;
+    stats.exact_fallbacks += qs[a].nexact;
+    stats.philox_blocks += qs[a].blocks;
+  }
+}
+
+void total_launches(aknn_stats &stats) {
+  stats.kernel_launches = stats.launches_init + stats.launches_select + stats.launches_filter +
+                          stats.launches_compact + stats.launches_advance + stats.launches_output;
+}
+
+// Completes the statistics of a deferred aknn_query_async call (waits for its copies).
+aknn_status finish_pending(aknn_index *ix) {
+  if (!ix->pending.on) return AKNN_OK;
+  ix->pending.on = false;
+  for (;;) {
+    const cudaError_t e = cudaEventQuery(ix->pending.ev);
+    if (e == cudaSuccess) break;
+    if (e != cudaErrorNotReady) return fail(AKNN_ECUDA, "waiting for the query: %s", cudaGetErrorString(e));
+  }
+  aknn_stats &stats = ix->stats;
+  const Geom &g = ix->pending_geom;
+  for (size_t b = 0; b < ix->pending.qn.size(); ++b) {
+    const char *base = static_cast<const char *>(ix->host.p) + 256 + b * ix->pending.slot;
+    const RoundCtl &ctl_h = *reinterpret_cast<const RoundCtl *>(base);
+    const QState *qs = reinterpret_cast<const QState *>(base + sizeof(RoundCtl));
+    fold_batch_stats(stats, ctl_h, qs, ix->pending.qn[b], true, g, 0, nullptr);
+    stats.launches_output += ix->pending_outputs_per_batch;
+  }
+  total_launches(stats);
+  return AKNN_OK;
+}
+
 // Runs the whole query on device pointers.  Q rows have stride `qstride`
 // bytes in `queries_dev` (device).  Outputs are device pointers.
 aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstride, int32_t q,
                       int32_t k, int32_t h, uint64_t seed, const double *alpha_dev,
-                      const aknn_opts *opts, const aknn_result *out, cudaStream_t st) {
+                      const aknn_opts *opts, const aknn_result *out, cudaStream_t st,
+                      bool may_defer = false) {
+  TRY(finish_pending(ix));
   const int64_t n = ix->n_local;
   const int32_t d = ix->d;
   KeyGeom kg;
@@ -443,11 +574,15 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   int64_t qb = q;
   const int64_t code_cap = 1ll << (32 - kg.ibits);
   if (qb > code_cap) qb = code_cap;
-  size_t free_b = 0, total_b = 0;
-  CU(cudaMemGetInfo(&free_b, &total_b));
   const size_t per_q = (size_t)npad * 10 + ix->pitch + sizeof(QState) + 64;
-  const size_t budget = (size_t)(0.6 * (double)(free_b + ix->ws.bytes));
-  if ((size_t)qb * per_q > budget) qb = (int64_t)(budget / per_q);
+  if ((size_t)qb * per_q > ix->ws.bytes) {
+    // only when the workspace must grow: cudaMemGetInfo is a driver round trip that
+    // sometimes stalls the enqueueing thread for tens of ms
+    size_t free_b = 0, total_b = 0;
+    CU(cudaMemGetInfo(&free_b, &total_b));
+    const size_t budget = (size_t)(0.6 * (double)(free_b + ix->ws.bytes));
+    if ((size_t)qb * per_q > budget) qb = (int64_t)(budget / per_q);
+  }
   if (qb < 1) return fail(AKNN_ENOMEM, "not enough device memory for one query row");
   // workspace layout
   const size_t szS = (size_t)qb * npad * 4, szL = (size_t)qb * npad, szA = szL,
@@ -462,6 +597,8 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   const size_t oQS = off; off = round_up(off + szQS, 256);
   const size_t oCtl = off; off = round_up(off + szCtl, 256);
   const size_t oXm = off; off = round_up(off + exact_mma_ws_bytes(qb, npad), 256);
+  const TileShape tsh = tile_shape(ix->pitch);
+  const size_t oTw = off; off = round_up(off + tile_ws_bytes(qb, npad, tsh), 256);
   TRY(ix->ws.ensure(off));
 
   Geom g{};
@@ -497,6 +634,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   g.force_radix = (o.flags & AKNN_FLAG_RADIX_SELECT) ? 1 : 0;
   g.stage_lo = stage_level(g.pitch);
   TRY(setup_exact_mma(ix, g, qb, ix->ws.as<uint8_t>(oXm), o, st));
+  setup_tiles(g, tsh, qb, ix->ws.as<uint8_t>(oTw), o);
 
   aknn_stats stats{};
   stats.pairs = (int64_t)q * n;
@@ -507,14 +645,24 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   PhaseTimer tm(o.timing != 0, st, &ix->events);
   tm.start();
   cudaEvent_t all_a = tm.open_a;
-  CU(ix->host.ensure(256 + sizeof(RoundCtl) + sizeof(QState) * (size_t)qb));
+  // pinned host staging: [256 B: active count][per sub-batch: RoundCtl | QState[qb]]
+  const int64_t nbatch = (q + qb - 1) / qb;
+  const size_t slot = round_up(sizeof(RoundCtl) + sizeof(QState) * (size_t)qb, 64);
+  CU(ix->host.ensure(256 + (size_t)nbatch * slot));
   unsigned int *h_active = static_cast<unsigned int *>(ix->host.p);
-  RoundCtl *h_ctl = reinterpret_cast<RoundCtl *>(static_cast<char *>(ix->host.p) + 256);
-  QState *h_qs = reinterpret_cast<QState *>(h_ctl + 1);
+  // defer the statistics (no host wait at all) on the async graph path without a
+  // round cap: the status cannot be EMAXROUNDS there
+  const bool defer = may_defer && use_graph && o.max_rounds <= 0;
+  const int outs_per_batch = (out->counts || out->sums) ? 2 : 1;
+  std::vector<int> batch_qn;
   tm.open_a = nullptr;
   aknn_status status = AKNN_OK;
   for (int64_t r0 = 0; r0 < q; r0 += qb) {
     const int qn = (int)std::min<int64_t>(qb, q - r0);
+    const int64_t b = r0 / qb;
+    RoundCtl *h_ctl = reinterpret_cast<RoundCtl *>(static_cast<char *>(ix->host.p) + 256 + (size_t)b * slot);
+    QState *h_qs = reinterpret_cast<QState *>(h_ctl + 1);
+    batch_qn.push_back(qn);
     g.q = qn;
     g.qi0 = (uint32_t)(o.qi_offset + r0);
     ++stats.query_batches;
@@ -535,7 +683,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
     tm.start();
     CU(launch_init(g, st));
     tm.stop(PH_INIT);
-    stats.launches_init += 2;
+    stats.launches_init += launches_init_of(g);
     unsigned evaluated = (unsigned)qn;  // queries the rank split looks at this round
     for (;;) {
       ++r;
@@ -563,11 +711,11 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
       tm.start();
       CU(launch_compact(g, st));
       tm.stop(PH_COMPACT);
-      stats.launches_compact += 2;
+      stats.launches_compact += launches_compact_of(g);
       tm.start();
       CU(launch_advance(g, ix->num_sms, st));
       tm.stop(PH_ADVANCE);
-      ++stats.launches_advance;
+      stats.launches_advance += launches_advance_of(g);
       if (r > 1 + 64 * 64) return fail(AKNN_ECUDA, "round loop did not terminate (internal error)");
     }
     }  // host-driven loop
@@ -575,34 +723,28 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
     tm.start();
     CU(launch_output(g, op, st));
     tm.stop(PH_OUTPUT);
-    stats.launches_output += (out->counts || out->sums) ? 2 : 1;
     CU(cudaMemcpyAsync(h_ctl, g.ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(h_qs, g.qs, sizeof(QState) * qn, cudaMemcpyDeviceToHost, st));
+    if (defer) continue;  // folded in by finish_pending
+    stats.launches_output += outs_per_batch;
     CU(sync_spin(st));
-    const RoundCtl &ctl_h = *h_ctl;
-    const QState *qs = h_qs;
-    if (use_graph) {
-      r = (int)ctl_h.round;
-      stats.query_rounds += (int64_t)ctl_h.qrounds;
-      stats.blocked_query_rounds += (int64_t)ctl_h.brounds;
-      stats.launches_init += 3;
-      stats.launches_select += 3 * r;  // pivot select + radix fallback + round control
-      stats.launches_filter += r - 1;
-      stats.launches_compact += 2 * (r - 1);
-      stats.launches_advance += 2 * (r - 1);  // advance + counter reset
-      if (ctl_h.n_active > 0) status = AKNN_EMAXROUNDS;
-    }
-    if (r > stats.rounds) stats.rounds = r;
-    stats.active_pair_rounds += (int64_t)ctl_h.advanced;
-    for (int a = 0; a < qn; ++a) {
-      stats.draws += qs[a].draws;
-      stats.exact_fallbacks += qs[a].nexact;
-      stats.philox_blocks += qs[a].blocks;
-    }
+    fold_batch_stats(stats, *h_ctl, h_qs, qn, use_graph, g, r, &status);
     if (status != AKNN_OK) break;
   }
   tm.open_a = all_a;
   tm.stop(PH_ALL);
+  if (defer) {
+    if (!ix->pending.ev) CU(cudaEventCreateWithFlags(&ix->pending.ev, cudaEventDisableTiming));
+    CU(cudaEventRecord(ix->pending.ev, st));
+    ix->pending.on = true;
+    ix->pending.qn = batch_qn;
+    ix->pending.slot = slot;
+    ix->pending_geom = g;
+    ix->pending_outputs_per_batch = outs_per_batch;
+    ix->stats = stats;  // completed by finish_pending
+    CU(cudaGetLastError());
+    return AKNN_OK;
+  }
   CU(sync_spin(st));
   double ms[PH_N];
   tm.resolve(ms);
@@ -613,8 +755,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   stats.ms_advance = ms[PH_ADVANCE];
   stats.ms_output = ms[PH_OUTPUT];
   stats.ms_total = ms[PH_ALL];
-  stats.kernel_launches = stats.launches_init + stats.launches_select + stats.launches_filter +
-                          stats.launches_compact + stats.launches_advance + stats.launches_output;
+  total_launches(stats);
   ix->stats = stats;
   CU(cudaGetLastError());
   return status;
@@ -633,6 +774,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
                               uint64_t seed, const double *alpha_dev, const aknn_opts *opts,
                               const aknn_result *out, int64_t out_ncols, cudaStream_t st) {
   aknn_index *ix0 = shards[0];
+  for (aknn_index *sh : shards) TRY(finish_pending(sh));
   const int32_t d = ix0->d;
   const int W = nccl ? ix0->world : (int)shards.size();
   const int kh = k + h;
@@ -691,6 +833,8 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     const size_t oSend = off; off = round_up(off + szSend, 256);
     const size_t oRecv = off; off = round_up(off + szRecv, 256);
     const size_t oXm = off; off = round_up(off + exact_mma_ws_bytes(qb, npad), 256);
+    const TileShape tsh = tile_shape(ix->pitch);
+    const size_t oTw = off; off = round_up(off + tile_ws_bytes(qb, npad, tsh), 256);
     TRY(ix->ws.ensure(off));
     Geom &g = G[si];
     g = Geom{};
@@ -727,6 +871,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     g.world = W;
     g.recv_stride = recv_stride;
     TRY(setup_exact_mma(ix, g, qb, ix->ws.as<uint8_t>(oXm), o, st));
+    setup_tiles(g, tsh, qb, ix->ws.as<uint8_t>(oTw), o);
     if (has_recv) g.recv = ix->ws.as<ShardRec>(oRecv);
     if (si == 0 && !nccl) recv_shared = ix->ws.as<ShardRec>(oRecv);
     if (nccl) g.send = ix->ws.as<ShardRec>(oSend);
@@ -764,7 +909,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
                            qn, cudaMemcpyDeviceToDevice, st));
       CU(cudaMemsetAsync(g.ctl, 0, sizeof(RoundCtl), st));
       CU(launch_init(g, st));
-      stats.launches_init += 2;
+      stats.launches_init += launches_init_of(g);
     }
     tm.stop(PH_INIT);
     if (!nccl && nS > 1) {  // shards add their counters into the output rows
@@ -813,11 +958,11 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
       tm.start();
       for (size_t si = 0; si < nS; ++si) CU(launch_compact(G[si], st));
       tm.stop(PH_COMPACT);
-      stats.launches_compact += 2 * nS;
+      stats.launches_compact += launches_compact_of(G[0]) * (int)nS;
       tm.start();
       for (size_t si = 0; si < nS; ++si) CU(launch_advance(G[si], shards[si]->num_sms, st));
       tm.stop(PH_ADVANCE);
-      stats.launches_advance += nS;
+      stats.launches_advance += launches_advance_of(G[0]) * (int)nS;
       if (r > 1 + 64 * 64) return fail(AKNN_ECUDA, "round loop did not terminate (internal error)");
     }
     if (r > stats.rounds) stats.rounds = r;
@@ -1006,7 +1151,7 @@ aknn_status aknn_query_async(const aknn_index *cix, const uint8_t *queries_dev, 
     std::vector<aknn_index *> one{ix};
     return run_query_sharded(one, true, queries_dev, q, k, h, seed, al, opts, out, ix->n_local, st);
   }
-  return run_query(ix, queries_dev, ix->d, q, k, h, seed, al, opts, out, st);
+  return run_query(ix, queries_dev, ix->d, q, k, h, seed, al, opts, out, st, /*may_defer=*/true);
 }
 
 }  // extern "C"
@@ -1218,6 +1363,7 @@ aknn_status aknn_shard_merge_host(const void *recs, int32_t world, int64_t n_glo
 
 aknn_status aknn_get_stats(const aknn_index *ix, aknn_stats *out) {
   if (!ix || !out) return fail(AKNN_EINVAL, "NULL argument");
+  TRY(finish_pending(const_cast<aknn_index *>(ix)));
   *out = ix->stats;
   return AKNN_OK;
 }
@@ -1302,6 +1448,8 @@ int32_t aknn_index_dim(const aknn_index *ix) { return ix ? ix->d : -1; }
 
 void aknn_free(aknn_index *ix) {
   if (!ix) return;
+  finish_pending(ix);  // its copies target ix->host
+  if (ix->pending.ev) cudaEventDestroy(ix->pending.ev);
 #ifdef AKNN_WITH_NCCL
   if (ix->comm) ncclCommDestroy(ix->comm);
 #endif

@@ -38,7 +38,7 @@ struct QState {
 // Per-round control block (device memory; one per batch).
 struct RoundCtl {
   unsigned int n_active;                  // queries failing Eq. (5) this round
-  unsigned int pad0;
+  unsigned int n_tiles;                   // dense tiles listed for k_advance_tiles
   unsigned int cnt[NSLOT];                // pairs per action slot
   unsigned int off[NSLOT + 1];            // list offsets per slot
   unsigned int cursor[NSLOT];             // scatter cursors
@@ -99,6 +99,14 @@ struct Geom {
   uint32_t *xflags;      // [ceil(q/128)][xf_cols] tile holds an ACT_EXACT pair this round
   const int32_t *nx;     // [n] ||x_i||^2
   int32_t *nq;           // [q] ||x_q||^2 of this batch
+  // tile-staged level gathers (advance_tiles.cu)
+  int tile_on;           // 1: dense (R x P) tiles advance from shared memory
+  int tile_lr, tile_lp;  // log2 R (queries per tile), log2 P (points per tile)
+  int tile_cols;         // row length of tilework: ceil(npad / P)
+  uint32_t *tilework;    // [ceil(qb / R)][tile_cols] draws of the tile's sampled blockers
+  uint32_t *tilelist;    // dense tiles of this round (k_tile_list), ctl->n_tiles of them
+  uint32_t tile_min;     // dense iff tilework >= tile_min
+  int tile_slot_l;       // log2 of a row slot in shared memory (>= pitch)
 };
 
 // ---- Philox4x32-10 (Salmon et al.), counter (x,y,z,w), key (k0,k1) --------

@@ -190,6 +190,14 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
     const unsigned slot = act == 0 ? NONE : (act == ACT_EXACT ? (unsigned)MAX_LEVELS : act - 1u);
     hist_add(scnt, slot);
   }
+  if (g.tile_on) {
+    // per-tile draws of the sampled blockers: the P/4 lanes of a tile segment add up
+    uint32_t v = (uint32_t)mydraw;
+    const int seg = min(32, (1 << g.tile_lp) >> 2);
+    for (int o = 1; o < seg; o <<= 1) v += __shfl_xor_sync(FULL, v, o);
+    if ((lane_id() & (seg - 1)) == 0 && v)
+      atomicAdd(&g.tilework[(size_t)(qi >> g.tile_lr) * g.tile_cols + (i0 >> g.tile_lp)], v);
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     mydraw += __shfl_xor_sync(FULL, mydraw, o);
@@ -254,6 +262,21 @@ __global__ void k_plan(RoundCtl *ctl, unsigned bpl, int stage_lo) {
   ctl->advanced += adv;
 }
 
+// After the scatter: the lists hold only the pairs of sparse tiles, cursor[s] of
+// them per slot; the advance kernels walk exactly those.
+__global__ void k_plan_lists(RoundCtl *ctl, unsigned bpl, int stage_lo) {
+  if (threadIdx.x != 0) return;
+  unsigned long long ch = 0;
+  for (int s = 0; s < NSLOT; ++s) {
+    const unsigned c = ctl->cursor[s];
+    ctl->cnt[s] = c;
+    ctl->chunk_off[s] = ch;
+    const unsigned ppc = pairs_per_chunk(s, bpl, stage_lo);
+    ch += (c + ppc - 1) / ppc;
+  }
+  ctl->chunk_off[NSLOT] = ch;
+}
+
 // a8: compaction of the action bytes into per-slot lists of (qi << ibits | i).
 // One CTA per (query, 1024-arm chunk); thread t owns arms chunk + t + 256 e, so for
 // each e a warp covers 32 consecutive arms.  Slots are counted in shared memory
@@ -275,6 +298,9 @@ __global__ void __launch_bounds__(FIL_NT) k_scatter(Geom g) {
     const int i = base_i + e * FIL_NT;
     const uint8_t act = i < g.n ? arow[i] : (uint8_t)0;
     slot[e] = act == 0 ? NONE : (act == ACT_EXACT ? (unsigned)MAX_LEVELS : act - 1u);
+    if (g.tile_on && slot[e] < (unsigned)MAX_LEVELS &&
+        g.tilework[(size_t)(qi >> g.tile_lr) * g.tile_cols + (i >> g.tile_lp)] >= g.tile_min)
+      slot[e] = NONE;  // k_advance_tiles takes it
     const unsigned m = __match_any_sync(FULL, slot[e]);
     const int leader = __ffs(m) - 1;
     unsigned b = 0;
@@ -650,6 +676,11 @@ cudaError_t launch_init(const Geom &g, cudaStream_t s) {
     if (e == cudaSuccess) e = launch_row_norms(g.Q, g.pitch, g.q, g.nq, s);
     if (e != cudaSuccess) return e;
   }
+  if (g.tile_on) {
+    const size_t rows = ((size_t)g.q + (1u << g.tile_lr) - 1) >> g.tile_lr;
+    const cudaError_t e = cudaMemsetAsync(g.tilework, 0, sizeof(uint32_t) * rows * g.tile_cols, s);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 
@@ -668,12 +699,21 @@ cudaError_t launch_filter(const Geom &g, cudaStream_t s) {
 cudaError_t launch_compact(const Geom &g, cudaStream_t s) {
   k_plan<<<1, 32, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo);
   k_scatter<<<dim3(g.q, cdiv(g.npad, FIL_NT * 4)), FIL_NT, 0, s>>>(g);
+  if (g.tile_on) {
+    k_plan_lists<<<1, 32, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo);
+    const cudaError_t e = launch_tile_list(g, s);
+    if (e != cudaSuccess) return e;
+  }
   return cudaGetLastError();
 }
 
 cudaError_t launch_advance(const Geom &g, int num_sms, cudaStream_t s) {
   if (g.exact_mma) {
     const cudaError_t e = launch_exact_fallback_mma(g, s);
+    if (e != cudaSuccess) return e;
+  }
+  if (g.tile_on) {
+    const cudaError_t e = launch_advance_tiles(g, num_sms, s);
     if (e != cudaSuccess) return e;
   }
   k_advance<<<num_sms * 8, ADV_NT, 0, s>>>(g);

@@ -285,3 +285,60 @@ def test_exact_fallback_tensor_cores_equals_rows(ak, n, d, q, k, h, kind):
     if n > 100:
         assert sa["exact_fallbacks"] > 0  # the tile pass was exercised
     _assert_parity(a, orc.query_br(X, Q, k, h, 21, al, want_sums=True))
+
+
+@pytest.mark.parametrize("n,d,q,k,h,kind", [(3001, 256, 6, 4, 6, "theory"), (1237, 100, 70, 3, 4, "theory"),
+                                            (4099, 128, 3, 10, 10, "exp"), (5, 16, 4, 2, 2, "theory"),
+                                            (2000, 784, 35, 10, 10, "theory"), (700, 5000, 3, 4, 4, "theory")])
+def test_tiled_advance_equals_lists(ak, n, d, q, k, h, kind):
+    """Level gathers of dense tiles from shared memory (default) and through the work
+    lists (AKNN_FLAG_NO_TILES) give identical bytes; both equal the oracle.  Ragged n
+    and q leave partial tiles; d = 5000 takes the smallest tile shape."""
+    X, Q = synth.small_instance(n + 3 * d, n, d, q=q)
+    al = orc.alpha_theory(n, 0.05, d) if kind == "theory" else orc.alpha_experimental(n, 0.05, d, 0.05)
+    ix = ak.Index(X)
+    a = ix.query(Q, k, h, 0.05, 33, al, counts=True, sums=True)
+    b = ix.query(Q, k, h, 0.05, 33, al, counts=True, sums=True, flags=ak.FLAG_NO_TILES)
+    c = ix.query(Q, k, h, 0.05, 33, al, counts=True, sums=True,
+                 flags=ak.FLAG_NO_TILES | ak.FLAG_EXACT_ROWS)
+    ix.close()
+    for key in KEYS:
+        assert np.array_equal(a[key], b[key]), key
+        assert np.array_equal(a[key], c[key]), key
+    _assert_parity(a, orc.query_br(X, Q, k, h, 33, al, want_sums=True))
+
+
+def test_sharded_tiles_equal_lists(ak):
+    X, Q = synth.small_instance(77, 9000, 200, q=5)
+    al = orc.alpha_theory(9000, 0.05, 200)
+    sh = [ak.Index(X[a:b], n_global=9000, offset=a) for a, b in ((0, 4001), (4001, 9000))]
+    a = ak.query_multi(sh, Q, 8, 8, 0.05, 4, al, counts=True, sums=True)
+    b = ak.query_multi(sh, Q, 8, 8, 0.05, 4, al, counts=True, sums=True, flags=ak.FLAG_NO_TILES)
+    for s in sh:
+        s.close()
+    for key in KEYS:
+        assert np.array_equal(a[key], b[key]), key
+    _assert_parity(a, orc.query_br(X, Q, 8, 8, 4, al, want_sums=True))
+
+
+def test_async_call_defers_stats(ak):
+    """aknn_query_async on the graph path returns without waiting; its statistics are
+    completed by aknn_get_stats or by the next call, and equal the host API's."""
+    import torch
+    X, Q = synth.small_instance(404, 3000, 160, q=300)  # several 128-query exact tiles
+    al = orc.alpha_theory(3000, 0.05, 160)
+    ix = ak.Index(X)
+    Qd = torch.from_numpy(Q).cuda()
+    a1 = ix.query_device(Qd, 5, 5, 0.05, 1, al)
+    a2 = ix.query_device(Qd, 5, 5, 0.05, 2, al)  # finishes the first call's statistics
+    torch.cuda.synchronize()
+    s2 = ix.stats()
+    h2 = ix.query(Q, 5, 5, 0.05, 2, al, counts=False)
+    hs2 = ix.stats()
+    h1 = ix.query(Q, 5, 5, 0.05, 1, al, counts=False)
+    ix.close()
+    for key in ("sets", "dhat", "evals", "draws", "rounds"):
+        assert np.array_equal(a1[key].cpu().numpy(), h1[key]), key
+        assert np.array_equal(a2[key].cpu().numpy(), h2[key]), key
+    for key in ("draws", "rounds", "exact_fallbacks", "philox_blocks", "query_rounds", "kernel_launches"):
+        assert s2[key] == hs2[key], key
