@@ -2,7 +2,7 @@
 //
 // The batch's (query x point) grid is cut into tiles of R = 2^tile_lr queries x
 // P = 2^tile_lp points.  k_filter adds, per tile, the draws its blockers take this
-// round (tilework); a tile whose draws reach tile_min is advanced here instead of
+// round (tilework); a tile whose draws reach tile_row_draws * (R + P) is advanced here instead of
 // through the work lists (k_scatter leaves its pairs out): the CTA copies the R
 // query rows and P point rows into shared memory once with 16-byte loads, then every
 // draw of every listed pair of the tile gathers its two bytes from there.
@@ -136,9 +136,11 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
     // ADV_TP / nb whole pairs per pass.  nb > ADV_TP: tpp lanes per pair (consecutive
     // lanes), each running ADV_TP independent Philox blocks at a time, then a shuffle
     // reduce inside the lane group; every pair's sum is written by one thread.
-    for (int c = 0; c < MAX_LEVELS; ++c) {
+    unsigned lmask = 0;  // levels present in the tile
+    for (int c = 0; c < MAX_LEVELS; ++c) lmask |= (lcnt[c] != 0u) << c;
+    for (; lmask; lmask &= lmask - 1) {
+      const int c = __ffs(lmask) - 1;
       const unsigned m = lcnt[c];
-      if (m == 0) continue;
       const int lb = c < 2 ? 0 : c - 2;  // log2 Philox blocks per pair
       const unsigned s = 1u << c, nb = 1u << lb;
       const uint16_t *L = lst + loff[c];
@@ -219,8 +221,8 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
   }
 }
 
-// The dense tiles of this round (tilework >= tile_min) in point-major numbering
-// t = tp * rows + tr; every counter is reset for the next round.  Runs after k_scatter.
+// The dense tiles of this round (tilework >= tile_row_draws * (R + P)) in point-major
+// numbering t = tp * rows + tr.  Runs after k_scatter (k_filter rewrites every count).
 __global__ void k_tile_list(Geom g) {
   const int rows = (g.q + (1 << g.tile_lr) - 1) >> g.tile_lr;
   const int cols = (g.n + (1 << g.tile_lp) - 1) >> g.tile_lp;
@@ -228,9 +230,8 @@ __global__ void k_tile_list(Geom g) {
   bool dense = false;
   if (t < (unsigned)rows * (unsigned)cols) {
     const int tp = (int)(t / (unsigned)rows), tr = (int)(t % (unsigned)rows);
-    uint32_t *w = g.tilework + (size_t)tr * g.tile_cols + tp;
-    dense = *w >= g.tile_min;
-    *w = 0u;
+    dense = (float)g.tilework[(size_t)tr * g.tile_cols + tp] >=
+            g.tile_row_draws * (float)((1 << g.tile_lr) + (1 << g.tile_lp));
   }
   const unsigned m = __ballot_sync(FULL, dense);
   unsigned b = 0;

@@ -248,13 +248,13 @@ aknn_status setup_exact_mma(aknn_index *ix, Geom &g, int64_t qb, uint8_t *ws, co
 
 // Tile-staged level gathers (advance_tiles.cu) unless AKNN_FLAG_NO_TILES / AKNN_TILE=0.
 // Tile shape: the largest R = P (powers of two, <= 32) whose rows fit a third of the
-// SM's shared memory (3 CTAs per SM), else half, else all of it.  AKNN_TILE_LR /
-// AKNN_TILE_LP override (experiments).  A tile is dense when its draws, at one 32-byte
-// sector each on the list path, cost at least AKNN_TILE_F (default 1) times its
-// staging bytes (R + P) * pitch.
+// SM's shared memory (3 CTAs per SM), else half, else all of it; rows of > 16 KB:
+// R = 1, P = 4.  AKNN_TILE_LR / AKNN_TILE_LP override (experiments).  A tile is dense
+// (staged) when its draws, at one 32-byte sector each on the list path, cost at least
+// AKNN_TILE_F (default 4) times its staging bytes (R + P) * pitch.
 struct TileShape {
   int on, lr, lp;
-  uint32_t min_draws;
+  float row_draws;
 };
 
 int env_int(const char *name, int dflt) {
@@ -263,27 +263,29 @@ int env_int(const char *name, int dflt) {
 }
 
 TileShape tile_shape(int64_t pitch) {
-  TileShape t{0, 0, 0, 0};
+  TileShape t{0, 0, 0, 0.f};
   if (env_int("AKNN_TILE", 1) == 0) return t;
-  int lr = -1;
+  int lr = -1, lp = -1;
   for (size_t cap : {(size_t)75 * 1024, (size_t)112 * 1024, (size_t)220 * 1024}) {
     for (int l = 5; l >= 2; --l)
       if (tile_smem_bytes(l, l, pitch) <= cap) {
-        lr = l;
+        lr = lp = l;
         break;
       }
     if (lr >= 0) break;
   }
+  if (lr < 0 && tile_smem_bytes(0, 2, pitch) <= (size_t)220 * 1024) {
+    lr = 0;
+    lp = 2;
+  }
   if (lr < 0) return t;
   t.lr = env_int("AKNN_TILE_LR", lr);
-  t.lp = env_int("AKNN_TILE_LP", lr);
-  if (t.lr < 0 || t.lr > 8 || t.lp < 2 || t.lp > 8 || t.lr + t.lp > 16 ||
-      tile_smem_bytes(t.lr, t.lp, pitch) > (size_t)220 * 1024)
-    return TileShape{0, 0, 0, 0};
+  t.lp = env_int("AKNN_TILE_LP", lp);
+  if (t.lr < 0 || t.lr > 5 || t.lp < 2 || t.lp > 5 || tile_smem_bytes(t.lr, t.lp, pitch) > (size_t)220 * 1024)
+    return TileShape{0, 0, 0, 0.f};
   const char *fe = getenv("AKNN_TILE_F");
-  const double f = fe && fe[0] ? atof(fe) : 1.0;
-  const double bytes = (double)(((int64_t)1 << t.lr) + ((int64_t)1 << t.lp)) * (double)pitch;
-  t.min_draws = (uint32_t)std::max(1.0, std::ceil(f * bytes / 32.0));
+  const double f = fe && fe[0] ? atof(fe) : 4.0;
+  t.row_draws = (float)(f * (double)pitch / 32.0);
   t.on = 1;
   return t;
 }
@@ -294,16 +296,32 @@ size_t tile_ws_bytes(int64_t qb, int64_t npad, const TileShape &t) {
   return 2 * round_up((size_t)(rows * cols) * 4, 256);  // tilework + tilelist
 }
 
-void setup_tiles(Geom &g, const TileShape &t, int64_t qb, uint8_t *ws, const aknn_opts &o) {
+void setup_tiles(Geom &g, const TileShape &t, const aknn_opts &o, int64_t qb, uint8_t *ws) {
   g.tile_on = (t.on && !(o.flags & AKNN_FLAG_NO_TILES)) ? 1 : 0;
+  g.advanced = &g.ctl->advanced;
   if (!g.tile_on) return;
   g.tile_lr = t.lr;
   g.tile_lp = t.lp;
   g.tile_cols = (int)((g.npad + (1ll << t.lp) - 1) >> t.lp);
   g.tilework = reinterpret_cast<uint32_t *>(ws);
   g.tilelist = reinterpret_cast<uint32_t *>(ws + tile_ws_bytes(qb, g.npad, t) / 2);
-  g.tile_min = t.min_draws;
   g.tile_slot_l = tile_slot_log2(g.pitch);
+  g.tile_row_draws = t.row_draws;
+}
+
+// One round after the rank split: filter -> plan/scatter (+ dense-tile list) ->
+// advance (tensor-core exact fallbacks, dense tiles, list levels).  timer(k): per-class
+// event brackets of the host-driven loop (0 start, 1 filter, 2 compact, 3 advance).
+template <class Timer>
+cudaError_t launch_round_body(const Geom &g, int num_sms, cudaStream_t st, Timer &&timer) {
+  timer(0);
+  cudaError_t e = launch_filter(g, st);
+  timer(1);
+  if (e == cudaSuccess) e = launch_compact(g, st);
+  timer(2);
+  if (e == cudaSuccess) e = launch_advance(g, num_sms, st);
+  timer(3);
+  return e;
 }
 
 // Builds the level geometry of the composite key (R9).
@@ -475,10 +493,8 @@ aknn_status loop_graph(aknn_index *ix, const Geom &g, int nbits, int max_rounds,
   }
   cudaGraph_t body = cp.conditional.phGraph_out[0];
   CU(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
-  e = launch_filter(g, cs);
-  if (e == cudaSuccess) e = launch_compact(g, cs);
-  if (e == cudaSuccess) e = launch_advance(g, ix->num_sms, cs);
-  if (e == cudaSuccess) e = launch_zero_round(g.ctl, cs);
+  e = launch_round_body(g, ix->num_sms, cs, [](int) {});
+  if (e == cudaSuccess) e = launch_zero_round(g, cs);
   if (e == cudaSuccess) e = launch_select(g, nbits, cs);
   if (e == cudaSuccess) e = launch_round_ctl(g.ctl, h, max_rounds, cs);
   cudaGraph_t body_out = nullptr;
@@ -498,10 +514,12 @@ aknn_status loop_graph(aknn_index *ix, const Geom &g, int nbits, int max_rounds,
 
 // Kernel launches per class (for aknn_stats; memset nodes excluded).
 int launches_init_of(const Geom &g) { return 2 + (g.exact_mma ? 1 : 0); }  // init, qstate, norms
+int launches_filter_of(const Geom &) { return 1; }
 int launches_compact_of(const Geom &g) { return 2 + (g.tile_on ? 2 : 0); }  // plan, scatter (+ lists)
 int launches_advance_of(const Geom &g) {
   return 1 + (g.tile_on ? 1 : 0) + (g.exact_mma ? 1 : 0) + (g.stage_lo < MAX_LEVELS ? 1 : 0);
 }
+int launches_output_of(const OutPtrs &o) { return 2 + ((o.counts || o.sums) ? 1 : 0); }  // tally, output
 
 // Folds one sub-batch's control block and query states (copied to the host) into
 // the statistics; graph = the device-driven loop counted the rounds itself.
@@ -512,8 +530,8 @@ void fold_batch_stats(aknn_stats &stats, const RoundCtl &ctl_h, const QState *qs
     stats.query_rounds += (int64_t)ctl_h.qrounds;
     stats.blocked_query_rounds += (int64_t)ctl_h.brounds;
     stats.launches_init += 1 + launches_init_of(g);  // + loop reset
-    stats.launches_select += 3 * r;                  // pivot, radix fallback, round control
-    stats.launches_filter += r - 1;
+    stats.launches_select += 4 * r;                  // pivot, radix fallback, thresholds, round control
+    stats.launches_filter += launches_filter_of(g) * (r - 1);
     stats.launches_compact += launches_compact_of(g) * (r - 1);
     stats.launches_advance += (launches_advance_of(g) + 1) * (r - 1);  // + counter reset
     if (ctl_h.n_active > 0 && status) *status = AKNN_EMAXROUNDS;
@@ -599,9 +617,11 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   const size_t oXm = off; off = round_up(off + exact_mma_ws_bytes(qb, npad), 256);
   const TileShape tsh = tile_shape(ix->pitch);
   const size_t oTw = off; off = round_up(off + tile_ws_bytes(qb, npad, tsh), 256);
+  const size_t oThr = off; off = round_up(off + sizeof(int32_t) * THR_STRIDE * (size_t)qb, 256);
   TRY(ix->ws.ensure(off));
 
   Geom g{};
+  g.thr = ix->ws.as<int32_t>(oThr);
   g.X = ix->X.as<uint8_t>();
   g.Q = ix->ws.as<uint8_t>(oQ);
   g.alpha = alpha_dev;
@@ -634,7 +654,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   g.force_radix = (o.flags & AKNN_FLAG_RADIX_SELECT) ? 1 : 0;
   g.stage_lo = stage_level(g.pitch);
   TRY(setup_exact_mma(ix, g, qb, ix->ws.as<uint8_t>(oXm), o, st));
-  setup_tiles(g, tsh, qb, ix->ws.as<uint8_t>(oTw), o);
+  setup_tiles(g, tsh, o, qb, ix->ws.as<uint8_t>(oTw));
 
   aknn_stats stats{};
   stats.pairs = (int64_t)q * n;
@@ -653,7 +673,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   // defer the statistics (no host wait at all) on the async graph path without a
   // round cap: the status cannot be EMAXROUNDS there
   const bool defer = may_defer && use_graph && o.max_rounds <= 0;
-  const int outs_per_batch = (out->counts || out->sums) ? 2 : 1;
+  const int outs_per_batch = (out->counts || out->sums) ? 3 : 2;  // tally, output, counts
   std::vector<int> batch_qn;
   tm.open_a = nullptr;
   aknn_status status = AKNN_OK;
@@ -688,11 +708,11 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
     for (;;) {
       ++r;
       // zero the per-round counters (everything but the cumulative `advanced`)
-      CU(cudaMemsetAsync(g.ctl, 0, offsetof(RoundCtl, advanced), st));
+      CU(launch_zero_round(g, st));
       tm.start();
       CU(launch_select(g, kg.nbits, st));
       tm.stop(PH_SELECT);
-      stats.launches_select += 2;
+      stats.launches_select += 3;
       stats.query_rounds += evaluated;
       CU(cudaMemcpyAsync(h_active, &g.ctl->n_active, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
       CU(sync_spin(st));
@@ -704,17 +724,21 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
         status = AKNN_EMAXROUNDS;
         break;
       }
-      tm.start();
-      CU(launch_filter(g, st));
-      tm.stop(PH_FILTER);
-      ++stats.launches_filter;
-      tm.start();
-      CU(launch_compact(g, st));
-      tm.stop(PH_COMPACT);
+      CU(launch_round_body(g, ix->num_sms, st, [&](int k) {
+        if (k == 0) {
+          tm.start();
+        } else if (k == 1) {
+          tm.stop(PH_FILTER);
+          tm.start();
+        } else if (k == 2) {
+          tm.stop(PH_COMPACT);
+          tm.start();
+        } else {
+          tm.stop(PH_ADVANCE);
+        }
+      }));
+      stats.launches_filter += launches_filter_of(g);
       stats.launches_compact += launches_compact_of(g);
-      tm.start();
-      CU(launch_advance(g, ix->num_sms, st));
-      tm.stop(PH_ADVANCE);
       stats.launches_advance += launches_advance_of(g);
       if (r > 1 + 64 * 64) return fail(AKNN_ECUDA, "round loop did not terminate (internal error)");
     }
@@ -726,7 +750,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
     CU(cudaMemcpyAsync(h_ctl, g.ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
     CU(cudaMemcpyAsync(h_qs, g.qs, sizeof(QState) * qn, cudaMemcpyDeviceToHost, st));
     if (defer) continue;  // folded in by finish_pending
-    stats.launches_output += outs_per_batch;
+    stats.launches_output += launches_output_of(op);
     CU(sync_spin(st));
     fold_batch_stats(stats, *h_ctl, h_qs, qn, use_graph, g, r, &status);
     if (status != AKNN_OK) break;
@@ -835,9 +859,11 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     const size_t oXm = off; off = round_up(off + exact_mma_ws_bytes(qb, npad), 256);
     const TileShape tsh = tile_shape(ix->pitch);
     const size_t oTw = off; off = round_up(off + tile_ws_bytes(qb, npad, tsh), 256);
+    const size_t oThr = off; off = round_up(off + sizeof(int32_t) * THR_STRIDE * (size_t)qb, 256);
     TRY(ix->ws.ensure(off));
     Geom &g = G[si];
     g = Geom{};
+    g.thr = ix->ws.as<int32_t>(oThr);
     g.X = ix->X.as<uint8_t>();
     g.Q = ix->ws.as<uint8_t>(oQ);
     g.alpha = alpha_dev;
@@ -871,7 +897,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     g.world = W;
     g.recv_stride = recv_stride;
     TRY(setup_exact_mma(ix, g, qb, ix->ws.as<uint8_t>(oXm), o, st));
-    setup_tiles(g, tsh, qb, ix->ws.as<uint8_t>(oTw), o);
+    setup_tiles(g, tsh, o, qb, ix->ws.as<uint8_t>(oTw));
     if (has_recv) g.recv = ix->ws.as<ShardRec>(oRecv);
     if (si == 0 && !nccl) recv_shared = ix->ws.as<ShardRec>(oRecv);
     if (nccl) g.send = ix->ws.as<ShardRec>(oSend);
@@ -922,7 +948,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
       ++r;
       tm.start();
       for (size_t si = 0; si < nS; ++si) {
-        CU(cudaMemsetAsync(G[si].ctl, 0, offsetof(RoundCtl, advanced), st));
+        CU(launch_zero_round(G[si], st));
         CU(launch_select_local(G[si], kg[si].nbits, st));
         ++stats.launches_select;
       }
@@ -937,7 +963,8 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
         OutPtrs op{(int)r0, 0, 0, 0, (nccl || si == 0) ? out->sets : nullptr,
                    (nccl || si == 0) ? out->dhat : nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
         CU(launch_merge(G[si], op, st));
-        ++stats.launches_select;
+        CU(launch_thresholds(G[si], st));
+        stats.launches_select += 2;  // merge + thresholds
       }
       tm.stop(PH_SELECT);
       stats.query_rounds += evaluated;
@@ -952,16 +979,10 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
         break;
       }
       tm.start();
-      for (size_t si = 0; si < nS; ++si) CU(launch_filter(G[si], st));
-      tm.stop(PH_FILTER);
-      stats.launches_filter += nS;
-      tm.start();
-      for (size_t si = 0; si < nS; ++si) CU(launch_compact(G[si], st));
-      tm.stop(PH_COMPACT);
+      for (size_t si = 0; si < nS; ++si) CU(launch_round_body(G[si], shards[si]->num_sms, st, [](int) {}));
+      tm.stop(PH_ADVANCE);  // sharded: the whole round body is timed as one class (advance)
+      stats.launches_filter += launches_filter_of(G[0]) * (int)nS;
       stats.launches_compact += launches_compact_of(G[0]) * (int)nS;
-      tm.start();
-      for (size_t si = 0; si < nS; ++si) CU(launch_advance(G[si], shards[si]->num_sms, st));
-      tm.stop(PH_ADVANCE);
       stats.launches_advance += launches_advance_of(G[0]) * (int)nS;
       if (r > 1 + 64 * 64) return fail(AKNN_ECUDA, "round loop did not terminate (internal error)");
     }
@@ -971,7 +992,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
       OutPtrs op{(int)r0, nccl ? 0 : shards[si]->offset, out_ncols, (!nccl && nS > 1) ? 1 : 0,
                  nullptr, nullptr, out->counts, out->sums, out->evals, out->draws, out->rounds};
       CU(launch_output_sharded(G[si], op, st));
-      stats.launches_output += (out->counts || out->sums) ? 2 : 1;
+      stats.launches_output += launches_output_of(op);
     }
 #ifdef AKNN_WITH_NCCL
     if (nccl) {
@@ -1268,7 +1289,7 @@ namespace {
 struct HostKey {
   KeyGeom kg;
   unsigned long long key(int32_t S, uint8_t l, uint32_t gid) const {
-    const unsigned long long mul = (l == LVL_EXACT) ? kg.Ld : (kg.L >> l);
+    const unsigned long long mul = lvl_exact(l) ? kg.Ld : (kg.L >> l);
     return (((unsigned long long)(uint32_t)S * mul) << kg.kbits) | gid;
   }
 };

@@ -155,13 +155,14 @@ struct EpiFallback {
         s4.z = xn.z + nqr - 2 * (int32_t)v[j0 + 2];
         s4.w = xn.w + nqr - 2 * (int32_t)v[j0 + 3];
         *reinterpret_cast<int4 *>(srow + j0) = s4;
-        *reinterpret_cast<uint32_t *>(lrow + j0) = 0xFFFFFFFFu;  // 4 x LVL_EXACT
+        uint32_t *l4 = reinterpret_cast<uint32_t *>(lrow + j0);
+        *l4 |= 0x80808080u;  // 4 x lvl_to_exact
       } else {
 #pragma unroll
         for (int j = j0; j < j0 + 4; ++j)
           if (a[j] == ACT_EXACT && col0 + j < g.n) {
             srow[j] = __ldg(g.nx + col0 + j) + nqr - 2 * (int32_t)v[j];
-            lrow[j] = LVL_EXACT;
+            lrow[j] = lvl_to_exact(lrow[j]);
           }
       }
     }

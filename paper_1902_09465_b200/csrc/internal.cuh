@@ -9,14 +9,25 @@
 namespace aknn {
 
 // Level byte per (query, point) pair: c = log2 T (T = 2^c sampled draws so
-// far), or LVL_EXACT once T = d.
-constexpr uint8_t LVL_EXACT = 0xFF;
+// far); once the arm went exact (T = d) the byte is LVL_EXACT | c with c
+// the last sampled level, so the arm's sampled draws (2^c) stay recoverable and
+// the per-query counters are tallied from the final state (k_tally).
+constexpr uint8_t LVL_EXACT = 0x80;
+__host__ __device__ __forceinline__ bool lvl_exact(uint8_t l) { return (l & LVL_EXACT) != 0; }
+__host__ __device__ __forceinline__ uint8_t lvl_to_exact(uint8_t l) { return (uint8_t)(l | LVL_EXACT); }
+__host__ __device__ __forceinline__ uint32_t lvl_sampled(uint8_t l) { return 1u << (l & 0x7F); }
 // Action byte written by the blocker filter: 0 = idle, c+1 = draw level c+1
 // (T -> 2T), ACT_EXACT = exact fallback.
 constexpr uint8_t ACT_EXACT = 0xFE;
 // d <= 33025 -> sampled levels c in [0, 15]; slot MAX_LEVELS = exact list.
 constexpr int MAX_LEVELS = 16;
 constexpr int NSLOT = MAX_LEVELS + 1;
+
+// Integer form of the blocker predicate of one query for a round, per sampled level c
+// (k_thresholds): U(S, c) > B  <=>  S >= Su[c];  L(S, c) < A  <=>  S < Sl[c];
+// alpha(2^c) > alpha_d2  <=>  bit c of the M mask.  Exact because U and L are
+// monotone non-decreasing in S (one correctly rounded division, one addition).
+constexpr int THR_STRIDE = 2 * MAX_LEVELS + 1;
 
 // Per-query state of the round loop (device memory, one per batch row).
 struct QState {
@@ -30,8 +41,8 @@ struct QState {
   int fallback;               // 1: the one-pass pivot select could not decide this
                               //    round; the multi-pass radix select does
   int rounds;                 // rounds evaluated
-  long long draws;            // sampled draws so far
-  long long nexact;           // exact fallbacks so far
+  long long draws;            // sampled draws      } tallied from the final
+  long long nexact;           // exact fallbacks    } arm states by k_tally
   long long blocks;           // Philox4x32-10 blocks the level gathers used
 };
 
@@ -101,12 +112,15 @@ struct Geom {
   int32_t *nq;           // [q] ||x_q||^2 of this batch
   // tile-staged level gathers (advance_tiles.cu)
   int tile_on;           // 1: dense (R x P) tiles advance from shared memory
-  int tile_lr, tile_lp;  // log2 R (queries per tile), log2 P (points per tile)
+  int tile_lr, tile_lp;  // log2 R (queries per tile), log2 P (points per tile); R | 32, 4 <= P <= 32
   int tile_cols;         // row length of tilework: ceil(npad / P)
   uint32_t *tilework;    // [ceil(qb / R)][tile_cols] draws of the tile's sampled blockers
   uint32_t *tilelist;    // dense tiles of this round (k_tile_list), ctl->n_tiles of them
-  uint32_t tile_min;     // dense iff tilework >= tile_min
+  float tile_row_draws;  // dense iff tilework >= tile_row_draws * (R + P)
   int tile_slot_l;       // log2 of a row slot in shared memory (>= pitch)
+  unsigned long long *advanced;  // pairs advanced (statistics), device counter
+  // the blocker predicate as integer thresholds per (query, level) (k_thresholds)
+  int32_t *thr;          // [q][THR_STRIDE]: Su[c], Sl[c] (c < MAX_LEVELS), M-mask
 };
 
 // ---- Philox4x32-10 (Salmon et al.), counter (x,y,z,w), key (k0,k1) --------
@@ -146,14 +160,14 @@ __device__ __forceinline__ uint32_t coord_of(uint32_t w, uint32_t d) { return __
 // different shards are comparable and unique.
 __device__ __forceinline__ unsigned long long arm_key(int32_t S, uint8_t l, uint32_t i,
                                                       const Geom &g) {
-  const unsigned long long mul = (l == LVL_EXACT) ? g.Ld : (g.L >> l);
+  const unsigned long long mul = lvl_exact(l) ? g.Ld : (g.L >> l);
   return (((unsigned long long)(uint32_t)S * mul) << g.kbits) | (i + g.id_offset);
 }
 
 // d_hat = S / (T * 65025), one correctly rounded fp64 division (P:121-124,
 // DESIGN.md reading R15).  T * 65025 is exact in fp64.
 __host__ __device__ __forceinline__ double dhat_of(int32_t S, uint8_t l, int d) {
-  const double T = (l == LVL_EXACT) ? (double)d : (double)(1u << l);
+  const double T = lvl_exact(l) ? (double)d : (double)(1u << l);
 #ifdef __CUDA_ARCH__
   return __ddiv_rn((double)S, __dmul_rn(T, 65025.0));
 #else
@@ -163,9 +177,9 @@ __host__ __device__ __forceinline__ double dhat_of(int32_t S, uint8_t l, int d) 
 
 __host__ __device__ __forceinline__ double alpha_of(uint8_t l, const double *alpha) {
 #ifdef __CUDA_ARCH__
-  return (l == LVL_EXACT) ? 0.0 : __ldg(alpha + (1u << l));
+  return lvl_exact(l) ? 0.0 : __ldg(alpha + (1u << l));
 #else
-  return (l == LVL_EXACT) ? 0.0 : alpha[1u << l];
+  return lvl_exact(l) ? 0.0 : alpha[1u << l];
 #endif
 }
 

@@ -25,6 +25,7 @@ struct OutPtrs {
 cudaError_t launch_init(const Geom &g, cudaStream_t s);
 cudaError_t launch_select(const Geom &g, int nbits, cudaStream_t s);
 cudaError_t launch_filter(const Geom &g, cudaStream_t s);
+cudaError_t launch_thresholds(const Geom &g, cudaStream_t s);  // after every rank split / merge
 cudaError_t launch_compact(const Geom &g, cudaStream_t s);
 cudaError_t launch_advance(const Geom &g, int num_sms, cudaStream_t s);
 int stage_level(int64_t pitch);
@@ -33,9 +34,11 @@ cudaError_t launch_advance_tiles(const Geom &g, int num_sms, cudaStream_t s);
 cudaError_t launch_tile_list(const Geom &g, cudaStream_t s);
 size_t tile_smem_bytes(int lr, int lp, int64_t pitch);
 int tile_slot_log2(int64_t pitch);
+// Per-query counters from the final arm states (before the outputs).
+cudaError_t launch_tally(const Geom &g, cudaStream_t s);
 // Device-driven round loop (CUDA graph with a conditional WHILE node).
 cudaError_t launch_ctl_reset(RoundCtl *ctl, unsigned q, cudaStream_t s);
-cudaError_t launch_zero_round(RoundCtl *ctl, cudaStream_t s);
+cudaError_t launch_zero_round(const Geom &g, cudaStream_t s);
 cudaError_t launch_round_ctl(RoundCtl *ctl, cudaGraphConditionalHandle h, int max_rounds, cudaStream_t s);
 cudaError_t launch_output(const Geom &g, const OutPtrs &o, cudaStream_t s);
 // Sharded rounds (shard_kernels.cu).

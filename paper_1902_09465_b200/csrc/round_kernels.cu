@@ -29,7 +29,7 @@ __global__ void k_init(Geom g) {
   const size_t o = (size_t)qi * g.npad + i;
   if (i >= g.n) {
     g.S[o] = 0;
-    g.lvl[o] = LVL_EXACT;
+    g.lvl[o] = LVL_EXACT;  // padding: never selected
     g.act[o] = 0;
     return;
   }
@@ -52,7 +52,7 @@ __global__ void k_init_qstate(Geom g) {
   s.done = 0;
   s.fallback = 0;
   s.rounds = 0;
-  s.draws = g.n;  // one initial draw per arm
+  s.draws = 0;  // tallied at the end (k_tally)
   s.nexact = 0;
   s.blocks = 0;
   g.qs[qi] = s;
@@ -128,93 +128,145 @@ __global__ void __launch_bounds__(SEL_NT) k_select(Geom g, int nbits) {
 // ---------------------------------------------------------------------------
 // a8: blocker filter.  Active = {C: U > B} u {F: L < A} u {M: alpha > alpha_d2}
 // minus exact arms; an active arm with 2T >= d goes exact.
+//
+// One CTA per block of FIL_ROWS queries x FIL_NT * 4 arms: each thread owns 4
+// consecutive arms and walks the block's query rows (the next row's state is loaded
+// before the current one is decided).  Per CTA: one global atomic per action slot
+// (the list plan), and -- with tiles on -- the exact draw count of every (R x P)
+// tile it covers (R | FIL_ROWS, P | FIL_NT * 4: each tile lies in one CTA), written
+// with a plain store.
 constexpr int FIL_NT = 256;
+constexpr int FIL_ROWS = 32;
 
-__global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
-  const int qi = blockIdx.y;
-  const QState st = g.qs[qi];
+// The round's blocker predicate as integer thresholds (see THR_STRIDE): one warp per
+// undecided query, lane c bisects S in [0, 65025 * 2^c] with the very fp64 operations
+// the predicate is defined by (dhat_of, __dadd_rn / __dsub_rn, P:118-138 estimates and
+// radii; R15), so the integer test decides every arm identically.
+__global__ void __launch_bounds__(128) k_thresholds(Geom g) {
+  const int qi = blockIdx.x * 4 + (threadIdx.x >> 5);
+  const int c = lane_id();
+  if (qi >= g.q) return;
+  const QState &st = g.qs[qi];
   if (st.done) return;
-  const int i0 = (blockIdx.x * FIL_NT + threadIdx.x) * 4;
-  __shared__ unsigned scnt[NSLOT];
-  __shared__ unsigned long long sdraw, sexact, sblk;
-  for (int s = threadIdx.x; s < NSLOT; s += FIL_NT) scnt[s] = 0;
-  if (threadIdx.x == 0) sdraw = sexact = sblk = 0;
-  __syncthreads();
-  unsigned long long mydraw = 0, myexact = 0, myblk = 0;
-  uint32_t actw = 0;
-  if (i0 < g.npad) {
-    if (i0 < g.n) {
-      const Arm4 a = load_arm4(g, qi, i0);
-#pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int i = i0 + e;
-        uint8_t act = 0;
-        if (i < g.n && a.l[e] != LVL_EXACT) {
-          const unsigned long long key = arm_key(a.S[e], a.l[e], (uint32_t)i, g);
-          const double dh = dhat_of(a.S[e], a.l[e], g.d);
-          const double al = alpha_of(a.l[e], g.alpha);
-          bool blk;
-          if (key <= st.thr_k)
-            blk = __dadd_rn(dh, al) > st.B;
-          else if (key <= st.thr_kh)
-            blk = al > st.a_d2;
-          else
-            blk = __dsub_rn(dh, al) < st.A;
-          if (blk) {
-            if ((2u << a.l[e]) >= (unsigned)g.d) {
-              act = ACT_EXACT;
-              myexact += 1;
-            } else {
-              act = (uint8_t)(a.l[e] + 1);
-              mydraw += 1ull << a.l[e];
-              myblk += a.l[e] < 2 ? 1ull : (1ull << (a.l[e] - 2));  // Philox blocks
-            }
-          }
-        }
-        actw |= (uint32_t)act << (8 * e);
-      }
+  int32_t *t = g.thr + (size_t)qi * THR_STRIDE;
+  bool mbit = false;
+  if (c < MAX_LEVELS && c <= g.cmax) {
+    const uint8_t l = (uint8_t)c;
+    const double al = alpha_of(l, g.alpha);
+    const int32_t smax = (int32_t)(65025u << c);  // every draw (a - b)^2 <= 255^2
+    // Su: first S with U(S) > B (smax + 1: none)
+    int32_t lo = 0, hi = smax + 1;
+    while (lo < hi) {
+      const int32_t mid = lo + ((hi - lo) >> 1);
+      if (__dadd_rn(dhat_of(mid, l, g.d), al) > st.B) hi = mid; else lo = mid + 1;
     }
-    *reinterpret_cast<uint32_t *>(g.act + (size_t)qi * g.npad + i0) = actw;
+    t[c] = lo;
+    // Sl: first S with L(S) >= A (blocker iff S < Sl)
+    lo = 0;
+    hi = smax + 1;
+    while (lo < hi) {
+      const int32_t mid = lo + ((hi - lo) >> 1);
+      if (!(__dsub_rn(dhat_of(mid, l, g.d), al) < st.A)) hi = mid; else lo = mid + 1;
+    }
+    t[MAX_LEVELS + c] = lo;
+    mbit = al > st.a_d2;
   }
-  if (g.exact_mma) {
-    // a warp's 128 arms lie in one 256-point tile: flag it for the tensor-core pass
-    bool ex = false;
-#pragma unroll
-    for (int e = 0; e < 4; ++e) ex |= (uint8_t)(actw >> (8 * e)) == ACT_EXACT;
-    if (__any_sync(FULL, ex) && lane_id() == 0)
-      g.xflags[(size_t)(qi >> 7) * g.xf_cols + (i0 >> 8)] = 1u;
-  }
+  const unsigned m = __ballot_sync(FULL, mbit);
+  if (c == 0) t[2 * MAX_LEVELS] = (int32_t)m;
+}
+
+cudaError_t launch_thresholds(const Geom &g, cudaStream_t s) {
+  k_thresholds<<<(unsigned)((g.q + 3) / 4), 128, 0, s>>>(g);
+  return cudaGetLastError();
+}
+
+__device__ __forceinline__ uint32_t filter_arms(const Geom &g, const QState &st, const int32_t *thr, const Arm4 &a,
+                                                int i0, uint32_t *draws) {
+  uint32_t actw = 0, dr = 0;
+  const uint32_t mmask = (uint32_t)__ldg(thr + 2 * MAX_LEVELS);
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const uint8_t act = (uint8_t)(actw >> (8 * e));
-    const unsigned slot = act == 0 ? NONE : (act == ACT_EXACT ? (unsigned)MAX_LEVELS : act - 1u);
-    hist_add(scnt, slot);
+    const int i = i0 + e;
+    const uint8_t l = a.l[e];
+    uint8_t act = 0;
+    if (i < g.n && !lvl_exact(l)) {
+      const unsigned long long key = arm_key(a.S[e], l, (uint32_t)i, g);
+      bool blk;
+      if (key <= st.thr_k)
+        blk = a.S[e] >= __ldg(thr + l);               // U > B
+      else if (key <= st.thr_kh)
+        blk = (mmask >> l) & 1u;                       // alpha > alpha_d2
+      else
+        blk = a.S[e] < __ldg(thr + MAX_LEVELS + l);   // L < A
+      if (blk) {
+        if ((2u << l) >= (unsigned)g.d) {
+          act = ACT_EXACT;
+        } else {
+          act = (uint8_t)(l + 1);
+          dr += 1u << l;
+        }
+      }
+    }
+    actw |= (uint32_t)act << (8 * e);
   }
-  if (g.tile_on) {
-    // per-tile draws of the sampled blockers: the P/4 lanes of a tile segment add up
-    uint32_t v = (uint32_t)mydraw;
-    const int seg = min(32, (1 << g.tile_lp) >> 2);
-    for (int o = 1; o < seg; o <<= 1) v += __shfl_xor_sync(FULL, v, o);
-    if ((lane_id() & (seg - 1)) == 0 && v)
-      atomicAdd(&g.tilework[(size_t)(qi >> g.tile_lr) * g.tile_cols + (i0 >> g.tile_lp)], v);
-  }
+  *draws = dr;
+  return actw;
+}
+
+__global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
+  extern __shared__ uint32_t tcnt[];  // [FIL_ROWS / R][FIL_NT * 4 / P] (tiles on)
+  __shared__ unsigned scnt[NSLOT];
+  const int q0 = blockIdx.y * FIL_ROWS;
+  const int rows = min(FIL_ROWS, g.q - q0);
+  const int i0 = (blockIdx.x * FIL_NT + threadIdx.x) * 4;
+  const int lane = lane_id();
+  const int tcols = g.tile_on ? (FIL_NT * 4) >> g.tile_lp : 0;
+  const int ntc = g.tile_on ? (FIL_ROWS >> g.tile_lr) * tcols : 0;
+  for (int s = threadIdx.x; s < NSLOT; s += FIL_NT) scnt[s] = 0;
+  for (int t = threadIdx.x; t < ntc; t += FIL_NT) tcnt[t] = 0;
+  __syncthreads();
+  const bool arms = i0 < g.n;
+  QState st = g.qs[q0];
+  Arm4 a{};
+  if (arms) a = load_arm4(g, q0, i0);
+  for (int r = 0; r < rows; ++r) {
+    const int qi = q0 + r;
+    const QState cur = st;
+    const Arm4 ca = a;
+    if (r + 1 < rows) {  // prefetch the next row
+      st = g.qs[qi + 1];
+      if (arms) a = load_arm4(g, qi + 1, i0);
+    }
+    if (cur.done) continue;  // uniform: one query row at a time
+    uint32_t dr = 0, actw = 0;
+    if (arms) actw = filter_arms(g, cur, g.thr + (size_t)qi * THR_STRIDE, ca, i0, &dr);
+    if (i0 < g.npad) *reinterpret_cast<uint32_t *>(g.act + (size_t)qi * g.npad + i0) = actw;
+    bool ex = false;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    mydraw += __shfl_xor_sync(FULL, mydraw, o);
-    myblk += __shfl_xor_sync(FULL, myblk, o);
-    myexact += __shfl_xor_sync(FULL, myexact, o);
-  }
-  if (lane_id() == 0 && (mydraw | myexact)) {
-    atomicAdd(&sdraw, mydraw);
-    atomicAdd(&sblk, myblk);
-    atomicAdd(&sexact, myexact);
+    for (int e = 0; e < 4; ++e) {
+      const uint8_t act = (uint8_t)(actw >> (8 * e));
+      ex |= act == ACT_EXACT;
+      hist_add(scnt, act == 0 ? NONE : (act == ACT_EXACT ? (unsigned)MAX_LEVELS : act - 1u));
+    }
+    if (g.exact_mma && __any_sync(FULL, ex) && lane == 0)
+      // a warp's 128 arms lie in one 256-point tile: flag it for the tensor-core pass
+      g.xflags[(size_t)(qi >> 7) * g.xf_cols + (i0 >> 8)] = 1u;
+    if (g.tile_on) {
+      // the P/4 lanes of a tile segment add up their sampled draws
+      const int seg = min(32, (1 << g.tile_lp) >> 2);
+      uint32_t v = dr;
+      for (int o = 1; o < seg; o <<= 1) v += __shfl_xor_sync(FULL, v, o);
+      if ((lane & (seg - 1)) == 0 && v)
+        atomicAdd(&tcnt[(r >> g.tile_lr) * tcols + ((threadIdx.x * 4) >> g.tile_lp)], v);
+    }
   }
   __syncthreads();
   if (threadIdx.x < NSLOT && scnt[threadIdx.x]) atomicAdd(&g.ctl->cnt[threadIdx.x], scnt[threadIdx.x]);
-  if (threadIdx.x == 0 && (sdraw | sexact)) {
-    atomicAdd(reinterpret_cast<unsigned long long *>(&g.qs[qi].draws), sdraw);
-    atomicAdd(reinterpret_cast<unsigned long long *>(&g.qs[qi].blocks), sblk);
-    atomicAdd(reinterpret_cast<unsigned long long *>(&g.qs[qi].nexact), sexact);
+  // every tile of this CTA, including those of finished queries (count 0)
+  for (int t = threadIdx.x; t < ntc; t += FIL_NT) {
+    const int tr = (q0 >> g.tile_lr) + t / tcols;
+    const int tc = ((blockIdx.x * FIL_NT * 4) >> g.tile_lp) + t % tcols;
+    if ((tr << g.tile_lr) < g.q && tc < g.tile_cols) g.tilework[(size_t)tr * g.tile_cols + tc] = tcnt[t];
   }
 }
 
@@ -299,7 +351,7 @@ __global__ void __launch_bounds__(FIL_NT) k_scatter(Geom g) {
     const uint8_t act = i < g.n ? arow[i] : (uint8_t)0;
     slot[e] = act == 0 ? NONE : (act == ACT_EXACT ? (unsigned)MAX_LEVELS : act - 1u);
     if (g.tile_on && slot[e] < (unsigned)MAX_LEVELS &&
-        g.tilework[(size_t)(qi >> g.tile_lr) * g.tile_cols + (i >> g.tile_lp)] >= g.tile_min)
+        (float)g.tilework[(size_t)(qi >> g.tile_lr) * g.tile_cols + (i >> g.tile_lp)] >= g.tile_row_draws * (float)((1 << g.tile_lr) + (1 << g.tile_lp)))
       slot[e] = NONE;  // k_advance_tiles takes it
     const unsigned m = __match_any_sync(FULL, slot[e]);
     const int leader = __ffs(m) - 1;
@@ -438,7 +490,7 @@ __device__ __forceinline__ void exact_rows(const Geom &g, const uint32_t *codes,
     decode(g, codes[lane], imask, qi, i);
     const size_t o = (size_t)qi * g.npad + i;
     g.S[o] = (int32_t)mine;
-    g.lvl[o] = LVL_EXACT;
+    g.lvl[o] = lvl_to_exact(g.lvl[o]);
   }
 }
 
@@ -653,6 +705,52 @@ __global__ void __launch_bounds__(OUT_NT) k_output(Geom g, OutPtrs o) {
   }
 }
 
+// Per-query counters from the final arm states (SPEC S:250-258 accounting): an arm
+// at sampled level c drew 2^c coordinates (1 at initialisation, then 1 + 2 + ...);
+// an exact arm drew 2^c before its fallback, which is charged d (d = 1: exact at
+// initialisation, no fallback).  Philox blocks of the level gathers: level c used
+// max(1, 2^(c-2)) per advance.
+__global__ void __launch_bounds__(256) k_tally(Geom g) {
+  const int qi = blockIdx.x;
+  unsigned long long dr = 0, ex = 0, bl = 0;
+  const uint8_t *lrow = g.lvl + (size_t)qi * g.npad;
+  for (int i = threadIdx.x; i < g.n; i += blockDim.x) {
+    const uint8_t l = lrow[i];
+    const uint32_t c = l & 0x7Fu;
+    dr += 1ull << c;
+    ex += (lvl_exact(l) && g.d > 1) ? 1u : 0u;
+    bl += c == 0 ? 0ull : (c == 1 ? 1ull : (1ull << (c - 2)) + 1ull);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    dr += __shfl_xor_sync(FULL, dr, o);
+    ex += __shfl_xor_sync(FULL, ex, o);
+    bl += __shfl_xor_sync(FULL, bl, o);
+  }
+  __shared__ unsigned long long red[3][8];
+  if (lane_id() == 0) {
+    red[0][threadIdx.x >> 5] = dr;
+    red[1][threadIdx.x >> 5] = ex;
+    red[2][threadIdx.x >> 5] = bl;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    for (int w = 1; w < 8; ++w) {
+      dr += red[0][w];
+      ex += red[1][w];
+      bl += red[2][w];
+    }
+    g.qs[qi].draws = (long long)dr;
+    g.qs[qi].nexact = (long long)ex;
+    g.qs[qi].blocks = (long long)bl;
+  }
+}
+
+cudaError_t launch_tally(const Geom &g, cudaStream_t s) {
+  k_tally<<<g.q, 256, 0, s>>>(g);
+  return cudaGetLastError();
+}
+
 __global__ void k_counts(Geom g, OutPtrs o) {
   const int qi = blockIdx.y;
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -660,7 +758,7 @@ __global__ void k_counts(Geom g, OutPtrs o) {
   const size_t src = (size_t)qi * g.npad + i;
   const size_t dst = (size_t)(o.row0 + qi) * o.ncols + o.col0 + i;
   const uint8_t l = g.lvl[src];
-  if (o.counts) o.counts[dst] = (l == LVL_EXACT) ? g.d : (int32_t)(1u << l);
+  if (o.counts) o.counts[dst] = lvl_exact(l) ? g.d : (int32_t)(1u << l);
   if (o.sums) o.sums[dst] = (int64_t)(uint32_t)g.S[src];
 }
 
@@ -671,14 +769,14 @@ static inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b
 cudaError_t launch_init(const Geom &g, cudaStream_t s) {
   k_init<<<dim3(cdiv(g.npad, 256), g.q), 256, 0, s>>>(g);
   k_init_qstate<<<cdiv(g.q, 128), 128, 0, s>>>(g);
-  if (g.exact_mma) {
-    cudaError_t e = cudaMemsetAsync(g.xflags, 0, sizeof(uint32_t) * (size_t)cdiv(g.q, 128) * g.xf_cols, s);
-    if (e == cudaSuccess) e = launch_row_norms(g.Q, g.pitch, g.q, g.nq, s);
-    if (e != cudaSuccess) return e;
-  }
   if (g.tile_on) {
     const size_t rows = ((size_t)g.q + (1u << g.tile_lr) - 1) >> g.tile_lr;
     const cudaError_t e = cudaMemsetAsync(g.tilework, 0, sizeof(uint32_t) * rows * g.tile_cols, s);
+    if (e != cudaSuccess) return e;
+  }
+  if (g.exact_mma) {
+    cudaError_t e = cudaMemsetAsync(g.xflags, 0, sizeof(uint32_t) * (size_t)cdiv(g.q, 128) * g.xf_cols, s);
+    if (e == cudaSuccess) e = launch_row_norms(g.Q, g.pitch, g.q, g.nq, s);
     if (e != cudaSuccess) return e;
   }
   return cudaGetLastError();
@@ -688,11 +786,16 @@ cudaError_t launch_select(const Geom &g, int nbits, cudaStream_t s) {
   const cudaError_t e = launch_select_pivot(g, s);
   if (e != cudaSuccess) return e;
   k_select<<<g.q, SEL_NT, 0, s>>>(g, nbits);
-  return cudaGetLastError();
+  return launch_thresholds(g, s);
 }
 
 cudaError_t launch_filter(const Geom &g, cudaStream_t s) {
-  k_filter<<<dim3(cdiv(g.npad, FIL_NT * 4), g.q), FIL_NT, 0, s>>>(g);
+  const size_t smem = g.tile_on ? sizeof(uint32_t) * (size_t)(FIL_ROWS >> g.tile_lr) * ((FIL_NT * 4) >> g.tile_lp) : 0;
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(k_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_filter<<<dim3(cdiv(g.npad, FIL_NT * 4), cdiv(g.q, FIL_ROWS)), FIL_NT, smem, s>>>(g);
   return cudaGetLastError();
 }
 
@@ -739,6 +842,8 @@ int stage_level(int64_t pitch) {
 }
 
 cudaError_t launch_output(const Geom &g, const OutPtrs &o, cudaStream_t s) {
+  const cudaError_t te = launch_tally(g, s);
+  if (te != cudaSuccess) return te;
   const int kh = g.k + g.h;
   const size_t smem = (size_t)kh * (8 + 4 + 4 + 1);
   k_output<<<g.q, OUT_NT, smem, s>>>(g, o);
@@ -779,8 +884,8 @@ cudaError_t launch_ctl_reset(RoundCtl *ctl, unsigned q, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_zero_round(RoundCtl *ctl, cudaStream_t s) {
-  k_zero_round<<<1, 128, 0, s>>>(ctl);
+cudaError_t launch_zero_round(const Geom &g, cudaStream_t s) {
+  k_zero_round<<<1, 128, 0, s>>>(g.ctl);
   return cudaGetLastError();
 }
 

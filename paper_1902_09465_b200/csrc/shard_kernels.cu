@@ -196,7 +196,7 @@ __global__ void k_counts_sharded(Geom g, OutPtrs o) {
   const size_t src = (size_t)qi * g.npad + i;
   const size_t dst = (size_t)(o.row0 + qi) * o.ncols + o.col0 + i;
   const uint8_t l = g.lvl[src];
-  if (o.counts) o.counts[dst] = (l == LVL_EXACT) ? g.d : (int32_t)(1u << l);
+  if (o.counts) o.counts[dst] = lvl_exact(l) ? g.d : (int32_t)(1u << l);
   if (o.sums) o.sums[dst] = (int64_t)(uint32_t)g.S[src];
 }
 
@@ -220,6 +220,8 @@ cudaError_t launch_merge(const Geom &g, const OutPtrs &o, cudaStream_t s) {
 }
 
 cudaError_t launch_output_sharded(const Geom &g, const OutPtrs &o, cudaStream_t s) {
+  const cudaError_t te = launch_tally(g, s);
+  if (te != cudaSuccess) return te;
   k_counters_sharded<<<cdiv(g.q, 128), 128, 0, s>>>(g, o);
   if (o.counts || o.sums) k_counts_sharded<<<dim3(cdiv(g.n, 256), g.q), 256, 0, s>>>(g, o);
   return cudaGetLastError();
