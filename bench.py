@@ -252,13 +252,16 @@ def _algorithmic_bytes(st: dict, n: int, d: int, q: int) -> dict:
         "select": st["query_rounds"] * n * 5,
         "filter": st["blocked_query_rounds"] * n * 6,
         "compact": st["blocked_query_rounds"] * n + st["active_pair_rounds"] * 4,
-        "advance": (st["draws"] - init_draws) * SECTOR + st["exact_fallbacks"] * d
-        + st["active_pair_rounds"] * 13,
+        # list path + exact fallbacks: sampled draws outside the tiles at one sector each
+        "advance": max(0, st["philox_blocks"] - st["tile_blocks"]) * 4 * SECTOR + st["exact_fallbacks"] * d,
+        # tiles stage rows (R + P) * pitch per dense tile: ALU-bound, no byte model here
+        "tiles": 0,
     }
 
 
-KERNEL_OF = {"init": "k_init", "select": "k_select", "filter": "k_filter",
-             "compact": "k_scatter", "advance": "k_advance", "output": "k_output"}
+KERNEL_OF = {"init": "k_init", "select": "k_select_pivot", "filter": "k_filter",
+             "compact": "k_scatter", "advance": "k_advance", "tiles": "k_advance_tiles",
+             "output": "k_output"}
 
 
 # ----------------------------------------------------------------------------- oracle legs
@@ -421,7 +424,7 @@ def run_ours(args, dist: Dist):
     agg = {key: sum(s[key] for s in stats) for key in stats[0]}
     draws = agg["draws"]
     evals_total = int(out["evals"].sum().item()) * args.steps
-    classes = ["init", "select", "filter", "compact", "advance", "output"]
+    classes = ["init", "select", "filter", "compact", "advance", "tiles", "output"]
     ms_cls = {c: agg[f"ms_{c}"] for c in classes}
     launches = {c: agg[f"launches_{c}"] for c in classes}
     abytes = {c: 0 for c in classes}
@@ -432,7 +435,7 @@ def run_ours(args, dist: Dist):
     peak, peak_src = _peaks()
     probes = _measure_probes(d, n * cfg.d)
     blocks = agg.get("philox_blocks", 0)
-    adv_draws = agg["draws"] - args.steps * qpr * n  # level-gather draws (init excluded)
+    adv_draws = max(0, blocks - agg.get("tile_blocks", 0)) * 4  # list-path level-gather draws
     x_in_l2 = n * d <= L2_BYTES * 0.8
     common = {"kernel": KERNEL_OF[dom], "launches": launches[dom],
               "avg_launch_ms": ms_cls[dom] / max(1, launches[dom]),
@@ -453,16 +456,29 @@ def run_ours(args, dist: Dist):
         "frac_of_measured_random_sector_rate": (adv_draws / adv_s) / probes["gather_loads_per_s"]
         if adv_s > 0 and probes.get("gather_loads_per_s") else None,
         "x_footprint_bytes": n * d, "x_l2_resident": x_in_l2}
-    if dom == "advance" and x_in_l2 and probes.get("philox_blocks_per_s"):
-        # X fits the 126 MB L2: the sampled levels are bound by the integer pipe running
-        # Philox4x32-10 (ncu: fma-heavy pipe busiest), not by memory
-        ach = blocks / adv_s / 1e9
+    tile_blocks = agg.get("tile_blocks", 0)
+    if dom == "tiles" and probes.get("philox_blocks_per_s"):
+        # dense tiles gather from shared memory: the sampled draws are bound by the
+        # integer pipes running Philox4x32-10 (ncu: fma-heavy + LDS wavefronts), not by
+        # memory
+        ts = ms_cls["tiles"] / 1e3
+        ach = tile_blocks / ts / 1e9
         pk = probes["philox_blocks_per_s"] / 1e9
         roofline = {"bound": "alu", "achieved": ach, "peak": pk, "unit": "G Philox blocks/s",
                     "frac": ach / pk,
                     "peak_source": "measured in this run: tools/probes.cu k_probe_philox "
                                    "(Philox4x32-10 + multiply-high map, no memory)",
-                    "algorithmic_units_per_launch": blocks / max(1, launches[dom]),
+                    "algorithmic_units_per_launch": tile_blocks / max(1, launches[dom]),
+                    "sector_view": sector_view, **common}
+    elif dom == "advance" and x_in_l2 and probes.get("philox_blocks_per_s"):
+        # X fits the 126 MB L2: the list-path levels are bound by the integer pipe
+        ach = (blocks - tile_blocks) / adv_s / 1e9
+        pk = probes["philox_blocks_per_s"] / 1e9
+        roofline = {"bound": "alu", "achieved": ach, "peak": pk, "unit": "G Philox blocks/s",
+                    "frac": ach / pk,
+                    "peak_source": "measured in this run: tools/probes.cu k_probe_philox "
+                                   "(Philox4x32-10 + multiply-high map, no memory)",
+                    "algorithmic_units_per_launch": (blocks - tile_blocks) / max(1, launches[dom]),
                     "sector_view": sector_view, **common}
     else:
         achieved = abytes.get(dom, 0) / (ms_cls[dom] / 1e3) / 1e9 if ms_cls[dom] > 0 else 0.0

@@ -93,7 +93,8 @@ typedef struct {
 /* Execution statistics of the last query call on an index (aknn_get_stats).
  * Kernel classes: init (a2), select (a6-a7: rank split, bounds, Eq. 5),
  * filter (a8 blocker predicate), compact (a8 list plan + scatter), advance
- * (a3-a4 level gathers and exact fallbacks), output (a9).  ms_* are device
+ * (a3-a4 list-path level gathers and exact fallbacks), tiles (a3 level gathers
+ * of dense tiles from shared memory), output (a9).  ms_* are device
  * times from CUDA events recorded on the launching stream around every
  * launch of that class (timing = 1 only; events are read after the call's
  * final synchronisation, so timing adds no host round trips).              */
@@ -117,6 +118,10 @@ typedef struct {
   int32_t graph_builds;       /* round-loop graphs captured + instantiated by
                                  this call (0 when the cached graph was reused) */
   int32_t pad0;
+  double ms_tiles;            /* device time of the shared-memory tile gathers
+                                 (k_advance_tiles; part of the advance rows a3)  */
+  int64_t launches_tiles;
+  int64_t tile_blocks;        /* Philox blocks drawn by the tile gathers        */
 } aknn_stats;
 
 /* ------------------------------------------------------------------------ */

@@ -80,6 +80,7 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
   const uint32_t d = (uint32_t)g.d;
   const unsigned ntiles = g.ctl->n_tiles;
 
+  unsigned long long my_blocks = 0;  // Philox blocks drawn (statistics)
   for (unsigned ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
     const uint32_t t = g.tilelist[ti];
     const int tp = (int)(t / (unsigned)rows), tr = (int)(t % (unsigned)rows);
@@ -138,6 +139,8 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
     // reduce inside the lane group; every pair's sum is written by one thread.
     unsigned lmask = 0;  // levels present in the tile
     for (int c = 0; c < MAX_LEVELS; ++c) lmask |= (lcnt[c] != 0u) << c;
+    if (tid == 0)
+      for (int c = 0; c < MAX_LEVELS; ++c) my_blocks += (unsigned long long)lcnt[c] << (c < 2 ? 0 : c - 2);
     for (; lmask; lmask &= lmask - 1) {
       const int c = __ffs(lmask) - 1;
       const unsigned m = lcnt[c];
@@ -219,6 +222,7 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
       }
     }
   }
+  if (threadIdx.x == 0 && my_blocks) atomicAdd(&g.ctl->tile_blocks, my_blocks);
 }
 
 // The dense tiles of this round (tilework >= tile_row_draws * (R + P)) in point-major

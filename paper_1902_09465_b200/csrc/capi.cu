@@ -310,8 +310,9 @@ void setup_tiles(Geom &g, const TileShape &t, const aknn_opts &o, int64_t qb, ui
 }
 
 // One round after the rank split: filter -> plan/scatter (+ dense-tile list) ->
-// advance (tensor-core exact fallbacks, dense tiles, list levels).  timer(k): per-class
-// event brackets of the host-driven loop (0 start, 1 filter, 2 compact, 3 advance).
+// advance (tensor-core exact fallbacks, list levels) -> dense tiles.  timer(k): per-class
+// event brackets of the host-driven loop (0 start, 1 filter, 2 compact, 3 advance,
+// 4 tiles).
 template <class Timer>
 cudaError_t launch_round_body(const Geom &g, int num_sms, cudaStream_t st, Timer &&timer) {
   timer(0);
@@ -321,6 +322,8 @@ cudaError_t launch_round_body(const Geom &g, int num_sms, cudaStream_t st, Timer
   timer(2);
   if (e == cudaSuccess) e = launch_advance(g, num_sms, st);
   timer(3);
+  if (e == cudaSuccess && g.tile_on) e = launch_advance_tiles(g, num_sms, st);
+  timer(4);
   return e;
 }
 
@@ -398,7 +401,7 @@ cudaError_t sync_spin(cudaStream_t st) {
 
 // Per-launch CUDA events on the launching stream, read after the call's final
 // synchronisation (no extra host round trips).  Events are pooled per index.
-enum Phase { PH_INIT = 0, PH_SELECT, PH_FILTER, PH_COMPACT, PH_ADVANCE, PH_OUTPUT, PH_ALL, PH_N };
+enum Phase { PH_INIT = 0, PH_SELECT, PH_FILTER, PH_COMPACT, PH_ADVANCE, PH_TILES, PH_OUTPUT, PH_ALL, PH_N };
 
 struct PhaseTimer {
   bool on;
@@ -517,7 +520,7 @@ int launches_init_of(const Geom &g) { return 2 + (g.exact_mma ? 1 : 0); }  // in
 int launches_filter_of(const Geom &) { return 1; }
 int launches_compact_of(const Geom &g) { return 2 + (g.tile_on ? 2 : 0); }  // plan, scatter (+ lists)
 int launches_advance_of(const Geom &g) {
-  return 1 + (g.tile_on ? 1 : 0) + (g.exact_mma ? 1 : 0) + (g.stage_lo < MAX_LEVELS ? 1 : 0);
+  return 1 + (g.exact_mma ? 1 : 0) + (g.stage_lo < MAX_LEVELS ? 1 : 0);
 }
 int launches_output_of(const OutPtrs &o) { return 2 + ((o.counts || o.sums) ? 1 : 0); }  // tally, output
 
@@ -534,10 +537,12 @@ void fold_batch_stats(aknn_stats &stats, const RoundCtl &ctl_h, const QState *qs
     stats.launches_filter += launches_filter_of(g) * (r - 1);
     stats.launches_compact += launches_compact_of(g) * (r - 1);
     stats.launches_advance += (launches_advance_of(g) + 1) * (r - 1);  // + counter reset
+    stats.launches_tiles += (g.tile_on ? 1 : 0) * (r - 1);
     if (ctl_h.n_active > 0 && status) *status = AKNN_EMAXROUNDS;
   }
   if (r > stats.rounds) stats.rounds = r;
   stats.active_pair_rounds += (int64_t)ctl_h.advanced;
+  stats.tile_blocks += (int64_t)ctl_h.tile_blocks;
   for (int a = 0; a < qn; ++a) {
     stats.draws += qs[a].draws;
     stats.exact_fallbacks += qs[a].nexact;
@@ -547,7 +552,8 @@ void fold_batch_stats(aknn_stats &stats, const RoundCtl &ctl_h, const QState *qs
 
 void total_launches(aknn_stats &stats) {
   stats.kernel_launches = stats.launches_init + stats.launches_select + stats.launches_filter +
-                          stats.launches_compact + stats.launches_advance + stats.launches_output;
+                          stats.launches_compact + stats.launches_advance + stats.launches_tiles +
+                          stats.launches_output;
 }
 
 // Completes the statistics of a deferred aknn_query_async call (waits for its copies).
@@ -733,10 +739,14 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
         } else if (k == 2) {
           tm.stop(PH_COMPACT);
           tm.start();
-        } else {
+        } else if (k == 3) {
           tm.stop(PH_ADVANCE);
+          tm.start();
+        } else {
+          tm.stop(PH_TILES);
         }
       }));
+      stats.launches_tiles += g.tile_on ? 1 : 0;
       stats.launches_filter += launches_filter_of(g);
       stats.launches_compact += launches_compact_of(g);
       stats.launches_advance += launches_advance_of(g);
@@ -777,6 +787,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   stats.ms_filter = ms[PH_FILTER];
   stats.ms_compact = ms[PH_COMPACT];
   stats.ms_advance = ms[PH_ADVANCE];
+  stats.ms_tiles = ms[PH_TILES];
   stats.ms_output = ms[PH_OUTPUT];
   stats.ms_total = ms[PH_ALL];
   total_launches(stats);
@@ -984,6 +995,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
       stats.launches_filter += launches_filter_of(G[0]) * (int)nS;
       stats.launches_compact += launches_compact_of(G[0]) * (int)nS;
       stats.launches_advance += launches_advance_of(G[0]) * (int)nS;
+      stats.launches_tiles += (G[0].tile_on ? 1 : 0) * (int)nS;
       if (r > 1 + 64 * 64) return fail(AKNN_ECUDA, "round loop did not terminate (internal error)");
     }
     if (r > stats.rounds) stats.rounds = r;
@@ -1010,6 +1022,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
       const RoundCtl &ctl_h = *h_ctl;
       const QState *qs = h_qs;
       stats.active_pair_rounds += (int64_t)ctl_h.advanced;
+      stats.tile_blocks += (int64_t)ctl_h.tile_blocks;
       for (int a = 0; a < qn; ++a) {
         stats.draws += qs[a].draws;
         stats.exact_fallbacks += qs[a].nexact;
@@ -1028,10 +1041,12 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
   stats.ms_filter = ms[PH_FILTER];
   stats.ms_compact = ms[PH_COMPACT];
   stats.ms_advance = ms[PH_ADVANCE];
+  stats.ms_tiles = ms[PH_TILES];
   stats.ms_output = ms[PH_OUTPUT];
   stats.ms_total = ms[PH_ALL];
   stats.kernel_launches = stats.launches_init + stats.launches_select + stats.launches_filter +
-                          stats.launches_compact + stats.launches_advance + stats.launches_output;
+                          stats.launches_compact + stats.launches_advance + stats.launches_tiles +
+                          stats.launches_output;
   ix0->stats = stats;
   CU(cudaGetLastError());
   return status;

@@ -810,13 +810,11 @@ cudaError_t launch_compact(const Geom &g, cudaStream_t s) {
   return cudaGetLastError();
 }
 
+// The list-path advance (and the tensor-core exact fallbacks); the dense tiles are
+// launch_advance_tiles.
 cudaError_t launch_advance(const Geom &g, int num_sms, cudaStream_t s) {
   if (g.exact_mma) {
     const cudaError_t e = launch_exact_fallback_mma(g, s);
-    if (e != cudaSuccess) return e;
-  }
-  if (g.tile_on) {
-    const cudaError_t e = launch_advance_tiles(g, num_sms, s);
     if (e != cudaSuccess) return e;
   }
   k_advance<<<num_sms * 8, ADV_NT, 0, s>>>(g);

@@ -18,7 +18,16 @@ KEY = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum"
        "smsp__inst_executed.sum", "launch__registers_per_thread", "launch__grid_size",
        "launch__block_size", "launch__occupancy_limit_registers",
        "sm__pipe_tensor_subpipe_imma_cycles_active.avg.pct_of_peak_sustained_active",
-       "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active"]
+       "sm__inst_executed_pipe_uniform.avg.pct_of_peak_sustained_active",
+       "sm__pipe_fmaheavy_cycles_active.avg.pct_of_peak_sustained_elapsed",
+       "sm__pipe_alu_cycles_active.avg.pct_of_peak_sustained_active",
+       "l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed",
+       "l1tex__data_bank_conflicts_pipe_lsu_mem_shared_op_ld.sum",
+       "launch__occupancy_limit_shared_mem",
+       "smsp__average_warps_issue_stalled_math_pipe_throttle_per_issue_active.ratio",
+       "smsp__average_warps_issue_stalled_short_scoreboard_per_issue_active.ratio",
+       "smsp__average_warps_issue_stalled_wait_per_issue_active.ratio",
+       "smsp__average_warps_issue_stalled_barrier_per_issue_active.ratio"]
 
 SCALE = {"nsecond": 1e-3, "ns": 1e-3, "usecond": 1.0, "us": 1.0, "msecond": 1e3, "ms": 1e3, "second": 1e6, "s": 1e6}
 
