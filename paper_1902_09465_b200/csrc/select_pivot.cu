@@ -3,14 +3,16 @@
 //
 // Only the k+h smallest composite keys matter (the split C | M | F).  Per undecided
 // query (one CTA):
-//   1. sample SS keys at fixed strided positions, bitonic-sort them, and take the
-//      sample key of rank r_s (about twice the expected rank of k+h in the sample,
-//      plus 16) as a pivot tau;
+//   1. sample SS keys at fixed strided positions and take the (r_s+1)-th smallest as a
+//      pivot tau (r_s+1 = twice the expected sample rank of k+h, plus 4), found by
+//      r_s+1 rounds of block-wide arg-min over the samples held in registers;
 //   2. ONE pass over the n arms: keys <= tau go to a shared-memory buffer, and every
-//      other arm feeds a running arg-min of L = d_hat - alpha (ties: smaller id);
-//   3. sort the buffer: ranks k and k+h are exact (keys are unique), A / d1 come
-//      from the first k entries, B / d2 = min(outside arg-min, buffer entries
-//      ranked > k+h), then Eq. (5).
+//      other arm feeds a running arg-min of L = d_hat - alpha (ties: smaller id),
+//      screened in fp32 so that only arms that can beat the running minimum pay the
+//      fp64 division;
+//   3. rank the buffer (by counting when small, else bitonic sort): ranks k and k+h
+//      are exact (keys are unique), A / d1 come from the k smallest, B / d2 =
+//      min(outside arg-min, buffer entries ranked > k+h), then Eq. (5).
 // If the buffer holds fewer than k+h keys or overflows (tau too small or too
 // large; rare), the query is flagged and the multi-pass radix select (k_select)
 // decides it instead.  Either way the result is the exact order statistics, so
@@ -23,7 +25,8 @@
 namespace aknn {
 
 constexpr int PIV_NT = 512;
-constexpr unsigned PIV_CAP = 8192;  // buffer keys (64 KB of dynamic shared memory)
+constexpr unsigned PIV_CAP = 8192;    // buffer keys (64 KB of dynamic shared memory)
+constexpr unsigned PIV_BRUTE = 1536;  // buffers up to this size are ranked by counting
 
 __host__ __device__ __forceinline__ unsigned piv_sample_size(int n) {
   unsigned ss = 1024;
@@ -48,30 +51,71 @@ __device__ void bitonic_keys(unsigned long long *buf, unsigned P) {
     }
 }
 
-// Fills buf[0..cnt) (sorted ascending, cnt <= PIV_CAP) with every key <= tau and
-// returns the arg-min of L over the arms with key > tau.  Returns false (and the
-// caller falls back) when fewer than `need` keys are <= tau or the buffer overflows.
-__device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long long *buf,
+// fp32 screen for the arg-min of L = d_hat - alpha over the arms outside the buffer:
+// Lf = S * inv(65025 T) - alpha in fp32 differs from the fp64 L by less than
+// eps_c = (alpha_c + 2) * 2^-20 (d_hat <= 1 because every sample is <= 1; each fp32
+// rounding is a relative 2^-24), so an arm with Lf - eps_c > (best L so far) cannot be
+// the arg-min and skips the fp64 division; the rest are decided in fp64 as before.
+
+// Fills buf[0..cnt) with every key <= tau (unsorted) and rank[t] = the rank of buf[t]
+// among them (0-based; keys are unique), and returns the arg-min of L over the arms
+// with key > tau.  Returns false (and the caller falls back) when fewer than `need`
+// keys are <= tau or the buffer overflows.
+__device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long long *buf, unsigned *rank,
                            unsigned *cnt_out, RecBest *outside, RecBest *wsm) {
   __shared__ unsigned cnt;
   __shared__ unsigned long long tau_s;
-  const int tid = threadIdx.x;
+  __shared__ unsigned long long wmin[PIV_NT / 32];
+  __shared__ float invT[MAX_LEVELS + 1], alf[MAX_LEVELS + 1], epsl[MAX_LEVELS + 1];
+  const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   const int n = g.n;
+  if (tid <= MAX_LEVELS) {
+    const bool ex = tid == MAX_LEVELS;  // slot MAX_LEVELS: exact arms (T = d, alpha = 0)
+    const double T = ex ? (double)g.d : (double)(1u << tid);
+    invT[tid] = (float)(1.0 / (T * 65025.0));
+    alf[tid] = (ex || tid > g.cmax) ? 0.f : (float)g.alpha[1u << tid];
+    epsl[tid] = (alf[tid] + 2.f) * 9.5367431640625e-07f;  // 2^-20
+  }
   if (n > (int)PIV_CAP) {
+    // tau = the (rs+1)-th smallest of ss strided sample keys, rs+1 about twice the
+    // expected sample rank of need, plus 8: found by rs+1 rounds of block arg-min
     const unsigned ss = piv_sample_size(n);
-    for (unsigned j = tid; j < ss; j += PIV_NT) {
-      const int i = (int)(((unsigned long long)j * (unsigned)n) / ss);
-      const size_t o = (size_t)qi * g.npad + i;
-      buf[j] = arm_key(g.S[o], g.lvl[o], (uint32_t)i, g);
+    const unsigned per = ss / PIV_NT;  // <= 16 samples per thread
+    unsigned long long mine[PIV_CAP / PIV_NT];
+#pragma unroll
+    for (unsigned u = 0; u < PIV_CAP / PIV_NT; ++u) {
+      mine[u] = KEY_INVALID;
+      if (u < per) {
+        const unsigned j = tid + u * PIV_NT;
+        const int i = (int)(((unsigned long long)j * (unsigned)n) / ss);
+        const size_t o = (size_t)qi * g.npad + i;
+        mine[u] = arm_key(g.S[o], g.lvl[o], (uint32_t)i, g);
+      }
     }
-    __syncthreads();
-    bitonic_keys(buf, ss);
-    if (tid == 0) {
-      const unsigned expect = (unsigned)(((unsigned long long)need * ss + n - 1) / n);
-      unsigned rs = 2 * expect + 16;
-      if (rs > ss - 1) rs = ss - 1;
-      tau_s = buf[rs];
+    const unsigned expect = (unsigned)(((unsigned long long)need * ss + n - 1) / n);
+    const unsigned rounds = 2 * expect + 4;
+    unsigned long long t = KEY_INVALID;
+    for (unsigned r = 0; r < rounds; ++r) {
+      unsigned long long m = KEY_INVALID;
+#pragma unroll
+      for (unsigned u = 0; u < PIV_CAP / PIV_NT; ++u) m = mine[u] < m ? mine[u] : m;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(FULL, m, o);
+        m = y < m ? y : m;
+      }
+      if (lane == 0) wmin[warp] = m;
+      __syncthreads();
+      m = wmin[0];
+#pragma unroll
+      for (int w = 1; w < PIV_NT / 32; ++w) m = wmin[w] < m ? wmin[w] : m;
+      t = m;
+#pragma unroll
+      for (unsigned u = 0; u < PIV_CAP / PIV_NT; ++u)
+        if (mine[u] == m) mine[u] = KEY_INVALID;  // unique keys: exactly one owner
+      __syncthreads();
     }
+    if (tid == 0) tau_s = t;
   } else if (tid == 0) {
     tau_s = KEY_INVALID - 1;  // every arm
   }
@@ -79,8 +123,20 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
   __syncthreads();
   const unsigned long long tau = tau_s;
   RecBest bl{1.0e300, 0xffffffffu, 0, 0};
-  for (int i0 = tid * 4; i0 < n; i0 += PIV_NT * 4) {
-    const Arm4 a = load_arm4(g, qi, i0);
+  double bound = 1.0e300;  // min L seen by the warp so far: the screen's bound
+  constexpr int U = 4;  // arm groups in flight per thread (the pass is load-latency bound)
+  for (int wb0 = (tid - lane) * 4; wb0 < n; wb0 += PIV_NT * 4 * U) {  // warp-uniform trips
+    const int b0 = wb0 + lane * 4;
+    Arm4 ag[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i0 = b0 + u * PIV_NT * 4;
+      if (i0 < n) ag[u] = load_arm4(g, qi, i0);
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+    const int i0 = b0 + u * PIV_NT * 4;
+    const Arm4 &a = ag[u];
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const int i = i0 + e;
@@ -90,21 +146,41 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
         const unsigned p = atomicAdd(&cnt, 1u);
         if (p < PIV_CAP) buf[p] = key;
       } else {
-        const RecBest c{lower_of(a.S[e], a.l[e], g.d, g.alpha), (uint32_t)i + g.id_offset, a.S[e], a.l[e]};
-        if (better_min(c, bl)) bl = c;
+        const int li = lvl_exact(a.l[e]) ? MAX_LEVELS : a.l[e];
+        const float lf = __fsub_rn(__fmul_rn((float)a.S[e], invT[li]), alf[li]);
+        if ((double)__fsub_rn(lf, epsl[li]) <= bound) {  // could be the arg-min: decide in fp64
+          const RecBest c{lower_of(a.S[e], a.l[e], g.d, g.alpha), (uint32_t)i + g.id_offset, a.S[e], a.l[e]};
+          if (better_min(c, bl)) bl = c;
+        }
       }
     }
+    }
+    double wb = bl.v;  // share the warp's best: an arm above it cannot be the arg-min
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) wb = fmin(wb, __shfl_xor_sync(FULL, wb, o));
+    bound = wb;
   }
   __syncthreads();
   const unsigned c = cnt;
   *outside = block_best<false>(bl, wsm);
   *cnt_out = c;
   if (c < need || c > PIV_CAP) return false;
-  unsigned P = 2;
-  while (P < c) P <<= 1;
-  for (unsigned t = c + tid; t < P; t += PIV_NT) buf[t] = KEY_INVALID;
+  if (c <= PIV_BRUTE) {
+    for (unsigned t = tid; t < c; t += PIV_NT) {  // rank by counting (no sync stages)
+      const unsigned long long k = buf[t];
+      unsigned r = 0;
+      for (unsigned j = 0; j < c; ++j) r += buf[j] < k;
+      rank[t] = r;
+    }
+  } else {
+    unsigned P = 2;
+    while (P < c) P <<= 1;
+    for (unsigned t = c + tid; t < P; t += PIV_NT) buf[t] = KEY_INVALID;
+    __syncthreads();
+    bitonic_keys(buf, P);
+    for (unsigned t = tid; t < c; t += PIV_NT) rank[t] = t;
+  }
   __syncthreads();
-  bitonic_keys(buf, P);
   return true;
 }
 
@@ -120,23 +196,28 @@ __device__ __forceinline__ RecBest rec_of_key(const Geom &g, int qi, unsigned lo
 // Unsharded rank split + bounds + Eq. (5) (same contract as k_select).
 __global__ void __launch_bounds__(PIV_NT) k_select_pivot(Geom g) {
   extern __shared__ unsigned long long pbuf[];
+  unsigned *prank = reinterpret_cast<unsigned *>(pbuf + PIV_CAP);
   __shared__ RecBest wsm[PIV_NT / 32];
+  __shared__ unsigned long long sthr[2];
   const int qi = blockIdx.x;
   QState *st = g.qs + qi;
   if (st->done) return;
   const unsigned k = (unsigned)g.k, kh = (unsigned)(g.k + g.h);
   unsigned cnt;
   RecBest outside;
-  if (g.force_radix || !pivot_pass(g, qi, kh, pbuf, &cnt, &outside, wsm)) {
+  if (g.force_radix || !pivot_pass(g, qi, kh, pbuf, prank, &cnt, &outside, wsm)) {
     if (threadIdx.x == 0) st->fallback = 1;
     return;
   }
   RecBest bu{-1.0e300, 0xffffffffu, 0, 0}, bl = outside;
   for (unsigned t = threadIdx.x; t < cnt; t += PIV_NT) {
-    if (t < k) {
+    const unsigned r = prank[t];
+    if (r == k - 1) sthr[0] = pbuf[t];
+    if (r == kh - 1) sthr[1] = pbuf[t];
+    if (r < k) {
       const RecBest c = rec_of_key(g, qi, pbuf[t], true);
       if (better_max(c, bu)) bu = c;
-    } else if (t >= kh) {
+    } else if (r >= kh) {
       const RecBest c = rec_of_key(g, qi, pbuf[t], false);
       if (better_min(c, bl)) bl = c;
     }
@@ -145,8 +226,8 @@ __global__ void __launch_bounds__(PIV_NT) k_select_pivot(Geom g) {
   bl = block_best<false>(bl, wsm);
   if (threadIdx.x == 0) {
     st->fallback = 0;
-    st->thr_k = pbuf[k - 1];
-    st->thr_kh = pbuf[kh - 1];
+    st->thr_k = sthr[0];
+    st->thr_kh = sthr[1];
     st->A = bu.v;
     st->B = bl.v;
     st->d1 = (int)(bu.gid - g.id_offset);
@@ -163,6 +244,7 @@ __global__ void __launch_bounds__(PIV_NT) k_select_pivot(Geom g) {
 // records and the remainder's minimum-L record.
 __global__ void __launch_bounds__(PIV_NT) k_select_local_pivot(Geom g) {
   extern __shared__ unsigned long long pbuf[];
+  unsigned *prank = reinterpret_cast<unsigned *>(pbuf + PIV_CAP);
   __shared__ RecBest wsm[PIV_NT / 32];
   const int qi = blockIdx.x;
   QState *st = g.qs + qi;
@@ -170,7 +252,7 @@ __global__ void __launch_bounds__(PIV_NT) k_select_local_pivot(Geom g) {
   const unsigned kh = (unsigned)(g.k + g.h);
   unsigned cnt;
   RecBest outside;
-  if (g.force_radix || !pivot_pass(g, qi, kh, pbuf, &cnt, &outside, wsm)) {
+  if (g.force_radix || !pivot_pass(g, qi, kh, pbuf, prank, &cnt, &outside, wsm)) {
     if (threadIdx.x == 0) st->fallback = 1;
     return;
   }
@@ -178,15 +260,16 @@ __global__ void __launch_bounds__(PIV_NT) k_select_local_pivot(Geom g) {
   RecBest bl = outside;
   for (unsigned t = threadIdx.x; t < cnt; t += PIV_NT) {
     const unsigned long long key = pbuf[t];
+    const unsigned r = prank[t];
     const uint32_t i = (uint32_t)(key & ((1ull << g.kbits) - 1ull)) - g.id_offset;
     const size_t o = (size_t)qi * g.npad + i;
-    if (t < kh) {
-      ShardRec r;
-      r.key = key;
-      r.S = g.S[o];
-      r.lvl = g.lvl[o];
-      r.pad[0] = r.pad[1] = r.pad[2] = 0;
-      out[t] = r;
+    if (r < kh) {  // the local top-(k+h) in rank order
+      ShardRec rr;
+      rr.key = key;
+      rr.S = g.S[o];
+      rr.lvl = g.lvl[o];
+      rr.pad[0] = rr.pad[1] = rr.pad[2] = 0;
+      out[r] = rr;
     } else {
       const RecBest c = rec_of_key(g, qi, key, false);
       if (better_min(c, bl)) bl = c;
@@ -204,7 +287,7 @@ __global__ void __launch_bounds__(PIV_NT) k_select_local_pivot(Geom g) {
   }
 }
 
-size_t pivot_smem_bytes() { return (size_t)PIV_CAP * sizeof(unsigned long long); }
+size_t pivot_smem_bytes() { return (size_t)PIV_CAP * (sizeof(unsigned long long) + sizeof(unsigned)); }
 
 cudaError_t launch_select_pivot(const Geom &g, cudaStream_t s) {
   const size_t smem = pivot_smem_bytes();
