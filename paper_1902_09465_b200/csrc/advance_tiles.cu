@@ -62,7 +62,6 @@ __device__ __forceinline__ uint32_t sq_diff4(uint32_t xa, uint32_t qa, uint4 w, 
 __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
   extern __shared__ __align__(16) unsigned char tsm[];
   __shared__ unsigned lcnt[MAX_LEVELS], loff[MAX_LEVELS + 1], lfill[MAX_LEVELS];
-  __shared__ int sdone[256];
   const int R = 1 << g.tile_lr, P = 1 << g.tile_lp, RP = R * P;
   const int pitch = (int)g.pitch, nv = pitch >> 4;
   const int sl = g.tile_slot_l;
@@ -87,7 +86,6 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
     const int r0 = tr << g.tile_lr, p0 = tp << g.tile_lp;
     __syncthreads();  // the previous tile's shared memory is no longer in use
     if (tid < MAX_LEVELS) lcnt[tid] = 0;
-    for (int r = tid; r < R; r += TILE_NT) sdone[r] = (r0 + r >= g.q) ? 1 : g.qs[r0 + r].done;
 
     // stage the rows: asynchronous 16-byte copies (cp.async), all in flight at once;
     // rows past q / n are never referenced and are left as they are
@@ -105,32 +103,60 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
                      : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
-    __syncthreads();  // sdone, lcnt
-    // action bytes of the tile -> per-level counts (pairs of finished queries: none)
-    for (int e = tid; e < RP; e += TILE_NT) {
-      const int r = e >> g.tile_lp, p = e & (P - 1);
-      uint8_t a = 0;
-      if (!sdone[r] && p0 + p < g.n) a = g.act[(size_t)(r0 + r) * g.npad + p0 + p];
-      if (a > MAX_LEVELS) a = 0;  // exact fallbacks are the tensor-core pass's
-      sact[e] = a;
-      if (a) atomicAdd(&lcnt[a - 1], 1u);
+    // thread -> 4 consecutive arms of one query row (RP <= 4 * TILE_NT, P >= 4): the
+    // query's done flag, the action bytes, S and the level bytes in ONE round trip
+    const int e4 = tid * 4;
+    const bool in = e4 < RP;
+    const int rr = in ? e4 >> g.tile_lp : 0, pp = e4 & (P - 1);
+    const bool live = in && r0 + rr < g.q && p0 + pp < g.n;
+    const size_t o4 = (size_t)(r0 + rr) * g.npad + p0 + pp;
+    int4 S4 = make_int4(0, 0, 0, 0);
+    uint32_t A4 = 0, L4 = 0;
+    int dn = 1;
+    if (live) {
+      dn = g.qs[r0 + rr].done;
+      A4 = *reinterpret_cast<const uint32_t *>(g.act + o4);
+      S4 = *reinterpret_cast<const int4 *>(g.S + o4);
+      L4 = *reinterpret_cast<const uint32_t *>(g.lvl + o4);
+    }
+    uint32_t act4 = 0;  // sampled actions only (exact fallbacks: tensor-core pass)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      uint8_t a = (uint8_t)(A4 >> (8 * k));
+      if (dn || a > MAX_LEVELS || p0 + pp + k >= g.n) a = 0;  // stale bytes of finished queries
+      act4 |= (uint32_t)a << (8 * k);
+      hist_add(lcnt, a ? a - 1u : NONE);
+    }
+    if (in) *reinterpret_cast<uint32_t *>(sact + e4) = act4;
+    __syncthreads();  // lcnt
+    if (tid < 32) {  // per-level list offsets
+      const unsigned v = tid < MAX_LEVELS ? lcnt[tid] : 0u;
+      unsigned x = v;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const unsigned y = __shfl_up_sync(FULL, x, o);
+        if (tid >= o) x += y;
+      }
+      if (tid < MAX_LEVELS) {
+        loff[tid] = x - v;
+        lfill[tid] = x - v;
+      }
+      if (tid == MAX_LEVELS - 1) loff[MAX_LEVELS] = x;
+    }
+    __syncthreads();
+    // list the pairs by level: one shared atomic per (warp, level)
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint8_t a = (uint8_t)(act4 >> (8 * k));
+      const unsigned key = a ? a - 1u : NONE;
+      const unsigned m = __match_any_sync(FULL, key);
+      const int leader = __ffs(m) - 1;
+      unsigned b0 = 0;
+      if (a && lane_id() == leader) b0 = atomicAdd(&lfill[key], (unsigned)__popc(m));
+      b0 = __shfl_sync(FULL, b0, leader);
+      if (a) lst[b0 + __popc(m & ((1u << lane_id()) - 1u))] = (uint16_t)(e4 + k);
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
-    __syncthreads();
-    if (tid == 0) {
-      unsigned o = 0;
-      for (int c = 0; c < MAX_LEVELS; ++c) {
-        loff[c] = o;
-        lfill[c] = o;
-        o += lcnt[c];
-      }
-      loff[MAX_LEVELS] = o;
-    }
-    __syncthreads();
-    for (int e = tid; e < RP; e += TILE_NT) {
-      const uint8_t a = sact[e];
-      if (a) lst[atomicAdd(&lfill[a - 1], 1u)] = (uint16_t)e;
-    }
     __syncthreads();
 
     // the draws, level by level.  nb <= ADV_TP blocks per pair: a thread owns
@@ -212,14 +238,23 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
       }
     }
     __syncthreads();
-    // commit: S += the level's sum, T -> 2T
-    for (int e = tid; e < RP; e += TILE_NT) {
-      const uint8_t a = sact[e];
-      if (a) {
-        const size_t o = (size_t)(r0 + (e >> g.tile_lp)) * g.npad + p0 + (e & (P - 1));
-        g.S[o] += acc[e];
-        g.lvl[o] = a;
+    // commit: S += the level's sum, T -> 2T (the thread's own 4 arms)
+    if (act4) {
+      int4 o = S4;
+      uint32_t l4 = L4;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t a = (act4 >> (8 * k)) & 0xFFu;
+        if (!a) continue;
+        const int32_t add = acc[e4 + k];
+        if (k == 0) o.x += add;
+        if (k == 1) o.y += add;
+        if (k == 2) o.z += add;
+        if (k == 3) o.w += add;
+        l4 = (l4 & ~(0xFFu << (8 * k))) | (a << (8 * k));
       }
+      *reinterpret_cast<int4 *>(g.S + o4) = o;
+      *reinterpret_cast<uint32_t *>(g.lvl + o4) = l4;
     }
   }
   if (threadIdx.x == 0 && my_blocks) atomicAdd(&g.ctl->tile_blocks, my_blocks);
