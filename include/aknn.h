@@ -89,6 +89,9 @@ typedef struct {
    of staging dense (query x point) tiles in shared memory (diagnostics; identical
    results)                                                                   */
 #define AKNN_FLAG_NO_TILES 4
+/* bit 3: every 128 x 256 tile with an exact fallback runs on the tensor cores (by
+   default tiles with fewer than 512 of them stream rows instead; identical results) */
+#define AKNN_FLAG_EXACT_MMA_ALL 8
 
 /* Execution statistics of the last query call on an index (aknn_get_stats).
  * Kernel classes: init (a2), select (a6-a7: rank split, bounds, Eq. 5),

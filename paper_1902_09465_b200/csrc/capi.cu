@@ -243,6 +243,13 @@ aknn_status setup_exact_mma(aknn_index *ix, Geom &g, int64_t qb, uint8_t *ws, co
   g.nq = reinterpret_cast<int32_t *>(ws);
   g.xflags = reinterpret_cast<uint32_t *>(ws + round_up((size_t)qb * 4, 256));
   g.xf_cols = (int)((g.npad + exact_tile_cols() - 1) / exact_tile_cols());
+  // a 128 x 256 tile costs about as much as streaming ~800 pairs' rows: smaller counts
+  // take the row path (AKNN_XMIN overrides)
+  static const int xmin = [] {
+    const char *e = getenv("AKNN_XMIN");
+    return e && e[0] ? atoi(e) : 512;
+  }();
+  g.xmin = (o.flags & AKNN_FLAG_EXACT_MMA_ALL) ? 1u : (uint32_t)(xmin < 1 ? 1 : xmin);
   return AKNN_OK;
 }
 
@@ -518,7 +525,7 @@ aknn_status loop_graph(aknn_index *ix, const Geom &g, int nbits, int max_rounds,
 // Kernel launches per class (for aknn_stats; memset nodes excluded).
 int launches_init_of(const Geom &g) { return 2 + (g.exact_mma ? 1 : 0); }  // init, qstate, norms
 int launches_filter_of(const Geom &) { return 1; }
-int launches_compact_of(const Geom &g) { return 2 + (g.tile_on ? 2 : 0); }  // plan, scatter (+ lists)
+int launches_compact_of(const Geom &g) { return 3 + (g.tile_on ? 1 : 0); }  // plan, scatter, lists (+ tiles)
 int launches_advance_of(const Geom &g) {
   return 1 + (g.exact_mma ? 1 : 0) + (g.stage_lo < MAX_LEVELS ? 1 : 0);
 }

@@ -113,8 +113,9 @@ struct EpiDistances {
 
 // Epilogue of the round loop's exact fallbacks (row a4): for every pair of
 // the tile whose action byte is ACT_EXACT, S = sum_j (x_j - q_j)^2 = D exactly and
-// the level becomes LVL_EXACT.  Tiles without a fallback (flag 0, set by k_filter)
-// exit before touching TMEM; the CTA clears its flag for the next round.
+// the level becomes exact.  k_filter counts the fallbacks per 128 x 256 tile; tiles
+// with fewer than g.xmin of them exit before touching TMEM (k_scatter listed their
+// pairs for the row-stream path instead); every CTA clears its count for the next round.
 struct EpiFallback {
   Geom g;
   __device__ __forceinline__ bool tile_active(int m0, int n0) const {
@@ -125,7 +126,7 @@ struct EpiFallback {
       if (sflag) *f = 0u;
     }
     __syncthreads();
-    return sflag != 0u;
+    return sflag >= g.xmin;
   }
   __device__ __forceinline__ void store(int row, int col0, const uint32_t (&v)[32]) const {
     if (row >= g.q || col0 >= g.n || g.qs[row].done) return;

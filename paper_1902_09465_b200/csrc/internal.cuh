@@ -108,7 +108,8 @@ struct Geom {
   // exact fallbacks on the tensor cores (exact_mma.cu, EpiFallback)
   int exact_mma;         // 1: k_filter flags tiles, k_mma_tiles<EpiFallback> computes them
   int xf_cols;           // columns of xflags (point tiles of 256)
-  uint32_t *xflags;      // [ceil(q/128)][xf_cols] tile holds an ACT_EXACT pair this round
+  uint32_t *xflags;      // [ceil(q/128)][xf_cols] ACT_EXACT pairs of the tile this round
+  uint32_t xmin;         // tiles with >= xmin of them run on the tensor cores
   const int32_t *nx;     // [n] ||x_i||^2
   int32_t *nq;           // [q] ||x_q||^2 of this batch
   // tile-staged level gathers (advance_tiles.cu)

@@ -241,16 +241,18 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
     uint32_t dr = 0, actw = 0;
     if (arms) actw = filter_arms(g, cur, g.thr + (size_t)qi * THR_STRIDE, ca, i0, &dr);
     if (i0 < g.npad) *reinterpret_cast<uint32_t *>(g.act + (size_t)qi * g.npad + i0) = actw;
-    bool ex = false;
+    unsigned ex = 0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const uint8_t act = (uint8_t)(actw >> (8 * e));
-      ex |= act == ACT_EXACT;
+      ex += act == ACT_EXACT;
       hist_add(scnt, act == 0 ? NONE : (act == ACT_EXACT ? (unsigned)MAX_LEVELS : act - 1u));
     }
-    if (g.exact_mma && __any_sync(FULL, ex) && lane == 0)
-      // a warp's 128 arms lie in one 256-point tile: flag it for the tensor-core pass
-      g.xflags[(size_t)(qi >> 7) * g.xf_cols + (i0 >> 8)] = 1u;
+    if (g.exact_mma) {
+      // a warp's 128 arms lie in one 128 x 256 tile of the tensor-core pass: count them
+      const unsigned wex = __reduce_add_sync(FULL, ex);
+      if (wex && lane == 0) atomicAdd(&g.xflags[(size_t)(qi >> 7) * g.xf_cols + (i0 >> 8)], wex);
+    }
     if (g.tile_on) {
       // the P/4 lanes of a tile segment add up their sampled draws
       const int seg = min(32, (1 << g.tile_lp) >> 2);
@@ -314,8 +316,9 @@ __global__ void k_plan(RoundCtl *ctl, unsigned bpl, int stage_lo) {
   ctl->advanced += adv;
 }
 
-// After the scatter: the lists hold only the pairs of sparse tiles, cursor[s] of
-// them per slot; the advance kernels walk exactly those.
+// After the scatter: the lists hold only the pairs of sparse tiles (and the exact
+// fallbacks of sparse tensor-core tiles), cursor[s] of them per slot; the advance
+// kernels walk exactly those.
 __global__ void k_plan_lists(RoundCtl *ctl, unsigned bpl, int stage_lo) {
   if (threadIdx.x != 0) return;
   unsigned long long ch = 0;
@@ -350,6 +353,9 @@ __global__ void __launch_bounds__(FIL_NT) k_scatter(Geom g) {
     const int i = base_i + e * FIL_NT;
     const uint8_t act = i < g.n ? arow[i] : (uint8_t)0;
     slot[e] = act == 0 ? NONE : (act == ACT_EXACT ? (unsigned)MAX_LEVELS : act - 1u);
+    if (g.exact_mma && slot[e] == (unsigned)MAX_LEVELS &&
+        g.xflags[(size_t)(qi >> 7) * g.xf_cols + (i >> 8)] >= g.xmin)
+      slot[e] = NONE;  // a dense tile of the tensor-core exact pass takes it
     if (g.tile_on && slot[e] < (unsigned)MAX_LEVELS &&
         (float)g.tilework[(size_t)(qi >> g.tile_lr) * g.tile_cols + (i >> g.tile_lp)] >= g.tile_row_draws * (float)((1 << g.tile_lr) + (1 << g.tile_lp)))
       slot[e] = NONE;  // k_advance_tiles takes it
@@ -364,10 +370,9 @@ __global__ void __launch_bounds__(FIL_NT) k_scatter(Geom g) {
   if (threadIdx.x < NSLOT && scnt[threadIdx.x])
     sbase[threadIdx.x] = g.ctl->off[threadIdx.x] + atomicAdd(&g.ctl->cursor[threadIdx.x], scnt[threadIdx.x]);
   __syncthreads();
-  const unsigned skip_slot = g.exact_mma ? (unsigned)MAX_LEVELS : NONE;  // tensor-core exact pass
 #pragma unroll
   for (int e = 0; e < 4; ++e)
-    if (slot[e] != NONE && slot[e] != skip_slot)
+    if (slot[e] != NONE)
       g.list[sbase[slot[e]] + loc[e]] = ((uint32_t)qi << g.ibits) | (uint32_t)(base_i + e * FIL_NT);
 }
 
@@ -509,8 +514,8 @@ __global__ void __launch_bounds__(ADV_NT) k_advance(Geom g) {
   // row-staged levels [stage_lo, MAX_LEVELS) belong to k_advance_staged
   const int slo = g.stage_lo < MAX_LEVELS ? g.stage_lo : MAX_LEVELS;
   const unsigned long long total_a = coff[slo], skip = coff[MAX_LEVELS] - coff[slo];
-  // exact fallbacks (the last slot) go to the tensor-core tile pass when g.exact_mma
-  const unsigned long long total = (g.exact_mma ? coff[MAX_LEVELS] : coff[NSLOT]) - skip;
+  // (exact fallbacks of dense tensor-core tiles are not listed: k_mma_tiles takes them)
+  const unsigned long long total = coff[NSLOT] - skip;
   const unsigned long long nwarps = (unsigned long long)gridDim.x * (ADV_NT / 32);
   const int lane = lane_id();
   const uint32_t imask = (1u << g.ibits) - 1u;
@@ -802,8 +807,8 @@ cudaError_t launch_filter(const Geom &g, cudaStream_t s) {
 cudaError_t launch_compact(const Geom &g, cudaStream_t s) {
   k_plan<<<1, 32, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo);
   k_scatter<<<dim3(g.q, cdiv(g.npad, FIL_NT * 4)), FIL_NT, 0, s>>>(g);
+  k_plan_lists<<<1, 32, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo);  // the lists as written
   if (g.tile_on) {
-    k_plan_lists<<<1, 32, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo);
     const cudaError_t e = launch_tile_list(g, s);
     if (e != cudaSuccess) return e;
   }

@@ -276,12 +276,14 @@ def test_exact_fallback_tensor_cores_equals_rows(ak, n, d, q, k, h, kind):
     X, Q = synth.small_instance(n + d, n, d, q=q)
     al = orc.alpha_theory(n, 0.05, d) if kind == "theory" else orc.alpha_experimental(n, 0.05, d, 0.05)
     ix = ak.Index(X)
-    a = ix.query(Q, k, h, 0.05, 21, al, counts=True, sums=True)
+    a = ix.query(Q, k, h, 0.05, 21, al, counts=True, sums=True, flags=ak.FLAG_EXACT_MMA_ALL)
     sa = ix.stats()
     b = ix.query(Q, k, h, 0.05, 21, al, counts=True, sums=True, flags=ak.FLAG_EXACT_ROWS)
+    c = ix.query(Q, k, h, 0.05, 21, al, counts=True, sums=True)  # dense tiles only on the MMA
     ix.close()
     for key in KEYS:
         assert np.array_equal(a[key], b[key]), key
+        assert np.array_equal(a[key], c[key]), key
     if n > 100:
         assert sa["exact_fallbacks"] > 0  # the tile pass was exercised
     _assert_parity(a, orc.query_br(X, Q, k, h, 21, al, want_sums=True))
