@@ -23,11 +23,17 @@ constexpr uint8_t ACT_EXACT = 0xFE;
 constexpr int MAX_LEVELS = 16;
 constexpr int NSLOT = MAX_LEVELS + 1;
 
-// Integer form of the blocker predicate of one query for a round, per sampled level c
-// (k_thresholds): U(S, c) > B  <=>  S >= Su[c];  L(S, c) < A  <=>  S < Sl[c];
-// alpha(2^c) > alpha_d2  <=>  bit c of the M mask.  Exact because U and L are
-// monotone non-decreasing in S (one correctly rounded division, one addition).
-constexpr int THR_STRIDE = 2 * MAX_LEVELS + 1;
+// Integer form of the blocker predicate of one query for a round (k_thresholds).
+// Per sampled level c, int4 {Su, Sl, Ck, Ckh}:
+//   U(S, c) > B            <=>  S >= Su
+//   L(S, c) < A            <=>  S <  Sl
+//   key(S, c, i) <= thr_k  <=>  S < Ck  or (eq_k bit c and S == Ck and gid <= id_k)
+//   key(S, c, i) <= thr_kh <=>  S < Ckh or (eq_kh bit c and S == Ckh and gid <= id_kh)
+// and a header {M mask (alpha(2^c) > alpha_d2), eq_k mask, eq_kh mask, id_k, id_kh}.
+// Exact because U and L are monotone non-decreasing in S (one correctly rounded
+// division, one addition) and the key is (S * (L / 2^c)) << kbits | gid.
+constexpr int THR_LEVEL_INTS = 4 * MAX_LEVELS;
+constexpr int THR_STRIDE = THR_LEVEL_INTS + 8;
 
 // Per-query state of the round loop (device memory, one per batch row).
 struct QState {

@@ -149,7 +149,8 @@ __global__ void __launch_bounds__(128) k_thresholds(Geom g) {
   const QState &st = g.qs[qi];
   if (st.done) return;
   int32_t *t = g.thr + (size_t)qi * THR_STRIDE;
-  bool mbit = false;
+  const unsigned long long kmask = (1ull << g.kbits) - 1ull;
+  bool mbit = false, eqk = false, eqkh = false;
   if (c < MAX_LEVELS && c <= g.cmax) {
     const uint8_t l = (uint8_t)c;
     const double al = alpha_of(l, g.alpha);
@@ -160,7 +161,7 @@ __global__ void __launch_bounds__(128) k_thresholds(Geom g) {
       const int32_t mid = lo + ((hi - lo) >> 1);
       if (__dadd_rn(dhat_of(mid, l, g.d), al) > st.B) hi = mid; else lo = mid + 1;
     }
-    t[c] = lo;
+    const int32_t su = lo;
     // Sl: first S with L(S) >= A (blocker iff S < Sl)
     lo = 0;
     hi = smax + 1;
@@ -168,11 +169,26 @@ __global__ void __launch_bounds__(128) k_thresholds(Geom g) {
       const int32_t mid = lo + ((hi - lo) >> 1);
       if (!(__dsub_rn(dhat_of(mid, l, g.d), al) < st.A)) hi = mid; else lo = mid + 1;
     }
-    t[MAX_LEVELS + c] = lo;
+    const int32_t sl = lo;
+    // the key thresholds on S at this level: S * mul <=> K = thr >> kbits
+    const unsigned long long mul = g.L >> c;
+    const unsigned long long Kk = st.thr_k >> g.kbits, Kkh = st.thr_kh >> g.kbits;
+    const unsigned long long ck = (Kk + mul - 1) / mul, ckh = (Kkh + mul - 1) / mul;
+    eqk = Kk % mul == 0;
+    eqkh = Kkh % mul == 0;
+    const int4 v = make_int4(su, sl, (int32_t)(ck > 0x7fffffffull ? 0x7fffffffull : ck),
+                             (int32_t)(ckh > 0x7fffffffull ? 0x7fffffffull : ckh));
+    *reinterpret_cast<int4 *>(t + 4 * c) = v;
     mbit = al > st.a_d2;
   }
-  const unsigned m = __ballot_sync(FULL, mbit);
-  if (c == 0) t[2 * MAX_LEVELS] = (int32_t)m;
+  const unsigned m = __ballot_sync(FULL, mbit), mk = __ballot_sync(FULL, eqk), mkh = __ballot_sync(FULL, eqkh);
+  if (c == 0) {
+    t[THR_LEVEL_INTS + 0] = (int32_t)m;
+    t[THR_LEVEL_INTS + 1] = (int32_t)mk;
+    t[THR_LEVEL_INTS + 2] = (int32_t)mkh;
+    t[THR_LEVEL_INTS + 3] = (int32_t)(uint32_t)(st.thr_k & kmask);
+    t[THR_LEVEL_INTS + 4] = (int32_t)(uint32_t)(st.thr_kh & kmask);
+  }
 }
 
 cudaError_t launch_thresholds(const Geom &g, cudaStream_t s) {
@@ -180,38 +196,52 @@ cudaError_t launch_thresholds(const Geom &g, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-__device__ __forceinline__ uint32_t filter_arms(const Geom &g, const QState &st, const int32_t *thr, const Arm4 &a,
-                                                int i0, uint32_t *draws) {
+// Branch-free decision of 4 arms (R5 with the integer thresholds of reading R20):
+// one 16-byte table load per arm, no 64-bit key arithmetic, no floating point.
+__device__ __forceinline__ uint32_t filter_arms(const Geom &g, const int32_t *thr, const Arm4 &a, int i0,
+                                                uint32_t *draws) {
   uint32_t actw = 0, dr = 0;
-  const uint32_t mmask = (uint32_t)__ldg(thr + 2 * MAX_LEVELS);
+  const int4 hdr = __ldg(reinterpret_cast<const int4 *>(thr + THR_LEVEL_INTS));
+  const uint32_t mmask = (uint32_t)hdr.x, eqk = (uint32_t)hdr.y, eqkh = (uint32_t)hdr.z;
+  const uint32_t idk = (uint32_t)hdr.w, idkh = (uint32_t)__ldg(thr + THR_LEVEL_INTS + 4);
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const int i = i0 + e;
     const uint8_t l = a.l[e];
-    uint8_t act = 0;
-    if (i < g.n && !lvl_exact(l)) {
-      const unsigned long long key = arm_key(a.S[e], l, (uint32_t)i, g);
-      bool blk;
-      if (key <= st.thr_k)
-        blk = a.S[e] >= __ldg(thr + l);               // U > B
-      else if (key <= st.thr_kh)
-        blk = (mmask >> l) & 1u;                       // alpha > alpha_d2
-      else
-        blk = a.S[e] < __ldg(thr + MAX_LEVELS + l);   // L < A
-      if (blk) {
-        if ((2u << l) >= (unsigned)g.d) {
-          act = ACT_EXACT;
-        } else {
-          act = (uint8_t)(l + 1);
-          dr += 1u << l;
-        }
-      }
-    }
-    actw |= (uint32_t)act << (8 * e);
+    const uint32_t c = l & 15u;
+    const bool live = i < g.n && !lvl_exact(l);
+    const int4 t = __ldg(reinterpret_cast<const int4 *>(thr) + c);  // Su, Sl, Ck, Ckh
+    const int32_t S = a.S[e];
+    const uint32_t gid = (uint32_t)i + g.id_offset;
+    const bool inC = S < t.z || (((eqk >> c) & 1u) && S == t.z && gid <= idk);
+    const bool inM = S < t.w || (((eqkh >> c) & 1u) && S == t.w && gid <= idkh);
+    const bool blk = live && (inC ? S >= t.x : (inM ? ((mmask >> c) & 1u) != 0u : S < t.y));
+    const bool ex = (2u << c) >= (unsigned)g.d;
+    const uint32_t act = blk ? (ex ? (uint32_t)ACT_EXACT : c + 1u) : 0u;
+    dr += (blk && !ex) ? (1u << c) : 0u;
+    actw |= act << (8 * e);
   }
   *draws = dr;
   return actw;
 }
+
+// Per-thread run-length counter of action slots: flushes to the CTA's shared counts
+// only when the slot changes (under lockstep levels: almost never).
+struct SlotRun {
+  unsigned slot = NONE, n = 0;
+  __device__ __forceinline__ void add(unsigned s, unsigned *scnt) {
+    if (s == slot) {
+      ++n;
+      return;
+    }
+    if (slot != NONE && n) atomicAdd(&scnt[slot], n);
+    slot = s;
+    n = 1;
+  }
+  __device__ __forceinline__ void flush(unsigned *scnt) {
+    if (slot != NONE && n) atomicAdd(&scnt[slot], n);
+  }
+};
 
 __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
   extern __shared__ uint32_t tcnt[];  // [FIL_ROWS / R][FIL_NT * 4 / P] (tiles on)
@@ -226,41 +256,47 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
   for (int t = threadIdx.x; t < ntc; t += FIL_NT) tcnt[t] = 0;
   __syncthreads();
   const bool arms = i0 < g.n;
-  QState st = g.qs[q0];
+  int st = g.qs[q0].done;
   Arm4 a{};
   if (arms) a = load_arm4(g, q0, i0);
+  SlotRun run;
+  unsigned ex_acc = 0;     // exact fallbacks of this thread (one 128-query tile row: 32 | 128)
+  uint32_t dr_acc = 0;     // sampled draws of this thread in the current tile row
+  int tr_cur = 0;
   for (int r = 0; r < rows; ++r) {
     const int qi = q0 + r;
-    const QState cur = st;
+    const int cur = st;
     const Arm4 ca = a;
     if (r + 1 < rows) {  // prefetch the next row
-      st = g.qs[qi + 1];
+      st = g.qs[qi + 1].done;
       if (arms) a = load_arm4(g, qi + 1, i0);
     }
-    if (cur.done) continue;  // uniform: one query row at a time
+    if (cur) continue;  // uniform: one query row at a time
     uint32_t dr = 0, actw = 0;
-    if (arms) actw = filter_arms(g, cur, g.thr + (size_t)qi * THR_STRIDE, ca, i0, &dr);
+    if (arms) actw = filter_arms(g, g.thr + (size_t)qi * THR_STRIDE, ca, i0, &dr);
     if (i0 < g.npad) *reinterpret_cast<uint32_t *>(g.act + (size_t)qi * g.npad + i0) = actw;
-    unsigned ex = 0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      const uint8_t act = (uint8_t)(actw >> (8 * e));
-      ex += act == ACT_EXACT;
-      hist_add(scnt, act == 0 ? NONE : (act == ACT_EXACT ? (unsigned)MAX_LEVELS : act - 1u));
-    }
-    if (g.exact_mma) {
-      // a warp's 128 arms lie in one 128 x 256 tile of the tensor-core pass: count them
-      const unsigned wex = __reduce_add_sync(FULL, ex);
-      if (wex && lane == 0) atomicAdd(&g.xflags[(size_t)(qi >> 7) * g.xf_cols + (i0 >> 8)], wex);
+      const uint32_t act = (actw >> (8 * e)) & 0xFFu;
+      ex_acc += act == ACT_EXACT;
+      if (act) run.add(act == ACT_EXACT ? (unsigned)MAX_LEVELS : act - 1u, scnt);
     }
     if (g.tile_on) {
-      // the P/4 lanes of a tile segment add up their sampled draws
-      const int seg = min(32, (1 << g.tile_lp) >> 2);
-      uint32_t v = dr;
-      for (int o = 1; o < seg; o <<= 1) v += __shfl_xor_sync(FULL, v, o);
-      if ((lane & (seg - 1)) == 0 && v)
-        atomicAdd(&tcnt[(r >> g.tile_lr) * tcols + ((threadIdx.x * 4) >> g.tile_lp)], v);
+      const int tr = r >> g.tile_lr;
+      if (tr != tr_cur) {  // entering the next tile row of this CTA: flush
+        if (dr_acc) atomicAdd(&tcnt[tr_cur * tcols + ((threadIdx.x * 4) >> g.tile_lp)], dr_acc);
+        dr_acc = 0;
+        tr_cur = tr;
+      }
+      dr_acc += dr;
     }
+  }
+  run.flush(scnt);
+  if (g.tile_on && dr_acc) atomicAdd(&tcnt[tr_cur * tcols + ((threadIdx.x * 4) >> g.tile_lp)], dr_acc);
+  if (g.exact_mma) {
+    // a warp's 128 arms lie in one 128 x 256 tile of the tensor-core pass: count them
+    const unsigned wex = __reduce_add_sync(FULL, ex_acc);
+    if (wex && lane == 0) atomicAdd(&g.xflags[(size_t)(q0 >> 7) * g.xf_cols + (i0 >> 8)], wex);
   }
   __syncthreads();
   if (threadIdx.x < NSLOT && scnt[threadIdx.x]) atomicAdd(&g.ctl->cnt[threadIdx.x], scnt[threadIdx.x]);
@@ -342,9 +378,35 @@ __global__ void __launch_bounds__(FIL_NT) k_scatter(Geom g) {
   const int qi = blockIdx.x;
   if (g.qs[qi].done) return;
   __shared__ unsigned scnt[NSLOT], sbase[NSLOT];
+  __shared__ uint8_t sdense[FIL_NT * 4 / 4];  // the chunk's (R x P) tiles: dense?
+  __shared__ uint8_t smma[FIL_NT * 4 / 256];   // its 128 x 256 exact tiles: tensor cores?
+  __shared__ int any_listed;
+  const int c0 = blockIdx.y * FIL_NT * 4;
+  const int ntile = g.tile_on ? (FIL_NT * 4) >> g.tile_lp : 0;
   for (int s = threadIdx.x; s < NSLOT; s += FIL_NT) scnt[s] = 0;
+  if (threadIdx.x == 0) any_listed = 0;
   __syncthreads();
-  const int base_i = blockIdx.y * FIL_NT * 4 + threadIdx.x;
+  // the chunk's tile decisions, once; a chunk whose sampled pairs all lie in dense
+  // tiles and whose exact ones all go to the tensor cores lists nothing
+  for (int t = threadIdx.x; t < ntile; t += FIL_NT) {
+    const int tc = (c0 >> g.tile_lp) + t;
+    const bool dense = tc < g.tile_cols &&
+                       (float)g.tilework[(size_t)(qi >> g.tile_lr) * g.tile_cols + tc] >=
+                           g.tile_row_draws * (float)((1 << g.tile_lr) + (1 << g.tile_lp));
+    sdense[t] = dense;
+    if (!dense) any_listed = 1;
+  }
+  if (!g.tile_on && threadIdx.x == 0) any_listed = 1;
+  if (threadIdx.x < (FIL_NT * 4) / 256) {
+    const int xc = (c0 >> 8) + (int)threadIdx.x;
+    const uint32_t cnt = (g.exact_mma && xc < g.xf_cols) ? g.xflags[(size_t)(qi >> 7) * g.xf_cols + xc] : 0u;
+    smma[threadIdx.x] = g.exact_mma && cnt >= g.xmin;
+    if (cnt != 0u && cnt < g.xmin) any_listed = 1;
+    if (!g.exact_mma) any_listed = 1;
+  }
+  __syncthreads();
+  if (!any_listed) return;
+  const int base_i = c0 + threadIdx.x;
   const uint8_t *arow = g.act + (size_t)qi * g.npad;
   const int lane = lane_id();
   unsigned slot[4], loc[4];
@@ -353,11 +415,9 @@ __global__ void __launch_bounds__(FIL_NT) k_scatter(Geom g) {
     const int i = base_i + e * FIL_NT;
     const uint8_t act = i < g.n ? arow[i] : (uint8_t)0;
     slot[e] = act == 0 ? NONE : (act == ACT_EXACT ? (unsigned)MAX_LEVELS : act - 1u);
-    if (g.exact_mma && slot[e] == (unsigned)MAX_LEVELS &&
-        g.xflags[(size_t)(qi >> 7) * g.xf_cols + (i >> 8)] >= g.xmin)
+    if (slot[e] == (unsigned)MAX_LEVELS && smma[(i - c0) >> 8])
       slot[e] = NONE;  // a dense tile of the tensor-core exact pass takes it
-    if (g.tile_on && slot[e] < (unsigned)MAX_LEVELS &&
-        (float)g.tilework[(size_t)(qi >> g.tile_lr) * g.tile_cols + (i >> g.tile_lp)] >= g.tile_row_draws * (float)((1 << g.tile_lr) + (1 << g.tile_lp)))
+    if (g.tile_on && slot[e] < (unsigned)MAX_LEVELS && sdense[(i - c0) >> g.tile_lp])
       slot[e] = NONE;  // k_advance_tiles takes it
     const unsigned m = __match_any_sync(FULL, slot[e]);
     const int leader = __ffs(m) - 1;
