@@ -40,6 +40,7 @@ import synth  # noqa: E402  (input generator only; no method arithmetic)
 METRIC = "adaptive k-NN queries/s (+ sampled coord-evals/s; % of HBM roofline)"
 UNIT = "queries/s"
 L2_FLUSH_BYTES = 512 << 20
+SHARD_ROWS = 1_000_000  # C5: points per GPU (BASELINE.json configs[4])
 
 
 def _args():
@@ -311,8 +312,12 @@ def run_reference(args, dist: Dist):
     cfg = synth.config(args.config)
     if args.q:
         cfg = synth.config(args.config, q=args.q)
-    X = synth.points(cfg)
     Q = synth.queries(cfg)
+    if cfg.shards > 1:  # C5: the same N * SHARD_ROWS points as our arm
+        X = synth.points(cfg, 0, SHARD_ROWS * args.gpus)
+        cfg = synth.config(args.config, q=cfg.q, n=SHARD_ROWS * args.gpus)
+    else:
+        X = synth.points(cfg)
     al = _oracle_alpha(cfg, args.alpha)
     cores = max(1, min(_cpu_cores(), 16))
     nq = min(cores, cfg.q)  # one query per core per step
@@ -356,18 +361,36 @@ def run_ours(args, dist: Dist):
     dev = torch.device("cuda", dist.local)
     base = synth.config(args.config)
     qpr = args.q or base.q
-    cfg = synth.config(args.config, q=qpr)
-    # every rank: the same X, its own slice of a (world * q)-query batch of the mixture
-    allq = synth.queries(synth.config(args.config, q=qpr * dist.world)) if dist.world > 1 \
-        else synth.queries(cfg)
-    Qh = np.ascontiguousarray(allq[dist.rank * qpr:(dist.rank + 1) * qpr])
-    X = synth.points(cfg)
+    sharded = base.shards > 1  # C5: point-sharded, SHARD_ROWS per GPU (weak scaling)
+    if sharded:
+        # rank r holds rows [r * SHARD_ROWS, (r+1) * SHARD_ROWS) of the C5 point set; the
+        # job answers ONE batch of q queries against all N * SHARD_ROWS points, with one
+        # ncclAllGather of the round summaries per round
+        n_global = SHARD_ROWS * dist.world
+        row0 = SHARD_ROWS * dist.rank
+        cfg = synth.config(args.config, q=qpr, n=n_global)
+        Qh = synth.queries(synth.config(args.config, q=qpr))
+        X = synth.points(base, row0, row0 + SHARD_ROWS)
+    else:
+        cfg = synth.config(args.config, q=qpr)
+        # every rank: the same X, its own slice of a (world * q)-query batch of the mixture
+        allq = synth.queries(synth.config(args.config, q=qpr * dist.world)) if dist.world > 1 \
+            else synth.queries(cfg)
+        Qh = np.ascontiguousarray(allq[dist.rank * qpr:(dist.rank + 1) * qpr])
+        X = synth.points(cfg)
     n, d, k, h = cfg.n, cfg.d, cfg.k, cfg.h
+    n_loc = X.shape[0]  # points on this GPU
     if args.alpha == "theory":
         alpha = ak.alpha_table(n, cfg.delta, d, "theory")
     else:
         alpha = ak.alpha_table(n, cfg.delta, d, "experimental", float(args.alpha.split(":", 1)[1]))
-    ix = ak.Index(torch.from_numpy(X).to(dev))
+    if sharded and dist.world > 1:
+        nid = [ak.nccl_unique_id() if dist.rank == 0 else None]
+        dist.pg.broadcast_object_list(nid, src=0)
+        ix = ak.Index(X, n_global=n_global, offset=row0, nccl_id=nid[0], rank=dist.rank, world=dist.world)
+        args.no_exact = True  # the exact pass is per shard: no global recall here
+    else:
+        ix = ak.Index(torch.from_numpy(X).to(dev))
     Qd = torch.from_numpy(Qh).to(dev)
     alpha_d = torch.from_numpy(alpha).to(dev)
     stream = torch.cuda.Stream(device=dev)
@@ -378,7 +401,7 @@ def run_ours(args, dist: Dist):
                sums=None, evals=torch.empty(qpr, dtype=torch.int64, device=dev),
                draws=torch.empty(qpr, dtype=torch.int64, device=dev),
                rounds=torch.empty(qpr, dtype=torch.int32, device=dev))
-    qi_off = dist.rank * qpr
+    qi_off = 0 if sharded else dist.rank * qpr
 
     def step(timing: bool):
         flush.zero_()
@@ -413,7 +436,7 @@ def run_ours(args, dist: Dist):
     times, gstats, clk = timed(False)
     ms_local = sum(times)
     ms_max = dist.max(ms_local)
-    total_q = dist.sum(qpr * args.steps)
+    total_q = qpr * args.steps if sharded else dist.sum(qpr * args.steps)
     value = total_q / (ms_max / 1e3)
     ms_per_step = ms_max / args.steps
     # (2) the same steps with per-launch CUDA events (host-driven loop) for the roofline
@@ -429,14 +452,14 @@ def run_ours(args, dist: Dist):
     launches = {c: agg[f"launches_{c}"] for c in classes}
     abytes = {c: 0 for c in classes}
     for s in stats:
-        for c, b in _algorithmic_bytes(s, n, d, qpr).items():
+        for c, b in _algorithmic_bytes(s, n_loc, d, qpr).items():
             abytes[c] += b
     dom = max(classes, key=lambda c: ms_cls[c])
     peak, peak_src = _peaks()
-    probes = _measure_probes(d, n * cfg.d)
+    probes = _measure_probes(d, n_loc * cfg.d)
     blocks = agg.get("philox_blocks", 0)
     adv_draws = max(0, blocks - agg.get("tile_blocks", 0)) * 4  # list-path level-gather draws
-    x_in_l2 = n * d <= L2_BYTES * 0.8
+    x_in_l2 = n_loc * d <= L2_BYTES * 0.8
     common = {"kernel": KERNEL_OF[dom], "launches": launches[dom],
               "avg_launch_ms": ms_cls[dom] / max(1, launches[dom]),
               "share_of_step": ms_cls[dom] / ms_local_instr,
@@ -455,7 +478,7 @@ def run_ours(args, dist: Dist):
         "sector_GBps": adv_draws * SECTOR / adv_s / 1e9 if adv_s > 0 else None,
         "frac_of_measured_random_sector_rate": (adv_draws / adv_s) / probes["gather_loads_per_s"]
         if adv_s > 0 and probes.get("gather_loads_per_s") else None,
-        "x_footprint_bytes": n * d, "x_l2_resident": x_in_l2}
+        "x_footprint_bytes": n_loc * d, "x_l2_resident": x_in_l2}
     tile_blocks = agg.get("tile_blocks", 0)
     if dom == "tiles" and probes.get("philox_blocks_per_s"):
         # dense tiles gather from shared memory: the sampled draws are bound by the
@@ -489,7 +512,8 @@ def run_ours(args, dist: Dist):
 
     extra = {
         "draws_per_s": dist.sum(draws) / (ms_max / 1e3),
-        "evals_per_s": dist.sum(evals_total) / (ms_max / 1e3),
+        # sharded: the library already sums evals over the ranks (ncclAllReduce)
+        "evals_per_s": (evals_total if sharded else dist.sum(evals_total)) / (ms_max / 1e3),
         "sample_fraction": evals_total / (args.steps * qpr * n * d),
         "rounds_max": int(out["rounds"].max().item()),
         "exact_fallbacks_per_query": agg["exact_fallbacks"] / (args.steps * qpr),
@@ -550,7 +574,7 @@ def run_ours(args, dist: Dist):
         e2e_s = dist.max(sum(wall))
         h2d = Qh.nbytes + alpha.nbytes
         d2h = sum(v.nbytes for key, v in hout.items() if key != "status" and v is not None)
-        e2e = {"value": dist.sum(qpr * args.steps) / e2e_s, "unit": UNIT,
+        e2e = {"value": (qpr * args.steps if sharded else dist.sum(qpr * args.steps)) / e2e_s, "unit": UNIT,
                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                "api": "aknn_query (host pointers, pinned), wall clock incl. copies"}
         if not np.array_equal(hout["sets"], out["sets"].cpu().numpy()):
@@ -560,7 +584,7 @@ def run_ours(args, dist: Dist):
     if not args.no_cpu_baseline and dist.rank == 0 and dist.world == 1:
         # a bounded sample of the same workload: ~10-30 s of oracle work on the host cores
         cores = max(1, min(_cpu_cores(), 16))
-        nq = min(qpr, 8 * cores)
+        nq = min(qpr, 8 * cores if n <= 200_000 else cores)
         dt, _ = _oracle_time(X, Qh, cfg, _oracle_alpha(cfg, args.alpha), nq, cores)
         cpu = {"value": nq / dt, "unit": UNIT, "cores": min(cores, nq), "kind": "oracle",
                "sample": f"first {nq} queries of {cfg.name} (full n={n}, d={d}), one "
@@ -574,7 +598,11 @@ def run_ours(args, dist: Dist):
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
             "data": "synthetic (seeded; synth/ recipes, DESIGN.md §5)",
-            "config": _config_desc(cfg, args),
+            "config": _config_desc(cfg, args, extra={
+                "parallelism": f"point-sharded x{dist.world}: {SHARD_ROWS:,} rows per GPU, one "
+                               f"ncclAllGather of the round summaries per round" if sharded and dist.world > 1
+                else ("point set of 1 shard (the N=1 point of the weak-scaling series)" if sharded
+                      else _config_desc(cfg, args)["parallelism"])}),
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": gpu_launches, "gpu_launches_per_step": gpu_launches / args.steps,
             "step_ms": [round(t, 3) for t in times],
