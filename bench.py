@@ -517,6 +517,9 @@ def run_ours(args, dist: Dist):
         "sample_fraction": evals_total / (args.steps * qpr * n * d),
         "rounds_max": int(out["rounds"].max().item()),
         "exact_fallbacks_per_query": agg["exact_fallbacks"] / (args.steps * qpr),
+        # G2 (k_init): one random 32-byte sector of X + 6 B of state per pair
+        "init_GBps_sector_model": (qpr * n_loc * (SECTOR + 6)) / (ms_cls["init"] / args.steps / 1e3) / 1e9
+        if ms_cls["init"] > 0 else None,
     }
 
     # exact comparison pass on the same queries: time + recall of the adaptive sets
@@ -548,7 +551,10 @@ def run_ours(args, dist: Dist):
             ok += strict <= s
         extra.update({"exact_pass_ms": ex_ms, "speedup_vs_exact": ex_ms / ms_per_step,
                       "recall_contains_knn": dist.sum(ok) / (qpr * dist.world),
-                      "exact_pass_kernel": "tcgen05 kind::i8 tiles (k_mma_tiles) + block top-k"})
+                      "exact_pass_kernel": "tcgen05 kind::i8 tiles (k_mma_tiles) + block top-k",
+                      # 2 q n d int8 ops (u8 x u8 -> s32 MACs) over the whole pass incl. top-k
+                      "exact_pass_tops": 2.0 * qpr * n_loc * d / (ex_ms / 1e3) / 1e12,
+                      "exact_pass_x_GBps": n_loc * d / (ex_ms / 1e3) / 1e9})
 
     # end to end through the host API (pinned host buffers, H2D + D2H inside the timed region)
     e2e = None

@@ -2,7 +2,7 @@
 //
 // The batch's (query x point) grid is cut into tiles of R = 2^tile_lr queries x
 // P = 2^tile_lp points.  k_filter adds, per tile, the draws its blockers take this
-// round (tilework); a tile whose draws reach tile_row_draws * (R + P) is advanced here instead of
+// round (tilework); a tile whose draws reach tile_min_draws is advanced here instead of
 // through the work lists (k_scatter leaves its pairs out): the CTA copies the R
 // query rows and P point rows into shared memory once with 16-byte loads, then every
 // draw of every listed pair of the tile gathers its two bytes from there.
@@ -67,34 +67,70 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
   const int sl = g.tile_slot_l;
   const uint32_t slot = 1u << sl;
   // rows: [R query rows][P point rows], slot-aligned; then acc [RP] int32, lst [RP] u16
+  // dynamic shared memory: [acc RP int32 | lst RP u16 | sact RP u8] at its start, then
+  // the R + P row slots from the next slot boundary (the host sized it for that)
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(tsm);
-  const uint32_t rows_s = (base + slot - 1) & ~(slot - 1);
-  unsigned char *rows_g = tsm + (rows_s - base);
-  int32_t *acc = reinterpret_cast<int32_t *>(rows_g + (size_t)(R + P) * slot);
+  int32_t *acc = reinterpret_cast<int32_t *>(tsm);
   uint16_t *lst = reinterpret_cast<uint16_t *>(acc + RP);
   uint8_t *sact = reinterpret_cast<uint8_t *>(lst + RP);  // [RP] action bytes of the tile
+  const uint32_t rows_s = (base + (uint32_t)RP * 7u + slot - 1) & ~(slot - 1);
+  {
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    if (rows_s + ((uint32_t)(R + P) << sl) > base + dyn) __trap();  // host sizing broken: fail loudly
+  }
   const uint32_t xs = rows_s + ((uint32_t)R << sl);  // first point row
   const int tid = threadIdx.x;
   const int rows = (g.q + R - 1) >> g.tile_lr;
   const uint32_t d = (uint32_t)g.d;
-  const unsigned ntiles = g.ctl->n_tiles;
+  const long long cols = (g.n + P - 1) >> g.tile_lp;
+  const long long ntot = (long long)rows * cols;
+  const float dthr = g.tile_min_draws;
+  __shared__ uint8_t dlist[TILE_NT];  // dense tiles of the chunk (offsets, in order)
+  __shared__ unsigned wcnt[TILE_NT / 32];
 
+  // each CTA walks a contiguous range of the point-major tile space (t = tp * rows +
+  // tr), so consecutive dense tiles of one point column reuse the staged point rows;
+  // density is read 256 tiles at a time and compacted in order
+  const long long t0 = (long long)blockIdx.x * ntot / gridDim.x, t1 = (long long)(blockIdx.x + 1) * ntot / gridDim.x;
+  int staged_tp = -1;
   unsigned long long my_blocks = 0;  // Philox blocks drawn (statistics)
-  for (unsigned ti = blockIdx.x; ti < ntiles; ti += gridDim.x) {
-    const uint32_t t = g.tilelist[ti];
-    const int tp = (int)(t / (unsigned)rows), tr = (int)(t % (unsigned)rows);
+  for (long long c0 = t0; c0 < t1; c0 += TILE_NT) {
+    __syncthreads();  // dlist of the previous chunk is consumed
+    {
+      const long long t = c0 + tid;
+      bool dense = false;
+      if (t < t1) {
+        const int tp = (int)(t / rows), tr = (int)(t % rows);
+        dense = (float)g.tilework[(size_t)tr * g.tile_cols + tp] >= dthr;
+      }
+      const unsigned m = __ballot_sync(FULL, dense);
+      if (lane_id() == 0) wcnt[tid >> 5] = __popc(m);
+      __syncthreads();
+      unsigned before = 0;
+      for (int w = 0; w < (tid >> 5); ++w) before += wcnt[w];
+      if (dense) dlist[before + __popc(m & ((1u << lane_id()) - 1u))] = (uint8_t)(t - c0);
+    }
+    __syncthreads();
+    unsigned nd = 0;
+    for (int w = 0; w < TILE_NT / 32; ++w) nd += wcnt[w];
+  for (unsigned ti = 0; ti < nd; ++ti) {
+    const long long t = c0 + dlist[ti];
+    const int tp = (int)(t / rows), tr = (int)(t % rows);
     const int r0 = tr << g.tile_lr, p0 = tp << g.tile_lp;
+    const bool reuse_x = tp == staged_tp;  // the point rows of this column are staged
+    staged_tp = tp;
     __syncthreads();  // the previous tile's shared memory is no longer in use
     if (tid < MAX_LEVELS) lcnt[tid] = 0;
 
     // stage the rows: asynchronous 16-byte copies (cp.async), all in flight at once;
     // rows past q / n are never referenced and are left as they are
-    for (int v = tid; v < (R + P) * nv; v += TILE_NT) {
+    for (int v = tid; v < (reuse_x ? R : R + P) * nv; v += TILE_NT) {
       const int row = v / nv, c = v - row * nv;
       const uint8_t *src = nullptr;
       if (row < R) {
         if (r0 + row < g.q) src = g.Q + (size_t)(r0 + row) * pitch + 16 * c;
-      } else if (p0 + row - R < g.n) {
+      } else if (!reuse_x && p0 + row - R < g.n) {
         src = g.X + (size_t)(p0 + row - R) * pitch + 16 * c;
       }
       if (src)
@@ -257,34 +293,8 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
       *reinterpret_cast<uint32_t *>(g.lvl + o4) = l4;
     }
   }
-  if (threadIdx.x == 0 && my_blocks) atomicAdd(&g.ctl->tile_blocks, my_blocks);
-}
-
-// The dense tiles of this round (tilework >= tile_row_draws * (R + P)) in point-major
-// numbering t = tp * rows + tr.  Runs after k_scatter (k_filter rewrites every count).
-__global__ void k_tile_list(Geom g) {
-  const int rows = (g.q + (1 << g.tile_lr) - 1) >> g.tile_lr;
-  const int cols = (g.n + (1 << g.tile_lp) - 1) >> g.tile_lp;
-  const unsigned t = blockIdx.x * blockDim.x + threadIdx.x;
-  bool dense = false;
-  if (t < (unsigned)rows * (unsigned)cols) {
-    const int tp = (int)(t / (unsigned)rows), tr = (int)(t % (unsigned)rows);
-    dense = (float)g.tilework[(size_t)tr * g.tile_cols + tp] >=
-            g.tile_row_draws * (float)((1 << g.tile_lr) + (1 << g.tile_lp));
   }
-  const unsigned m = __ballot_sync(FULL, dense);
-  unsigned b = 0;
-  if (lane_id() == 0 && m) b = atomicAdd(&g.ctl->n_tiles, (unsigned)__popc(m));
-  b = __shfl_sync(FULL, b, 0);
-  if (dense) g.tilelist[b + __popc(m & ((1u << lane_id()) - 1u))] = t;
-}
-
-cudaError_t launch_tile_list(const Geom &g, cudaStream_t s) {
-  const long long rows = (g.q + (1ll << g.tile_lr) - 1) >> g.tile_lr;
-  const long long cols = (g.n + (1ll << g.tile_lp) - 1) >> g.tile_lp;
-  const long long nt = rows * cols;
-  if (nt > 0) k_tile_list<<<(unsigned)((nt + 255) / 256), 256, 0, s>>>(g);
-  return cudaGetLastError();
+  if (threadIdx.x == 0 && my_blocks) atomicAdd(&g.ctl->tile_blocks, my_blocks);
 }
 
 int tile_slot_log2(int64_t pitch) {
@@ -293,13 +303,34 @@ int tile_slot_log2(int64_t pitch) {
   return l;
 }
 
-size_t tile_smem_bytes(int lr, int lp, int64_t pitch) {
+// The tile kernel's shared-memory window per CTA (static + reserved + dynamic), given
+// where its dynamic region starts (`base`): the small arrays, then the row slots from
+// the next slot boundary.
+static size_t tile_window(int lr, int lp, int64_t pitch, size_t base) {
   const size_t R = (size_t)1 << lr, P = (size_t)1 << lp, slot = (size_t)1 << tile_slot_log2(pitch);
-  return (R + P + 1) * slot + R * P * (4 + 2 + 1);  // + one slot of alignment slack
+  const size_t rows0 = (base + R * P * 7 + slot - 1) / slot * slot;
+  return rows0 + (R + P) * slot;
 }
 
+static size_t tile_base() {  // static shared memory + the per-CTA system reservation
+  static size_t b = [] {
+    cudaFuncAttributes fa{};
+    int dev = 0, rsv = 0;
+    if (cudaFuncGetAttributes(&fa, k_advance_tiles) != cudaSuccess) fa.sharedSizeBytes = 2048;
+    if (cudaGetDevice(&dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev) != cudaSuccess)
+      rsv = 1024;
+    return (size_t)fa.sharedSizeBytes + (size_t)rsv;
+  }();
+  return b;
+}
+
+// Shared memory per CTA of a tile shape (the occupancy the shape chooser reasons about).
+size_t tile_smem_bytes(int lr, int lp, int64_t pitch) { return tile_window(lr, lp, pitch, tile_base()); }
+
 cudaError_t launch_advance_tiles(const Geom &g, int num_sms, cudaStream_t s) {
-  const size_t smem = tile_smem_bytes(g.tile_lr, g.tile_lp, g.pitch);
+  const size_t base = tile_base();
+  const size_t smem = tile_window(g.tile_lr, g.tile_lp, g.pitch, base) - base;
   cudaError_t e = cudaFuncSetAttribute(k_advance_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;

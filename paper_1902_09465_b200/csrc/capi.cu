@@ -254,9 +254,8 @@ aknn_status setup_exact_mma(aknn_index *ix, Geom &g, int64_t qb, uint8_t *ws, co
 }
 
 // Tile-staged level gathers (advance_tiles.cu) unless AKNN_FLAG_NO_TILES / AKNN_TILE=0.
-// Tile shape: the largest R = P (powers of two, <= 32) whose rows fit a third of the
-// SM's shared memory (3 CTAs per SM), else half, else all of it; rows of > 16 KB:
-// R = 1, P = 4.  AKNN_TILE_LR / AKNN_TILE_LP override (experiments).  A tile is dense
+// Tile shape: the largest R x P (powers of two, R <= P, 4 <= P <= 32) whose shared
+// memory fits 3 CTAs per SM, else 2, else 1.  AKNN_TILE_LR / AKNN_TILE_LP override (experiments).  A tile is dense
 // (staged) when its draws, at one 32-byte sector each on the list path, cost at least
 // AKNN_TILE_F (default 4) times its staging bytes (R + P) * pitch.
 struct TileShape {
@@ -272,23 +271,21 @@ int env_int(const char *name, int dflt) {
 TileShape tile_shape(int64_t pitch) {
   TileShape t{0, 0, 0, 0.f};
   if (env_int("AKNN_TILE", 1) == 0) return t;
+  // the largest tile (R * P) whose shared memory fits 3, 2 or 1 CTAs per SM (228 KB)
   int lr = -1, lp = -1;
-  for (size_t cap : {(size_t)75 * 1024, (size_t)112 * 1024, (size_t)220 * 1024}) {
-    for (int l = 5; l >= 2; --l)
-      if (tile_smem_bytes(l, l, pitch) <= cap) {
-        lr = lp = l;
-        break;
-      }
+  for (size_t cap : {(size_t)233472 / 3, (size_t)233472 / 2, (size_t)233472}) {
+    for (int a = 5; a >= 0; --a)
+      for (int b = 5; b >= 2; --b)
+        if (a <= b && tile_smem_bytes(a, b, pitch) <= cap && (lr < 0 || a + b > lr + lp)) {
+          lr = a;
+          lp = b;
+        }
     if (lr >= 0) break;
-  }
-  if (lr < 0 && tile_smem_bytes(0, 2, pitch) <= (size_t)220 * 1024) {
-    lr = 0;
-    lp = 2;
   }
   if (lr < 0) return t;
   t.lr = env_int("AKNN_TILE_LR", lr);
   t.lp = env_int("AKNN_TILE_LP", lp);
-  if (t.lr < 0 || t.lr > 5 || t.lp < 2 || t.lp > 5 || tile_smem_bytes(t.lr, t.lp, pitch) > (size_t)220 * 1024)
+  if (t.lr < 0 || t.lr > 5 || t.lp < 2 || t.lp > 5 || tile_smem_bytes(t.lr, t.lp, pitch) > (size_t)233472)
     return TileShape{0, 0, 0, 0.f};
   const char *fe = getenv("AKNN_TILE_F");
   const double f = fe && fe[0] ? atof(fe) : 4.0;
@@ -300,7 +297,7 @@ TileShape tile_shape(int64_t pitch) {
 size_t tile_ws_bytes(int64_t qb, int64_t npad, const TileShape &t) {
   if (!t.on) return 0;
   const int64_t rows = (qb + (1ll << t.lr) - 1) >> t.lr, cols = (npad + (1ll << t.lp) - 1) >> t.lp;
-  return 2 * round_up((size_t)(rows * cols) * 4, 256);  // tilework + tilelist
+  return round_up((size_t)(rows * cols) * 4, 256);  // tilework
 }
 
 void setup_tiles(Geom &g, const TileShape &t, const aknn_opts &o, int64_t qb, uint8_t *ws) {
@@ -311,9 +308,10 @@ void setup_tiles(Geom &g, const TileShape &t, const aknn_opts &o, int64_t qb, ui
   g.tile_lp = t.lp;
   g.tile_cols = (int)((g.npad + (1ll << t.lp) - 1) >> t.lp);
   g.tilework = reinterpret_cast<uint32_t *>(ws);
-  g.tilelist = reinterpret_cast<uint32_t *>(ws + tile_ws_bytes(qb, g.npad, t) / 2);
   g.tile_slot_l = tile_slot_log2(g.pitch);
-  g.tile_row_draws = t.row_draws;
+  // consecutive tiles of a point column share the staged point rows: a tile stages
+  // about its R query rows (+ one point row's share)
+  g.tile_min_draws = t.row_draws * (float)((1 << t.lr) + 1);
 }
 
 // One round after the rank split: filter -> plan/scatter (+ dense-tile list) ->
@@ -525,7 +523,7 @@ aknn_status loop_graph(aknn_index *ix, const Geom &g, int nbits, int max_rounds,
 // Kernel launches per class (for aknn_stats; memset nodes excluded).
 int launches_init_of(const Geom &g) { return 2 + (g.exact_mma ? 1 : 0); }  // init, qstate, norms
 int launches_filter_of(const Geom &) { return 1; }
-int launches_compact_of(const Geom &g) { return 3 + (g.tile_on ? 1 : 0); }  // plan, scatter, lists (+ tiles)
+int launches_compact_of(const Geom &) { return 3; }  // plan, scatter, list sizes
 int launches_advance_of(const Geom &g) {
   return 1 + (g.exact_mma ? 1 : 0) + (g.stage_lo < MAX_LEVELS ? 1 : 0);
 }

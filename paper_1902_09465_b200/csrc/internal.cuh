@@ -55,7 +55,7 @@ struct QState {
 // Per-round control block (device memory; one per batch).
 struct RoundCtl {
   unsigned int n_active;                  // queries failing Eq. (5) this round
-  unsigned int n_tiles;                   // dense tiles listed for k_advance_tiles
+  unsigned int pad0;
   unsigned int cnt[NSLOT];                // pairs per action slot
   unsigned int off[NSLOT + 1];            // list offsets per slot
   unsigned int cursor[NSLOT];             // scatter cursors
@@ -123,8 +123,7 @@ struct Geom {
   int tile_lr, tile_lp;  // log2 R (queries per tile), log2 P (points per tile); R | 32, 4 <= P <= 32
   int tile_cols;         // row length of tilework: ceil(npad / P)
   uint32_t *tilework;    // [ceil(qb / R)][tile_cols] draws of the tile's sampled blockers
-  uint32_t *tilelist;    // dense tiles of this round (k_tile_list), ctl->n_tiles of them
-  float tile_row_draws;  // dense iff tilework >= tile_row_draws * (R + P)
+  float tile_min_draws;  // dense iff tilework >= tile_min_draws
   int tile_slot_l;       // log2 of a row slot in shared memory (>= pitch)
   unsigned long long *advanced;  // pairs advanced (statistics), device counter
   // the blocker predicate as integer thresholds per (query, level) (k_thresholds)

@@ -392,7 +392,7 @@ __global__ void __launch_bounds__(FIL_NT) k_scatter(Geom g) {
     const int tc = (c0 >> g.tile_lp) + t;
     const bool dense = tc < g.tile_cols &&
                        (float)g.tilework[(size_t)(qi >> g.tile_lr) * g.tile_cols + tc] >=
-                           g.tile_row_draws * (float)((1 << g.tile_lr) + (1 << g.tile_lp));
+                           g.tile_min_draws;
     sdense[t] = dense;
     if (!dense) any_listed = 1;
   }
@@ -868,10 +868,6 @@ cudaError_t launch_compact(const Geom &g, cudaStream_t s) {
   k_plan<<<1, 32, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo);
   k_scatter<<<dim3(g.q, cdiv(g.npad, FIL_NT * 4)), FIL_NT, 0, s>>>(g);
   k_plan_lists<<<1, 32, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo);  // the lists as written
-  if (g.tile_on) {
-    const cudaError_t e = launch_tile_list(g, s);
-    if (e != cudaSuccess) return e;
-  }
   return cudaGetLastError();
 }
 

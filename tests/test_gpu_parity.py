@@ -134,15 +134,18 @@ def test_config2_full_size_sampled_queries(ak):
     _assert_parity(got, ref, rows=rows)
 
 
-@pytest.mark.parametrize("i,nsample", [(3, 1), (4, 2)])
+@pytest.mark.parametrize("i,nsample", [(3, 1), (4, 2), (5, 1)])
 def test_full_size_configs_sampled_queries(ak, i, nsample):
-    """Configs 3 and 4 at their BASELINE sizes through the bench launch path (device API,
+    """Configs 3 and 4 at their BASELINE sizes, config 5 at one GPU's shard (its first
+    1,000,000 rows: the N=1 bench workload), through the bench launch path (device API,
     the whole query batch in one call, graph-launched loop); the oracle recomputes
     `nsample` seeded queries of the batch in full (sets, d_hat, per-pair T and S,
     draws, evals, rounds)."""
     import torch
     cfg = synth.config(i)
-    X = synth.points(cfg)
+    X = synth.points(cfg, 0, 1_000_000) if cfg.shards > 1 else synth.points(cfg)
+    if cfg.shards > 1:
+        cfg = synth.config(i, n=X.shape[0])
     Q = synth.queries(cfg)
     al = orc.alpha_theory(cfg.n, cfg.delta, cfg.d)
     ix = ak.Index(torch.from_numpy(X).cuda())
