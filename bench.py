@@ -53,6 +53,9 @@ def _args():
     ap.add_argument("--alpha", default="theory",
                     help="'theory' (footnote 2, P:132-138) or 'exp:<C_alpha>' (§5, P:349)")
     ap.add_argument("--q", type=int, default=0, help="override queries per rank (0 = config)")
+    ap.add_argument("--draws", choices=("per-query", "shared"), default="per-query",
+                    help="per-query Philox streams (default, DESIGN.md R19) or query-independent "
+                         "draws (SURVEY §8(f1), AKNN_FLAG_SHARED_DRAWS)")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-exact", action="store_true")
@@ -273,17 +276,18 @@ def _orc_worker(i):
     import oracle.oracle as orc
     X, Q, cfg, al = _ORC["X"], _ORC["Q"], _ORC["cfg"], _ORC["alpha"]
     r = orc.query_br(X, Q[i:i + 1], cfg.k, cfg.h, cfg.seed, al,
-                     qids=np.array([i], np.int32), want_counts=False)
+                     qids=np.array([i], np.int32), want_counts=False,
+                     shared_draws=_ORC.get("shared", False))
     return int(r["evals"][0])
 
 
-def _oracle_time(X, Q, cfg, alpha, nq: int, cores: int):
+def _oracle_time(X, Q, cfg, alpha, nq: int, cores: int, shared: bool = False):
     """Wall time of the oracle (as it stands, single-threaded C) on nq queries spread
     over `cores` worker processes (one query per task)."""
     import multiprocessing as mp
     import oracle.oracle as orc
     orc.lib()  # build/load before forking
-    _ORC.update(X=X, Q=Q, cfg=cfg, alpha=alpha)
+    _ORC.update(X=X, Q=Q, cfg=cfg, alpha=alpha, shared=shared)
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
     with ctx.Pool(cores) as pool:
@@ -324,7 +328,7 @@ def run_reference(args, dist: Dist):
     times = []
     for it in range(args.warmup + args.steps):
         off = (it * nq) % max(1, cfg.q - nq + 1)
-        dt, _ = _oracle_time(X, Q[off:off + nq], cfg, al, nq, cores)
+        dt, _ = _oracle_time(X, Q[off:off + nq], cfg, al, nq, cores, args.draws == "shared")
         if it >= args.warmup:
             times.append(dt)
     ms = 1e3 * sum(times) / len(times)
@@ -343,7 +347,8 @@ def run_reference(args, dist: Dist):
 
 
 def _config_desc(cfg, args, extra=None):
-    d = {"workload": cfg.name, "n": cfg.n, "d": cfg.d, "q_per_rank": cfg.q, "k": cfg.k,
+    d = {"workload": cfg.name + ("_shared_draws" if getattr(args, "draws", "per-query") == "shared" else ""),
+         "n": cfg.n, "d": cfg.d, "q_per_rank": cfg.q, "k": cfg.k,
          "h": cfg.h, "delta": cfg.delta, "seed": cfg.seed, "alpha": _alpha_desc(args.alpha),
          "parallelism": f"query-parallel x{args.gpus} (X replicated)" if args.gpus > 1 else "1 GPU",
          "l2": "flushed before every step (512 MiB write, outside the timed events)"}
@@ -402,6 +407,7 @@ def run_ours(args, dist: Dist):
                draws=torch.empty(qpr, dtype=torch.int64, device=dev),
                rounds=torch.empty(qpr, dtype=torch.int32, device=dev))
     qi_off = 0 if sharded else dist.rank * qpr
+    qflags = ak.FLAG_SHARED_DRAWS if args.draws == "shared" else 0
 
     def step(timing: bool):
         flush.zero_()
@@ -409,7 +415,7 @@ def run_ours(args, dist: Dist):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         ix.query_device(Qd, k, h, cfg.delta, cfg.seed, alpha_d, qi_offset=qi_off, timing=timing,
-                        stream=stream, out=out)
+                        stream=stream, out=out, flags=qflags)
         e1.record(stream)
         torch.cuda.synchronize()
         return e0.elapsed_time(e1), ix.stats()
@@ -568,14 +574,14 @@ def run_ours(args, dist: Dist):
                     rounds=torch.empty(qpr, dtype=torch.int32).pin_memory().numpy())
         Qpin_np = Qpin.numpy()
         for _ in range(1):
-            ix.query(Qpin_np, k, h, cfg.delta, cfg.seed, alpha, qi_offset=qi_off, out=hout)
+            ix.query(Qpin_np, k, h, cfg.delta, cfg.seed, alpha, qi_offset=qi_off, out=hout, flags=qflags)
         dist.barrier()
         wall = []
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            ix.query(Qpin_np, k, h, cfg.delta, cfg.seed, alpha, qi_offset=qi_off, out=hout)
+            ix.query(Qpin_np, k, h, cfg.delta, cfg.seed, alpha, qi_offset=qi_off, out=hout, flags=qflags)
             wall.append(time.perf_counter() - t0)
         e2e_s = dist.max(sum(wall))
         h2d = Qh.nbytes + alpha.nbytes
@@ -591,7 +597,7 @@ def run_ours(args, dist: Dist):
         # a bounded sample of the same workload: ~10-30 s of oracle work on the host cores
         cores = max(1, min(_cpu_cores(), 16))
         nq = min(qpr, 8 * cores if n <= 200_000 else cores)
-        dt, _ = _oracle_time(X, Qh, cfg, _oracle_alpha(cfg, args.alpha), nq, cores)
+        dt, _ = _oracle_time(X, Qh, cfg, _oracle_alpha(cfg, args.alpha), nq, cores, args.draws == "shared")
         cpu = {"value": nq / dt, "unit": UNIT, "cores": min(cores, nq), "kind": "oracle",
                "sample": f"first {nq} queries of {cfg.name} (full n={n}, d={d}), one "
                          f"single-threaded oracle process per core, {dt:.1f} s wall"}

@@ -92,6 +92,12 @@ typedef struct {
 /* bit 3: every 128 x 256 tile with an exact fallback runs on the tensor cores (by
    default tiles with fewer than 512 of them stream rows instead; identical results) */
 #define AKNN_FLAG_EXACT_MMA_ALL 8
+/* bit 4: query-independent coordinate draws: the Philox counter's
+   query word is 0xFFFFFFFF for every query, so arm i's t-th sampled coordinate is the
+   same for all queries (each query's samples stay i.i.d. uniform, so the
+   guarantee of P:395-399 holds per query).  A different -- equally valid -- stream:
+   results differ from the default and match the oracle run with qids = 0xFFFFFFFF. */
+#define AKNN_FLAG_SHARED_DRAWS 16
 
 /* Execution statistics of the last query call on an index (aknn_get_stats).
  * Kernel classes: init (a2), select (a6-a7: rank split, bounds, Eq. 5),

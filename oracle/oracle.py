@@ -134,9 +134,15 @@ def round_step(S, T, d: int, k: int, h: int, alpha, want_active: bool = True):
                 active=None if act is None else act.astype(bool))
 
 
+SHARED_QI = 0xFFFFFFFF  # the counter word of query-independent draws
+
+
 def query_br(X, Q, k: int, h: int, seed: int, alpha, qids=None, id_offset: int = 0,
-             max_rounds: int = 0, want_counts: bool = True, want_sums: bool = False):
-    """Batched round rule BR, one query at a time."""
+             max_rounds: int = 0, want_counts: bool = True, want_sums: bool = False,
+             shared_draws: bool = False):
+    """Batched round rule BR, one query at a time.  shared_draws:
+    every query's counter word is SHARED_QI, i.e. arm i's t-th coordinate is the same
+    for all queries; each query alone is unchanged in law."""
     X = np.ascontiguousarray(X, np.uint8)
     Q = np.ascontiguousarray(np.atleast_2d(Q), np.uint8)
     alpha = np.ascontiguousarray(alpha, np.float64)
@@ -144,6 +150,8 @@ def query_br(X, Q, k: int, h: int, seed: int, alpha, qids=None, id_offset: int =
     q = Q.shape[0]
     assert Q.shape[1] == d and alpha.shape[0] == d + 1
     qids = np.arange(q, dtype=np.int32) if qids is None else np.ascontiguousarray(qids, np.int32)
+    if shared_draws:
+        qids = np.full(q, SHARED_QI, np.uint32).view(np.int32)
     kh = k + h
     out = dict(
         sets=np.zeros((q, kh), np.int32), dhat=np.zeros((q, kh), np.float64),

@@ -51,6 +51,7 @@ FLAG_RADIX_SELECT = 1
 FLAG_EXACT_ROWS = 2  # exact fallbacks as per-pair row streams instead of tensor-core tiles
 FLAG_NO_TILES = 4  # every level gather through the work lists (no shared-memory tiles)
 FLAG_EXACT_MMA_ALL = 8  # every tile with an exact fallback on the tensor cores
+FLAG_SHARED_DRAWS = 16  # query-independent coordinate draws
 
 
 class Stats(C.Structure):

@@ -59,6 +59,117 @@ __device__ __forceinline__ uint32_t sq_diff4(uint32_t xa, uint32_t qa, uint4 w, 
   return __dp4a(t, t, acc);
 }
 
+// ---------------------------------------------------------------------------
+// Query-independent draws (AKNN_FLAG_SHARED_DRAWS) with R = 32 query
+// rows per tile: arm p's t-th coordinate is the same for every query, so a level's
+// draws of a point column are generated ONCE (Philox + the point's byte) into a
+// packed list (j | x_j << 16) and every query row of every tile of the column reuses
+// them: the per-pair work is one conflict-free byte gather from the transposed query
+// tile Qt[j][32] (lane = query row) and one multiply-add.  Philox work drops by the
+// 32 query rows of a tile (and by the column's tile rows when a level fits one chunk).
+constexpr int F1_R = 32;
+
+// Qt[j * 32 + r] = Q[r0 + r][j] for the tile's 32 query rows: 4 x 4 byte blocks
+// transposed with PRMT (4-byte loads, 4-byte stores); QT_U blocks per thread in flight.
+constexpr int QT_U = 4;
+__device__ __forceinline__ void f1_stage_qt(const Geom &g, int r0, uint32_t *qt) {
+  const int nj4 = (int)(g.pitch >> 2);  // 4-byte columns (pitch is a multiple of 16)
+  const int total = 8 * nj4;
+  for (int it0 = threadIdx.x; it0 < total; it0 += TILE_NT * QT_U) {
+    uint32_t a[QT_U][4];
+#pragma unroll
+    for (int u = 0; u < QT_U; ++u) {
+      const int it = it0 + u * TILE_NT, rb = it & 7, jb = it >> 3;
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const int r = r0 + rb * 4 + k;
+        a[u][k] = (it < total && r < g.q) ? __ldg(reinterpret_cast<const uint32_t *>(g.Q + (size_t)r * g.pitch) + jb) : 0u;
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < QT_U; ++u) {
+      const int it = it0 + u * TILE_NT, rb = it & 7, jb = it >> 3;
+      if (it >= total) break;
+      const uint32_t t01 = __byte_perm(a[u][0], a[u][1], 0x5140), t23 = __byte_perm(a[u][2], a[u][3], 0x5140);
+      const uint32_t u01 = __byte_perm(a[u][0], a[u][1], 0x7362), u23 = __byte_perm(a[u][2], a[u][3], 0x7362);
+      uint32_t *col = qt + (size_t)(jb * 4) * (F1_R / 4) + rb;  // word (j * 32 + 4 rb) / 4
+      col[0 * (F1_R / 4)] = __byte_perm(t01, t23, 0x5410);
+      col[1 * (F1_R / 4)] = __byte_perm(t01, t23, 0x7632);
+      col[2 * (F1_R / 4)] = __byte_perm(u01, u23, 0x5410);
+      col[3 * (F1_R / 4)] = __byte_perm(u01, u23, 0x7632);
+    }
+  }
+}
+
+// The draws u0 .. u0+ch-1 of level c for the P points of the column: dbuf[p * ch + u]
+// = j | X[p0 + p][j] << 16.  Returns the Philox blocks drawn.
+__device__ __forceinline__ unsigned f1_generate(const Geom &g, int p0, int P, int c, unsigned u0, unsigned ch,
+                                                uint32_t *dbuf) {
+  const unsigned s = 1u << c;
+  const unsigned nbk = (ch + 3) / 4;  // blocks of this chunk per point
+  const uint32_t lv = (uint32_t)(c + 1), d = (uint32_t)g.d;
+  for (unsigned it = threadIdx.x; it < (unsigned)P * nbk; it += TILE_NT) {
+    const int p = (int)(it / nbk);
+    const unsigned bk = it - (unsigned)p * nbk, u = u0 + 4 * bk;
+    const int i = p0 + p;
+    const uint8_t *xr = g.X + (size_t)(i < g.n ? i : 0) * g.pitch;
+    const uint4 w = philox4x32_10_rk(make_uint4(u >> 2, (uint32_t)i + g.id_offset, SHARED_QI, lv), g.rk0, g.rk1);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      if (u + e < s && u + e < u0 + ch) {
+        const uint32_t j = coord_of(ws[e], d);
+        dbuf[p * ch + (u - u0) + e] = j | ((uint32_t)__ldg(xr + j) << 16);
+      }
+    }
+  }
+  return (unsigned)P * nbk;
+}
+
+// Sum over the chunk's draws of (x_j - Qt[j][r])^2 for pair (r = lane, p): warp w takes
+// points w, w + 8, ...; acc[k] accumulates point w + 8k.  qt_s / dbuf_s: shared-memory
+// addresses; ch is a multiple of 4 except for levels 0 and 1 (1 and 2 draws).
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+  uint32_t v;
+  asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+  return v;
+}
+__device__ __forceinline__ uint4 lds_u128(uint32_t addr) {
+  uint4 v;
+  asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(addr));
+  return v;
+}
+
+__device__ __forceinline__ void f1_accumulate(uint32_t qt_s, uint32_t dbuf_s, int P, unsigned ch, uint32_t (&acc)[4]) {
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t ql = qt_s + lane;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const uint32_t p = warp + 8 * k;
+    if (p >= (uint32_t)P) break;
+    const uint32_t dp = dbuf_s + p * ch * 4u;
+    uint32_t sum = 0;
+    if ((ch & 3u) == 0) {
+      for (uint32_t u = 0; u < ch; u += 4) {
+        const uint4 pk = lds_u128(dp + u * 4u);  // broadcast
+        const uint32_t v[4] = {pk.x, pk.y, pk.z, pk.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int diff = (int)(v[e] >> 16) - (int)lds_u8(ql + (v[e] & 0xFFFFu) * F1_R);
+          sum += (uint32_t)(diff * diff);
+        }
+      }
+    } else {
+      for (uint32_t u = 0; u < ch; ++u) {
+        const uint32_t v = lds_u32(dp + u * 4u);
+        const int diff = (int)(v >> 16) - (int)lds_u8(ql + (v & 0xFFFFu) * F1_R);
+        sum += (uint32_t)(diff * diff);
+      }
+    }
+    acc[k] += sum;
+  }
+}
+
 __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
   extern __shared__ __align__(16) unsigned char tsm[];
   __shared__ unsigned lcnt[MAX_LEVELS], loff[MAX_LEVELS + 1], lfill[MAX_LEVELS];
@@ -94,6 +205,7 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
   // density is read 256 tiles at a time and compacted in order
   const long long t0 = (long long)blockIdx.x * ntot / gridDim.x, t1 = (long long)(blockIdx.x + 1) * ntot / gridDim.x;
   int staged_tp = -1;
+  int gen_tp = -1, gen_c = -1;  // shared draws: the column / level whose draw list is in dbuf
   unsigned long long my_blocks = 0;  // Philox blocks drawn (statistics)
   for (long long c0 = t0; c0 < t1; c0 += TILE_NT) {
     __syncthreads();  // dlist of the previous chunk is consumed
@@ -120,12 +232,15 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
     const int r0 = tr << g.tile_lr, p0 = tp << g.tile_lp;
     const bool reuse_x = tp == staged_tp;  // the point rows of this column are staged
     staged_tp = tp;
+    const bool f1 = g.shared_draws && R == F1_R;  // query-independent draws, R = 32
     __syncthreads();  // the previous tile's shared memory is no longer in use
     if (tid < MAX_LEVELS) lcnt[tid] = 0;
 
     // stage the rows: asynchronous 16-byte copies (cp.async), all in flight at once;
-    // rows past q / n are never referenced and are left as they are
-    for (int v = tid; v < (reuse_x ? R : R + P) * nv; v += TILE_NT) {
+    // rows past q / n are never referenced and are left as they are.  Shared draws:
+    // the query rows transposed (Qt), no point rows (their bytes are in the draw list)
+    if (f1) f1_stage_qt(g, r0, reinterpret_cast<uint32_t *>(tsm + (rows_s - base)));
+    for (int v = tid; v < (f1 ? 0 : (reuse_x ? R : R + P) * nv); v += TILE_NT) {
       const int row = v / nv, c = v - row * nv;
       const uint8_t *src = nullptr;
       if (row < R) {
@@ -201,8 +316,40 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
     // reduce inside the lane group; every pair's sum is written by one thread.
     unsigned lmask = 0;  // levels present in the tile
     for (int c = 0; c < MAX_LEVELS; ++c) lmask |= (lcnt[c] != 0u) << c;
-    if (tid == 0)
+    if (f1) {
+      // shared draws: per level, the column's draw list (cached across the column's
+      // tiles while a level fits one chunk), then every (row, point) pair of the tile
+      uint32_t *dbuf = reinterpret_cast<uint32_t *>(tsm + (rows_s - base) + ((size_t)R << sl));
+      const uint32_t qt_s = rows_s, dbuf_s = rows_s + ((uint32_t)R << sl);
+      const unsigned chmax = min(256u, (1u << sl) / 4u);
+      for (; lmask; lmask &= lmask - 1) {
+        const int c = __ffs(lmask) - 1;
+        const unsigned s = 1u << c;
+        uint32_t accp[4] = {0u, 0u, 0u, 0u};
+        for (unsigned u0 = 0; u0 < s; u0 += chmax) {
+          const unsigned ch = min(chmax, s - u0);
+          const bool cached = s <= chmax && gen_tp == tp && gen_c == c;
+          if (!cached) {
+            __syncthreads();  // the previous chunk's draws are consumed
+            const unsigned nb = f1_generate(g, p0, P, c, u0, ch, dbuf);
+            if (tid == 0) my_blocks += nb;
+            __syncthreads();
+            gen_tp = s <= chmax ? tp : -1;
+            gen_c = c;
+          }
+          f1_accumulate(qt_s, dbuf_s, P, ch, accp);
+        }
+        // pair (lane, warp + 8k): its sum if it advances at this level
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const int p = (tid >> 5) + 8 * k, e = lane_id() * P + p;
+          if (p < P && sact[e] == (uint8_t)(c + 1)) acc[e] = (int32_t)accp[k];
+        }
+      }
+      lmask = 0;  // done: skip the per-pair Philox path below
+    } else if (tid == 0) {
       for (int c = 0; c < MAX_LEVELS; ++c) my_blocks += (unsigned long long)lcnt[c] << (c < 2 ? 0 : c - 2);
+    }
     for (; lmask; lmask &= lmask - 1) {
       const int c = __ffs(lmask) - 1;
       const unsigned m = lcnt[c];
@@ -222,7 +369,7 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
             pr[k] = ok ? (int)L[li] : -1;
             const int e = ok ? pr[k] : 0;
             const uint32_t gi = (uint32_t)(p0 + (e & (P - 1))) + g.id_offset;
-            const uint32_t gq = (uint32_t)(r0 + (e >> g.tile_lp)) + g.qi0;
+            const uint32_t gq = rng_qi(g, (uint32_t)(r0 + (e >> g.tile_lp)));
             w[k] = philox4x32_10_rk(make_uint4((uint32_t)k & (nb - 1), gi, gq, lv), g.rk0, g.rk1);
           }
           uint32_t sum = 0;
@@ -256,7 +403,7 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
           const uint32_t xa = xs + ((uint32_t)(pe & (P - 1)) << sl);
           const uint32_t qa = rows_s + ((uint32_t)(pe >> g.tile_lp) << sl);
           const uint32_t gi = (uint32_t)(p0 + (pe & (P - 1))) + g.id_offset;
-          const uint32_t gq = (uint32_t)(r0 + (pe >> g.tile_lp)) + g.qi0;
+          const uint32_t gq = rng_qi(g, (uint32_t)(r0 + (pe >> g.tile_lp)));
           uint32_t sum = 0;
           if (ok) {
             for (unsigned b0 = sub * ADV_TP; b0 < nb; b0 += tpp * ADV_TP) {

@@ -663,6 +663,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   g.cmax = kg.cmax;
   g.adv_bpl = adv_bpl();
   g.force_radix = (o.flags & AKNN_FLAG_RADIX_SELECT) ? 1 : 0;
+  g.shared_draws = (o.flags & AKNN_FLAG_SHARED_DRAWS) ? 1 : 0;
   g.stage_lo = stage_level(g.pitch);
   TRY(setup_exact_mma(ix, g, qb, ix->ws.as<uint8_t>(oXm), o, st));
   setup_tiles(g, tsh, o, qb, ix->ws.as<uint8_t>(oTw));
@@ -909,6 +910,8 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     g.cmax = kg[si].cmax;
     g.adv_bpl = adv_bpl();
     g.force_radix = (o.flags & AKNN_FLAG_RADIX_SELECT) ? 1 : 0;
+    g.shared_draws = (o.flags & AKNN_FLAG_SHARED_DRAWS) ? 1 : 0;
+  g.shared_draws = (o.flags & AKNN_FLAG_SHARED_DRAWS) ? 1 : 0;
     g.stage_lo = stage_level(g.pitch);
     g.world = W;
     g.recv_stride = recv_stride;

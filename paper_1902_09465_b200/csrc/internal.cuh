@@ -96,6 +96,7 @@ struct Geom {
   int k, h;
   uint32_t id_offset;    // global id of local row 0
   uint32_t qi0;          // RNG query index of batch row 0
+  int shared_draws;      // 1: query-independent draws: counter word 0xFFFFFFFF
   uint32_t seed_lo, seed_hi;
   uint32_t rk0[10], rk1[10]; // Philox round keys of (seed_lo, seed_hi): kernel-param
                              // constants, so each round's key XOR is one LOP3
@@ -156,6 +157,12 @@ __device__ __forceinline__ uint4 philox4x32_10_rk(uint4 c, const uint32_t *rk0, 
   }
   return c;
 }
+
+// The query word of the Philox counter of batch row qi (R19): the query's
+// RNG index, or -- with query-independent draws -- one word shared by
+// every query, so that arm i's t-th coordinate is the same for all queries.
+constexpr uint32_t SHARED_QI = 0xFFFFFFFFu;
+__device__ __forceinline__ uint32_t rng_qi(const Geom &g, uint32_t qi) { return g.shared_draws ? SHARED_QI : qi + g.qi0; }
 
 // Multiply-high map of a 32-bit word onto [0, d) (reading R5).
 __device__ __forceinline__ uint32_t coord_of(uint32_t w, uint32_t d) { return __umulhi(w, d); }

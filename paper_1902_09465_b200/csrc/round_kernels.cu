@@ -33,7 +33,7 @@ __global__ void k_init(Geom g) {
     g.act[o] = 0;
     return;
   }
-  const uint4 w = philox4x32_10(make_uint4(0u, (uint32_t)i + g.id_offset, (uint32_t)qi + g.qi0, 0u),
+  const uint4 w = philox4x32_10(make_uint4(0u, (uint32_t)i + g.id_offset, rng_qi(g, (uint32_t)qi), 0u),
                                 g.seed_lo, g.seed_hi);
   const uint32_t j = coord_of(w.x, (uint32_t)g.d);
   const int diff = (int)__ldg(g.X + (size_t)i * g.pitch + j) - (int)__ldg(g.Q + (size_t)qi * g.pitch + j);
@@ -615,7 +615,7 @@ __global__ void __launch_bounds__(ADV_NT) k_advance(Geom g) {
         code[k] = ok ? lst[p] : 0u;
         decode(g, code[k], imask, qi, i);
         t[k] = BlockTask{g.X + (size_t)i * g.pitch, g.Q + (size_t)qi * g.pitch, i + g.id_offset,
-                         qi + g.qi0, blk, ok};
+                         rng_qi(g, qi), blk, ok};
       }
       uint32_t acc[ADV_P];
       draw_blocks(g, t, c, s, acc);
@@ -647,7 +647,7 @@ __global__ void __launch_bounds__(ADV_NT) k_advance(Geom g) {
       const uint8_t *qr = reinterpret_cast<const uint8_t *>(
           __shfl_sync(FULL, reinterpret_cast<unsigned long long>(g.Q + (size_t)qi * g.pitch), lane));
       if (ok) {
-        const uint32_t gi = i + g.id_offset, gq = qi + g.qi0, lv = (uint32_t)(c + 1);
+        const uint32_t gi = i + g.id_offset, gq = rng_qi(g, qi), lv = (uint32_t)(c + 1);
         for (unsigned b0 = sub * ADV_P; b0 < nb; b0 += tpp * ADV_P) sum += draw4_pair(g, xr, qr, gi, gq, lv, b0);
       }
       for (unsigned o = tpp >> 1; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
@@ -709,7 +709,7 @@ __global__ void __launch_bounds__(ADV_NT) k_advance_staged(Geom g) {
     __syncwarp();
     const uint8_t *sxb = reinterpret_cast<const uint8_t *>(sx);
     const uint8_t *qr = g.Q + (size_t)qi * g.pitch;
-    const uint32_t gi = i + g.id_offset, gq = qi + g.qi0, lv = (uint32_t)(c + 1);
+    const uint32_t gi = i + g.id_offset, gq = rng_qi(g, qi), lv = (uint32_t)(c + 1);
     uint32_t sum = 0;
     for (unsigned b0 = lane * ADV_P; b0 < nb; b0 += 32 * ADV_P) sum += draw4_pair_srow(g, sxb, qr, gi, gq, lv, b0);
 #pragma unroll

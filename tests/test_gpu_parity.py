@@ -347,3 +347,42 @@ def test_async_call_defers_stats(ak):
         assert np.array_equal(a2[key].cpu().numpy(), h2[key]), key
     for key in ("draws", "rounds", "exact_fallbacks", "philox_blocks", "query_rounds", "kernel_launches"):
         assert s2[key] == hs2[key], key
+
+
+# --------------------------------------------------------------- query-independent draws
+@pytest.mark.parametrize("n,d,q,k,h,kind", [(3001, 256, 40, 4, 6, "theory"), (1237, 100, 70, 3, 4, "exp"),
+                                            (2000, 784, 35, 10, 10, "theory"), (700, 5000, 3, 4, 4, "theory")])
+def test_shared_draws_bit_exact(ak, n, d, q, k, h, kind):
+    """AKNN_FLAG_SHARED_DRAWS == the oracle with the shared counter word,
+    through the tiles and through the lists."""
+    X, Q = synth.small_instance(n + 5 * d, n, d, q=q)
+    al = orc.alpha_theory(n, 0.05, d) if kind == "theory" else orc.alpha_experimental(n, 0.05, d, 0.05)
+    ix = ak.Index(X)
+    a = ix.query(Q, k, h, 0.05, 41, al, counts=True, sums=True, flags=ak.FLAG_SHARED_DRAWS)
+    b = ix.query(Q, k, h, 0.05, 41, al, counts=True, sums=True,
+                 flags=ak.FLAG_SHARED_DRAWS | ak.FLAG_NO_TILES)
+    ix.close()
+    for key in KEYS:
+        assert np.array_equal(a[key], b[key]), key
+    _assert_parity(a, orc.query_br(X, Q, k, h, 41, al, want_sums=True, shared_draws=True))
+
+
+def test_shared_draws_config1_and_reduced_config2(ak):
+    cfg = synth.config(1)
+    X, Q, planted = synth.planted(cfg)
+    al = orc.alpha_theory(cfg.n, cfg.delta, cfg.d)
+    ix = ak.Index(X)
+    got = ix.query(Q, cfg.k, cfg.h, cfg.delta, cfg.seed, al, counts=True, sums=True,
+                   flags=ak.FLAG_SHARED_DRAWS)
+    ix.close()
+    _assert_parity(got, orc.query_br(X, Q, cfg.k, cfg.h, cfg.seed, al, want_sums=True, shared_draws=True))
+    assert sorted(got["sets"][0].tolist()) == planted.tolist()
+    cfg = synth.config(2)
+    X = synth.points(cfg, 0, 6000)
+    Q = synth.queries(cfg)[:40]
+    al = orc.alpha_theory(6000, cfg.delta, cfg.d)
+    ix = ak.Index(X)
+    got = ix.query(Q, cfg.k, cfg.h, cfg.delta, cfg.seed, al, counts=True, sums=True,
+                   flags=ak.FLAG_SHARED_DRAWS)
+    ix.close()
+    _assert_parity(got, orc.query_br(X, Q, cfg.k, cfg.h, cfg.seed, al, want_sums=True, shared_draws=True))

@@ -395,3 +395,66 @@ def test_a1_literal_contains_knn():
         X, Q = synth.small_instance(200 + s, 30, 16, q=1)
         r = orc.query_a1(X, Q[0], 2, 2, s, orc.alpha_theory(30, 0.05, 16))
         assert _recall_ok(X, Q[0], r["set"], 2)
+
+
+# ----------------------------------------------------------------- query-independent draws
+# every query's Philox counter word is SHARED_QI, so arm i's t-th
+# coordinate is the same for all queries.  Each query alone is still the paper's
+# algorithm with i.i.d. uniform coordinates, so the same pins hold.
+
+def test_shared_draws_planted_config1_returns_planted_set():
+    cfg = synth.config(1)
+    X, Q, planted = synth.planted(cfg)
+    al = orc.alpha_theory(cfg.n, cfg.delta, cfg.d)
+    r = orc.query_br(X, Q, cfg.k, cfg.h, cfg.seed, al, shared_draws=True)
+    assert sorted(r["sets"][0].tolist()) == planted.tolist()
+
+
+def test_shared_draws_same_coordinates_for_every_query():
+    """With shared draws two queries that agree on every coordinate but one, c, have
+    per-arm sums that differ only through the draws landing on c: S1_i - S2_i ==
+    n_c(i) * ((x_ic - q1_c)^2 - (x_ic - q2_c)^2) where n_c(i) = how many of arm i's T_i
+    draws hit c -- so n_c(i) is the same for both queries (checked against the draw
+    index, which is pinned to cuRAND's Philox above)."""
+    X, Q = synth.small_instance(31, 200, 16, q=1)
+    q1 = Q[0].copy()
+    q2 = q1.copy()
+    q2[5] = (int(q2[5]) + 97) % 256
+    al = orc.alpha_experimental(200, 0.05, 16, 1e-6)  # tiny radius: stops early, T small
+    r = orc.query_br(X, np.stack([q1, q2]), 3, 3, 9, al, want_sums=True, shared_draws=True,
+                     max_rounds=1)
+    T = r["counts"]
+    assert np.array_equal(T[0], T[1])  # round 1: every arm has T = 1
+    for i in range(200):
+        t0 = 0
+        hits = sum(orc.draw_index(9, orc.SHARED_QI, i, t, 16) == 5 for t in range(t0, T[0, i]))
+        a = int(X[i, 5])
+        want = hits * ((a - int(q1[5])) ** 2 - (a - int(q2[5])) ** 2)
+        assert r["sums"][0, i] - r["sums"][1, i] == want
+
+
+def test_shared_draws_identical_queries_identical_results():
+    X, Q = synth.small_instance(33, 500, 40, q=1)
+    al = orc.alpha_theory(500, 0.05, 40)
+    QQ = np.repeat(Q, 3, axis=0)
+    r = orc.query_br(X, QQ, 4, 4, 2, al, want_sums=True, shared_draws=True)
+    for k in ("sets", "dhat", "counts", "sums", "evals", "draws", "rounds"):
+        assert np.array_equal(r[k][0], r[k][1]) and np.array_equal(r[k][0], r[k][2]), k
+    d = orc.query_br(X, QQ, 4, 4, 2, al, want_sums=True)  # per-query streams differ
+    assert not np.array_equal(d["sums"][0], d["sums"][1])
+
+
+def test_shared_draws_exact_arms_and_theorem1():
+    """Exact arms equal brute force; the Theorem-1 failure rate stays <= delta."""
+    X, Q = synth.small_instance(21, 300, 48, q=3)
+    al = orc.alpha_theory(300, 0.05, 48)
+    r = orc.query_br(X, Q, 5, 5, 3, al, want_sums=True, shared_draws=True)
+    D = ((X[None].astype(np.int64) - Q[:, None].astype(np.int64)) ** 2).sum(-1)
+    ex = r["counts"] == 48
+    assert ex.sum() > 0 and np.array_equal(r["sums"][ex], D[ex])
+    delta, fails, runs = 0.1, 0, 100
+    for s in range(runs):
+        X, Q = synth.small_instance(2000 + s, 80, 24, q=1, centres=3, sigma=40.0)
+        r = orc.query_br(X, Q, 3, 3, s, orc.alpha_theory(80, delta, 24), shared_draws=True)
+        fails += not _recall_ok(X, Q[0], r["sets"][0], 3)
+    assert fails / runs <= delta
