@@ -102,7 +102,8 @@ __device__ __forceinline__ void f1_stage_qt(const Geom &g, int r0, uint32_t *qt)
 }
 
 // The draws u0 .. u0+ch-1 of level c for the P points of the column: dbuf[p * ch + u]
-// = j | X[p0 + p][j] << 16.  Returns the Philox blocks drawn.
+// = 32 j | X[p0 + p][j] << 24 (32 j < 2^21: the Qt offset of coordinate j).  Returns
+// the Philox blocks drawn.
 __device__ __forceinline__ unsigned f1_generate(const Geom &g, int p0, int P, int c, unsigned u0, unsigned ch,
                                                 uint32_t *dbuf) {
   const unsigned s = 1u << c;
@@ -119,7 +120,7 @@ __device__ __forceinline__ unsigned f1_generate(const Geom &g, int p0, int P, in
     for (int e = 0; e < 4; ++e) {
       if (u + e < s && u + e < u0 + ch) {
         const uint32_t j = coord_of(ws[e], d);
-        dbuf[p * ch + (u - u0) + e] = j | ((uint32_t)__ldg(xr + j) << 16);
+        dbuf[p * ch + (u - u0) + e] = (j * F1_R) | ((uint32_t)__ldg(xr + j) << 24);
       }
     }
   }
@@ -152,17 +153,19 @@ __device__ __forceinline__ void f1_accumulate(uint32_t qt_s, uint32_t dbuf_s, in
     if ((ch & 3u) == 0) {
       for (uint32_t u = 0; u < ch; u += 4) {
         const uint4 pk = lds_u128(dp + u * 4u);  // broadcast
-        const uint32_t v[4] = {pk.x, pk.y, pk.z, pk.w};
-#pragma unroll
-        for (int e = 0; e < 4; ++e) {
-          const int diff = (int)(v[e] >> 16) - (int)lds_u8(ql + (v[e] & 0xFFFFu) * F1_R);
-          sum += (uint32_t)(diff * diff);
-        }
+        // the 4 point bytes (top bytes of the packed words) and the 4 query bytes, packed;
+        // |x - q|^2 summed by VABSDIFF4 + IDP.4A
+        const uint32_t x4 = __byte_perm(__byte_perm(pk.x, pk.y, 0x0073), __byte_perm(pk.z, pk.w, 0x0073), 0x5410);
+        const uint32_t q0 = lds_u8(ql + (pk.x & 0x1FFFFFu)), q1 = lds_u8(ql + (pk.y & 0x1FFFFFu));
+        const uint32_t q2 = lds_u8(ql + (pk.z & 0x1FFFFFu)), q3 = lds_u8(ql + (pk.w & 0x1FFFFFu));
+        const uint32_t q4 = __byte_perm(__byte_perm(q0, q1, 0x0040), __byte_perm(q2, q3, 0x0040), 0x5410);
+        const uint32_t t = __vabsdiffu4(x4, q4);
+        sum = __dp4a(t, t, sum);
       }
     } else {
       for (uint32_t u = 0; u < ch; ++u) {
         const uint32_t v = lds_u32(dp + u * 4u);
-        const int diff = (int)(v >> 16) - (int)lds_u8(ql + (v & 0xFFFFu) * F1_R);
+        const int diff = (int)(v >> 24) - (int)lds_u8(ql + (v & 0x1FFFFFu));
         sum += (uint32_t)(diff * diff);
       }
     }

@@ -312,6 +312,7 @@ void setup_tiles(Geom &g, const TileShape &t, const aknn_opts &o, int64_t qb, ui
   // consecutive tiles of a point column share the staged point rows: a tile stages
   // about its R query rows (+ one point row's share)
   g.tile_min_draws = t.row_draws * (float)((1 << t.lr) + 1);
+
 }
 
 // One round after the rank split: filter -> plan/scatter (+ dense-tile list) ->
