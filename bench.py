@@ -244,7 +244,9 @@ def _measure_probes(d: int, x_bytes: int) -> dict:
         L = rp.load()
         pb = rp.philox_blocks_per_s(L, d=d)
         gl, fb = rp.gather_sectors_per_s(L, x_bytes)
-        return {"philox_blocks_per_s": pb, "gather_loads_per_s": gl, "gather_footprint_bytes": fb}
+        sd = rp.shared_draws_per_s(L)
+        return {"philox_blocks_per_s": pb, "gather_loads_per_s": gl, "gather_footprint_bytes": fb,
+                "shared_draws_per_s": sd}
     except Exception as e:  # the probes are evidence, never a reason to fail the bench
         return {"error": repr(e)}
 
@@ -257,7 +259,7 @@ def _algorithmic_bytes(st: dict, n: int, d: int, q: int) -> dict:
         "filter": st["blocked_query_rounds"] * n * 6,
         "compact": st["blocked_query_rounds"] * n + st["active_pair_rounds"] * 4,
         # list path + exact fallbacks: sampled draws outside the tiles at one sector each
-        "advance": max(0, st["philox_blocks"] - st["tile_blocks"]) * 4 * SECTOR + st["exact_fallbacks"] * d,
+        "advance": max(0, st["draws"] - init_draws - st["tile_draws"]) * SECTOR + st["exact_fallbacks"] * d,
         # tiles stage rows (R + P) * pitch per dense tile: ALU-bound, no byte model here
         "tiles": 0,
     }
@@ -464,7 +466,8 @@ def run_ours(args, dist: Dist):
     peak, peak_src = _peaks()
     probes = _measure_probes(d, n_loc * cfg.d)
     blocks = agg.get("philox_blocks", 0)
-    adv_draws = max(0, blocks - agg.get("tile_blocks", 0)) * 4  # list-path level-gather draws
+    # list-path level-gather draws: all sampled draws minus initialisation minus the tiles'
+    adv_draws = max(0, agg["draws"] - args.steps * qpr * n_loc - agg.get("tile_draws", 0))
     x_in_l2 = n_loc * d <= L2_BYTES * 0.8
     common = {"kernel": KERNEL_OF[dom], "launches": launches[dom],
               "avg_launch_ms": ms_cls[dom] / max(1, launches[dom]),
@@ -486,7 +489,20 @@ def run_ours(args, dist: Dist):
         if adv_s > 0 and probes.get("gather_loads_per_s") else None,
         "x_footprint_bytes": n_loc * d, "x_l2_resident": x_in_l2}
     tile_blocks = agg.get("tile_blocks", 0)
-    if dom == "tiles" and probes.get("philox_blocks_per_s"):
+    if dom == "tiles" and args.draws == "shared" and probes.get("shared_draws_per_s"):
+        # shared draws: Philox runs once per point column; the tile gathers are bound by
+        # the byte gathers + multiply-adds of the (query, point) draws: measured ceiling of
+        # that instruction mix in tools/probes.cu k_probe_shared
+        ts = ms_cls["tiles"] / 1e3
+        ach = agg.get("tile_draws", 0) / ts / 1e9
+        pk = probes["shared_draws_per_s"] / 1e9
+        roofline = {"bound": "alu", "achieved": ach, "peak": pk, "unit": "G pair-draws/s",
+                    "frac": ach / pk,
+                    "peak_source": "measured in this run: tools/probes.cu k_probe_shared (the "
+                                   "shared-draw gather loop alone, full occupancy)",
+                    "algorithmic_units_per_launch": agg.get("tile_draws", 0) / max(1, launches[dom]),
+                    "sector_view": sector_view, **common}
+    elif dom == "tiles" and probes.get("philox_blocks_per_s"):
         # dense tiles gather from shared memory: the sampled draws are bound by the
         # integer pipes running Philox4x32-10 (ncu: fma-heavy + LDS wavefronts), not by
         # memory

@@ -131,6 +131,7 @@ typedef struct {
                                  (k_advance_tiles; part of the advance rows a3)  */
   int64_t launches_tiles;
   int64_t tile_blocks;        /* Philox blocks drawn by the tile gathers        */
+  int64_t tile_draws;         /* (query, point) draws summed by the tile gathers */
 } aknn_stats;
 
 /* ------------------------------------------------------------------------ */

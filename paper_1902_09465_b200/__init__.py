@@ -66,7 +66,8 @@ class Stats(C.Structure):
                 ("launches_filter", C.c_int64), ("launches_compact", C.c_int64),
                 ("launches_advance", C.c_int64), ("launches_output", C.c_int64),
                 ("philox_blocks", C.c_int64), ("graph_builds", C.c_int32), ("pad0", C.c_int32),
-                ("ms_tiles", C.c_double), ("launches_tiles", C.c_int64), ("tile_blocks", C.c_int64)]
+                ("ms_tiles", C.c_double), ("launches_tiles", C.c_int64), ("tile_blocks", C.c_int64),
+                ("tile_draws", C.c_int64)]
 
 
 class MergeResult(C.Structure):

@@ -71,7 +71,7 @@ constexpr int F1_R = 32;
 
 // Qt[j * 32 + r] = Q[r0 + r][j] for the tile's 32 query rows: 4 x 4 byte blocks
 // transposed with PRMT (4-byte loads, 4-byte stores); QT_U blocks per thread in flight.
-constexpr int QT_U = 4;
+constexpr int QT_U = 2;
 __device__ __forceinline__ void f1_stage_qt(const Geom &g, int r0, uint32_t *qt) {
   const int nj4 = (int)(g.pitch >> 2);  // 4-byte columns (pitch is a multiple of 16)
   const int total = 8 * nj4;
@@ -209,7 +209,8 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
   const long long t0 = (long long)blockIdx.x * ntot / gridDim.x, t1 = (long long)(blockIdx.x + 1) * ntot / gridDim.x;
   int staged_tp = -1;
   int gen_tp = -1, gen_c = -1;  // shared draws: the column / level whose draw list is in dbuf
-  unsigned long long my_blocks = 0;  // Philox blocks drawn (statistics)
+  __shared__ unsigned long long s_blocks, s_draws;  // Philox blocks and pair draws (statistics)
+  if (tid == 0) s_blocks = s_draws = 0;
   for (long long c0 = t0; c0 < t1; c0 += TILE_NT) {
     __syncthreads();  // dlist of the previous chunk is consumed
     {
@@ -319,6 +320,11 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
     // reduce inside the lane group; every pair's sum is written by one thread.
     unsigned lmask = 0;  // levels present in the tile
     for (int c = 0; c < MAX_LEVELS; ++c) lmask |= (lcnt[c] != 0u) << c;
+    if (tid == 0) {
+      unsigned long long dr = 0;
+      for (int c = 0; c < MAX_LEVELS; ++c) dr += (unsigned long long)lcnt[c] << c;
+      s_draws += dr;
+    }
     if (f1) {
       // shared draws: per level, the column's draw list (cached across the column's
       // tiles while a level fits one chunk), then every (row, point) pair of the tile
@@ -335,7 +341,7 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
           if (!cached) {
             __syncthreads();  // the previous chunk's draws are consumed
             const unsigned nb = f1_generate(g, p0, P, c, u0, ch, dbuf);
-            if (tid == 0) my_blocks += nb;
+            if (tid == 0) s_blocks += nb;
             __syncthreads();
             gen_tp = s <= chmax ? tp : -1;
             gen_c = c;
@@ -351,7 +357,9 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
       }
       lmask = 0;  // done: skip the per-pair Philox path below
     } else if (tid == 0) {
-      for (int c = 0; c < MAX_LEVELS; ++c) my_blocks += (unsigned long long)lcnt[c] << (c < 2 ? 0 : c - 2);
+      unsigned long long b = 0;
+      for (int c = 0; c < MAX_LEVELS; ++c) b += (unsigned long long)lcnt[c] << (c < 2 ? 0 : c - 2);
+      s_blocks += b;
     }
     for (; lmask; lmask &= lmask - 1) {
       const int c = __ffs(lmask) - 1;
@@ -444,7 +452,8 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
     }
   }
   }
-  if (threadIdx.x == 0 && my_blocks) atomicAdd(&g.ctl->tile_blocks, my_blocks);
+  if (threadIdx.x == 0 && s_blocks) atomicAdd(&g.ctl->tile_blocks, s_blocks);
+  if (threadIdx.x == 0 && s_draws) atomicAdd(&g.ctl->tile_draws, s_draws);
 }
 
 int tile_slot_log2(int64_t pitch) {

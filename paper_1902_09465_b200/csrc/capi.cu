@@ -549,6 +549,7 @@ void fold_batch_stats(aknn_stats &stats, const RoundCtl &ctl_h, const QState *qs
   if (r > stats.rounds) stats.rounds = r;
   stats.active_pair_rounds += (int64_t)ctl_h.advanced;
   stats.tile_blocks += (int64_t)ctl_h.tile_blocks;
+  stats.tile_draws += (int64_t)ctl_h.tile_draws;
   for (int a = 0; a < qn; ++a) {
     stats.draws += qs[a].draws;
     stats.exact_fallbacks += qs[a].nexact;
@@ -1032,6 +1033,8 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
       const QState *qs = h_qs;
       stats.active_pair_rounds += (int64_t)ctl_h.advanced;
       stats.tile_blocks += (int64_t)ctl_h.tile_blocks;
+      stats.tile_draws += (int64_t)ctl_h.tile_draws;
+  stats.tile_draws += (int64_t)ctl_h.tile_draws;
       for (int a = 0; a < qn; ++a) {
         stats.draws += qs[a].draws;
         stats.exact_fallbacks += qs[a].nexact;

@@ -62,6 +62,7 @@ struct RoundCtl {
   unsigned long long chunk_off[NSLOT + 1];// warp-chunk prefix per slot
   unsigned long long advanced;            // pairs advanced, cumulative
   unsigned long long tile_blocks;         // Philox blocks of the tile gathers, cumulative
+  unsigned long long tile_draws;          // (query, point) draws of the tile gathers, cumulative
   // cumulative, maintained on the device by k_round_ctl (graph-launched loop)
   unsigned int round;                     // rounds evaluated
   unsigned int evaluated;                 // queries the next rank split looks at

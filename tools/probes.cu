@@ -7,6 +7,11 @@
 //   probe_gather   the achievable rate of random one-byte gathers (one 32-B sector
 //                  each) from a buffer of a given footprint: the sector ceiling
 //                  (L2-resident footprint vs HBM footprint).
+//   probe_shared   the achievable rate of the shared-draw tile gathers:
+//                  per 4 draws one broadcast 16-byte load of packed (32 j | x << 24)
+//                  words, 4 conflict-free byte gathers from a transposed 32-row query
+//                  tile, VABSDIFF4 + IDP.4A -- the same instruction mix as
+//                  k_advance_tiles' accumulate loop, with nothing else: its ceiling.
 //
 // C-ABI: each returns the best device time in ms over `reps` launches (CUDA events).
 #include <cuda_runtime.h>
@@ -60,6 +65,35 @@ __global__ void __launch_bounds__(256) k_probe_gather(const uint8_t *__restrict_
   out[t] = acc;
 }
 
+__global__ void __launch_bounds__(256) k_probe_shared(int iters, uint32_t *out) {
+  __shared__ uint8_t qt[784 * 32];
+  __shared__ uint32_t dbuf[8][256];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int i = tid; i < 784 * 32; i += 256) qt[i] = (uint8_t)(i * 2654435761u >> 24);
+  for (int i = tid; i < 8 * 256; i += 256) {
+    const uint32_t j = (i * 2654435761u) % 784u;
+    (&dbuf[0][0])[i] = (j * 32u) | ((uint32_t)(i * 40503u) << 24);
+  }
+  __syncthreads();
+  const uint32_t ql = (uint32_t)__cvta_generic_to_shared(qt) + lane;
+  const uint4 *dp = reinterpret_cast<const uint4 *>(dbuf[warp]);
+  uint32_t sum = 0;
+  for (int it = 0; it < iters; ++it) {
+    for (int u = 0; u < 64; ++u) {
+      const uint4 pk = dp[u];
+      uint32_t q[4];
+      const uint32_t v[4] = {pk.x, pk.y, pk.z, pk.w};
+#pragma unroll
+      for (int e = 0; e < 4; ++e) asm volatile("ld.shared.u8 %0, [%1];" : "=r"(q[e]) : "r"(ql + (v[e] & 0x1FFFFFu)));
+      const uint32_t x4 = __byte_perm(__byte_perm(pk.x, pk.y, 0x0073), __byte_perm(pk.z, pk.w, 0x0073), 0x5410);
+      const uint32_t q4 = __byte_perm(__byte_perm(q[0], q[1], 0x0040), __byte_perm(q[2], q[3], 0x0040), 0x5410);
+      const uint32_t t = __vabsdiffu4(x4, q4);
+      sum = __dp4a(t, t, sum);
+    }
+  }
+  out[blockIdx.x * 256 + tid] = sum;
+}
+
 template <class F>
 double best_ms(F launch, int reps) {
   cudaEvent_t a, b;
@@ -110,6 +144,16 @@ double probe_gather(int grid_threads, int loads_per_thread, unsigned long long b
   const double ms = best_ms([&] { k_probe_gather<<<nb, 256>>>(buf, bytes, loads_per_thread, out); }, reps);
   cudaError_t e = cudaDeviceSynchronize();
   cudaFree(buf);
+  cudaFree(out);
+  return e == cudaSuccess ? ms : -1.0;
+}
+
+// (query, point) draws = blocks * 256 * iters * 256; returns best ms.
+double probe_shared(int blocks, int iters, int reps) {
+  uint32_t *out = nullptr;
+  if (cudaMalloc(&out, sizeof(uint32_t) * 256 * (size_t)blocks) != cudaSuccess) return -1.0;
+  const double ms = best_ms([&] { k_probe_shared<<<blocks, 256>>>(iters, out); }, reps);
+  cudaError_t e = cudaDeviceSynchronize();
   cudaFree(out);
   return e == cudaSuccess ? ms : -1.0;
 }
