@@ -256,20 +256,26 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
   for (int t = threadIdx.x; t < ntc; t += FIL_NT) tcnt[t] = 0;
   __syncthreads();
   const bool arms = i0 < g.n;
-  int st = g.qs[q0].done;
-  Arm4 a{};
-  if (arms) a = load_arm4(g, q0, i0);
+  // two rows of loads in flight ahead of the row being decided
+  int st0 = g.qs[q0].done, st1 = rows > 1 ? g.qs[q0 + 1].done : 1;
+  Arm4 a0{}, a1{};
+  if (arms) {
+    a0 = load_arm4(g, q0, i0);
+    if (rows > 1) a1 = load_arm4(g, q0 + 1, i0);
+  }
   SlotRun run;
   unsigned ex_acc = 0;     // exact fallbacks of this thread (one 128-query tile row: 32 | 128)
   uint32_t dr_acc = 0;     // sampled draws of this thread in the current tile row
   int tr_cur = 0;
   for (int r = 0; r < rows; ++r) {
     const int qi = q0 + r;
-    const int cur = st;
-    const Arm4 ca = a;
-    if (r + 1 < rows) {  // prefetch the next row
-      st = g.qs[qi + 1].done;
-      if (arms) a = load_arm4(g, qi + 1, i0);
+    const int cur = st0;
+    const Arm4 ca = a0;
+    st0 = st1;
+    a0 = a1;
+    if (r + 2 < rows) {  // prefetch the row after next
+      st1 = g.qs[qi + 2].done;
+      if (arms) a1 = load_arm4(g, qi + 2, i0);
     }
     if (cur) continue;  // uniform: one query row at a time
     uint32_t dr = 0, actw = 0;

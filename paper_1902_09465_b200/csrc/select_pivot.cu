@@ -194,7 +194,7 @@ __device__ __forceinline__ RecBest rec_of_key(const Geom &g, int qi, unsigned lo
 }
 
 // Unsharded rank split + bounds + Eq. (5) (same contract as k_select).
-__global__ void __launch_bounds__(PIV_NT) k_select_pivot(Geom g) {
+__global__ void __launch_bounds__(PIV_NT, 2) k_select_pivot(Geom g) {
   extern __shared__ unsigned long long pbuf[];
   unsigned *prank = reinterpret_cast<unsigned *>(pbuf + PIV_CAP);
   __shared__ RecBest wsm[PIV_NT / 32];
@@ -242,7 +242,7 @@ __global__ void __launch_bounds__(PIV_NT) k_select_pivot(Geom g) {
 
 // Sharded local summary (same contract as k_select_local): the local top-(k+h)
 // records and the remainder's minimum-L record.
-__global__ void __launch_bounds__(PIV_NT) k_select_local_pivot(Geom g) {
+__global__ void __launch_bounds__(PIV_NT, 2) k_select_local_pivot(Geom g) {
   extern __shared__ unsigned long long pbuf[];
   unsigned *prank = reinterpret_cast<unsigned *>(pbuf + PIV_CAP);
   __shared__ RecBest wsm[PIV_NT / 32];
