@@ -18,7 +18,7 @@ from typing import Optional
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libaknn.so")
+LIB_PATH = os.environ.get("AKNN_LIB") or os.path.join(_HERE, "libaknn.so")  # AKNN_LIB: A/B builds
 
 if not os.path.exists(LIB_PATH):
     raise ImportError(

@@ -173,6 +173,7 @@ __device__ __forceinline__ void f1_accumulate(uint32_t qt_s, uint32_t dbuf_s, in
   }
 }
 
+template <bool F1>
 __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
   extern __shared__ __align__(16) unsigned char tsm[];
   __shared__ unsigned lcnt[MAX_LEVELS], loff[MAX_LEVELS + 1], lfill[MAX_LEVELS];
@@ -236,7 +237,7 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
     const int r0 = tr << g.tile_lr, p0 = tp << g.tile_lp;
     const bool reuse_x = tp == staged_tp;  // the point rows of this column are staged
     staged_tp = tp;
-    const bool f1 = g.shared_draws && R == F1_R;  // query-independent draws, R = 32
+    constexpr bool f1 = F1;  // query-independent draws with R = 32 (host-selected instantiation)
     __syncthreads();  // the previous tile's shared memory is no longer in use
     if (tid < MAX_LEVELS) lcnt[tid] = 0;
 
@@ -475,7 +476,10 @@ static size_t tile_base() {  // static shared memory + the per-CTA system reserv
   static size_t b = [] {
     cudaFuncAttributes fa{};
     int dev = 0, rsv = 0;
-    if (cudaFuncGetAttributes(&fa, k_advance_tiles) != cudaSuccess) fa.sharedSizeBytes = 2048;
+    cudaFuncAttributes fb{};
+    if (cudaFuncGetAttributes(&fa, k_advance_tiles<false>) != cudaSuccess) fa.sharedSizeBytes = 2048;
+    if (cudaFuncGetAttributes(&fb, k_advance_tiles<true>) == cudaSuccess && fb.sharedSizeBytes > fa.sharedSizeBytes)
+      fa.sharedSizeBytes = fb.sharedSizeBytes;
     if (cudaGetDevice(&dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev) != cudaSuccess)
       rsv = 1024;
@@ -487,17 +491,23 @@ static size_t tile_base() {  // static shared memory + the per-CTA system reserv
 // Shared memory per CTA of a tile shape (the occupancy the shape chooser reasons about).
 size_t tile_smem_bytes(int lr, int lp, int64_t pitch) { return tile_window(lr, lp, pitch, tile_base()); }
 
+template <bool F1>
+static cudaError_t launch_tiles_k(const Geom &g, int num_sms, size_t smem, cudaStream_t s) {
+  cudaError_t e = cudaFuncSetAttribute(k_advance_tiles<F1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int per_sm = 0;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_advance_tiles<F1>, TILE_NT, smem);
+  if (e != cudaSuccess) return e;
+  if (per_sm < 1) per_sm = 1;
+  k_advance_tiles<F1><<<num_sms * per_sm, TILE_NT, smem, s>>>(g);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_advance_tiles(const Geom &g, int num_sms, cudaStream_t s) {
   const size_t base = tile_base();
   const size_t smem = tile_window(g.tile_lr, g.tile_lp, g.pitch, base) - base;
-  cudaError_t e = cudaFuncSetAttribute(k_advance_tiles, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_advance_tiles, TILE_NT, smem);
-  if (e != cudaSuccess) return e;
-  if (per_sm < 1) per_sm = 1;
-  k_advance_tiles<<<num_sms * per_sm, TILE_NT, smem, s>>>(g);
-  return cudaGetLastError();
+  if (g.shared_draws && g.tile_lr == 5) return launch_tiles_k<true>(g, num_sms, smem, s);
+  return launch_tiles_k<false>(g, num_sms, smem, s);
 }
 
 }  // namespace aknn
