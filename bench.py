@@ -57,6 +57,7 @@ def _args():
                     help="per-query Philox streams (default, DESIGN.md R19) or query-independent "
                          "draws (SURVEY §8(f1), AKNN_FLAG_SHARED_DRAWS)")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-variant", action="store_true", help="skip the shared-draw variant timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-exact", action="store_true")
     ap.add_argument("--clock-sampler", choices=("nvml", "smi", "none"), default="nvml")
@@ -411,29 +412,29 @@ def run_ours(args, dist: Dist):
     qi_off = 0 if sharded else dist.rank * qpr
     qflags = ak.FLAG_SHARED_DRAWS if args.draws == "shared" else 0
 
-    def step(timing: bool):
+    def step(timing: bool, flags=None):
         flush.zero_()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         ix.query_device(Qd, k, h, cfg.delta, cfg.seed, alpha_d, qi_offset=qi_off, timing=timing,
-                        stream=stream, out=out, flags=qflags)
+                        stream=stream, out=out, flags=qflags if flags is None else flags)
         e1.record(stream)
         torch.cuda.synchronize()
         return e0.elapsed_time(e1), ix.stats()
 
-    def timed(timing: bool):
+    def timed(timing: bool, flags=None):
         """W warm-up steps, then K steps bracketed by barrier + synchronize; per-step CUDA
         events on the library's stream (L2 flushed before each step, outside the events)."""
         for _ in range(args.warmup):
-            step(timing)
+            step(timing, flags)
         clocks = ClockSampler(dist.local, args.clock_sampler)
         dist.barrier()
         torch.cuda.synchronize()
         clocks.start()
         times, stats = [], []
         for _ in range(args.steps):
-            ms, st = step(timing)
+            ms, st = step(timing, flags)
             times.append(ms)
             stats.append(st)
         dist.barrier()
@@ -447,6 +448,15 @@ def run_ours(args, dist: Dist):
     total_q = qpr * args.steps if sharded else dist.sum(qpr * args.steps)
     value = total_q / (ms_max / 1e3)
     ms_per_step = ms_max / args.steps
+    # (1b) the query-independent-draw variant on the same workload:
+    # reported beside the headline, which keeps the per-query streams (R19)
+    variant = None
+    if args.draws == "per-query" and not args.no_variant:
+        vtimes, _, vclk = timed(False, ak.FLAG_SHARED_DRAWS)
+        vms = dist.max(sum(vtimes))
+        variant = {"draws": "shared (AKNN_FLAG_SHARED_DRAWS, DESIGN.md §12)",
+                   "value": total_q / (vms / 1e3), "unit": UNIT, "ms_per_step": vms / args.steps,
+                   "step_ms": [round(t, 3) for t in vtimes], "clocks": vclk}
     # (2) the same steps with per-launch CUDA events (host-driven loop) for the roofline
     itimes, stats, _ = timed(True)
     ms_local_instr = sum(itimes)
@@ -634,6 +644,7 @@ def run_ours(args, dist: Dist):
             "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
             "gpu_launches": gpu_launches, "gpu_launches_per_step": gpu_launches / args.steps,
             "step_ms": [round(t, 3) for t in times],
+            "variant_shared_draws": variant,
             **extra,
         }
         print(json.dumps(line), flush=True)
