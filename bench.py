@@ -214,6 +214,16 @@ def _peaks():
         return 6650.0, "fallback (B200_PROFILING.md: 6.65 TB/s)"
 
 
+def _bf16_peak():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(p) as f:
+            j = json.load(f)
+        return float(j["bf16_tflops"]), "measured (MEASURED_PEAKS.json bf16_tflops, cuBLAS 8192^3)"
+    except Exception:
+        return 2250.0, "fallback (nominal 2.25 PFLOP/s bf16 dense)"
+
+
 def _traffic_from_profiles(kernel: str):
     """dram bytes per launch of `kernel` from the committed ncu --set full summary, if any."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -269,6 +279,7 @@ def _algorithmic_bytes(st: dict, n: int, d: int, q: int) -> dict:
 KERNEL_OF = {"init": "k_init", "select": "k_select_pivot", "filter": "k_filter",
              "compact": "k_scatter", "advance": "k_advance", "tiles": "k_advance_tiles",
              "output": "k_output"}
+KERNEL_OF_SHARED = dict(KERNEL_OF, tiles="k_level_mma")
 
 
 # ----------------------------------------------------------------------------- oracle legs
@@ -479,13 +490,14 @@ def run_ours(args, dist: Dist):
     # list-path level-gather draws: all sampled draws minus initialisation minus the tiles'
     adv_draws = max(0, agg["draws"] - args.steps * qpr * n_loc - agg.get("tile_draws", 0))
     x_in_l2 = n_loc * d <= L2_BYTES * 0.8
-    common = {"kernel": KERNEL_OF[dom], "launches": launches[dom],
+    kof = KERNEL_OF_SHARED if (args.draws == "shared" and agg.get("level_mma_tiles", 0) > 0) else KERNEL_OF
+    common = {"kernel": kof[dom], "launches": launches[dom],
               "avg_launch_ms": ms_cls[dom] / max(1, launches[dom]),
               "share_of_step": ms_cls[dom] / ms_local_instr,
               "timing": "CUDA events around every launch on the library stream, K instrumented "
                         "steps (host-driven loop) right after the K graph-launched timed steps",
               "ms_per_step_instrumented": dist.max(ms_local_instr) / args.steps,
-              "traffic": _traffic_from_profiles(KERNEL_OF[dom]),
+              "traffic": _traffic_from_profiles(kof[dom]),
               "per_class": {c: {"ms": ms_cls[c], "launches": launches[c],
                                 "GBps_algorithmic": (abytes[c] / (ms_cls[c] / 1e3) / 1e9)
                                 if c in abytes and ms_cls[c] > 0 else None}
@@ -499,7 +511,20 @@ def run_ours(args, dist: Dist):
         if adv_s > 0 and probes.get("gather_loads_per_s") else None,
         "x_footprint_bytes": n_loc * d, "x_l2_resident": x_in_l2}
     tile_blocks = agg.get("tile_blocks", 0)
-    if dom == "tiles" and args.draws == "shared" and probes.get("shared_draws_per_s"):
+    lm_tiles = agg.get("level_mma_tiles", 0)
+    if dom == "tiles" and args.draws == "shared" and lm_tiles > 0:
+        # shared draws, dominant level as 4 integer GEMMs (u8 x u8 -> s32) per 128 x 128
+        # (query x point) tile over K = d: tensor-bound; int8 dense peak = 2 x the measured
+        # bf16 dense peak (B200 nominal ratio 4.5 / 2.25 PFLOP/s)
+        ts = ms_cls["tiles"] / 1e3
+        ops = lm_tiles * 128 * 128 * d * 2 * 4
+        pk_bf16, pk_src = _bf16_peak()
+        roofline = {"bound": "tensor", "achieved": ops / ts / 1e12, "peak": 2 * pk_bf16,
+                    "unit": "TOP/s (int8)", "frac": ops / ts / 1e12 / (2 * pk_bf16),
+                    "peak_source": pk_src + " x 2 (int8 : bf16 dense, B200_PROFILING.md nominal)",
+                    "algorithmic_units_per_launch": ops / max(1, launches[dom]),
+                    "level_mma_tiles": lm_tiles, "sector_view": sector_view, **common}
+    elif dom == "tiles" and args.draws == "shared" and probes.get("shared_draws_per_s"):
         # shared draws: Philox runs once per point column; the tile gathers are bound by
         # the byte gathers + multiply-adds of the (query, point) draws: measured ceiling of
         # that instruction mix in tools/probes.cu k_probe_shared

@@ -98,6 +98,9 @@ typedef struct {
    guarantee of P:395-399 holds per query).  A different -- equally valid -- stream:
    results differ from the default and match the oracle run with qids = 0xFFFFFFFF. */
 #define AKNN_FLAG_SHARED_DRAWS 16
+/* bit 5: with shared draws, keep every level on the per-pair gathers instead of the
+   tensor-core level GEMMs (k_level_mma; diagnostics, identical results)      */
+#define AKNN_FLAG_NO_LEVEL_MMA 32
 
 /* Execution statistics of the last query call on an index (aknn_get_stats).
  * Kernel classes: init (a2), select (a6-a7: rank split, bounds, Eq. 5),
@@ -127,11 +130,13 @@ typedef struct {
   int32_t graph_builds;       /* round-loop graphs captured + instantiated by
                                  this call (0 when the cached graph was reused) */
   int32_t pad0;
-  double ms_tiles;            /* device time of the shared-memory tile gathers
-                                 (k_advance_tiles; part of the advance rows a3)  */
+  double ms_tiles;            /* device time of the dense-tile gathers: shared-memory
+                                 tiles (k_advance_tiles) or, with shared draws, the
+                                 tensor-core level GEMMs (k_level_mma); rows a3  */
   int64_t launches_tiles;
   int64_t tile_blocks;        /* Philox blocks drawn by the tile gathers        */
   int64_t tile_draws;         /* (query, point) draws summed by the tile gathers */
+  int64_t level_mma_tiles;    /* 128 x 128 tiles of shared-draw levels run as tensor-core GEMMs */
 } aknn_stats;
 
 /* ------------------------------------------------------------------------ */

@@ -52,6 +52,7 @@ FLAG_EXACT_ROWS = 2  # exact fallbacks as per-pair row streams instead of tensor
 FLAG_NO_TILES = 4  # every level gather through the work lists (no shared-memory tiles)
 FLAG_EXACT_MMA_ALL = 8  # every tile with an exact fallback on the tensor cores
 FLAG_SHARED_DRAWS = 16  # query-independent coordinate draws
+FLAG_NO_LEVEL_MMA = 32  # shared draws without the tensor-core level GEMMs
 
 
 class Stats(C.Structure):
@@ -67,7 +68,7 @@ class Stats(C.Structure):
                 ("launches_advance", C.c_int64), ("launches_output", C.c_int64),
                 ("philox_blocks", C.c_int64), ("graph_builds", C.c_int32), ("pad0", C.c_int32),
                 ("ms_tiles", C.c_double), ("launches_tiles", C.c_int64), ("tile_blocks", C.c_int64),
-                ("tile_draws", C.c_int64)]
+                ("tile_draws", C.c_int64), ("level_mma_tiles", C.c_int64)]
 
 
 class MergeResult(C.Structure):

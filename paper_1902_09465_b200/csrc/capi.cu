@@ -319,18 +319,55 @@ void setup_tiles(Geom &g, const TileShape &t, const aknn_opts &o, int64_t qb, ui
 // advance (tensor-core exact fallbacks, list levels) -> dense tiles.  timer(k): per-class
 // event brackets of the host-driven loop (0 start, 1 filter, 2 compact, 3 advance,
 // 4 tiles).
+size_t lvcnt_bytes(int64_t qb, int64_t npad);  // (below)
+
 template <class Timer>
 cudaError_t launch_round_body(const Geom &g, int num_sms, cudaStream_t st, Timer &&timer) {
   timer(0);
-  cudaError_t e = launch_filter(g, st);
+  cudaError_t e = cudaSuccess;
+  if (g.level_mma) e = cudaMemsetAsync(g.lvcnt, 0, lvcnt_bytes(g.q, g.npad), st);
+  if (e == cudaSuccess) e = launch_filter(g, st);
   timer(1);
   if (e == cudaSuccess) e = launch_compact(g, st);
   timer(2);
   if (e == cudaSuccess) e = launch_advance(g, num_sms, st);
   timer(3);
   if (e == cudaSuccess && g.tile_on) e = launch_advance_tiles(g, num_sms, st);
+  if (e == cudaSuccess && g.level_mma) e = launch_level_mma(g, st);
   timer(4);
   return e;
+}
+
+// Shared draws on the tensor cores (k_level_mma): q^2 planes [qb][pitch] x 2, the
+// level's w planes [n][pitch] x 3, wa [n], wovf [n], per-(128 x 128, level) counts.
+bool level_mma_on(const aknn_opts &o) {
+  return (o.flags & AKNN_FLAG_SHARED_DRAWS) && !(o.flags & AKNN_FLAG_NO_LEVEL_MMA) && env_int("AKNN_LEVEL_MMA", 1);
+}
+size_t lvcnt_bytes(int64_t qb, int64_t npad) {
+  return (size_t)((qb + level_tile_rows() - 1) / level_tile_rows()) *
+         (size_t)((npad + level_tile_cols() - 1) / level_tile_cols()) * MAX_LEVELS * sizeof(uint32_t);
+}
+size_t level_ws_bytes(int64_t qb, int64_t n, int64_t npad, int64_t pitch, const aknn_opts &o) {
+  if (!level_mma_on(o)) return 0;
+  return 2 * round_up((size_t)qb * pitch, 256) + 3 * round_up((size_t)n * pitch, 256) +
+         round_up((size_t)npad * 4, 256) + round_up((size_t)n, 256) + round_up(lvcnt_bytes(qb, npad), 256);
+}
+void setup_level_mma(Geom &g, int64_t qb, uint8_t *ws, const aknn_opts &o) {
+  g.level_mma = level_mma_on(o) ? 1 : 0;
+  if (!g.level_mma) return;
+  g.tile_on = 0;  // the non-GEMM pairs take the lists
+  const size_t qp = round_up((size_t)qb * g.pitch, 256), np = round_up((size_t)g.n * g.pitch, 256);
+  g.q2lo = ws;
+  g.q2hi = ws + qp;
+  g.wx0 = ws + 2 * qp;
+  g.wx1 = g.wx0 + np;
+  g.wc = g.wx1 + np;
+  g.wa = reinterpret_cast<int32_t *>(g.wc + np);
+  g.wovf = reinterpret_cast<uint8_t *>(g.wa) + round_up((size_t)g.npad * 4, 256);  // wa: npad ints
+  g.lvcnt = reinterpret_cast<uint32_t *>(g.wovf + round_up((size_t)g.n, 256));
+  g.lv_cols = (int)((g.npad + level_tile_cols() - 1) / level_tile_cols());
+  static const int lmin = env_int("AKNN_LMIN", 2048);
+  g.lmin = (uint32_t)(lmin < 1 ? 1 : lmin);
 }
 
 // Builds the level geometry of the composite key (R9).
@@ -522,9 +559,9 @@ aknn_status loop_graph(aknn_index *ix, const Geom &g, int nbits, int max_rounds,
 }
 
 // Kernel launches per class (for aknn_stats; memset nodes excluded).
-int launches_init_of(const Geom &g) { return 2 + (g.exact_mma ? 1 : 0); }  // init, qstate, norms
+int launches_init_of(const Geom &g) { return 2 + (g.exact_mma ? 1 : 0) + (g.level_mma ? 1 : 0); }  // init, qstate, norms, q^2
 int launches_filter_of(const Geom &) { return 1; }
-int launches_compact_of(const Geom &) { return 3; }  // plan, scatter, list sizes
+int launches_compact_of(const Geom &g) { return 3 + (g.level_mma ? 1 : 0); }  // plan, (w planes,) scatter, list sizes
 int launches_advance_of(const Geom &g) {
   return 1 + (g.exact_mma ? 1 : 0) + (g.stage_lo < MAX_LEVELS ? 1 : 0);
 }
@@ -543,13 +580,14 @@ void fold_batch_stats(aknn_stats &stats, const RoundCtl &ctl_h, const QState *qs
     stats.launches_filter += launches_filter_of(g) * (r - 1);
     stats.launches_compact += launches_compact_of(g) * (r - 1);
     stats.launches_advance += (launches_advance_of(g) + 1) * (r - 1);  // + counter reset
-    stats.launches_tiles += (g.tile_on ? 1 : 0) * (r - 1);
+    stats.launches_tiles += ((g.tile_on ? 1 : 0) + (g.level_mma ? 1 : 0)) * (r - 1);
     if (ctl_h.n_active > 0 && status) *status = AKNN_EMAXROUNDS;
   }
   if (r > stats.rounds) stats.rounds = r;
   stats.active_pair_rounds += (int64_t)ctl_h.advanced;
   stats.tile_blocks += (int64_t)ctl_h.tile_blocks;
   stats.tile_draws += (int64_t)ctl_h.tile_draws;
+  stats.level_mma_tiles += (int64_t)ctl_h.lmma_tiles;
   for (int a = 0; a < qn; ++a) {
     stats.draws += qs[a].draws;
     stats.exact_fallbacks += qs[a].nexact;
@@ -631,6 +669,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   const TileShape tsh = tile_shape(ix->pitch);
   const size_t oTw = off; off = round_up(off + tile_ws_bytes(qb, npad, tsh), 256);
   const size_t oThr = off; off = round_up(off + sizeof(int32_t) * THR_STRIDE * (size_t)qb, 256);
+  const size_t oLm = off; off = round_up(off + level_ws_bytes(qb, n, npad, ix->pitch, o), 256);
   TRY(ix->ws.ensure(off));
 
   Geom g{};
@@ -669,6 +708,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   g.stage_lo = stage_level(g.pitch);
   TRY(setup_exact_mma(ix, g, qb, ix->ws.as<uint8_t>(oXm), o, st));
   setup_tiles(g, tsh, o, qb, ix->ws.as<uint8_t>(oTw));
+  setup_level_mma(g, qb, ix->ws.as<uint8_t>(oLm), o);
 
   aknn_stats stats{};
   stats.pairs = (int64_t)q * n;
@@ -754,7 +794,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
           tm.stop(PH_TILES);
         }
       }));
-      stats.launches_tiles += g.tile_on ? 1 : 0;
+      stats.launches_tiles += (g.tile_on ? 1 : 0) + (g.level_mma ? 1 : 0);
       stats.launches_filter += launches_filter_of(g);
       stats.launches_compact += launches_compact_of(g);
       stats.launches_advance += launches_advance_of(g);
@@ -879,6 +919,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     const TileShape tsh = tile_shape(ix->pitch);
     const size_t oTw = off; off = round_up(off + tile_ws_bytes(qb, npad, tsh), 256);
     const size_t oThr = off; off = round_up(off + sizeof(int32_t) * THR_STRIDE * (size_t)qb, 256);
+    const size_t oLm = off; off = round_up(off + level_ws_bytes(qb, ix->n_local, npad, ix->pitch, o), 256);
     TRY(ix->ws.ensure(off));
     Geom &g = G[si];
     g = Geom{};
@@ -919,6 +960,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     g.recv_stride = recv_stride;
     TRY(setup_exact_mma(ix, g, qb, ix->ws.as<uint8_t>(oXm), o, st));
     setup_tiles(g, tsh, o, qb, ix->ws.as<uint8_t>(oTw));
+    setup_level_mma(g, qb, ix->ws.as<uint8_t>(oLm), o);
     if (has_recv) g.recv = ix->ws.as<ShardRec>(oRecv);
     if (si == 0 && !nccl) recv_shared = ix->ws.as<ShardRec>(oRecv);
     if (nccl) g.send = ix->ws.as<ShardRec>(oSend);
@@ -1005,7 +1047,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
       stats.launches_filter += launches_filter_of(G[0]) * (int)nS;
       stats.launches_compact += launches_compact_of(G[0]) * (int)nS;
       stats.launches_advance += launches_advance_of(G[0]) * (int)nS;
-      stats.launches_tiles += (G[0].tile_on ? 1 : 0) * (int)nS;
+      stats.launches_tiles += ((G[0].tile_on ? 1 : 0) + (G[0].level_mma ? 1 : 0)) * (int)nS;
       if (r > 1 + 64 * 64) return fail(AKNN_ECUDA, "round loop did not terminate (internal error)");
     }
     if (r > stats.rounds) stats.rounds = r;
@@ -1034,7 +1076,10 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
       stats.active_pair_rounds += (int64_t)ctl_h.advanced;
       stats.tile_blocks += (int64_t)ctl_h.tile_blocks;
       stats.tile_draws += (int64_t)ctl_h.tile_draws;
+      stats.level_mma_tiles += (int64_t)ctl_h.lmma_tiles;
+  stats.level_mma_tiles += (int64_t)ctl_h.lmma_tiles;
   stats.tile_draws += (int64_t)ctl_h.tile_draws;
+  stats.level_mma_tiles += (int64_t)ctl_h.lmma_tiles;
       for (int a = 0; a < qn; ++a) {
         stats.draws += qs[a].draws;
         stats.exact_fallbacks += qs[a].nexact;

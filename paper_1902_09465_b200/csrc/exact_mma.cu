@@ -356,4 +356,275 @@ cudaError_t launch_exact_fallback_mma(const Geom &g, cudaStream_t s) {
 int exact_tile_rows() { return MM_BM; }
 int exact_tile_cols() { return MM_BN; }
 
+
+// ===========================================================================
+// Query-independent draws on the tensor cores.
+//
+// With shared draws every query sees the same s = 2^c coordinates j_1..j_s of point i
+// at level c.  With w_j their multiplicities, the level's update of pair (q, i) is
+//   sum_t (x_ij_t - q_j_t)^2 = sum_j w_j x_ij^2 - 2 sum_j (w_j x_ij) q_j + sum_j w_j q_j^2,
+// i.e. two integer GEMMs over K = d for a (query x point) tile: Q . (w o x) and
+// (Q o Q) . w.  Operands are unsigned bytes (kind::i8): w o x <= 255 w splits into
+// two byte planes, q^2 <= 65025 into two, w (<= 255, else the point is left to the
+// lists) is one: four tcgen05.mma accumulators of 128 x 128 int32 fill the 512 TMEM
+// columns.  Exact in int32 (every partial sum < 2^31), so S is bit-identical to the
+// per-draw sums.  k_build_w writes the planes of the round's level (one warp per
+// point: Philox once per point, not per pair); k_level_mma runs the 128 x 128 tiles
+// that k_filter found holding >= g.lmin pairs at that level; its epilogue updates
+// exactly those pairs (S += wa + B - 2 C, level c -> c + 1).
+constexpr int LM_BM = 128, LM_BN = 128, LM_STAGES = 2;
+constexpr uint32_t LM_PLANE = LM_BM * MM_BK;                 // 16 KB per operand plane
+constexpr uint32_t LM_STAGE_BYTES = 6 * LM_PLANE;            // Q, Q2lo, Q2hi | Wx0, Wx1, Wc
+constexpr size_t LM_SMEM = (size_t)LM_STAGES * LM_STAGE_BYTES + 1024 + 256;
+constexpr uint32_t LM_TMEM_COLS = 512;
+constexpr int LM_DS = LM_BN + 4;  // ints per row of the staged B - 2C tile
+
+__global__ void k_q2_planes(Geom g) {  // q_j^2 as two byte planes (low, high)
+  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x, tot = (size_t)g.q * g.pitch;
+  if (t >= tot) return;
+  const uint32_t v = g.Q[t], sq = v * v;
+  g.q2lo[t] = (uint8_t)(sq & 255u);
+  g.q2hi[t] = (uint8_t)(sq >> 8);
+}
+
+// The level's planes for every point: w_j (multiplicity of coordinate j among the
+// s = 2^c shared draws), w_j x_j (two bytes), wa = sum_j w_j x_j^2.  wovf[i] = 1 when
+// some w_j > 255 (the point's pairs then take the list path).  One warp per point.
+__global__ void __launch_bounds__(256) k_build_w(Geom g) {
+  extern __shared__ uint32_t wcnt[];  // [8 warps][pitch]
+  const int c = g.ctl->gemm_level;
+  if (c < 0) return;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int i = blockIdx.x * 8 + warp;
+  if (i >= g.n) return;
+  const int pitch = (int)g.pitch;
+  uint32_t *cnt = wcnt + (size_t)warp * pitch;
+  for (int j = lane; j < pitch; j += 32) cnt[j] = 0;
+  __syncwarp();
+  const uint32_t s = 1u << c, nb = (s + 3) / 4, lv = (uint32_t)(c + 1), d = (uint32_t)g.d;
+  for (uint32_t b = lane; b < nb; b += 32) {
+    const uint4 w = philox4x32_10_rk(make_uint4(b, (uint32_t)i + g.id_offset, SHARED_QI, lv), g.rk0, g.rk1);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e)
+      if (4 * b + e < s) atomicAdd(&cnt[coord_of(ws[e], d)], 1u);
+  }
+  __syncwarp();
+  const uint8_t *xr = g.X + (size_t)i * pitch;
+  const size_t o = (size_t)i * pitch;
+  int32_t wa = 0;
+  bool ovf = false;
+  for (int j = lane; j < pitch; j += 32) {
+    const uint32_t wj = cnt[j], x = xr[j], wx = wj * x;
+    ovf |= wj > 255u;
+    g.wc[o + j] = (uint8_t)(wj > 255u ? 0u : wj);
+    g.wx0[o + j] = (uint8_t)(wx & 255u);
+    g.wx1[o + j] = (uint8_t)(wx >> 8);
+    wa += (int32_t)(wj * x * x);
+  }
+#pragma unroll
+  for (int k = 16; k > 0; k >>= 1) wa += __shfl_xor_sync(0xffffffffu, wa, k);
+  ovf = __any_sync(0xffffffffu, ovf);
+  if (lane == 0) {
+    g.wa[i] = wa;
+    g.wovf[i] = ovf ? 1 : 0;
+  }
+}
+
+__global__ void __launch_bounds__(MM_NT, 1)
+    k_level_mma(const __grid_constant__ CUtensorMap tQ, const __grid_constant__ CUtensorMap tQ2l,
+                const __grid_constant__ CUtensorMap tQ2h, const __grid_constant__ CUtensorMap tWx0,
+                const __grid_constant__ CUtensorMap tWx1, const __grid_constant__ CUtensorMap tWc, Geom g) {
+  const int m0 = blockIdx.y * LM_BM, n0 = blockIdx.x * LM_BN;
+  const int c = g.ctl->gemm_level;
+  __shared__ uint32_t sflag;
+  if (threadIdx.x == 0) {
+    uint32_t *f = g.lvcnt + ((size_t)(m0 / LM_BM) * g.lv_cols + (n0 / LM_BN)) * MAX_LEVELS;
+    sflag = (c >= 0 && f[c] >= g.lmin) ? 1u : 0u;
+  }
+  __syncthreads();
+  if (!sflag) return;  // uniform
+  if (threadIdx.x == 0) atomicAdd(&g.ctl->lmma_tiles, 1ull);
+  extern __shared__ __align__(1024) unsigned char smraw[];
+  unsigned char *sm = reinterpret_cast<unsigned char *>(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
+  uint64_t *full = reinterpret_cast<uint64_t *>(sm + LM_STAGES * LM_STAGE_BYTES);
+  uint64_t *empty = full + LM_STAGES;
+  uint64_t *tfull = empty + LM_STAGES;
+  uint32_t *tmem_base = reinterpret_cast<uint32_t *>(tfull + 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nk = (g.d + MM_BK - 1) / MM_BK;
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < LM_STAGES; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, 1);
+    }
+    mbar_init(tfull, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base)),
+                 "n"(LM_TMEM_COLS));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_base;
+
+  if (warp == 0) {
+    if (lane == 0) {  // TMA producer: 6 planes per k-block
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % LM_STAGES;
+        if (kb >= LM_STAGES) mbar_wait(empty + s, ((kb / LM_STAGES) - 1) & 1);
+        unsigned char *sa = sm + s * LM_STAGE_BYTES;
+        mbar_expect_tx(full + s, LM_STAGE_BYTES);
+        tma_load_2d(sa + 0 * LM_PLANE, &tQ, full + s, kb * MM_BK, m0);
+        tma_load_2d(sa + 1 * LM_PLANE, &tQ2l, full + s, kb * MM_BK, m0);
+        tma_load_2d(sa + 2 * LM_PLANE, &tQ2h, full + s, kb * MM_BK, m0);
+        tma_load_2d(sa + 3 * LM_PLANE, &tWx0, full + s, kb * MM_BK, n0);
+        tma_load_2d(sa + 4 * LM_PLANE, &tWx1, full + s, kb * MM_BK, n0);
+        tma_load_2d(sa + 5 * LM_PLANE, &tWc, full + s, kb * MM_BK, n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // MMA issuer: acc0 = Q.Wx0, acc1 = Q.Wx1, acc2 = Q2lo.Wc, acc3 = Q2hi.Wc
+      constexpr uint32_t idesc = umma_idesc_u8(LM_BM, LM_BN);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % LM_STAGES;
+        mbar_wait(full + s, (kb / LM_STAGES) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t sb = smem_u32(sm + s * LM_STAGE_BYTES);
+#pragma unroll
+        for (int a = 0; a < 4; ++a) {
+          const uint32_t pa = sb + (uint32_t)(a < 2 ? 0 : a - 1) * LM_PLANE;  // Q, Q, Q2lo, Q2hi
+          const uint32_t pb = sb + (uint32_t)(a == 0 ? 3 : (a == 1 ? 4 : 5)) * LM_PLANE;
+#pragma unroll
+          for (int kk = 0; kk < MM_BK / 32; ++kk) {
+            const uint64_t da = umma_desc_sw128(pa + kk * 32), db = umma_desc_sw128(pb + kk * 32);
+            const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+            asm volatile(
+                "{\n\t.reg .pred p;\n\t"
+                "setp.ne.b32 p, %4, 0;\n\t"
+                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (uint32_t)a * LM_BN),
+                "l"(da), "l"(db), "r"(idesc), "r"(acc));
+          }
+        }
+        asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                         smem_u32(empty + s))
+                     : "memory");
+      }
+      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                       smem_u32(tfull))
+                   : "memory");
+    }
+  } else if (warp >= 4) {  // epilogue: TMEM lanes 32*(warp-4) .. +31 = query rows
+    const int quad = warp - 4;
+    mbar_wait(tfull, 0);
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    // B - 2C of the tile into shared memory (the operand buffers are free now), rows of
+    // LM_DS ints (padded against bank conflicts); the update pass below is coalesced
+    int32_t *dt = reinterpret_cast<int32_t *>(sm);
+    const int r = quad * 32 + lane;
+#pragma unroll 1
+    for (int c0 = 0; c0 < LM_BN; c0 += 32) {
+      uint32_t v[32];
+      int32_t C[32], B[32];
+      const uint32_t lane_addr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0;
+#pragma unroll
+      for (int a = 0; a < 4; ++a) {
+        asm volatile(
+            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
+              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
+              "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
+              "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
+              "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+            : "r"(lane_addr + (uint32_t)a * LM_BN));
+        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          if (a == 0) C[j] = (int32_t)v[j];
+          if (a == 1) C[j] += (int32_t)v[j] << 8;
+          if (a == 2) B[j] = (int32_t)v[j];
+          if (a == 3) B[j] += (int32_t)v[j] << 8;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < 32; j += 4)
+        *reinterpret_cast<int4 *>(dt + r * LM_DS + c0 + j) =
+            make_int4(B[j] - 2 * C[j], B[j + 1] - 2 * C[j + 1], B[j + 2] - 2 * C[j + 2], B[j + 3] - 2 * C[j + 3]);
+    }
+  }
+  __syncwarp();
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  // the update, coalesced: a warp takes 128 consecutive pairs of one query row;
+  // S += wa + (B - 2C) and c -> c + 1 for the pairs whose action is this level
+  {
+    const int32_t *dt = reinterpret_cast<const int32_t *>(sm);
+    const uint8_t lvc = (uint8_t)(c + 1);
+    for (int it = threadIdx.x; it < LM_BM * LM_BN / 4; it += MM_NT) {
+      const int rr = it / (LM_BN / 4), cc = (it % (LM_BN / 4)) * 4;
+      const int row = m0 + rr, col = n0 + cc;
+      if (row >= g.q || col >= g.n) continue;
+      if (g.qs[row].done) continue;
+      const size_t o = (size_t)row * g.npad + col;  // npad % 16 == 0: 16-byte aligned
+      const uint32_t a4 = *reinterpret_cast<const uint32_t *>(g.act + o);
+      uint32_t hit = 0;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        hit |= (((a4 >> (8 * k)) & 0xFFu) == lvc && col + k < g.n && !g.wovf[col + k]) ? (1u << k) : 0u;
+      if (!hit) continue;
+      int4 S4 = *reinterpret_cast<const int4 *>(g.S + o);
+      uint32_t l4 = *reinterpret_cast<const uint32_t *>(g.lvl + o);
+      const int4 dd = *reinterpret_cast<const int4 *>(dt + rr * LM_DS + cc);
+      const int4 wa4 = *reinterpret_cast<const int4 *>(g.wa + col);  // wa padded to npad
+      if (hit & 1u) { S4.x += wa4.x + dd.x; l4 = (l4 & ~0xFFu) | lvc; }
+      if (hit & 2u) { S4.y += wa4.y + dd.y; l4 = (l4 & ~0xFF00u) | ((uint32_t)lvc << 8); }
+      if (hit & 4u) { S4.z += wa4.z + dd.z; l4 = (l4 & ~0xFF0000u) | ((uint32_t)lvc << 16); }
+      if (hit & 8u) { S4.w += wa4.w + dd.w; l4 = (l4 & ~0xFF000000u) | ((uint32_t)lvc << 24); }
+      *reinterpret_cast<int4 *>(g.S + o) = S4;
+      *reinterpret_cast<uint32_t *>(g.lvl + o) = l4;
+    }
+  }
+  if (warp == 2) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(LM_TMEM_COLS));
+  }
+}
+
+cudaError_t launch_q2_planes(const Geom &g, cudaStream_t s) {
+  const size_t tot = (size_t)g.q * g.pitch;
+  if (tot) k_q2_planes<<<(unsigned)((tot + 255) / 256), 256, 0, s>>>(g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_build_w(const Geom &g, cudaStream_t s) {
+  const size_t smem = (size_t)8 * g.pitch * sizeof(uint32_t);
+  cudaError_t e = cudaFuncSetAttribute(k_build_w, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_build_w<<<(unsigned)((g.n + 7) / 8), 256, smem, s>>>(g);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_level_mma(const Geom &g, cudaStream_t s) {
+  CUtensorMap tq, tq2l, tq2h, tw0, tw1, twc;
+  cudaError_t err = make_map(&tq, g.Q, g.q, g.d, g.pitch, LM_BM);
+  if (err == cudaSuccess) err = make_map(&tq2l, g.q2lo, g.q, g.d, g.pitch, LM_BM);
+  if (err == cudaSuccess) err = make_map(&tq2h, g.q2hi, g.q, g.d, g.pitch, LM_BM);
+  if (err == cudaSuccess) err = make_map(&tw0, g.wx0, g.n, g.d, g.pitch, LM_BN);
+  if (err == cudaSuccess) err = make_map(&tw1, g.wx1, g.n, g.d, g.pitch, LM_BN);
+  if (err == cudaSuccess) err = make_map(&twc, g.wc, g.n, g.d, g.pitch, LM_BN);
+  if (err != cudaSuccess) return err;
+  err = cudaFuncSetAttribute(k_level_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LM_SMEM);
+  if (err != cudaSuccess) return err;
+  dim3 grid((g.n + LM_BN - 1) / LM_BN, (g.q + LM_BM - 1) / LM_BM);
+  k_level_mma<<<grid, MM_NT, LM_SMEM, s>>>(tq, tq2l, tq2h, tw0, tw1, twc, g);
+  return cudaGetLastError();
+}
+
+int level_tile_rows() { return LM_BM; }
+int level_tile_cols() { return LM_BN; }
+
 }  // namespace aknn

@@ -55,7 +55,7 @@ struct QState {
 // Per-round control block (device memory; one per batch).
 struct RoundCtl {
   unsigned int n_active;                  // queries failing Eq. (5) this round
-  unsigned int pad0;
+  int gemm_level;                         // shared draws: the slot k_level_mma takes this round (-1: none)
   unsigned int cnt[NSLOT];                // pairs per action slot
   unsigned int off[NSLOT + 1];            // list offsets per slot
   unsigned int cursor[NSLOT];             // scatter cursors
@@ -63,6 +63,7 @@ struct RoundCtl {
   unsigned long long advanced;            // pairs advanced, cumulative
   unsigned long long tile_blocks;         // Philox blocks of the tile gathers, cumulative
   unsigned long long tile_draws;          // (query, point) draws of the tile gathers, cumulative
+  unsigned long long lmma_tiles;          // 128 x 128 tiles run by k_level_mma, cumulative
   // cumulative, maintained on the device by k_round_ctl (graph-launched loop)
   unsigned int round;                     // rounds evaluated
   unsigned int evaluated;                 // queries the next rank split looks at
@@ -98,6 +99,15 @@ struct Geom {
   uint32_t id_offset;    // global id of local row 0
   uint32_t qi0;          // RNG query index of batch row 0
   int shared_draws;      // 1: query-independent draws: counter word 0xFFFFFFFF
+  // shared draws on the tensor cores (exact_mma.cu, k_level_mma)
+  int level_mma;         // 1: the round's dominant level runs as integer GEMMs
+  uint8_t *q2lo, *q2hi;  // [q][pitch] q_j^2 byte planes
+  uint8_t *wx0, *wx1, *wc;  // [n][pitch] w_j x_j (two bytes) and w_j of the level
+  int32_t *wa;           // [n] sum_j w_j x_j^2
+  uint8_t *wovf;         // [n] some w_j > 255: the point's pairs take the lists
+  uint32_t *lvcnt;       // [ceil(q/128)][lv_cols][MAX_LEVELS] pairs per level in the 128 x 128 tile
+  int lv_cols;
+  uint32_t lmin;         // tiles with >= lmin pairs at the level run on the tensor cores
   uint32_t seed_lo, seed_hi;
   uint32_t rk0[10], rk1[10]; // Philox round keys of (seed_lo, seed_hi): kernel-param
                              // constants, so each round's key XOR is one LOP3

@@ -70,6 +70,12 @@ cudaError_t launch_exact_mma(const ExactGeom &e, const int32_t *nq, const int32_
 // Exact fallbacks of a round on the tensor cores (flagged tiles only).
 cudaError_t launch_exact_fallback_mma(const Geom &g, cudaStream_t s);
 int exact_tile_rows();
+// Shared draws on the tensor cores (exact_mma.cu).
+cudaError_t launch_q2_planes(const Geom &g, cudaStream_t s);
+cudaError_t launch_build_w(const Geom &g, cudaStream_t s);
+cudaError_t launch_level_mma(const Geom &g, cudaStream_t s);
+int level_tile_rows();
+int level_tile_cols();
 int exact_tile_cols();
 cudaError_t launch_row_norms(const uint8_t *A, int64_t pitch, int rows, int32_t *out, cudaStream_t s);
 

@@ -246,6 +246,7 @@ struct SlotRun {
 __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
   extern __shared__ uint32_t tcnt[];  // [FIL_ROWS / R][FIL_NT * 4 / P] (tiles on)
   __shared__ unsigned scnt[NSLOT];
+  __shared__ unsigned lvc[(FIL_NT * 4 / 128) * MAX_LEVELS];
   const int q0 = blockIdx.y * FIL_ROWS;
   const int rows = min(FIL_ROWS, g.q - q0);
   const int i0 = (blockIdx.x * FIL_NT + threadIdx.x) * 4;
@@ -254,6 +255,7 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
   const int ntc = g.tile_on ? (FIL_ROWS >> g.tile_lr) * tcols : 0;
   for (int s = threadIdx.x; s < NSLOT; s += FIL_NT) scnt[s] = 0;
   for (int t = threadIdx.x; t < ntc; t += FIL_NT) tcnt[t] = 0;
+  for (int t = threadIdx.x; t < (FIL_NT * 4 / 128) * MAX_LEVELS; t += FIL_NT) lvc[t] = 0;
   __syncthreads();
   const bool arms = i0 < g.n;
   // two rows of loads in flight ahead of the row being decided
@@ -263,7 +265,7 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
     a0 = load_arm4(g, q0, i0);
     if (rows > 1) a1 = load_arm4(g, q0 + 1, i0);
   }
-  SlotRun run;
+  SlotRun run, lrun;      // lrun: the thread's pairs per level in its 128 x 128 level tile
   unsigned ex_acc = 0;     // exact fallbacks of this thread (one 128-query tile row: 32 | 128)
   uint32_t dr_acc = 0;     // sampled draws of this thread in the current tile row
   int tr_cur = 0;
@@ -286,6 +288,7 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
       const uint32_t act = (actw >> (8 * e)) & 0xFFu;
       ex_acc += act == ACT_EXACT;
       if (act) run.add(act == ACT_EXACT ? (unsigned)MAX_LEVELS : act - 1u, scnt);
+      if (g.level_mma && act && act != ACT_EXACT) lrun.add(act - 1u, lvc + ((threadIdx.x * 4) >> 7) * MAX_LEVELS);
     }
     if (g.tile_on) {
       const int tr = r >> g.tile_lr;
@@ -298,6 +301,7 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
     }
   }
   run.flush(scnt);
+  if (g.level_mma) lrun.flush(lvc + ((threadIdx.x * 4) >> 7) * MAX_LEVELS);
   if (g.tile_on && dr_acc) atomicAdd(&tcnt[tr_cur * tcols + ((threadIdx.x * 4) >> g.tile_lp)], dr_acc);
   if (g.exact_mma) {
     // a warp's 128 arms lie in one 128 x 256 tile of the tensor-core pass: count them
@@ -306,6 +310,12 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
   }
   __syncthreads();
   if (threadIdx.x < NSLOT && scnt[threadIdx.x]) atomicAdd(&g.ctl->cnt[threadIdx.x], scnt[threadIdx.x]);
+  if (g.level_mma)
+    for (int t = threadIdx.x; t < (FIL_NT * 4 / 128) * MAX_LEVELS; t += FIL_NT) {
+      const int lc = ((blockIdx.x * FIL_NT * 4) >> 7) + t / MAX_LEVELS;
+      if (lvc[t] && lc < g.lv_cols)
+        atomicAdd(&g.lvcnt[((size_t)(q0 >> 7) * g.lv_cols + lc) * MAX_LEVELS + t % MAX_LEVELS], lvc[t]);
+    }
   // every tile of this CTA, including those of finished queries (count 0)
   for (int t = threadIdx.x; t < ntc; t += FIL_NT) {
     const int tr = (q0 >> g.tile_lr) + t / tcols;
@@ -339,8 +349,20 @@ __host__ __device__ __forceinline__ unsigned pairs_per_chunk(int slot, unsigned 
   return nb <= (unsigned)ADV_P ? 32u * ADV_P / nb : 32u / lanes_per_pair(nb, bpl);
 }
 
-__global__ void k_plan(RoundCtl *ctl, unsigned bpl, int stage_lo) {
+__global__ void k_plan(RoundCtl *ctl, unsigned bpl, int stage_lo, int level_mma, unsigned level_min) {
   if (threadIdx.x != 0) return;
+  if (level_mma) {  // shared draws: the most populated sampled level goes to the tensor cores
+    int best = -1;
+    unsigned bc = 0;
+    for (int s = 0; s < MAX_LEVELS; ++s)
+      if (ctl->cnt[s] > bc) {
+        bc = ctl->cnt[s];
+        best = s;
+      }
+    ctl->gemm_level = (best >= 0 && bc >= level_min) ? best : -1;
+  } else {
+    ctl->gemm_level = -1;
+  }
   unsigned off = 0;
   unsigned long long ch = 0, adv = 0;
   for (int s = 0; s < NSLOT; ++s) {
@@ -403,6 +425,13 @@ __global__ void __launch_bounds__(FIL_NT) k_scatter(Geom g) {
     if (!dense) any_listed = 1;
   }
   if (!g.tile_on && threadIdx.x == 0) any_listed = 1;
+  __shared__ uint8_t slv[FIL_NT * 4 / 128];  // the chunk's 128 x 128 level tiles: tensor cores?
+  const int glev = g.level_mma ? g.ctl->gemm_level : -1;
+  if (threadIdx.x < (FIL_NT * 4) / 128) {
+    const int lc = (c0 >> 7) + (int)threadIdx.x;
+    slv[threadIdx.x] = glev >= 0 && lc < g.lv_cols &&
+                       g.lvcnt[((size_t)(qi >> 7) * g.lv_cols + lc) * MAX_LEVELS + glev] >= g.lmin;
+  }
   if (threadIdx.x < (FIL_NT * 4) / 256) {
     const int xc = (c0 >> 8) + (int)threadIdx.x;
     const uint32_t cnt = (g.exact_mma && xc < g.xf_cols) ? g.xflags[(size_t)(qi >> 7) * g.xf_cols + xc] : 0u;
@@ -425,6 +454,8 @@ __global__ void __launch_bounds__(FIL_NT) k_scatter(Geom g) {
       slot[e] = NONE;  // a dense tile of the tensor-core exact pass takes it
     if (g.tile_on && slot[e] < (unsigned)MAX_LEVELS && sdense[(i - c0) >> g.tile_lp])
       slot[e] = NONE;  // k_advance_tiles takes it
+    if (g.level_mma && (int)slot[e] == glev && slv[(i - c0) >> 7] && !g.wovf[i])
+      slot[e] = NONE;  // k_level_mma takes it
     const unsigned m = __match_any_sync(FULL, slot[e]);
     const int leader = __ffs(m) - 1;
     unsigned b = 0;
@@ -840,6 +871,10 @@ static inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b
 cudaError_t launch_init(const Geom &g, cudaStream_t s) {
   k_init<<<dim3(cdiv(g.npad, 256), g.q), 256, 0, s>>>(g);
   k_init_qstate<<<cdiv(g.q, 128), 128, 0, s>>>(g);
+  if (g.level_mma) {
+    const cudaError_t e = launch_q2_planes(g, s);
+    if (e != cudaSuccess) return e;
+  }
   if (g.tile_on) {
     const size_t rows = ((size_t)g.q + (1u << g.tile_lr) - 1) >> g.tile_lr;
     const cudaError_t e = cudaMemsetAsync(g.tilework, 0, sizeof(uint32_t) * rows * g.tile_cols, s);
@@ -871,7 +906,11 @@ cudaError_t launch_filter(const Geom &g, cudaStream_t s) {
 }
 
 cudaError_t launch_compact(const Geom &g, cudaStream_t s) {
-  k_plan<<<1, 32, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo);
+  k_plan<<<1, 32, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo, g.level_mma, 1u << 16);
+  if (g.level_mma) {
+    const cudaError_t e = launch_build_w(g, s);
+    if (e != cudaSuccess) return e;
+  }
   k_scatter<<<dim3(g.q, cdiv(g.npad, FIL_NT * 4)), FIL_NT, 0, s>>>(g);
   k_plan_lists<<<1, 32, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo);  // the lists as written
   return cudaGetLastError();

@@ -386,3 +386,25 @@ def test_shared_draws_config1_and_reduced_config2(ak):
                    flags=ak.FLAG_SHARED_DRAWS)
     ix.close()
     _assert_parity(got, orc.query_br(X, Q, cfg.k, cfg.h, cfg.seed, al, want_sums=True, shared_draws=True))
+
+
+@pytest.mark.parametrize("n,d,q,k,h,kind", [(20011, 100, 130, 5, 5, "theory"), (9000, 784, 64, 10, 10, "theory"),
+                                            (6001, 48, 257, 4, 4, "exp")])
+def test_shared_draws_level_mma(ak, n, d, q, k, h, kind):
+    """Shared draws with the round's dominant level as tensor-core GEMMs (k_level_mma,
+    default) == the per-pair gathers (AKNN_FLAG_NO_LEVEL_MMA) == the oracle.  Ragged n
+    and q leave partial 128 x 128 tiles; the GEMM path must actually have run."""
+    X, Q = synth.small_instance(n + 7 * d, n, d, q=q)
+    al = orc.alpha_theory(n, 0.05, d) if kind == "theory" else orc.alpha_experimental(n, 0.05, d, 0.05)
+    ix = ak.Index(X)
+    a = ix.query(Q, k, h, 0.05, 43, al, counts=True, sums=True, flags=ak.FLAG_SHARED_DRAWS)
+    sa = ix.stats()
+    b = ix.query(Q, k, h, 0.05, 43, al, counts=True, sums=True,
+                 flags=ak.FLAG_SHARED_DRAWS | ak.FLAG_NO_LEVEL_MMA)
+    ix.close()
+    assert sa["level_mma_tiles"] > 0
+    for key in KEYS:
+        assert np.array_equal(a[key], b[key]), key
+    rows = np.arange(0, q, max(1, q // 6))
+    ref = orc.query_br(X, Q[rows], k, h, 43, al, want_sums=True, shared_draws=True)
+    _assert_parity(a, ref, rows=rows)
