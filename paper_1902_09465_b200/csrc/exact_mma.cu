@@ -89,6 +89,7 @@ struct EpiDistances {
   int32_t *D;
   int64_t ldd;
   int q, n;
+  __device__ __forceinline__ int rows() const { return q; }
   __device__ __forceinline__ bool tile_active(int, int) const { return true; }
   __device__ __forceinline__ void store(int row, int col0, const uint32_t (&v)[32]) const {
     if (row >= q) return;
@@ -118,6 +119,7 @@ struct EpiDistances {
 // pairs for the row-stream path instead); every CTA clears its count for the next round.
 struct EpiFallback {
   Geom g;
+  __device__ __forceinline__ int rows() const { return g.q; }
   __device__ __forceinline__ bool tile_active(int m0, int n0) const {
     __shared__ uint32_t sflag;
     uint32_t *f = g.xflags + (size_t)(m0 / MM_BM) * g.xf_cols + (n0 / MM_BN);
@@ -174,7 +176,10 @@ template <class Epi>
 __global__ void __launch_bounds__(MM_NT, 1)
     k_mma_tiles(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmX, int d,
                 const __grid_constant__ Epi epi) {
-  const int m0 = blockIdx.y * MM_BM, n0 = blockIdx.x * MM_BN;
+  // query tiles fastest: the CTAs resident at once share each point tile through L2,
+  // so X (or the level's w planes) streams from HBM about once per launch
+  const int mt = (epi.rows() + MM_BM - 1) / MM_BM;
+  const int m0 = (int)(blockIdx.x % mt) * MM_BM, n0 = (int)(blockIdx.x / mt) * MM_BN;
   if (!epi.tile_active(m0, n0)) return;  // uniform across the CTA
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char *sm = reinterpret_cast<unsigned char *>(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
@@ -331,7 +336,7 @@ cudaError_t launch_exact_mma(const ExactGeom &e, const int32_t *nq, const int32_
   err = cudaFuncSetAttribute(k_mma_tiles<EpiDistances>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MM_SMEM);
   if (err != cudaSuccess) return err;
   const EpiDistances epi{nq, nx, e.D, e.npad, e.q, e.n};
-  dim3 grid((e.n + MM_BN - 1) / MM_BN, (e.q + MM_BM - 1) / MM_BM);
+  const unsigned grid = (unsigned)(((e.q + MM_BM - 1) / MM_BM) * ((e.n + MM_BN - 1) / MM_BN));
   k_mma_tiles<EpiDistances><<<grid, MM_NT, MM_SMEM, s>>>(tq, tx, e.d, epi);
   return cudaGetLastError();
 }
@@ -348,7 +353,7 @@ cudaError_t launch_exact_fallback_mma(const Geom &g, cudaStream_t s) {
   err = cudaFuncSetAttribute(k_mma_tiles<EpiFallback>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MM_SMEM);
   if (err != cudaSuccess) return err;
   const EpiFallback epi{g};
-  dim3 grid((g.n + MM_BN - 1) / MM_BN, (g.q + MM_BM - 1) / MM_BM);
+  const unsigned grid = (unsigned)(((g.q + MM_BM - 1) / MM_BM) * ((g.n + MM_BN - 1) / MM_BN));
   k_mma_tiles<EpiFallback><<<grid, MM_NT, MM_SMEM, s>>>(tq, tx, g.d, epi);
   return cudaGetLastError();
 }
@@ -377,7 +382,6 @@ constexpr uint32_t LM_PLANE = LM_BM * MM_BK;                 // 16 KB per operan
 constexpr uint32_t LM_STAGE_BYTES = 6 * LM_PLANE;            // Q, Q2lo, Q2hi | Wx0, Wx1, Wc
 constexpr size_t LM_SMEM = (size_t)LM_STAGES * LM_STAGE_BYTES + 1024 + 256;
 constexpr uint32_t LM_TMEM_COLS = 512;
-constexpr int LM_DS = LM_BN + 4;  // ints per row of the staged B - 2C tile
 
 __global__ void k_q2_planes(Geom g) {  // q_j^2 as two byte planes (low, high)
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x, tot = (size_t)g.q * g.pitch;
@@ -428,29 +432,66 @@ __global__ void __launch_bounds__(256) k_build_w(Geom g) {
   if (lane == 0) {
     g.wa[i] = wa;
     g.wovf[i] = ovf ? 1 : 0;
+    if (ovf) atomicOr(&g.ctl->wovf_any, 1u);
   }
 }
 
-__global__ void __launch_bounds__(MM_NT, 1)
+// Persistent: one CTA per SM walks the flagged 128 x 128 tiles (query tiles fastest,
+// so the resident CTAs share each point tile's planes through L2).  Warp 0 issues
+// the TMA loads and runs ahead across tiles through the LM_STAGES ring; warp 1
+// issues the MMAs of a tile once the epilogue has drained the previous tile's
+// accumulators (warp 1 also owns the TMEM allocation); warps 2..9 drain TMEM into registers (a warp: its 32-lane quadrant
+// x 64 columns), release TMEM at once and then update S / lvl from registers while
+// the next tile's loads and MMAs run.
+constexpr int LM_EPI_WARP0 = 2, LM_EPI_WARPS = 8;
+constexpr int LM_EPI_COLS = LM_BN * 4 / LM_EPI_WARPS;  // columns per epilogue thread
+constexpr int LM_NT = 32 * (LM_EPI_WARP0 + LM_EPI_WARPS);
+
+__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+
+__device__ __forceinline__ bool level_tile_on(const Geom &g, int c, int mt, int t) {
+  const int mi = t % mt, ni = t / mt;
+  return g.lvcnt[((size_t)mi * g.lv_cols + ni) * MAX_LEVELS + c] >= g.lmin;
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+        "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
+        "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
+        "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
+      : "r"(taddr));
+}
+
+__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
+      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
+        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
+        "=r"(v[15])
+      : "r"(taddr));
+}
+
+__global__ void __launch_bounds__(LM_NT, 1)
     k_level_mma(const __grid_constant__ CUtensorMap tQ, const __grid_constant__ CUtensorMap tQ2l,
                 const __grid_constant__ CUtensorMap tQ2h, const __grid_constant__ CUtensorMap tWx0,
                 const __grid_constant__ CUtensorMap tWx1, const __grid_constant__ CUtensorMap tWc, Geom g) {
-  const int m0 = blockIdx.y * LM_BM, n0 = blockIdx.x * LM_BN;
   const int c = g.ctl->gemm_level;
-  __shared__ uint32_t sflag;
-  if (threadIdx.x == 0) {
-    uint32_t *f = g.lvcnt + ((size_t)(m0 / LM_BM) * g.lv_cols + (n0 / LM_BN)) * MAX_LEVELS;
-    sflag = (c >= 0 && f[c] >= g.lmin) ? 1u : 0u;
-  }
-  __syncthreads();
-  if (!sflag) return;  // uniform
-  if (threadIdx.x == 0) atomicAdd(&g.ctl->lmma_tiles, 1ull);
+  if (c < 0) return;  // uniform
+  const int mt = (g.q + LM_BM - 1) / LM_BM;
+  const int ntiles = mt * ((g.n + LM_BN - 1) / LM_BN);
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char *sm = reinterpret_cast<unsigned char *>(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
   uint64_t *full = reinterpret_cast<uint64_t *>(sm + LM_STAGES * LM_STAGE_BYTES);
   uint64_t *empty = full + LM_STAGES;
   uint64_t *tfull = empty + LM_STAGES;
-  uint32_t *tmem_base = reinterpret_cast<uint32_t *>(tfull + 1);
+  uint64_t *tempty = tfull + 1;
+  uint32_t *tmem_base = reinterpret_cast<uint32_t *>(tempty + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int nk = (g.d + MM_BK - 1) / MM_BK;
   if (warp == 0 && lane == 0) {
@@ -459,9 +500,10 @@ __global__ void __launch_bounds__(MM_NT, 1)
       mbar_init(empty + s, 1);
     }
     mbar_init(tfull, 1);
+    mbar_init(tempty, LM_EPI_WARPS);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (warp == 2) {
+  if (warp == 1) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_base)),
                  "n"(LM_TMEM_COLS));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -472,123 +514,149 @@ __global__ void __launch_bounds__(MM_NT, 1)
   const uint32_t tmem = *tmem_base;
 
   if (warp == 0) {
-    if (lane == 0) {  // TMA producer: 6 planes per k-block
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % LM_STAGES;
-        if (kb >= LM_STAGES) mbar_wait(empty + s, ((kb / LM_STAGES) - 1) & 1);
-        unsigned char *sa = sm + s * LM_STAGE_BYTES;
-        mbar_expect_tx(full + s, LM_STAGE_BYTES);
-        tma_load_2d(sa + 0 * LM_PLANE, &tQ, full + s, kb * MM_BK, m0);
-        tma_load_2d(sa + 1 * LM_PLANE, &tQ2l, full + s, kb * MM_BK, m0);
-        tma_load_2d(sa + 2 * LM_PLANE, &tQ2h, full + s, kb * MM_BK, m0);
-        tma_load_2d(sa + 3 * LM_PLANE, &tWx0, full + s, kb * MM_BK, n0);
-        tma_load_2d(sa + 4 * LM_PLANE, &tWx1, full + s, kb * MM_BK, n0);
-        tma_load_2d(sa + 5 * LM_PLANE, &tWc, full + s, kb * MM_BK, n0);
+    if (lane == 0) {  // TMA producer: 6 planes per k-block, running ahead across tiles
+      uint32_t kg = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        if (!level_tile_on(g, c, mt, t)) continue;
+        const int m0 = (t % mt) * LM_BM, n0 = (t / mt) * LM_BN;
+        for (int kb = 0; kb < nk; ++kb, ++kg) {
+          const uint32_t s = kg % LM_STAGES;
+          if (kg >= LM_STAGES) mbar_wait(empty + s, ((kg / LM_STAGES) - 1) & 1);
+          unsigned char *sa = sm + s * LM_STAGE_BYTES;
+          mbar_expect_tx(full + s, LM_STAGE_BYTES);
+          tma_load_2d(sa + 0 * LM_PLANE, &tQ, full + s, kb * MM_BK, m0);
+          tma_load_2d(sa + 1 * LM_PLANE, &tQ2l, full + s, kb * MM_BK, m0);
+          tma_load_2d(sa + 2 * LM_PLANE, &tQ2h, full + s, kb * MM_BK, m0);
+          tma_load_2d(sa + 3 * LM_PLANE, &tWx0, full + s, kb * MM_BK, n0);
+          tma_load_2d(sa + 4 * LM_PLANE, &tWx1, full + s, kb * MM_BK, n0);
+          tma_load_2d(sa + 5 * LM_PLANE, &tWc, full + s, kb * MM_BK, n0);
+        }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer: acc0 = Q.Wx0, acc1 = Q.Wx1, acc2 = Q2lo.Wc, acc3 = Q2hi.Wc
       constexpr uint32_t idesc = umma_idesc_u8(LM_BM, LM_BN);
-      for (int kb = 0; kb < nk; ++kb) {
-        const int s = kb % LM_STAGES;
-        mbar_wait(full + s, (kb / LM_STAGES) & 1);
-        asm volatile("tcgen05.fence::after_thread_sync;");
-        const uint32_t sb = smem_u32(sm + s * LM_STAGE_BYTES);
+      uint32_t kg = 0, tl = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        if (!level_tile_on(g, c, mt, t)) continue;
+        if (tl > 0) {  // the epilogue has drained the previous tile's accumulators
+          mbar_wait(tempty, (tl - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+        }
+        for (int kb = 0; kb < nk; ++kb, ++kg) {
+          const uint32_t s = kg % LM_STAGES;
+          mbar_wait(full + s, (kg / LM_STAGES) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t sb = smem_u32(sm + s * LM_STAGE_BYTES);
 #pragma unroll
-        for (int a = 0; a < 4; ++a) {
-          const uint32_t pa = sb + (uint32_t)(a < 2 ? 0 : a - 1) * LM_PLANE;  // Q, Q, Q2lo, Q2hi
-          const uint32_t pb = sb + (uint32_t)(a == 0 ? 3 : (a == 1 ? 4 : 5)) * LM_PLANE;
+          for (int a = 0; a < 4; ++a) {
+            const uint32_t pa = sb + (uint32_t)(a < 2 ? 0 : a - 1) * LM_PLANE;  // Q, Q, Q2lo, Q2hi
+            const uint32_t pb = sb + (uint32_t)(a == 0 ? 3 : (a == 1 ? 4 : 5)) * LM_PLANE;
 #pragma unroll
-          for (int kk = 0; kk < MM_BK / 32; ++kk) {
-            const uint64_t da = umma_desc_sw128(pa + kk * 32), db = umma_desc_sw128(pb + kk * 32);
-            const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
-            asm volatile(
-                "{\n\t.reg .pred p;\n\t"
-                "setp.ne.b32 p, %4, 0;\n\t"
-                "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (uint32_t)a * LM_BN),
-                "l"(da), "l"(db), "r"(idesc), "r"(acc));
+            for (int kk = 0; kk < MM_BK / 32; ++kk) {
+              const uint64_t da = umma_desc_sw128(pa + kk * 32), db = umma_desc_sw128(pb + kk * 32);
+              const uint32_t acc = (kb > 0 || kk > 0) ? 1u : 0u;
+              asm volatile(
+                  "{\n\t.reg .pred p;\n\t"
+                  "setp.ne.b32 p, %4, 0;\n\t"
+                  "tcgen05.mma.cta_group::1.kind::i8 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem + (uint32_t)a * LM_BN),
+                  "l"(da), "l"(db), "r"(idesc), "r"(acc));
+            }
           }
+          asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+                           smem_u32(empty + s))
+                       : "memory");
         }
         asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                         smem_u32(empty + s))
+                         smem_u32(tfull))
                      : "memory");
+        ++tl;
       }
-      asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
-                       smem_u32(tfull))
-                   : "memory");
     }
-  } else if (warp >= 4) {  // epilogue: TMEM lanes 32*(warp-4) .. +31 = query rows
-    const int quad = warp - 4;
-    mbar_wait(tfull, 0);
-    asm volatile("tcgen05.fence::after_thread_sync;");
-    // B - 2C of the tile into shared memory (the operand buffers are free now), rows of
-    // LM_DS ints (padded against bank conflicts); the update pass below is coalesced
-    int32_t *dt = reinterpret_cast<int32_t *>(sm);
-    const int r = quad * 32 + lane;
-#pragma unroll 1
-    for (int c0 = 0; c0 < LM_BN; c0 += 32) {
-      uint32_t v[32];
-      int32_t C[32], B[32];
-      const uint32_t lane_addr = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)c0;
+  } else if (warp >= LM_EPI_WARP0) {
+    // epilogue: TMEM lanes 32 * (warp % 4) .. + 31 = query rows, LM_EPI_COLS columns per warp
+    const int quad = warp & 3, part = (warp - LM_EPI_WARP0) >> 2;
+    const uint8_t lvc = (uint8_t)(c + 1);
+    uint32_t tl = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+      if (!level_tile_on(g, c, mt, t)) continue;
+      const int m0 = (t % mt) * LM_BM, n0 = (t / mt) * LM_BN;
+      const int row = m0 + quad * 32 + lane, cb = n0 + part * LM_EPI_COLS;
+      if (warp == LM_EPI_WARP0 && lane == 0) atomicAdd(&g.ctl->lmma_tiles, 1ull);
+      // D = wa + B - 2C for the thread's pairs (uint32: the wrap-around sum is exact
+      // because the final S fits 31 bits); wa is loaded while the MMAs run
+      uint32_t D[LM_EPI_COLS];
+#pragma unroll
+      for (int j = 0; j < LM_EPI_COLS / 4; ++j) {
+        const int4 w = (cb + j * 4 < g.npad) ? *reinterpret_cast<const int4 *>(g.wa + cb + j * 4)
+                                             : make_int4(0, 0, 0, 0);
+        D[j * 4 + 0] = (uint32_t)w.x;
+        D[j * 4 + 1] = (uint32_t)w.y;
+        D[j * 4 + 2] = (uint32_t)w.z;
+        D[j * 4 + 3] = (uint32_t)w.w;
+      }
+      mbar_wait(tfull, tl & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      const uint32_t ta = tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(part * LM_EPI_COLS);
 #pragma unroll
       for (int a = 0; a < 4; ++a) {
-        asm volatile(
-            "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-            "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-            : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]),
-              "=r"(v[7]), "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]),
-              "=r"(v[14]), "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]),
-              "=r"(v[20]), "=r"(v[21]), "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]),
-              "=r"(v[26]), "=r"(v[27]), "=r"(v[28]), "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-            : "r"(lane_addr + (uint32_t)a * LM_BN));
-        asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+        const uint32_t mul = a == 0 ? 0xFFFFFFFEu : (a == 1 ? 0xFFFFFE00u : (a == 2 ? 1u : 256u));  // -2, -512, 1, 256
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          if (a == 0) C[j] = (int32_t)v[j];
-          if (a == 1) C[j] += (int32_t)v[j] << 8;
-          if (a == 2) B[j] = (int32_t)v[j];
-          if (a == 3) B[j] += (int32_t)v[j] << 8;
+        for (int h = 0; h < LM_EPI_COLS / 16; ++h) {
+          uint32_t v[16];
+          tmem_ld16(ta + (uint32_t)a * LM_BN + (uint32_t)(h * 16), v);
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int j = 0; j < 16; ++j) D[h * 16 + j] += mul * v[j];
         }
       }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(tempty);  // TMEM free for the next tile's MMAs
+      ++tl;
+      if (row < g.q && cb < g.npad && !g.qs[row].done) {
+        const size_t o = (size_t)row * g.npad + cb;  // npad % 16 == 0: 16-column groups are aligned
 #pragma unroll
-      for (int j = 0; j < 32; j += 4)
-        *reinterpret_cast<int4 *>(dt + r * LM_DS + c0 + j) =
-            make_int4(B[j] - 2 * C[j], B[j + 1] - 2 * C[j + 1], B[j + 2] - 2 * C[j + 2], B[j + 3] - 2 * C[j + 3]);
+        for (int b = 0; b < LM_EPI_COLS / 16; ++b) {  // 16 pairs at a time
+          const int c16 = b * 16;
+          if (cb + c16 >= g.npad) break;
+          const uint4 a16 = *reinterpret_cast<const uint4 *>(g.act + o + c16);
+          const uint4 w16 = *reinterpret_cast<const uint4 *>(g.wovf + cb + c16);
+          const uint32_t aw[4] = {a16.x, a16.y, a16.z, a16.w};
+          const uint32_t ww[4] = {w16.x, w16.y, w16.z, w16.w};
+          uint32_t hit = 0;  // bit e: pair cb + c16 + e takes this level's update
+#pragma unroll
+          for (int e = 0; e < 16; ++e) {
+            const uint32_t av = (aw[e >> 2] >> (8 * (e & 3))) & 0xFFu, wv = (ww[e >> 2] >> (8 * (e & 3))) & 0xFFu;
+            hit |= (av == lvc && wv == 0u) ? (1u << e) : 0u;
+          }
+          if (!hit) continue;
+          int4 S4[4];
+#pragma unroll
+          for (int j = 0; j < 4; ++j)
+            if ((hit >> (j * 4)) & 15u) S4[j] = *reinterpret_cast<const int4 *>(g.S + o + c16 + j * 4);
+          const uint4 l16 = *reinterpret_cast<const uint4 *>(g.lvl + o + c16);
+          uint32_t lw[4] = {l16.x, l16.y, l16.z, l16.w};
+#pragma unroll
+          for (int j = 0; j < 4; ++j) {
+            const uint32_t hv = (hit >> (j * 4)) & 15u;
+            if (!hv) continue;
+            uint32_t sv[4] = {(uint32_t)S4[j].x, (uint32_t)S4[j].y, (uint32_t)S4[j].z, (uint32_t)S4[j].w};
+#pragma unroll
+            for (int e = 0; e < 4; ++e)
+              if ((hv >> e) & 1u) {
+                sv[e] += D[c16 + j * 4 + e];
+                lw[j] = (lw[j] & ~(0xFFu << (8 * e))) | ((uint32_t)lvc << (8 * e));
+              }
+            *reinterpret_cast<int4 *>(g.S + o + c16 + j * 4) = make_int4((int)sv[0], (int)sv[1], (int)sv[2], (int)sv[3]);
+          }
+          *reinterpret_cast<uint4 *>(g.lvl + o + c16) = make_uint4(lw[0], lw[1], lw[2], lw[3]);
+        }
+      }
     }
   }
-  __syncwarp();
-  asm volatile("tcgen05.fence::before_thread_sync;");
   __syncthreads();
-  // the update, coalesced: a warp takes 128 consecutive pairs of one query row;
-  // S += wa + (B - 2C) and c -> c + 1 for the pairs whose action is this level
-  {
-    const int32_t *dt = reinterpret_cast<const int32_t *>(sm);
-    const uint8_t lvc = (uint8_t)(c + 1);
-    for (int it = threadIdx.x; it < LM_BM * LM_BN / 4; it += MM_NT) {
-      const int rr = it / (LM_BN / 4), cc = (it % (LM_BN / 4)) * 4;
-      const int row = m0 + rr, col = n0 + cc;
-      if (row >= g.q || col >= g.n) continue;
-      if (g.qs[row].done) continue;
-      const size_t o = (size_t)row * g.npad + col;  // npad % 16 == 0: 16-byte aligned
-      const uint32_t a4 = *reinterpret_cast<const uint32_t *>(g.act + o);
-      uint32_t hit = 0;
-#pragma unroll
-      for (int k = 0; k < 4; ++k)
-        hit |= (((a4 >> (8 * k)) & 0xFFu) == lvc && col + k < g.n && !g.wovf[col + k]) ? (1u << k) : 0u;
-      if (!hit) continue;
-      int4 S4 = *reinterpret_cast<const int4 *>(g.S + o);
-      uint32_t l4 = *reinterpret_cast<const uint32_t *>(g.lvl + o);
-      const int4 dd = *reinterpret_cast<const int4 *>(dt + rr * LM_DS + cc);
-      const int4 wa4 = *reinterpret_cast<const int4 *>(g.wa + col);  // wa padded to npad
-      if (hit & 1u) { S4.x += wa4.x + dd.x; l4 = (l4 & ~0xFFu) | lvc; }
-      if (hit & 2u) { S4.y += wa4.y + dd.y; l4 = (l4 & ~0xFF00u) | ((uint32_t)lvc << 8); }
-      if (hit & 4u) { S4.z += wa4.z + dd.z; l4 = (l4 & ~0xFF0000u) | ((uint32_t)lvc << 16); }
-      if (hit & 8u) { S4.w += wa4.w + dd.w; l4 = (l4 & ~0xFF000000u) | ((uint32_t)lvc << 24); }
-      *reinterpret_cast<int4 *>(g.S + o) = S4;
-      *reinterpret_cast<uint32_t *>(g.lvl + o) = l4;
-    }
-  }
-  if (warp == 2) {
+  if (warp == 1) {
     asm volatile("tcgen05.fence::after_thread_sync;");
     asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "n"(LM_TMEM_COLS));
   }
@@ -619,8 +687,15 @@ cudaError_t launch_level_mma(const Geom &g, cudaStream_t s) {
   if (err != cudaSuccess) return err;
   err = cudaFuncSetAttribute(k_level_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)LM_SMEM);
   if (err != cudaSuccess) return err;
-  dim3 grid((g.n + LM_BN - 1) / LM_BN, (g.q + LM_BM - 1) / LM_BM);
-  k_level_mma<<<grid, MM_NT, LM_SMEM, s>>>(tq, tq2l, tq2h, tw0, tw1, twc, g);
+  static int sms = 0;
+  if (!sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms < 1) sms = 148;
+  }
+  const long long tiles = (long long)((g.q + LM_BM - 1) / LM_BM) * ((g.n + LM_BN - 1) / LM_BN);
+  const unsigned grid = (unsigned)(tiles < sms ? tiles : sms);
+  if (grid) k_level_mma<<<grid, LM_NT, LM_SMEM, s>>>(tq, tq2l, tq2h, tw0, tw1, twc, g);
   return cudaGetLastError();
 }
 

@@ -60,6 +60,8 @@ struct RoundCtl {
   unsigned int off[NSLOT + 1];            // list offsets per slot
   unsigned int cursor[NSLOT];             // scatter cursors
   unsigned long long chunk_off[NSLOT + 1];// warp-chunk prefix per slot
+  unsigned int wovf_any;                  // shared draws: some point's w_j > 255 this round
+  unsigned int pad1;
   unsigned long long advanced;            // pairs advanced, cumulative
   unsigned long long tile_blocks;         // Philox blocks of the tile gathers, cumulative
   unsigned long long tile_draws;          // (query, point) draws of the tile gathers, cumulative

@@ -424,13 +424,25 @@ __global__ void __launch_bounds__(FIL_NT) k_scatter(Geom g) {
     sdense[t] = dense;
     if (!dense) any_listed = 1;
   }
-  if (!g.tile_on && threadIdx.x == 0) any_listed = 1;
+  if (!g.tile_on && !g.level_mma && threadIdx.x == 0) any_listed = 1;
   __shared__ uint8_t slv[FIL_NT * 4 / 128];  // the chunk's 128 x 128 level tiles: tensor cores?
   const int glev = g.level_mma ? g.ctl->gemm_level : -1;
-  if (threadIdx.x < (FIL_NT * 4) / 128) {
+  if (g.level_mma && threadIdx.x < (FIL_NT * 4) / 128) {
+    // a level tile lists nothing when all its sampled pairs sit at the GEMM level, the
+    // GEMM takes it and no point of the round overflows its w planes
     const int lc = (c0 >> 7) + (int)threadIdx.x;
-    slv[threadIdx.x] = glev >= 0 && lc < g.lv_cols &&
-                       g.lvcnt[((size_t)(qi >> 7) * g.lv_cols + lc) * MAX_LEVELS + glev] >= g.lmin;
+    bool mma = false, other = false;
+    if (lc < g.lv_cols) {
+      const uint32_t *f = g.lvcnt + ((size_t)(qi >> 7) * g.lv_cols + lc) * MAX_LEVELS;
+      for (int s = 0; s < MAX_LEVELS; ++s) {
+        const uint32_t v = f[s];
+        if (s == glev) mma = v >= g.lmin;
+        else other |= v != 0u;
+      }
+      if (glev >= 0 && !mma && f[glev] != 0u) other = true;
+    }
+    slv[threadIdx.x] = mma;
+    if (other || (mma && g.ctl->wovf_any)) any_listed = 1;
   }
   if (threadIdx.x < (FIL_NT * 4) / 256) {
     const int xc = (c0 >> 8) + (int)threadIdx.x;
