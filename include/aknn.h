@@ -222,6 +222,25 @@ aknn_status aknn_query_multi(const aknn_index *const *shards, int32_t nshards,
                              double delta, uint64_t seed, const double *alpha,
                              const aknn_opts *opts, aknn_result *out);
 
+/* The literal Algorithm 1 schedule for q
+ * queries (host uint8 [q][d]) on an unsharded index.  Each iteration
+ * re-evaluates the rank split (C = ranks 1..k, M = k+1..k+h, F = the rest, by
+ * (d_hat, id)), d1 = argmax_C U and d2 = argmin_F L (Eq. 2-3), stops when
+ * Eq. (5) A <= B holds, and otherwise samples one coordinate of d1 and of
+ * b2 = argmax_{{d2} u M} alpha (Eq. 4; ties to d2, then the smaller id); an arm
+ * whose count reaches T = d takes its exact distance, charged d
+ * evaluations.  The t-th sample of an arm is the batched rule's (the same
+ * Philox counter), so only the schedule differs.  Arguments as aknn_query_ex;
+ * opts->max_rounds caps the ITERATIONS (AKNN_EMAXROUNDS, outputs = the state
+ * reached), opts->timing and opts->flags are ignored.  Outputs: sets/dhat of
+ * the final top-(k+h) in rank order, counts = T_i (1..d), sums = S_i,
+ * draws, evals = draws + d * (#arms that went exact), rounds = iterations
+ * (including the last, stopping one).  EINVAL: the aknn_query_ex domain, a
+ * sharded index, or k + h > 512.  Bit-identical to the oracle's A1 mode.     */
+aknn_status aknn_query_a1(const aknn_index *ix, const uint8_t *queries, int32_t q, int32_t k,
+                          int32_t h, double delta, uint64_t seed, const double *alpha,
+                          const aknn_opts *opts, aknn_result *out);
+
 /* Statistics of the last aknn_query* call on `ix`.                          */
 aknn_status aknn_get_stats(const aknn_index *ix, aknn_stats *out);
 

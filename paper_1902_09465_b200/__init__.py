@@ -93,6 +93,8 @@ _sig = {
                        C.POINTER(Result)], _I),
     "aknn_query_async": ([_P, _P, _I, _I, _I, C.c_double, C.c_uint64, _P, C.POINTER(Opts),
                           C.POINTER(Result), _P], _I),
+    "aknn_query_a1": ([_P, _P, _I, _I, _I, C.c_double, C.c_uint64, _P, C.POINTER(Opts),
+                       C.POINTER(Result)], _I),
     "aknn_query_multi": ([C.POINTER(_P), _I, _P, _I, _I, _I, C.c_double, C.c_uint64, _P,
                           C.POINTER(Opts), C.POINTER(Result)], _I),
     "aknn_get_stats": ([_P, C.POINTER(Stats)], _I),
@@ -246,11 +248,15 @@ class Index:
     def query(self, queries, k: int, h: int, delta: float, seed: int = 0, alpha=None, *,
               counts: bool = True, sums: bool = False, dhat: bool = True, max_rounds: int = 0,
               qi_offset: int = 0, timing: bool = False, out: Optional[dict] = None,
-              flags: int = 0) -> dict:
+              flags: int = 0, schedule: str = "br") -> dict:
         """aknn_query_ex on host arrays; returns numpy arrays.
 
+        ``schedule="a1"`` runs the literal Algorithm 1 instead (aknn_query_a1;
+        ``rounds`` then counts iterations and ``max_rounds`` caps them).
         ``out`` may pass preallocated (e.g. pinned) host arrays with the keys of the
         returned dict; a key mapped to None skips that output."""
+        if schedule not in ("br", "a1"):
+            raise AknnError(AKNN_EINVAL, f"schedule must be 'br' or 'a1', not {schedule!r}")
         Q = np.ascontiguousarray(np.atleast_2d(queries), np.uint8)
         q, d = Q.shape
         if d != self.d:
@@ -280,8 +286,9 @@ class Index:
         if al is not None and al.shape != (self.d + 1,):
             raise AknnError(AKNN_EINVAL, f"alpha must have d+1={self.d + 1} entries")
         opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags)
-        st = _lib.aknn_query_ex(self._h, _ptr(Q), q, k, h, delta, seed & (2**64 - 1), _ptr(al),
-                                C.byref(opts), C.byref(res))
+        fn = _lib.aknn_query_a1 if schedule == "a1" else _lib.aknn_query_ex
+        st = fn(self._h, _ptr(Q), q, k, h, delta, seed & (2**64 - 1), _ptr(al), C.byref(opts),
+                C.byref(res))
         out["status"] = st
         if st != AKNN_EMAXROUNDS:
             _check(st)

@@ -1252,9 +1252,62 @@ aknn_status aknn_query_async(const aknn_index *cix, const uint8_t *queries_dev, 
 namespace {
 // Host-pointer query over one index (unsharded, or one NCCL shard) or over several
 // shards of one point set on the current device (multi = true).
+// Literal Algorithm 1 on device buffers: one warp per
+// query (a1_kernels.cu), queries in launches whose workspace fits `budget`.
+aknn_status run_query_a1(aknn_index *ix, const uint8_t *queries_dev, int32_t q, int32_t k, int32_t h,
+                         uint64_t seed, const double *alpha_dev, const aknn_opts *opts,
+                         const aknn_result *out, cudaStream_t st) {
+  const int kh = k + h;
+  if (kh > A1_MAX_KH) return fail(AKNN_EINVAL, "Algorithm 1 mode supports k+h <= %d (got %d)", A1_MAX_KH, kh);
+  const size_t per = a1_ws_per_query(ix->n_local, kh);
+  size_t budget = (size_t)1 << 30;
+  int qb = (int)std::max<size_t>(1, std::min<size_t>((size_t)q, budget / per));
+  TRY(ix->ws.ensure(256 + per * (size_t)qb));
+  A1Geom g{};
+  g.X = ix->X.as<uint8_t>();
+  g.pitch = ix->pitch;
+  g.Q = queries_dev;
+  g.alpha = alpha_dev;
+  g.n = (int)ix->n_local;
+  g.d = ix->d;
+  g.k = k;
+  g.kh = kh;
+  g.id_offset = (uint32_t)ix->offset;
+  g.qi0 = opts ? (uint32_t)opts->qi_offset : 0u;
+  g.max_iters = opts ? opts->max_rounds : 0;
+  const uint32_t lo = (uint32_t)(seed & 0xffffffffu), hi = (uint32_t)(seed >> 32);
+  for (int r = 0; r < 10; ++r) {
+    g.rk0[r] = lo + (uint32_t)r * 0x9E3779B9u;
+    g.rk1[r] = hi + (uint32_t)r * 0xBB67AE85u;
+  }
+  g.status = ix->ws.as<int>();
+  g.ws = ix->ws.as<unsigned char>(256);
+  g.ws_per_query = per;
+  g.out = OutPtrs{0, 0, ix->n_local, 0, out->sets, out->dhat, out->counts, out->sums,
+                  out->evals, out->draws, out->rounds};
+  CU(cudaMemsetAsync(g.status, 0, sizeof(int), st));
+  int64_t launches = 1;
+  for (int q0 = 0; q0 < q; q0 += qb) {
+    g.q0 = q0;
+    g.qb = std::min(qb, q - q0);
+    CU(launch_a1(g, st));
+    ++launches;
+  }
+  int *hs = nullptr;
+  CU(ix->host.ensure(sizeof(int)));
+  hs = static_cast<int *>(ix->host.p);
+  CU(cudaMemcpyAsync(hs, g.status, sizeof(int), cudaMemcpyDeviceToHost, st));
+  CU(sync_spin(st));
+  ix->stats = aknn_stats{};
+  ix->stats.query_batches = (int32_t)((q + qb - 1) / qb);
+  ix->stats.kernel_launches = launches;
+  ix->stats.pairs = (int64_t)q * ix->n_local;
+  return (*hs & 1) ? AKNN_EMAXROUNDS : AKNN_OK;
+}
+
 aknn_status host_query(const std::vector<aknn_index *> &shards, bool multi, const uint8_t *queries,
                        int32_t q, int32_t k, int32_t h, double delta, uint64_t seed,
-                       const double *alpha, const aknn_opts *opts, aknn_result *out) {
+                       const double *alpha, const aknn_opts *opts, aknn_result *out, bool a1 = false) {
   aknn_index *ix = shards[0];
   if (q == 0) return AKNN_OK;
   cudaStream_t st = ix->stream;
@@ -1290,7 +1343,9 @@ aknn_status host_query(const std::vector<aknn_index *> &shards, bool multi, cons
                    out->sums ? ix->outs.as<int64_t>(oSum) : nullptr, ix->outs.as<int64_t>(oEv),
                    ix->outs.as<int64_t>(oDr), ix->outs.as<int32_t>(oRo)};
   aknn_status s;
-  if (multi || ix->world > 1)
+  if (a1)
+    s = run_query_a1(ix, ix->outs.as<uint8_t>(oQ), q, k, h, seed, ix->outs.as<double>(oA), opts, &dout, st);
+  else if (multi || ix->world > 1)
     s = run_query_sharded(shards, !multi, ix->outs.as<uint8_t>(oQ), q, k, h, seed,
                           ix->outs.as<double>(oA), opts, &dout, n, st);
   else
@@ -1347,6 +1402,19 @@ aknn_status aknn_query_multi(const aknn_index *const *shards, int32_t nshards, c
                 (long long)v[0]->n_global);
   if (q > 0 && !queries) return fail(AKNN_EINVAL, "queries is NULL");
   return host_query(v, true, queries, q, k, h, delta, seed, alpha, opts, out);
+}
+
+aknn_status aknn_query_a1(const aknn_index *cix, const uint8_t *queries, int32_t q, int32_t k,
+                          int32_t h, double delta, uint64_t seed, const double *alpha,
+                          const aknn_opts *opts, aknn_result *out) {
+  aknn_index *ix = const_cast<aknn_index *>(cix);
+  TRY(check_query_args(ix, q, k, h, delta, out));
+  if (ix->world != 1 || ix->n_local != ix->n_global)
+    return fail(AKNN_EINVAL, "Algorithm 1 mode needs an unsharded index");
+  if (q > 0 && !queries) return fail(AKNN_EINVAL, "queries is NULL");
+  if (ix->pending.on) TRY(finish_pending(ix));
+  std::vector<aknn_index *> one{ix};
+  return host_query(one, false, queries, q, k, h, delta, seed, alpha, opts, out, true);
 }
 
 aknn_status aknn_query(const aknn_index *ix, const uint8_t *queries, int32_t q, int32_t k, int32_t h,

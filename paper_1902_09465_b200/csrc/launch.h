@@ -22,6 +22,26 @@ struct OutPtrs {
   int32_t *rounds;
 };
 
+// Literal Algorithm 1 (a1_kernels.cu): one warp per query, state in `ws`.
+constexpr int A1_MAX_KH = 512;
+struct A1Geom {
+  const uint8_t *X;      // [n][pitch]
+  int64_t pitch;
+  const uint8_t *Q;      // [q][d] queries of the call (unpadded)
+  const double *alpha;   // [d+1]
+  int n, d, k, kh;
+  int q0, qb;            // this launch: queries q0 .. q0 + qb - 1
+  uint32_t id_offset, qi0;
+  int max_iters;         // 0 = unlimited
+  uint32_t rk0[10], rk1[10];
+  unsigned char *ws;     // qb slices of ws_per_query bytes
+  size_t ws_per_query;
+  int *status;           // bit 0: some query reached max_iters
+  OutPtrs out;
+};
+cudaError_t launch_a1(const A1Geom &g, cudaStream_t s);
+size_t a1_ws_per_query(int64_t n, int kh);
+
 cudaError_t launch_init(const Geom &g, cudaStream_t s);
 cudaError_t launch_select(const Geom &g, int nbits, cudaStream_t s);
 cudaError_t launch_filter(const Geom &g, cudaStream_t s);
