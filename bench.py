@@ -49,7 +49,11 @@ def _args():
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
-    ap.add_argument("--config", type=int, default=2, help="BASELINE.json config (1-based)")
+    ap.add_argument("--config", type=int, default=None,
+                    help="BASELINE.json config (1-based; default 2, or 1 with --schedule a1)")
+    ap.add_argument("--schedule", choices=("br", "a1"), default="br",
+                    help="batched round rule (default) or the literal Algorithm 1 "
+                         "(SURVEY §8(f) row 2, aknn_query_a1)")
     ap.add_argument("--alpha", default="theory",
                     help="'theory' (footnote 2, P:132-138) or 'exp:<C_alpha>' (§5, P:349)")
     ap.add_argument("--q", type=int, default=0, help="override queries per rank (0 = config)")
@@ -61,7 +65,10 @@ def _args():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-exact", action="store_true")
     ap.add_argument("--clock-sampler", choices=("nvml", "smi", "none"), default="nvml")
-    return ap.parse_args()
+    a = ap.parse_args()
+    if a.config is None:
+        a.config = 1 if a.schedule == "a1" else 2
+    return a
 
 
 def _alpha_desc(a: str) -> str:
@@ -675,12 +682,181 @@ def run_ours(args, dist: Dist):
         print(json.dumps(line), flush=True)
 
 
+# ----------------------------------------------------------------------------- Algorithm 1
+def _a1_inputs(args):
+    cfg = synth.config(args.config)
+    if args.config == 1:
+        X, Q, _ = synth.planted(cfg)
+    else:
+        if args.q:
+            cfg = synth.config(args.config, q=args.q)
+        X, Q = synth.points(cfg), synth.queries(cfg)
+    return cfg, X, Q
+
+
+def _a1_orc_worker(i):
+    import oracle.oracle as orc
+    X, Q, cfg, al = _ORC["X"], _ORC["Q"], _ORC["cfg"], _ORC["alpha"]
+    return int(orc.query_a1(X, Q[i], cfg.k, cfg.h, cfg.seed, al, qi=i)["evals"])
+
+
+def _a1_oracle_time(X, Q, cfg, alpha, nq: int, cores: int):
+    import multiprocessing as mp
+    import oracle.oracle as orc
+    orc.lib()
+    _ORC.update(X=X, Q=Q, cfg=cfg, alpha=alpha)
+    t0 = time.perf_counter()
+    with mp.get_context("fork").Pool(min(cores, nq)) as pool:
+        pool.map(_a1_orc_worker, range(nq), chunksize=1)
+    return time.perf_counter() - t0
+
+
+def _a1_desc(cfg, args):
+    return {"workload": cfg.name + "_algorithm1", "schedule": "literal Algorithm 1 (P:159-191): "
+            "{d1, b2} sampled once per iteration", "n": cfg.n, "d": cfg.d, "q_per_rank": cfg.q,
+            "k": cfg.k, "h": cfg.h, "delta": cfg.delta, "seed": cfg.seed,
+            "alpha": _alpha_desc(args.alpha), "parallelism": "1 GPU, one warp per query",
+            "l2": "inputs smaller than L2; the iteration chain is latency-bound (no flush)"}
+
+
+def run_reference_a1(args, dist: Dist):
+    if dist.rank != 0:
+        return
+    cfg, X, Q = _a1_inputs(args)
+    al = _oracle_alpha(cfg, args.alpha)
+    cores = max(1, min(_cpu_cores(), 16))
+    nq = min(cores, cfg.q)
+    times = []
+    for it in range(min(args.warmup, 1) + args.steps):  # each step ~ seconds: one warm-up
+        dt = _a1_oracle_time(X, Q, cfg, al, nq, cores)
+        if it >= min(args.warmup, 1):
+            times.append(dt)
+    ms = 1e3 * sum(times) / len(times)
+    value = nq / (ms / 1e3)
+    print(json.dumps({
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "u8", "data": "synthetic",
+        "config": _a1_desc(cfg, args),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": min(cores, nq), "kind": "oracle",
+                         "sample": f"{nq} queries of {cfg.name} per step, oracle A1 mode "
+                                   f"(one full sort per iteration), one process per query"},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+        flush=True)
+
+
+def run_a1(args, dist: Dist):
+    """--schedule a1: the literal Algorithm 1 (aknn_query_a1_device) on the config's
+    queries; one step = one call over all of them, inputs resident in HBM."""
+    import torch
+    import paper_1902_09465_b200 as ak
+
+    torch.cuda.set_device(dist.local)
+    dev = torch.device("cuda", dist.local)
+    cfg, X, Qh = _a1_inputs(args)
+    n, d, k, h, q = cfg.n, cfg.d, cfg.k, cfg.h, Qh.shape[0]
+    alpha = ak.alpha_table(n, cfg.delta, d, "theory") if args.alpha == "theory" else \
+        ak.alpha_table(n, cfg.delta, d, "experimental", float(args.alpha.split(":", 1)[1]))
+    ix = ak.Index(torch.from_numpy(X).to(dev))
+    Qd = torch.from_numpy(Qh).to(dev)
+    alpha_d = torch.from_numpy(alpha).to(dev)
+    stream = torch.cuda.Stream(device=dev)
+    kh = k + h
+    out = dict(sets=torch.empty((q, kh), dtype=torch.int32, device=dev),
+               dhat=torch.empty((q, kh), dtype=torch.float64, device=dev), counts=None, sums=None,
+               evals=torch.empty(q, dtype=torch.int64, device=dev),
+               draws=torch.empty(q, dtype=torch.int64, device=dev),
+               rounds=torch.empty(q, dtype=torch.int32, device=dev))
+
+    def step():
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        ix.query_device(Qd, k, h, cfg.delta, cfg.seed, alpha_d, stream=stream, out=out, schedule="a1")
+        e1.record(stream)
+        torch.cuda.synchronize()
+        return e0.elapsed_time(e1), ix.stats()
+
+    for _ in range(args.warmup):
+        step()
+    clocks = ClockSampler(dist.local, args.clock_sampler)
+    dist.barrier()
+    torch.cuda.synchronize()
+    clocks.start()
+    times, stats = [], []
+    for _ in range(args.steps):
+        ms, st = step()
+        times.append(ms)
+        stats.append(st)
+    dist.barrier()
+    torch.cuda.synchronize()
+    clk = clocks.stop()
+    ms_max = dist.max(sum(times))
+    value = dist.sum(q * args.steps) / (ms_max / 1e3)
+    draws = int(out["draws"].sum().item())
+    evals = int(out["evals"].sum().item())
+    iters = out["rounds"].cpu().numpy()
+    probes = _measure_probes(d, n * d)
+    s_step = ms_max / args.steps / 1e3
+    pk = probes.get("philox_blocks_per_s")
+    roofline = {
+        "bound": "alu", "achieved": draws / s_step / 1e9, "peak": pk / 1e9 if pk else None,
+        "unit": "G Philox blocks/s (one block per Algorithm-1 draw)",
+        "frac": (draws / s_step) / pk if pk else None,
+        "peak_source": "measured in this run: tools/probes.cu k_probe_philox",
+        "kernel": "k_a1", "launches": args.steps, "avg_launch_ms": ms_max / args.steps,
+        "share_of_step": 1.0,
+        "note": "latency-bound by design: every query is one dependent chain of iterations "
+                "(rank split, Eq. 2-5, two draws); the GPU runs one warp per query",
+        "us_per_iteration": s_step * 1e6 / float(iters.max()), "traffic": None}
+    # the batched rule on the same queries (untimed): sample efficiency of the schedules
+    bout = ix.query(Qh, k, h, cfg.delta, cfg.seed, alpha, counts=False)
+    e2e = None
+    if not args.no_e2e:
+        wall = []
+        for _ in range(args.steps):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            r = ix.query(Qh, k, h, cfg.delta, cfg.seed, alpha, counts=False, schedule="a1")
+            wall.append(time.perf_counter() - t0)
+        e2e = {"value": q * args.steps / dist.max(sum(wall)), "unit": UNIT,
+               "h2d_bytes_per_step": int(Qh.nbytes + alpha.nbytes),
+               "d2h_bytes_per_step": int(sum(v.nbytes for key, v in r.items()
+                                             if key != "status" and v is not None)),
+               "api": "aknn_query_a1 (host pointers), wall clock incl. copies"}
+    cpu = None
+    if not args.no_cpu_baseline and dist.rank == 0 and dist.world == 1:
+        cores = max(1, min(_cpu_cores(), 16))
+        nq = min(q, cores)
+        dt = _a1_oracle_time(X, Qh, cfg, _oracle_alpha(cfg, args.alpha), nq, cores)
+        cpu = {"value": nq / dt, "unit": UNIT, "cores": min(cores, nq), "kind": "oracle",
+               "sample": f"first {nq} queries of {cfg.name}, oracle A1 mode, {dt:.1f} s wall"}
+    ix.close()
+    if dist.rank == 0:
+        print(json.dumps({
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": dist.world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_max / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
+            "data": "synthetic (seeded; synth/ recipes, DESIGN.md §5)", "config": _a1_desc(cfg, args),
+            "roofline": roofline, "cpu_baseline": cpu, "e2e": e2e, "clocks": clk,
+            "gpu_launches": int(sum(s["kernel_launches"] for s in stats)),
+            "step_ms": [round(t, 3) for t in times],
+            "iterations": iters.tolist() if q <= 16 else {"mean": float(iters.mean()), "max": int(iters.max())},
+            "draws_per_s": draws / s_step, "evals_per_s": evals / s_step,
+            "sample_fraction": evals / (q * n * d),
+            "batched_rule_same_queries": {"sample_fraction": int(bout["evals"].sum()) / (q * n * d),
+                                          "rounds_max": int(bout["rounds"].max())},
+        }), flush=True)
+
+
 def main():
     args = _args()
     dist = Dist()
     try:
         if args.impl == "reference":
-            run_reference(args, dist)
+            (run_reference_a1 if args.schedule == "a1" else run_reference)(args, dist)
+        elif args.schedule == "a1":
+            run_a1(args, dist)
         else:
             run_ours(args, dist)
     finally:

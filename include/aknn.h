@@ -241,6 +241,15 @@ aknn_status aknn_query_a1(const aknn_index *ix, const uint8_t *queries, int32_t 
                           int32_t h, double delta, uint64_t seed, const double *alpha,
                           const aknn_opts *opts, aknn_result *out);
 
+/* aknn_query_a1 on device buffers (queries_dev uint8 [q][d], alpha_dev fp64
+ * [d+1] or NULL = footnote-2 table, `out` device pointers), enqueued on
+ * `cuda_stream`; returns after the stream has finished the call (the status
+ * reports the iteration cap).                                                 */
+aknn_status aknn_query_a1_device(const aknn_index *ix, const uint8_t *queries_dev, int32_t q,
+                                 int32_t k, int32_t h, double delta, uint64_t seed,
+                                 const double *alpha_dev, const aknn_opts *opts,
+                                 aknn_result *out, void *cuda_stream);
+
 /* Statistics of the last aknn_query* call on `ix`.                          */
 aknn_status aknn_get_stats(const aknn_index *ix, aknn_stats *out);
 

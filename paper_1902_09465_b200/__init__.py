@@ -95,6 +95,8 @@ _sig = {
                           C.POINTER(Result), _P], _I),
     "aknn_query_a1": ([_P, _P, _I, _I, _I, C.c_double, C.c_uint64, _P, C.POINTER(Opts),
                        C.POINTER(Result)], _I),
+    "aknn_query_a1_device": ([_P, _P, _I, _I, _I, C.c_double, C.c_uint64, _P, C.POINTER(Opts),
+                              C.POINTER(Result), _P], _I),
     "aknn_query_multi": ([C.POINTER(_P), _I, _P, _I, _I, _I, C.c_double, C.c_uint64, _P,
                           C.POINTER(Opts), C.POINTER(Result)], _I),
     "aknn_get_stats": ([_P, C.POINTER(Stats)], _I),
@@ -297,8 +299,14 @@ class Index:
     def query_device(self, queries, k: int, h: int, delta: float, seed: int = 0, alpha=None, *,
                      counts: bool = False, sums: bool = False, dhat: bool = True,
                      max_rounds: int = 0, qi_offset: int = 0, timing: bool = False,
-                     stream=None, out: Optional[dict] = None, flags: int = 0) -> dict:
-        """aknn_query_async on torch CUDA tensors (current stream); returns device tensors."""
+                     stream=None, out: Optional[dict] = None, flags: int = 0,
+                     schedule: str = "br") -> dict:
+        """aknn_query_async on torch CUDA tensors (current stream); returns device tensors.
+
+        ``schedule="a1"``: the literal Algorithm 1 (aknn_query_a1_device; waits for the
+        stream before returning)."""
+        if schedule not in ("br", "a1"):
+            raise AknnError(AKNN_EINVAL, f"schedule must be 'br' or 'a1', not {schedule!r}")
         torch = _torch()
         assert queries.is_cuda and queries.dtype == torch.uint8
         Q = queries.contiguous()
@@ -319,8 +327,9 @@ class Index:
             al = alpha if (hasattr(alpha, "is_cuda") and alpha.is_cuda) else \
                 torch.as_tensor(np.ascontiguousarray(alpha, np.float64)).to(dev)
         opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags)
-        st = _lib.aknn_query_async(self._h, _ptr(Q), q, k, h, delta, seed & (2**64 - 1), _ptr(al),
-                                   C.byref(opts), C.byref(res), _stream_ptr(stream))
+        fn = _lib.aknn_query_a1_device if schedule == "a1" else _lib.aknn_query_async
+        st = fn(self._h, _ptr(Q), q, k, h, delta, seed & (2**64 - 1), _ptr(al), C.byref(opts),
+                C.byref(res), _stream_ptr(stream))
         out["status"] = st
         if st != AKNN_EMAXROUNDS:
             _check(st)

@@ -36,10 +36,10 @@ struct A1Arm {  // per-query state, one workspace slice per query
   double *dh, *L;
   int32_t *S, *T, *cm;
   uint8_t *incm;
+  const double *alpha;  // [d+1]: a shared-memory copy in shared-memory mode
 };
 
-__device__ __forceinline__ A1Arm a1_state(const A1Geom &g, int slot) {
-  unsigned char *b = g.ws + (size_t)slot * g.ws_per_query;
+__device__ __forceinline__ A1Arm a1_state(const A1Geom &g, unsigned char *b) {
   const size_t n = (size_t)g.n;
   A1Arm a;
   a.dh = reinterpret_cast<double *>(b);
@@ -48,6 +48,7 @@ __device__ __forceinline__ A1Arm a1_state(const A1Geom &g, int slot) {
   a.T = a.S + n;
   a.cm = a.T + n;
   a.incm = reinterpret_cast<uint8_t *>(a.cm + g.kh);
+  a.alpha = g.alpha;
   return a;
 }
 
@@ -55,7 +56,7 @@ __device__ __forceinline__ bool key_less(double da, int ia, double db, int ib) {
   return da < db || (da == db && ia < ib);
 }
 
-__device__ __forceinline__ double a1_alpha(const A1Geom &g, int T) { return T >= g.d ? 0.0 : g.alpha[T]; }
+__device__ __forceinline__ double a1_alpha(const A1Geom &g, const A1Arm &a, int T) { return T >= g.d ? 0.0 : a.alpha[T]; }
 
 __device__ __forceinline__ double a1_dhat(int32_t S, int32_t T) {
   return (double)S / ((double)T * 65025.0);  // reading R15: one pinned expression
@@ -113,18 +114,24 @@ __device__ __forceinline__ KeyArg warp_max(KeyArg a) {  // ties: smaller id
   return a;
 }
 
-// One pass over F (the arms outside cm): its minimum key (d_hat, id) and its
-// argmin of L (ties: smaller id).
-__device__ __forceinline__ void scan_far(const A1Geom &g, const A1Arm &a, int lane, KeyArg *kmin, KeyArg *lmin) {
+// The lane's share of F (arms i = lane mod 32 outside cm): its minimum key
+// (d_hat, id) and its argmin of L (ties: smaller id).  Kept in registers and
+// rescanned only when an arm of the lane left F or changed inside it.
+__device__ __forceinline__ void lane_scan(const A1Geom &g, const A1Arm &a, int lane, KeyArg *pk, KeyArg *pl) {
   KeyArg km{0.0, -1}, lm{0.0, -1};
+#pragma unroll 4
   for (int i = lane; i < g.n; i += 32) {
     if (a.incm[i]) continue;
     const double dh = a.dh[i], L = a.L[i];
     if (km.i < 0 || key_less(dh, i, km.v, km.i)) km = KeyArg{dh, i};
     if (lm.i < 0 || key_less(L, i, lm.v, lm.i)) lm = KeyArg{L, i};
   }
-  *kmin = warp_min(km);
-  *lmin = warp_min(lm);
+  *pk = km;
+  *pl = lm;
+}
+
+__device__ __forceinline__ void fold_min(KeyArg *m, double v, int i) {
+  if (m->i < 0 || key_less(v, i, m->v, m->i)) *m = KeyArg{v, i};
 }
 
 // cm without the entry at position p, then `arm` inserted at its rank: every lane
@@ -173,12 +180,24 @@ __device__ __forceinline__ int cm_find(const A1Geom &g, const A1Arm &a, int arm,
 }
 
 __global__ void __launch_bounds__(32 * A1_WARPS) k_a1(A1Geom g) {
+  extern __shared__ __align__(16) unsigned char a1sm[];
   const int lane = threadIdx.x & 31;
-  const int slot = blockIdx.x * A1_WARPS + (threadIdx.x >> 5);
+  const int wpc = g.smem ? 1 : A1_WARPS;  // warps per CTA
+  const int slot = blockIdx.x * wpc + (threadIdx.x >> 5);
   const int qi = g.q0 + slot;
-  if (slot >= g.qb) return;  // warp-uniform
-  const A1Arm a = a1_state(g, slot);
+  if (slot >= g.qb || (threadIdx.x >> 5) >= wpc) return;  // warp-uniform
+  A1Arm a = a1_state(g, g.smem ? a1sm : g.ws + (size_t)slot * g.ws_per_query);
   const uint8_t *x = g.Q + (size_t)qi * g.d;
+  if (g.smem) {  // alpha and the query row next to the state (latency of every iteration)
+    const size_t off = ((size_t)g.n * 24 + (size_t)g.kh * 4 + (size_t)g.n + 7) & ~(size_t)7;
+    double *al = reinterpret_cast<double *>(a1sm + off);
+    uint8_t *xs = reinterpret_cast<uint8_t *>(al + g.d + 1);
+    for (int t = lane; t <= g.d; t += 32) al[t] = g.alpha[t];
+    for (int j = lane; j < g.d; j += 32) xs[j] = x[j];
+    __syncwarp();
+    a.alpha = al;
+    x = xs;
+  }
   const uint32_t qrng = (uint32_t)qi + g.qi0;
   const int n = g.n, k = g.k, kh = g.kh, d = g.d;
 
@@ -190,20 +209,22 @@ __global__ void __launch_bounds__(32 * A1_WARPS) k_a1(A1Geom g) {
     a.T[i] = T;
     const double dh = a1_dhat(S, T);
     a.dh[i] = dh;
-    a.L[i] = dh - a1_alpha(g, T);
+    a.L[i] = dh - a1_alpha(g, a, T);
     a.incm[i] = 0;
   }
   __syncwarp();
   long long draws = n, nexact = 0;
+  KeyArg pk, pl;  // the lane's share of F
+  lane_scan(g, a, lane, &pk, &pl);
   // the initial top-(k + h), in rank order
   for (int r = 0; r < kh; ++r) {
-    KeyArg km, lm;
-    scan_far(g, a, lane, &km, &lm);
+    const KeyArg km = warp_min(pk);
     if (lane == 0) {
       a.cm[r] = km.i;
       a.incm[km.i] = 1;
     }
     __syncwarp();
+    if ((km.i & 31) == lane) lane_scan(g, a, lane, &pk, &pl);
   }
   int it = 0, status = 0;
   for (;;) {
@@ -211,21 +232,28 @@ __global__ void __launch_bounds__(32 * A1_WARPS) k_a1(A1Geom g) {
     // R2: the top-(k + h) band against F
     KeyArg km, d2;
     for (;;) {
-      scan_far(g, a, lane, &km, &d2);
+      km = warp_min(pk);
+      d2 = warp_min(pl);
       const int last = a.cm[kh - 1];
-      if (!key_less(km.v, km.i, a.dh[last], last)) break;
+      const double dl = a.dh[last];
+      if (!key_less(km.v, km.i, dl, last)) break;
       if (lane == 0) {
         a.incm[last] = 0;
         a.incm[km.i] = 1;
       }
       __syncwarp();
       cm_reinsert(g, a, kh - 1, km.i, lane);
+      if ((km.i & 31) == lane) lane_scan(g, a, lane, &pk, &pl);  // its minimum left F
+      if ((last & 31) == lane) {  // `last` joins F
+        fold_min(&pk, dl, last);
+        fold_min(&pl, a.L[last], last);
+      }
     }
     // R3: d1 over C
     KeyArg d1{0.0, -1};
     for (int r = lane; r < k; r += 32) {
       const int i = a.cm[r];
-      const double U = a.dh[i] + a1_alpha(g, a.T[i]);
+      const double U = a.dh[i] + a1_alpha(g, a, a.T[i]);
       if (d1.i < 0 || U > d1.v || (U == d1.v && i < d1.i)) d1 = KeyArg{U, i};
     }
     d1 = warp_max(d1);
@@ -239,36 +267,44 @@ __global__ void __launch_bounds__(32 * A1_WARPS) k_a1(A1Geom g) {
     KeyArg bm{0.0, -1};
     for (int r = k + lane; r < kh; r += 32) {
       const int i = a.cm[r];
-      const double al = a1_alpha(g, a.T[i]);
+      const double al = a1_alpha(g, a, a.T[i]);
       if (bm.i < 0 || al > bm.v || (al == bm.v && i < bm.i)) bm = KeyArg{al, i};
     }
     bm = warp_max(bm);
-    const int b2 = (bm.i >= 0 && bm.v > a1_alpha(g, a.T[d2.i])) ? bm.i : d2.i;
-    // a3: one sample of d1 and one of b2 (distinct: d1 in C, b2 not)
-    const int sel[2] = {d1.i, b2};
+    const int b2 = (bm.i >= 0 && bm.v > a1_alpha(g, a, a.T[d2.i])) ? bm.i : d2.i;
+    // a3: one sample of d1 and one of b2 (distinct arms: d1 in C, b2
+    // not), drawn side by side by lanes 0 and 1
+    const int32_t T1 = a.T[d1.i], T2 = a.T[b2];
+    int32_t v = 0;
+    if (lane < 2) {
+      const int l = lane == 0 ? d1.i : b2;
+      const int32_t T = lane == 0 ? T1 : T2;
+      if (T + 1 < d) v = a1_draw(g, x, l, T, qrng);
+    }
+    int32_t S1 = a.S[d1.i] + __shfl_sync(FULL, v, 0), S2 = a.S[b2] + __shfl_sync(FULL, v, 1);
+    if (T1 + 1 == d) S1 = a1_exact(g, x, d1.i, lane);  // "If T_l = m ... exactly"
+    if (T2 + 1 == d) S2 = a1_exact(g, x, b2, lane);
+    draws += (T1 < d) + (T2 < d);
+    nexact += (T1 + 1 == d) + (T2 + 1 == d);
+    // apply one arm at a time: cm_reinsert ranks an arm against a band whose other
+    // entries are in order
 #pragma unroll
-    for (int s = 0; s < 2; ++s) {
-      const int l = sel[s];
-      const int32_t T = a.T[l];
+    for (int s2 = 0; s2 < 2; ++s2) {
+      const int l = s2 == 0 ? d1.i : b2;
+      const int32_t T = s2 == 0 ? T1 : T2;
       if (T >= d) continue;  // uniform
-      int32_t S = a.S[l];
-      if (T + 1 == d) {
-        S = a1_exact(g, x, l, lane);  // "If T_l = m ... exactly"
-        ++nexact;
-      } else {
-        S += __shfl_sync(FULL, lane == 0 ? a1_draw(g, x, l, T, qrng) : 0, 0);
-      }
-      ++draws;
       __syncwarp();
       if (lane == 0) {
+        const int32_t S = s2 == 0 ? S1 : S2;
         a.S[l] = S;
         a.T[l] = T + 1;
         const double dh = a1_dhat(S, T + 1);
         a.dh[l] = dh;
-        a.L[l] = dh - a1_alpha(g, T + 1);
+        a.L[l] = dh - a1_alpha(g, a, T + 1);
       }
       __syncwarp();
       if (a.incm[l]) cm_reinsert(g, a, cm_find(g, a, l, lane), l, lane);
+      else if ((l & 31) == lane) lane_scan(g, a, lane, &pk, &pl);  // an F arm moved
     }
   }
   // outputs: the band in rank order, its estimates, the per-arm state
@@ -293,14 +329,23 @@ __global__ void __launch_bounds__(32 * A1_WARPS) k_a1(A1Geom g) {
 
 }  // namespace
 
+// State in shared memory (one warp per CTA) when a query's slice fits
+// A1_SMEM_MAX, else in the global workspace (A1_WARPS warps per CTA).
 cudaError_t launch_a1(const A1Geom &g, cudaStream_t s) {
   if (g.qb <= 0) return cudaSuccess;
-  k_a1<<<(unsigned)((g.qb + A1_WARPS - 1) / A1_WARPS), 32 * A1_WARPS, 0, s>>>(g);
+  if (g.smem) {
+    cudaError_t e = cudaFuncSetAttribute(k_a1, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)g.ws_per_query);
+    if (e != cudaSuccess) return e;
+    k_a1<<<(unsigned)g.qb, 32, g.ws_per_query, s>>>(g);
+  } else {
+    k_a1<<<(unsigned)((g.qb + A1_WARPS - 1) / A1_WARPS), 32 * A1_WARPS, 0, s>>>(g);
+  }
   return cudaGetLastError();
 }
 
-size_t a1_ws_per_query(int64_t n, int kh) {
-  const size_t b = (size_t)n * (8 + 8 + 4 + 4) + (size_t)kh * 4 + (size_t)n;
+size_t a1_ws_per_query(int64_t n, int kh, int d, bool tables) {
+  size_t b = ((size_t)n * (8 + 8 + 4 + 4) + (size_t)kh * 4 + (size_t)n + 7) & ~(size_t)7;
+  if (tables) b += (size_t)(d + 1) * 8 + (size_t)d;
   return (b + 255) / 256 * 256;
 }
 

@@ -1259,10 +1259,11 @@ aknn_status run_query_a1(aknn_index *ix, const uint8_t *queries_dev, int32_t q, 
                          const aknn_result *out, cudaStream_t st) {
   const int kh = k + h;
   if (kh > A1_MAX_KH) return fail(AKNN_EINVAL, "Algorithm 1 mode supports k+h <= %d (got %d)", A1_MAX_KH, kh);
-  const size_t per = a1_ws_per_query(ix->n_local, kh);
-  size_t budget = (size_t)1 << 30;
-  int qb = (int)std::max<size_t>(1, std::min<size_t>((size_t)q, budget / per));
-  TRY(ix->ws.ensure(256 + per * (size_t)qb));
+  const size_t per_s = a1_ws_per_query(ix->n_local, kh, ix->d, true);
+  const size_t per = per_s <= A1_SMEM_MAX ? per_s : a1_ws_per_query(ix->n_local, kh, ix->d, false);
+  const size_t budget = (size_t)1 << 30;
+  const int qb = per <= A1_SMEM_MAX ? q : (int)std::max<size_t>(1, std::min<size_t>((size_t)q, budget / per));
+  TRY(ix->ws.ensure(256 + (per <= A1_SMEM_MAX ? 0 : per * (size_t)qb)));
   A1Geom g{};
   g.X = ix->X.as<uint8_t>();
   g.pitch = ix->pitch;
@@ -1283,10 +1284,11 @@ aknn_status run_query_a1(aknn_index *ix, const uint8_t *queries_dev, int32_t q, 
   g.status = ix->ws.as<int>();
   g.ws = ix->ws.as<unsigned char>(256);
   g.ws_per_query = per;
+  g.smem = per <= A1_SMEM_MAX ? 1 : 0;
   g.out = OutPtrs{0, 0, ix->n_local, 0, out->sets, out->dhat, out->counts, out->sums,
                   out->evals, out->draws, out->rounds};
   CU(cudaMemsetAsync(g.status, 0, sizeof(int), st));
-  int64_t launches = 1;
+  int64_t launches = 0;
   for (int q0 = 0; q0 < q; q0 += qb) {
     g.q0 = q0;
     g.qb = std::min(qb, q - q0);
@@ -1415,6 +1417,28 @@ aknn_status aknn_query_a1(const aknn_index *cix, const uint8_t *queries, int32_t
   if (ix->pending.on) TRY(finish_pending(ix));
   std::vector<aknn_index *> one{ix};
   return host_query(one, false, queries, q, k, h, delta, seed, alpha, opts, out, true);
+}
+
+aknn_status aknn_query_a1_device(const aknn_index *cix, const uint8_t *queries_dev, int32_t q, int32_t k,
+                                 int32_t h, double delta, uint64_t seed, const double *alpha_dev,
+                                 const aknn_opts *opts, aknn_result *out, void *cuda_stream) {
+  aknn_index *ix = const_cast<aknn_index *>(cix);
+  TRY(check_query_args(ix, q, k, h, delta, out));
+  if (ix->world != 1 || ix->n_local != ix->n_global)
+    return fail(AKNN_EINVAL, "Algorithm 1 mode needs an unsharded index");
+  if (q > 0 && !queries_dev) return fail(AKNN_EINVAL, "queries is NULL");
+  if (ix->pending.on) TRY(finish_pending(ix));
+  cudaStream_t st = (cudaStream_t)cuda_stream;
+  const double *al = alpha_dev;
+  if (!al) {
+    std::vector<double> a(ix->d + 1);
+    TRY(host_alpha_table(0, ix->n_global, delta, 0.0, ix->d, a.data()));
+    TRY(ix->alpha.ensure(sizeof(double) * (ix->d + 1)));
+    CU(cudaMemcpyAsync(ix->alpha.p, a.data(), sizeof(double) * (ix->d + 1), cudaMemcpyHostToDevice, st));
+    al = ix->alpha.as<double>();
+  }
+  if (q == 0) return AKNN_OK;
+  return run_query_a1(ix, queries_dev, q, k, h, seed, al, opts, out, st);
 }
 
 aknn_status aknn_query(const aknn_index *ix, const uint8_t *queries, int32_t q, int32_t k, int32_t h,

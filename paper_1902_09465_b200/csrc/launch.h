@@ -37,10 +37,12 @@ struct A1Geom {
   unsigned char *ws;     // qb slices of ws_per_query bytes
   size_t ws_per_query;
   int *status;           // bit 0: some query reached max_iters
+  int smem;              // 1: state in shared memory (ws_per_query <= A1_SMEM_MAX)
   OutPtrs out;
 };
+constexpr size_t A1_SMEM_MAX = 96 * 1024;
 cudaError_t launch_a1(const A1Geom &g, cudaStream_t s);
-size_t a1_ws_per_query(int64_t n, int kh);
+size_t a1_ws_per_query(int64_t n, int kh, int d, bool tables);
 
 cudaError_t launch_init(const Geom &g, cudaStream_t s);
 cudaError_t launch_select(const Geom &g, int nbits, cudaStream_t s);

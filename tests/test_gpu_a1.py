@@ -78,6 +78,8 @@ A1_CASES = [
     ("d1", 50, 1, 2, 3, 3, "theory", 0, 6, "uniform"),
     ("d2", 64, 2, 3, 3, 3, "exp", 0.1, 7, "uniform"),
     ("wide_band", 700, 12, 2, 60, 50, "exp", 0.1, 8, "mixture"),
+    # 4000 arms x 25 B > A1_SMEM_MAX: the state lives in the global workspace
+    ("global_state", 4000, 4, 2, 3, 3, "exp", 0.01, 9, "mixture"),
 ]
 
 
@@ -109,3 +111,21 @@ def test_a1_rejects_wide_band(ak):
             ix.query(Q, 300, 213, 0.05, 0, orc.alpha_theory(800, 0.05, 8), schedule="a1")
     finally:
         ix.close()
+
+
+def test_a1_device_api_matches_host(ak):
+    """aknn_query_a1_device (device buffers, a stream) gives the host call's bytes."""
+    import torch
+    X, Q = synth.small_instance(352, 300, 48, q=5)
+    al = orc.alpha_experimental(300, 0.05, 48, 0.05)
+    ix = ak.Index(torch.from_numpy(X).cuda())
+    try:
+        host = ix.query(Q, 3, 3, 0.05, 11, al, counts=True, sums=True, schedule="a1", qi_offset=7)
+        dev = ix.query_device(torch.from_numpy(Q).cuda(), 3, 3, 0.05, 11, torch.from_numpy(al).cuda(),
+                              counts=True, sums=True, schedule="a1", qi_offset=7)
+        st = ix.stats()
+    finally:
+        ix.close()
+    for key in ("sets", "dhat", "counts", "sums", "evals", "draws", "rounds"):
+        assert np.array_equal(dev[key].cpu().numpy(), host[key]), key
+    assert st["kernel_launches"] == 1
