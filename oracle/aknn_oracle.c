@@ -19,6 +19,9 @@
  *   orc_round_step        pinned: hand-built states (S:139-171 examples), brute sort
  *   orc_query_br          pinned: planted set, d=1, all-exact, Theorem-1 rate,
  *                         closed-form draw/eval accounting, A1 stream prefix
+ *   orc_wor_*             pinned: exhaustive bijection of [0, d) (many d, keys),
+ *                         uniformity of pi(t) over keys, A1 full-permutation
+ *                         sums equal brute force, evals = sum of counts
  *   per-arm counts, round numbers and the order of the returned set:
  *                         parity unpinned beyond the invariants above.
  */
@@ -105,12 +108,79 @@ uint32_t orc_draw_index(uint64_t seed, uint32_t qi, uint32_t i, int64_t t, uint3
   return orc_lemire(w[u & 3u], d);
 }
 
+/* ------------------------------------------------------------------------ */
+/* Sampling WITHOUT replacement (footnote 1 to P:120;  */
+/* DESIGN.md reading R23).  The t-th sample of arm (qi, i), t = 0 .. d-1, is  */
+/* coordinate pi(t) of a permutation pi of [0, d) keyed per arm:              */
+/*   w = the Philox4x32-10 block of counter (0, i, qi, 0x80000000) under the  */
+/*       seed (a level word no draw uses);                                    */
+/*   E = a balanced 8-round Feistel network on 2*hb bits (the smallest        */
+/*       hb >= 1 with 2^(2 hb) >= d), round r: (L, R) -> (R, L ^ F_r(R)),     */
+/*       F_r(R) = the top hb bits of g((R xor k_r) * 0x9E3779B1 mod 2^32),    */
+/*       g(h) = (h xor (h >> 16)) * 0x85EBCA6B mod 2^32,                      */
+/*       k_r = w[r mod 4] + r * 0x9E3779B9 mod 2^32;                          */
+/*   rho(t) = E^m(t) for the smallest m >= 1 with E^m(t) < d (cycle walking:  */
+/*       a permutation of a superset restricted this way permutes [0, d));    */
+/*   pi(t) = (rho(t) + b) mod d, b = floor((w0 xor w2) * d / 2^32) (a uniform */
+/*       rotation: the position of every t is uniform over keys).             */
+/* ------------------------------------------------------------------------ */
+uint32_t orc_wor_half_bits(uint32_t d) {
+  uint32_t hb = 1;
+  while (((uint64_t)1 << (2 * hb)) < (uint64_t)d) ++hb;
+  return hb;
+}
+
+void orc_wor_keys(uint64_t seed, uint32_t qi, uint32_t i, uint32_t keys[4]) {
+  const uint32_t ctr[4] = {0u, i, qi, 0x80000000u};
+  const uint32_t key[2] = {(uint32_t)(seed & 0xffffffffu), (uint32_t)(seed >> 32)};
+  orc_philox4x32_10(ctr, key, keys);
+}
+
+uint32_t orc_feistel(const uint32_t keys[4], uint32_t hb, uint32_t x) {
+  const uint32_t mask = (1u << hb) - 1u;
+  uint32_t L = x >> hb, R = x & mask;
+  for (uint32_t r = 0; r < 8; ++r) {
+    const uint32_t kr = keys[r & 3u] + r * 0x9E3779B9u;
+    uint32_t f = (R ^ kr) * 0x9E3779B1u;
+    f = (f ^ (f >> 16)) * 0x85EBCA6Bu;
+    f >>= 32u - hb;
+    const uint32_t newL = R;
+    R = L ^ f;
+    L = newL;
+  }
+  return (L << hb) | R;
+}
+
+uint32_t orc_wor_index(const uint32_t keys[4], uint32_t d, uint32_t t) {
+  const uint32_t hb = orc_wor_half_bits(d);
+  uint32_t x = t;
+  do {
+    x = orc_feistel(keys, hb, x);
+  } while (x >= d);
+  const uint32_t b = orc_lemire(keys[0] ^ keys[2], d);
+  return x + b >= d ? x + b - d : x + b;
+}
+
+/* pi(0..d-1) of arm (qi, i), for the pins (a bijection of [0, d)).          */
+void orc_wor_perm(uint64_t seed, uint32_t qi, uint32_t i, uint32_t d, uint32_t *out) {
+  uint32_t keys[4];
+  orc_wor_keys(seed, qi, i, keys);
+  for (uint32_t t = 0; t < d; ++t) out[t] = orc_wor_index(keys, d, t);
+}
+
 /* One sampled squared coordinate difference |[x_i]_j - [x]_j|^2,
  * kept as the exact integer (a-b)^2; the [0,1] sample is that / 65025
  * (reading R2).                                            */
 static int64_t draw_sq(const uint8_t *xi, const uint8_t *x, uint64_t seed, uint32_t qi,
-                       uint32_t i, int64_t t, uint32_t d) {
-  const uint32_t j = orc_draw_index(seed, qi, i, t, d);
+                       uint32_t i, int64_t t, uint32_t d, int wor) {
+  uint32_t j;
+  if (wor) {
+    uint32_t keys[4];
+    orc_wor_keys(seed, qi, i, keys);
+    j = orc_wor_index(keys, d, (uint32_t)t);
+  } else {
+    j = orc_draw_index(seed, qi, i, t, d);
+  }
   const int64_t diff = (int64_t)xi[j] - (int64_t)x[j];
   return diff * diff;
 }
@@ -311,8 +381,8 @@ int orc_round_step(int64_t n, int32_t d, const int64_t *S, const int32_t *T, int
  */
 int orc_query_br(const uint8_t *X, int64_t n, int32_t d, const uint8_t *Qrows, int32_t q,
                  const int32_t *qids, int64_t id_offset, int32_t k, int32_t h, uint64_t seed,
-                 const double *alpha, int32_t max_rounds, int32_t *sets, double *dhat,
-                 int32_t *counts, int64_t *sums, int64_t *evals, int64_t *draws,
+                 const double *alpha, int32_t max_rounds, int32_t wor, int32_t *sets,
+                 double *dhat, int32_t *counts, int64_t *sums, int64_t *evals, int64_t *draws,
                  int32_t *rounds) {
   if (n < 2 || d < 1 || q < 0 || k < 1 || h < 0 || (int64_t)k + h >= n || !alpha || !sets)
     return ORC_EINVAL;
@@ -328,10 +398,10 @@ int orc_query_br(const uint8_t *X, int64_t n, int32_t d, const uint8_t *Qrows, i
   for (int32_t a = 0; a < q; ++a) {
     const uint8_t *x = Qrows + (size_t)a * d;
     const uint32_t qi = (uint32_t)qids[a];
-    int64_t ndraws = 0, nexact = 0;
+    int64_t ndraws = 0, ncharge = 0;
     /* R0, Algorithm 1 initialisation: one sample per arm, T=1. */
     for (int64_t i = 0; i < n; ++i) {
-      S[i] = draw_sq(X + (size_t)i * d, x, seed, qi, (uint32_t)(i + id_offset), 0, (uint32_t)d);
+      S[i] = draw_sq(X + (size_t)i * d, x, seed, qi, (uint32_t)(i + id_offset), 0, (uint32_t)d, wor);
       T[i] = 1;
       ndraws += 1;
       if (d == 1) T[i] = d; /* the single coordinate is the exact distance */
@@ -352,13 +422,15 @@ int orc_query_br(const uint8_t *X, int64_t n, int32_t d, const uint8_t *Qrows, i
         ++nact;
         const uint8_t *xi = X + (size_t)i * d;
         if (2 * (int64_t)T[i] >= d) {
-          /* P:176 exact fallback, taken before the draws that would reach m */
+          /* P:176 exact fallback, taken before the draws that would reach m;
+           * charged d evaluations, or without replacement the d - T
+           * coordinates the permutation had not drawn yet (reading R23)   */
           S[i] = exact_sq(xi, x, d);
+          ncharge += wor ? (int64_t)d - T[i] : (int64_t)d;
           T[i] = d;
-          ++nexact;
         } else {
           for (int64_t t = T[i]; t < 2 * (int64_t)T[i]; ++t)
-            S[i] += draw_sq(xi, x, seed, qi, (uint32_t)(i + id_offset), t, (uint32_t)d);
+            S[i] += draw_sq(xi, x, seed, qi, (uint32_t)(i + id_offset), t, (uint32_t)d, wor);
           ndraws += T[i];
           T[i] *= 2;
         }
@@ -374,7 +446,7 @@ int orc_query_br(const uint8_t *X, int64_t n, int32_t d, const uint8_t *Qrows, i
     if (counts) memcpy(counts + (size_t)a * n, T, sizeof(int32_t) * (size_t)n);
     if (sums) memcpy(sums + (size_t)a * n, S, sizeof(int64_t) * (size_t)n);
     if (draws) draws[a] = ndraws;
-    if (evals) evals[a] = ndraws + (int64_t)d * nexact;
+    if (evals) evals[a] = ndraws + ncharge;
     if (rounds) rounds[a] = r;
     if (status == ORC_EMAXROUNDS) {  /* every query still runs to its own cap */
       hit_max = 1;
@@ -392,7 +464,7 @@ int orc_query_br(const uint8_t *X, int64_t n, int32_t d, const uint8_t *Qrows, i
 /* ------------------------------------------------------------------------ */
 int orc_query_a1(const uint8_t *X, int64_t n, int32_t d, const uint8_t *x, int32_t qi,
                  int32_t k, int32_t h, uint64_t seed, const double *alpha, int64_t max_iters,
-                 int32_t *set, int32_t *counts, int64_t *sums, int64_t *evals,
+                 int32_t wor, int32_t *set, int32_t *counts, int64_t *sums, int64_t *evals,
                  int64_t *draws, int64_t *iters) {
   if (n < 2 || d < 1 || k < 1 || h < 0 || (int64_t)k + h >= n || !alpha || !set)
     return ORC_EINVAL;
@@ -406,7 +478,7 @@ int orc_query_a1(const uint8_t *X, int64_t n, int32_t d, const uint8_t *x, int32
   int64_t ndraws = 0, nexact = 0, it = 0;
   int status = ORC_OK;
   for (int64_t i = 0; i < n; ++i) {
-    S[i] = draw_sq(X + (size_t)i * d, x, seed, (uint32_t)qi, (uint32_t)i, 0, (uint32_t)d);
+    S[i] = draw_sq(X + (size_t)i * d, x, seed, (uint32_t)qi, (uint32_t)i, 0, (uint32_t)d, wor);
     T[i] = 1;
     ndraws += 1;
     if (d == 1) T[i] = d;
@@ -435,14 +507,19 @@ int orc_query_a1(const uint8_t *X, int64_t n, int32_t d, const uint8_t *x, int32
     for (int s = 0; s < 2; ++s) {         /* "For l in {d1, b2}" */
       const int32_t l = sel[s];
       if (T[l] >= d) continue;
-      S[l] += draw_sq(X + (size_t)l * d, x, seed, (uint32_t)qi, (uint32_t)l, T[l], (uint32_t)d);
+      S[l] += draw_sq(X + (size_t)l * d, x, seed, (uint32_t)qi, (uint32_t)l, T[l], (uint32_t)d, wor);
       T[l] += 1;
       ndraws += 1;
       if (T[l] == d) {                     /* "If T_l = m ... exactly" */
-        S[l] = exact_sq(X + (size_t)l * d, x, d);
-        ++nexact;
+        const int64_t ex = exact_sq(X + (size_t)l * d, x, d);
+        /* without replacement the d samples ARE every coordinate once: the
+         * running sum already is the exact one, and nothing more is charged */
+        if (wor && S[l] != ex) { status = ORC_EINTERNAL; break; }
+        S[l] = ex;
+        if (!wor) ++nexact;
       }
     }
+    if (status != ORC_OK) break;
   }
   for (int32_t r = 0; r < k + h; ++r) set[r] = order[r];
   if (counts) memcpy(counts, T, sizeof(int32_t) * (size_t)n);

@@ -53,9 +53,17 @@ def lib():
                                      P, P, P, P, P]
         L.orc_query_br.argtypes = [P, C.c_int64, C.c_int32, P, C.c_int32, P, C.c_int64,
                                    C.c_int32, C.c_int32, C.c_uint64, P, C.c_int32,
-                                   P, P, P, P, P, P, P]
+                                   C.c_int32, P, P, P, P, P, P, P]
         L.orc_query_a1.argtypes = [P, C.c_int64, C.c_int32, P, C.c_int32, C.c_int32,
-                                   C.c_int32, C.c_uint64, P, C.c_int64, P, P, P, P, P, P]
+                                   C.c_int32, C.c_uint64, P, C.c_int64, C.c_int32, P, P, P, P, P, P]
+        L.orc_wor_half_bits.restype = C.c_uint32
+        L.orc_wor_half_bits.argtypes = [C.c_uint32]
+        L.orc_wor_keys.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, P]
+        L.orc_feistel.restype = C.c_uint32
+        L.orc_feistel.argtypes = [P, C.c_uint32, C.c_uint32]
+        L.orc_wor_index.restype = C.c_uint32
+        L.orc_wor_index.argtypes = [P, C.c_uint32, C.c_uint32]
+        L.orc_wor_perm.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, P]
         _lib = L
     return _lib
 
@@ -139,7 +147,7 @@ SHARED_QI = 0xFFFFFFFF  # the counter word of query-independent draws (SURVEY §
 
 def query_br(X, Q, k: int, h: int, seed: int, alpha, qids=None, id_offset: int = 0,
              max_rounds: int = 0, want_counts: bool = True, want_sums: bool = False,
-             shared_draws: bool = False):
+             shared_draws: bool = False, without_replacement: bool = False):
     """Batched round rule BR, one query at a time.  shared_draws:
     every query's counter word is SHARED_QI, i.e. arm i's t-th coordinate is the same
     for all queries; each query alone is unchanged in law."""
@@ -160,7 +168,7 @@ def query_br(X, Q, k: int, h: int, seed: int, alpha, qids=None, id_offset: int =
         evals=np.zeros(q, np.int64), draws=np.zeros(q, np.int64), rounds=np.zeros(q, np.int32))
     rc = lib().orc_query_br(_p(X), n, d, _p(Q), q, _p(qids), id_offset, k, h,
                             C.c_uint64(seed & (2**64 - 1)), _p(alpha), max_rounds,
-                            _p(out["sets"]), _p(out["dhat"]), _p(out["counts"]),
+                            1 if without_replacement else 0, _p(out["sets"]), _p(out["dhat"]), _p(out["counts"]),
                             _p(out["sums"]), _p(out["evals"]), _p(out["draws"]),
                             _p(out["rounds"]))
     out["status"] = rc
@@ -169,7 +177,8 @@ def query_br(X, Q, k: int, h: int, seed: int, alpha, qids=None, id_offset: int =
     return out
 
 
-def query_a1(X, x, k: int, h: int, seed: int, alpha, qi: int = 0, max_iters: int = 0):
+def query_a1(X, x, k: int, h: int, seed: int, alpha, qi: int = 0, max_iters: int = 0,
+             without_replacement: bool = False):
     """Literal Algorithm 1 for one query; tiny inputs only."""
     X = np.ascontiguousarray(X, np.uint8)
     x = np.ascontiguousarray(x, np.uint8).reshape(-1)
@@ -180,9 +189,37 @@ def query_a1(X, x, k: int, h: int, seed: int, alpha, qi: int = 0, max_iters: int
                sums=np.zeros(n, np.int64))
     ev, dr, it = C.c_int64(), C.c_int64(), C.c_int64()
     rc = lib().orc_query_a1(_p(X), n, d, _p(x), qi, k, h, C.c_uint64(seed & (2**64 - 1)),
-                            _p(alpha), max_iters, _p(out["set"]), _p(out["counts"]),
+                            _p(alpha), max_iters, 1 if without_replacement else 0, _p(out["set"]), _p(out["counts"]),
                             _p(out["sums"]), C.byref(ev), C.byref(dr), C.byref(it))
     if rc not in (OK, EMAXROUNDS):
         raise ValueError(f"query_a1 rc={rc}")
     out.update(status=rc, evals=ev.value, draws=dr.value, iters=it.value)
+    return out
+
+
+# ---- sampling without replacement (footnote 1 to P:120; reading R23) ----
+def wor_half_bits(d: int) -> int:
+    return int(lib().orc_wor_half_bits(d))
+
+
+def wor_keys(seed: int, qi: int, i: int) -> np.ndarray:
+    k = np.zeros(4, np.uint32)
+    lib().orc_wor_keys(C.c_uint64(seed & (2**64 - 1)), qi, i, _p(k))
+    return k
+
+
+def feistel(keys, hb: int, x: int) -> int:
+    k = np.ascontiguousarray(keys, np.uint32)
+    return int(lib().orc_feistel(_p(k), hb, x))
+
+
+def wor_index(keys, d: int, t: int) -> int:
+    k = np.ascontiguousarray(keys, np.uint32)
+    return int(lib().orc_wor_index(_p(k), d, t))
+
+
+def wor_perm(seed: int, qi: int, i: int, d: int) -> np.ndarray:
+    """pi(0..d-1) of arm (qi, i): the order in which it samples its coordinates."""
+    out = np.zeros(d, np.uint32)
+    lib().orc_wor_perm(C.c_uint64(seed & (2**64 - 1)), qi, i, d, _p(out))
     return out
