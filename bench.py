@@ -64,6 +64,15 @@ def _args():
     ap.add_argument("--no-variant", action="store_true", help="skip the shared-draw variant timing")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-exact", action="store_true")
+    ap.add_argument("--workload", choices=("config", "sec5"), default="config",
+                    help="sec5: the paper's §5 sweep (recall / fraction vs C_alpha, sec5.py)")
+    ap.add_argument("--trials", type=int, default=20, help="sec5: trials per (workload, C_alpha)")
+    ap.add_argument("--c-alpha", default="1e-5,1e-4,1e-3,1e-2", help="sec5: C_alpha values")
+    ap.add_argument("--sec5-schedules", default="a1,br", help="sec5: a1 and/or br")
+    ap.add_argument("--sec5-workloads", default="p10,p100,p1000,images")
+    ap.add_argument("--sec5-threads", type=int, default=80, help="sec5: trials in flight")
+    ap.add_argument("--sec5-a1-max-iters", type=int, default=0,
+                    help="sec5: cap on Algorithm-1 iterations per query (0: none; capped trials are counted)")
     ap.add_argument("--clock-sampler", choices=("nvml", "smi", "none"), default="nvml")
     a = ap.parse_args()
     if a.config is None:
@@ -853,7 +862,15 @@ def main():
     args = _args()
     dist = Dist()
     try:
-        if args.impl == "reference":
+        if args.workload == "sec5":
+            if args.impl == "reference":
+                if dist.rank == 0:
+                    print(json.dumps({"impl": "reference", "unavailable": "the §5 sweep has no "
+                                      "reference arm (bench.py --workload config times the oracle)"}))
+            else:
+                import sec5
+                sec5.run(args, dist)
+        elif args.impl == "reference":
             (run_reference_a1 if args.schedule == "a1" else run_reference)(args, dist)
         elif args.schedule == "a1":
             run_a1(args, dist)

@@ -101,6 +101,18 @@ typedef struct {
 /* bit 5: with shared draws, keep every level on the per-pair gathers instead of the
    tensor-core level GEMMs (k_level_mma; diagnostics, identical results)      */
 #define AKNN_FLAG_NO_LEVEL_MMA 32
+/* bit 6: sampling WITHOUT replacement (footnote 1 to P:120; SURVEY.md §8(f) row 4;
+   DESIGN.md reading R23): the t-th sample of arm (qi, i) is coordinate pi(t) of a
+   permutation of [0, d) keyed per arm (an 8-round Feistel network on the smallest
+   even-bit domain >= d with cycle walking and a keyed rotation; its keys are the
+   Philox4x32-10 block of counter (0, i, qi, 0x80000000)).  Estimates stay unbiased
+   and the footnote-2 / §5 radii stay valid (Hoeffding's bound holds without
+   replacement).  An exact fallback is charged only the d - T coordinates
+   not drawn yet, so evals = the sum of the final counts <= n d; in Algorithm 1 an
+   arm reaching T = d has drawn every coordinate once (no extra charge).  Results
+   differ from the default stream and match the oracle's without_replacement mode.
+   Not combinable with AKNN_FLAG_SHARED_DRAWS (EINVAL).                        */
+#define AKNN_FLAG_WITHOUT_REPLACEMENT 64
 
 /* Execution statistics of the last query call on an index (aknn_get_stats).
  * Kernel classes: init (a2), select (a6-a7: rank split, bounds, Eq. 5),
@@ -232,8 +244,9 @@ aknn_status aknn_query_multi(const aknn_index *const *shards, int32_t nshards,
  * evaluations.  The t-th sample of an arm is the batched rule's (the same
  * Philox counter), so only the schedule differs.  Arguments as aknn_query_ex;
  * opts->max_rounds caps the ITERATIONS (AKNN_EMAXROUNDS, outputs = the state
- * reached), opts->timing and opts->flags are ignored.  Outputs: sets/dhat of
- * the final top-(k+h) in rank order, counts = T_i (1..d), sums = S_i,
+ * reached), opts->timing is ignored, and of opts->flags only
+ * AKNN_FLAG_WITHOUT_REPLACEMENT applies (reading R23; evals = draws then).
+ * Outputs: sets/dhat of the final top-(k+h) in rank order, counts = T_i (1..d), sums = S_i,
  * draws, evals = draws + d * (#arms that went exact), rounds = iterations
  * (including the last, stopping one).  EINVAL: the aknn_query_ex domain, a
  * sharded index, or k + h > 512.  Bit-identical to the oracle's A1 mode.     */

@@ -53,6 +53,7 @@ FLAG_NO_TILES = 4  # every level gather through the work lists (no shared-memory
 FLAG_EXACT_MMA_ALL = 8  # every tile with an exact fallback on the tensor cores
 FLAG_SHARED_DRAWS = 16  # query-independent coordinate draws
 FLAG_NO_LEVEL_MMA = 32  # shared draws without the tensor-core level GEMMs
+FLAG_WITHOUT_REPLACEMENT = 64  # sampling without replacement (footnote 1 to P:120; reading R23)
 
 
 class Stats(C.Structure):

@@ -15,12 +15,14 @@
 //   R4  stop iff A <= B
 //   Eq. (4) b2 = argmax_{{d2} u M} alpha (ties: d2, then smaller id)
 //   a3  sample d1 and b2 once each (T += 1); at T == d the arm's S becomes the
-//       exact sum, charged d evaluations
+//       exact sum, charged d evaluations (without replacement, reading
+//       R23: the d samples are every coordinate once, so no extra charge)
 // The per-arm sample stream is the batched rule's (Philox counter
 // (u >> 2, id, qi, b) of the t-th sample, b = its doubling level), so the two
 // schedules see the same coordinates.  Ranking by the cached fp64 d_hat with the
 // id as tie-break is the exact rational order (reading R9).
 #include <cstdint>
+#include <cstdio>
 
 #include "internal.cuh"
 #include "launch.h"
@@ -28,6 +30,12 @@
 namespace aknn {
 
 namespace {
+
+#ifdef AKNN_A1_CHECK
+#define A1_CHECK(c, ...) do { if (!(c)) { printf("A1_CHECK %s line %d: ", #c, __LINE__); printf(__VA_ARGS__); printf("\n"); __trap(); } } while (0)
+#else
+#define A1_CHECK(c, ...) do { } while (0)
+#endif
 
 constexpr int A1_WARPS = 4;  // queries per CTA
 constexpr unsigned FULL = 0xffffffffu;
@@ -71,9 +79,15 @@ __device__ __forceinline__ int32_t a1_draw(const A1Geom &g, const uint8_t *x, in
     b = lg + 1u;
     u = (uint32_t)t - (1u << lg);
   }
-  const uint4 w = philox4x32_10_rk(make_uint4(u >> 2, (uint32_t)i + g.id_offset, qrng, b), g.rk0, g.rk1);
-  const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-  const uint32_t j = coord_of(ws[u & 3u], (uint32_t)g.d);
+  uint32_t j;
+  if (g.wor) {  // reading R23: pi(t) of the arm's permutation
+    j = wor_coord(wor_keys(g.rk0, g.rk1, (uint32_t)i + g.id_offset, qrng), g.wor_hb, (uint32_t)g.d, (uint32_t)t);
+  } else {
+    const uint4 w = philox4x32_10_rk(make_uint4(u >> 2, (uint32_t)i + g.id_offset, qrng, b), g.rk0, g.rk1);
+    const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+    j = coord_of(ws[u & 3u], (uint32_t)g.d);
+  }
+  A1_CHECK(i >= 0 && i < g.n && j < (uint32_t)g.d && t >= 0 && t < g.d, "i %d j %u t %d", i, j, t);
   const int32_t diff = (int32_t)g.X[(size_t)i * g.pitch + j] - (int32_t)x[j];
   return diff * diff;
 }
@@ -235,6 +249,7 @@ __global__ void __launch_bounds__(32 * A1_WARPS) k_a1(A1Geom g) {
       km = warp_min(pk);
       d2 = warp_min(pl);
       const int last = a.cm[kh - 1];
+      A1_CHECK(km.i >= 0 && km.i < n && d2.i >= 0 && d2.i < n && last >= 0 && last < n, "km %d d2 %d last %d it %d", km.i, d2.i, last, it);
       const double dl = a.dh[last];
       if (!key_less(km.v, km.i, dl, last)) break;
       if (lane == 0) {
@@ -272,6 +287,7 @@ __global__ void __launch_bounds__(32 * A1_WARPS) k_a1(A1Geom g) {
     }
     bm = warp_max(bm);
     const int b2 = (bm.i >= 0 && bm.v > a1_alpha(g, a, a.T[d2.i])) ? bm.i : d2.i;
+    A1_CHECK(d1.i >= 0 && d1.i < n && b2 >= 0 && b2 < n && d1.i != b2, "d1 %d b2 %d it %d", d1.i, b2, it);
     // a3: one sample of d1 and one of b2 (distinct arms: d1 in C, b2
     // not), drawn side by side by lanes 0 and 1
     const int32_t T1 = a.T[d1.i], T2 = a.T[b2];
@@ -303,7 +319,11 @@ __global__ void __launch_bounds__(32 * A1_WARPS) k_a1(A1Geom g) {
         a.L[l] = dh - a1_alpha(g, a, T + 1);
       }
       __syncwarp();
-      if (a.incm[l]) cm_reinsert(g, a, cm_find(g, a, l, lane), l, lane);
+      if (a.incm[l]) {
+        const int p = cm_find(g, a, l, lane);
+        A1_CHECK(p >= 0 && p < kh, "cm_find %d arm %d it %d", p, l, it);
+        cm_reinsert(g, a, p, l, lane);
+      }
       else if ((l & 31) == lane) lane_scan(g, a, lane, &pk, &pl);  // an F arm moved
     }
   }
@@ -321,7 +341,8 @@ __global__ void __launch_bounds__(32 * A1_WARPS) k_a1(A1Geom g) {
   }
   if (lane == 0) {
     if (o.draws) o.draws[row] = draws;
-    if (o.evals) o.evals[row] = draws + (long long)d * nexact;
+    // without replacement an arm reaching T = d drew every coordinate once: no charge
+    if (o.evals) o.evals[row] = g.wor ? draws : draws + (long long)d * nexact;
     if (o.rounds) o.rounds[row] = it;
     if (status) atomicOr(g.status, 1);
   }

@@ -49,14 +49,25 @@ __device__ __forceinline__ uint32_t sq_diff(uint32_t xa, uint32_t qa, uint32_t j
 // Four draws of one Philox block: the bytes are packed four to a word (PRMT, ALU)
 // and summed with one VABSDIFF4 + one IDP.4A, instead of four subtractions and four
 // multiply-adds on the fma-heavy pipe.  Exact: |x - q|^2 summed in uint32.
-__device__ __forceinline__ uint32_t sq_diff4(uint32_t xa, uint32_t qa, uint4 w, uint32_t d, uint32_t acc) {
-  const uint32_t j0 = coord_of(w.x, d), j1 = coord_of(w.y, d), j2 = coord_of(w.z, d), j3 = coord_of(w.w, d);
+__device__ __forceinline__ uint32_t sq_diff4_j(uint32_t xa, uint32_t qa, uint32_t j0, uint32_t j1, uint32_t j2,
+                                               uint32_t j3, uint32_t acc) {
   const uint32_t x01 = __byte_perm(lds_u8(xa | j0), lds_u8(xa | j1), 0x1140);
   const uint32_t x23 = __byte_perm(lds_u8(xa | j2), lds_u8(xa | j3), 0x4011);
   const uint32_t q01 = __byte_perm(lds_u8(qa | j0), lds_u8(qa | j1), 0x1140);
   const uint32_t q23 = __byte_perm(lds_u8(qa | j2), lds_u8(qa | j3), 0x4011);
   const uint32_t t = __vabsdiffu4(__byte_perm(x01, x23, 0x7610), __byte_perm(q01, q23, 0x7610));
   return __dp4a(t, t, acc);
+}
+
+__device__ __forceinline__ uint32_t sq_diff4(uint32_t xa, uint32_t qa, uint4 w, uint32_t d, uint32_t acc) {
+  return sq_diff4_j(xa, qa, coord_of(w.x, d), coord_of(w.y, d), coord_of(w.z, d), coord_of(w.w, d), acc);
+}
+
+// Without replacement (reading R23): the draws t0 .. t0 + 3 are pi(t) under the keys w.
+__device__ __forceinline__ uint32_t sq_diff4_wor(uint32_t xa, uint32_t qa, uint4 w, uint32_t hb, uint32_t d,
+                                                 uint32_t t0, uint32_t acc) {
+  return sq_diff4_j(xa, qa, wor_coord(w, hb, d, t0), wor_coord(w, hb, d, t0 + 1u), wor_coord(w, hb, d, t0 + 2u),
+                    wor_coord(w, hb, d, t0 + 3u), acc);
 }
 
 // ---------------------------------------------------------------------------
@@ -173,7 +184,9 @@ __device__ __forceinline__ void f1_accumulate(uint32_t qt_s, uint32_t dbuf_s, in
   }
 }
 
-template <bool F1>
+// MODE 0: per-query draws with replacement; 1: query-independent draws (R = 32);
+// 2: per-query draws without replacement (reading R23).
+template <int MODE>
 __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
   extern __shared__ __align__(16) unsigned char tsm[];
   __shared__ unsigned lcnt[MAX_LEVELS], loff[MAX_LEVELS + 1], lfill[MAX_LEVELS];
@@ -237,7 +250,8 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
     const int r0 = tr << g.tile_lr, p0 = tp << g.tile_lp;
     const bool reuse_x = tp == staged_tp;  // the point rows of this column are staged
     staged_tp = tp;
-    constexpr bool f1 = F1;  // query-independent draws with R = 32 (host-selected instantiation)
+    constexpr bool f1 = MODE == 1;  // query-independent draws with R = 32 (host-selected instantiation)
+    constexpr bool wor = MODE == 2;
     __syncthreads();  // the previous tile's shared memory is no longer in use
     if (tid < MAX_LEVELS) lcnt[tid] = 0;
 
@@ -382,7 +396,8 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
             const int e = ok ? pr[k] : 0;
             const uint32_t gi = (uint32_t)(p0 + (e & (P - 1))) + g.id_offset;
             const uint32_t gq = rng_qi(g, (uint32_t)(r0 + (e >> g.tile_lp)));
-            w[k] = philox4x32_10_rk(make_uint4((uint32_t)k & (nb - 1), gi, gq, lv), g.rk0, g.rk1);
+            w[k] = wor ? wor_keys(g.rk0, g.rk1, gi, gq)
+                       : philox4x32_10_rk(make_uint4((uint32_t)k & (nb - 1), gi, gq, lv), g.rk0, g.rk1);
           }
           uint32_t sum = 0;
 #pragma unroll
@@ -390,7 +405,15 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
             if (pr[k] >= 0) {
               const uint32_t xa = xs + ((uint32_t)(pr[k] & (P - 1)) << sl);
               const uint32_t qa = rows_s + ((uint32_t)(pr[k] >> g.tile_lp) << sl);
-              if (s >= 4) {
+              if (wor) {  // draws t = s + 4 blk + e, e < min(s, 4)
+                const uint32_t t0 = s + 4u * ((uint32_t)k & (nb - 1));
+                if (s >= 4) {
+                  sum = sq_diff4_wor(xa, qa, w[k], g.wor_hb, d, t0, sum);
+                } else {
+                  sum += sq_diff(xa, qa, wor_coord(w[k], g.wor_hb, d, t0));
+                  if (s == 2) sum += sq_diff(xa, qa, wor_coord(w[k], g.wor_hb, d, t0 + 1u));
+                }
+              } else if (s >= 4) {
                 sum = sq_diff4(xa, qa, w[k], d, sum);
               } else {  // levels 0 and 1 use 1 and 2 words of the block
                 sum += sq_diff(xa, qa, coord_of(w[k].x, d));
@@ -417,7 +440,13 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
           const uint32_t gi = (uint32_t)(p0 + (pe & (P - 1))) + g.id_offset;
           const uint32_t gq = rng_qi(g, (uint32_t)(r0 + (pe >> g.tile_lp)));
           uint32_t sum = 0;
-          if (ok) {
+          if (ok && wor) {
+            const uint4 kk = wor_keys(g.rk0, g.rk1, gi, gq);
+            for (unsigned b0 = sub * ADV_TP; b0 < nb; b0 += tpp * ADV_TP) {
+#pragma unroll
+              for (int k = 0; k < ADV_TP; ++k) sum = sq_diff4_wor(xa, qa, kk, g.wor_hb, d, s + 4u * (b0 + k), sum);
+            }
+          } else if (ok) {
             for (unsigned b0 = sub * ADV_TP; b0 < nb; b0 += tpp * ADV_TP) {
               uint4 w[ADV_TP];
 #pragma unroll
@@ -477,8 +506,10 @@ static size_t tile_base() {  // static shared memory + the per-CTA system reserv
     cudaFuncAttributes fa{};
     int dev = 0, rsv = 0;
     cudaFuncAttributes fb{};
-    if (cudaFuncGetAttributes(&fa, k_advance_tiles<false>) != cudaSuccess) fa.sharedSizeBytes = 2048;
-    if (cudaFuncGetAttributes(&fb, k_advance_tiles<true>) == cudaSuccess && fb.sharedSizeBytes > fa.sharedSizeBytes)
+    if (cudaFuncGetAttributes(&fa, k_advance_tiles<0>) != cudaSuccess) fa.sharedSizeBytes = 2048;
+    if (cudaFuncGetAttributes(&fb, k_advance_tiles<1>) == cudaSuccess && fb.sharedSizeBytes > fa.sharedSizeBytes)
+      fa.sharedSizeBytes = fb.sharedSizeBytes;
+    if (cudaFuncGetAttributes(&fb, k_advance_tiles<2>) == cudaSuccess && fb.sharedSizeBytes > fa.sharedSizeBytes)
       fa.sharedSizeBytes = fb.sharedSizeBytes;
     if (cudaGetDevice(&dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev) != cudaSuccess)
@@ -491,23 +522,24 @@ static size_t tile_base() {  // static shared memory + the per-CTA system reserv
 // Shared memory per CTA of a tile shape (the occupancy the shape chooser reasons about).
 size_t tile_smem_bytes(int lr, int lp, int64_t pitch) { return tile_window(lr, lp, pitch, tile_base()); }
 
-template <bool F1>
+template <int MODE>
 static cudaError_t launch_tiles_k(const Geom &g, int num_sms, size_t smem, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(k_advance_tiles<F1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_advance_tiles<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_advance_tiles<F1>, TILE_NT, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_advance_tiles<MODE>, TILE_NT, smem);
   if (e != cudaSuccess) return e;
   if (per_sm < 1) per_sm = 1;
-  k_advance_tiles<F1><<<num_sms * per_sm, TILE_NT, smem, s>>>(g);
+  k_advance_tiles<MODE><<<num_sms * per_sm, TILE_NT, smem, s>>>(g);
   return cudaGetLastError();
 }
 
 cudaError_t launch_advance_tiles(const Geom &g, int num_sms, cudaStream_t s) {
   const size_t base = tile_base();
   const size_t smem = tile_window(g.tile_lr, g.tile_lp, g.pitch, base) - base;
-  if (g.shared_draws && g.tile_lr == 5) return launch_tiles_k<true>(g, num_sms, smem, s);
-  return launch_tiles_k<false>(g, num_sms, smem, s);
+  if (g.shared_draws && g.tile_lr == 5) return launch_tiles_k<1>(g, num_sms, smem, s);
+  if (g.wor) return launch_tiles_k<2>(g, num_sms, smem, s);
+  return launch_tiles_k<0>(g, num_sms, smem, s);
 }
 
 }  // namespace aknn

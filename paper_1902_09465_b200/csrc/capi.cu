@@ -625,6 +625,13 @@ aknn_status finish_pending(aknn_index *ix) {
 
 // Runs the whole query on device pointers.  Q rows have stride `qstride`
 // bytes in `queries_dev` (device).  Outputs are device pointers.
+// Flag combinations the path does not define.
+aknn_status check_flags(const aknn_opts &o) {
+  if ((o.flags & AKNN_FLAG_WITHOUT_REPLACEMENT) && (o.flags & AKNN_FLAG_SHARED_DRAWS))
+    return fail(AKNN_EINVAL, "AKNN_FLAG_WITHOUT_REPLACEMENT cannot be combined with AKNN_FLAG_SHARED_DRAWS");
+  return AKNN_OK;
+}
+
 aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstride, int32_t q,
                       int32_t k, int32_t h, uint64_t seed, const double *alpha_dev,
                       const aknn_opts *opts, const aknn_result *out, cudaStream_t st,
@@ -637,6 +644,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   if (k + h > output_max_kh())
     return fail(AKNN_EINVAL, "k+h=%d exceeds the supported %d", k + h, output_max_kh());
   const aknn_opts o = opts ? *opts : aknn_opts{};
+  TRY(check_flags(o));
   const int64_t npad = round_up(n, 16);
   // sub-batch size: the code (qi << ibits | i) must fit 32 bits; the
   // workspace (S 4 B + lvl 1 B + act 1 B + list 4 B per pair) fits in memory.
@@ -705,6 +713,8 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   g.adv_bpl = adv_bpl();
   g.force_radix = (o.flags & AKNN_FLAG_RADIX_SELECT) ? 1 : 0;
   g.shared_draws = (o.flags & AKNN_FLAG_SHARED_DRAWS) ? 1 : 0;
+  g.wor = (o.flags & AKNN_FLAG_WITHOUT_REPLACEMENT) ? 1 : 0;
+  g.wor_hb = wor_half_bits(d);
   g.stage_lo = stage_level(g.pitch);
   TRY(setup_exact_mma(ix, g, qb, ix->ws.as<uint8_t>(oXm), o, st));
   setup_tiles(g, tsh, o, qb, ix->ws.as<uint8_t>(oTw));
@@ -864,6 +874,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
   if ((int64_t)W * kh > 16384)
     return fail(AKNN_EINVAL, "world * (k+h) = %lld exceeds 16384 (merge buffer)", (long long)W * kh);
   const aknn_opts o = opts ? *opts : aknn_opts{};
+  TRY(check_flags(o));
   std::vector<KeyGeom> kg(shards.size());
   for (size_t s = 0; s < shards.size(); ++s) TRY(key_geom(shards[s]->n_local, ix0->n_global, d, &kg[s]));
   // sub-batch size: list codes fit 32 bits on every shard; memory on this device
@@ -954,7 +965,8 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     g.adv_bpl = adv_bpl();
     g.force_radix = (o.flags & AKNN_FLAG_RADIX_SELECT) ? 1 : 0;
     g.shared_draws = (o.flags & AKNN_FLAG_SHARED_DRAWS) ? 1 : 0;
-  g.shared_draws = (o.flags & AKNN_FLAG_SHARED_DRAWS) ? 1 : 0;
+    g.wor = (o.flags & AKNN_FLAG_WITHOUT_REPLACEMENT) ? 1 : 0;
+    g.wor_hb = wor_half_bits(d);
     g.stage_lo = stage_level(g.pitch);
     g.world = W;
     g.recv_stride = recv_stride;
@@ -1259,11 +1271,14 @@ aknn_status run_query_a1(aknn_index *ix, const uint8_t *queries_dev, int32_t q, 
                          const aknn_result *out, cudaStream_t st) {
   const int kh = k + h;
   if (kh > A1_MAX_KH) return fail(AKNN_EINVAL, "Algorithm 1 mode supports k+h <= %d (got %d)", A1_MAX_KH, kh);
+  // shared-memory mode needs the state AND the alpha / query tables in one CTA's
+  // window; otherwise every query's state lives in the global workspace
   const size_t per_s = a1_ws_per_query(ix->n_local, kh, ix->d, true);
-  const size_t per = per_s <= A1_SMEM_MAX ? per_s : a1_ws_per_query(ix->n_local, kh, ix->d, false);
+  const bool smem = per_s <= A1_SMEM_MAX;
+  const size_t per = smem ? per_s : a1_ws_per_query(ix->n_local, kh, ix->d, false);
   const size_t budget = (size_t)1 << 30;
-  const int qb = per <= A1_SMEM_MAX ? q : (int)std::max<size_t>(1, std::min<size_t>((size_t)q, budget / per));
-  TRY(ix->ws.ensure(256 + (per <= A1_SMEM_MAX ? 0 : per * (size_t)qb)));
+  const int qb = smem ? q : (int)std::max<size_t>(1, std::min<size_t>((size_t)q, budget / per));
+  TRY(ix->ws.ensure(256 + (smem ? 0 : per * (size_t)qb)));
   A1Geom g{};
   g.X = ix->X.as<uint8_t>();
   g.pitch = ix->pitch;
@@ -1284,7 +1299,9 @@ aknn_status run_query_a1(aknn_index *ix, const uint8_t *queries_dev, int32_t q, 
   g.status = ix->ws.as<int>();
   g.ws = ix->ws.as<unsigned char>(256);
   g.ws_per_query = per;
-  g.smem = per <= A1_SMEM_MAX ? 1 : 0;
+  g.smem = smem ? 1 : 0;
+  g.wor = (opts && (opts->flags & AKNN_FLAG_WITHOUT_REPLACEMENT)) ? 1 : 0;
+  g.wor_hb = wor_half_bits(ix->d);
   g.out = OutPtrs{0, 0, ix->n_local, 0, out->sets, out->dhat, out->counts, out->sums,
                   out->evals, out->draws, out->rounds};
   CU(cudaMemsetAsync(g.status, 0, sizeof(int), st));

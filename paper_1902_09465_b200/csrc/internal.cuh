@@ -49,6 +49,7 @@ struct QState {
   int rounds;                 // rounds evaluated
   long long draws;            // sampled draws      } tallied from the final
   long long nexact;           // exact fallbacks    } arm states by k_tally
+  long long exact_evals;      // evaluations charged for them (d each; d - T without replacement)
   long long blocks;           // Philox4x32-10 blocks the level gathers used
 };
 
@@ -101,6 +102,8 @@ struct Geom {
   uint32_t id_offset;    // global id of local row 0
   uint32_t qi0;          // RNG query index of batch row 0
   int shared_draws;      // 1: query-independent draws: counter word 0xFFFFFFFF
+  int wor;               // 1: sampling without replacement (AKNN_FLAG_WITHOUT_REPLACEMENT, R23)
+  uint32_t wor_hb;       //    half width of its Feistel domain (2^(2 hb) >= d)
   // shared draws on the tensor cores (exact_mma.cu, k_level_mma)
   int level_mma;         // 1: the round's dominant level runs as integer GEMMs
   uint8_t *q2lo, *q2hi;  // [q][pitch] q_j^2 byte planes
@@ -179,6 +182,44 @@ __device__ __forceinline__ uint32_t rng_qi(const Geom &g, uint32_t qi) { return 
 
 // Multiply-high map of a 32-bit word onto [0, d) (reading R5).
 __device__ __forceinline__ uint32_t coord_of(uint32_t w, uint32_t d) { return __umulhi(w, d); }
+
+// ---- Sampling without replacement (AKNN_FLAG_WITHOUT_REPLACEMENT; R23) ----
+// The t-th sample of an arm is pi(t), pi a permutation of [0, d) keyed by the arm's
+// Philox block w of counter (0, i, qi, WOR_LEVEL): rho = an 8-round balanced Feistel
+// network E on 2*hb bits, round r: (L, R) -> (R, L ^ top_hb(g((R ^ k_r) * 0x9E3779B1))),
+// g(h) = (h ^ (h >> 16)) * 0x85EBCA6B, k_r = w[r mod 4] + r * 0x9E3779B9, walked until
+// the value is < d; pi(t) = (rho(t) + b) mod d with b = (w.x ^ w.z) mapped onto [0, d).
+constexpr uint32_t WOR_LEVEL = 0x80000000u;  // a level word no draw uses
+__host__ inline uint32_t wor_half_bits(int d) {
+  uint32_t hb = 1;
+  while ((1ull << (2 * hb)) < (unsigned long long)d) ++hb;
+  return hb;
+}
+__device__ __forceinline__ uint4 wor_keys(const uint32_t *rk0, const uint32_t *rk1, uint32_t gi, uint32_t gq) {
+  return philox4x32_10_rk(make_uint4(0u, gi, gq, WOR_LEVEL), rk0, rk1);
+}
+__device__ __forceinline__ uint32_t wor_feistel(uint4 w, uint32_t hb, uint32_t x) {
+  const uint32_t sh = 32u - hb;
+  uint32_t L = x >> hb, R = x & ((1u << hb) - 1u);
+#pragma unroll
+  for (uint32_t r = 0; r < 8; ++r) {
+    const uint32_t kw = (r & 3u) == 0 ? w.x : (r & 3u) == 1 ? w.y : (r & 3u) == 2 ? w.z : w.w;
+    uint32_t f = (R ^ (kw + r * 0x9E3779B9u)) * 0x9E3779B1u;
+    f = (f ^ (f >> 16)) * 0x85EBCA6Bu;
+    const uint32_t nl = R;
+    R = L ^ (f >> sh);
+    L = nl;
+  }
+  return (L << hb) | R;
+}
+__device__ __forceinline__ uint32_t wor_coord(uint4 w, uint32_t hb, uint32_t d, uint32_t t) {
+  uint32_t x = t;
+  do {
+    x = wor_feistel(w, hb, x);
+  } while (x >= d);
+  x += coord_of(w.x ^ w.z, d);
+  return x >= d ? x - d : x;
+}
 
 // Exact order key of an arm: K = S * (L / T).  S/T ranks exactly like the
 // fp64 estimate S/(65025 T) (reading R9), and with the local index

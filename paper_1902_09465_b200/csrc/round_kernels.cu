@@ -33,9 +33,15 @@ __global__ void k_init(Geom g) {
     g.act[o] = 0;
     return;
   }
-  const uint4 w = philox4x32_10(make_uint4(0u, (uint32_t)i + g.id_offset, rng_qi(g, (uint32_t)qi), 0u),
-                                g.seed_lo, g.seed_hi);
-  const uint32_t j = coord_of(w.x, (uint32_t)g.d);
+  uint32_t j;
+  if (g.wor) {  // pi(0) of the arm's permutation (reading R23)
+    j = wor_coord(wor_keys(g.rk0, g.rk1, (uint32_t)i + g.id_offset, rng_qi(g, (uint32_t)qi)), g.wor_hb,
+                  (uint32_t)g.d, 0u);
+  } else {
+    const uint4 w = philox4x32_10(make_uint4(0u, (uint32_t)i + g.id_offset, rng_qi(g, (uint32_t)qi), 0u),
+                                  g.seed_lo, g.seed_hi);
+    j = coord_of(w.x, (uint32_t)g.d);
+  }
   const int diff = (int)__ldg(g.X + (size_t)i * g.pitch + j) - (int)__ldg(g.Q + (size_t)qi * g.pitch + j);
   g.S[o] = diff * diff;
   g.lvl[o] = (g.d == 1) ? LVL_EXACT : (uint8_t)0;  // d = 1: the draw is exact
@@ -54,6 +60,7 @@ __global__ void k_init_qstate(Geom g) {
   s.rounds = 0;
   s.draws = 0;  // tallied at the end (k_tally)
   s.nexact = 0;
+  s.exact_evals = 0;
   s.blocks = 0;
   g.qs[qi] = s;
 }
@@ -499,10 +506,11 @@ struct BlockTask {
 
 __device__ __forceinline__ void draw_blocks(const Geom &g, const BlockTask (&t)[ADV_P], int c,
                                             uint32_t s, uint32_t (&acc)[ADV_P]) {
-  uint4 w[ADV_P];
+  uint4 w[ADV_P];  // Philox words, or the arm's permutation keys (without replacement)
 #pragma unroll
   for (int k = 0; k < ADV_P; ++k)
-    w[k] = philox4x32_10_rk(make_uint4(t[k].blk, t[k].i, t[k].qi, (uint32_t)(c + 1)), g.rk0, g.rk1);
+    w[k] = g.wor ? wor_keys(g.rk0, g.rk1, t[k].i, t[k].qi)
+                 : philox4x32_10_rk(make_uint4(t[k].blk, t[k].i, t[k].qi, (uint32_t)(c + 1)), g.rk0, g.rk1);
 #pragma unroll
   for (int k = 0; k < ADV_P; ++k) {
     const uint32_t ws[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
@@ -511,13 +519,30 @@ __device__ __forceinline__ void draw_blocks(const Geom &g, const BlockTask (&t)[
     for (int e = 0; e < 4; ++e) {
       // s < 4 only at levels 0 and 1 (1 and 2 draws); the word is discarded
       if (t[k].valid && (s >= 4 || (uint32_t)e < s)) {
-        const uint32_t j = coord_of(ws[e], (uint32_t)g.d);
+        const uint32_t j = g.wor ? wor_coord(w[k], g.wor_hb, (uint32_t)g.d, s + 4u * t[k].blk + (uint32_t)e)
+                                 : coord_of(ws[e], (uint32_t)g.d);
         const int diff = (int)__ldg(t[k].xr + j) - (int)__ldg(t[k].qr + j);
         a += (uint32_t)(diff * diff);
       }
     }
     acc[k] = a;
   }
+}
+
+// Without replacement: the draws 4 blk0 .. 4 (blk0 + ADV_P) - 1 of the level are
+// pi(2^c + u) under the arm's keys kk (reading R23).
+__device__ __forceinline__ uint32_t draw4_pair_wor(const Geom &g, const uint8_t *__restrict__ xr,
+                                                   const uint8_t *__restrict__ qr, uint4 kk, uint32_t lv,
+                                                   uint32_t blk0) {
+  const uint32_t t0 = (1u << (lv - 1u)) + 4u * blk0;
+  uint32_t acc = 0;
+#pragma unroll
+  for (int e = 0; e < 4 * ADV_P; ++e) {
+    const uint32_t j = wor_coord(kk, g.wor_hb, (uint32_t)g.d, t0 + (uint32_t)e);
+    const int diff = (int)__ldg(xr + j) - (int)__ldg(qr + j);
+    acc += (uint32_t)(diff * diff);
+  }
+  return acc;
 }
 
 // ADV_P consecutive Philox blocks blk0.. of ONE pair (all 4 draws of each used: s >= 4).
@@ -697,7 +722,12 @@ __global__ void __launch_bounds__(ADV_NT) k_advance(Geom g) {
           __shfl_sync(FULL, reinterpret_cast<unsigned long long>(g.Q + (size_t)qi * g.pitch), lane));
       if (ok) {
         const uint32_t gi = i + g.id_offset, gq = rng_qi(g, qi), lv = (uint32_t)(c + 1);
-        for (unsigned b0 = sub * ADV_P; b0 < nb; b0 += tpp * ADV_P) sum += draw4_pair(g, xr, qr, gi, gq, lv, b0);
+        if (g.wor) {
+          const uint4 kk = wor_keys(g.rk0, g.rk1, gi, gq);
+          for (unsigned b0 = sub * ADV_P; b0 < nb; b0 += tpp * ADV_P) sum += draw4_pair_wor(g, xr, qr, kk, lv, b0);
+        } else {
+          for (unsigned b0 = sub * ADV_P; b0 < nb; b0 += tpp * ADV_P) sum += draw4_pair(g, xr, qr, gi, gq, lv, b0);
+        }
       }
       for (unsigned o = tpp >> 1; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
       if (ok && sub == 0) commit(g, qi, i, sum, newlvl);
@@ -760,7 +790,17 @@ __global__ void __launch_bounds__(ADV_NT) k_advance_staged(Geom g) {
     const uint8_t *qr = g.Q + (size_t)qi * g.pitch;
     const uint32_t gi = i + g.id_offset, gq = rng_qi(g, qi), lv = (uint32_t)(c + 1);
     uint32_t sum = 0;
-    for (unsigned b0 = lane * ADV_P; b0 < nb; b0 += 32 * ADV_P) sum += draw4_pair_srow(g, sxb, qr, gi, gq, lv, b0);
+    if (g.wor) {  // reading R23: pi(2^c + u) under the arm's keys
+      const uint4 kk = wor_keys(g.rk0, g.rk1, gi, gq);
+      const uint32_t t0 = 1u << c;
+      for (unsigned u = lane; u < (1u << c); u += 32) {
+        const uint32_t j = wor_coord(kk, g.wor_hb, (uint32_t)g.d, t0 + u);
+        const int diff = (int)sxb[j] - (int)__ldg(qr + j);
+        sum += (uint32_t)(diff * diff);
+      }
+    } else {
+      for (unsigned b0 = lane * ADV_P; b0 < nb; b0 += 32 * ADV_P) sum += draw4_pair_srow(g, sxb, qr, gi, gq, lv, b0);
+    }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
     if (lane == 0) commit(g, qi, i, sum, (uint8_t)(c + 1));
@@ -814,7 +854,7 @@ __global__ void __launch_bounds__(OUT_NT) k_output(Geom g, OutPtrs o) {
   if (threadIdx.x == 0) {
     const size_t row = (size_t)(o.row0 + qi);
     if (o.draws) o.draws[row] = st.draws;
-    if (o.evals) o.evals[row] = st.draws + (long long)g.d * st.nexact;
+    if (o.evals) o.evals[row] = st.draws + st.exact_evals;
     if (o.rounds) o.rounds[row] = st.rounds;
   }
 }
@@ -826,13 +866,17 @@ __global__ void __launch_bounds__(OUT_NT) k_output(Geom g, OutPtrs o) {
 // max(1, 2^(c-2)) per advance.
 __global__ void __launch_bounds__(256) k_tally(Geom g) {
   const int qi = blockIdx.x;
-  unsigned long long dr = 0, ex = 0, bl = 0;
+  unsigned long long dr = 0, ex = 0, bl = 0, xe = 0;
   const uint8_t *lrow = g.lvl + (size_t)qi * g.npad;
   for (int i = threadIdx.x; i < g.n; i += blockDim.x) {
     const uint8_t l = lrow[i];
     const uint32_t c = l & 0x7Fu;
     dr += 1ull << c;
-    ex += (lvl_exact(l) && g.d > 1) ? 1u : 0u;
+    const bool fb = lvl_exact(l) && g.d > 1;
+    ex += fb ? 1u : 0u;
+    // charge of the fallback: d, or without replacement the d - 2^c coordinates the
+    // arm's permutation had not drawn yet (reading R23)
+    xe += fb ? (g.wor ? (unsigned long long)g.d - (1ull << c) : (unsigned long long)g.d) : 0ull;
     bl += c == 0 ? 0ull : (c == 1 ? 1ull : (1ull << (c - 2)) + 1ull);
   }
 #pragma unroll
@@ -840,12 +884,14 @@ __global__ void __launch_bounds__(256) k_tally(Geom g) {
     dr += __shfl_xor_sync(FULL, dr, o);
     ex += __shfl_xor_sync(FULL, ex, o);
     bl += __shfl_xor_sync(FULL, bl, o);
+    xe += __shfl_xor_sync(FULL, xe, o);
   }
-  __shared__ unsigned long long red[3][8];
+  __shared__ unsigned long long red[4][8];
   if (lane_id() == 0) {
     red[0][threadIdx.x >> 5] = dr;
     red[1][threadIdx.x >> 5] = ex;
     red[2][threadIdx.x >> 5] = bl;
+    red[3][threadIdx.x >> 5] = xe;
   }
   __syncthreads();
   if (threadIdx.x == 0) {
@@ -853,9 +899,11 @@ __global__ void __launch_bounds__(256) k_tally(Geom g) {
       dr += red[0][w];
       ex += red[1][w];
       bl += red[2][w];
+      xe += red[3][w];
     }
     g.qs[qi].draws = (long long)dr;
     g.qs[qi].nexact = (long long)ex;
+    g.qs[qi].exact_evals = (long long)xe;
     g.qs[qi].blocks = (long long)bl;
   }
 }

@@ -171,14 +171,14 @@ __global__ void __launch_bounds__(MRG_NT) k_merge(Geom g, OutPtrs o) {
   }
 }
 
-// Per-shard counters (draws, evals = draws + d * exact fallbacks), rounds, and the
+// Per-shard counters (draws, evals = draws + the exact fallbacks' charge), rounds, and the
 // optional per-pair counts/sums at this shard's columns.
 __global__ void k_counters_sharded(Geom g, OutPtrs o) {
   const int qi = blockIdx.x * blockDim.x + threadIdx.x;
   if (qi >= g.q) return;
   const QState st = g.qs[qi];
   const size_t row = (size_t)(o.row0 + qi);
-  const long long ev = st.draws + (long long)g.d * st.nexact;
+  const long long ev = st.draws + st.exact_evals;
   if (o.accumulate) {
     if (o.draws) atomicAdd(reinterpret_cast<unsigned long long *>(o.draws + row), (unsigned long long)st.draws);
     if (o.evals) atomicAdd(reinterpret_cast<unsigned long long *>(o.evals + row), (unsigned long long)ev);

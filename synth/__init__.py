@@ -130,3 +130,45 @@ def small_instance(seed: int, n: int, d: int, q: int = 1, kind: str = "mixture",
         return X, Q
     cen = rng.uniform(0.0, 255.0, (centres, d))
     return _mixture_rows(rng, cen, sigma, n), _mixture_rows(rng, cen, sigma, q)
+
+
+# ---------------------------------------------------------------------------
+# §5 workloads.  Each trial is an independent
+# problem: n points and one query drawn from the same generator.
+SEC5 = dict(n=1_000, m=12_288, k=10, h=10, delta=0.001, trials=20, seed=1902)
+SEC5_WORKLOADS = ("p10", "p100", "p1000", "images")
+
+
+def subspace_trial(p: int, trial: int, n: int = SEC5["n"], m: int = SEC5["m"],
+                   seed: int = SEC5["seed"]):
+    """x = c Q y, Q in R^{m x p} i.i.d. Gaussian with unit-norm columns, y uniform
+    on the unit sphere of R^p, c the largest scalar with ||x||_inf <= 1/2 over the
+    generated set (the n points and the query).  Stored as uint8 u = rint(255 (x + 1/2))
+    (reading R22: one sample (u_a - u_b)^2 / 65025 ~ (x_a - x_b)^2, the
+    paper's [0, 1] sample range).  Returns (X uint8 [n, m], q uint8 [1, m])."""
+    rng = np.random.default_rng(np.random.SeedSequence([seed, p, trial]))
+    Qm = rng.standard_normal((m, p))
+    Qm /= np.linalg.norm(Qm, axis=0, keepdims=True)
+    Y = rng.standard_normal((n + 1, p))
+    Y /= np.linalg.norm(Y, axis=1, keepdims=True)
+    Xr = Y @ Qm.T
+    Xr *= 0.5 / np.abs(Xr).max()
+    U = np.clip(np.rint((Xr + 0.5) * 255.0), 0, 255).astype(np.uint8)
+    return np.ascontiguousarray(U[:n]), np.ascontiguousarray(U[n:])
+
+
+def images_trial(trial: int, n: int = SEC5["n"], seed: int = SEC5["seed"]):
+    """Stand-in for P:349's Tiny ImageNet trials (the dataset is not in the container):
+    n + 1 rows of config 3's mixture recipe (its 200 centres, sigma 30, d = 12,288), the
+    last one the query.  Returns (X uint8 [n, d], q uint8 [1, d])."""
+    c3 = config(3)
+    centres = np.random.default_rng(_seqs(c3, 0)[0]).uniform(0.0, 255.0, (c3.centres, c3.d))
+    rows = _mixture_rows(np.random.default_rng(np.random.SeedSequence([seed, 0, trial])), centres, c3.sigma, n + 1)
+    return np.ascontiguousarray(rows[:n]), np.ascontiguousarray(rows[n:])
+
+
+def sec5_trial(workload: str, trial: int, **kw):
+    """One §5 trial of `workload` in SEC5_WORKLOADS."""
+    if workload == "images":
+        return images_trial(trial, **{k: v for k, v in kw.items() if k in ("n", "seed")})
+    return subspace_trial(int(workload[1:]), trial, **kw)

@@ -80,6 +80,9 @@ A1_CASES = [
     ("wide_band", 700, 12, 2, 60, 50, "exp", 0.1, 8, "mixture"),
     # 4000 arms x 25 B > A1_SMEM_MAX: the state lives in the global workspace
     ("global_state", 4000, 4, 2, 3, 3, "exp", 0.01, 9, "mixture"),
+    # the state (600 x 25 B) fits a CTA but not with the alpha / query tables of
+    # d = 9000: global workspace (a launch-mode regression)
+    ("tables_global", 600, 9000, 2, 3, 3, "exp", 0.001, 10, "mixture"),
 ]
 
 
