@@ -478,12 +478,20 @@ def run_ours(args, dist: Dist):
     # (1b) the query-independent-draw variant on the same workload:
     # reported beside the headline, which keeps the per-query streams (R19)
     variant = None
+    variants = {}
     if args.draws == "per-query" and not args.no_variant:
-        vtimes, _, vclk = timed(False, ak.FLAG_SHARED_DRAWS)
-        vms = dist.max(sum(vtimes))
-        variant = {"draws": "shared (AKNN_FLAG_SHARED_DRAWS, DESIGN.md §12)",
-                   "value": total_q / (vms / 1e3), "unit": UNIT, "ms_per_step": vms / args.steps,
-                   "step_ms": [round(t, 3) for t in vtimes], "clocks": vclk}
+        for vname, vflag, vdesc in (
+                ("shared_draws", ak.FLAG_SHARED_DRAWS, "query-independent draws (AKNN_FLAG_SHARED_DRAWS, DESIGN.md §12)"),
+                ("without_replacement", ak.FLAG_WITHOUT_REPLACEMENT,
+                 "per-query draws without replacement (AKNN_FLAG_WITHOUT_REPLACEMENT, DESIGN.md §15)")):
+            vtimes, _, vclk = timed(False, vflag)
+            vms = dist.max(sum(vtimes))
+            vev = int(out["evals"].sum().item())  # sharded: already summed over the shards
+            frac = vev / (qpr * cfg.n * d) if sharded else dist.sum(vev) / (dist.world * qpr * n_loc * d)
+            variants[vname] = {"what": vdesc, "value": total_q / (vms / 1e3), "unit": UNIT,
+                               "ms_per_step": vms / args.steps, "step_ms": [round(t, 3) for t in vtimes],
+                               "sample_fraction": frac, "clocks": vclk}
+        variant = dict(variants["shared_draws"], draws="shared (AKNN_FLAG_SHARED_DRAWS, DESIGN.md §12)")
     # (2) the same steps with per-launch CUDA events (host-driven loop) for the roofline
     itimes, stats, _ = timed(True)
     ms_local_instr = sum(itimes)
@@ -686,6 +694,7 @@ def run_ours(args, dist: Dist):
             "gpu_launches": gpu_launches, "gpu_launches_per_step": gpu_launches / args.steps,
             "step_ms": [round(t, 3) for t in times],
             "variant_shared_draws": variant,
+            "variants": variants or None,
             **extra,
         }
         print(json.dumps(line), flush=True)
