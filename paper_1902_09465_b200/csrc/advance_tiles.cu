@@ -66,8 +66,8 @@ __device__ __forceinline__ uint32_t sq_diff4(uint32_t xa, uint32_t qa, uint4 w, 
 // Without replacement (reading R23): the draws t0 .. t0 + 3 are pi(t) under the keys w.
 __device__ __forceinline__ uint32_t sq_diff4_wor(uint32_t xa, uint32_t qa, uint4 w, uint32_t hb, uint32_t d,
                                                  uint32_t t0, uint32_t acc) {
-  return sq_diff4_j(xa, qa, wor_coord(w, hb, d, t0), wor_coord(w, hb, d, t0 + 1u), wor_coord(w, hb, d, t0 + 2u),
-                    wor_coord(w, hb, d, t0 + 3u), acc);
+  const uint4 j = wor_coords4(w, hb, d, t0);
+  return sq_diff4_j(xa, qa, j.x, j.y, j.z, j.w, acc);
 }
 
 // ---------------------------------------------------------------------------

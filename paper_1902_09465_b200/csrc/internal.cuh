@@ -212,6 +212,23 @@ __device__ __forceinline__ uint32_t wor_feistel(uint4 w, uint32_t hb, uint32_t x
   }
   return (L << hb) | R;
 }
+// Four consecutive draws t0 .. t0 + 3 of one arm: the four first encryptions are
+// independent chains (ILP); only values >= d walk further.
+__device__ __forceinline__ uint4 wor_coords4(uint4 w, uint32_t hb, uint32_t d, uint32_t t0) {
+  uint32_t x[4];
+#pragma unroll
+  for (int e = 0; e < 4; ++e) x[e] = wor_feistel(w, hb, t0 + (uint32_t)e);
+#pragma unroll
+  for (int e = 0; e < 4; ++e)
+    while (x[e] >= d) x[e] = wor_feistel(w, hb, x[e]);
+  const uint32_t b = coord_of(w.x ^ w.z, d);
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    x[e] += b;
+    x[e] = x[e] >= d ? x[e] - d : x[e];
+  }
+  return make_uint4(x[0], x[1], x[2], x[3]);
+}
 __device__ __forceinline__ uint32_t wor_coord(uint4 w, uint32_t hb, uint32_t d, uint32_t t) {
   uint32_t x = t;
   do {

@@ -537,10 +537,14 @@ __device__ __forceinline__ uint32_t draw4_pair_wor(const Geom &g, const uint8_t 
   const uint32_t t0 = (1u << (lv - 1u)) + 4u * blk0;
   uint32_t acc = 0;
 #pragma unroll
-  for (int e = 0; e < 4 * ADV_P; ++e) {
-    const uint32_t j = wor_coord(kk, g.wor_hb, (uint32_t)g.d, t0 + (uint32_t)e);
-    const int diff = (int)__ldg(xr + j) - (int)__ldg(qr + j);
-    acc += (uint32_t)(diff * diff);
+  for (int k = 0; k < ADV_P; ++k) {
+    const uint4 j4 = wor_coords4(kk, g.wor_hb, (uint32_t)g.d, t0 + 4u * (uint32_t)k);
+    const uint32_t js[4] = {j4.x, j4.y, j4.z, j4.w};
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const int diff = (int)__ldg(xr + js[e]) - (int)__ldg(qr + js[e]);
+      acc += (uint32_t)(diff * diff);
+    }
   }
   return acc;
 }
@@ -792,11 +796,15 @@ __global__ void __launch_bounds__(ADV_NT) k_advance_staged(Geom g) {
     uint32_t sum = 0;
     if (g.wor) {  // reading R23: pi(2^c + u) under the arm's keys
       const uint4 kk = wor_keys(g.rk0, g.rk1, gi, gq);
-      const uint32_t t0 = 1u << c;
-      for (unsigned u = lane; u < (1u << c); u += 32) {
-        const uint32_t j = wor_coord(kk, g.wor_hb, (uint32_t)g.d, t0 + u);
-        const int diff = (int)sxb[j] - (int)__ldg(qr + j);
-        sum += (uint32_t)(diff * diff);
+      const uint32_t t0 = 1u << c;  // staged levels draw >= 64 per pair: 4 per lane step
+      for (unsigned u = 4 * lane; u < (1u << c); u += 128) {
+        const uint4 j4 = wor_coords4(kk, g.wor_hb, (uint32_t)g.d, t0 + u);
+        const uint32_t js[4] = {j4.x, j4.y, j4.z, j4.w};
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          const int diff = (int)sxb[js[e]] - (int)__ldg(qr + js[e]);
+          sum += (uint32_t)(diff * diff);
+        }
       }
     } else {
       for (unsigned b0 = lane * ADV_P; b0 < nb; b0 += 32 * ADV_P) sum += draw4_pair_srow(g, sxb, qr, gi, gq, lv, b0);

@@ -51,11 +51,22 @@ __device__ void bitonic_keys(unsigned long long *buf, unsigned P) {
     }
 }
 
-// fp32 screen for the arg-min of L = d_hat - alpha over the arms outside the buffer:
-// Lf = S * inv(65025 T) - alpha in fp32 differs from the fp64 L by less than
-// eps_c = (alpha_c + 2) * 2^-20 (d_hat <= 1 because every sample is <= 1; each fp32
-// rounding is a relative 2^-24), so an arm with Lf - eps_c > (best L so far) cannot be
-// the arg-min and skips the fp64 division; the rest are decided in fp64 as before.
+// Per-level table of the streaming pass (one 16-byte shared-memory load per arm):
+//   key <= tau   as integer tests on S (no 64-bit key per arm): with Kt = tau >> kbits,
+//                S * mul_c < Kt  <=>  S < ceil(Kt / mul_c) = lt, and S * mul_c == Kt <=>
+//                S == Kt / mul_c = eq when mul_c divides Kt (else eq = -1), in which case
+//                the id decides (gid <= tau's id);
+//   fp32 screen  for the arg-min of L = d_hat - alpha over the arms outside the buffer:
+//                r = fma(S, inv(65025 T), -(alpha_c + eps_c)) in fp32 differs from
+//                S / (65025 T) - alpha - eps_c by less than (alpha_c + 2) 2^-23 (d_hat <= 1:
+//                every sample is <= 1; each fp32 rounding is a relative 2^-24), and
+//                eps_c = (alpha_c + 2) 2^-20 exceeds that, so r > bound (rounded up to
+//                fp32) proves L > bound: such an arm cannot be the arg-min and skips the
+//                fp64 division; the rest are decided in fp64 as before.
+struct PivLevel {
+  int32_t lt, eq;  // key <= tau  <=>  S < lt  ||  (S == eq && gid <= id(tau))
+  float invT, nae;  // 1 / (65025 T) and -(alpha + eps) in fp32
+};
 
 // Fills buf[0..cnt) with every key <= tau (unsorted) and rank[t] = the rank of buf[t]
 // among them (0-based; keys are unique), and returns the arg-min of L over the arms
@@ -66,16 +77,9 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
   __shared__ unsigned cnt;
   __shared__ unsigned long long tau_s;
   __shared__ unsigned long long wmin[PIV_NT / 32];
-  __shared__ float invT[MAX_LEVELS + 1], alf[MAX_LEVELS + 1], epsl[MAX_LEVELS + 1];
+  __shared__ PivLevel lvt[MAX_LEVELS + 1];
   const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   const int n = g.n;
-  if (tid <= MAX_LEVELS) {
-    const bool ex = tid == MAX_LEVELS;  // slot MAX_LEVELS: exact arms (T = d, alpha = 0)
-    const double T = ex ? (double)g.d : (double)(1u << tid);
-    invT[tid] = (float)(1.0 / (T * 65025.0));
-    alf[tid] = (ex || tid > g.cmax) ? 0.f : (float)g.alpha[1u << tid];
-    epsl[tid] = (alf[tid] + 2.f) * 9.5367431640625e-07f;  // 2^-20
-  }
   if (n > (int)PIV_CAP) {
     // tau = the (rs+1)-th smallest of ss strided sample keys, rs+1 about twice the
     // expected sample rank of need, plus 8: found by rs+1 rounds of block arg-min
@@ -122,43 +126,65 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
   if (tid == 0) cnt = 0;
   __syncthreads();
   const unsigned long long tau = tau_s;
+  if (tid <= MAX_LEVELS) {
+    const bool ex = tid == MAX_LEVELS;  // slot MAX_LEVELS: exact arms (T = d, alpha = 0)
+    const double T = ex ? (double)g.d : (double)(1u << tid);
+    const unsigned long long mul = ex ? g.Ld : (g.L >> tid), Kt = tau >> g.kbits;
+    const unsigned long long qt = Kt / mul, rt = Kt % mul, lt = qt + (rt != 0);
+    const float alf = (ex || tid > g.cmax) ? 0.f : (float)g.alpha[1u << tid];
+    const float eps = (alf + 2.f) * 9.5367431640625e-07f;  // 2^-20
+    PivLevel v;
+    v.lt = lt > 0x7fffffffull ? 0x7fffffff : (int32_t)lt;
+    v.eq = (rt == 0 && qt <= 0x7fffffffull) ? (int32_t)qt : -1;
+    v.invT = (float)(1.0 / (T * 65025.0));
+    v.nae = -__fadd_ru(alf, eps);
+    lvt[tid] = v;
+  }
+  __syncthreads();
+  const uint32_t idt = (uint32_t)(tau & ((1ull << g.kbits) - 1ull));
+  const uint32_t gid0 = g.id_offset;
+  const int32_t *Srow = g.S + (size_t)qi * g.npad;
+  const uint8_t *Lrow = g.lvl + (size_t)qi * g.npad;
   RecBest bl{1.0e300, 0xffffffffu, 0, 0};
-  double bound = 1.0e300;  // min L seen by the warp so far: the screen's bound
+  float boundf = __int_as_float(0x7f800000);  // warp's min L so far, rounded up to fp32
   constexpr int U = 4;  // arm groups in flight per thread (the pass is load-latency bound)
   for (int wb0 = (tid - lane) * 4; wb0 < n; wb0 += PIV_NT * 4 * U) {  // warp-uniform trips
     const int b0 = wb0 + lane * 4;
-    Arm4 ag[U];
+    int4 sg[U];
+    uint32_t lg[U];
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i0 = b0 + u * PIV_NT * 4;
-      if (i0 < n) ag[u] = load_arm4(g, qi, i0);
+      if (i0 < n) {
+        sg[u] = *reinterpret_cast<const int4 *>(Srow + i0);
+        lg[u] = *reinterpret_cast<const uint32_t *>(Lrow + i0);
+      }
     }
 #pragma unroll
     for (int u = 0; u < U; ++u) {
-    const int i0 = b0 + u * PIV_NT * 4;
-    const Arm4 &a = ag[u];
+      const int i0 = b0 + u * PIV_NT * 4;
+      const int32_t Sv[4] = {sg[u].x, sg[u].y, sg[u].z, sg[u].w};
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const int i = i0 + e;
-      if (i >= n) break;
-      const unsigned long long key = arm_key(a.S[e], a.l[e], (uint32_t)i, g);
-      if (key <= tau) {
-        const unsigned p = atomicAdd(&cnt, 1u);
-        if (p < PIV_CAP) buf[p] = key;
-      } else {
-        const int li = lvl_exact(a.l[e]) ? MAX_LEVELS : a.l[e];
-        const float lf = __fsub_rn(__fmul_rn((float)a.S[e], invT[li]), alf[li]);
-        if ((double)__fsub_rn(lf, epsl[li]) <= bound) {  // could be the arg-min: decide in fp64
-          const RecBest c{lower_of(a.S[e], a.l[e], g.d, g.alpha), (uint32_t)i + g.id_offset, a.S[e], a.l[e]};
+      for (int e = 0; e < 4; ++e) {
+        const int i = i0 + e;
+        if (i >= n) break;
+        const uint32_t l = (lg[u] >> (8 * e)) & 0xFFu;
+        const int32_t S = Sv[e];
+        const PivLevel v = lvt[(l & LVL_EXACT) ? MAX_LEVELS : l];
+        const uint32_t gid = (uint32_t)i + gid0;
+        if (S < v.lt || (S == v.eq && gid <= idt)) {  // key <= tau
+          const unsigned p = atomicAdd(&cnt, 1u);
+          if (p < PIV_CAP) buf[p] = arm_key(S, (uint8_t)l, (uint32_t)i, g);
+        } else if (!(__fmaf_rn((float)S, v.invT, v.nae) > boundf)) {  // could be the arg-min
+          const RecBest c{lower_of(S, (uint8_t)l, g.d, g.alpha), gid, S, (uint8_t)l};
           if (better_min(c, bl)) bl = c;
         }
       }
     }
-    }
     double wb = bl.v;  // share the warp's best: an arm above it cannot be the arg-min
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) wb = fmin(wb, __shfl_xor_sync(FULL, wb, o));
-    bound = wb;
+    boundf = __double2float_ru(wb);
   }
   __syncthreads();
   const unsigned c = cnt;
