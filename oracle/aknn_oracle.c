@@ -114,20 +114,28 @@ uint32_t orc_draw_index(uint64_t seed, uint32_t qi, uint32_t i, int64_t t, uint3
 /* coordinate pi(t) of a permutation pi of [0, d) keyed per arm:              */
 /*   w = the Philox4x32-10 block of counter (0, i, qi, 0x80000000) under the  */
 /*       seed (a level word no draw uses);                                    */
-/*   E = a balanced 8-round Feistel network on 2*hb bits (the smallest        */
-/*       hb >= 1 with 2^(2 hb) >= d), round r: (L, R) -> (R, L ^ F_r(R)),     */
-/*       F_r(R) = the top hb bits of g((R xor k_r) * 0x9E3779B1 mod 2^32),    */
+/*   E = a 6-round mixed-radix Feistel network on Z_a x Z_b, a = ceil(sqrt d),*/
+/*       b = ceil(d / a) (so d <= a b < d + a): x = L b + R with L in Z_a,    */
+/*       R in Z_b; round r maps (L, R) in Z_m x Z_m' to                       */
+/*       (R, (L + F_r(R, m)) mod m) in Z_m' x Z_m, m = a for even r, b for    */
+/*       odd r (each round is invertible, six rounds return to Z_a x Z_b);    */
+/*       F_r(R, m) = floor(g((R xor k_r) * 0x9E3779B1 mod 2^32) * m / 2^32),  */
 /*       g(h) = (h xor (h >> 16)) * 0x85EBCA6B mod 2^32,                      */
 /*       k_r = w[r mod 4] + r * 0x9E3779B9 mod 2^32;                          */
-/*   rho(t) = E^m(t) for the smallest m >= 1 with E^m(t) < d (cycle walking:  */
-/*       a permutation of a superset restricted this way permutes [0, d));    */
-/*   pi(t) = (rho(t) + b) mod d, b = floor((w0 xor w2) * d / 2^32) (a uniform */
-/*       rotation: the position of every t is uniform over keys).             */
+/*   rho(t) = E^m(t) for the smallest m >= 1 with E^m(t) < d (cycle walking;  */
+/*       needed only when a b > d, with probability < 1/b per step);          */
+/*   pi(t) = (rho(t) + rot) mod d, rot = floor((w0 xor w2) * d / 2^32) (a    */
+/*       uniform rotation: the position of every t is uniform over keys).     */
+/* (An earlier power-of-two domain walked with probability up to 3/4 per      */
+/* step; on the GPU the walk diverges inside a warp, so the domain is now the */
+/* tight a x b one.)                                                          */
 /* ------------------------------------------------------------------------ */
-uint32_t orc_wor_half_bits(uint32_t d) {
-  uint32_t hb = 1;
-  while (((uint64_t)1 << (2 * hb)) < (uint64_t)d) ++hb;
-  return hb;
+/* a = ceil(sqrt(d)), b = ceil(d / a).                                        */
+void orc_wor_radix(uint32_t d, uint32_t *a, uint32_t *b) {
+  uint32_t r = 1;
+  while (r * r < d) ++r;
+  *a = r;
+  *b = (d + r - 1) / r;
 }
 
 void orc_wor_keys(uint64_t seed, uint32_t qi, uint32_t i, uint32_t keys[4]) {
@@ -136,29 +144,32 @@ void orc_wor_keys(uint64_t seed, uint32_t qi, uint32_t i, uint32_t keys[4]) {
   orc_philox4x32_10(ctr, key, keys);
 }
 
-uint32_t orc_feistel(const uint32_t keys[4], uint32_t hb, uint32_t x) {
-  const uint32_t mask = (1u << hb) - 1u;
-  uint32_t L = x >> hb, R = x & mask;
-  for (uint32_t r = 0; r < 8; ++r) {
+uint32_t orc_feistel(const uint32_t keys[4], uint32_t a, uint32_t b, uint32_t x) {
+  uint32_t L = x / b, R = x % b, m = a, m2 = b;
+  for (uint32_t r = 0; r < 6; ++r) {
     const uint32_t kr = keys[r & 3u] + r * 0x9E3779B9u;
-    uint32_t f = (R ^ kr) * 0x9E3779B1u;
-    f = (f ^ (f >> 16)) * 0x85EBCA6Bu;
-    f >>= 32u - hb;
-    const uint32_t newL = R;
-    R = L ^ f;
-    L = newL;
+    uint32_t h = (R ^ kr) * 0x9E3779B1u;
+    h = (h ^ (h >> 16)) * 0x85EBCA6Bu;
+    const uint32_t f = (uint32_t)(((uint64_t)h * m) >> 32);
+    const uint32_t nr = (L + f) % m;
+    L = R;
+    R = nr;
+    const uint32_t t = m;  /* the halves swap roles */
+    m = m2;
+    m2 = t;
   }
-  return (L << hb) | R;
+  return L * b + R;
 }
 
 uint32_t orc_wor_index(const uint32_t keys[4], uint32_t d, uint32_t t) {
-  const uint32_t hb = orc_wor_half_bits(d);
+  uint32_t a, b;
+  orc_wor_radix(d, &a, &b);
   uint32_t x = t;
   do {
-    x = orc_feistel(keys, hb, x);
+    x = orc_feistel(keys, a, b, x);
   } while (x >= d);
-  const uint32_t b = orc_lemire(keys[0] ^ keys[2], d);
-  return x + b >= d ? x + b - d : x + b;
+  const uint32_t rot = orc_lemire(keys[0] ^ keys[2], d);
+  return x + rot >= d ? x + rot - d : x + rot;
 }
 
 /* pi(0..d-1) of arm (qi, i), for the pins (a bijection of [0, d)).          */

@@ -56,11 +56,10 @@ def lib():
                                    C.c_int32, P, P, P, P, P, P, P]
         L.orc_query_a1.argtypes = [P, C.c_int64, C.c_int32, P, C.c_int32, C.c_int32,
                                    C.c_int32, C.c_uint64, P, C.c_int64, C.c_int32, P, P, P, P, P, P]
-        L.orc_wor_half_bits.restype = C.c_uint32
-        L.orc_wor_half_bits.argtypes = [C.c_uint32]
+        L.orc_wor_radix.argtypes = [C.c_uint32, P, P]
         L.orc_wor_keys.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, P]
         L.orc_feistel.restype = C.c_uint32
-        L.orc_feistel.argtypes = [P, C.c_uint32, C.c_uint32]
+        L.orc_feistel.argtypes = [P, C.c_uint32, C.c_uint32, C.c_uint32]
         L.orc_wor_index.restype = C.c_uint32
         L.orc_wor_index.argtypes = [P, C.c_uint32, C.c_uint32]
         L.orc_wor_perm.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, P]
@@ -198,8 +197,11 @@ def query_a1(X, x, k: int, h: int, seed: int, alpha, qi: int = 0, max_iters: int
 
 
 # ---- sampling without replacement (footnote 1 to P:120; reading R23) ----
-def wor_half_bits(d: int) -> int:
-    return int(lib().orc_wor_half_bits(d))
+def wor_radix(d: int):
+    """(a, b) of the mixed-radix Feistel domain Z_a x Z_b: a = ceil(sqrt d), b = ceil(d / a)."""
+    a, b = C.c_uint32(), C.c_uint32()
+    lib().orc_wor_radix(d, C.byref(a), C.byref(b))
+    return a.value, b.value
 
 
 def wor_keys(seed: int, qi: int, i: int) -> np.ndarray:
@@ -208,9 +210,9 @@ def wor_keys(seed: int, qi: int, i: int) -> np.ndarray:
     return k
 
 
-def feistel(keys, hb: int, x: int) -> int:
+def feistel(keys, a: int, b: int, x: int) -> int:
     k = np.ascontiguousarray(keys, np.uint32)
-    return int(lib().orc_feistel(_p(k), hb, x))
+    return int(lib().orc_feistel(_p(k), a, b, x))
 
 
 def wor_index(keys, d: int, t: int) -> int:

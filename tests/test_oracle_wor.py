@@ -23,17 +23,19 @@ def test_permutation_is_a_bijection(d):
         assert np.array_equal(np.sort(p), np.arange(d, dtype=np.uint32))
 
 
-def test_half_bits_is_the_smallest_even_domain():
-    for d in DS:
-        hb = orc.wor_half_bits(d)
-        assert hb >= 1 and 4 ** hb >= d and (hb == 1 or 4 ** (hb - 1) < d)
+def test_radix_domain_is_tight():
+    # a = ceil(sqrt d), b = ceil(d / a): d <= a b < d + a, so cycle walking is rare
+    for d in DS + [2, 7, 99, 33025]:
+        a, b = orc.wor_radix(d)
+        assert (a - 1) ** 2 < d <= a * a and d <= a * b < d + a
 
 
-@pytest.mark.parametrize("hb", [1, 2, 5, 7])
-def test_feistel_is_a_bijection_of_its_domain(hb):  # before the cycle walk and rotation
-    keys = orc.wor_keys(3, 1, 2)
-    img = sorted(orc.feistel(keys, hb, x) for x in range(4 ** hb))
-    assert img == list(range(4 ** hb))
+@pytest.mark.parametrize("d", [2, 6, 17, 40, 784, 1000, 12288])
+def test_feistel_is_a_bijection_of_its_domain(d):  # before the cycle walk and rotation
+    a, b = orc.wor_radix(d)
+    keys = orc.wor_keys(3, 1, d)
+    img = sorted(orc.feistel(keys, a, b, x) for x in range(a * b))
+    assert img == list(range(a * b))
 
 
 def test_keys_are_the_philox_block_of_the_reserved_level():
