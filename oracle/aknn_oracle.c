@@ -392,9 +392,9 @@ int orc_round_step(int64_t n, int32_t d, const int64_t *S, const int32_t *T, int
  */
 int orc_query_br(const uint8_t *X, int64_t n, int32_t d, const uint8_t *Qrows, int32_t q,
                  const int32_t *qids, int64_t id_offset, int32_t k, int32_t h, uint64_t seed,
-                 const double *alpha, int32_t max_rounds, int32_t wor, int32_t *sets,
-                 double *dhat, int32_t *counts, int64_t *sums, int64_t *evals, int64_t *draws,
-                 int32_t *rounds) {
+                 const double *alpha, int32_t max_rounds, int32_t wor, int32_t lead,
+                 int32_t *sets, double *dhat, int32_t *counts, int64_t *sums, int64_t *evals,
+                 int64_t *draws, int32_t *rounds) {
   if (n < 2 || d < 1 || q < 0 || k < 1 || h < 0 || (int64_t)k + h >= n || !alpha || !sets)
     return ORC_EINVAL;
   int64_t *S = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
@@ -428,22 +428,28 @@ int orc_query_br(const uint8_t *X, int64_t n, int32_t d, const uint8_t *Qrows, i
       if (stop) break;                                   /* R4, Eq. (5) */
       if (max_rounds > 0 && r >= max_rounds) { status = ORC_EMAXROUNDS; break; }
       int64_t nact = 0;
-      for (int64_t i = 0; i < n; ++i) {                  /* R6 */
-        if (!act[i]) continue;
-        ++nact;
-        const uint8_t *xi = X + (size_t)i * d;
-        if (2 * (int64_t)T[i] >= d) {
-          /* P:176 exact fallback, taken before the draws that would reach m;
-           * charged d evaluations, or without replacement the d - T
-           * coordinates the permutation had not drawn yet (reading R23)   */
-          S[i] = exact_sq(xi, x, d);
-          ncharge += wor ? (int64_t)d - T[i] : (int64_t)d;
-          T[i] = d;
-        } else {
-          for (int64_t t = T[i]; t < 2 * (int64_t)T[i]; ++t)
-            S[i] += draw_sq(xi, x, seed, qi, (uint32_t)(i + id_offset), t, (uint32_t)d, wor);
-          ndraws += T[i];
-          T[i] *= 2;
+      /* R6: every blocker advances once; with a close-side lead L > 1 (reading
+       * R24) the blockers ranked in C or M this round
+       * advance L - 1 more times (each the same P:176 / doubling step).     */
+      for (int64_t r = 0; r < (int64_t)k + h; ++r) act[order[r]] |= (uint8_t)(act[order[r]] ? 2 : 0);
+      for (int32_t pass = 0; pass < (lead > 1 ? lead : 1); ++pass) {
+        for (int64_t i = 0; i < n; ++i) {
+          if (!act[i] || (pass > 0 && !(act[i] & 2)) || T[i] == d) continue;
+          if (pass == 0) ++nact;
+          const uint8_t *xi = X + (size_t)i * d;
+          if (2 * (int64_t)T[i] >= d) {
+            /* P:176 exact fallback, taken before the draws that would reach m;
+             * charged d evaluations, or without replacement the d - T
+             * coordinates the permutation had not drawn yet (reading R23)   */
+            S[i] = exact_sq(xi, x, d);
+            ncharge += wor ? (int64_t)d - T[i] : (int64_t)d;
+            T[i] = d;
+          } else {
+            for (int64_t t = T[i]; t < 2 * (int64_t)T[i]; ++t)
+              S[i] += draw_sq(xi, x, seed, qi, (uint32_t)(i + id_offset), t, (uint32_t)d, wor);
+            ndraws += T[i];
+            T[i] *= 2;
+          }
         }
       }
       if (nact == 0) { status = ORC_EINTERNAL; break; } /* impossible, §8(c) */

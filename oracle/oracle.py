@@ -53,7 +53,7 @@ def lib():
                                      P, P, P, P, P]
         L.orc_query_br.argtypes = [P, C.c_int64, C.c_int32, P, C.c_int32, P, C.c_int64,
                                    C.c_int32, C.c_int32, C.c_uint64, P, C.c_int32,
-                                   C.c_int32, P, P, P, P, P, P, P]
+                                   C.c_int32, C.c_int32, P, P, P, P, P, P, P]
         L.orc_query_a1.argtypes = [P, C.c_int64, C.c_int32, P, C.c_int32, C.c_int32,
                                    C.c_int32, C.c_uint64, P, C.c_int64, C.c_int32, P, P, P, P, P, P]
         L.orc_wor_radix.argtypes = [C.c_uint32, P, P]
@@ -146,7 +146,7 @@ SHARED_QI = 0xFFFFFFFF  # the counter word of query-independent draws (SURVEY §
 
 def query_br(X, Q, k: int, h: int, seed: int, alpha, qids=None, id_offset: int = 0,
              max_rounds: int = 0, want_counts: bool = True, want_sums: bool = False,
-             shared_draws: bool = False, without_replacement: bool = False):
+             shared_draws: bool = False, without_replacement: bool = False, lead: int = 1):
     """Batched round rule BR, one query at a time.  shared_draws:
     every query's counter word is SHARED_QI, i.e. arm i's t-th coordinate is the same
     for all queries; each query alone is unchanged in law."""
@@ -167,7 +167,7 @@ def query_br(X, Q, k: int, h: int, seed: int, alpha, qids=None, id_offset: int =
         evals=np.zeros(q, np.int64), draws=np.zeros(q, np.int64), rounds=np.zeros(q, np.int32))
     rc = lib().orc_query_br(_p(X), n, d, _p(Q), q, _p(qids), id_offset, k, h,
                             C.c_uint64(seed & (2**64 - 1)), _p(alpha), max_rounds,
-                            1 if without_replacement else 0, _p(out["sets"]), _p(out["dhat"]), _p(out["counts"]),
+                            1 if without_replacement else 0, lead, _p(out["sets"]), _p(out["dhat"]), _p(out["counts"]),
                             _p(out["sums"]), _p(out["evals"]), _p(out["draws"]),
                             _p(out["rounds"]))
     out["status"] = rc
