@@ -79,6 +79,12 @@ typedef struct {
                          pivot select (diagnostics; results are identical);
                          bits 1, 2 (AKNN_FLAG_EXACT_ROWS, AKNN_FLAG_NO_TILES): see
                          below                                                   */
+  int32_t lead;       /* close-side lead L (DESIGN.md
+                         reading R24): 0 or 1 = the batched rule; L > 1 = the
+                         blockers of a round that rank in C or M (ranks 1..k+h)
+                         advance L times (each the doubling / P:176 exact step),
+                         the far blockers once.  1 <= L <= 8 (else EINVAL);
+                         ignored by the Algorithm-1 entry points.              */
 } aknn_opts;
 
 #define AKNN_FLAG_RADIX_SELECT 1

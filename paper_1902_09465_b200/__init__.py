@@ -44,7 +44,7 @@ class Result(C.Structure):
 
 class Opts(C.Structure):
     _fields_ = [("qi_offset", C.c_int32), ("max_rounds", C.c_int32), ("timing", C.c_int32),
-                ("flags", C.c_int32)]
+                ("flags", C.c_int32), ("lead", C.c_int32)]
 
 
 FLAG_RADIX_SELECT = 1
@@ -143,7 +143,7 @@ def alpha_table(n: int, delta: float, d: int, kind: str = "theory", c_alpha: flo
 
 def query_multi(shards, queries, k: int, h: int, delta: float, seed: int = 0, alpha=None, *,
                 counts: bool = True, sums: bool = False, dhat: bool = True, max_rounds: int = 0,
-                qi_offset: int = 0, timing: bool = False, flags: int = 0) -> dict:
+                qi_offset: int = 0, timing: bool = False, flags: int = 0, lead: int = 1) -> dict:
     """aknn_query_multi: one query batch over shard indices on the current device.
 
     ``shards`` are Index objects built with ``Index(rows, n_global=..., offset=...)``
@@ -161,7 +161,7 @@ def query_multi(shards, queries, k: int, h: int, delta: float, seed: int = 0, al
     res = Result(*[_ptr(out[f]) for f, _ in Result._fields_])
     al = None if alpha is None else np.ascontiguousarray(alpha, np.float64)
     arr = (_P * len(shards))(*[s._h for s in shards])
-    opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags)
+    opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags, lead)
     st = _lib.aknn_query_multi(arr, len(shards), _ptr(Q), q, k, h, delta, seed & (2**64 - 1),
                                _ptr(al), C.byref(opts), C.byref(res))
     out["status"] = st
@@ -251,7 +251,7 @@ class Index:
     def query(self, queries, k: int, h: int, delta: float, seed: int = 0, alpha=None, *,
               counts: bool = True, sums: bool = False, dhat: bool = True, max_rounds: int = 0,
               qi_offset: int = 0, timing: bool = False, out: Optional[dict] = None,
-              flags: int = 0, schedule: str = "br") -> dict:
+              flags: int = 0, schedule: str = "br", lead: int = 1) -> dict:
         """aknn_query_ex on host arrays; returns numpy arrays.
 
         ``schedule="a1"`` runs the literal Algorithm 1 instead (aknn_query_a1;
@@ -288,7 +288,7 @@ class Index:
         al = None if alpha is None else np.ascontiguousarray(alpha, np.float64)
         if al is not None and al.shape != (self.d + 1,):
             raise AknnError(AKNN_EINVAL, f"alpha must have d+1={self.d + 1} entries")
-        opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags)
+        opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags, lead)
         fn = _lib.aknn_query_a1 if schedule == "a1" else _lib.aknn_query_ex
         st = fn(self._h, _ptr(Q), q, k, h, delta, seed & (2**64 - 1), _ptr(al), C.byref(opts),
                 C.byref(res))
@@ -301,7 +301,7 @@ class Index:
                      counts: bool = False, sums: bool = False, dhat: bool = True,
                      max_rounds: int = 0, qi_offset: int = 0, timing: bool = False,
                      stream=None, out: Optional[dict] = None, flags: int = 0,
-                     schedule: str = "br") -> dict:
+                     schedule: str = "br", lead: int = 1) -> dict:
         """aknn_query_async on torch CUDA tensors (current stream); returns device tensors.
 
         ``schedule="a1"``: the literal Algorithm 1 (aknn_query_a1_device; waits for the
@@ -327,7 +327,7 @@ class Index:
         if alpha is not None:
             al = alpha if (hasattr(alpha, "is_cuda") and alpha.is_cuda) else \
                 torch.as_tensor(np.ascontiguousarray(alpha, np.float64)).to(dev)
-        opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags)
+        opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags, lead)
         fn = _lib.aknn_query_a1_device if schedule == "a1" else _lib.aknn_query_async
         st = fn(self._h, _ptr(Q), q, k, h, delta, seed & (2**64 - 1), _ptr(al), C.byref(opts),
                 C.byref(res), _stream_ptr(stream))

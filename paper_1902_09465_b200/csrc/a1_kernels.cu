@@ -81,7 +81,7 @@ __device__ __forceinline__ int32_t a1_draw(const A1Geom &g, const uint8_t *x, in
   }
   uint32_t j;
   if (g.wor) {  // reading R23: pi(t) of the arm's permutation
-    j = wor_coord(wor_keys(g.rk0, g.rk1, (uint32_t)i + g.id_offset, qrng), g.wor_hb, (uint32_t)g.d, (uint32_t)t);
+    j = wor_coord(wor_keys(g.rk0, g.rk1, (uint32_t)i + g.id_offset, qrng), g.wor_z, (uint32_t)g.d, (uint32_t)t);
   } else {
     const uint4 w = philox4x32_10_rk(make_uint4(u >> 2, (uint32_t)i + g.id_offset, qrng, b), g.rk0, g.rk1);
     const uint32_t ws[4] = {w.x, w.y, w.z, w.w};

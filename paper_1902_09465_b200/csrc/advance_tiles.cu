@@ -64,9 +64,9 @@ __device__ __forceinline__ uint32_t sq_diff4(uint32_t xa, uint32_t qa, uint4 w, 
 }
 
 // Without replacement (reading R23): the draws t0 .. t0 + 3 are pi(t) under the keys w.
-__device__ __forceinline__ uint32_t sq_diff4_wor(uint32_t xa, uint32_t qa, uint4 w, uint32_t hb, uint32_t d,
-                                                 uint32_t t0, uint32_t acc) {
-  const uint4 j = wor_coords4(w, hb, d, t0);
+__device__ __forceinline__ uint32_t sq_diff4_wor(uint32_t xa, uint32_t qa, uint4 w, const WorRadix &z,
+                                                 uint32_t d, uint32_t t0, uint32_t acc) {
+  const uint4 j = wor_coords4(w, z, d, t0);
   return sq_diff4_j(xa, qa, j.x, j.y, j.z, j.w, acc);
 }
 
@@ -408,10 +408,10 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
               if (wor) {  // draws t = s + 4 blk + e, e < min(s, 4)
                 const uint32_t t0 = s + 4u * ((uint32_t)k & (nb - 1));
                 if (s >= 4) {
-                  sum = sq_diff4_wor(xa, qa, w[k], g.wor_hb, d, t0, sum);
+                  sum = sq_diff4_wor(xa, qa, w[k], g.wor_z, d, t0, sum);
                 } else {
-                  sum += sq_diff(xa, qa, wor_coord(w[k], g.wor_hb, d, t0));
-                  if (s == 2) sum += sq_diff(xa, qa, wor_coord(w[k], g.wor_hb, d, t0 + 1u));
+                  sum += sq_diff(xa, qa, wor_coord(w[k], g.wor_z, d, t0));
+                  if (s == 2) sum += sq_diff(xa, qa, wor_coord(w[k], g.wor_z, d, t0 + 1u));
                 }
               } else if (s >= 4) {
                 sum = sq_diff4(xa, qa, w[k], d, sum);
@@ -444,7 +444,7 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
             const uint4 kk = wor_keys(g.rk0, g.rk1, gi, gq);
             for (unsigned b0 = sub * ADV_TP; b0 < nb; b0 += tpp * ADV_TP) {
 #pragma unroll
-              for (int k = 0; k < ADV_TP; ++k) sum = sq_diff4_wor(xa, qa, kk, g.wor_hb, d, s + 4u * (b0 + k), sum);
+              for (int k = 0; k < ADV_TP; ++k) sum = sq_diff4_wor(xa, qa, kk, g.wor_z, d, s + 4u * (b0 + k), sum);
             }
           } else if (ok) {
             for (unsigned b0 = sub * ADV_TP; b0 < nb; b0 += tpp * ADV_TP) {

@@ -322,7 +322,7 @@ void setup_tiles(Geom &g, const TileShape &t, const aknn_opts &o, int64_t qb, ui
 size_t lvcnt_bytes(int64_t qb, int64_t npad);  // (below)
 
 template <class Timer>
-cudaError_t launch_round_body(const Geom &g, int num_sms, cudaStream_t st, Timer &&timer) {
+cudaError_t launch_round_pass(const Geom &g, int num_sms, cudaStream_t st, Timer &timer) {
   timer(0);
   cudaError_t e = cudaSuccess;
   if (g.level_mma) e = cudaMemsetAsync(g.lvcnt, 0, lvcnt_bytes(g.q, g.npad), st);
@@ -335,6 +335,22 @@ cudaError_t launch_round_body(const Geom &g, int num_sms, cudaStream_t st, Timer
   if (e == cudaSuccess && g.tile_on) e = launch_advance_tiles(g, num_sms, st);
   if (e == cudaSuccess && g.level_mma) e = launch_level_mma(g, st);
   timer(4);
+  return e;
+}
+
+// One round's advances: every blocker once, then (close-side lead L > 1, reading R24)
+// L - 1 lead passes in which the blockers ranked in C or M advance again.
+template <class Timer>
+cudaError_t launch_round_body(const Geom &g, int num_sms, cudaStream_t st, Timer &&timer) {
+  cudaError_t e = launch_round_pass(g, num_sms, st, timer);
+  if (g.lead > 1) {
+    Geom gl = g;
+    gl.lead_pass = 1;
+    for (int p = 1; p < g.lead && e == cudaSuccess; ++p) {
+      e = launch_zero_round(g, st);  // the per-pass slot counters
+      if (e == cudaSuccess) e = launch_round_pass(gl, num_sms, st, timer);
+    }
+  }
   return e;
 }
 
@@ -560,11 +576,13 @@ aknn_status loop_graph(aknn_index *ix, const Geom &g, int nbits, int max_rounds,
 
 // Kernel launches per class (for aknn_stats; memset nodes excluded).
 int launches_init_of(const Geom &g) { return 2 + (g.exact_mma ? 1 : 0) + (g.level_mma ? 1 : 0); }  // init, qstate, norms, q^2
-int launches_filter_of(const Geom &) { return 1; }
-int launches_compact_of(const Geom &g) { return 3 + (g.level_mma ? 1 : 0); }  // plan, (w planes,) scatter, list sizes
+// (every pass of a round: with a close-side lead L, L passes and L - 1 counter resets)
+int launches_filter_of(const Geom &g) { return g.lead; }
+int launches_compact_of(const Geom &g) { return (3 + (g.level_mma ? 1 : 0)) * g.lead; }  // plan, (w planes,) scatter, list sizes
 int launches_advance_of(const Geom &g) {
-  return 1 + (g.exact_mma ? 1 : 0) + (g.stage_lo < MAX_LEVELS ? 1 : 0);
+  return (1 + (g.exact_mma ? 1 : 0) + (g.stage_lo < MAX_LEVELS ? 1 : 0)) * g.lead + (g.lead - 1);
 }
+int launches_tiles_of(const Geom &g) { return ((g.tile_on ? 1 : 0) + (g.level_mma ? 1 : 0)) * g.lead; }
 int launches_output_of(const OutPtrs &o) { return 2 + ((o.counts || o.sums) ? 1 : 0); }  // tally, output
 
 // Folds one sub-batch's control block and query states (copied to the host) into
@@ -580,7 +598,7 @@ void fold_batch_stats(aknn_stats &stats, const RoundCtl &ctl_h, const QState *qs
     stats.launches_filter += launches_filter_of(g) * (r - 1);
     stats.launches_compact += launches_compact_of(g) * (r - 1);
     stats.launches_advance += (launches_advance_of(g) + 1) * (r - 1);  // + counter reset
-    stats.launches_tiles += ((g.tile_on ? 1 : 0) + (g.level_mma ? 1 : 0)) * (r - 1);
+    stats.launches_tiles += launches_tiles_of(g) * (r - 1);
     if (ctl_h.n_active > 0 && status) *status = AKNN_EMAXROUNDS;
   }
   if (r > stats.rounds) stats.rounds = r;
@@ -629,6 +647,7 @@ aknn_status finish_pending(aknn_index *ix) {
 aknn_status check_flags(const aknn_opts &o) {
   if ((o.flags & AKNN_FLAG_WITHOUT_REPLACEMENT) && (o.flags & AKNN_FLAG_SHARED_DRAWS))
     return fail(AKNN_EINVAL, "AKNN_FLAG_WITHOUT_REPLACEMENT cannot be combined with AKNN_FLAG_SHARED_DRAWS");
+  if (o.lead < 0 || o.lead > 8) return fail(AKNN_EINVAL, "lead must be in [0, 8] (got %d)", o.lead);
   return AKNN_OK;
 }
 
@@ -678,6 +697,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   const size_t oTw = off; off = round_up(off + tile_ws_bytes(qb, npad, tsh), 256);
   const size_t oThr = off; off = round_up(off + sizeof(int32_t) * THR_STRIDE * (size_t)qb, 256);
   const size_t oLm = off; off = round_up(off + level_ws_bytes(qb, n, npad, ix->pitch, o), 256);
+  const size_t oLead = off; off = round_up(off + (o.lead > 1 ? szL : 0), 256);
   TRY(ix->ws.ensure(off));
 
   Geom g{};
@@ -688,6 +708,8 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   g.S = ix->ws.as<int32_t>(oS);
   g.lvl = ix->ws.as<uint8_t>(oL);
   g.act = ix->ws.as<uint8_t>(oA);
+  g.lead = o.lead > 1 ? o.lead : 1;
+  g.leadb = o.lead > 1 ? ix->ws.as<uint8_t>(oLead) : nullptr;
   g.list = ix->ws.as<uint32_t>(oList);
   g.qs = ix->ws.as<QState>(oQS);
   g.ctl = ix->ws.as<RoundCtl>(oCtl);
@@ -714,7 +736,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   g.force_radix = (o.flags & AKNN_FLAG_RADIX_SELECT) ? 1 : 0;
   g.shared_draws = (o.flags & AKNN_FLAG_SHARED_DRAWS) ? 1 : 0;
   g.wor = (o.flags & AKNN_FLAG_WITHOUT_REPLACEMENT) ? 1 : 0;
-  g.wor_hb = wor_half_bits(d);
+  g.wor_z = wor_radix(d);
   g.stage_lo = stage_level(g.pitch);
   TRY(setup_exact_mma(ix, g, qb, ix->ws.as<uint8_t>(oXm), o, st));
   setup_tiles(g, tsh, o, qb, ix->ws.as<uint8_t>(oTw));
@@ -804,7 +826,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
           tm.stop(PH_TILES);
         }
       }));
-      stats.launches_tiles += (g.tile_on ? 1 : 0) + (g.level_mma ? 1 : 0);
+      stats.launches_tiles += launches_tiles_of(g);
       stats.launches_filter += launches_filter_of(g);
       stats.launches_compact += launches_compact_of(g);
       stats.launches_advance += launches_advance_of(g);
@@ -931,6 +953,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     const size_t oTw = off; off = round_up(off + tile_ws_bytes(qb, npad, tsh), 256);
     const size_t oThr = off; off = round_up(off + sizeof(int32_t) * THR_STRIDE * (size_t)qb, 256);
     const size_t oLm = off; off = round_up(off + level_ws_bytes(qb, ix->n_local, npad, ix->pitch, o), 256);
+    const size_t oLead = off; off = round_up(off + (o.lead > 1 ? szL : 0), 256);
     TRY(ix->ws.ensure(off));
     Geom &g = G[si];
     g = Geom{};
@@ -941,6 +964,8 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     g.S = ix->ws.as<int32_t>(oS);
     g.lvl = ix->ws.as<uint8_t>(oL);
     g.act = ix->ws.as<uint8_t>(oA);
+    g.lead = o.lead > 1 ? o.lead : 1;
+    g.leadb = o.lead > 1 ? ix->ws.as<uint8_t>(oLead) : nullptr;
     g.list = ix->ws.as<uint32_t>(oList);
     g.qs = ix->ws.as<QState>(oQS);
     g.ctl = ix->ws.as<RoundCtl>(oCtl);
@@ -966,7 +991,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     g.force_radix = (o.flags & AKNN_FLAG_RADIX_SELECT) ? 1 : 0;
     g.shared_draws = (o.flags & AKNN_FLAG_SHARED_DRAWS) ? 1 : 0;
     g.wor = (o.flags & AKNN_FLAG_WITHOUT_REPLACEMENT) ? 1 : 0;
-    g.wor_hb = wor_half_bits(d);
+    g.wor_z = wor_radix(d);
     g.stage_lo = stage_level(g.pitch);
     g.world = W;
     g.recv_stride = recv_stride;
@@ -1059,7 +1084,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
       stats.launches_filter += launches_filter_of(G[0]) * (int)nS;
       stats.launches_compact += launches_compact_of(G[0]) * (int)nS;
       stats.launches_advance += launches_advance_of(G[0]) * (int)nS;
-      stats.launches_tiles += ((G[0].tile_on ? 1 : 0) + (G[0].level_mma ? 1 : 0)) * (int)nS;
+      stats.launches_tiles += launches_tiles_of(G[0]) * (int)nS;
       if (r > 1 + 64 * 64) return fail(AKNN_ECUDA, "round loop did not terminate (internal error)");
     }
     if (r > stats.rounds) stats.rounds = r;
@@ -1301,7 +1326,7 @@ aknn_status run_query_a1(aknn_index *ix, const uint8_t *queries_dev, int32_t q, 
   g.ws_per_query = per;
   g.smem = smem ? 1 : 0;
   g.wor = (opts && (opts->flags & AKNN_FLAG_WITHOUT_REPLACEMENT)) ? 1 : 0;
-  g.wor_hb = wor_half_bits(ix->d);
+  g.wor_z = wor_radix(ix->d);
   g.out = OutPtrs{0, 0, ix->n_local, 0, out->sets, out->dhat, out->counts, out->sums,
                   out->evals, out->draws, out->rounds};
   CU(cudaMemsetAsync(g.status, 0, sizeof(int), st));

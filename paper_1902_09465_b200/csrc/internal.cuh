@@ -83,6 +83,11 @@ struct ShardRec {
 };
 
 // Everything a round kernel needs, passed by value.
+// Domain Z_a x Z_b of the permutation network of sampling without replacement (R23).
+struct WorRadix {
+  uint32_t a, b, binv;  // binv = ceil(2^32 / b): x / b = umulhi(x, binv) for x < a b (b >= 2)
+};
+
 struct Geom {
   const uint8_t *X;      // [n][pitch] points (zero padded)
   const uint8_t *Q;      // [q][pitch] queries of this batch (zero padded)
@@ -102,8 +107,11 @@ struct Geom {
   uint32_t id_offset;    // global id of local row 0
   uint32_t qi0;          // RNG query index of batch row 0
   int shared_draws;      // 1: query-independent draws: counter word 0xFFFFFFFF
+  int lead;              // close-side lead L (aknn_opts.lead, reading R24): C/M blockers advance L times
+  int lead_pass;         // 1: this filter decides a lead pass (from leadb and the levels reached)
+  uint8_t *leadb;        // [q][npad] 1 = a blocker of this round ranked in C or M (lead > 1 only)
   int wor;               // 1: sampling without replacement (AKNN_FLAG_WITHOUT_REPLACEMENT, R23)
-  uint32_t wor_hb;       //    half width of its Feistel domain (2^(2 hb) >= d)
+  WorRadix wor_z;        //    its Feistel domain Z_a x Z_b
   // shared draws on the tensor cores (exact_mma.cu, k_level_mma)
   int level_mma;         // 1: the round's dominant level runs as integer GEMMs
   uint8_t *q2lo, *q2hi;  // [q][pitch] q_j^2 byte planes
@@ -185,54 +193,61 @@ __device__ __forceinline__ uint32_t coord_of(uint32_t w, uint32_t d) { return __
 
 // ---- Sampling without replacement (AKNN_FLAG_WITHOUT_REPLACEMENT; R23) ----
 // The t-th sample of an arm is pi(t), pi a permutation of [0, d) keyed by the arm's
-// Philox block w of counter (0, i, qi, WOR_LEVEL): rho = an 8-round balanced Feistel
-// network E on 2*hb bits, round r: (L, R) -> (R, L ^ top_hb(g((R ^ k_r) * 0x9E3779B1))),
-// g(h) = (h ^ (h >> 16)) * 0x85EBCA6B, k_r = w[r mod 4] + r * 0x9E3779B9, walked until
-// the value is < d; pi(t) = (rho(t) + b) mod d with b = (w.x ^ w.z) mapped onto [0, d).
+// Philox block w of counter (0, i, qi, WOR_LEVEL): rho = a 6-round mixed-radix Feistel
+// network on Z_a x Z_b (a = ceil(sqrt d), b = ceil(d / a); x = L b + R), round r:
+// (L, R) -> (R, (L + F_r(R)) mod m), m = a for even r, b for odd r,
+// F_r(R) = umulhi(g((R ^ k_r) * 0x9E3779B1), m), g(h) = (h ^ (h >> 16)) * 0x85EBCA6B,
+// k_r = w[r mod 4] + r * 0x9E3779B9, walked until the value is < d (rare: a b < d + a);
+// pi(t) = (rho(t) + rot) mod d with rot = (w.x ^ w.z) mapped onto [0, d).
 constexpr uint32_t WOR_LEVEL = 0x80000000u;  // a level word no draw uses
-__host__ inline uint32_t wor_half_bits(int d) {
-  uint32_t hb = 1;
-  while ((1ull << (2 * hb)) < (unsigned long long)d) ++hb;
-  return hb;
+__host__ inline WorRadix wor_radix(int d) {
+  uint32_t r = 1;
+  while (r * r < (uint32_t)d) ++r;
+  WorRadix w;
+  w.a = r;
+  w.b = ((uint32_t)d + r - 1) / r;
+  w.binv = w.b >= 2 ? (uint32_t)(((1ull << 32) + w.b - 1) / w.b) : 0u;
+  return w;
 }
 __device__ __forceinline__ uint4 wor_keys(const uint32_t *rk0, const uint32_t *rk1, uint32_t gi, uint32_t gq) {
   return philox4x32_10_rk(make_uint4(0u, gi, gq, WOR_LEVEL), rk0, rk1);
 }
-__device__ __forceinline__ uint32_t wor_feistel(uint4 w, uint32_t hb, uint32_t x) {
-  const uint32_t sh = 32u - hb;
-  uint32_t L = x >> hb, R = x & ((1u << hb) - 1u);
+__device__ __forceinline__ uint32_t wor_feistel(uint4 w, const WorRadix &z, uint32_t x) {
+  uint32_t L = z.b >= 2 ? __umulhi(x, z.binv) : x;
+  uint32_t R = x - L * z.b;
 #pragma unroll
-  for (uint32_t r = 0; r < 8; ++r) {
+  for (uint32_t r = 0; r < 6; ++r) {
+    const uint32_t m = (r & 1u) ? z.b : z.a;
     const uint32_t kw = (r & 3u) == 0 ? w.x : (r & 3u) == 1 ? w.y : (r & 3u) == 2 ? w.z : w.w;
-    uint32_t f = (R ^ (kw + r * 0x9E3779B9u)) * 0x9E3779B1u;
-    f = (f ^ (f >> 16)) * 0x85EBCA6Bu;
-    const uint32_t nl = R;
-    R = L ^ (f >> sh);
-    L = nl;
+    uint32_t h = (R ^ (kw + r * 0x9E3779B9u)) * 0x9E3779B1u;
+    h = (h ^ (h >> 16)) * 0x85EBCA6Bu;
+    uint32_t nr = L + __umulhi(h, m);  // L < m and the map < m: one conditional subtract
+    nr = nr >= m ? nr - m : nr;
+    L = R;
+    R = nr;
   }
-  return (L << hb) | R;
+  return L * z.b + R;
 }
-// Four consecutive draws t0 .. t0 + 3 of one arm: the four first encryptions are
-// independent chains (ILP); only values >= d walk further.
-__device__ __forceinline__ uint4 wor_coords4(uint4 w, uint32_t hb, uint32_t d, uint32_t t0) {
+// Four consecutive draws t0 .. t0 + 3 of one arm (independent chains: ILP).
+__device__ __forceinline__ uint4 wor_coords4(uint4 w, const WorRadix &z, uint32_t d, uint32_t t0) {
   uint32_t x[4];
 #pragma unroll
-  for (int e = 0; e < 4; ++e) x[e] = wor_feistel(w, hb, t0 + (uint32_t)e);
+  for (int e = 0; e < 4; ++e) x[e] = wor_feistel(w, z, t0 + (uint32_t)e);
 #pragma unroll
   for (int e = 0; e < 4; ++e)
-    while (x[e] >= d) x[e] = wor_feistel(w, hb, x[e]);
-  const uint32_t b = coord_of(w.x ^ w.z, d);
+    while (x[e] >= d) x[e] = wor_feistel(w, z, x[e]);
+  const uint32_t rot = coord_of(w.x ^ w.z, d);
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    x[e] += b;
+    x[e] += rot;
     x[e] = x[e] >= d ? x[e] - d : x[e];
   }
   return make_uint4(x[0], x[1], x[2], x[3]);
 }
-__device__ __forceinline__ uint32_t wor_coord(uint4 w, uint32_t hb, uint32_t d, uint32_t t) {
+__device__ __forceinline__ uint32_t wor_coord(uint4 w, const WorRadix &z, uint32_t d, uint32_t t) {
   uint32_t x = t;
   do {
-    x = wor_feistel(w, hb, x);
+    x = wor_feistel(w, z, x);
   } while (x >= d);
   x += coord_of(w.x ^ w.z, d);
   return x >= d ? x - d : x;

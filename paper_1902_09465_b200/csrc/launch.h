@@ -39,7 +39,7 @@ struct A1Geom {
   int *status;           // bit 0: some query reached max_iters
   int smem;              // 1: state in shared memory (ws_per_query <= A1_SMEM_MAX)
   int wor;               // 1: sampling without replacement (R23)
-  uint32_t wor_hb;
+  WorRadix wor_z;
   OutPtrs out;
 };
 constexpr size_t A1_SMEM_MAX = 96 * 1024;

@@ -35,7 +35,7 @@ __global__ void k_init(Geom g) {
   }
   uint32_t j;
   if (g.wor) {  // pi(0) of the arm's permutation (reading R23)
-    j = wor_coord(wor_keys(g.rk0, g.rk1, (uint32_t)i + g.id_offset, rng_qi(g, (uint32_t)qi)), g.wor_hb,
+    j = wor_coord(wor_keys(g.rk0, g.rk1, (uint32_t)i + g.id_offset, rng_qi(g, (uint32_t)qi)), g.wor_z,
                   (uint32_t)g.d, 0u);
   } else {
     const uint4 w = philox4x32_10(make_uint4(0u, (uint32_t)i + g.id_offset, rng_qi(g, (uint32_t)qi), 0u),
@@ -206,8 +206,8 @@ cudaError_t launch_thresholds(const Geom &g, cudaStream_t s) {
 // Branch-free decision of 4 arms (R5 with the integer thresholds of reading R20):
 // one 16-byte table load per arm, no 64-bit key arithmetic, no floating point.
 __device__ __forceinline__ uint32_t filter_arms(const Geom &g, const int32_t *thr, const Arm4 &a, int i0,
-                                                uint32_t *draws) {
-  uint32_t actw = 0, dr = 0;
+                                                uint32_t *draws, uint32_t *leadw) {
+  uint32_t actw = 0, dr = 0, lw = 0;
   const int4 hdr = __ldg(reinterpret_cast<const int4 *>(thr + THR_LEVEL_INTS));
   const uint32_t mmask = (uint32_t)hdr.x, eqk = (uint32_t)hdr.y, eqkh = (uint32_t)hdr.z;
   const uint32_t idk = (uint32_t)hdr.w, idkh = (uint32_t)__ldg(thr + THR_LEVEL_INTS + 4);
@@ -226,6 +226,26 @@ __device__ __forceinline__ uint32_t filter_arms(const Geom &g, const int32_t *th
     const bool ex = (2u << c) >= (unsigned)g.d;
     const uint32_t act = blk ? (ex ? (uint32_t)ACT_EXACT : c + 1u) : 0u;
     dr += (blk && !ex) ? (1u << c) : 0u;
+    actw |= act << (8 * e);
+    lw |= (blk && !ex && inM) ? (1u << (8 * e)) : 0u;  // inM: ranks 1..k+h (C or M)
+  }
+  *draws = dr;
+  *leadw = lw;
+  return actw;
+}
+
+// A lead pass (reading R24): the arms flagged in leadb advance once more from the
+// level they reached (exact when the next level would reach d).
+__device__ __forceinline__ uint32_t lead_arms(const Geom &g, const Arm4 &a, uint32_t lb, int i0, uint32_t *draws) {
+  uint32_t actw = 0, dr = 0;
+#pragma unroll
+  for (int e = 0; e < 4; ++e) {
+    const uint8_t l = a.l[e];
+    const uint32_t c = l & 15u;
+    const bool go = i0 + e < g.n && ((lb >> (8 * e)) & 0xFFu) && !lvl_exact(l);
+    const bool ex = (2u << c) >= (unsigned)g.d;
+    const uint32_t act = go ? (ex ? (uint32_t)ACT_EXACT : c + 1u) : 0u;
+    dr += (go && !ex) ? (1u << c) : 0u;
     actw |= act << (8 * e);
   }
   *draws = dr;
@@ -287,8 +307,13 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
       if (arms) a1 = load_arm4(g, qi + 2, i0);
     }
     if (cur) continue;  // uniform: one query row at a time
-    uint32_t dr = 0, actw = 0;
-    if (arms) actw = filter_arms(g, g.thr + (size_t)qi * THR_STRIDE, ca, i0, &dr);
+    uint32_t dr = 0, actw = 0, lw = 0;
+    if (g.lead_pass) {
+      if (arms) actw = lead_arms(g, ca, *reinterpret_cast<const uint32_t *>(g.leadb + (size_t)qi * g.npad + i0), i0, &dr);
+    } else {
+      if (arms) actw = filter_arms(g, g.thr + (size_t)qi * THR_STRIDE, ca, i0, &dr, &lw);
+      if (g.lead > 1 && i0 < g.npad) *reinterpret_cast<uint32_t *>(g.leadb + (size_t)qi * g.npad + i0) = lw;
+    }
     if (i0 < g.npad) *reinterpret_cast<uint32_t *>(g.act + (size_t)qi * g.npad + i0) = actw;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -519,7 +544,7 @@ __device__ __forceinline__ void draw_blocks(const Geom &g, const BlockTask (&t)[
     for (int e = 0; e < 4; ++e) {
       // s < 4 only at levels 0 and 1 (1 and 2 draws); the word is discarded
       if (t[k].valid && (s >= 4 || (uint32_t)e < s)) {
-        const uint32_t j = g.wor ? wor_coord(w[k], g.wor_hb, (uint32_t)g.d, s + 4u * t[k].blk + (uint32_t)e)
+        const uint32_t j = g.wor ? wor_coord(w[k], g.wor_z, (uint32_t)g.d, s + 4u * t[k].blk + (uint32_t)e)
                                  : coord_of(ws[e], (uint32_t)g.d);
         const int diff = (int)__ldg(t[k].xr + j) - (int)__ldg(t[k].qr + j);
         a += (uint32_t)(diff * diff);
@@ -538,7 +563,7 @@ __device__ __forceinline__ uint32_t draw4_pair_wor(const Geom &g, const uint8_t 
   uint32_t acc = 0;
 #pragma unroll
   for (int k = 0; k < ADV_P; ++k) {
-    const uint4 j4 = wor_coords4(kk, g.wor_hb, (uint32_t)g.d, t0 + 4u * (uint32_t)k);
+    const uint4 j4 = wor_coords4(kk, g.wor_z, (uint32_t)g.d, t0 + 4u * (uint32_t)k);
     const uint32_t js[4] = {j4.x, j4.y, j4.z, j4.w};
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
@@ -798,7 +823,7 @@ __global__ void __launch_bounds__(ADV_NT) k_advance_staged(Geom g) {
       const uint4 kk = wor_keys(g.rk0, g.rk1, gi, gq);
       const uint32_t t0 = 1u << c;  // staged levels draw >= 64 per pair: 4 per lane step
       for (unsigned u = 4 * lane; u < (1u << c); u += 128) {
-        const uint4 j4 = wor_coords4(kk, g.wor_hb, (uint32_t)g.d, t0 + u);
+        const uint4 j4 = wor_coords4(kk, g.wor_z, (uint32_t)g.d, t0 + u);
         const uint32_t js[4] = {j4.x, j4.y, j4.z, j4.w};
 #pragma unroll
         for (int e = 0; e < 4; ++e) {

@@ -29,8 +29,8 @@ constexpr unsigned PIV_CAP = 8192;    // buffer keys (64 KB of dynamic shared me
 constexpr unsigned PIV_BRUTE = 1536;  // buffers up to this size are ranked by counting
 
 __host__ __device__ __forceinline__ unsigned piv_sample_size(int n) {
-  unsigned ss = 1024;
-  while (ss < PIV_CAP && (int)(ss * 64u) < n) ss <<= 1;
+  unsigned ss = 1024;  // >= n / 16 samples (capped): tau's rank, hence the buffer, stays small
+  while (ss < PIV_CAP && (int)(ss * 16u) < n) ss <<= 1;
   return ss;
 }
 
@@ -77,7 +77,9 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
   __shared__ unsigned cnt;
   __shared__ unsigned long long tau_s;
   __shared__ unsigned long long wmin[PIV_NT / 32];
-  __shared__ PivLevel lvt[MAX_LEVELS + 1];
+  __shared__ double wbnd[PIV_NT / 32];
+  __shared__ double bound0_s;  // min L over the sampled arms with key > tau (screen start)
+  __shared__ __align__(16) PivLevel lvt[MAX_LEVELS + 1];
   const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   const int n = g.n;
   if (n > (int)PIV_CAP) {
@@ -99,10 +101,13 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
     const unsigned expect = (unsigned)(((unsigned long long)need * ss + n - 1) / n);
     const unsigned rounds = 2 * expect + 4;
     unsigned long long t = KEY_INVALID;
-    for (unsigned r = 0; r < rounds; ++r) {
-      unsigned long long m = KEY_INVALID;
+    // the thread's smallest remaining sample; only the owner of a round's minimum
+    // rescans its registers (keys are unique), so a round costs one warp reduction
+    unsigned long long head = KEY_INVALID;
 #pragma unroll
-      for (unsigned u = 0; u < PIV_CAP / PIV_NT; ++u) m = mine[u] < m ? mine[u] : m;
+    for (unsigned u = 0; u < PIV_CAP / PIV_NT; ++u) head = mine[u] < head ? mine[u] : head;
+    for (unsigned r = 0; r < rounds; ++r) {
+      unsigned long long m = head;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         const unsigned long long y = __shfl_xor_sync(FULL, m, o);
@@ -114,14 +119,41 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
 #pragma unroll
       for (int w = 1; w < PIV_NT / 32; ++w) m = wmin[w] < m ? wmin[w] : m;
       t = m;
+      if (head == m) {  // unique keys: exactly one owner
+        head = KEY_INVALID;
 #pragma unroll
-      for (unsigned u = 0; u < PIV_CAP / PIV_NT; ++u)
-        if (mine[u] == m) mine[u] = KEY_INVALID;  // unique keys: exactly one owner
+        for (unsigned u = 0; u < PIV_CAP / PIV_NT; ++u) {
+          if (mine[u] == m) mine[u] = KEY_INVALID;
+          head = mine[u] < head ? mine[u] : head;
+        }
+      }
       __syncthreads();
     }
     if (tid == 0) tau_s = t;
+    // the samples left in `mine` have keys > tau: they are arms outside the buffer, so
+    // their minimum L bounds the outside arg-min from above -- the screen starts there
+    // instead of at +inf (which sent the whole first stretch of arms to fp64)
+    double b = 1.0e300;
+#pragma unroll
+    for (unsigned u = 0; u < PIV_CAP / PIV_NT; ++u) {
+      if (u < per && mine[u] != KEY_INVALID) {
+        const unsigned j = tid + u * PIV_NT;
+        const int i = (int)(((unsigned long long)j * (unsigned)n) / ss);
+        const size_t o = (size_t)qi * g.npad + i;
+        b = fmin(b, lower_of(g.S[o], g.lvl[o], g.d, g.alpha));
+      }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) b = fmin(b, __shfl_xor_sync(FULL, b, o));
+    if (lane == 0) wbnd[warp] = b;
+    __syncthreads();
+    if (tid == 0) {
+      for (int w = 1; w < PIV_NT / 32; ++w) b = fmin(b, wbnd[w]);
+      bound0_s = fmin(b, wbnd[0]);
+    }
   } else if (tid == 0) {
     tau_s = KEY_INVALID - 1;  // every arm
+    bound0_s = 1.0e300;
   }
   if (tid == 0) cnt = 0;
   __syncthreads();
@@ -146,7 +178,7 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
   const int32_t *Srow = g.S + (size_t)qi * g.npad;
   const uint8_t *Lrow = g.lvl + (size_t)qi * g.npad;
   RecBest bl{1.0e300, 0xffffffffu, 0, 0};
-  float boundf = __int_as_float(0x7f800000);  // warp's min L so far, rounded up to fp32
+  float boundf = __double2float_ru(bound0_s);  // min L known so far, rounded up to fp32
   constexpr int U = 4;  // arm groups in flight per thread (the pass is load-latency bound)
   for (int wb0 = (tid - lane) * 4; wb0 < n; wb0 += PIV_NT * 4 * U) {  // warp-uniform trips
     const int b0 = wb0 + lane * 4;
@@ -170,7 +202,12 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
         if (i >= n) break;
         const uint32_t l = (lg[u] >> (8 * e)) & 0xFFu;
         const int32_t S = Sv[e];
-        const PivLevel v = lvt[(l & LVL_EXACT) ? MAX_LEVELS : l];
+        const uint4 vv = reinterpret_cast<const uint4 *>(lvt)[(l & LVL_EXACT) ? MAX_LEVELS : l];
+        PivLevel v;
+        v.lt = (int32_t)vv.x;
+        v.eq = (int32_t)vv.y;
+        v.invT = __uint_as_float(vv.z);
+        v.nae = __uint_as_float(vv.w);
         const uint32_t gid = (uint32_t)i + gid0;
         if (S < v.lt || (S == v.eq && gid <= idt)) {  // key <= tau
           const unsigned p = atomicAdd(&cnt, 1u);
@@ -184,7 +221,7 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
     double wb = bl.v;  // share the warp's best: an arm above it cannot be the arg-min
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) wb = fmin(wb, __shfl_xor_sync(FULL, wb, o));
-    boundf = __double2float_ru(wb);
+    boundf = fminf(boundf, __double2float_ru(wb));
   }
   __syncthreads();
   const unsigned c = cnt;

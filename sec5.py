@@ -16,7 +16,8 @@ reports the median and interquartile range over the trials of
     algorithm's (reading R14).
 Both schedules run on the GPU: "a1" is the literal Algorithm 1 (the paper's own,
 aknn_query_a1, one warp per query; trials in flight concurrently, one index and
-stream each), "br" the batched round rule (aknn_query_ex).  The exact k-NN per trial
+stream each), "br" the batched round rule (aknn_query_ex), "br_lead<L>" the batched rule with a
+close-side lead L (aknn_opts.lead, reading R24).  The exact k-NN per trial
 comes from the exact tensor-core pass (aknn_exact).  The oracle is not used here.
 """
 from __future__ import annotations
@@ -82,10 +83,14 @@ def run(args, dist) -> None:
         _, dist2 = ix.exact(q, k)
         dks[wt] = int(dist2[0, k - 1])
         for c in calphas:
-            if "br" in scheds:
+            for sname in scheds:
+                if not sname.startswith("br"):
+                    continue
+                # "br": the batched rule; "br_lead<L>": with a close-side lead L (reading R24)
+                lead = int(sname[len("br_lead"):]) if sname.startswith("br_lead") else 1
                 t1 = time.perf_counter()
-                r = ix.query(q, k, h, delta, t, alphas[c], counts=False, dhat=False)
-                rows.append(dict(w=w, trial=t, c=c, s="br", recall=_recall(X, q[0], r["sets"][0], dks[wt], k),
+                r = ix.query(q, k, h, delta, t, alphas[c], counts=False, dhat=False, lead=lead)
+                rows.append(dict(w=w, trial=t, c=c, s=sname, recall=_recall(X, q[0], r["sets"][0], dks[wt], k),
                                  fraction=int(r["evals"][0]) / (n * m), rounds=int(r["rounds"][0]),
                                  draws=int(r["draws"][0]), wall_s=time.perf_counter() - t1))
         if "a1" in scheds:

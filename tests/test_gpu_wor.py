@@ -73,8 +73,9 @@ def test_wor_bit_exact_three_paths(ak, case):
     _eq(c2, ref)
     # the closed form of reading R23: evals = sum of the final counts <= n d
     assert np.array_equal(a["evals"], a["counts"].astype(np.int64).sum(1))
-    if d > 3 and n > 100:
-        assert not np.array_equal(plain["sums"], a["sums"])  # a different stream
+    sampled = (a["counts"] < d) & (plain["counts"] < d) & (a["counts"] > 1)
+    if sampled.any():  # a different stream (arms that went exact agree by construction)
+        assert not np.array_equal(plain["sums"][sampled], a["sums"][sampled])
 
 
 def test_wor_config1_planted(ak):
