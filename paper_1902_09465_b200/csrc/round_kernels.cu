@@ -220,9 +220,11 @@ __device__ __forceinline__ uint32_t filter_arms(const Geom &g, const int32_t *th
     const int4 t = __ldg(reinterpret_cast<const int4 *>(thr) + c);  // Su, Sl, Ck, Ckh
     const int32_t S = a.S[e];
     const uint32_t gid = (uint32_t)i + g.id_offset;
-    const bool inC = S < t.z || (((eqk >> c) & 1u) && S == t.z && gid <= idk);
-    const bool inM = S < t.w || (((eqkh >> c) & 1u) && S == t.w && gid <= idkh);
-    const bool blk = live && (inC ? S >= t.x : (inM ? ((mmask >> c) & 1u) != 0u : S < t.y));
+    // non-short-circuit operators: predicated compares, no branches (ties at the k-th /
+    // (k+h)-th key are decided by the id)
+    const bool inC = (S < t.z) | ((((eqk >> c) & 1u) != 0u) & (S == t.z) & (gid <= idk));
+    const bool inM = (S < t.w) | ((((eqkh >> c) & 1u) != 0u) & (S == t.w) & (gid <= idkh));
+    const bool blk = live & (inC ? (S >= t.x) : (inM ? (((mmask >> c) & 1u) != 0u) : (S < t.y)));
     const bool ex = (2u << c) >= (unsigned)g.d;
     const uint32_t act = blk ? (ex ? (uint32_t)ACT_EXACT : c + 1u) : 0u;
     dr += (blk && !ex) ? (1u << c) : 0u;
@@ -270,7 +272,7 @@ struct SlotRun {
   }
 };
 
-__global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
+__global__ void __launch_bounds__(FIL_NT, 4) k_filter(Geom g) {
   extern __shared__ uint32_t tcnt[];  // [FIL_ROWS / R][FIL_NT * 4 / P] (tiles on)
   __shared__ unsigned scnt[NSLOT];
   __shared__ unsigned lvc[(FIL_NT * 4 / 128) * MAX_LEVELS];
@@ -320,7 +322,13 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
       const uint32_t act = (actw >> (8 * e)) & 0xFFu;
       ex_acc += act == ACT_EXACT;
       if (act) run.add(act == ACT_EXACT ? (unsigned)MAX_LEVELS : act - 1u, scnt);
-      if (g.level_mma && act && act != ACT_EXACT) lrun.add(act - 1u, lvc + ((threadIdx.x * 4) >> 7) * MAX_LEVELS);
+    }
+    if (g.level_mma) {
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        const uint32_t act = (actw >> (8 * e)) & 0xFFu;
+        if (act && act != ACT_EXACT) lrun.add(act - 1u, lvc + ((threadIdx.x * 4) >> 7) * MAX_LEVELS);
+      }
     }
     if (g.tile_on) {
       const int tr = r >> g.tile_lr;
