@@ -220,11 +220,9 @@ __device__ __forceinline__ uint32_t filter_arms(const Geom &g, const int32_t *th
     const int4 t = __ldg(reinterpret_cast<const int4 *>(thr) + c);  // Su, Sl, Ck, Ckh
     const int32_t S = a.S[e];
     const uint32_t gid = (uint32_t)i + g.id_offset;
-    // non-short-circuit operators: predicated compares, no branches (ties at the k-th /
-    // (k+h)-th key are decided by the id)
-    const bool inC = (S < t.z) | ((((eqk >> c) & 1u) != 0u) & (S == t.z) & (gid <= idk));
-    const bool inM = (S < t.w) | ((((eqkh >> c) & 1u) != 0u) & (S == t.w) & (gid <= idkh));
-    const bool blk = live & (inC ? (S >= t.x) : (inM ? (((mmask >> c) & 1u) != 0u) : (S < t.y)));
+    const bool inC = S < t.z || (((eqk >> c) & 1u) && S == t.z && gid <= idk);
+    const bool inM = S < t.w || (((eqkh >> c) & 1u) && S == t.w && gid <= idkh);
+    const bool blk = live && (inC ? S >= t.x : (inM ? ((mmask >> c) & 1u) != 0u : S < t.y));
     const bool ex = (2u << c) >= (unsigned)g.d;
     const uint32_t act = blk ? (ex ? (uint32_t)ACT_EXACT : c + 1u) : 0u;
     dr += (blk && !ex) ? (1u << c) : 0u;
@@ -272,7 +270,10 @@ struct SlotRun {
   }
 };
 
-__global__ void __launch_bounds__(FIL_NT, 4) k_filter(Geom g) {
+// MODE 0: the round's filter; 1: the same, also writing the lead bytes (lead > 1);
+// 2: a lead pass (reading R24).  Separate instantiations keep MODE 0's registers.
+template <int MODE>
+__global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
   extern __shared__ uint32_t tcnt[];  // [FIL_ROWS / R][FIL_NT * 4 / P] (tiles on)
   __shared__ unsigned scnt[NSLOT];
   __shared__ unsigned lvc[(FIL_NT * 4 / 128) * MAX_LEVELS];
@@ -310,11 +311,11 @@ __global__ void __launch_bounds__(FIL_NT, 4) k_filter(Geom g) {
     }
     if (cur) continue;  // uniform: one query row at a time
     uint32_t dr = 0, actw = 0, lw = 0;
-    if (g.lead_pass) {
+    if (MODE == 2) {
       if (arms) actw = lead_arms(g, ca, *reinterpret_cast<const uint32_t *>(g.leadb + (size_t)qi * g.npad + i0), i0, &dr);
     } else {
       if (arms) actw = filter_arms(g, g.thr + (size_t)qi * THR_STRIDE, ca, i0, &dr, &lw);
-      if (g.lead > 1 && i0 < g.npad) *reinterpret_cast<uint32_t *>(g.leadb + (size_t)qi * g.npad + i0) = lw;
+      if (MODE == 1 && i0 < g.npad) *reinterpret_cast<uint32_t *>(g.leadb + (size_t)qi * g.npad + i0) = lw;
     }
     if (i0 < g.npad) *reinterpret_cast<uint32_t *>(g.act + (size_t)qi * g.npad + i0) = actw;
 #pragma unroll
@@ -998,12 +999,18 @@ cudaError_t launch_select(const Geom &g, int nbits, cudaStream_t s) {
 
 cudaError_t launch_filter(const Geom &g, cudaStream_t s) {
   const size_t smem = g.tile_on ? sizeof(uint32_t) * (size_t)(FIL_ROWS >> g.tile_lr) * ((FIL_NT * 4) >> g.tile_lp) : 0;
-  if (smem > 48 * 1024) {
-    const cudaError_t e = cudaFuncSetAttribute(k_filter, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
-  }
-  k_filter<<<dim3(cdiv(g.npad, FIL_NT * 4), cdiv(g.q, FIL_ROWS)), FIL_NT, smem, s>>>(g);
-  return cudaGetLastError();
+  const dim3 grid(cdiv(g.npad, FIL_NT * 4), cdiv(g.q, FIL_ROWS));
+  auto go = [&](auto kern) {
+    if (smem > 48 * 1024) {
+      const cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+    }
+    kern<<<grid, FIL_NT, smem, s>>>(g);
+    return cudaGetLastError();
+  };
+  if (g.lead_pass) return go(k_filter<2>);
+  if (g.lead > 1) return go(k_filter<1>);
+  return go(k_filter<0>);
 }
 
 cudaError_t launch_compact(const Geom &g, cudaStream_t s) {
