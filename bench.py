@@ -74,6 +74,8 @@ def _args():
     ap.add_argument("--sec5-threads", type=int, default=80, help="sec5: trials in flight")
     ap.add_argument("--sec5-a1-max-iters", type=int, default=0,
                     help="sec5: cap on Algorithm-1 iterations per query (0: none; capped trials are counted)")
+    ap.add_argument("--lead", type=int, default=1,
+                    help="close-side lead L of the batched rule (aknn_opts.lead, DESIGN.md §16)")
     ap.add_argument("--clock-sampler", choices=("nvml", "smi", "none"), default="nvml")
     a = ap.parse_args()
     if a.config is None:
@@ -308,17 +310,17 @@ def _orc_worker(i):
     X, Q, cfg, al = _ORC["X"], _ORC["Q"], _ORC["cfg"], _ORC["alpha"]
     r = orc.query_br(X, Q[i:i + 1], cfg.k, cfg.h, cfg.seed, al,
                      qids=np.array([i], np.int32), want_counts=False,
-                     shared_draws=_ORC.get("shared", False))
+                     shared_draws=_ORC.get("shared", False), lead=_ORC.get("lead", 1))
     return int(r["evals"][0])
 
 
-def _oracle_time(X, Q, cfg, alpha, nq: int, cores: int, shared: bool = False):
+def _oracle_time(X, Q, cfg, alpha, nq: int, cores: int, shared: bool = False, lead: int = 1):
     """Wall time of the oracle (as it stands, single-threaded C) on nq queries spread
     over `cores` worker processes (one query per task)."""
     import multiprocessing as mp
     import oracle.oracle as orc
     orc.lib()  # build/load before forking
-    _ORC.update(X=X, Q=Q, cfg=cfg, alpha=alpha, shared=shared)
+    _ORC.update(X=X, Q=Q, cfg=cfg, alpha=alpha, shared=shared, lead=lead)
     ctx = mp.get_context("fork")
     t0 = time.perf_counter()
     with ctx.Pool(cores) as pool:
@@ -359,7 +361,7 @@ def run_reference(args, dist: Dist):
     times = []
     for it in range(args.warmup + args.steps):
         off = (it * nq) % max(1, cfg.q - nq + 1)
-        dt, _ = _oracle_time(X, Q[off:off + nq], cfg, al, nq, cores, args.draws == "shared")
+        dt, _ = _oracle_time(X, Q[off:off + nq], cfg, al, nq, cores, args.draws == "shared", args.lead)
         if it >= args.warmup:
             times.append(dt)
     ms = 1e3 * sum(times) / len(times)
@@ -381,6 +383,7 @@ def _config_desc(cfg, args, extra=None):
     d = {"workload": cfg.name + ("_shared_draws" if getattr(args, "draws", "per-query") == "shared" else ""),
          "n": cfg.n, "d": cfg.d, "q_per_rank": cfg.q, "k": cfg.k,
          "h": cfg.h, "delta": cfg.delta, "seed": cfg.seed, "alpha": _alpha_desc(args.alpha),
+         "lead": getattr(args, "lead", 1),
          "parallelism": f"query-parallel x{args.gpus} (X replicated)" if args.gpus > 1 else "1 GPU",
          "l2": "flushed before every step (512 MiB write, outside the timed events)"}
     if extra:
@@ -446,7 +449,7 @@ def run_ours(args, dist: Dist):
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
         ix.query_device(Qd, k, h, cfg.delta, cfg.seed, alpha_d, qi_offset=qi_off, timing=timing,
-                        stream=stream, out=out, flags=qflags if flags is None else flags)
+                        stream=stream, out=out, flags=qflags if flags is None else flags, lead=args.lead)
         e1.record(stream)
         torch.cuda.synchronize()
         return e0.elapsed_time(e1), ix.stats()
@@ -650,14 +653,16 @@ def run_ours(args, dist: Dist):
                     rounds=torch.empty(qpr, dtype=torch.int32).pin_memory().numpy())
         Qpin_np = Qpin.numpy()
         for _ in range(1):
-            ix.query(Qpin_np, k, h, cfg.delta, cfg.seed, alpha, qi_offset=qi_off, out=hout, flags=qflags)
+            ix.query(Qpin_np, k, h, cfg.delta, cfg.seed, alpha, qi_offset=qi_off, out=hout, flags=qflags,
+                     lead=args.lead)
         dist.barrier()
         wall = []
         for _ in range(args.steps):
             flush.zero_()
             torch.cuda.synchronize()
             t0 = time.perf_counter()
-            ix.query(Qpin_np, k, h, cfg.delta, cfg.seed, alpha, qi_offset=qi_off, out=hout, flags=qflags)
+            ix.query(Qpin_np, k, h, cfg.delta, cfg.seed, alpha, qi_offset=qi_off, out=hout, flags=qflags,
+                     lead=args.lead)
             wall.append(time.perf_counter() - t0)
         e2e_s = dist.max(sum(wall))
         h2d = Qh.nbytes + alpha.nbytes
@@ -673,7 +678,8 @@ def run_ours(args, dist: Dist):
         # a bounded sample of the same workload: ~10-30 s of oracle work on the host cores
         cores = max(1, min(_cpu_cores(), 16))
         nq = min(qpr, 8 * cores if n <= 200_000 else cores)
-        dt, _ = _oracle_time(X, Qh, cfg, _oracle_alpha(cfg, args.alpha), nq, cores, args.draws == "shared")
+        dt, _ = _oracle_time(X, Qh, cfg, _oracle_alpha(cfg, args.alpha), nq, cores, args.draws == "shared",
+                             args.lead)
         cpu = {"value": nq / dt, "unit": UNIT, "cores": min(cores, nq), "kind": "oracle",
                "sample": f"first {nq} queries of {cfg.name} (full n={n}, d={d}), one "
                          f"single-threaded oracle process per core, {dt:.1f} s wall"}
