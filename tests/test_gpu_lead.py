@@ -108,3 +108,21 @@ def test_lead_out_of_range_rejected(ak):
             ix.query(Q, 3, 3, 0.05, 0, orc.alpha_theory(200, 0.05, 16), lead=9)
     finally:
         ix.close()
+
+
+@pytest.mark.parametrize("max_rounds", [1, 2, 4])
+def test_lead_round_cap_partial_state(ak, max_rounds):
+    """A round cap stops after whole rounds (every lead pass of the last round done):
+    the partial state equals the oracle's, on the graph loop and the host loop."""
+    X, Q = synth.small_instance(1360, 1500, 96, q=6)
+    al = orc.alpha_experimental(1500, 0.05, 96, 0.05)
+    ix = ak.Index(X)
+    try:
+        g = ix.query(Q, 5, 5, 0.05, 8, al, counts=True, sums=True, lead=3, max_rounds=max_rounds)
+        t = ix.query(Q, 5, 5, 0.05, 8, al, counts=True, sums=True, lead=3, max_rounds=max_rounds,
+                     timing=True)
+    finally:
+        ix.close()
+    ref = orc.query_br(X, Q, 5, 5, 8, al, want_sums=True, lead=3, max_rounds=max_rounds)
+    _eq(g, ref)
+    _eq(t, ref)
