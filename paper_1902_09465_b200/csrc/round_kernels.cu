@@ -208,20 +208,24 @@ cudaError_t launch_thresholds(const Geom &g, cudaStream_t s) {
 __device__ __forceinline__ uint32_t filter_arms(const Geom &g, const int32_t *thr, const Arm4 &a, int i0,
                                                 uint32_t *draws, uint32_t *leadw) {
   uint32_t actw = 0, dr = 0, lw = 0;
-  const int4 hdr = __ldg(reinterpret_cast<const int4 *>(thr + THR_LEVEL_INTS));
+  // thr: the row's table staged in shared memory by k_filter
+  const int4 hdr = *reinterpret_cast<const int4 *>(thr + THR_LEVEL_INTS);
   const uint32_t mmask = (uint32_t)hdr.x, eqk = (uint32_t)hdr.y, eqkh = (uint32_t)hdr.z;
-  const uint32_t idk = (uint32_t)hdr.w, idkh = (uint32_t)__ldg(thr + THR_LEVEL_INTS + 4);
+  const uint32_t idk = (uint32_t)hdr.w, idkh = (uint32_t)thr[THR_LEVEL_INTS + 4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const int i = i0 + e;
     const uint8_t l = a.l[e];
     const uint32_t c = l & 15u;
     const bool live = i < g.n && !lvl_exact(l);
-    const int4 t = __ldg(reinterpret_cast<const int4 *>(thr) + c);  // Su, Sl, Ck, Ckh
+    const int4 t = reinterpret_cast<const int4 *>(thr)[c];  // Su, Sl, Ck, Ckh
     const int32_t S = a.S[e];
-    const uint32_t gid = (uint32_t)i + g.id_offset;
-    const bool inC = S < t.z || (((eqk >> c) & 1u) && S == t.z && gid <= idk);
-    const bool inM = S < t.w || (((eqkh >> c) & 1u) && S == t.w && gid <= idkh);
+    bool inC = S < t.z, inM = S < t.w;
+    if ((S == t.z) | (S == t.w)) {  // rare: the id decides a tie with the k-th / (k+h)-th key
+      const uint32_t gid = (uint32_t)i + g.id_offset;
+      inC = inC || (((eqk >> c) & 1u) && S == t.z && gid <= idk);
+      inM = inM || (((eqkh >> c) & 1u) && S == t.w && gid <= idkh);
+    }
     const bool blk = live && (inC ? S >= t.x : (inM ? ((mmask >> c) & 1u) != 0u : S < t.y));
     const bool ex = (2u << c) >= (unsigned)g.d;
     const uint32_t act = blk ? (ex ? (uint32_t)ACT_EXACT : c + 1u) : 0u;
@@ -286,6 +290,11 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
   for (int s = threadIdx.x; s < NSLOT; s += FIL_NT) scnt[s] = 0;
   for (int t = threadIdx.x; t < ntc; t += FIL_NT) tcnt[t] = 0;
   for (int t = threadIdx.x; t < (FIL_NT * 4 / 128) * MAX_LEVELS; t += FIL_NT) lvc[t] = 0;
+  // the CTA's rows of blocker thresholds (reading R20), staged once
+  __shared__ __align__(16) int32_t sthr[MODE == 2 ? 4 : FIL_ROWS * THR_STRIDE];
+  if (MODE != 2)
+    for (int t = threadIdx.x; t < rows * (THR_STRIDE / 4); t += FIL_NT)
+      reinterpret_cast<int4 *>(sthr)[t] = __ldg(reinterpret_cast<const int4 *>(g.thr + (size_t)q0 * THR_STRIDE) + t);
   __syncthreads();
   const bool arms = i0 < g.n;
   // two rows of loads in flight ahead of the row being decided
@@ -314,7 +323,7 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
     if (MODE == 2) {
       if (arms) actw = lead_arms(g, ca, *reinterpret_cast<const uint32_t *>(g.leadb + (size_t)qi * g.npad + i0), i0, &dr);
     } else {
-      if (arms) actw = filter_arms(g, g.thr + (size_t)qi * THR_STRIDE, ca, i0, &dr, &lw);
+      if (arms) actw = filter_arms(g, sthr + r * THR_STRIDE, ca, i0, &dr, &lw);
       if (MODE == 1 && i0 < g.npad) *reinterpret_cast<uint32_t *>(g.leadb + (size_t)qi * g.npad + i0) = lw;
     }
     if (i0 < g.npad) *reinterpret_cast<uint32_t *>(g.act + (size_t)qi * g.npad + i0) = actw;
