@@ -698,6 +698,8 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   const size_t oThr = off; off = round_up(off + sizeof(int32_t) * THR_STRIDE * (size_t)qb, 256);
   const size_t oLm = off; off = round_up(off + level_ws_bytes(qb, n, npad, ix->pitch, o), 256);
   const size_t oLead = off; off = round_up(off + (o.lead > 1 ? szL : 0), 256);
+  const int rowany_cols = (int)((npad + 1023) / 1024);
+  const size_t oRany = off; off = round_up(off + (size_t)((qb + 31) / 32) * rowany_cols * 4, 256);
   TRY(ix->ws.ensure(off));
 
   Geom g{};
@@ -710,6 +712,8 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   g.act = ix->ws.as<uint8_t>(oA);
   g.lead = o.lead > 1 ? o.lead : 1;
   g.leadb = o.lead > 1 ? ix->ws.as<uint8_t>(oLead) : nullptr;
+  g.rowany = ix->ws.as<uint32_t>(oRany);
+  g.rowany_cols = rowany_cols;
   g.list = ix->ws.as<uint32_t>(oList);
   g.qs = ix->ws.as<QState>(oQS);
   g.ctl = ix->ws.as<RoundCtl>(oCtl);
@@ -954,6 +958,8 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     const size_t oThr = off; off = round_up(off + sizeof(int32_t) * THR_STRIDE * (size_t)qb, 256);
     const size_t oLm = off; off = round_up(off + level_ws_bytes(qb, ix->n_local, npad, ix->pitch, o), 256);
     const size_t oLead = off; off = round_up(off + (o.lead > 1 ? szL : 0), 256);
+    const int rowany_cols = (int)((npad + 1023) / 1024);
+    const size_t oRany = off; off = round_up(off + (size_t)((qb + 31) / 32) * rowany_cols * 4, 256);
     TRY(ix->ws.ensure(off));
     Geom &g = G[si];
     g = Geom{};
@@ -966,6 +972,8 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     g.act = ix->ws.as<uint8_t>(oA);
     g.lead = o.lead > 1 ? o.lead : 1;
     g.leadb = o.lead > 1 ? ix->ws.as<uint8_t>(oLead) : nullptr;
+    g.rowany = ix->ws.as<uint32_t>(oRany);
+    g.rowany_cols = rowany_cols;
     g.list = ix->ws.as<uint32_t>(oList);
     g.qs = ix->ws.as<QState>(oQS);
     g.ctl = ix->ws.as<RoundCtl>(oCtl);

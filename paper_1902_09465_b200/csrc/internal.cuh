@@ -148,6 +148,8 @@ struct Geom {
   int tile_lr, tile_lp;  // log2 R (queries per tile), log2 P (points per tile); R | 32, 4 <= P <= 32
   int tile_cols;         // row length of tilework: ceil(npad / P)
   uint32_t *tilework;    // [ceil(qb / R)][tile_cols] draws of the tile's sampled blockers
+  uint32_t *rowany;      // [ceil(qb / 32)][rowany_cols] bit r: row r of the 32-row group has an
+  int rowany_cols;       //   action in this 1024-arm chunk (k_filter -> k_scatter early exit)
   float tile_min_draws;  // dense iff tilework >= tile_min_draws
   int tile_slot_l;       // log2 of a row slot in shared memory (>= pitch)
   unsigned long long *advanced;  // pairs advanced (statistics), device counter

@@ -290,6 +290,8 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
   for (int s = threadIdx.x; s < NSLOT; s += FIL_NT) scnt[s] = 0;
   for (int t = threadIdx.x; t < ntc; t += FIL_NT) tcnt[t] = 0;
   for (int t = threadIdx.x; t < (FIL_NT * 4 / 128) * MAX_LEVELS; t += FIL_NT) lvc[t] = 0;
+  __shared__ uint32_t srow_any;  // bit r: row r has an action in this chunk
+  if (threadIdx.x == 0) srow_any = 0;
   // the CTA's rows of blocker thresholds (reading R20), staged once
   __shared__ __align__(16) int32_t sthr[MODE == 2 ? 4 : FIL_ROWS * THR_STRIDE];
   if (MODE != 2)
@@ -307,6 +309,7 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
   SlotRun run, lrun;      // lrun: the thread's pairs per level in its 128 x 128 level tile
   unsigned ex_acc = 0;     // exact fallbacks of this thread (one 128-query tile row: 32 | 128)
   uint32_t dr_acc = 0;     // sampled draws of this thread in the current tile row
+  uint32_t rany = 0;       // bit r: this thread's arms of row r have an action
   int tr_cur = 0;
   for (int r = 0; r < rows; ++r) {
     const int qi = q0 + r;
@@ -327,6 +330,7 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
       if (MODE == 1 && i0 < g.npad) *reinterpret_cast<uint32_t *>(g.leadb + (size_t)qi * g.npad + i0) = lw;
     }
     if (i0 < g.npad) *reinterpret_cast<uint32_t *>(g.act + (size_t)qi * g.npad + i0) = actw;
+    rany |= (actw != 0u ? 1u : 0u) << r;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
       const uint32_t act = (actw >> (8 * e)) & 0xFFu;
@@ -353,6 +357,10 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
   run.flush(scnt);
   if (g.level_mma) lrun.flush(lvc + ((threadIdx.x * 4) >> 7) * MAX_LEVELS);
   if (g.tile_on && dr_acc) atomicAdd(&tcnt[tr_cur * tcols + ((threadIdx.x * 4) >> g.tile_lp)], dr_acc);
+  {
+    const uint32_t w = __reduce_or_sync(FULL, rany);
+    if (lane == 0 && w) atomicOr(&srow_any, w);
+  }
   if (g.exact_mma) {
     // a warp's 128 arms lie in one 128 x 256 tile of the tensor-core pass: count them
     const unsigned wex = __reduce_add_sync(FULL, ex_acc);
@@ -360,6 +368,7 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
   }
   __syncthreads();
   if (threadIdx.x < NSLOT && scnt[threadIdx.x]) atomicAdd(&g.ctl->cnt[threadIdx.x], scnt[threadIdx.x]);
+  if (threadIdx.x == 0) g.rowany[(size_t)blockIdx.y * g.rowany_cols + blockIdx.x] = srow_any;
   if (g.level_mma)
     for (int t = threadIdx.x; t < (FIL_NT * 4 / 128) * MAX_LEVELS; t += FIL_NT) {
       const int lc = ((blockIdx.x * FIL_NT * 4) >> 7) + t / MAX_LEVELS;
@@ -454,7 +463,9 @@ __global__ void k_plan_lists(RoundCtl *ctl, unsigned bpl, int stage_lo) {
 // of each warp, so the advance kernel reads S / level nearly sequentially.
 __global__ void __launch_bounds__(FIL_NT) k_scatter(Geom g) {
   const int qi = blockIdx.x;
-  if (g.qs[qi].done) return;
+  // nothing to list in this row's chunk (k_filter's per-row action mask; finished
+  // queries have no actions): exit before the tile decisions
+  if (!((g.rowany[(size_t)(qi >> 5) * g.rowany_cols + blockIdx.y] >> (qi & 31)) & 1u)) return;
   __shared__ unsigned scnt[NSLOT], sbase[NSLOT];
   __shared__ uint8_t sdense[FIL_NT * 4 / 4];  // the chunk's (R x P) tiles: dense?
   __shared__ uint8_t smma[FIL_NT * 4 / 256];   // its 128 x 256 exact tiles: tensor cores?
