@@ -271,9 +271,13 @@ int env_int(const char *name, int dflt) {
 TileShape tile_shape(int64_t pitch) {
   TileShape t{0, 0, 0, 0.f};
   if (env_int("AKNN_TILE", 1) == 0) return t;
-  // the largest tile (R * P) whose shared memory fits 3, 2 or 1 CTAs per SM (228 KB)
+  // the largest tile (R * P) whose shared memory fits 3, 2 or 1 CTAs per SM (228 KB);
+  // rows wider than 8 KB: the largest tile at one CTA per SM (C3, d = 12,288: 4 x 8 at
+  // one CTA beat 2 x 4 at two by 14 % -- staging amortised over 4x the pairs)
   int lr = -1, lp = -1;
-  for (size_t cap : {(size_t)233472 / 3, (size_t)233472 / 2, (size_t)233472}) {
+  const std::vector<size_t> caps = pitch > 8192 ? std::vector<size_t>{(size_t)233472}
+                                                 : std::vector<size_t>{(size_t)233472 / 3, (size_t)233472 / 2, (size_t)233472};
+  for (size_t cap : caps) {
     for (int a = 5; a >= 0; --a)
       for (int b = 5; b >= 2; --b)
         if (a <= b && tile_smem_bytes(a, b, pitch) <= cap && (lr < 0 || a + b > lr + lp)) {
