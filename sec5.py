@@ -17,7 +17,8 @@ reports the median and interquartile range over the trials of
 Both schedules run on the GPU: "a1" is the literal Algorithm 1 (the paper's own,
 aknn_query_a1, one warp per query; trials in flight concurrently, one index and
 stream each), "br" the batched round rule (aknn_query_ex), "br_lead<L>" the batched rule with a
-close-side lead L (aknn_opts.lead, reading R24).  The exact k-NN per trial
+close-side lead L (aknn_opts.lead, reading R24), "br_wor" the batched rule sampling
+without replacement (AKNN_FLAG_WITHOUT_REPLACEMENT, reading R23).  The exact k-NN per trial
 comes from the exact tensor-core pass (aknn_exact).  The oracle is not used here.
 """
 from __future__ import annotations
@@ -86,10 +87,12 @@ def run(args, dist) -> None:
             for sname in scheds:
                 if not sname.startswith("br"):
                     continue
-                # "br": the batched rule; "br_lead<L>": with a close-side lead L (reading R24)
+                # "br": the batched rule; "br_lead<L>": with a close-side lead L (reading R24);
+                # "br_wor": sampling without replacement (reading R23)
                 lead = int(sname[len("br_lead"):]) if sname.startswith("br_lead") else 1
+                flags = ak.FLAG_WITHOUT_REPLACEMENT if sname == "br_wor" else 0
                 t1 = time.perf_counter()
-                r = ix.query(q, k, h, delta, t, alphas[c], counts=False, dhat=False, lead=lead)
+                r = ix.query(q, k, h, delta, t, alphas[c], counts=False, dhat=False, lead=lead, flags=flags)
                 rows.append(dict(w=w, trial=t, c=c, s=sname, recall=_recall(X, q[0], r["sets"][0], dks[wt], k),
                                  fraction=int(r["evals"][0]) / (n * m), rounds=int(r["rounds"][0]),
                                  draws=int(r["draws"][0]), wall_s=time.perf_counter() - t1))
