@@ -85,6 +85,11 @@ typedef struct {
                          advance L times (each the doubling / P:176 exact step),
                          the far blockers once.  1 <= L <= 8 (else EINVAL);
                          ignored by the Algorithm-1 entry points.              */
+  int32_t batch_queries; /* 0 = automatic; else at most this many queries per
+                         internal sub-batch (the round workspace is ~10 B per
+                         (query, point) pair; the automatic size fits 60 % of
+                         free device memory).  Results do not depend on it.
+                         Ignored by the Algorithm-1 entry points.  < 0: EINVAL */
 } aknn_opts;
 
 #define AKNN_FLAG_RADIX_SELECT 1
@@ -109,9 +114,10 @@ typedef struct {
 #define AKNN_FLAG_NO_LEVEL_MMA 32
 /* bit 6: sampling WITHOUT replacement (footnote 1 to P:120; SURVEY.md §8(f) row 4;
    DESIGN.md reading R23): the t-th sample of arm (qi, i) is coordinate pi(t) of a
-   permutation of [0, d) keyed per arm (an 8-round Feistel network on the smallest
-   even-bit domain >= d with cycle walking and a keyed rotation; its keys are the
-   Philox4x32-10 block of counter (0, i, qi, 0x80000000)).  Estimates stay unbiased
+   permutation of [0, d) keyed per arm: a 6-round mixed-radix Feistel network on
+   Z_a x Z_b (a = ceil(sqrt d), b = ceil(d / a)) cycle-walked into [0, d), then a
+   keyed rotation; its keys are the Philox4x32-10 block of counter
+   (0, i, qi, 0x80000000).  Estimates stay unbiased
    and the footnote-2 / §5 radii stay valid (Hoeffding's bound holds without
    replacement).  An exact fallback is charged only the d - T coordinates
    not drawn yet, so evals = the sum of the final counts <= n d; in Algorithm 1 an
@@ -161,17 +167,27 @@ typedef struct {
 /* Index construction.                                                       */
 /* ------------------------------------------------------------------------ */
 
-/* Copy points (host, uint8 [n][d]) to the current CUDA device.
- * Domain: n >= 2, 1 <= d <= 33025 (so that d * 255^2 < 2^31), n < 2^31.
- * The caller may free `points` on return.                                   */
+/* Copy points (host, uint8 [n][d]) to the current CUDA device: the point set X
+ * of the problem statement (§3; one point per row, one uint8 coordinate
+ * per byte, reading R2).  The device copy is row-major with the row pitch padded
+ * to 16 bytes (zero filled); ||x_i||^2 is computed lazily by the first exact pass.
+ * Domain (EINVAL otherwise): n >= 2, n < 2^31, 1 <= d <= 33025 (so that
+ * d * 255^2 < 2^31), and the composite rank key of DESIGN.md reading R9 fits 63
+ * bits: bit_length(65025 * lcm(2^c, d)) + bit_length(n - 1) <= 63 with c the
+ * largest integer such that 2^c < d (c = 0 for d <= 2).  Every d <= 258 fits
+ * for any n < 2^31, every d <= 4128 for n <= 8e6, every d <= 16384 for
+ * n <= 1e6 and every d <= 33025 for n <= 1e5 (all five BASELINE configs fit).
+ * ENOMEM when the device copy does not fit; ECUDA on a
+ * failed copy.  The caller may free `points` on return.                     */
 aknn_status aknn_build(const uint8_t *points, int64_t n, int32_t d, aknn_index **out);
 
 /* Same, from a DEVICE buffer, copied on `cuda_stream` (the index keeps its own
- * copy; the caller's buffer may be freed after the stream completes).       */
+ * copy; the caller's buffer may be freed after the stream completes; queries on
+ * another stream must be ordered after it by the caller).  Same domain.      */
 aknn_status aknn_build_async(const uint8_t *points_dev, int64_t n, int32_t d,
                              void *cuda_stream, aknn_index **out);
 
-/* Sharded index (DESIGN.md §9): this process holds rows
+/* Sharded index (DESIGN.md §9; SURVEY.md §8(e)): this process holds rows
  * [offset, offset + n_local) of an n_global-point set.  Point ids in the RNG
  * counter and in the returned sets are global ids.  `nccl_unique_id` points
  * to an ncclUniqueId (128 bytes) shared by the `world` ranks (rank 0 creates
@@ -180,6 +196,9 @@ aknn_status aknn_build_async(const uint8_t *points_dev, int64_t n, int32_t d,
 aknn_status aknn_build_shard(const uint8_t *shard, int64_t n_local, int64_t n_global,
                              int64_t offset, int32_t d, const void *nccl_unique_id,
                              int32_t rank, int32_t world, aknn_index **out);
+/* Domain as aknn_build with n = n_global for the key, plus
+ * 0 <= offset, offset + n_local <= n_global, 0 <= rank < world (EINVAL);
+ * ENCCL when world > 1 and the communicator cannot be created.               */
 /* aknn_query* on an index built with world > 1 runs the point-sharded round
  * loop: one ncclAllGather per round of (k+h+1) 16-byte records per query and
  * rank, a deterministic merge on every rank, and at the end an ncclAllReduce of

@@ -44,7 +44,7 @@ class Result(C.Structure):
 
 class Opts(C.Structure):
     _fields_ = [("qi_offset", C.c_int32), ("max_rounds", C.c_int32), ("timing", C.c_int32),
-                ("flags", C.c_int32), ("lead", C.c_int32)]
+                ("flags", C.c_int32), ("lead", C.c_int32), ("batch_queries", C.c_int32)]
 
 
 FLAG_RADIX_SELECT = 1
@@ -143,13 +143,18 @@ def alpha_table(n: int, delta: float, d: int, kind: str = "theory", c_alpha: flo
 
 def query_multi(shards, queries, k: int, h: int, delta: float, seed: int = 0, alpha=None, *,
                 counts: bool = True, sums: bool = False, dhat: bool = True, max_rounds: int = 0,
-                qi_offset: int = 0, timing: bool = False, flags: int = 0, lead: int = 1) -> dict:
+                qi_offset: int = 0, timing: bool = False, flags: int = 0, lead: int = 1,
+                batch_queries: int = 0) -> dict:
     """aknn_query_multi: one query batch over shard indices on the current device.
 
     ``shards`` are Index objects built with ``Index(rows, n_global=..., offset=...)``
     tiling [0, n_global) in order; counts/sums come back with n_global columns."""
     Q = np.ascontiguousarray(np.atleast_2d(queries), np.uint8)
     q, d = Q.shape
+    if not shards:
+        raise AknnError(AKNN_EINVAL, "need at least one shard")
+    if d != shards[0].d:
+        raise AknnError(AKNN_EINVAL, f"query dimension {d} != index dimension {shards[0].d}")
     n = shards[0].n_global
     kh = k + h
     out = dict(sets=np.zeros((q, kh), np.int32),
@@ -160,8 +165,10 @@ def query_multi(shards, queries, k: int, h: int, delta: float, seed: int = 0, al
                rounds=np.zeros(q, np.int32))
     res = Result(*[_ptr(out[f]) for f, _ in Result._fields_])
     al = None if alpha is None else np.ascontiguousarray(alpha, np.float64)
+    if al is not None and al.shape != (d + 1,):
+        raise AknnError(AKNN_EINVAL, f"alpha must have d+1={d + 1} entries")
     arr = (_P * len(shards))(*[s._h for s in shards])
-    opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags, lead)
+    opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags, lead, batch_queries)
     st = _lib.aknn_query_multi(arr, len(shards), _ptr(Q), q, k, h, delta, seed & (2**64 - 1),
                                _ptr(al), C.byref(opts), C.byref(res))
     out["status"] = st
@@ -251,7 +258,7 @@ class Index:
     def query(self, queries, k: int, h: int, delta: float, seed: int = 0, alpha=None, *,
               counts: bool = True, sums: bool = False, dhat: bool = True, max_rounds: int = 0,
               qi_offset: int = 0, timing: bool = False, out: Optional[dict] = None,
-              flags: int = 0, schedule: str = "br", lead: int = 1) -> dict:
+              flags: int = 0, schedule: str = "br", lead: int = 1, batch_queries: int = 0) -> dict:
         """aknn_query_ex on host arrays; returns numpy arrays.
 
         ``schedule="a1"`` runs the literal Algorithm 1 instead (aknn_query_a1;
@@ -288,7 +295,7 @@ class Index:
         al = None if alpha is None else np.ascontiguousarray(alpha, np.float64)
         if al is not None and al.shape != (self.d + 1,):
             raise AknnError(AKNN_EINVAL, f"alpha must have d+1={self.d + 1} entries")
-        opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags, lead)
+        opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags, lead, batch_queries)
         fn = _lib.aknn_query_a1 if schedule == "a1" else _lib.aknn_query_ex
         st = fn(self._h, _ptr(Q), q, k, h, delta, seed & (2**64 - 1), _ptr(al), C.byref(opts),
                 C.byref(res))
@@ -301,7 +308,7 @@ class Index:
                      counts: bool = False, sums: bool = False, dhat: bool = True,
                      max_rounds: int = 0, qi_offset: int = 0, timing: bool = False,
                      stream=None, out: Optional[dict] = None, flags: int = 0,
-                     schedule: str = "br", lead: int = 1) -> dict:
+                     schedule: str = "br", lead: int = 1, batch_queries: int = 0) -> dict:
         """aknn_query_async on torch CUDA tensors (current stream); returns device tensors.
 
         ``schedule="a1"``: the literal Algorithm 1 (aknn_query_a1_device; waits for the
@@ -309,9 +316,12 @@ class Index:
         if schedule not in ("br", "a1"):
             raise AknnError(AKNN_EINVAL, f"schedule must be 'br' or 'a1', not {schedule!r}")
         torch = _torch()
-        assert queries.is_cuda and queries.dtype == torch.uint8
+        if not (queries.is_cuda and queries.dtype == torch.uint8 and queries.dim() == 2):
+            raise AknnError(AKNN_EINVAL, "queries must be a 2-D uint8 CUDA tensor")
         Q = queries.contiguous()
         q, d = Q.shape
+        if d != self.d:
+            raise AknnError(AKNN_EINVAL, f"query dimension {d} != index dimension {self.d}")
         kh = k + h
         dev = Q.device
         if out is None:
@@ -327,7 +337,9 @@ class Index:
         if alpha is not None:
             al = alpha if (hasattr(alpha, "is_cuda") and alpha.is_cuda) else \
                 torch.as_tensor(np.ascontiguousarray(alpha, np.float64)).to(dev)
-        opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags, lead)
+            if al.dtype != torch.float64 or al.numel() != self.d + 1 or not al.is_contiguous():
+                raise AknnError(AKNN_EINVAL, f"alpha must be a contiguous float64 tensor of d+1={self.d + 1} entries")
+        opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags, lead, batch_queries)
         fn = _lib.aknn_query_a1_device if schedule == "a1" else _lib.aknn_query_async
         st = fn(self._h, _ptr(Q), q, k, h, delta, seed & (2**64 - 1), _ptr(al), C.byref(opts),
                 C.byref(res), _stream_ptr(stream))
@@ -346,6 +358,8 @@ class Index:
         """aknn_exact: exact k nearest by (sum (a-b)^2, id); host arrays."""
         Q = np.ascontiguousarray(np.atleast_2d(queries), np.uint8)
         q = Q.shape[0]
+        if Q.shape[1] != self.d:
+            raise AknnError(AKNN_EINVAL, f"query dimension {Q.shape[1]} != index dimension {self.d}")
         idx = np.zeros((q, k), np.int32)
         dist = np.zeros((q, k), np.int32)
         _check(_lib.aknn_exact(self._h, _ptr(Q), q, k, _ptr(idx), _ptr(dist)))
@@ -354,6 +368,9 @@ class Index:
     def exact_device(self, queries, k: int, stream=None, out=None):
         """aknn_exact_async on torch CUDA tensors."""
         torch = _torch()
+        if not (queries.is_cuda and queries.dtype == torch.uint8 and queries.dim() == 2
+                and queries.shape[1] == self.d):
+            raise AknnError(AKNN_EINVAL, f"queries must be a uint8 CUDA tensor [q][{self.d}]")
         Q = queries.contiguous()
         q = Q.shape[0]
         if out is None:

@@ -151,7 +151,8 @@ struct aknn_index {
   DevBuf exact_ws;
   HostBuf host;            // pinned: n_active | RoundCtl | QState[qb]
   DevBuf nx;               // [n_local] ||x_i||^2 for the tensor-core exact pass (lazy)
-  bool nx_ready = false;
+  bool nx_ready = false;   // the row-norm kernel has been enqueued ...
+  cudaEvent_t nx_ev = nullptr;  // ... and completes at this event (other streams wait on it)
   EventPool events;
   // cached graph of the device-driven round loop (one query sub-batch shape)
   cudaStream_t cap_stream = nullptr;
@@ -177,11 +178,6 @@ struct aknn_index {
 
 namespace {
 
-aknn_status validate_build(int64_t n, int32_t d) {
-  if (n < 2 || n >= (1ll << 31)) return fail(AKNN_EINVAL, "n=%lld outside [2, 2^31)", (long long)n);
-  if (d < 1 || d > 33025) return fail(AKNN_EINVAL, "d=%d outside [1, 33025]", d);
-  return AKNN_OK;
-}
 
 aknn_status make_index(int64_t n_local, int64_t n_global, int64_t offset, int32_t d,
                        aknn_index **out) {
@@ -228,17 +224,29 @@ size_t exact_mma_ws_bytes(int64_t qb, int64_t npad) {
   return round_up((size_t)qb * 4, 256) + round_up((size_t)(rt * ct) * 4, 256);
 }
 
+// ||x_i||^2 for the tensor-core passes: computed once per index on the first
+// stream that needs it; every later user (possibly on another stream) waits on the
+// event recorded behind that kernel, so it never reads the norms early.
+aknn_status ensure_row_norms(aknn_index *ix, cudaStream_t st) {
+  if (!ix->nx_ready) {
+    const int64_t npad = round_up(ix->n_local, 16);
+    TRY(ix->nx.ensure(sizeof(int32_t) * (size_t)npad));
+    if (!ix->nx_ev) CU(cudaEventCreateWithFlags(&ix->nx_ev, cudaEventDisableTiming));
+    CU(cudaMemsetAsync(ix->nx.p, 0, sizeof(int32_t) * (size_t)npad, st));
+    CU(launch_row_norms(ix->X.as<uint8_t>(), ix->pitch, (int)ix->n_local, ix->nx.as<int32_t>(), st));
+    CU(cudaEventRecord(ix->nx_ev, st));
+    ix->nx_ready = true;
+    return AKNN_OK;
+  }
+  CU(cudaStreamWaitEvent(st, ix->nx_ev, 0));
+  return AKNN_OK;
+}
+
 aknn_status setup_exact_mma(aknn_index *ix, Geom &g, int64_t qb, uint8_t *ws, const aknn_opts &o,
                             cudaStream_t st) {
   g.exact_mma = (o.flags & AKNN_FLAG_EXACT_ROWS) ? 0 : 1;
   if (!g.exact_mma) return AKNN_OK;
-  if (!ix->nx_ready) {
-    const int64_t npad = round_up(ix->n_local, 16);
-    TRY(ix->nx.ensure(sizeof(int32_t) * (size_t)npad));
-    CU(cudaMemsetAsync(ix->nx.p, 0, sizeof(int32_t) * (size_t)npad, st));
-    CU(launch_row_norms(ix->X.as<uint8_t>(), ix->pitch, (int)ix->n_local, ix->nx.as<int32_t>(), st));
-    ix->nx_ready = true;
-  }
+  TRY(ensure_row_norms(ix, st));
   g.nx = ix->nx.as<int32_t>();
   g.nq = reinterpret_cast<int32_t *>(ws);
   g.xflags = reinterpret_cast<uint32_t *>(ws + round_up((size_t)qb * 4, 256));
@@ -414,6 +422,17 @@ aknn_status key_geom(int64_t n_local, int64_t n_global, int32_t d, KeyGeom *kg) 
     return fail(AKNN_EINVAL, "composite key needs %d bits (> 63) for n=%lld, d=%d", kg->nbits,
                 (long long)n_global, d);
   return AKNN_OK;
+}
+
+// Build-time domain (include/aknn.h): sizes, and the composite rank key of the
+// whole point set must fit 63 bits, so every later query on the index can rank.
+aknn_status validate_build(int64_t n, int32_t d, int64_t n_global) {
+  if (n < 2 || n >= (1ll << 31)) return fail(AKNN_EINVAL, "n=%lld outside [2, 2^31)", (long long)n);
+  if (d < 1 || d > 33025) return fail(AKNN_EINVAL, "d=%d outside [1, 33025]", d);
+  if (n_global < n || n_global >= (1ll << 31))
+    return fail(AKNN_EINVAL, "n_global=%lld outside [n_local, 2^31)", (long long)n_global);
+  KeyGeom kg;
+  return key_geom(n, n_global, d, &kg);
 }
 
 aknn_status host_alpha_table(int kind, int64_t n, double delta, double c_alpha, int32_t d,
@@ -652,6 +671,7 @@ aknn_status check_flags(const aknn_opts &o) {
   if ((o.flags & AKNN_FLAG_WITHOUT_REPLACEMENT) && (o.flags & AKNN_FLAG_SHARED_DRAWS))
     return fail(AKNN_EINVAL, "AKNN_FLAG_WITHOUT_REPLACEMENT cannot be combined with AKNN_FLAG_SHARED_DRAWS");
   if (o.lead < 0 || o.lead > 8) return fail(AKNN_EINVAL, "lead must be in [0, 8] (got %d)", o.lead);
+  if (o.batch_queries < 0) return fail(AKNN_EINVAL, "batch_queries must be >= 0 (got %d)", o.batch_queries);
   return AKNN_OK;
 }
 
@@ -671,7 +691,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   const int64_t npad = round_up(n, 16);
   // sub-batch size: the code (qi << ibits | i) must fit 32 bits; the
   // workspace (S 4 B + lvl 1 B + act 1 B + list 4 B per pair) fits in memory.
-  int64_t qb = q;
+  int64_t qb = o.batch_queries > 0 ? std::min<int64_t>(q, o.batch_queries) : q;
   const int64_t code_cap = 1ll << (32 - kg.ibits);
   if (qb > code_cap) qb = code_cap;
   const size_t per_q = (size_t)npad * 10 + ix->pitch + sizeof(QState) + 64;
@@ -850,8 +870,9 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
     if (defer) continue;  // folded in by finish_pending
     stats.launches_output += launches_output_of(op);
     CU(sync_spin(st));
+    // EMAXROUNDS is recorded and the remaining sub-batches still run, so every
+    // output row holds the state its query reached
     fold_batch_stats(stats, *h_ctl, h_qs, qn, use_graph, g, r, &status);
-    if (status != AKNN_OK) break;
   }
   tm.open_a = all_a;
   tm.stop(PH_ALL);
@@ -908,7 +929,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
   std::vector<KeyGeom> kg(shards.size());
   for (size_t s = 0; s < shards.size(); ++s) TRY(key_geom(shards[s]->n_local, ix0->n_global, d, &kg[s]));
   // sub-batch size: list codes fit 32 bits on every shard; memory on this device
-  int64_t qb = q;
+  int64_t qb = o.batch_queries > 0 ? std::min<int64_t>(q, o.batch_queries) : q;
   size_t free_b = 0, total_b = 0;
   CU(cudaMemGetInfo(&free_b, &total_b));
   size_t held = 0, per_q = (size_t)W * (kh + 1) * sizeof(ShardRec);
@@ -1126,16 +1147,12 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
       stats.tile_blocks += (int64_t)ctl_h.tile_blocks;
       stats.tile_draws += (int64_t)ctl_h.tile_draws;
       stats.level_mma_tiles += (int64_t)ctl_h.lmma_tiles;
-  stats.level_mma_tiles += (int64_t)ctl_h.lmma_tiles;
-  stats.tile_draws += (int64_t)ctl_h.tile_draws;
-  stats.level_mma_tiles += (int64_t)ctl_h.lmma_tiles;
       for (int a = 0; a < qn; ++a) {
         stats.draws += qs[a].draws;
         stats.exact_fallbacks += qs[a].nexact;
         stats.philox_blocks += qs[a].blocks;
       }
     }
-    if (status != AKNN_OK) break;
   }
   tm.open_a = all_a;
   tm.stop(PH_ALL);
@@ -1179,7 +1196,7 @@ extern "C" {
 
 aknn_status aknn_build(const uint8_t *points, int64_t n, int32_t d, aknn_index **out) {
   if (!points || !out) return fail(AKNN_EINVAL, "NULL argument");
-  TRY(validate_build(n, d));
+  TRY(validate_build(n, d, n));
   aknn_index *ix = nullptr;
   TRY(make_index(n, n, 0, d, &ix));
   cudaError_t e = cudaMemsetAsync(ix->X.p, 0, ix->X.bytes, ix->stream);
@@ -1197,7 +1214,7 @@ aknn_status aknn_build(const uint8_t *points, int64_t n, int32_t d, aknn_index *
 aknn_status aknn_build_async(const uint8_t *points_dev, int64_t n, int32_t d, void *cuda_stream,
                              aknn_index **out) {
   if (!points_dev || !out) return fail(AKNN_EINVAL, "NULL argument");
-  TRY(validate_build(n, d));
+  TRY(validate_build(n, d, n));
   aknn_index *ix = nullptr;
   TRY(make_index(n, n, 0, d, &ix));
   cudaStream_t s = (cudaStream_t)cuda_stream;
@@ -1228,7 +1245,9 @@ aknn_status aknn_build_shard(const uint8_t *shard, int64_t n_local, int64_t n_gl
                              int32_t d, const void *nccl_unique_id, int32_t rank, int32_t world,
                              aknn_index **out) {
   if (!shard || !out) return fail(AKNN_EINVAL, "NULL argument");
-  TRY(validate_build(n_local, d));
+  if (n_global < n_local || n_global >= (1ll << 31))
+    return fail(AKNN_EINVAL, "n_global=%lld < n_local=%lld", (long long)n_global, (long long)n_local);
+  TRY(validate_build(n_local, d, n_global));
   if (n_global < n_local || offset < 0 || offset + n_local > n_global || n_global >= (1ll << 31))
     return fail(AKNN_EINVAL, "shard [%lld, %lld) outside [0, %lld)", (long long)offset,
                 (long long)(offset + n_local), (long long)n_global);
@@ -1626,12 +1645,7 @@ aknn_status aknn_exact_async(const aknn_index *cix, const uint8_t *queries_dev, 
   const size_t szD = (size_t)qc * npad * 4, szQ = (size_t)qc * ix->pitch, szN = (size_t)qc * 4;
   TRY(ix->exact_ws.ensure(round_up(szD, 256) + round_up(szQ, 256) + szN));
   static const bool use_dp4a = getenv("AKNN_EXACT_DP4A") && getenv("AKNN_EXACT_DP4A")[0] == '1';
-  if (!use_dp4a && !ix->nx_ready) {
-    TRY(ix->nx.ensure(sizeof(int32_t) * (size_t)npad));
-    CU(cudaMemsetAsync(ix->nx.p, 0, sizeof(int32_t) * (size_t)npad, st));
-    CU(launch_row_norms(ix->X.as<uint8_t>(), ix->pitch, (int)n, ix->nx.as<int32_t>(), st));
-    ix->nx_ready = true;
-  }
+  if (!use_dp4a) TRY(ensure_row_norms(ix, st));
   for (int64_t r0 = 0; r0 < q; r0 += qc) {
     const int qn = (int)std::min<int64_t>(qc, q - r0);
     uint8_t *qpad = ix->exact_ws.as<uint8_t>(round_up(szD, 256));
@@ -1689,6 +1703,7 @@ void aknn_free(aknn_index *ix) {
   if (!ix) return;
   finish_pending(ix);  // its copies target ix->host
   if (ix->pending.ev) cudaEventDestroy(ix->pending.ev);
+  if (ix->nx_ev) cudaEventDestroy(ix->nx_ev);
 #ifdef AKNN_WITH_NCCL
   if (ix->comm) ncclCommDestroy(ix->comm);
 #endif

@@ -115,10 +115,13 @@ def _golden_alpha():
     return rows
 
 
-@pytest.mark.parametrize("row", _golden_alpha(), ids=lambda r: r["variant"])
+@pytest.mark.parametrize("row", _golden_alpha(),
+                         ids=lambda r: f"{r['variant']}-n{r['n']}-u{r['u']}-c{r['c']}")
 def test_alpha_worked_values(row):
-    """SPEC.md:78-79 worked values of alpha(1)."""
-    d = 16
+    """Worked values of alpha(u): SPEC.md:78-79 at u = 1, hand derivations at u > 1
+    (the u-dependent term 1.5 log(1 + log u) of footnote 2 and (1 + log u) of §5), and
+    the survey-time values at each config's last sampled level."""
+    d = max(16, row["u"] + 1)
     if row["variant"] == "theory":
         a = orc.alpha_theory(row["n"], row["delta"], d)
     else:
