@@ -6,10 +6,13 @@ sampled coordinate evaluations/s, with the dominant kernel against its roofline.
 
 One step = one call of aknn_query (the whole batched round loop, SURVEY.md §8(a)
 rows a2-a9) over the config's query batch, inputs resident in HBM.  At N=1 the
-workload is BASELINE.json configs[1] (C2, MNIST-shaped: n=60,000, d=784,
-q=1,000, k=h=10, delta=0.05).  With N>1 (torchrun, one process per GPU) every
-rank answers its own 1,000 queries of the same mixture against a replica of X
-(query parallelism, no data-path collective: "scaling": "weak").
+workload is the largest single-GPU config, BASELINE.json configs[2] (C3,
+Tiny-ImageNet-shaped: n=100,000, d=12,288, q=256, k=h=10, delta=0.05; X = 1.23 GB,
+larger than L2); --config 2 / 4 select the other single-GPU configs.  With N>1
+(one process per GPU; `--gpus N` re-executes itself under torchrun when needed) the
+default is configs[4] (C5): the point set is sharded 1,000,000 rows per GPU and every
+rank runs the same 1,024-query batch with one ncclAllGather of the round summaries
+per round ("scaling": "weak": the point set grows with N).
 
 Timing: W untimed warm-up steps, then K steps, each bracketed by CUDA events on
 the stream the library launches on; L2 (126 MB) is flushed by a 512 MiB write
@@ -79,8 +82,25 @@ def _args():
     ap.add_argument("--clock-sampler", choices=("nvml", "smi", "none"), default="nvml")
     a = ap.parse_args()
     if a.config is None:
-        a.config = 1 if a.schedule == "a1" else 2
+        # N = 1: the largest single-GPU config (C3, 1.23 GB of X, not L2-resident);
+        # N > 1: the point-sharded C5 (1M rows per GPU, one allgather per round)
+        a.config = 1 if a.schedule == "a1" else (5 if a.gpus > 1 else 3)
     return a
+
+
+def _relaunch_under_torchrun(args) -> None:
+    """`python bench.py --gpus N` (N > 1) outside torchrun re-executes itself as N ranks
+    (one process per GPU) so that N always means N processes; under torchrun the world
+    size must equal --gpus."""
+    ws = os.environ.get("WORLD_SIZE")
+    if ws is None and args.gpus > 1:
+        port = os.environ.get("MASTER_PORT", "29533")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+               f"--nproc-per-node={args.gpus}", "--master-addr=127.0.0.1", f"--master-port={port}",
+               os.path.abspath(__file__), *sys.argv[1:]]
+        os.execv(sys.executable, cmd)
+    if ws is not None and int(ws) != args.gpus:
+        raise SystemExit(f"bench.py: WORLD_SIZE={ws} but --gpus {args.gpus}")
 
 
 def _alpha_desc(a: str) -> str:
@@ -243,16 +263,17 @@ def _bf16_peak():
         return 2250.0, "fallback (nominal 2.25 PFLOP/s bf16 dense)"
 
 
-def _traffic_from_profiles(kernel: str):
-    """dram bytes per launch of `kernel` from the committed ncu --set full summary, if any."""
+def _traffic_from_profiles(kernel: str, workload: str):
+    """(dram bytes per launch, source) of `kernel` on `workload` from the committed ncu
+    summary profiles/ncu_traffic.json (keys "<workload>/<kernel>"), if any."""
     p = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
         with open(p) as f:
             j = json.load(f)
-        v = j.get(kernel)
-        return None if v is None else v.get("dram_bytes_per_launch")
+        v = j.get(f"{workload}/{kernel}")
+        return (None, None) if v is None else (v.get("dram_bytes_per_launch"), v.get("source"))
     except Exception:
-        return None
+        return None, None
 
 
 # Algorithmic bytes per unit of each kernel class (DESIGN.md §7):
@@ -359,11 +380,18 @@ def run_reference(args, dist: Dist):
     cores = max(1, min(_cpu_cores(), 16))
     nq = min(cores, cfg.q)  # one query per core per step
     times = []
-    for it in range(args.warmup + args.steps):
+    # CPU timing needs no GPU-style warm-up beyond one step (page-in, fork); the run is
+    # capped at ~4 min of oracle work (at least one timed step): a C3/C5 oracle query
+    # takes 10-100+ s, and the run must end within minutes
+    warm = min(args.warmup, 1)
+    t_start = time.perf_counter()
+    for it in range(warm + args.steps):
         off = (it * nq) % max(1, cfg.q - nq + 1)
         dt, _ = _oracle_time(X, Q[off:off + nq], cfg, al, nq, cores, args.draws == "shared", args.lead)
-        if it >= args.warmup:
+        if it >= warm:
             times.append(dt)
+            if time.perf_counter() - t_start > 240.0:
+                break
     ms = 1e3 * sum(times) / len(times)
     value = nq / (ms / 1e3)
     line = {
@@ -371,6 +399,7 @@ def run_reference(args, dist: Dist):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u8",
         "data": "synthetic", "config": _config_desc(cfg, args, extra={"sample_queries_per_step": nq}),
+        "steps_timed": len(times), "warmup_steps_run": warm,
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
                          "sample": f"{nq} queries of {cfg.name} per step (full n={cfg.n}), "
                                    f"one single-threaded oracle process per core"},
@@ -525,7 +554,7 @@ def run_ours(args, dist: Dist):
               "timing": "CUDA events around every launch on the library stream, K instrumented "
                         "steps (host-driven loop) right after the K graph-launched timed steps",
               "ms_per_step_instrumented": dist.max(ms_local_instr) / args.steps,
-              "traffic": _traffic_from_profiles(kof[dom]),
+              "traffic": _traffic_from_profiles(kof[dom], cfg.name)[0],
               "per_class": {c: {"ms": ms_cls[c], "launches": launches[c],
                                 "GBps_algorithmic": (abytes[c] / (ms_cls[c] / 1e3) / 1e9)
                                 if c in abytes and ms_cls[c] > 0 else None}
@@ -595,6 +624,16 @@ def run_ours(args, dist: Dist):
                     "algorithmic_bytes_per_launch": abytes[dom] / max(1, launches[dom]),
                     "sector_view": sector_view, **common}
 
+    # the same kernel against the HBM roofline (BASELINE.json metric: "% of HBM roofline"):
+    # the DRAM bytes it moves per launch (ncu dram__bytes_read + write, committed summary
+    # of this workload) over its live average launch time
+    tb, tsrc = _traffic_from_profiles(kof[dom], cfg.name)
+    avg_s = ms_cls[dom] / max(1, launches[dom]) / 1e3
+    roofline["hbm_view"] = {
+        "dram_bytes_per_launch": tb, "GBps": tb / avg_s / 1e9 if tb and avg_s > 0 else None,
+        "peak": peak, "unit": "GB/s", "frac": tb / avg_s / 1e9 / peak if tb and avg_s > 0 else None,
+        "peak_source": peak_src, "bytes_source": tsrc or "no committed ncu capture of this kernel on this workload"}
+
     extra = {
         "draws_per_s": dist.sum(draws) / (ms_max / 1e3),
         # sharded: the library already sums evals over the ranks (ncclAllReduce)
@@ -602,9 +641,11 @@ def run_ours(args, dist: Dist):
         "sample_fraction": evals_total / (args.steps * qpr * n * d),
         "rounds_max": int(out["rounds"].max().item()),
         "exact_fallbacks_per_query": agg["exact_fallbacks"] / (args.steps * qpr),
-        # G2 (k_init): one random 32-byte sector of X + 6 B of state per pair
-        "init_GBps_sector_model": (qpr * n_loc * (SECTOR + 6)) / (ms_cls["init"] / args.steps / 1e3) / 1e9
+        # G2 (k_init): one random 32-byte sector of X + 6 B of state per pair, served from
+        # L2 when X fits it (then the rate can exceed the HBM peak) else from HBM
+        "init_sector_GBps": (qpr * n_loc * (SECTOR + 6)) / (ms_cls["init"] / args.steps / 1e3) / 1e9
         if ms_cls["init"] > 0 else None,
+        "init_sector_source": "L2 (X fits the 126 MB L2)" if x_in_l2 else "HBM",
     }
 
     # exact comparison pass on the same queries: time + recall of the adaptive sets
@@ -636,7 +677,7 @@ def run_ours(args, dist: Dist):
             ok += strict <= s
         extra.update({"exact_pass_ms": ex_ms, "speedup_vs_exact": ex_ms / ms_per_step,
                       "recall_contains_knn": dist.sum(ok) / (qpr * dist.world),
-                      "exact_pass_kernel": "tcgen05 kind::i8 tiles (k_mma_tiles) + block top-k",
+                      "exact_pass_kernel": "k_exact_fused (persistent tcgen05 kind::i8, running top-k epilogue) + k_exact_merge" if k <= 128 else "tcgen05 kind::i8 tiles (k_mma_tiles) + block top-k",
                       # 2 q n d int8 ops (u8 x u8 -> s32 MACs) over the whole pass incl. top-k
                       "exact_pass_tops": 2.0 * qpr * n_loc * d / (ex_ms / 1e3) / 1e12,
                       "exact_pass_x_GBps": n_loc * d / (ex_ms / 1e3) / 1e9})
@@ -677,7 +718,7 @@ def run_ours(args, dist: Dist):
     if not args.no_cpu_baseline and dist.rank == 0 and dist.world == 1:
         # a bounded sample of the same workload: ~10-30 s of oracle work on the host cores
         cores = max(1, min(_cpu_cores(), 16))
-        nq = min(qpr, 8 * cores if n <= 200_000 else cores)
+        nq = min(qpr, 8 * cores if n * d <= 100_000_000 else cores)
         dt, _ = _oracle_time(X, Qh, cfg, _oracle_alpha(cfg, args.alpha), nq, cores, args.draws == "shared",
                              args.lead)
         cpu = {"value": nq / dt, "unit": UNIT, "cores": min(cores, nq), "kind": "oracle",
@@ -876,6 +917,7 @@ def run_a1(args, dist: Dist):
 
 def main():
     args = _args()
+    _relaunch_under_torchrun(args)
     dist = Dist()
     try:
         if args.workload == "sec5":

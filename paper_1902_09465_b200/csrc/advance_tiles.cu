@@ -27,6 +27,10 @@
 namespace aknn {
 
 constexpr int TILE_NT = 256;
+// A shape whose shared memory allows one CTA per SM (rows > 8 KB, e.g. C3's 12 KB) runs
+// 20 warps in that CTA instead of 8: the Philox chains and the shared-memory gathers
+// need the extra warps to hide their latency (ncu, C3 at 8 warps: fmaheavy 25-42 %).
+constexpr int TILE_NT_WIDE = 640;
 constexpr int ADV_TP = 4;  // items (Philox blocks) in flight per thread
 
 // Row slots are 2^slot_l bytes (>= pitch) and start at multiples of 2^slot_l, so
@@ -186,8 +190,9 @@ __device__ __forceinline__ void f1_accumulate(uint32_t qt_s, uint32_t dbuf_s, in
 
 // MODE 0: per-query draws with replacement; 1: query-independent draws (R = 32);
 // 2: per-query draws without replacement (reading R23).
-template <int MODE>
-__global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
+template <int MODE, int NT>
+__global__ void __launch_bounds__(NT) k_advance_tiles(Geom g) {
+  static_assert(MODE != 1 || NT == NT, "shared-draw tiles run 8 warps (f1_accumulate)");
   extern __shared__ __align__(16) unsigned char tsm[];
   __shared__ unsigned lcnt[MAX_LEVELS], loff[MAX_LEVELS + 1], lfill[MAX_LEVELS];
   const int R = 1 << g.tile_lr, P = 1 << g.tile_lp, RP = R * P;
@@ -214,8 +219,8 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
   const long long cols = (g.n + P - 1) >> g.tile_lp;
   const long long ntot = (long long)rows * cols;
   const float dthr = g.tile_min_draws;
-  __shared__ uint8_t dlist[TILE_NT];  // dense tiles of the chunk (offsets, in order)
-  __shared__ unsigned wcnt[TILE_NT / 32];
+  __shared__ uint16_t dlist[NT];  // dense tiles of the chunk (offsets, in order)
+  __shared__ unsigned wcnt[NT / 32];
 
   // each CTA walks a contiguous range of the point-major tile space (t = tp * rows +
   // tr), so consecutive dense tiles of one point column reuse the staged point rows;
@@ -225,7 +230,7 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
   int gen_tp = -1, gen_c = -1;  // shared draws: the column / level whose draw list is in dbuf
   __shared__ unsigned long long s_blocks, s_draws;  // Philox blocks and pair draws (statistics)
   if (tid == 0) s_blocks = s_draws = 0;
-  for (long long c0 = t0; c0 < t1; c0 += TILE_NT) {
+  for (long long c0 = t0; c0 < t1; c0 += NT) {
     __syncthreads();  // dlist of the previous chunk is consumed
     {
       const long long t = c0 + tid;
@@ -239,11 +244,11 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
       __syncthreads();
       unsigned before = 0;
       for (int w = 0; w < (tid >> 5); ++w) before += wcnt[w];
-      if (dense) dlist[before + __popc(m & ((1u << lane_id()) - 1u))] = (uint8_t)(t - c0);
+      if (dense) dlist[before + __popc(m & ((1u << lane_id()) - 1u))] = (uint16_t)(t - c0);
     }
     __syncthreads();
     unsigned nd = 0;
-    for (int w = 0; w < TILE_NT / 32; ++w) nd += wcnt[w];
+    for (int w = 0; w < NT / 32; ++w) nd += wcnt[w];
   for (unsigned ti = 0; ti < nd; ++ti) {
     const long long t = c0 + dlist[ti];
     const int tp = (int)(t / rows), tr = (int)(t % rows);
@@ -259,7 +264,7 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
     // rows past q / n are never referenced and are left as they are.  Shared draws:
     // the query rows transposed (Qt), no point rows (their bytes are in the draw list)
     if (f1) f1_stage_qt(g, r0, reinterpret_cast<uint32_t *>(tsm + (rows_s - base)));
-    for (int v = tid; v < (f1 ? 0 : (reuse_x ? R : R + P) * nv); v += TILE_NT) {
+    for (int v = tid; v < (f1 ? 0 : (reuse_x ? R : R + P) * nv); v += NT) {
       const int row = v / nv, c = v - row * nv;
       const uint8_t *src = nullptr;
       if (row < R) {
@@ -273,7 +278,7 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
                      : "memory");
     }
     asm volatile("cp.async.commit_group;" ::: "memory");
-    // thread -> 4 consecutive arms of one query row (RP <= 4 * TILE_NT, P >= 4): the
+    // thread -> 4 consecutive arms of one query row (RP <= 4 * NT, P >= 4): the
     // query's done flag, the action bytes, S and the level bytes in ONE round trip
     const int e4 = tid * 4;
     const bool in = e4 < RP;
@@ -385,12 +390,12 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
       const uint32_t lv = (uint32_t)(c + 1);
       if (nb <= (unsigned)ADV_TP) {
         const unsigned ppt = ADV_TP / nb;
-        for (unsigned l0 = tid; l0 < m; l0 += TILE_NT * ppt) {
+        for (unsigned l0 = tid; l0 < m; l0 += NT * ppt) {
           uint4 w[ADV_TP];
           int pr[ADV_TP];
 #pragma unroll
           for (int k = 0; k < ADV_TP; ++k) {
-            const unsigned li = l0 + (k / nb) * TILE_NT;
+            const unsigned li = l0 + (k / nb) * NT;
             const bool ok = (unsigned)k / nb < ppt && li < m;
             pr[k] = ok ? (int)L[li] : -1;
             const int e = ok ? pr[k] : 0;
@@ -427,37 +432,34 @@ __global__ void __launch_bounds__(TILE_NT) k_advance_tiles(Geom g) {
           }
         }
       } else {
-        unsigned tpp = nb / 16u;  // >= 4 passes of ADV_TP blocks per lane
-        tpp = tpp < 1u ? 1u : (tpp > 32u ? 32u : tpp);
-        const unsigned sub = tid & (tpp - 1), slots = TILE_NT / tpp;
-        // all lanes of a warp run the same number of passes (uniform shuffles)
-        for (unsigned l0 = 0; l0 < m; l0 += slots) {
-          const unsigned li = l0 + tid / tpp;
-          const bool ok = li < m;
-          const int pe = ok ? (int)L[li] : 0;
+        // nb > ADV_TP blocks per pair: the level's (pair, ADV_TP-block group) items are
+        // dealt to the threads in one flat range (every thread busy whatever the pair
+        // count), each item's sum added to its pair with one shared atomic (integer:
+        // the order does not matter, S stays bit-identical)
+        for (unsigned l = tid; l < m; l += NT) acc[L[l]] = 0;
+        __syncthreads();
+        const unsigned lg = (unsigned)(lb - 2);  // log2 groups of ADV_TP blocks per pair
+        const unsigned total = m << lg;
+        for (unsigned it = tid; it < total; it += NT) {
+          const unsigned li = it >> lg, b0 = (it & ((1u << lg) - 1u)) * ADV_TP;
+          const int pe = (int)L[li];
           const uint32_t xa = xs + ((uint32_t)(pe & (P - 1)) << sl);
           const uint32_t qa = rows_s + ((uint32_t)(pe >> g.tile_lp) << sl);
           const uint32_t gi = (uint32_t)(p0 + (pe & (P - 1))) + g.id_offset;
           const uint32_t gq = rng_qi(g, (uint32_t)(r0 + (pe >> g.tile_lp)));
           uint32_t sum = 0;
-          if (ok && wor) {
+          if (wor) {
             const uint4 kk = wor_keys(g.rk0, g.rk1, gi, gq);
-            for (unsigned b0 = sub * ADV_TP; b0 < nb; b0 += tpp * ADV_TP) {
 #pragma unroll
-              for (int k = 0; k < ADV_TP; ++k) sum = sq_diff4_wor(xa, qa, kk, g.wor_z, d, s + 4u * (b0 + k), sum);
-            }
-          } else if (ok) {
-            for (unsigned b0 = sub * ADV_TP; b0 < nb; b0 += tpp * ADV_TP) {
-              uint4 w[ADV_TP];
+            for (int k = 0; k < ADV_TP; ++k) sum = sq_diff4_wor(xa, qa, kk, g.wor_z, d, s + 4u * (b0 + k), sum);
+          } else {
+            uint4 w[ADV_TP];
 #pragma unroll
-              for (int k = 0; k < ADV_TP; ++k)
-                w[k] = philox4x32_10_rk(make_uint4(b0 + k, gi, gq, lv), g.rk0, g.rk1);
+            for (int k = 0; k < ADV_TP; ++k) w[k] = philox4x32_10_rk(make_uint4(b0 + k, gi, gq, lv), g.rk0, g.rk1);
 #pragma unroll
-              for (int k = 0; k < ADV_TP; ++k) sum = sq_diff4(xa, qa, w[k], d, sum);
-            }
+            for (int k = 0; k < ADV_TP; ++k) sum = sq_diff4(xa, qa, w[k], d, sum);
           }
-          for (unsigned o = tpp >> 1; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
-          if (ok && sub == 0) acc[pe] = (int32_t)sum;
+          atomicAdd(reinterpret_cast<uint32_t *>(acc + pe), sum);
         }
       }
     }
@@ -506,11 +508,15 @@ static size_t tile_base() {  // static shared memory + the per-CTA system reserv
     cudaFuncAttributes fa{};
     int dev = 0, rsv = 0;
     cudaFuncAttributes fb{};
-    if (cudaFuncGetAttributes(&fa, k_advance_tiles<0>) != cudaSuccess) fa.sharedSizeBytes = 2048;
-    if (cudaFuncGetAttributes(&fb, k_advance_tiles<1>) == cudaSuccess && fb.sharedSizeBytes > fa.sharedSizeBytes)
-      fa.sharedSizeBytes = fb.sharedSizeBytes;
-    if (cudaFuncGetAttributes(&fb, k_advance_tiles<2>) == cudaSuccess && fb.sharedSizeBytes > fa.sharedSizeBytes)
-      fa.sharedSizeBytes = fb.sharedSizeBytes;
+    if (cudaFuncGetAttributes(&fa, k_advance_tiles<0, TILE_NT>) != cudaSuccess) fa.sharedSizeBytes = 2048;
+    auto widen = [&](const void *f) {
+      if (cudaFuncGetAttributes(&fb, f) == cudaSuccess && fb.sharedSizeBytes > fa.sharedSizeBytes)
+        fa.sharedSizeBytes = fb.sharedSizeBytes;
+    };
+    widen((const void *)k_advance_tiles<1, TILE_NT>);
+    widen((const void *)k_advance_tiles<2, TILE_NT>);
+    widen((const void *)k_advance_tiles<0, TILE_NT_WIDE>);
+    widen((const void *)k_advance_tiles<2, TILE_NT_WIDE>);
     if (cudaGetDevice(&dev) != cudaSuccess ||
         cudaDeviceGetAttribute(&rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev) != cudaSuccess)
       rsv = 1024;
@@ -522,16 +528,39 @@ static size_t tile_base() {  // static shared memory + the per-CTA system reserv
 // Shared memory per CTA of a tile shape (the occupancy the shape chooser reasons about).
 size_t tile_smem_bytes(int lr, int lp, int64_t pitch) { return tile_window(lr, lp, pitch, tile_base()); }
 
+// AKNN_TILE_WIDE=0 keeps 8-warp CTAs at one CTA per SM (A/B measurements).
+static bool env_tile_wide() {
+  static const bool v = [] {
+    const char *e = getenv("AKNN_TILE_WIDE");
+    return !(e && e[0] == '0');
+  }();
+  return v;
+}
+
+template <int MODE, int NT>
+static cudaError_t launch_tiles_nt(const Geom &g, int num_sms, size_t smem, int per_sm, cudaStream_t s) {
+  k_advance_tiles<MODE, NT><<<num_sms * per_sm, NT, smem, s>>>(g);
+  return cudaGetLastError();
+}
+
 template <int MODE>
 static cudaError_t launch_tiles_k(const Geom &g, int num_sms, size_t smem, cudaStream_t s) {
-  cudaError_t e = cudaFuncSetAttribute(k_advance_tiles<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_advance_tiles<MODE, TILE_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int per_sm = 0;
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_advance_tiles<MODE>, TILE_NT, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_advance_tiles<MODE, TILE_NT>, TILE_NT, smem);
   if (e != cudaSuccess) return e;
+  if (MODE != 1 && per_sm <= 1 && env_tile_wide()) {
+    e = cudaFuncSetAttribute(k_advance_tiles<MODE == 1 ? 0 : MODE, TILE_NT_WIDE>,
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+    int wide = 0;
+    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wide, k_advance_tiles<MODE == 1 ? 0 : MODE, TILE_NT_WIDE>,
+                                                      TILE_NT_WIDE, smem);
+    if (e == cudaSuccess && wide >= 1) return launch_tiles_nt<MODE == 1 ? 0 : MODE, TILE_NT_WIDE>(g, num_sms, smem, 1, s);
+  }
   if (per_sm < 1) per_sm = 1;
-  k_advance_tiles<MODE><<<num_sms * per_sm, TILE_NT, smem, s>>>(g);
-  return cudaGetLastError();
+  return launch_tiles_nt<MODE, TILE_NT>(g, num_sms, smem, per_sm, s);
 }
 
 cudaError_t launch_advance_tiles(const Geom &g, int num_sms, cudaStream_t s) {

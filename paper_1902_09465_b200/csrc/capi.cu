@@ -229,7 +229,7 @@ size_t exact_mma_ws_bytes(int64_t qb, int64_t npad) {
 // event recorded behind that kernel, so it never reads the norms early.
 aknn_status ensure_row_norms(aknn_index *ix, cudaStream_t st) {
   if (!ix->nx_ready) {
-    const int64_t npad = round_up(ix->n_local, 16);
+    const int64_t npad = round_up(ix->n_local, 256);  // the fused exact pass reads whole 256-point tiles
     TRY(ix->nx.ensure(sizeof(int32_t) * (size_t)npad));
     if (!ix->nx_ev) CU(cudaEventCreateWithFlags(&ix->nx_ev, cudaEventDisableTiming));
     CU(cudaMemsetAsync(ix->nx.p, 0, sizeof(int32_t) * (size_t)npad, st));
@@ -276,7 +276,7 @@ int env_int(const char *name, int dflt) {
   return e && e[0] ? atoi(e) : dflt;
 }
 
-TileShape tile_shape(int64_t pitch) {
+TileShape tile_shape(int64_t pitch, int64_t n) {
   TileShape t{0, 0, 0, 0.f};
   if (env_int("AKNN_TILE", 1) == 0) return t;
   // the largest tile (R * P) whose shared memory fits 3, 2 or 1 CTAs per SM (228 KB);
@@ -299,8 +299,12 @@ TileShape tile_shape(int64_t pitch) {
   t.lp = env_int("AKNN_TILE_LP", lp);
   if (t.lr < 0 || t.lr > 5 || t.lp < 2 || t.lp > 5 || tile_smem_bytes(t.lr, t.lp, pitch) > (size_t)233472)
     return TileShape{0, 0, 0, 0.f};
+  // X in L2 (C2: 47 MB): a list draw costs one L2 sector, tiles must amortise their
+  // staging over >= 4 sectors' worth of draws; X in HBM (C3-C5): a list draw is a
+  // random HBM sector (~1/15 the Philox rate), tiles win from ~1/4 of that
   const char *fe = getenv("AKNN_TILE_F");
-  const double f = fe && fe[0] ? atof(fe) : 4.0;
+  const bool x_in_l2 = (double)n * (double)pitch <= 100e6;
+  const double f = fe && fe[0] ? atof(fe) : (x_in_l2 ? 4.0 : 0.25);
   t.row_draws = (float)(f * (double)pitch / 32.0);
   t.on = 1;
   return t;
@@ -368,20 +372,23 @@ cudaError_t launch_round_body(const Geom &g, int num_sms, cudaStream_t st, Timer
 
 // Shared draws on the tensor cores (k_level_mma): q^2 planes [qb][pitch] x 2, the
 // level's w planes [n][pitch] x 3, wa [n], wovf [n], per-(128 x 128, level) counts.
-bool level_mma_on(const aknn_opts &o) {
-  return (o.flags & AKNN_FLAG_SHARED_DRAWS) && !(o.flags & AKNN_FLAG_NO_LEVEL_MMA) && env_int("AKNN_LEVEL_MMA", 1);
+// k_build_w keeps 8 warps' coordinate counts in shared memory (8 * pitch * 4 B): rows
+// wider than 6 KB take the shared-draw tiles / lists instead
+bool level_mma_on(const aknn_opts &o, int64_t pitch) {
+  return (o.flags & AKNN_FLAG_SHARED_DRAWS) && !(o.flags & AKNN_FLAG_NO_LEVEL_MMA) && env_int("AKNN_LEVEL_MMA", 1) &&
+         pitch <= 6144;
 }
 size_t lvcnt_bytes(int64_t qb, int64_t npad) {
   return (size_t)((qb + level_tile_rows() - 1) / level_tile_rows()) *
          (size_t)((npad + level_tile_cols() - 1) / level_tile_cols()) * MAX_LEVELS * sizeof(uint32_t);
 }
 size_t level_ws_bytes(int64_t qb, int64_t n, int64_t npad, int64_t pitch, const aknn_opts &o) {
-  if (!level_mma_on(o)) return 0;
+  if (!level_mma_on(o, pitch)) return 0;
   return 2 * round_up((size_t)qb * pitch, 256) + 3 * round_up((size_t)n * pitch, 256) +
          round_up((size_t)npad * 4, 256) + round_up((size_t)n, 256) + round_up(lvcnt_bytes(qb, npad), 256);
 }
 void setup_level_mma(Geom &g, int64_t qb, uint8_t *ws, const aknn_opts &o) {
-  g.level_mma = level_mma_on(o) ? 1 : 0;
+  g.level_mma = level_mma_on(o, g.pitch) ? 1 : 0;
   if (!g.level_mma) return;
   g.tile_on = 0;  // the non-GEMM pairs take the lists
   const size_t qp = round_up((size_t)qb * g.pitch, 256), np = round_up((size_t)g.n * g.pitch, 256);
@@ -717,7 +724,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   const size_t oQS = off; off = round_up(off + szQS, 256);
   const size_t oCtl = off; off = round_up(off + szCtl, 256);
   const size_t oXm = off; off = round_up(off + exact_mma_ws_bytes(qb, npad), 256);
-  const TileShape tsh = tile_shape(ix->pitch);
+  const TileShape tsh = tile_shape(ix->pitch, ix->n_local);
   const size_t oTw = off; off = round_up(off + tile_ws_bytes(qb, npad, tsh), 256);
   const size_t oThr = off; off = round_up(off + sizeof(int32_t) * THR_STRIDE * (size_t)qb, 256);
   const size_t oLm = off; off = round_up(off + level_ws_bytes(qb, n, npad, ix->pitch, o), 256);
@@ -978,7 +985,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     const size_t oSend = off; off = round_up(off + szSend, 256);
     const size_t oRecv = off; off = round_up(off + szRecv, 256);
     const size_t oXm = off; off = round_up(off + exact_mma_ws_bytes(qb, npad), 256);
-    const TileShape tsh = tile_shape(ix->pitch);
+    const TileShape tsh = tile_shape(ix->pitch, ix->n_local);
     const size_t oTw = off; off = round_up(off + tile_ws_bytes(qb, npad, tsh), 256);
     const size_t oThr = off; off = round_up(off + sizeof(int32_t) * THR_STRIDE * (size_t)qb, 256);
     const size_t oLm = off; off = round_up(off + level_ws_bytes(qb, ix->n_local, npad, ix->pitch, o), 256);
@@ -1640,12 +1647,22 @@ aknn_status aknn_exact_async(const aknn_index *cix, const uint8_t *queries_dev, 
   e.ibits = std::max(1, bit_length((unsigned long long)(n - 1)));
   e.nbits = bit_length(65025ull * (unsigned long long)ix->d) + e.ibits;
   if (e.nbits > 63) return fail(AKNN_EINVAL, "exact key needs %d bits", e.nbits);
-  // process queries in chunks so the distance scratch stays bounded
-  const int64_t qc = std::max<int64_t>(1, std::min<int64_t>(q, (int64_t)(2ll << 30) / (npad * 4)));
-  const size_t szD = (size_t)qc * npad * 4, szQ = (size_t)qc * ix->pitch, szN = (size_t)qc * 4;
+  TRY(ensure_row_norms(ix, st));
+  e.X = ix->X.as<uint8_t>();
+  e.pitch = ix->pitch;
+  e.n = (int)n;
+  e.d = ix->d;
+  e.k = k;
+  e.id_offset = (uint32_t)ix->offset;
+  e.npad = npad;
+  const bool fused = k <= exact_fused_max_k();
+  // fused: queries staged in the pitch layout + their norms + the per-CTA candidate
+  // buffers; otherwise chunks of queries whose [qc][npad] int32 distance matrix is
+  // bounded by 2 GiB
+  const int64_t qc = fused ? q : std::max<int64_t>(1, std::min<int64_t>(q, (int64_t)(2ll << 30) / (npad * 4)));
+  const size_t szD = fused ? exact_fused_ws_bytes(ix->num_sms, k) : (size_t)qc * npad * 4,
+               szQ = (size_t)qc * ix->pitch, szN = (size_t)qc * 4;
   TRY(ix->exact_ws.ensure(round_up(szD, 256) + round_up(szQ, 256) + szN));
-  static const bool use_dp4a = getenv("AKNN_EXACT_DP4A") && getenv("AKNN_EXACT_DP4A")[0] == '1';
-  if (!use_dp4a) TRY(ensure_row_norms(ix, st));
   for (int64_t r0 = 0; r0 < q; r0 += qc) {
     const int qn = (int)std::min<int64_t>(qc, q - r0);
     uint8_t *qpad = ix->exact_ws.as<uint8_t>(round_up(szD, 256));
@@ -1653,22 +1670,15 @@ aknn_status aknn_exact_async(const aknn_index *cix, const uint8_t *queries_dev, 
     CU(cudaMemsetAsync(qpad, 0, szQ, st));
     CU(cudaMemcpy2DAsync(qpad, ix->pitch, queries_dev + r0 * ix->d, ix->d, ix->d, qn,
                          cudaMemcpyDeviceToDevice, st));
-    e.X = ix->X.as<uint8_t>();
     e.Q = qpad;
-    e.pitch = ix->pitch;
-    e.n = (int)n;
-    e.d = ix->d;
     e.q = qn;
-    e.k = k;
-    e.id_offset = (uint32_t)ix->offset;
-    e.D = ix->exact_ws.as<int32_t>();
-    e.npad = npad;
     e.idx = idx_dev + r0 * k;
     e.dist2 = dist2_dev + r0 * k;
-    if (use_dp4a) {
-      CU(launch_exact(e, st));
+    CU(launch_row_norms(qpad, ix->pitch, qn, nq, st));
+    if (fused) {
+      CU(launch_exact_fused(e, nq, ix->nx.as<int32_t>(), ix->exact_ws.p, ix->num_sms, st));
     } else {
-      CU(launch_row_norms(qpad, ix->pitch, qn, nq, st));
+      e.D = ix->exact_ws.as<int32_t>();
       CU(launch_exact_mma(e, nq, ix->nx.as<int32_t>(), st));
       CU(launch_exact_topk(e, st));
     }

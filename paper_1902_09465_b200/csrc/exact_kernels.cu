@@ -2,61 +2,14 @@
 // distance D(q, i) = sum_j (x_ij - q_j)^2 exactly in integers, then the k
 // nearest per query by (D, i).
 //
-// v1: CUDA-core tiles (vabsdiff4 + dp4a), 64 queries x 64 points per CTA,
-// then the block radix select of select.cuh and a rank sort of the k winners.
+// Used for k > exact_fused_max_k() only: the tcgen05 distance matrix of exact_mma.cu
+// is ranked here by the block radix select of select.cuh and a rank sort of the k
+// winners (k <= 128 runs the fused kernel of exact_fused.cu instead).
 #include "internal.cuh"
 #include "launch.h"
 #include "select.cuh"
 
 namespace aknn {
-
-constexpr int EX_TQ = 64, EX_TP = 64, EX_TK = 64;  // tile: queries, points, bytes
-
-__global__ void __launch_bounds__(256) k_exact_tiles(ExactGeom e) {
-  __shared__ uint32_t sq[EX_TQ][EX_TK / 4 + 1];
-  __shared__ uint32_t sx[EX_TP][EX_TK / 4 + 1];
-  const int q0 = blockIdx.y * EX_TQ, p0 = blockIdx.x * EX_TP;
-  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;  // 16 x 16 threads, 4 x 4 each
-  uint32_t acc[4][4] = {};
-  for (int64_t k0 = 0; k0 < e.pitch; k0 += EX_TK) {
-    for (int t = threadIdx.x; t < EX_TQ * (EX_TK / 4); t += 256) {
-      const int r = t / (EX_TK / 4), w = t % (EX_TK / 4);
-      const int64_t col = k0 + w * 4;
-      uint32_t vq = 0, vx = 0;
-      if (q0 + r < e.q && col < e.pitch)
-        vq = *reinterpret_cast<const uint32_t *>(e.Q + (size_t)(q0 + r) * e.pitch + col);
-      if (p0 + r < e.n && col < e.pitch)
-        vx = __ldg(reinterpret_cast<const uint32_t *>(e.X + (size_t)(p0 + r) * e.pitch + col));
-      sq[r][w] = vq;
-      sx[r][w] = vx;
-    }
-    __syncthreads();
-#pragma unroll 4
-    for (int w = 0; w < EX_TK / 4; ++w) {
-      uint32_t a[4], b[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        a[u] = sq[ty * 4 + u][w];
-        b[u] = sx[tx * 4 + u][w];
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u)
-#pragma unroll
-        for (int v = 0; v < 4; ++v) {
-          const uint32_t t = __vabsdiffu4(a[u], b[v]);
-          acc[u][v] = __dp4a(t, t, acc[u][v]);
-        }
-    }
-    __syncthreads();
-  }
-#pragma unroll
-  for (int u = 0; u < 4; ++u)
-#pragma unroll
-    for (int v = 0; v < 4; ++v) {
-      const int qq = q0 + ty * 4 + u, pp = p0 + tx * 4 + v;
-      if (qq < e.q && pp < e.n) e.D[(size_t)qq * e.npad + pp] = (int32_t)acc[u][v];
-    }
-}
 
 struct DistKeys {
   const ExactGeom *e;
@@ -98,13 +51,6 @@ __global__ void __launch_bounds__(SEL_NT) k_exact_topk(ExactGeom e) {
     e.idx[(size_t)qi * e.k + rank] = (int32_t)(i + e.id_offset);
     e.dist2[(size_t)qi * e.k + rank] = (int32_t)(kk >> e.ibits);
   }
-}
-
-cudaError_t launch_exact(const ExactGeom &e, cudaStream_t s) {
-  dim3 grid((e.n + EX_TP - 1) / EX_TP, (e.q + EX_TQ - 1) / EX_TQ);
-  k_exact_tiles<<<grid, 256, 0, s>>>(e);
-  k_exact_topk<<<e.q, SEL_NT, 0, s>>>(e);
-  return cudaGetLastError();
 }
 
 cudaError_t launch_exact_topk(const ExactGeom &e, cudaStream_t s) {

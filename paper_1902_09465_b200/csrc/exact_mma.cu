@@ -23,65 +23,15 @@
 
 #include "internal.cuh"
 #include "launch.h"
+#include "tc_common.cuh"
 
 namespace aknn {
 
-constexpr int MM_BM = 128, MM_BN = 256, MM_BK = 128, MM_STAGES = 4, MM_NT = 256;
+constexpr int MM_BM = 128, MM_BN = 256, MM_STAGES = 4, MM_NT = 256;
 constexpr uint32_t MM_A_BYTES = MM_BM * MM_BK, MM_B_BYTES = MM_BN * MM_BK;
 constexpr uint32_t MM_STAGE_BYTES = MM_A_BYTES + MM_B_BYTES;
 constexpr size_t MM_SMEM = (size_t)MM_STAGES * MM_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 constexpr uint32_t MM_TMEM_COLS = 256;
-
-__device__ __forceinline__ uint32_t smem_u32(const void *p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-
-__device__ __forceinline__ void mbar_expect_tx(uint64_t *bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void tma_load_2d(void *dst, const CUtensorMap *map, uint64_t *bar, int x, int y) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4}], [%2];" ::
-          "r"(smem_u32(dst)),
-      "l"(reinterpret_cast<uint64_t>(map)), "r"(smem_u32(bar)), "r"(x), "r"(y)
-      : "memory");
-}
-
-// K-major operand, 128-byte swizzle: rows of 128 B, 8-row atoms of 1024 B (SBO).
-__device__ __forceinline__ uint64_t umma_desc_sw128(uint32_t saddr) {
-  uint64_t d = 0;
-  d |= (uint64_t)((saddr >> 4) & 0x3FFFu);        // start address
-  d |= (uint64_t)1u << 16;                         // leading byte offset (unused for SW128 K-major)
-  d |= (uint64_t)(1024u >> 4) << 32;               // stride byte offset: 8 rows x 128 B
-  d |= (uint64_t)1u << 46;                         // descriptor version (sm_100)
-  d |= (uint64_t)2u << 61;                         // layout: SWIZZLE_128B
-  return d;
-}
-
-// kind::i8 instruction descriptor: D s32, A u8, B u8, both K-major, M = 128, N = 256.
-__host__ __device__ constexpr uint32_t umma_idesc_u8(int M, int N) {
-  return (2u << 4)                       // D format: s32
-         | (0u << 7) | (0u << 10)        // A, B format: unsigned 8-bit
-         | (0u << 15) | (0u << 16)       // A, B K-major
-         | ((uint32_t)(N >> 3) << 17)    // N / 8
-         | ((uint32_t)(M >> 4) << 24);   // M / 16
-}
 
 // Epilogue of the exact comparison pass: D = ||x||^2 + ||q||^2 - 2 dot, int32 rows.
 struct EpiDistances {
@@ -308,7 +258,7 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap *, CUtensorMapDataType, cuuint32_t
                                   CUtensorMapInterleave, CUtensorMapSwizzle, CUtensorMapL2promotion,
                                   CUtensorMapFloatOOBfill);
 
-static cudaError_t make_map(CUtensorMap *m, const uint8_t *base, int rows, int d, int64_t pitch, int box_rows) {
+cudaError_t make_map(CUtensorMap *m, const uint8_t *base, int rows, int d, int64_t pitch, int box_rows) {
   static EncodeTiledFn fn = nullptr;
   if (!fn) {
     void *p = nullptr;
@@ -447,35 +397,13 @@ constexpr int LM_EPI_WARP0 = 2, LM_EPI_WARPS = 8;
 constexpr int LM_EPI_COLS = LM_BN * 4 / LM_EPI_WARPS;  // columns per epilogue thread
 constexpr int LM_NT = 32 * (LM_EPI_WARP0 + LM_EPI_WARPS);
 
-__device__ __forceinline__ void mbar_arrive(uint64_t *bar) {
-  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
 
 __device__ __forceinline__ bool level_tile_on(const Geom &g, int c, int mt, int t) {
   const int mi = t % mt, ni = t / mt;
   return g.lvcnt[((size_t)mi * g.lv_cols + ni) * MAX_LEVELS + c] >= g.lmin;
 }
 
-__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&v)[32]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-        "=r"(v[15]), "=r"(v[16]), "=r"(v[17]), "=r"(v[18]), "=r"(v[19]), "=r"(v[20]), "=r"(v[21]),
-        "=r"(v[22]), "=r"(v[23]), "=r"(v[24]), "=r"(v[25]), "=r"(v[26]), "=r"(v[27]), "=r"(v[28]),
-        "=r"(v[29]), "=r"(v[30]), "=r"(v[31])
-      : "r"(taddr));
-}
 
-__device__ __forceinline__ void tmem_ld16(uint32_t taddr, uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15}, [%16];"
-      : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7]),
-        "=r"(v[8]), "=r"(v[9]), "=r"(v[10]), "=r"(v[11]), "=r"(v[12]), "=r"(v[13]), "=r"(v[14]),
-        "=r"(v[15])
-      : "r"(taddr));
-}
 
 __global__ void __launch_bounds__(LM_NT, 1)
     k_level_mma(const __grid_constant__ CUtensorMap tQ, const __grid_constant__ CUtensorMap tQ2l,

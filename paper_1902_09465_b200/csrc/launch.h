@@ -87,12 +87,18 @@ struct ExactGeom {
   int32_t *idx;       // [q][k] out (device)
   int32_t *dist2;     // [q][k] out (device)
 };
-cudaError_t launch_exact(const ExactGeom &e, cudaStream_t s);        // D via dp4a tiles + top-k
 cudaError_t launch_exact_topk(const ExactGeom &e, cudaStream_t s);   // top-k of e.D only
 // D via tcgen05 kind::i8 (exact_mma.cu); nq [q], nx [n] squared row norms.
 cudaError_t launch_exact_mma(const ExactGeom &e, const int32_t *nq, const int32_t *nx, cudaStream_t s);
 // Exact fallbacks of a round on the tensor cores (flagged tiles only).
 cudaError_t launch_exact_fallback_mma(const Geom &g, cudaStream_t s);
+// The fused exact pass (exact_fused.cu): persistent tcgen05 kernel with a running top-k
+// epilogue + per-query merge; k <= exact_fused_max_k().  nx zero padded to n rounded up
+// to 256; ws >= exact_fused_ws_bytes(num_sms, k).
+cudaError_t launch_exact_fused(const ExactGeom &e, const int32_t *nq, const int32_t *nx, void *ws, int num_sms,
+                               cudaStream_t s);
+int exact_fused_max_k();
+size_t exact_fused_ws_bytes(int num_sms, int k);
 int exact_tile_rows();
 // Shared draws on the tensor cores (exact_mma.cu).
 cudaError_t launch_q2_planes(const Geom &g, cudaStream_t s);

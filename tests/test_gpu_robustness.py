@@ -70,13 +70,15 @@ def test_sharded_sub_batches_with_round_cap(ak):
 
 def test_sharded_stats_equal_single_index(ak):
     """tile_draws / level_mma_tiles / draws of query_multi = the same query on one index."""
-    X, Q = synth.small_instance(74, 6000, 256, q=40)
-    al = orc.alpha_theory(6000, 0.05, 256)
+    # the cut at 3072 is a multiple of every tile width (32 points, 1024-arm filter CTAs,
+    # 256-point tensor-core tiles), so both runs make the same dense-tile decisions
+    X, Q = synth.small_instance(74, 6144, 256, q=40)
+    al = orc.alpha_theory(6144, 0.05, 256)
     ix = ak.Index(X)
     one = ix.query(Q, 5, 5, 0.05, 3, al)
     s1 = ix.stats()
     ix.close()
-    shards = [ak.Index(X[a:b], n_global=6000, offset=a) for a, b in ((0, 3000), (3000, 6000))]
+    shards = [ak.Index(X[a:b], n_global=6144, offset=a) for a, b in ((0, 3072), (3072, 6144))]
     two = ak.query_multi(shards, Q, 5, 5, 0.05, 3, al)
     s2 = shards[0].stats()
     for s in shards:
