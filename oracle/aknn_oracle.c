@@ -18,7 +18,10 @@
  *   orc_bruteforce        pinned: numpy / torch._int_mm brute force
  *   orc_round_step        pinned: hand-built states (S:139-171 examples), brute sort
  *   orc_query_br          pinned: planted set, d=1, all-exact, Theorem-1 rate,
- *                         closed-form draw/eval accounting, A1 stream prefix
+ *                         closed-form draw/eval accounting, A1 stream prefix;
+ *                         growth schedule: hand-written count sequences, growth 1
+ *                         = BR, per-arm sums = prefixes of the arm's own stream
+ *   orc_next_count        pinned: hand-written sequences of G_1, G_2, G_4
  *   orc_wor_*             pinned: exhaustive bijection of [0, d) (many d, keys),
  *                         uniformity of pi(t) over keys, A1 full-permutation
  *                         sums equal brute force, evals = sum of counts
@@ -378,6 +381,32 @@ int orc_round_step(int64_t n, int32_t d, const int64_t *S, const int32_t *T, int
 }
 
 /* ------------------------------------------------------------------------ */
+/* Growth schedule of R6 (reading R25).      */
+/* The paper increments T by one per selection; the batched rule  */
+/* doubles it (reading R7).  A growth factor < 2 takes the next count from the */
+/* grid G_m = { (m + r) 2^j / m : j >= 0, 0 <= r < m } of integers: m = 1 is   */
+/* doubling (1, 2, 4, 8, ...), m = 2 the schedule 1, 2, 3, 4, 6, 8, 12, 16, ... */
+/* (factors 3/2 and 4/3, sqrt 2 per level on average).  Every power of two is  */
+/* in G_m, so each advance [T, next(T)) lies inside one sample level b of the  */
+/* Draw stream.                                                               */
+/* ------------------------------------------------------------------------ */
+
+/* The smallest integer of G_m greater than T (T >= 1, m in {1, 2, 4}).        */
+int64_t orc_next_count(int64_t T, int32_t m) {
+  int64_t best = -1;
+  for (int32_t j = 0; j < 62; ++j) {
+    for (int32_t r = 0; r < m; ++r) {
+      const int64_t v = (int64_t)(m + r) << j;
+      if (v % m != 0) continue;
+      const int64_t c = v / m;
+      if (c > T && (best < 0 || c < best)) best = c;
+    }
+    if (((int64_t)1 << j) > 2 * T) break;
+  }
+  return best;
+}
+
+/* ------------------------------------------------------------------------ */
 /* The batched round rule BR, one query at a time.         */
 /* ------------------------------------------------------------------------ */
 
@@ -392,10 +421,11 @@ int orc_round_step(int64_t n, int32_t d, const int64_t *S, const int32_t *T, int
  */
 int orc_query_br(const uint8_t *X, int64_t n, int32_t d, const uint8_t *Qrows, int32_t q,
                  const int32_t *qids, int64_t id_offset, int32_t k, int32_t h, uint64_t seed,
-                 const double *alpha, int32_t max_rounds, int32_t wor, int32_t lead,
+                 const double *alpha, int32_t max_rounds, int32_t wor, int32_t lead, int32_t growth,
                  int32_t *sets, double *dhat, int32_t *counts, int64_t *sums, int64_t *evals,
                  int64_t *draws, int32_t *rounds) {
-  if (n < 2 || d < 1 || q < 0 || k < 1 || h < 0 || (int64_t)k + h >= n || !alpha || !sets)
+  if (n < 2 || d < 1 || q < 0 || k < 1 || h < 0 || (int64_t)k + h >= n || !alpha || !sets ||
+      !(growth == 0 || growth == 1 || growth == 2 || growth == 4))
     return ORC_EINVAL;
   int64_t *S = (int64_t *)malloc(sizeof(int64_t) * (size_t)n);
   int32_t *T = (int32_t *)malloc(sizeof(int32_t) * (size_t)n);
@@ -437,7 +467,9 @@ int orc_query_br(const uint8_t *X, int64_t n, int32_t d, const uint8_t *Qrows, i
           if (!act[i] || (pass > 0 && !(act[i] & 2)) || T[i] == d) continue;
           if (pass == 0) ++nact;
           const uint8_t *xi = X + (size_t)i * d;
-          if (2 * (int64_t)T[i] >= d) {
+          /* the next count: 2T (reading R7), or the next grid value of reading R25 */
+          const int64_t Tn = growth > 1 ? orc_next_count(T[i], growth) : 2 * (int64_t)T[i];
+          if (Tn >= d) {
             /* P:176 exact fallback, taken before the draws that would reach m;
              * charged d evaluations, or without replacement the d - T
              * coordinates the permutation had not drawn yet (reading R23)   */
@@ -445,10 +477,10 @@ int orc_query_br(const uint8_t *X, int64_t n, int32_t d, const uint8_t *Qrows, i
             ncharge += wor ? (int64_t)d - T[i] : (int64_t)d;
             T[i] = d;
           } else {
-            for (int64_t t = T[i]; t < 2 * (int64_t)T[i]; ++t)
+            for (int64_t t = T[i]; t < Tn; ++t)
               S[i] += draw_sq(xi, x, seed, qi, (uint32_t)(i + id_offset), t, (uint32_t)d, wor);
-            ndraws += T[i];
-            T[i] *= 2;
+            ndraws += Tn - T[i];
+            T[i] = (int32_t)Tn;
           }
         }
       }

@@ -53,7 +53,9 @@ def lib():
                                      P, P, P, P, P]
         L.orc_query_br.argtypes = [P, C.c_int64, C.c_int32, P, C.c_int32, P, C.c_int64,
                                    C.c_int32, C.c_int32, C.c_uint64, P, C.c_int32,
-                                   C.c_int32, C.c_int32, P, P, P, P, P, P, P]
+                                   C.c_int32, C.c_int32, C.c_int32, P, P, P, P, P, P, P]
+        L.orc_next_count.argtypes = [C.c_int64, C.c_int32]
+        L.orc_next_count.restype = C.c_int64
         L.orc_query_a1.argtypes = [P, C.c_int64, C.c_int32, P, C.c_int32, C.c_int32,
                                    C.c_int32, C.c_uint64, P, C.c_int64, C.c_int32, P, P, P, P, P, P]
         L.orc_wor_radix.argtypes = [C.c_uint32, P, P]
@@ -146,7 +148,8 @@ SHARED_QI = 0xFFFFFFFF  # the counter word of query-independent draws (SURVEY §
 
 def query_br(X, Q, k: int, h: int, seed: int, alpha, qids=None, id_offset: int = 0,
              max_rounds: int = 0, want_counts: bool = True, want_sums: bool = False,
-             shared_draws: bool = False, without_replacement: bool = False, lead: int = 1):
+             shared_draws: bool = False, without_replacement: bool = False, lead: int = 1,
+             growth: int = 1):
     """Batched round rule BR, one query at a time.  shared_draws:
     every query's counter word is SHARED_QI, i.e. arm i's t-th coordinate is the same
     for all queries; each query alone is unchanged in law."""
@@ -167,13 +170,18 @@ def query_br(X, Q, k: int, h: int, seed: int, alpha, qids=None, id_offset: int =
         evals=np.zeros(q, np.int64), draws=np.zeros(q, np.int64), rounds=np.zeros(q, np.int32))
     rc = lib().orc_query_br(_p(X), n, d, _p(Q), q, _p(qids), id_offset, k, h,
                             C.c_uint64(seed & (2**64 - 1)), _p(alpha), max_rounds,
-                            1 if without_replacement else 0, lead, _p(out["sets"]), _p(out["dhat"]), _p(out["counts"]),
+                            1 if without_replacement else 0, lead, growth, _p(out["sets"]), _p(out["dhat"]), _p(out["counts"]),
                             _p(out["sums"]), _p(out["evals"]), _p(out["draws"]),
                             _p(out["rounds"]))
     out["status"] = rc
     if rc not in (OK, EMAXROUNDS):
         raise ValueError(f"query_br rc={rc}")
     return out
+
+
+def next_count(T: int, m: int) -> int:
+    """The next per-arm sample count after T under the growth-m schedule (reading R25)."""
+    return int(lib().orc_next_count(T, m))
 
 
 def query_a1(X, x, k: int, h: int, seed: int, alpha, qi: int = 0, max_iters: int = 0,
