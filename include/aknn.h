@@ -90,6 +90,16 @@ typedef struct {
                          (query, point) pair; the automatic size fits 60 % of
                          free device memory).  Results do not depend on it.
                          Ignored by the Algorithm-1 entry points.  < 0: EINVAL */
+  int32_t growth;     /* sample-count schedule of an advance (SURVEY.md §8(f) row 4,
+                         DESIGN.md reading R25): 0 or 1 = doubling T -> 2T (reading
+                         R7); 2 = growth factor < 2: T runs through 1, 2, 3, 4, 6,
+                         8, 12, 16, ... (factors 3/2 and 4/3; the advance from T
+                         draws the next count minus T samples, the exact fallback
+                         of P:176 when the next count would reach d).  Growth 2
+                         runs the list path (no shared-memory tiles) and needs
+                         per-query draws with replacement (EINVAL with
+                         AKNN_FLAG_SHARED_DRAWS / _WITHOUT_REPLACEMENT); other
+                         values: EINVAL.  Ignored by the Algorithm-1 entry points. */
 } aknn_opts;
 
 #define AKNN_FLAG_RADIX_SELECT 1
@@ -206,6 +216,15 @@ aknn_status aknn_build_shard(const uint8_t *shard, int64_t n_local, int64_t n_gl
  * evals, draws and rounds are then identical on every rank (global ids), and
  * counts/sums hold this rank's n_local columns.  Needs world * (k+h) <= 16384
  * and n_local > k + h on every rank.                                          */
+
+/* Failure detection of the sharded query: while a rank waits for a
+ * round it also polls ncclCommGetAsyncError and a wall-clock deadline; on a peer
+ * error or when no progress is made for timeout_ms (default 300000; 0 = no
+ * deadline) it calls ncclCommAbort -- the pending collective then fails on every
+ * rank instead of hanging -- and returns AKNN_ENCCL.  An aborted index returns
+ * AKNN_ENCCL from every later sharded query (rebuild it).  EINVAL: NULL index or
+ * timeout_ms < 0.  No effect on indexes without a communicator.              */
+aknn_status aknn_set_timeout(aknn_index *ix, double timeout_ms);
 
 /* Write a fresh ncclUniqueId (128 bytes) to `id_out`.                       */
 aknn_status aknn_nccl_unique_id(void *id_out);

@@ -44,7 +44,8 @@ class Result(C.Structure):
 
 class Opts(C.Structure):
     _fields_ = [("qi_offset", C.c_int32), ("max_rounds", C.c_int32), ("timing", C.c_int32),
-                ("flags", C.c_int32), ("lead", C.c_int32), ("batch_queries", C.c_int32)]
+                ("flags", C.c_int32), ("lead", C.c_int32), ("batch_queries", C.c_int32),
+                ("growth", C.c_int32)]
 
 
 FLAG_RADIX_SELECT = 1
@@ -89,6 +90,7 @@ _sig = {
     "aknn_build_async": ([_P, _L, _I, _P, C.POINTER(_P)], _I),
     "aknn_build_shard": ([_P, _L, _L, _L, _I, _P, _I, _I, C.POINTER(_P)], _I),
     "aknn_nccl_unique_id": ([_P], _I),
+    "aknn_set_timeout": ([_P, C.c_double], _I),
     "aknn_query": ([_P, _P, _I, _I, _I, C.c_double, C.c_uint64, _P, C.POINTER(Result)], _I),
     "aknn_query_ex": ([_P, _P, _I, _I, _I, C.c_double, C.c_uint64, _P, C.POINTER(Opts),
                        C.POINTER(Result)], _I),
@@ -144,7 +146,7 @@ def alpha_table(n: int, delta: float, d: int, kind: str = "theory", c_alpha: flo
 def query_multi(shards, queries, k: int, h: int, delta: float, seed: int = 0, alpha=None, *,
                 counts: bool = True, sums: bool = False, dhat: bool = True, max_rounds: int = 0,
                 qi_offset: int = 0, timing: bool = False, flags: int = 0, lead: int = 1,
-                batch_queries: int = 0) -> dict:
+                batch_queries: int = 0, growth: int = 1) -> dict:
     """aknn_query_multi: one query batch over shard indices on the current device.
 
     ``shards`` are Index objects built with ``Index(rows, n_global=..., offset=...)``
@@ -168,7 +170,7 @@ def query_multi(shards, queries, k: int, h: int, delta: float, seed: int = 0, al
     if al is not None and al.shape != (d + 1,):
         raise AknnError(AKNN_EINVAL, f"alpha must have d+1={d + 1} entries")
     arr = (_P * len(shards))(*[s._h for s in shards])
-    opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags, lead, batch_queries)
+    opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags, lead, batch_queries, growth)
     st = _lib.aknn_query_multi(arr, len(shards), _ptr(Q), q, k, h, delta, seed & (2**64 - 1),
                                _ptr(al), C.byref(opts), C.byref(res))
     out["status"] = st
@@ -246,6 +248,10 @@ class Index:
         self.n_global = int(_lib.aknn_index_n_global(h))
         self.d = int(_lib.aknn_index_dim(h))
 
+    def set_timeout(self, timeout_ms: float):
+        """aknn_set_timeout: deadline of a sharded round (peer failure detection)."""
+        _check(_lib.aknn_set_timeout(self._h, float(timeout_ms)))
+
     def close(self):
         if getattr(self, "_h", None) and _lib is not None:
             _lib.aknn_free(self._h)
@@ -258,7 +264,8 @@ class Index:
     def query(self, queries, k: int, h: int, delta: float, seed: int = 0, alpha=None, *,
               counts: bool = True, sums: bool = False, dhat: bool = True, max_rounds: int = 0,
               qi_offset: int = 0, timing: bool = False, out: Optional[dict] = None,
-              flags: int = 0, schedule: str = "br", lead: int = 1, batch_queries: int = 0) -> dict:
+              flags: int = 0, schedule: str = "br", lead: int = 1, batch_queries: int = 0,
+              growth: int = 1) -> dict:
         """aknn_query_ex on host arrays; returns numpy arrays.
 
         ``schedule="a1"`` runs the literal Algorithm 1 instead (aknn_query_a1;
@@ -295,7 +302,7 @@ class Index:
         al = None if alpha is None else np.ascontiguousarray(alpha, np.float64)
         if al is not None and al.shape != (self.d + 1,):
             raise AknnError(AKNN_EINVAL, f"alpha must have d+1={self.d + 1} entries")
-        opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags, lead, batch_queries)
+        opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags, lead, batch_queries, growth)
         fn = _lib.aknn_query_a1 if schedule == "a1" else _lib.aknn_query_ex
         st = fn(self._h, _ptr(Q), q, k, h, delta, seed & (2**64 - 1), _ptr(al), C.byref(opts),
                 C.byref(res))
@@ -308,7 +315,8 @@ class Index:
                      counts: bool = False, sums: bool = False, dhat: bool = True,
                      max_rounds: int = 0, qi_offset: int = 0, timing: bool = False,
                      stream=None, out: Optional[dict] = None, flags: int = 0,
-                     schedule: str = "br", lead: int = 1, batch_queries: int = 0) -> dict:
+                     schedule: str = "br", lead: int = 1, batch_queries: int = 0,
+                     growth: int = 1) -> dict:
         """aknn_query_async on torch CUDA tensors (current stream); returns device tensors.
 
         ``schedule="a1"``: the literal Algorithm 1 (aknn_query_a1_device; waits for the
@@ -339,7 +347,7 @@ class Index:
                 torch.as_tensor(np.ascontiguousarray(alpha, np.float64)).to(dev)
             if al.dtype != torch.float64 or al.numel() != self.d + 1 or not al.is_contiguous():
                 raise AknnError(AKNN_EINVAL, f"alpha must be a contiguous float64 tensor of d+1={self.d + 1} entries")
-        opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags, lead, batch_queries)
+        opts = Opts(qi_offset, max_rounds, 1 if timing else 0, flags, lead, batch_queries, growth)
         fn = _lib.aknn_query_a1_device if schedule == "a1" else _lib.aknn_query_async
         st = fn(self._h, _ptr(Q), q, k, h, delta, seed & (2**64 - 1), _ptr(al), C.byref(opts),
                 C.byref(res), _stream_ptr(stream))

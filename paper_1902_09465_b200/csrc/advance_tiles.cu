@@ -537,38 +537,53 @@ static bool env_tile_wide() {
   return v;
 }
 
+// Dynamic shared memory of one instantiation: its own static size + the reservation
+// places the dynamic window (the slot alignment of the rows depends on where it starts).
 template <int MODE, int NT>
-static cudaError_t launch_tiles_nt(const Geom &g, int num_sms, size_t smem, int per_sm, cudaStream_t s) {
-  k_advance_tiles<MODE, NT><<<num_sms * per_sm, NT, smem, s>>>(g);
+static size_t tiles_dyn_smem(const Geom &g) {
+  cudaFuncAttributes fa{};
+  int dev = 0, rsv = 0;
+  if (cudaFuncGetAttributes(&fa, k_advance_tiles<MODE, NT>) != cudaSuccess) fa.sharedSizeBytes = 2048;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev) != cudaSuccess)
+    rsv = 1024;
+  const size_t base = (size_t)fa.sharedSizeBytes + (size_t)rsv;
+  return tile_window(g.tile_lr, g.tile_lp, g.pitch, base) - base;
+}
+
+template <int MODE, int NT>
+static cudaError_t launch_tiles_nt(const Geom &g, int num_sms, int *per_sm, cudaStream_t s) {
+  const size_t smem = tiles_dyn_smem<MODE, NT>(g);
+  cudaError_t e = cudaFuncSetAttribute(k_advance_tiles<MODE, NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, k_advance_tiles<MODE, NT>, NT, smem);
+  if (e != cudaSuccess) return e;
+  if (*per_sm < 1) return cudaErrorInvalidConfiguration;
+  k_advance_tiles<MODE, NT><<<num_sms * *per_sm, NT, smem, s>>>(g);
   return cudaGetLastError();
 }
 
+// 8-warp CTAs, or one 20-warp CTA per SM when the shape leaves room for one CTA only
 template <int MODE>
-static cudaError_t launch_tiles_k(const Geom &g, int num_sms, size_t smem, cudaStream_t s) {
+static cudaError_t launch_tiles_k(const Geom &g, int num_sms, cudaStream_t s) {
+  int per_sm = 0;
+  const size_t smem = tiles_dyn_smem<MODE, TILE_NT>(g);
   cudaError_t e = cudaFuncSetAttribute(k_advance_tiles<MODE, TILE_NT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  int per_sm = 0;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_advance_tiles<MODE, TILE_NT>, TILE_NT, smem);
   if (e != cudaSuccess) return e;
   if (MODE != 1 && per_sm <= 1 && env_tile_wide()) {
-    e = cudaFuncSetAttribute(k_advance_tiles<MODE == 1 ? 0 : MODE, TILE_NT_WIDE>,
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (e != cudaSuccess) return e;
     int wide = 0;
-    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&wide, k_advance_tiles<MODE == 1 ? 0 : MODE, TILE_NT_WIDE>,
-                                                      TILE_NT_WIDE, smem);
-    if (e == cudaSuccess && wide >= 1) return launch_tiles_nt<MODE == 1 ? 0 : MODE, TILE_NT_WIDE>(g, num_sms, smem, 1, s);
+    if (launch_tiles_nt<MODE == 1 ? 0 : MODE, TILE_NT_WIDE>(g, num_sms, &wide, s) == cudaSuccess) return cudaSuccess;
+    cudaGetLastError();
   }
-  if (per_sm < 1) per_sm = 1;
-  return launch_tiles_nt<MODE, TILE_NT>(g, num_sms, smem, per_sm, s);
+  return launch_tiles_nt<MODE, TILE_NT>(g, num_sms, &per_sm, s);
 }
 
 cudaError_t launch_advance_tiles(const Geom &g, int num_sms, cudaStream_t s) {
-  const size_t base = tile_base();
-  const size_t smem = tile_window(g.tile_lr, g.tile_lp, g.pitch, base) - base;
-  if (g.shared_draws && g.tile_lr == 5) return launch_tiles_k<1>(g, num_sms, smem, s);
-  if (g.wor) return launch_tiles_k<2>(g, num_sms, smem, s);
-  return launch_tiles_k<0>(g, num_sms, smem, s);
+  if (g.shared_draws && g.tile_lr == 5) return launch_tiles_k<1>(g, num_sms, s);
+  if (g.wor) return launch_tiles_k<2>(g, num_sms, s);
+  return launch_tiles_k<0>(g, num_sms, s);
 }
 
 }  // namespace aknn

@@ -8,6 +8,7 @@
 // k_output.  Every device step is a kernel of round_kernels.cu; the host
 // only sequences launches and validates arguments.
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
@@ -17,6 +18,7 @@
 #include <vector>
 
 #include "../../include/aknn.h"
+#include "host_wait.h"
 #include "internal.cuh"
 #include "launch.h"
 
@@ -162,6 +164,8 @@ struct aknn_index {
 #ifdef AKNN_WITH_NCCL
   ncclComm_t comm = nullptr;
 #endif
+  bool nccl_failed = false;        // the communicator was aborted (peer error / timeout)
+  double nccl_timeout_ms = 300000.0;  // aknn_set_timeout
   aknn_stats stats{};
   // statistics of an aknn_query_async call whose control blocks are still being
   // copied to `host` (graph loop, no round cap): finished on the next call on this
@@ -317,7 +321,8 @@ size_t tile_ws_bytes(int64_t qb, int64_t npad, const TileShape &t) {
 }
 
 void setup_tiles(Geom &g, const TileShape &t, const aknn_opts &o, int64_t qb, uint8_t *ws) {
-  g.tile_on = (t.on && !(o.flags & AKNN_FLAG_NO_TILES)) ? 1 : 0;
+  // (the tile kernels implement the doubling schedule; growth 2 takes the lists)
+  g.tile_on = (t.on && !(o.flags & AKNN_FLAG_NO_TILES) && g.growth <= 1) ? 1 : 0;
   g.advanced = &g.ctl->advanced;
   if (!g.tile_on) return;
   g.tile_lr = t.lr;
@@ -405,20 +410,28 @@ void setup_level_mma(Geom &g, int64_t qb, uint8_t *ws, const aknn_opts &o) {
   g.lmin = (uint32_t)(lmin < 1 ? 1 : lmin);
 }
 
-// Builds the level geometry of the composite key (R9).
+// Builds the level geometry of the composite key (R9) for a count
+// schedule (growth 1: doubling, reading R7; growth 2: reading R25).
 struct KeyGeom {
-  unsigned long long L, Ld;
-  int cmax, ibits, kbits, nbits;
+  unsigned long long L, Ld, L3;
+  int cmax, ibits, kbits, nbits, growth;
 };
 
 // ibits: local index bits of a work-list code; kbits: GLOBAL id bits of the key.
-aknn_status key_geom(int64_t n_local, int64_t n_global, int32_t d, KeyGeom *kg) {
+// L = lcm(T_0 .. T_cmax, d) over the sampled counts, so S * (L / T) is an integer order
+// key for every level.
+aknn_status key_geom(int64_t n_local, int64_t n_global, int32_t d, KeyGeom *kg, int growth = 1) {
   int cmax = 0;
-  while (d >= 2 && (1ll << (cmax + 1)) < d) ++cmax;  // largest c with 2^c < d
-  const unsigned long long p2 = 1ull << cmax;
-  const unsigned long long L = p2 / gcd_u64(p2, (unsigned long long)d) * (unsigned long long)d;
+  while (d >= 2 && cmax + 1 < MAX_LEVELS && lvl_count((uint32_t)cmax + 1u, growth) < (uint32_t)d) ++cmax;
+  unsigned long long L = (unsigned long long)d;
+  for (int c = 0; c <= cmax; ++c) {
+    const unsigned long long t = lvl_count((uint32_t)c, growth);
+    L = L / gcd_u64(L, t) * t;
+  }
+  kg->growth = growth;
   kg->L = L;
   kg->Ld = L / (unsigned long long)d;
+  kg->L3 = L % 3ull == 0 ? L / 3ull : 0ull;
   kg->cmax = cmax;
   kg->ibits = bit_length((unsigned long long)(n_local - 1));
   if (kg->ibits < 1) kg->ibits = 1;
@@ -426,8 +439,8 @@ aknn_status key_geom(int64_t n_local, int64_t n_global, int32_t d, KeyGeom *kg) 
   if (kg->kbits < 1) kg->kbits = 1;
   kg->nbits = bit_length(65025ull * L) + kg->kbits;
   if (kg->nbits > 63)
-    return fail(AKNN_EINVAL, "composite key needs %d bits (> 63) for n=%lld, d=%d", kg->nbits,
-                (long long)n_global, d);
+    return fail(AKNN_EINVAL, "composite key needs %d bits (> 63) for n=%lld, d=%d, growth %d", kg->nbits,
+                (long long)n_global, d, growth);
   return AKNN_OK;
 }
 
@@ -486,6 +499,58 @@ cudaError_t sync_spin(cudaStream_t st) {
     e = cudaEventQuery(ev);
     if (e != cudaErrorNotReady) return e;
   }
+}
+
+// Waits for `st` on an index of an NCCL communicator: the event poll of sync_spin plus
+// the communicator's asynchronous error state and a wall-clock deadline (host_wait.h);
+// on a peer error or a timeout the communicator is aborted -- the pending collective
+// then fails on every rank instead of hanging -- and the call returns AKNN_ENCCL.
+aknn_status wait_stream(aknn_index *ix, cudaStream_t st) {
+#ifdef AKNN_WITH_NCCL
+  if (ix->world > 1) {
+    if (ix->nccl_failed || !ix->comm) return fail(AKNN_ENCCL, "the communicator was aborted by an earlier failure");
+    thread_local cudaEvent_t ev = nullptr;
+    if (!ev) CU(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    CU(cudaEventRecord(ev, st));
+    cudaError_t dev_err = cudaSuccess;
+    ncclResult_t peer = ncclSuccess;
+    const WaitResult w = wait_loop(
+        [&] {
+          const cudaError_t e = cudaEventQuery(ev);
+          if (e == cudaSuccess) return 1;
+          if (e == cudaErrorNotReady) return 0;
+          dev_err = e;
+          return -1;
+        },
+        [&] {
+          ncclResult_t r = ncclSuccess;
+          if (ncclCommGetAsyncError(ix->comm, &r) != ncclSuccess) r = ncclInternalError;
+          peer = r;
+          return r != ncclSuccess && r != ncclInProgress;
+        },
+        [&] {
+          ncclCommAbort(ix->comm);
+          ix->comm = nullptr;
+          ix->nccl_failed = true;
+        },
+        [] {
+          return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now().time_since_epoch())
+              .count();
+        },
+        ix->nccl_timeout_ms);
+    if (w == WAIT_DEVICE_ERROR)
+      return fail(AKNN_ECUDA, "waiting for the sharded round: %s", cudaGetErrorString(dev_err));
+    if (w == WAIT_PEER_ERROR)
+      return fail(AKNN_ENCCL, "NCCL reported %s on rank %d; communicator aborted", ncclGetErrorString(peer),
+                  ix->rank);
+    if (w == WAIT_TIMEOUT)
+      return fail(AKNN_ENCCL, "no progress for %.0f ms on rank %d (dead peer?); communicator aborted",
+                  ix->nccl_timeout_ms, ix->rank);
+    return AKNN_OK;
+  }
+#endif
+  CU(sync_spin(st));
+  return AKNN_OK;
 }
 
 // Per-launch CUDA events on the launching stream, read after the call's final
@@ -679,6 +744,9 @@ aknn_status check_flags(const aknn_opts &o) {
     return fail(AKNN_EINVAL, "AKNN_FLAG_WITHOUT_REPLACEMENT cannot be combined with AKNN_FLAG_SHARED_DRAWS");
   if (o.lead < 0 || o.lead > 8) return fail(AKNN_EINVAL, "lead must be in [0, 8] (got %d)", o.lead);
   if (o.batch_queries < 0) return fail(AKNN_EINVAL, "batch_queries must be >= 0 (got %d)", o.batch_queries);
+  if (o.growth < 0 || o.growth > 2) return fail(AKNN_EINVAL, "growth must be 0, 1 or 2 (got %d)", o.growth);
+  if (o.growth == 2 && (o.flags & (AKNN_FLAG_SHARED_DRAWS | AKNN_FLAG_WITHOUT_REPLACEMENT)))
+    return fail(AKNN_EINVAL, "growth 2 runs with per-query draws with replacement only");
   return AKNN_OK;
 }
 
@@ -690,11 +758,12 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   const int64_t n = ix->n_local;
   const int32_t d = ix->d;
   KeyGeom kg;
-  TRY(key_geom(n, ix->n_global, d, &kg));
-  if (k + h > output_max_kh())
-    return fail(AKNN_EINVAL, "k+h=%d exceeds the supported %d", k + h, output_max_kh());
   const aknn_opts o = opts ? *opts : aknn_opts{};
   TRY(check_flags(o));
+  const int growth = o.growth > 1 ? o.growth : 1;
+  TRY(key_geom(n, ix->n_global, d, &kg, growth));
+  if (k + h > output_max_kh())
+    return fail(AKNN_EINVAL, "k+h=%d exceeds the supported %d", k + h, output_max_kh());
   const int64_t npad = round_up(n, 16);
   // sub-batch size: the code (qi << ibits | i) must fit 32 bits; the
   // workspace (S 4 B + lvl 1 B + act 1 B + list 4 B per pair) fits in memory.
@@ -763,6 +832,8 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   }
   g.L = kg.L;
   g.Ld = kg.Ld;
+  g.L3 = kg.L3;
+  g.growth = kg.growth;
   g.ibits = kg.ibits;
   g.kbits = kg.kbits;
   g.world = 1;
@@ -772,7 +843,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   g.shared_draws = (o.flags & AKNN_FLAG_SHARED_DRAWS) ? 1 : 0;
   g.wor = (o.flags & AKNN_FLAG_WITHOUT_REPLACEMENT) ? 1 : 0;
   g.wor_z = wor_radix(d);
-  g.stage_lo = stage_level(g.pitch);
+  g.stage_lo = g.growth > 1 ? MAX_LEVELS : stage_level(g.pitch);  // staged rows: doubling only
   TRY(setup_exact_mma(ix, g, qb, ix->ws.as<uint8_t>(oXm), o, st));
   setup_tiles(g, tsh, o, qb, ix->ws.as<uint8_t>(oTw));
   setup_level_mma(g, qb, ix->ws.as<uint8_t>(oLm), o);
@@ -925,6 +996,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
                               uint64_t seed, const double *alpha_dev, const aknn_opts *opts,
                               const aknn_result *out, int64_t out_ncols, cudaStream_t st) {
   aknn_index *ix0 = shards[0];
+  if (nccl && ix0->nccl_failed) return fail(AKNN_ENCCL, "the communicator was aborted by an earlier failure");
   for (aknn_index *sh : shards) TRY(finish_pending(sh));
   const int32_t d = ix0->d;
   const int W = nccl ? ix0->world : (int)shards.size();
@@ -934,7 +1006,8 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
   const aknn_opts o = opts ? *opts : aknn_opts{};
   TRY(check_flags(o));
   std::vector<KeyGeom> kg(shards.size());
-  for (size_t s = 0; s < shards.size(); ++s) TRY(key_geom(shards[s]->n_local, ix0->n_global, d, &kg[s]));
+  const int growth = o.growth > 1 ? o.growth : 1;
+  for (size_t s = 0; s < shards.size(); ++s) TRY(key_geom(shards[s]->n_local, ix0->n_global, d, &kg[s], growth));
   // sub-batch size: list codes fit 32 bits on every shard; memory on this device
   int64_t qb = o.batch_queries > 0 ? std::min<int64_t>(q, o.batch_queries) : q;
   size_t free_b = 0, total_b = 0;
@@ -956,7 +1029,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     if (ncclAllReduce(tmp.p, tmp.p, 1, ncclInt64, ncclMin, ix0->comm, st) != ncclSuccess)
       return fail(AKNN_ENCCL, "ncclAllReduce(qb) failed");
     CU(cudaMemcpyAsync(&qb, tmp.p, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-    CU(sync_spin(st));
+    TRY(wait_stream(ix0, st));
   }
 #endif
   if (qb < 1) return fail(AKNN_ENOMEM, "not enough device memory for one query row");
@@ -1024,6 +1097,8 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     }
     g.L = kg[si].L;
     g.Ld = kg[si].Ld;
+    g.L3 = kg[si].L3;
+    g.growth = kg[si].growth;
     g.ibits = kg[si].ibits;
     g.kbits = kg[si].kbits;
     g.cmax = kg[si].cmax;
@@ -1032,7 +1107,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     g.shared_draws = (o.flags & AKNN_FLAG_SHARED_DRAWS) ? 1 : 0;
     g.wor = (o.flags & AKNN_FLAG_WITHOUT_REPLACEMENT) ? 1 : 0;
     g.wor_z = wor_radix(d);
-    g.stage_lo = stage_level(g.pitch);
+    g.stage_lo = g.growth > 1 ? MAX_LEVELS : stage_level(g.pitch);  // staged rows: doubling only
     g.world = W;
     g.recv_stride = recv_stride;
     TRY(setup_exact_mma(ix, g, qb, ix->ws.as<uint8_t>(oXm), o, st));
@@ -1109,7 +1184,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
       tm.stop(PH_SELECT);
       stats.query_rounds += evaluated;
       CU(cudaMemcpyAsync(h_active, &G[0].ctl->n_active, sizeof(unsigned int), cudaMemcpyDeviceToHost, st));
-      CU(sync_spin(st));
+      TRY(wait_stream(ix0, st));
       const unsigned nact = *h_active;
       stats.blocked_query_rounds += nact;
       evaluated = nact;
@@ -1147,7 +1222,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     for (size_t si = 0; si < nS; ++si) {
       CU(cudaMemcpyAsync(h_ctl, G[si].ctl, sizeof(RoundCtl), cudaMemcpyDeviceToHost, st));
       CU(cudaMemcpyAsync(h_qs, G[si].qs, sizeof(QState) * qn, cudaMemcpyDeviceToHost, st));
-      CU(sync_spin(st));
+      TRY(wait_stream(ix0, st));
       const RoundCtl &ctl_h = *h_ctl;
       const QState *qs = h_qs;
       stats.active_pair_rounds += (int64_t)ctl_h.advanced;
@@ -1163,7 +1238,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
   }
   tm.open_a = all_a;
   tm.stop(PH_ALL);
-  CU(sync_spin(st));
+  TRY(wait_stream(ix0, st));
   double ms[PH_N];
   tm.resolve(ms);
   stats.ms_init = ms[PH_INIT];
@@ -1441,7 +1516,7 @@ aknn_status host_query(const std::vector<aknn_index *> &shards, bool multi, cons
   if (out->evals) CU(cudaMemcpyAsync(out->evals, dout.evals, szEv, cudaMemcpyDeviceToHost, st));
   if (out->draws) CU(cudaMemcpyAsync(out->draws, dout.draws, szDr, cudaMemcpyDeviceToHost, st));
   if (out->rounds) CU(cudaMemcpyAsync(out->rounds, dout.rounds, szRo, cudaMemcpyDeviceToHost, st));
-  CU(sync_spin(st));
+  TRY(wait_stream(ix, st));
   return s;
 }
 }  // namespace
@@ -1533,7 +1608,7 @@ namespace {
 struct HostKey {
   KeyGeom kg;
   unsigned long long key(int32_t S, uint8_t l, uint32_t gid) const {
-    const unsigned long long mul = lvl_exact(l) ? kg.Ld : (kg.L >> l);
+    const unsigned long long mul = lvl_exact(l) ? kg.Ld : lvl_mul(l, kg.L, kg.L3, kg.growth);
     return (((unsigned long long)(uint32_t)S * mul) << kg.kbits) | gid;
   }
 };
@@ -1565,7 +1640,7 @@ aknn_status aknn_shard_summary_host(const int32_t *S, const uint8_t *lvl, int64_
       r.lvl = lvl[i];
       out[p++] = r;
     } else {
-      const double L = lower_of(S[i], lvl[i], d, alpha);
+      const double L = lower_of(S[i], lvl[i], d, alpha, 1);
       if (best < 0 || L < bl) {  // ascending i: ties keep the smaller id
         best = i;
         bl = L;
@@ -1599,7 +1674,7 @@ aknn_status aknn_shard_merge_host(const void *recs, int32_t world, int64_t n_glo
   const ShardRec *b1 = nullptr;
   double A = 0.0;
   for (int t = 0; t < k; ++t) {
-    const double U = upper_of(top[t]->S, top[t]->lvl, d, alpha);
+    const double U = upper_of(top[t]->S, top[t]->lvl, d, alpha, 1);
     if (!b1 || U > A || (U == A && gid(top[t]) < gid(b1))) { b1 = top[t]; A = U; }
   }
   // d2 = argmin L over ranks > k+h and every shard's remainder arm (Eq. 3)
@@ -1608,12 +1683,12 @@ aknn_status aknn_shard_merge_host(const void *recs, int32_t world, int64_t n_glo
   const ShardRec *b2 = nullptr;
   double B = 0.0;
   for (const ShardRec *r : far) {
-    const double L = lower_of(r->S, r->lvl, d, alpha);
+    const double L = lower_of(r->S, r->lvl, d, alpha, 1);
     if (!b2 || L < B || (L == B && gid(r) < gid(b2))) { b2 = r; B = L; }
   }
   for (int t = 0; t < kh; ++t) {
     res->sets[t] = (int32_t)gid(top[t]);
-    if (res->dhat) res->dhat[t] = dhat_of(top[t]->S, top[t]->lvl, d);
+    if (res->dhat) res->dhat[t] = dhat_of(top[t]->S, top[t]->lvl, d, 1);
   }
   res->thr_k = top[k - 1]->key;
   res->thr_kh = top[kh - 1]->key;
@@ -1621,7 +1696,7 @@ aknn_status aknn_shard_merge_host(const void *recs, int32_t world, int64_t n_glo
   res->B = B;
   res->d1 = gid(b1);
   res->d2 = gid(b2);
-  res->alpha_d2 = alpha_of(b2->lvl, alpha);
+  res->alpha_d2 = alpha_of(b2->lvl, alpha, 1);
   res->stop = A <= B;  // Eq. (5)
   return AKNN_OK;
 }
@@ -1705,6 +1780,13 @@ aknn_status aknn_exact(const aknn_index *cix, const uint8_t *queries, int32_t q,
   return AKNN_OK;
 }
 
+aknn_status aknn_set_timeout(aknn_index *ix, double timeout_ms) {
+  if (!ix) return fail(AKNN_EINVAL, "NULL argument");
+  if (!(timeout_ms >= 0.0)) return fail(AKNN_EINVAL, "timeout_ms must be >= 0 (0 = no deadline)");
+  ix->nccl_timeout_ms = timeout_ms;
+  return AKNN_OK;
+}
+
 int64_t aknn_index_n_local(const aknn_index *ix) { return ix ? ix->n_local : -1; }
 int64_t aknn_index_n_global(const aknn_index *ix) { return ix ? ix->n_global : -1; }
 int32_t aknn_index_dim(const aknn_index *ix) { return ix ? ix->d : -1; }
@@ -1715,7 +1797,7 @@ void aknn_free(aknn_index *ix) {
   if (ix->pending.ev) cudaEventDestroy(ix->pending.ev);
   if (ix->nx_ev) cudaEventDestroy(ix->nx_ev);
 #ifdef AKNN_WITH_NCCL
-  if (ix->comm) ncclCommDestroy(ix->comm);
+  if (ix->comm) ncclCommDestroy(ix->comm);  // (an aborted communicator is already gone)
 #endif
   if (ix->stream) cudaStreamSynchronize(ix->stream);
   if (ix->loop_exec) cudaGraphExecDestroy(ix->loop_exec);

@@ -15,12 +15,12 @@ namespace aknn {
 constexpr uint8_t LVL_EXACT = 0x80;
 __host__ __device__ __forceinline__ bool lvl_exact(uint8_t l) { return (l & LVL_EXACT) != 0; }
 __host__ __device__ __forceinline__ uint8_t lvl_to_exact(uint8_t l) { return (uint8_t)(l | LVL_EXACT); }
-__host__ __device__ __forceinline__ uint32_t lvl_sampled(uint8_t l) { return 1u << (l & 0x7F); }
 // Action byte written by the blocker filter: 0 = idle, c+1 = draw level c+1
-// (T -> 2T), ACT_EXACT = exact fallback.
+// (T_c -> T_{c+1}), ACT_EXACT = exact fallback.
 constexpr uint8_t ACT_EXACT = 0xFE;
-// d <= 33025 -> sampled levels c in [0, 15]; slot MAX_LEVELS = exact list.
-constexpr int MAX_LEVELS = 16;
+// d <= 33025 -> sampled levels c in [0, 15] under doubling, [0, 30] under growth 2
+// (reading R25); slot MAX_LEVELS = exact list.  Per-level bit masks are 32-bit.
+constexpr int MAX_LEVELS = 32;
 constexpr int NSLOT = MAX_LEVELS + 1;
 
 // Integer form of the blocker predicate of one query for a round (k_thresholds).
@@ -124,15 +124,17 @@ struct Geom {
   uint32_t seed_lo, seed_hi;
   uint32_t rk0[10], rk1[10]; // Philox round keys of (seed_lo, seed_hi): kernel-param
                              // constants, so each round's key XOR is one LOP3
-  unsigned long long L;  // lcm(2^cmax, d): K = S * (L / T) is an exact order key
+  unsigned long long L;  // lcm(T_0..T_cmax, d): K = S * (L / T) is an exact order key
   unsigned long long Ld; // L / d
+  unsigned long long L3; // L / 3 (growth 2: the counts 3 * 2^j)
+  int growth;            // sample-count schedule: 1 doubling (R7), 2 (reading R25)
   int ibits;             // bits of the local point index in a work-list code
   int kbits;             // bits of the GLOBAL point id in the composite key
   ShardRec *send;        // [q][k+h+1] this shard's summary (sharded query only)
   const ShardRec *recv;  // [world][recv_stride] every shard's summary
   int64_t recv_stride;   // records per shard slot of recv (qb * (k+h+1))
   int world;             // shards taking part (1 = unsharded)
-  int cmax;              // largest sampled level (2^cmax < d)
+  int cmax;              // largest sampled level (T_cmax < d)
   unsigned adv_bpl;      // advance: Philox blocks per lane before a lane-group reduce
   int force_radix;       // 1: skip the pivot select (aknn_opts.flags bit 0)
   int stage_lo;          // first row-staged advance level (MAX_LEVELS = none)
@@ -255,6 +257,43 @@ __device__ __forceinline__ uint32_t wor_coord(uint4 w, const WorRadix &z, uint32
   return x >= d ? x - d : x;
 }
 
+// The sample-count schedule: level c holds T_c samples.  growth 1 (readings R7): T_c =
+// 2^c; growth 2 (reading R25): 1, 2, 3, 4, 6, 8, 12, 16, ... (factors
+// 3/2 and 4/3), i.e. T_c = 2^((c+1)/2) for odd c and 3 * 2^((c-2)/2) for even c >= 2.
+// Every power of two is a count, so the advance [T_c, T_{c+1}) stays inside one sample
+// level b of the Draw stream (reading R19).
+__host__ __device__ __forceinline__ uint32_t lvl_count(uint32_t c, int growth) {
+  if (growth <= 1) return c < 32u ? 1u << c : 0xFFFFFFFFu;
+  if (c == 0) return 1u;
+  return (c & 1u) ? (1u << ((c + 1) >> 1)) : (3u << ((c - 2) >> 1));
+}
+// The samples of an arm in level byte l: d once exact, else T_c.
+__host__ __device__ __forceinline__ uint32_t count_of(uint8_t l, int d, int growth) {
+  return lvl_exact(l) ? (uint32_t)d : lvl_count(l & 0x7Fu, growth);
+}
+// L / T_c for the exact order key (L = lcm of every sampled count and d; L3 = L / 3).
+__host__ __device__ __forceinline__ unsigned long long lvl_mul(uint32_t c, unsigned long long L,
+                                                               unsigned long long L3, int growth) {
+  if (growth <= 1) return L >> c;
+  if (c == 0) return L;
+  return (c & 1u) ? (L >> ((c + 1) >> 1)) : (L3 >> ((c - 2) >> 1));
+}
+// The advance out of level c draws the samples t = T_c .. T_{c+1} - 1: sample level
+// b = 1 + floor(log2 T_c), in-level ordinals u = u0 .. u0 + cnt - 1 (reading R19).
+struct LevelAdvance {
+  uint32_t b, u0, cnt;
+};
+__host__ __device__ __forceinline__ LevelAdvance lvl_advance(uint32_t c, int growth) {
+  const uint32_t t0 = lvl_count(c, growth), t1 = lvl_count(c + 1, growth);
+#ifdef __CUDA_ARCH__
+  const uint32_t b = 31u - (uint32_t)__clz(t0);  // floor(log2 t0)
+#else
+  uint32_t b = 0;
+  while ((t0 >> b) > 1u) ++b;
+#endif
+  return LevelAdvance{b + 1u, t0 - (1u << b), t1 - t0};
+}
+
 // Exact order key of an arm: K = S * (L / T).  S/T ranks exactly like the
 // fp64 estimate S/(65025 T) (reading R9), and with the local index
 // in the low bits every key is unique: (d_hat, i) lexicographic order.
@@ -262,14 +301,14 @@ __device__ __forceinline__ uint32_t wor_coord(uint4 w, const WorRadix &z, uint32
 // different shards are comparable and unique.
 __device__ __forceinline__ unsigned long long arm_key(int32_t S, uint8_t l, uint32_t i,
                                                       const Geom &g) {
-  const unsigned long long mul = lvl_exact(l) ? g.Ld : (g.L >> l);
+  const unsigned long long mul = lvl_exact(l) ? g.Ld : lvl_mul(l, g.L, g.L3, g.growth);
   return (((unsigned long long)(uint32_t)S * mul) << g.kbits) | (i + g.id_offset);
 }
 
 // d_hat = S / (T * 65025), one correctly rounded fp64 division (P:121-124,
 // DESIGN.md reading R15).  T * 65025 is exact in fp64.
-__host__ __device__ __forceinline__ double dhat_of(int32_t S, uint8_t l, int d) {
-  const double T = lvl_exact(l) ? (double)d : (double)(1u << l);
+__host__ __device__ __forceinline__ double dhat_of(int32_t S, uint8_t l, int d, int growth) {
+  const double T = (double)count_of(l, d, growth);
 #ifdef __CUDA_ARCH__
   return __ddiv_rn((double)S, __dmul_rn(T, 65025.0));
 #else
@@ -277,27 +316,27 @@ __host__ __device__ __forceinline__ double dhat_of(int32_t S, uint8_t l, int d) 
 #endif
 }
 
-__host__ __device__ __forceinline__ double alpha_of(uint8_t l, const double *alpha) {
+__host__ __device__ __forceinline__ double alpha_of(uint8_t l, const double *alpha, int growth) {
 #ifdef __CUDA_ARCH__
-  return lvl_exact(l) ? 0.0 : __ldg(alpha + (1u << l));
+  return lvl_exact(l) ? 0.0 : __ldg(alpha + lvl_count(l, growth));
 #else
-  return lvl_exact(l) ? 0.0 : alpha[1u << l];
+  return lvl_exact(l) ? 0.0 : alpha[lvl_count(l, growth)];
 #endif
 }
 
-__host__ __device__ __forceinline__ double upper_of(int32_t S, uint8_t l, int d, const double *alpha) {
+__host__ __device__ __forceinline__ double upper_of(int32_t S, uint8_t l, int d, const double *alpha, int growth) {
 #ifdef __CUDA_ARCH__
-  return __dadd_rn(dhat_of(S, l, d), alpha_of(l, alpha));
+  return __dadd_rn(dhat_of(S, l, d, growth), alpha_of(l, alpha, growth));
 #else
-  return dhat_of(S, l, d) + alpha_of(l, alpha);
+  return dhat_of(S, l, d, growth) + alpha_of(l, alpha, growth);
 #endif
 }
 
-__host__ __device__ __forceinline__ double lower_of(int32_t S, uint8_t l, int d, const double *alpha) {
+__host__ __device__ __forceinline__ double lower_of(int32_t S, uint8_t l, int d, const double *alpha, int growth) {
 #ifdef __CUDA_ARCH__
-  return __dsub_rn(dhat_of(S, l, d), alpha_of(l, alpha));
+  return __dsub_rn(dhat_of(S, l, d, growth), alpha_of(l, alpha, growth));
 #else
-  return dhat_of(S, l, d) - alpha_of(l, alpha);
+  return dhat_of(S, l, d, growth) - alpha_of(l, alpha, growth);
 #endif
 }
 

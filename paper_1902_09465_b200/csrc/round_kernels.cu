@@ -88,11 +88,11 @@ __global__ void __launch_bounds__(SEL_NT) k_select(Geom g, int nbits) {
       if (i >= g.n) break;
       const unsigned long long key = arm_key(a.S[e], a.l[e], (uint32_t)i, g);
       if (key <= thk) {
-        const double U = __dadd_rn(dhat_of(a.S[e], a.l[e], g.d), alpha_of(a.l[e], g.alpha));
+        const double U = __dadd_rn(dhat_of(a.S[e], a.l[e], g.d, g.growth), alpha_of(a.l[e], g.alpha, g.growth));
         if (U > bu.v || (U == bu.v && i < bu.i)) bu = Best{U, i, 0.0};
       } else if (key > thkh) {
-        const double al = alpha_of(a.l[e], g.alpha);
-        const double L = __dsub_rn(dhat_of(a.S[e], a.l[e], g.d), al);
+        const double al = alpha_of(a.l[e], g.alpha, g.growth);
+        const double L = __dsub_rn(dhat_of(a.S[e], a.l[e], g.d, g.growth), al);
         if (L < bl.v || (L == bl.v && i < bl.i)) bl = Best{L, i, al};
       }
     }
@@ -160,13 +160,13 @@ __global__ void __launch_bounds__(128) k_thresholds(Geom g) {
   bool mbit = false, eqk = false, eqkh = false;
   if (c < MAX_LEVELS && c <= g.cmax) {
     const uint8_t l = (uint8_t)c;
-    const double al = alpha_of(l, g.alpha);
-    const int32_t smax = (int32_t)(65025u << c);  // every draw (a - b)^2 <= 255^2
+    const double al = alpha_of(l, g.alpha, g.growth);
+    const int32_t smax = (int32_t)(65025u * lvl_count((uint32_t)c, g.growth));  // every draw (a - b)^2 <= 255^2
     // Su: first S with U(S) > B (smax + 1: none)
     int32_t lo = 0, hi = smax + 1;
     while (lo < hi) {
       const int32_t mid = lo + ((hi - lo) >> 1);
-      if (__dadd_rn(dhat_of(mid, l, g.d), al) > st.B) hi = mid; else lo = mid + 1;
+      if (__dadd_rn(dhat_of(mid, l, g.d, g.growth), al) > st.B) hi = mid; else lo = mid + 1;
     }
     const int32_t su = lo;
     // Sl: first S with L(S) >= A (blocker iff S < Sl)
@@ -174,11 +174,11 @@ __global__ void __launch_bounds__(128) k_thresholds(Geom g) {
     hi = smax + 1;
     while (lo < hi) {
       const int32_t mid = lo + ((hi - lo) >> 1);
-      if (!(__dsub_rn(dhat_of(mid, l, g.d), al) < st.A)) hi = mid; else lo = mid + 1;
+      if (!(__dsub_rn(dhat_of(mid, l, g.d, g.growth), al) < st.A)) hi = mid; else lo = mid + 1;
     }
     const int32_t sl = lo;
     // the key thresholds on S at this level: S * mul <=> K = thr >> kbits
-    const unsigned long long mul = g.L >> c;
+    const unsigned long long mul = lvl_mul((uint32_t)c, g.L, g.L3, g.growth);
     const unsigned long long Kk = st.thr_k >> g.kbits, Kkh = st.thr_kh >> g.kbits;
     const unsigned long long ck = (Kk + mul - 1) / mul, ckh = (Kkh + mul - 1) / mul;
     eqk = Kk % mul == 0;
@@ -216,7 +216,7 @@ __device__ __forceinline__ uint32_t filter_arms(const Geom &g, const int32_t *th
   for (int e = 0; e < 4; ++e) {
     const int i = i0 + e;
     const uint8_t l = a.l[e];
-    const uint32_t c = l & 15u;
+    const uint32_t c = l & 31u;
     const bool live = i < g.n && !lvl_exact(l);
     const int4 t = reinterpret_cast<const int4 *>(thr)[c];  // Su, Sl, Ck, Ckh
     const int32_t S = a.S[e];
@@ -227,9 +227,10 @@ __device__ __forceinline__ uint32_t filter_arms(const Geom &g, const int32_t *th
       inM = inM || (((eqkh >> c) & 1u) && S == t.w && gid <= idkh);
     }
     const bool blk = live && (inC ? S >= t.x : (inM ? ((mmask >> c) & 1u) != 0u : S < t.y));
-    const bool ex = (2u << c) >= (unsigned)g.d;
+    // P:176 (reading R8): exact when the next count would reach d
+    const bool ex = lvl_count(c + 1u, g.growth) >= (unsigned)g.d;
     const uint32_t act = blk ? (ex ? (uint32_t)ACT_EXACT : c + 1u) : 0u;
-    dr += (blk && !ex) ? (1u << c) : 0u;
+    dr += (blk && !ex) ? lvl_count(c, g.growth) : 0u;  // the advance draws T_{c+1} - T_c = T_c (doubling)
     actw |= act << (8 * e);
     lw |= (blk && !ex && inM) ? (1u << (8 * e)) : 0u;  // inM: ranks 1..k+h (C or M)
   }
@@ -245,11 +246,11 @@ __device__ __forceinline__ uint32_t lead_arms(const Geom &g, const Arm4 &a, uint
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const uint8_t l = a.l[e];
-    const uint32_t c = l & 15u;
+    const uint32_t c = l & 31u;
     const bool go = i0 + e < g.n && ((lb >> (8 * e)) & 0xFFu) && !lvl_exact(l);
-    const bool ex = (2u << c) >= (unsigned)g.d;
+    const bool ex = lvl_count(c + 1u, g.growth) >= (unsigned)g.d;
     const uint32_t act = go ? (ex ? (uint32_t)ACT_EXACT : c + 1u) : 0u;
-    dr += (go && !ex) ? (1u << c) : 0u;
+    dr += (go && !ex) ? lvl_count(c, g.growth) : 0u;
     actw |= act << (8 * e);
   }
   *draws = dr;
@@ -394,21 +395,25 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
 constexpr int ADV_P = 4;
 constexpr int ADV_XP = 4;
 
-__host__ __device__ __forceinline__ unsigned nblk_of(int c) { return c < 2 ? 1u : (1u << (c - 2)); }
+// Philox blocks per pair of the advance out of level c (doubling: max(1, 2^(c-2))).
+__host__ __device__ __forceinline__ unsigned nblk_of(int c, int growth) {
+  const LevelAdvance a = lvl_advance((uint32_t)c, growth);
+  return a.cnt < 4u ? 1u : a.cnt / 4u;
+}
 // Lanes per pair at levels with nb > ADV_P blocks: each lane runs >= ADV_BPL blocks
 // (two rounds of ADV_P independent Philox blocks) before the group reduce.
 __host__ __device__ __forceinline__ unsigned lanes_per_pair(unsigned nb, unsigned bpl) {
   const unsigned t = nb / bpl;
   return t < 1u ? 1u : (t > 32u ? 32u : t);
 }
-__host__ __device__ __forceinline__ unsigned pairs_per_chunk(int slot, unsigned bpl, int stage_lo) {
+__host__ __device__ __forceinline__ unsigned pairs_per_chunk(int slot, unsigned bpl, int stage_lo, int growth) {
   if (slot == MAX_LEVELS) return ADV_XP;
   if (slot >= stage_lo) return 1u;  // row-staged levels: one pair per warp
-  const unsigned nb = nblk_of(slot);
+  const unsigned nb = nblk_of(slot, growth);
   return nb <= (unsigned)ADV_P ? 32u * ADV_P / nb : 32u / lanes_per_pair(nb, bpl);
 }
 
-__global__ void k_plan(RoundCtl *ctl, unsigned bpl, int stage_lo, int level_mma, unsigned level_min) {
+__global__ void k_plan(RoundCtl *ctl, unsigned bpl, int stage_lo, int level_mma, unsigned level_min, int growth) {
   if (threadIdx.x != 0) return;
   if (level_mma) {  // shared draws: the most populated sampled level goes to the tensor cores
     int best = -1;
@@ -431,7 +436,7 @@ __global__ void k_plan(RoundCtl *ctl, unsigned bpl, int stage_lo, int level_mma,
     ctl->cursor[s] = 0;
     off += c;
     adv += c;
-    const unsigned ppc = pairs_per_chunk(s, bpl, stage_lo);
+    const unsigned ppc = pairs_per_chunk(s, bpl, stage_lo, growth);
     ch += (c + ppc - 1) / ppc;
   }
   ctl->off[NSLOT] = off;
@@ -442,14 +447,14 @@ __global__ void k_plan(RoundCtl *ctl, unsigned bpl, int stage_lo, int level_mma,
 // After the scatter: the lists hold only the pairs of sparse tiles (and the exact
 // fallbacks of sparse tensor-core tiles), cursor[s] of them per slot; the advance
 // kernels walk exactly those.
-__global__ void k_plan_lists(RoundCtl *ctl, unsigned bpl, int stage_lo) {
+__global__ void k_plan_lists(RoundCtl *ctl, unsigned bpl, int stage_lo, int growth) {
   if (threadIdx.x != 0) return;
   unsigned long long ch = 0;
   for (int s = 0; s < NSLOT; ++s) {
     const unsigned c = ctl->cursor[s];
     ctl->cnt[s] = c;
     ctl->chunk_off[s] = ch;
-    const unsigned ppc = pairs_per_chunk(s, bpl, stage_lo);
+    const unsigned ppc = pairs_per_chunk(s, bpl, stage_lo, growth);
     ch += (c + ppc - 1) / ppc;
   }
   ctl->chunk_off[NSLOT] = ch;
@@ -558,21 +563,25 @@ struct BlockTask {
   bool valid;
 };
 
-__device__ __forceinline__ void draw_blocks(const Geom &g, const BlockTask (&t)[ADV_P], int c,
-                                            uint32_t s, uint32_t (&acc)[ADV_P]) {
+// The advance out of level c draws the in-level ordinals u0 .. u0 + s - 1 of sample
+// level b (doubling: b = c + 1, u0 = 0, s = 2^c); with s < 4 the block's words
+// w0 = u0 & 3 .. w0 + s - 1 are the draws, the others are discarded.
+__device__ __forceinline__ void draw_blocks(const Geom &g, const BlockTask (&t)[ADV_P], const LevelAdvance &av,
+                                            uint32_t (&acc)[ADV_P]) {
+  const uint32_t s = av.cnt, w0 = av.u0 & 3u, blk0 = av.u0 >> 2;
   uint4 w[ADV_P];  // Philox words, or the arm's permutation keys (without replacement)
 #pragma unroll
   for (int k = 0; k < ADV_P; ++k)
     w[k] = g.wor ? wor_keys(g.rk0, g.rk1, t[k].i, t[k].qi)
-                 : philox4x32_10_rk(make_uint4(t[k].blk, t[k].i, t[k].qi, (uint32_t)(c + 1)), g.rk0, g.rk1);
+                 : philox4x32_10_rk(make_uint4(blk0 + t[k].blk, t[k].i, t[k].qi, av.b), g.rk0, g.rk1);
 #pragma unroll
   for (int k = 0; k < ADV_P; ++k) {
     const uint32_t ws[4] = {w[k].x, w[k].y, w[k].z, w[k].w};
     uint32_t a = 0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      // s < 4 only at levels 0 and 1 (1 and 2 draws); the word is discarded
-      if (t[k].valid && (s >= 4 || (uint32_t)e < s)) {
+      // s < 4 only at the first levels (1 or 2 draws); other words are discarded
+      if (t[k].valid && (s >= 4 || ((uint32_t)e >= w0 && (uint32_t)e < w0 + s))) {
         const uint32_t j = g.wor ? wor_coord(w[k], g.wor_z, (uint32_t)g.d, s + 4u * t[k].blk + (uint32_t)e)
                                  : coord_of(ws[e], (uint32_t)g.d);
         const int diff = (int)__ldg(t[k].xr + j) - (int)__ldg(t[k].qr + j);
@@ -724,10 +733,10 @@ __global__ void __launch_bounds__(ADV_NT) k_advance(Geom g) {
       continue;
     }
     const int c = slot;
-    const uint32_t s = 1u << c;
-    const unsigned nb = nblk_of(c);
+    const LevelAdvance av = lvl_advance((uint32_t)c, g.growth);
+    const unsigned nb = nblk_of(c, g.growth);
     const uint8_t newlvl = (uint8_t)(c + 1);
-    const unsigned ppc = pairs_per_chunk(c, g.adv_bpl, g.stage_lo);
+    const unsigned ppc = pairs_per_chunk(c, g.adv_bpl, g.stage_lo, g.growth);
     const unsigned pbase = (unsigned)rel * ppc;  // first pair of this chunk
     const uint32_t *lst = g.list + soff[c];
     const unsigned cnt = scnt[c];
@@ -750,7 +759,7 @@ __global__ void __launch_bounds__(ADV_NT) k_advance(Geom g) {
                          rng_qi(g, qi), blk, ok};
       }
       uint32_t acc[ADV_P];
-      draw_blocks(g, t, c, s, acc);
+      draw_blocks(g, t, av, acc);
 #pragma unroll
       for (int k = 0; k < ADV_P; ++k) {
         if (k % nb != 0 || !t[k].valid) continue;
@@ -779,12 +788,13 @@ __global__ void __launch_bounds__(ADV_NT) k_advance(Geom g) {
       const uint8_t *qr = reinterpret_cast<const uint8_t *>(
           __shfl_sync(FULL, reinterpret_cast<unsigned long long>(g.Q + (size_t)qi * g.pitch), lane));
       if (ok) {
-        const uint32_t gi = i + g.id_offset, gq = rng_qi(g, qi), lv = (uint32_t)(c + 1);
-        if (g.wor) {
+        const uint32_t gi = i + g.id_offset, gq = rng_qi(g, qi), lv = av.b, blk0 = av.u0 >> 2;
+        if (g.wor) {  // (doubling only: u0 = 0)
           const uint4 kk = wor_keys(g.rk0, g.rk1, gi, gq);
           for (unsigned b0 = sub * ADV_P; b0 < nb; b0 += tpp * ADV_P) sum += draw4_pair_wor(g, xr, qr, kk, lv, b0);
         } else {
-          for (unsigned b0 = sub * ADV_P; b0 < nb; b0 += tpp * ADV_P) sum += draw4_pair(g, xr, qr, gi, gq, lv, b0);
+          for (unsigned b0 = sub * ADV_P; b0 < nb; b0 += tpp * ADV_P)
+            sum += draw4_pair(g, xr, qr, gi, gq, lv, blk0 + b0);
         }
       }
       for (unsigned o = tpp >> 1; o > 0; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
@@ -835,8 +845,8 @@ __global__ void __launch_bounds__(ADV_NT) k_advance_staged(Geom g) {
        vch += nwarps) {
     const unsigned long long ch = c0 + vch;
     while (coff[slot + 1] <= ch) ++slot;
-    const int c = slot;
-    const unsigned nb = nblk_of(c);
+    const int c = slot;  // (doubling only: staged levels are off under growth 2)
+    const unsigned nb = nblk_of(c, g.growth);
     const uint32_t code = g.list[soff[c] + (ch - coff[c])];
     uint32_t qi, i;
     decode(g, code, imask, qi, i);
@@ -911,7 +921,7 @@ __global__ void __launch_bounds__(OUT_NT) k_output(Geom g, OutPtrs o) {
     for (int t = 0; t < m; ++t) rank += key[t] < key[r];
     const size_t oo = (size_t)(o.row0 + qi) * kh + rank;
     o.sets[oo] = (int32_t)(iv[r] + g.id_offset);
-    if (o.dhat) o.dhat[oo] = dhat_of(sv[r], lv[r], g.d);
+    if (o.dhat) o.dhat[oo] = dhat_of(sv[r], lv[r], g.d, g.growth);
   }
   if (threadIdx.x == 0) {
     const size_t row = (size_t)(o.row0 + qi);
@@ -922,24 +932,33 @@ __global__ void __launch_bounds__(OUT_NT) k_output(Geom g, OutPtrs o) {
 }
 
 // Per-query counters from the final arm states (SPEC S:250-258 accounting): an arm
-// at sampled level c drew 2^c coordinates (1 at initialisation, then 1 + 2 + ...);
-// an exact arm drew 2^c before its fallback, which is charged d (d = 1: exact at
-// initialisation, no fallback).  Philox blocks of the level gathers: level c used
-// max(1, 2^(c-2)) per advance.
+// at sampled level c drew T_c coordinates (1 at initialisation, then the advances);
+// an exact arm drew T_c before its fallback, which is charged d (d = 1: exact at
+// initialisation, no fallback).  Philox blocks of the level gathers: the advance out
+// of level l used nblk_of(l) (doubling: max(1, 2^(l-2))).
 __global__ void __launch_bounds__(256) k_tally(Geom g) {
   const int qi = blockIdx.x;
+  __shared__ unsigned long long cumbl[MAX_LEVELS + 1];  // blocks to reach level c
+  if (threadIdx.x == 0) {
+    unsigned long long a = 0;
+    for (int c = 0; c <= MAX_LEVELS; ++c) {
+      cumbl[c] = a;
+      if (c < MAX_LEVELS) a += nblk_of(c, g.growth);
+    }
+  }
+  __syncthreads();
   unsigned long long dr = 0, ex = 0, bl = 0, xe = 0;
   const uint8_t *lrow = g.lvl + (size_t)qi * g.npad;
   for (int i = threadIdx.x; i < g.n; i += blockDim.x) {
     const uint8_t l = lrow[i];
     const uint32_t c = l & 0x7Fu;
-    dr += 1ull << c;
+    dr += lvl_count(c, g.growth);
     const bool fb = lvl_exact(l) && g.d > 1;
     ex += fb ? 1u : 0u;
     // charge of the fallback: d, or without replacement the d - 2^c coordinates the
     // arm's permutation had not drawn yet (reading R23)
-    xe += fb ? (g.wor ? (unsigned long long)g.d - (1ull << c) : (unsigned long long)g.d) : 0ull;
-    bl += c == 0 ? 0ull : (c == 1 ? 1ull : (1ull << (c - 2)) + 1ull);
+    xe += fb ? (g.wor ? (unsigned long long)g.d - lvl_count(c, g.growth) : (unsigned long long)g.d) : 0ull;
+    bl += cumbl[c];
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -982,7 +1001,7 @@ __global__ void k_counts(Geom g, OutPtrs o) {
   const size_t src = (size_t)qi * g.npad + i;
   const size_t dst = (size_t)(o.row0 + qi) * o.ncols + o.col0 + i;
   const uint8_t l = g.lvl[src];
-  if (o.counts) o.counts[dst] = lvl_exact(l) ? g.d : (int32_t)(1u << l);
+  if (o.counts) o.counts[dst] = (int32_t)count_of(l, g.d, g.growth);
   if (o.sums) o.sums[dst] = (int64_t)(uint32_t)g.S[src];
 }
 
@@ -1034,13 +1053,13 @@ cudaError_t launch_filter(const Geom &g, cudaStream_t s) {
 }
 
 cudaError_t launch_compact(const Geom &g, cudaStream_t s) {
-  k_plan<<<1, 32, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo, g.level_mma, 1u << 16);
+  k_plan<<<1, 32, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo, g.level_mma, 1u << 16, g.growth);
   if (g.level_mma) {
     const cudaError_t e = launch_build_w(g, s);
     if (e != cudaSuccess) return e;
   }
   k_scatter<<<dim3(g.q, cdiv(g.npad, FIL_NT * 4)), FIL_NT, 0, s>>>(g);
-  k_plan_lists<<<1, 32, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo);  // the lists as written
+  k_plan_lists<<<1, 32, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo, g.growth);  // the lists as written
   return cudaGetLastError();
 }
 

@@ -140,7 +140,7 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
         const unsigned j = tid + u * PIV_NT;
         const int i = (int)(((unsigned long long)j * (unsigned)n) / ss);
         const size_t o = (size_t)qi * g.npad + i;
-        b = fmin(b, lower_of(g.S[o], g.lvl[o], g.d, g.alpha));
+        b = fmin(b, lower_of(g.S[o], g.lvl[o], g.d, g.alpha, g.growth));
       }
     }
 #pragma unroll
@@ -160,10 +160,12 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
   const unsigned long long tau = tau_s;
   if (tid <= MAX_LEVELS) {
     const bool ex = tid == MAX_LEVELS;  // slot MAX_LEVELS: exact arms (T = d, alpha = 0)
-    const double T = ex ? (double)g.d : (double)(1u << tid);
-    const unsigned long long mul = ex ? g.Ld : (g.L >> tid), Kt = tau >> g.kbits;
+    const bool live = !ex && tid <= g.cmax;
+    const double T = ex ? (double)g.d : (double)lvl_count((uint32_t)tid, g.growth);
+    const unsigned long long mul = ex ? g.Ld : (live ? lvl_mul((uint32_t)tid, g.L, g.L3, g.growth) : 1ull),
+                             Kt = tau >> g.kbits;
     const unsigned long long qt = Kt / mul, rt = Kt % mul, lt = qt + (rt != 0);
-    const float alf = (ex || tid > g.cmax) ? 0.f : (float)g.alpha[1u << tid];
+    const float alf = live ? (float)g.alpha[lvl_count((uint32_t)tid, g.growth)] : 0.f;
     const float eps = (alf + 2.f) * 9.5367431640625e-07f;  // 2^-20
     PivLevel v;
     v.lt = lt > 0x7fffffffull ? 0x7fffffff : (int32_t)lt;
@@ -213,7 +215,7 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
           const unsigned p = atomicAdd(&cnt, 1u);
           if (p < PIV_CAP) buf[p] = arm_key(S, (uint8_t)l, (uint32_t)i, g);
         } else if (!(__fmaf_rn((float)S, v.invT, v.nae) > boundf)) {  // could be the arg-min
-          const RecBest c{lower_of(S, (uint8_t)l, g.d, g.alpha), gid, S, (uint8_t)l};
+          const RecBest c{lower_of(S, (uint8_t)l, g.d, g.alpha, g.growth), gid, S, (uint8_t)l};
           if (better_min(c, bl)) bl = c;
         }
       }
@@ -253,7 +255,7 @@ __device__ __forceinline__ RecBest rec_of_key(const Geom &g, int qi, unsigned lo
   const size_t o = (size_t)qi * g.npad + i;
   const int32_t S = g.S[o];
   const uint8_t l = g.lvl[o];
-  return RecBest{upper ? upper_of(S, l, g.d, g.alpha) : lower_of(S, l, g.d, g.alpha), gid, S, l};
+  return RecBest{upper ? upper_of(S, l, g.d, g.alpha, g.growth) : lower_of(S, l, g.d, g.alpha, g.growth), gid, S, l};
 }
 
 // Unsharded rank split + bounds + Eq. (5) (same contract as k_select).
@@ -295,7 +297,7 @@ __global__ void __launch_bounds__(PIV_NT, 2) k_select_pivot(Geom g) {
     st->B = bl.v;
     st->d1 = (int)(bu.gid - g.id_offset);
     st->d2 = (int)(bl.gid - g.id_offset);
-    st->a_d2 = alpha_of(bl.lvl, g.alpha);
+    st->a_d2 = alpha_of(bl.lvl, g.alpha, g.growth);
     st->rounds += 1;
     const int stop = bu.v <= bl.v;  // Eq. (5), "<=" as written
     st->done = stop;

@@ -54,7 +54,7 @@ __global__ void __launch_bounds__(SEL_NT) k_select_local(Geom g, int nbits) {
         r.pad[0] = r.pad[1] = r.pad[2] = 0;
         out[p] = r;
       } else {
-        const RecBest c{lower_of(a.S[e], a.l[e], g.d, g.alpha), (uint32_t)i + g.id_offset, a.S[e],
+        const RecBest c{lower_of(a.S[e], a.l[e], g.d, g.alpha, g.growth), (uint32_t)i + g.id_offset, a.S[e],
                         a.l[e]};
         if (better_min(c, bl)) bl = c;
       }
@@ -134,12 +134,12 @@ __global__ void __launch_bounds__(MRG_NT) k_merge(Geom g, OutPtrs o) {
   for (unsigned t = threadIdx.x; t < m + W; t += MRG_NT) {
     if (t < (unsigned)g.k) {
       const ShardRec &r = rec(pos[t] / kh, pos[t] % kh);
-      const RecBest c{upper_of(r.S, r.lvl, g.d, g.alpha), (uint32_t)(key[t] & gmask), r.S, r.lvl};
+      const RecBest c{upper_of(r.S, r.lvl, g.d, g.alpha, g.growth), (uint32_t)(key[t] & gmask), r.S, r.lvl};
       if (better_max(c, bu)) bu = c;
     } else if (t >= kh) {
       const ShardRec &r = t < m ? rec(pos[t] / kh, pos[t] % kh) : rec(t - m, kh);
       const unsigned long long kk = t < m ? key[t] : r.key;
-      const RecBest c{lower_of(r.S, r.lvl, g.d, g.alpha), (uint32_t)(kk & gmask), r.S, r.lvl};
+      const RecBest c{lower_of(r.S, r.lvl, g.d, g.alpha, g.growth), (uint32_t)(kk & gmask), r.S, r.lvl};
       if (better_min(c, bl)) bl = c;
     }
   }
@@ -152,7 +152,7 @@ __global__ void __launch_bounds__(MRG_NT) k_merge(Geom g, OutPtrs o) {
       o.sets[oo] = (int32_t)(key[t] & gmask);
       if (o.dhat) {
         const ShardRec &r = rec(pos[t] / kh, pos[t] % kh);
-        o.dhat[oo] = dhat_of(r.S, r.lvl, g.d);
+        o.dhat[oo] = dhat_of(r.S, r.lvl, g.d, g.growth);
       }
     }
   }
@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(MRG_NT) k_merge(Geom g, OutPtrs o) {
     st->B = bl.v;
     st->d1 = (int)bu.gid;
     st->d2 = (int)bl.gid;
-    st->a_d2 = alpha_of(bl.lvl, g.alpha);
+    st->a_d2 = alpha_of(bl.lvl, g.alpha, g.growth);
     st->rounds += 1;
     const int stop = bu.v <= bl.v;  // Eq. (5), "<=" as written
     st->done = stop;
@@ -196,7 +196,7 @@ __global__ void k_counts_sharded(Geom g, OutPtrs o) {
   const size_t src = (size_t)qi * g.npad + i;
   const size_t dst = (size_t)(o.row0 + qi) * o.ncols + o.col0 + i;
   const uint8_t l = g.lvl[src];
-  if (o.counts) o.counts[dst] = lvl_exact(l) ? g.d : (int32_t)(1u << l);
+  if (o.counts) o.counts[dst] = (int32_t)count_of(l, g.d, g.growth);
   if (o.sums) o.sums[dst] = (int64_t)(uint32_t)g.S[src];
 }
 

@@ -117,7 +117,8 @@ def test_bindings_validate_dimensions(ak):
 
 def test_build_rejects_key_overflow(ak):
     """aknn.h domain: the composite rank key must fit 63 bits at build time."""
-    X = np.zeros((70000, 33025), np.uint8)  # 33025 odd: 65025 * 2^15 * 33025 * 2^17 > 2^63
+    # 33025 odd: bit_length(65025 * 2^15 * 33025) = 46, plus 18 bits of id for n > 2^17: 64 > 63
+    X = np.zeros(((1 << 17) + 1, 33025), np.uint8)  # calloc: never touched
     with pytest.raises(ak.AknnError) as e:
         ak.Index(X)
     assert e.value.status == ak.AKNN_EINVAL
