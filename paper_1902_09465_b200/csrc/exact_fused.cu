@@ -59,6 +59,7 @@ struct XfGeom {
   const int32_t *nx;    // [>= nt * 256] ||x_i||^2 (zero padded)
   unsigned long long *buf;   // [grid][XF_STREAMS][XF_BUF]
   unsigned long long *part;  // [grid][XF_STREAMS][k]
+  const unsigned long long *bound;  // [q] initial per-query threshold (the pilot's k-th key), or null
 };
 
 __device__ __forceinline__ unsigned long long shfl64(unsigned long long v, int src) {
@@ -255,7 +256,9 @@ __global__ void __launch_bounds__(XF_NT, 1)
     unsigned long long *mybuf = g.buf + ((size_t)b * XF_STREAMS + stream) * XF_BUF;
     const bool vrow = row < g.q;
     const int32_t nqr = vrow ? __ldg(g.nq + row) : 0;
-    unsigned long long tau = vrow ? XF_NONE : 0ull;  // an invalid row appends nothing
+    // an invalid row appends nothing; with a pilot bound (the k-th smallest key of a
+    // point sample, itself >= the k-th smallest key overall) only keys <= it are kept
+    unsigned long long tau = !vrow ? 0ull : (g.bound ? g.bound[row] + 1ull : XF_NONE);
     int cnt = 0;
     for (int t = 0; t < ntl; ++t) {
       const uint32_t a = (uint32_t)t & 1u;
@@ -330,7 +333,9 @@ __global__ void __launch_bounds__(XF_NT, 1)
 // One CTA per query: the k smallest keys of its 2 G partial lists (block radix select,
 // 8-bit digits from the top set bit), ranked, -> idx / dist2 rows in (D, id) order.
 constexpr int XM_NT = 512;
-__global__ void __launch_bounds__(XM_NT) k_exact_merge(XfGeom g, int row0, int32_t *idx, int32_t *dist2) {
+// idx == nullptr: the pilot pass -- write the k-th smallest key to bound[row0 + r].
+__global__ void __launch_bounds__(XM_NT) k_exact_merge(XfGeom g, int row0, int32_t *idx, int32_t *dist2,
+                                                       unsigned long long *bound) {
   __shared__ uint32_t hist[256];
   __shared__ unsigned long long red[XM_NT / 32];
   __shared__ int sh_bin, sh_before, sh_cb;
@@ -404,6 +409,10 @@ __global__ void __launch_bounds__(XM_NT) k_exact_merge(XfGeom g, int row0, int32
     __syncthreads();
   }
   if (!found) kth = prefix;
+  if (!idx) {  // pilot: every one of the k keys <= kth is a real point's key
+    if (tid == 0) bound[row0 + r] = kth;
+    return;
+  }
   if (tid == 0) wcount = 0;
   __syncthreads();
   for (int c = tid; c < M; c += XM_NT) {
@@ -426,8 +435,14 @@ __global__ void __launch_bounds__(XM_NT) k_exact_merge(XfGeom g, int row0, int32
 
 int exact_fused_max_k() { return XF_MAX_K; }
 
+// Pilot sample: the first XF_PILOT points (when n >= 4 XF_PILOT) give every query an
+// initial threshold, so the streams of the full pass append only keys that can still
+// reach the top k (without it every stream fills its buffer from the first tiles).
+constexpr int XF_PILOT = 2048;
+
 size_t exact_fused_ws_bytes(int num_sms, int k) {
-  return (size_t)num_sms * XF_STREAMS * (XF_BUF + k) * sizeof(unsigned long long);
+  return (size_t)num_sms * XF_STREAMS * (XF_BUF + k) * sizeof(unsigned long long) +
+         (size_t)num_sms * XF_BM * sizeof(unsigned long long);  // pilot bounds of one launch
 }
 
 // Queries in chunks of at most num_sms m-blocks; ws >= exact_fused_ws_bytes(num_sms, k).
@@ -435,34 +450,51 @@ size_t exact_fused_ws_bytes(int num_sms, int k) {
 cudaError_t launch_exact_fused(const ExactGeom &e, const int32_t *nq, const int32_t *nx, void *ws, int num_sms,
                                cudaStream_t s) {
   if (e.k < 1 || e.k > XF_MAX_K || e.q < 1) return cudaErrorInvalidValue;
-  cudaError_t err = cudaFuncSetAttribute(k_exact_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XF_SMEM);
-  if (err != cudaSuccess) return err;
-  CUtensorMap tx;
-  err = make_map(&tx, e.X, e.n, e.d, e.pitch, XF_BN);
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t err = cudaFuncSetAttribute(k_exact_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XF_SMEM);
+    if (err != cudaSuccess) return err;
+    attr = true;
+  }
+  const bool pilot = e.n >= 4 * XF_PILOT && e.k <= XF_PILOT;
+  CUtensorMap tx, txp;
+  cudaError_t err = make_map(&tx, e.X, e.n, e.d, e.pitch, XF_BN);
+  if (err == cudaSuccess && pilot) err = make_map(&txp, e.X, XF_PILOT, e.d, e.pitch, XF_BN);
   if (err != cudaSuccess) return err;
   const int mt_all = (e.q + XF_BM - 1) / XF_BM;
-  const int nt = (e.n + XF_BN - 1) / XF_BN;
+  unsigned long long *buf = static_cast<unsigned long long *>(ws);
+  unsigned long long *part = buf + (size_t)num_sms * XF_STREAMS * XF_BUF;
+  unsigned long long *bnd = part + (size_t)num_sms * XF_STREAMS * e.k;
   for (int mb0 = 0; mb0 < mt_all; mb0 += num_sms) {
     const int mt = std::min(num_sms, mt_all - mb0);
     const int row0 = mb0 * XF_BM, qn = std::min(e.q - row0, mt * XF_BM);
+    CUtensorMap tq;
+    err = make_map(&tq, e.Q + (size_t)row0 * e.pitch, qn, e.d, e.pitch, XF_BM);
+    if (err != cudaSuccess) return err;
     XfGeom g{};
     g.q = qn;
-    g.n = e.n;
     g.k = e.k;
     g.mt = mt;
-    g.G = std::max(1, std::min(nt, num_sms / mt));
-    g.nt = nt;
     g.nk = (e.d + MM_BK - 1) / MM_BK;
     g.id_offset = e.id_offset;
     g.nq = nq + row0;
     g.nx = nx;
-    g.buf = static_cast<unsigned long long *>(ws);
-    g.part = g.buf + (size_t)num_sms * XF_STREAMS * XF_BUF;
-    CUtensorMap tq;
-    err = make_map(&tq, e.Q + (size_t)row0 * e.pitch, qn, e.d, e.pitch, XF_BM);
-    if (err != cudaSuccess) return err;
+    g.buf = buf;
+    g.part = part;
+    if (pilot) {  // the same kernel over the sample, then its k-th key per query
+      g.n = XF_PILOT;
+      g.nt = XF_PILOT / XF_BN;
+      g.G = std::max(1, std::min(g.nt, num_sms / mt));
+      g.bound = nullptr;
+      k_exact_fused<<<mt * g.G, XF_NT, XF_SMEM, s>>>(tq, txp, g);
+      k_exact_merge<<<qn, XM_NT, 0, s>>>(g, 0, nullptr, nullptr, bnd);
+    }
+    g.n = e.n;
+    g.nt = (e.n + XF_BN - 1) / XF_BN;
+    g.G = std::max(1, std::min(g.nt, num_sms / mt));
+    g.bound = pilot ? bnd : nullptr;
     k_exact_fused<<<mt * g.G, XF_NT, XF_SMEM, s>>>(tq, tx, g);
-    k_exact_merge<<<qn, XM_NT, 0, s>>>(g, row0, e.idx, e.dist2);
+    k_exact_merge<<<qn, XM_NT, 0, s>>>(g, row0, e.idx, e.dist2, nullptr);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
   }
