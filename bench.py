@@ -71,8 +71,8 @@ def _args():
                     help="sec5: the paper's §5 sweep (recall / fraction vs C_alpha, sec5.py)")
     ap.add_argument("--trials", type=int, default=20, help="sec5: trials per (workload, C_alpha)")
     ap.add_argument("--c-alpha", default="1e-5,1e-4,1e-3,1e-2", help="sec5: C_alpha values")
-    ap.add_argument("--sec5-schedules", default="a1,br,br_lead3",
-                    help="sec5: a1, br and/or br_lead<L> (close-side lead L)")
+    ap.add_argument("--sec5-schedules", default="a1,br,br_lead3,br_g2",
+                    help="sec5: a1, br, br_lead<L> (close-side lead L), br_g2[_lead<L>] (growth < 2), br_wor")
     ap.add_argument("--sec5-workloads", default="p10,p100,p1000,images")
     ap.add_argument("--sec5-threads", type=int, default=80, help="sec5: trials in flight")
     ap.add_argument("--sec5-a1-max-iters", type=int, default=0,

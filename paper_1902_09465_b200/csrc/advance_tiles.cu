@@ -227,6 +227,13 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Geom g) {
   // density is read 256 tiles at a time and compacted in order
   const long long t0 = (long long)blockIdx.x * ntot / gridDim.x, t1 = (long long)(blockIdx.x + 1) * ntot / gridDim.x;
   int staged_tp = -1;
+  __shared__ __align__(8) uint64_t tbar;  // row staging mbarrier (bulk TMA copies)
+  const uint32_t bar_s = (uint32_t)__cvta_generic_to_shared(&tbar);
+  uint32_t bar_phase = 0;
+  if (tid == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(bar_s));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   int gen_tp = -1, gen_c = -1;  // shared draws: the column / level whose draw list is in dbuf
   __shared__ unsigned long long s_blocks, s_draws;  // Philox blocks and pair draws (statistics)
   if (tid == 0) s_blocks = s_draws = 0;
@@ -260,11 +267,33 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Geom g) {
     __syncthreads();  // the previous tile's shared memory is no longer in use
     if (tid < MAX_LEVELS) lcnt[tid] = 0;
 
-    // stage the rows: asynchronous 16-byte copies (cp.async), all in flight at once;
-    // rows past q / n are never referenced and are left as they are.  Shared draws:
-    // the query rows transposed (Qt), no point rows (their bytes are in the draw list)
+    // stage the rows.  Bulk TMA copies (one cp.async.bulk per row, issued by thread 0,
+    // completion counted in bytes on an mbarrier) unless g.tile_tma == 0; otherwise
+    // 16-byte cp.async copies, all in flight at once.  Rows past q / n are never
+    // referenced and are left as they are.  Shared draws: the query rows transposed
+    // (Qt), no point rows (their bytes are in the draw list)
+    const bool tma = !f1 && g.tile_tma;
+    if (tma && tid == 0) {
+      uint32_t bytes = 0;
+      const int nrow = reuse_x ? R : R + P;
+      for (int row = 0; row < nrow; ++row)
+        bytes += (row < R ? r0 + row < g.q : p0 + row - R < g.n) ? (uint32_t)pitch : 0u;
+      // the previous tile's generic-proxy reads of these slots precede the async writes
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar_s), "r"(bytes) : "memory");
+      for (int row = 0; row < nrow; ++row) {
+        const uint8_t *src = row < R ? (r0 + row < g.q ? g.Q + (size_t)(r0 + row) * pitch : nullptr)
+                                     : (p0 + row - R < g.n ? g.X + (size_t)(p0 + row - R) * pitch : nullptr);
+        if (src)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  rows_s + ((uint32_t)row << sl)),
+              "l"(src), "r"((uint32_t)pitch), "r"(bar_s)
+              : "memory");
+      }
+    }
     if (f1) f1_stage_qt(g, r0, reinterpret_cast<uint32_t *>(tsm + (rows_s - base)));
-    for (int v = tid; v < (f1 ? 0 : (reuse_x ? R : R + P) * nv); v += NT) {
+    for (int v = tid; v < ((f1 || tma) ? 0 : (reuse_x ? R : R + P) * nv); v += NT) {
       const int row = v / nv, c = v - row * nv;
       const uint8_t *src = nullptr;
       if (row < R) {
@@ -332,6 +361,16 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Geom g) {
       if (a) lst[b0 + __popc(m & ((1u << lane_id()) - 1u))] = (uint16_t)(e4 + k);
     }
     asm volatile("cp.async.wait_group 0;" ::: "memory");
+    if (tma) {  // every thread waits for the tile's bytes (phase bar_phase)
+      asm volatile(
+          "{\n\t.reg .pred p;\n\t"
+          "TW_%=:\n\t"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+          "@!p bra TW_%=;\n\t}" ::"r"(bar_s),
+          "r"(bar_phase)
+          : "memory");
+      bar_phase ^= 1u;
+    }
     __syncthreads();
 
     // the draws, level by level.  nb <= ADV_TP blocks per pair: a thread owns

@@ -330,6 +330,7 @@ void setup_tiles(Geom &g, const TileShape &t, const aknn_opts &o, int64_t qb, ui
   g.tile_cols = (int)((g.npad + (1ll << t.lp) - 1) >> t.lp);
   g.tilework = reinterpret_cast<uint32_t *>(ws);
   g.tile_slot_l = tile_slot_log2(g.pitch);
+  g.tile_tma = env_int("AKNN_TILE_TMA", 1) ? 1 : 0;  // A/B measurements only
   // consecutive tiles of a point column share the staged point rows: a tile stages
   // about its R query rows (+ one point row's share)
   g.tile_min_draws = t.row_draws * (float)((1 << t.lr) + 1);

@@ -1,6 +1,6 @@
 // exact_fused.cu -- the exact comparison pass (row a10; "compute all distances,
 // then sort") as ONE persistent tensor-core kernel whose epilogue keeps each query's
-// running top-k, so the [q][n] distance matrix is never written.
+// running top-k candidates, so the [q][n] distance matrix is never written.
 //
 //   D(q, i) = ||x_i||^2 + ||q||^2 - 2 <x_i, q>   (u8 x u8 -> s32 on tcgen05, exact:
 //   d * 255^2 < 2^31 for d <= 33025), ranked by the composite key (D << 32 | i), i.e.
@@ -11,22 +11,26 @@
 // G = #SMs / mt contiguous ranges of point tiles, so the mt CTAs of one range stream
 // the same X tiles at the same time (X read from HBM about once, the other m-blocks
 // hit L2).  Per CTA:
-//   warp 0 lane 0   TMA producer: Q k-block (128 x 128 B) + X k-block (256 x 128 B) per
-//                   stage, 4-stage ring, running ahead across the CTA's tiles
+//   warp 0 lane 0   TMA producer.  d <= 1152 (QRES): the CTA's 128 query rows are
+//                   loaded into shared memory ONCE (nk k-blocks of 128 x 128 B), then
+//                   only X k-blocks (256 x 128 B) stream through a ring of 2-6 stages;
+//                   wider rows stream Q and X k-blocks together through 4 stages
 //   warp 1          TMEM owner (512 columns = two 128 x 256 int32 accumulators) and,
 //                   lane 0, the MMA issuer: 4 x tcgen05.mma kind::i8 (K = 32 B) per
-//                   stage into accumulator t & 1, commit -> stage free / tile done
+//                   k-block into accumulator t & 1, commit -> stage free / tile done
 //   warps 4..11     epilogue (TMEM lane quadrant = warp % 4, column half = (warp-4)/4):
 //                   thread = one (query row, column half) STREAM with a candidate
-//                   buffer (global, L2-resident) and a threshold tau = the k-th
-//                   smallest key kept so far; a key < tau is appended.  When a buffer
-//                   is full the warp compacts it to its k smallest with a warp radix
-//                   select (tau = the k-th).  The accumulator is released as soon as
-//                   its last chunk is in registers, so the MMAs of tile t+2 overlap.
-//   end of range    each stream's k smallest -> part[]; k_exact_merge then picks each
-//                   query's k smallest of its 2 G lists and sorts them.
-// Expected appends per stream ~ CAP * log_{CAP/k}(points/CAP): a few compactions per
-// stream.
+//                   buffer (global, L2-resident) and a threshold tau; a key < tau is
+//                   appended.  tau starts at the pilot bound (below) and, when a buffer
+//                   fills, the warp compacts it to its k smallest (warp radix select,
+//                   tau = the k-th).  The accumulator is released as soon as its last
+//                   chunk is in registers, so the MMAs of tile t+2 overlap.
+//   end             each stream leaves its candidates (unsorted) and their count;
+//                   k_exact_merge selects each query's k smallest of all its streams'
+//                   candidates (block radix select in shared memory) and sorts them.
+// Pilot: for n >= 4 * XF_PILOT the same two kernels first run over the first XF_PILOT
+// points; each query's k-th smallest key there bounds its k-th smallest key overall,
+// so the full pass appends only keys that can still reach the top k.
 #include <cuda.h>
 
 #include <algorithm>
@@ -37,28 +41,31 @@
 
 namespace aknn {
 
-constexpr int XF_BM = 128, XF_BN = 256, XF_STAGES = 4;
+constexpr int XF_BM = 128, XF_BN = 256;
 constexpr int XF_EPI_WARP0 = 4, XF_EPI_WARPS = 8, XF_NT = 32 * (XF_EPI_WARP0 + XF_EPI_WARPS);
 constexpr uint32_t XF_A_BYTES = XF_BM * MM_BK, XF_B_BYTES = XF_BN * MM_BK;
-constexpr uint32_t XF_STAGE_BYTES = XF_A_BYTES + XF_B_BYTES;
 constexpr int XF_CAP = 512;             // compaction threshold of a stream's buffer
 constexpr int XF_BUF = XF_CAP + 32;     // + one 32-column chunk of slack
 constexpr int XF_E = XF_BUF / 32;       // keys per lane in a warp compaction
 constexpr int XF_MAX_K = 128;
 constexpr int XF_STREAMS = 2 * XF_BM;   // streams per CTA: (column half, row)
-constexpr size_t XF_SMEM = (size_t)XF_STAGES * XF_STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/ +
-                           (size_t)XF_EPI_WARPS * 256 * 4 /*radix histograms*/;
+constexpr int XF_PILOT = 2048;
+constexpr size_t XF_SMEM_MAX = 227 * 1024;
+constexpr size_t XF_HIST_BYTES = (size_t)XF_EPI_WARPS * 256 * 4;  // static: radix histograms
+constexpr size_t XF_FIXED = 1024 /*align*/ + 256 /*barriers*/;
+constexpr int XF_QRES_MAXK = 9;         // Q resident for d <= 9 * 128
 constexpr unsigned long long XF_NONE = ~0ull;
 
 struct XfGeom {
   int q, n, k;          // queries of this launch, points, neighbours
   int mt, G, nt;        // m-blocks, point-tile ranges per m-block, point tiles
   int nk;               // 128-byte k-blocks of d
+  int nstages;          // ring stages
   uint32_t id_offset;
   const int32_t *nq;    // [q] ||q||^2 of this launch's queries
   const int32_t *nx;    // [>= nt * 256] ||x_i||^2 (zero padded)
-  unsigned long long *buf;   // [grid][XF_STREAMS][XF_BUF]
-  unsigned long long *part;  // [grid][XF_STREAMS][k]
+  unsigned long long *buf;   // [grid][XF_STREAMS][XF_BUF] candidate keys
+  uint32_t *pcnt;            // [grid][XF_STREAMS] candidates per stream
   const unsigned long long *bound;  // [q] initial per-query threshold (the pilot's k-th key), or null
 };
 
@@ -67,31 +74,49 @@ __device__ __forceinline__ unsigned long long shfl64(unsigned long long v, int s
   return ((unsigned long long)hi << 32) | lo;
 }
 
+// Radix digit start: the highest 8-bit digit in which the valid keys differ (the
+// common higher bits are fixed at once, so no pass piles every key into one bin).
+__device__ __forceinline__ int radix_top_shift(unsigned long long andk, unsigned long long ork) {
+  const unsigned long long diff = andk ^ ork;
+  return diff ? ((63 - __clzll((long long)diff)) >> 3) << 3 : -8;
+}
+
 // Warp-cooperative: the c keys in b[0..c) (unique), k <= c.  Finds the k-th smallest by
-// an 8-bit radix select (histogram in `hist`, 256 words of this warp's shared memory),
-// moves the k smallest to b[0..k) (any order) and returns the k-th smallest.
+// an 8-bit radix select (histogram `hist`: 256 words of this warp's shared memory,
+// warp-aggregated increments), moves the k smallest to b[0..k) (any order) and returns
+// the k-th smallest.
 __device__ unsigned long long warp_compact(unsigned long long *b, int c, int k, uint32_t *hist, int lane) {
   unsigned long long key[XF_E];
-  unsigned long long orr = 0;
+  unsigned long long orr = 0, andk = XF_NONE;
 #pragma unroll
   for (int e = 0; e < XF_E; ++e) {
     const int i = lane + 32 * e;
     key[e] = i < c ? b[i] : XF_NONE;
-    if (i < c) orr |= key[e];
+    if (i < c) {
+      orr |= key[e];
+      andk &= key[e];
+    }
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) orr |= shfl64(orr, lane ^ o);
-  const int top = orr ? 63 - __clzll((long long)orr) : 0;
-  unsigned long long prefix = 0, pmask = 0, kth = 0;
+  for (int o = 16; o > 0; o >>= 1) {
+    orr |= shfl64(orr, lane ^ o);
+    andk &= shfl64(andk, lane ^ o);
+  }
+  int shift = radix_top_shift(andk, orr);
+  unsigned long long pmask = shift >= 0 ? ~((1ull << (shift + 8)) - 1ull) : XF_NONE;
+  unsigned long long prefix = andk & pmask, kth = prefix;
   int want = k;
-  bool found = false;
-  for (int shift = (top >> 3) << 3; shift >= 0; shift -= 8) {
+  for (; shift >= 0; shift -= 8) {
 #pragma unroll
     for (int i = 0; i < 8; ++i) hist[lane * 8 + i] = 0;
     __syncwarp();
 #pragma unroll
-    for (int e = 0; e < XF_E; ++e)
-      if (key[e] != XF_NONE && (key[e] & pmask) == prefix) atomicAdd(&hist[(uint32_t)(key[e] >> shift) & 255u], 1u);
+    for (int e = 0; e < XF_E; ++e) {
+      const bool v = key[e] != XF_NONE && (key[e] & pmask) == prefix;
+      const uint32_t bin = v ? (uint32_t)(key[e] >> shift) & 255u : 256u;
+      const uint32_t m = __match_any_sync(0xffffffffu, bin);
+      if (v && lane == __ffs(m) - 1) atomicAdd(&hist[bin], (uint32_t)__popc(m));
+    }
     __syncwarp();
     uint32_t h[8], loc = 0;
 #pragma unroll
@@ -127,6 +152,7 @@ __device__ unsigned long long warp_compact(unsigned long long *b, int c, int k, 
     prefix |= (unsigned long long)bin << shift;
     pmask |= 255ull << shift;
     want -= (int)before;
+    kth = prefix;
     if (cb == 1u) {  // the k-th key is the only one with this prefix
       unsigned long long mine = 0;
       bool has = false;
@@ -138,12 +164,10 @@ __device__ unsigned long long warp_compact(unsigned long long *b, int c, int k, 
         }
       const int s2 = __ffs(__ballot_sync(0xffffffffu, has)) - 1;
       kth = shfl64(mine, s2);
-      found = true;
       break;
     }
     __syncwarp();
   }
-  if (!found) kth = prefix;  // all 64 bits decided
   // keep the keys <= kth: exactly k of them (keys are unique)
   int base = 0;
   const uint32_t lt = (1u << lane) - 1u;
@@ -158,25 +182,31 @@ __device__ unsigned long long warp_compact(unsigned long long *b, int c, int k, 
   return kth;
 }
 
+template <bool QRES>
 __global__ void __launch_bounds__(XF_NT, 1)
     k_exact_fused(const __grid_constant__ CUtensorMap tmQ, const __grid_constant__ CUtensorMap tmX,
                   const __grid_constant__ XfGeom g) {
+  __shared__ uint32_t hist_all[XF_EPI_WARPS][256];
   const int b = blockIdx.x, mb = b % g.mt, seg = b / g.mt;
   const int t_begin = (int)((long long)seg * g.nt / g.G), t_end = (int)((long long)(seg + 1) * g.nt / g.G);
   const int ntl = t_end - t_begin;
   const int m0 = mb * XF_BM;
+  const uint32_t stage_bytes = QRES ? XF_B_BYTES : XF_A_BYTES + XF_B_BYTES;
+  const uint32_t qres_bytes = QRES ? (uint32_t)g.nk * XF_A_BYTES : 0u;
   extern __shared__ __align__(1024) unsigned char smraw[];
   unsigned char *sm = reinterpret_cast<unsigned char *>(((uintptr_t)smraw + 1023) & ~(uintptr_t)1023);
-  uint64_t *full = reinterpret_cast<uint64_t *>(sm + XF_STAGES * XF_STAGE_BYTES);
-  uint64_t *empty = full + XF_STAGES;
-  uint64_t *tfull = empty + XF_STAGES;  // [2]
-  uint64_t *tempty = tfull + 2;         // [2]
-  uint32_t *tmem_base = reinterpret_cast<uint32_t *>(tempty + 2);
-  uint32_t *hist_all = reinterpret_cast<uint32_t *>(sm + XF_STAGES * XF_STAGE_BYTES + 256);
+  unsigned char *ring = sm + qres_bytes;  // QRES: [Q k-blocks][ring]; else [ring of Q|X]
+  uint64_t *full = reinterpret_cast<uint64_t *>(ring + (size_t)g.nstages * stage_bytes);
+  uint64_t *empty = full + 8;
+  uint64_t *tfull = empty + 8;   // [2]
+  uint64_t *tempty = tfull + 2;  // [2]
+  uint64_t *qfull = tempty + 2;
+  uint32_t *tmem_base = reinterpret_cast<uint32_t *>(qfull + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t S = (uint32_t)g.nstages;
 
   if (warp == 0 && lane == 0) {
-    for (int s = 0; s < XF_STAGES; ++s) {
+    for (uint32_t s = 0; s < S; ++s) {
       mbar_init(full + s, 1);
       mbar_init(empty + s, 1);
     }
@@ -184,6 +214,7 @@ __global__ void __launch_bounds__(XF_NT, 1)
       mbar_init(tfull + a, 1);
       mbar_init(tempty + a, XF_EPI_WARPS);
     }
+    mbar_init(qfull, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmQ)) : "memory");
     asm volatile("prefetch.tensormap [%0];" ::"l"(reinterpret_cast<uint64_t>(&tmX)) : "memory");
@@ -200,22 +231,31 @@ __global__ void __launch_bounds__(XF_NT, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // TMA producer
+      if (QRES) {     // the CTA's query rows, once
+        mbar_expect_tx(qfull, qres_bytes);
+        for (int kb = 0; kb < g.nk; ++kb) tma_load_2d(sm + (size_t)kb * XF_A_BYTES, &tmQ, qfull, kb * MM_BK, m0);
+      }
       uint32_t kg = 0;
       for (int t = 0; t < ntl; ++t) {
         const int n0 = (t_begin + t) * XF_BN;
         for (int kb = 0; kb < g.nk; ++kb, ++kg) {
-          const uint32_t s = kg % XF_STAGES;
-          if (kg >= XF_STAGES) mbar_wait(empty + s, ((kg / XF_STAGES) - 1) & 1);
-          unsigned char *sa = sm + s * XF_STAGE_BYTES;
-          mbar_expect_tx(full + s, XF_STAGE_BYTES);
-          tma_load_2d(sa, &tmQ, full + s, kb * MM_BK, m0);
-          tma_load_2d(sa + XF_A_BYTES, &tmX, full + s, kb * MM_BK, n0);
+          const uint32_t s = kg % S;
+          if (kg >= S) mbar_wait(empty + s, ((kg / S) - 1) & 1);
+          unsigned char *sa = ring + s * stage_bytes;
+          mbar_expect_tx(full + s, stage_bytes);
+          if (QRES) {
+            tma_load_2d(sa, &tmX, full + s, kb * MM_BK, n0);
+          } else {
+            tma_load_2d(sa, &tmQ, full + s, kb * MM_BK, m0);
+            tma_load_2d(sa + XF_A_BYTES, &tmX, full + s, kb * MM_BK, n0);
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // MMA issuer
       constexpr uint32_t idesc = umma_idesc_u8(XF_BM, XF_BN);
+      if (QRES) mbar_wait(qfull, 0);
       uint32_t kg = 0;
       for (int t = 0; t < ntl; ++t) {
         const uint32_t a = (uint32_t)t & 1u;
@@ -225,10 +265,12 @@ __global__ void __launch_bounds__(XF_NT, 1)
         }
         const uint32_t acc_addr = tmem + a * XF_BN;
         for (int kb = 0; kb < g.nk; ++kb, ++kg) {
-          const uint32_t s = kg % XF_STAGES;
-          mbar_wait(full + s, (kg / XF_STAGES) & 1);
+          const uint32_t s = kg % S;
+          mbar_wait(full + s, (kg / S) & 1);
           asm volatile("tcgen05.fence::after_thread_sync;");
-          const uint32_t sa = smem_u32(sm + s * XF_STAGE_BYTES), sb = sa + XF_A_BYTES;
+          const uint32_t st = smem_u32(ring + s * stage_bytes);
+          const uint32_t sa = QRES ? smem_u32(sm + (size_t)kb * XF_A_BYTES) : st;
+          const uint32_t sb = QRES ? st : st + XF_A_BYTES;
 #pragma unroll
           for (int kk = 0; kk < MM_BK / 32; ++kk) {
             const uint64_t da = umma_desc_sw128(sa + kk * 32), db = umma_desc_sw128(sb + kk * 32);
@@ -252,7 +294,7 @@ __global__ void __launch_bounds__(XF_NT, 1)
     const int quad = warp & 3, half = (warp - XF_EPI_WARP0) >> 2;
     const int lrow = quad * 32 + lane, row = m0 + lrow;
     const int stream = half * XF_BM + lrow;
-    uint32_t *hist = hist_all + (warp - XF_EPI_WARP0) * 256;
+    uint32_t *hist = hist_all[warp - XF_EPI_WARP0];
     unsigned long long *mybuf = g.buf + ((size_t)b * XF_STREAMS + stream) * XF_BUF;
     const bool vrow = row < g.q;
     const int32_t nqr = vrow ? __ldg(g.nq + row) : 0;
@@ -305,21 +347,7 @@ __global__ void __launch_bounds__(XF_NT, 1)
         }
       }
     }
-    // end of the range: each stream's k smallest -> part
-    __syncwarp();
-    uint32_t need = __ballot_sync(0xffffffffu, cnt > g.k);
-    while (need) {
-      const int L = __ffs(need) - 1;
-      need &= need - 1u;
-      unsigned long long *bl =
-          reinterpret_cast<unsigned long long *>(shfl64(reinterpret_cast<unsigned long long>(mybuf), L));
-      const int cl = __shfl_sync(0xffffffffu, cnt, L);
-      warp_compact(bl, cl, g.k, hist, lane);
-      if (lane == L) cnt = g.k;
-    }
-    __syncwarp();
-    unsigned long long *out = g.part + ((size_t)b * XF_STREAMS + stream) * g.k;
-    for (int j = 0; j < g.k; ++j) out[j] = j < cnt ? mybuf[j] : XF_NONE;
+    g.pcnt[(size_t)b * XF_STREAMS + stream] = (uint32_t)cnt;  // unsorted candidates for the merge
   }
   __syncwarp();
   asm volatile("tcgen05.fence::before_thread_sync;");
@@ -330,53 +358,100 @@ __global__ void __launch_bounds__(XF_NT, 1)
   }
 }
 
-// One CTA per query: the k smallest keys of its 2 G partial lists (block radix select,
-// 8-bit digits from the top set bit), ranked, -> idx / dist2 rows in (D, id) order.
+// One CTA per query: the k smallest of the candidates of its 2 G streams.  The
+// streams' counts are scanned into offsets; the candidates (<= XM_SMEM_KEYS of them)
+// are copied into shared memory once and selected there by an 8-bit radix select from
+// the highest differing digit with warp-aggregated histogram increments (beyond that
+// the passes read them from global memory).  The k winners are ranked and written.
+// idx == nullptr: the pilot -- write the k-th smallest key to bound[row0 + r].
 constexpr int XM_NT = 512;
-// idx == nullptr: the pilot pass -- write the k-th smallest key to bound[row0 + r].
+constexpr int XM_SMEM_KEYS = 20480;       // 160 KB of dynamic shared memory
+constexpr int XM_MAX_STREAMS = 2 * 160;
+
 __global__ void __launch_bounds__(XM_NT) k_exact_merge(XfGeom g, int row0, int32_t *idx, int32_t *dist2,
                                                        unsigned long long *bound) {
+  extern __shared__ unsigned long long skeys[];
   __shared__ uint32_t hist[256];
-  __shared__ unsigned long long red[XM_NT / 32];
+  __shared__ uint32_t soff[XM_MAX_STREAMS + 1];
+  __shared__ unsigned long long red_o[XM_NT / 32], red_a[XM_NT / 32];
   __shared__ int sh_bin, sh_before, sh_cb;
+  __shared__ unsigned long long sh_kth;
   __shared__ unsigned long long win[XF_MAX_K];
   __shared__ unsigned wcount;
   const int r = blockIdx.x;  // query of this launch
   const int mb = r / XF_BM, lrow = r % XF_BM, k = g.k;
-  const int nlist = 2 * g.G, M = nlist * k;
-  auto cand = [&](int c) -> unsigned long long {
-    const int l = c / k, j = c - l * k;
-    const int seg = l >> 1, half = l & 1;
-    const size_t cta = (size_t)seg * g.mt + mb;
-    return g.part[(cta * XF_STREAMS + half * XF_BM + lrow) * k + j];
-  };
+  const int nl = 2 * g.G;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
-  unsigned long long orr = 0;
+  auto stream_base = [&](int l) -> size_t {
+    const int seg = l >> 1, half = l & 1;
+    return ((size_t)seg * g.mt + mb) * XF_STREAMS + half * XF_BM + lrow;
+  };
+  if (tid == 0) {
+    uint32_t a = 0;
+    for (int l = 0; l < nl; ++l) {
+      soff[l] = a;
+      a += g.pcnt[stream_base(l)];
+    }
+    soff[nl] = a;
+  }
+  __syncthreads();
+  const int M = (int)soff[nl];
+  const bool in_smem = M <= XM_SMEM_KEYS;
+  auto gkey = [&](int c) -> unsigned long long {  // candidate c in global memory
+    int lo = 0, hi = nl;                          // the stream l with soff[l] <= c < soff[l+1]
+    while (hi - lo > 1) {
+      const int mid = (lo + hi) >> 1;
+      if (soff[mid] <= (uint32_t)c) lo = mid; else hi = mid;
+    }
+    return g.buf[stream_base(lo) * XF_BUF + (c - (int)soff[lo])];
+  };
+  if (in_smem)
+    for (int c = tid; c < M; c += XM_NT) skeys[c] = gkey(c);
+  __syncthreads();
+  auto key_at = [&](int c) -> unsigned long long { return in_smem ? skeys[c] : gkey(c); };
+  // common high bits of all candidates
+  unsigned long long orr = 0, andk = XF_NONE;
   for (int c = tid; c < M; c += XM_NT) {
-    const unsigned long long v = cand(c);
-    if (v != XF_NONE) orr |= v;
+    const unsigned long long v = key_at(c);
+    orr |= v;
+    andk &= v;
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) orr |= shfl64(orr, lane ^ o);
-  if (lane == 0) red[wid] = orr;
-  __syncthreads();
-  if (tid == 0) {
-    unsigned long long a = 0;
-    for (int w = 0; w < XM_NT / 32; ++w) a |= red[w];
-    red[0] = a;
+  for (int o = 16; o > 0; o >>= 1) {
+    orr |= shfl64(orr, lane ^ o);
+    andk &= shfl64(andk, lane ^ o);
+  }
+  if (lane == 0) {
+    red_o[wid] = orr;
+    red_a[wid] = andk;
   }
   __syncthreads();
-  orr = red[0];
-  const int top = orr ? 63 - __clzll((long long)orr) : 0;
-  unsigned long long prefix = 0, pmask = 0, kth = 0;
+  if (tid == 0) {
+    unsigned long long o2 = 0, a2 = XF_NONE;
+    for (int w = 0; w < XM_NT / 32; ++w) {
+      o2 |= red_o[w];
+      a2 &= red_a[w];
+    }
+    red_o[0] = o2;
+    red_a[0] = a2;
+  }
+  __syncthreads();
+  orr = red_o[0];
+  andk = red_a[0];
+  int shift = radix_top_shift(andk, orr);
+  unsigned long long pmask = shift >= 0 ? ~((1ull << (shift + 8)) - 1ull) : XF_NONE;
+  unsigned long long prefix = andk & pmask, kth = prefix;
   int want = k;
-  bool found = false;
-  for (int shift = (top >> 3) << 3; shift >= 0 && !found; shift -= 8) {
+  for (; shift >= 0; shift -= 8) {
     for (int i = tid; i < 256; i += XM_NT) hist[i] = 0;
     __syncthreads();
-    for (int c = tid; c < M; c += XM_NT) {
-      const unsigned long long v = cand(c);
-      if (v != XF_NONE && (v & pmask) == prefix) atomicAdd(&hist[(uint32_t)(v >> shift) & 255u], 1u);
+    for (int c0 = 0; c0 < M; c0 += XM_NT) {  // every thread runs every iteration: full-warp match
+      const int c = c0 + tid;
+      const unsigned long long v = c < M ? key_at(c) : XF_NONE;
+      const bool ok = c < M && (v & pmask) == prefix;
+      const uint32_t bin = ok ? (uint32_t)(v >> shift) & 255u : 256u;
+      const uint32_t m = __match_any_sync(0xffffffffu, bin);
+      if (ok && lane == __ffs(m) - 1) atomicAdd(&hist[bin], (uint32_t)__popc(m));
     }
     __syncthreads();
     if (tid == 0) {
@@ -397,18 +472,18 @@ __global__ void __launch_bounds__(XM_NT) k_exact_merge(XfGeom g, int row0, int32
     prefix |= (unsigned long long)sh_bin << shift;
     pmask |= 255ull << shift;
     want -= sh_before;
-    if (sh_cb == 1) {
+    kth = prefix;
+    if (sh_cb == 1) {  // unique: locate it
       for (int c = tid; c < M; c += XM_NT) {
-        const unsigned long long v = cand(c);
-        if (v != XF_NONE && (v & pmask) == prefix) red[0] = v;
+        const unsigned long long v = key_at(c);
+        if ((v & pmask) == prefix) sh_kth = v;
       }
       __syncthreads();
-      kth = red[0];
-      found = true;
+      kth = sh_kth;
+      break;
     }
     __syncthreads();
   }
-  if (!found) kth = prefix;
   if (!idx) {  // pilot: every one of the k keys <= kth is a real point's key
     if (tid == 0) bound[row0 + r] = kth;
     return;
@@ -416,8 +491,8 @@ __global__ void __launch_bounds__(XM_NT) k_exact_merge(XfGeom g, int row0, int32
   if (tid == 0) wcount = 0;
   __syncthreads();
   for (int c = tid; c < M; c += XM_NT) {
-    const unsigned long long v = cand(c);
-    if (v <= kth && v != XF_NONE) {
+    const unsigned long long v = key_at(c);
+    if (v <= kth) {
       const unsigned p = atomicAdd(&wcount, 1u);
       if (p < XF_MAX_K) win[p] = v;
     }
@@ -435,24 +510,34 @@ __global__ void __launch_bounds__(XM_NT) k_exact_merge(XfGeom g, int row0, int32
 
 int exact_fused_max_k() { return XF_MAX_K; }
 
-// Pilot sample: the first XF_PILOT points (when n >= 4 XF_PILOT) give every query an
-// initial threshold, so the streams of the full pass append only keys that can still
-// reach the top k (without it every stream fills its buffer from the first tiles).
-constexpr int XF_PILOT = 2048;
-
 size_t exact_fused_ws_bytes(int num_sms, int k) {
-  return (size_t)num_sms * XF_STREAMS * (XF_BUF + k) * sizeof(unsigned long long) +
-         (size_t)num_sms * XF_BM * sizeof(unsigned long long);  // pilot bounds of one launch
+  (void)k;
+  return (size_t)num_sms * XF_STREAMS * XF_BUF * sizeof(unsigned long long) +  // candidates
+         (size_t)num_sms * XF_STREAMS * sizeof(uint32_t) +                     // their counts
+         (size_t)num_sms * XF_BM * sizeof(unsigned long long);                  // pilot bounds
 }
 
 // Queries in chunks of at most num_sms m-blocks; ws >= exact_fused_ws_bytes(num_sms, k).
 // nx must be readable (zero padded) up to round_up(n, 256).
 cudaError_t launch_exact_fused(const ExactGeom &e, const int32_t *nq, const int32_t *nx, void *ws, int num_sms,
                                cudaStream_t s) {
-  if (e.k < 1 || e.k > XF_MAX_K || e.q < 1) return cudaErrorInvalidValue;
+  if (e.k < 1 || e.k > XF_MAX_K || e.q < 1 || 2 * num_sms > XM_MAX_STREAMS) return cudaErrorInvalidValue;
+  const int nk = (e.d + MM_BK - 1) / MM_BK;
+  const bool qres = nk <= XF_QRES_MAXK;
+  const size_t stage = qres ? XF_B_BYTES : XF_A_BYTES + XF_B_BYTES;
+  const size_t dyn_max = XF_SMEM_MAX - XF_HIST_BYTES;  // the histograms are static shared memory
+  const size_t avail = dyn_max - XF_FIXED - (qres ? (size_t)nk * XF_A_BYTES : 0);
+  const int nst = (int)std::min<size_t>(qres ? 6 : 4, avail / stage);
+  if (nst < 2) return cudaErrorInvalidValue;
+  const size_t smem = XF_FIXED + (qres ? (size_t)nk * XF_A_BYTES : 0) + (size_t)nst * stage;
   static bool attr = false;
   if (!attr) {
-    cudaError_t err = cudaFuncSetAttribute(k_exact_fused, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XF_SMEM);
+    cudaError_t err = cudaFuncSetAttribute(k_exact_fused<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max);
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(k_exact_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max);
+    if (err == cudaSuccess)
+      err = cudaFuncSetAttribute(k_exact_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(XM_SMEM_KEYS * sizeof(unsigned long long)));
     if (err != cudaSuccess) return err;
     attr = true;
   }
@@ -463,8 +548,9 @@ cudaError_t launch_exact_fused(const ExactGeom &e, const int32_t *nq, const int3
   if (err != cudaSuccess) return err;
   const int mt_all = (e.q + XF_BM - 1) / XF_BM;
   unsigned long long *buf = static_cast<unsigned long long *>(ws);
-  unsigned long long *part = buf + (size_t)num_sms * XF_STREAMS * XF_BUF;
-  unsigned long long *bnd = part + (size_t)num_sms * XF_STREAMS * e.k;
+  uint32_t *pcnt = reinterpret_cast<uint32_t *>(buf + (size_t)num_sms * XF_STREAMS * XF_BUF);
+  unsigned long long *bnd = reinterpret_cast<unsigned long long *>(pcnt + (size_t)num_sms * XF_STREAMS);
+  const size_t msmem = XM_SMEM_KEYS * sizeof(unsigned long long);
   for (int mb0 = 0; mb0 < mt_all; mb0 += num_sms) {
     const int mt = std::min(num_sms, mt_all - mb0);
     const int row0 = mb0 * XF_BM, qn = std::min(e.q - row0, mt * XF_BM);
@@ -475,26 +561,33 @@ cudaError_t launch_exact_fused(const ExactGeom &e, const int32_t *nq, const int3
     g.q = qn;
     g.k = e.k;
     g.mt = mt;
-    g.nk = (e.d + MM_BK - 1) / MM_BK;
+    g.nk = nk;
+    g.nstages = nst;
     g.id_offset = e.id_offset;
     g.nq = nq + row0;
     g.nx = nx;
     g.buf = buf;
-    g.part = part;
-    if (pilot) {  // the same kernel over the sample, then its k-th key per query
+    g.pcnt = pcnt;
+    auto run = [&](const CUtensorMap &txm) {
+      if (qres)
+        k_exact_fused<true><<<mt * g.G, XF_NT, smem, s>>>(tq, txm, g);
+      else
+        k_exact_fused<false><<<mt * g.G, XF_NT, smem, s>>>(tq, txm, g);
+    };
+    if (pilot) {  // the same kernels over the sample, then its k-th key per query
       g.n = XF_PILOT;
       g.nt = XF_PILOT / XF_BN;
       g.G = std::max(1, std::min(g.nt, num_sms / mt));
       g.bound = nullptr;
-      k_exact_fused<<<mt * g.G, XF_NT, XF_SMEM, s>>>(tq, txp, g);
-      k_exact_merge<<<qn, XM_NT, 0, s>>>(g, 0, nullptr, nullptr, bnd);
+      run(txp);
+      k_exact_merge<<<qn, XM_NT, msmem, s>>>(g, 0, nullptr, nullptr, bnd);
     }
     g.n = e.n;
     g.nt = (e.n + XF_BN - 1) / XF_BN;
     g.G = std::max(1, std::min(g.nt, num_sms / mt));
     g.bound = pilot ? bnd : nullptr;
-    k_exact_fused<<<mt * g.G, XF_NT, XF_SMEM, s>>>(tq, tx, g);
-    k_exact_merge<<<qn, XM_NT, 0, s>>>(g, row0, e.idx, e.dist2, nullptr);
+    run(tx);
+    k_exact_merge<<<qn, XM_NT, msmem, s>>>(g, row0, e.idx, e.dist2, nullptr);
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
   }

@@ -17,7 +17,8 @@ reports the median and interquartile range over the trials of
 Both schedules run on the GPU: "a1" is the literal Algorithm 1 (the paper's own,
 aknn_query_a1, one warp per query; trials in flight concurrently, one index and
 stream each), "br" the batched round rule (aknn_query_ex), "br_lead<L>" the batched rule with a
-close-side lead L (aknn_opts.lead, reading R24), "br_wor" the batched rule sampling
+close-side lead L (aknn_opts.lead, reading R24), "br_g2" the batched rule with growth factor < 2 (aknn_opts.growth = 2,
+reading R25; "br_g2_lead<L>" with a lead), "br_wor" the batched rule sampling
 without replacement (AKNN_FLAG_WITHOUT_REPLACEMENT, reading R23).  The exact k-NN per trial
 comes from the exact tensor-core pass (aknn_exact).  The oracle is not used here.
 """
@@ -89,10 +90,15 @@ def run(args, dist) -> None:
                     continue
                 # "br": the batched rule; "br_lead<L>": with a close-side lead L (reading R24);
                 # "br_wor": sampling without replacement (reading R23)
-                lead = int(sname[len("br_lead"):]) if sname.startswith("br_lead") else 1
+                # "br_g2": the growth-factor-< 2 schedule (aknn_opts.growth = 2, reading R25),
+                # "br_g2_lead<L>": with a lead as well
+                g2 = sname.startswith("br_g2")
+                base = sname[len("br_g2"):] if g2 else sname[len("br"):]
+                lead = int(base[len("_lead"):]) if base.startswith("_lead") else 1
                 flags = ak.FLAG_WITHOUT_REPLACEMENT if sname == "br_wor" else 0
                 t1 = time.perf_counter()
-                r = ix.query(q, k, h, delta, t, alphas[c], counts=False, dhat=False, lead=lead, flags=flags)
+                r = ix.query(q, k, h, delta, t, alphas[c], counts=False, dhat=False, lead=lead, flags=flags,
+                             growth=2 if g2 else 1)
                 rows.append(dict(w=w, trial=t, c=c, s=sname, recall=_recall(X, q[0], r["sets"][0], dks[wt], k),
                                  fraction=int(r["evals"][0]) / (n * m), rounds=int(r["rounds"][0]),
                                  draws=int(r["draws"][0]), wall_s=time.perf_counter() - t1))

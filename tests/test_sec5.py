@@ -99,14 +99,17 @@ def ak():
 @pytest.mark.gpu
 @pytest.mark.parametrize("w,trial,c,sched", [
     ("p10", 0, 1e-5, "a1"), ("p10", 0, 1e-4, "br"), ("p1000", 1, 1e-4, "br"),
-    ("images", 0, 1e-3, "a1"), ("images", 2, 1e-3, "br")])
+    ("images", 0, 1e-3, "a1"), ("images", 2, 1e-3, "br"), ("p10", 3, 1e-3, "br_g2"),
+    ("p100", 4, 1e-4, "br_g2")])
 def test_gpu_sec5_bit_exact(ak, w, trial, c, sched):
     X, q = synth.sec5_trial(w, trial)
     n, m, k, h = P["n"], P["m"], P["k"], P["h"]
     al = orc.alpha_experimental(n, P["delta"], m, c)
     ix = ak.Index(X)
     try:
-        got = ix.query(q, k, h, P["delta"], trial, al, counts=True, sums=True, schedule=sched)
+        g2 = sched == "br_g2"  # growth factor < 2 (reading R25)
+        got = ix.query(q, k, h, P["delta"], trial, al, counts=True, sums=True,
+                       schedule="br" if g2 else sched, growth=2 if g2 else 1)
     finally:
         ix.close()
     if sched == "a1":
@@ -117,6 +120,6 @@ def test_gpu_sec5_bit_exact(ak, w, trial, c, sched):
         assert np.array_equal(got["sums"][0], r["sums"])
         assert (got["evals"][0], got["draws"][0], got["rounds"][0]) == (r["evals"], r["draws"], r["iters"])
     else:
-        r = orc.query_br(X, q, k, h, trial, al, want_sums=True)
+        r = orc.query_br(X, q, k, h, trial, al, want_sums=True, growth=2 if g2 else 1)
         for key in ("sets", "dhat", "counts", "sums", "evals", "draws", "rounds"):
             assert np.array_equal(got[key], r[key]), key
