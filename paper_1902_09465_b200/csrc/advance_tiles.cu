@@ -492,9 +492,10 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Geom g) {
 #pragma unroll
             for (int k = 0; k < ADV_TP; ++k) sum = sq_diff4_wor(xa, qa, kk, g.wor_z, d, s + 4u * (b0 + k), sum);
           } else {
+            const PhiloxPair pc = philox_pair(gi, gq, g.rk0);
             uint4 w[ADV_TP];
 #pragma unroll
-            for (int k = 0; k < ADV_TP; ++k) w[k] = philox4x32_10_rk(make_uint4(b0 + k, gi, gq, lv), g.rk0, g.rk1);
+            for (int k = 0; k < ADV_TP; ++k) w[k] = philox_from_pair(b0 + k, lv, pc, g.rk0, g.rk1);
 #pragma unroll
             for (int k = 0; k < ADV_TP; ++k) sum = sq_diff4(xa, qa, w[k], d, sum);
           }
@@ -611,12 +612,17 @@ static cudaError_t launch_tiles_k(const Geom &g, int num_sms, cudaStream_t s) {
   if (e != cudaSuccess) return e;
   e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_advance_tiles<MODE, TILE_NT>, TILE_NT, smem);
   if (e != cudaSuccess) return e;
+  // bulk TMA row staging pays at one CTA per SM (C3: -3 % tile time), where nothing else
+  // hides the staging latency; with 2-3 CTAs per SM (C2, C4) 16-byte cp.async is faster
+  // (bulk copies: +7 % / +10 % tile time, measured)
+  Geom gt = g;
   if (MODE != 1 && per_sm <= 1 && env_tile_wide()) {
     int wide = 0;
-    if (launch_tiles_nt<MODE == 1 ? 0 : MODE, TILE_NT_WIDE>(g, num_sms, &wide, s) == cudaSuccess) return cudaSuccess;
+    if (launch_tiles_nt<MODE == 1 ? 0 : MODE, TILE_NT_WIDE>(gt, num_sms, &wide, s) == cudaSuccess) return cudaSuccess;
     cudaGetLastError();
   }
-  return launch_tiles_nt<MODE, TILE_NT>(g, num_sms, &per_sm, s);
+  gt.tile_tma = per_sm <= 1 ? g.tile_tma : 0;
+  return launch_tiles_nt<MODE, TILE_NT>(gt, num_sms, &per_sm, s);
 }
 
 cudaError_t launch_advance_tiles(const Geom &g, int num_sms, cudaStream_t s) {

@@ -305,10 +305,11 @@ TileShape tile_shape(int64_t pitch, int64_t n) {
     return TileShape{0, 0, 0, 0.f};
   // X in L2 (C2: 47 MB): a list draw costs one L2 sector, tiles must amortise their
   // staging over >= 4 sectors' worth of draws; X in HBM (C3-C5): a list draw is a
-  // random HBM sector (~1/15 the Philox rate), tiles win from ~1/4 of that
+  // random HBM sector (~1/15 the Philox rate): F = 1 measured best on C3 (-2 %) and
+  // equal on C4 (F = 0.25 / 1 / 4: 101.0 / 100.0 / 100.4 ms)
   const char *fe = getenv("AKNN_TILE_F");
   const bool x_in_l2 = (double)n * (double)pitch <= 100e6;
-  const double f = fe && fe[0] ? atof(fe) : (x_in_l2 ? 4.0 : 0.25);
+  const double f = fe && fe[0] ? atof(fe) : (x_in_l2 ? 4.0 : 1.0);
   t.row_draws = (float)(f * (double)pitch / 32.0);
   t.on = 1;
   return t;
@@ -796,7 +797,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   const size_t oXm = off; off = round_up(off + exact_mma_ws_bytes(qb, npad), 256);
   const TileShape tsh = tile_shape(ix->pitch, ix->n_local);
   const size_t oTw = off; off = round_up(off + tile_ws_bytes(qb, npad, tsh), 256);
-  const size_t oThr = off; off = round_up(off + sizeof(int32_t) * THR_STRIDE * (size_t)qb, 256);
+  const size_t oThr = off; off = round_up(off + sizeof(int32_t) * THR_STRIDE * (size_t)qb, 256);  // (max stride)
   const size_t oLm = off; off = round_up(off + level_ws_bytes(qb, n, npad, ix->pitch, o), 256);
   const size_t oLead = off; off = round_up(off + (o.lead > 1 ? szL : 0), 256);
   const int rowany_cols = (int)((npad + 1023) / 1024);
@@ -1061,7 +1062,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     const size_t oXm = off; off = round_up(off + exact_mma_ws_bytes(qb, npad), 256);
     const TileShape tsh = tile_shape(ix->pitch, ix->n_local);
     const size_t oTw = off; off = round_up(off + tile_ws_bytes(qb, npad, tsh), 256);
-    const size_t oThr = off; off = round_up(off + sizeof(int32_t) * THR_STRIDE * (size_t)qb, 256);
+    const size_t oThr = off; off = round_up(off + sizeof(int32_t) * THR_STRIDE * (size_t)qb, 256);  // (max stride)  // (max stride)
     const size_t oLm = off; off = round_up(off + level_ws_bytes(qb, ix->n_local, npad, ix->pitch, o), 256);
     const size_t oLead = off; off = round_up(off + (o.lead > 1 ? szL : 0), 256);
     const int rowany_cols = (int)((npad + 1023) / 1024);

@@ -28,9 +28,9 @@
 //   end             each stream leaves its candidates (unsorted) and their count;
 //                   k_exact_merge selects each query's k smallest of all its streams'
 //                   candidates (block radix select in shared memory) and sorts them.
-// Pilot: for n >= 4 * XF_PILOT the same two kernels first run over the first XF_PILOT
-// points; each query's k-th smallest key there bounds its k-th smallest key overall,
-// so the full pass appends only keys that can still reach the top k.
+// Pilot: for n >= 4 * 2048 the same two kernels first run over the first 2048 points
+// (8192 when n >= 65536); each query's k-th smallest key there bounds its k-th smallest
+// key overall, so the full pass appends only keys that can still reach the top k.
 #include <cuda.h>
 
 #include <algorithm>
@@ -49,7 +49,7 @@ constexpr int XF_BUF = XF_CAP + 32;     // + one 32-column chunk of slack
 constexpr int XF_E = XF_BUF / 32;       // keys per lane in a warp compaction
 constexpr int XF_MAX_K = 128;
 constexpr int XF_STREAMS = 2 * XF_BM;   // streams per CTA: (column half, row)
-constexpr int XF_PILOT = 2048;
+constexpr int XF_PILOT = 2048, XF_PILOT_BIG = 8192;  // pilot samples: n >= 4x / 8x them
 constexpr size_t XF_SMEM_MAX = 227 * 1024;
 constexpr size_t XF_HIST_BYTES = (size_t)XF_EPI_WARPS * 256 * 4;  // static: radix histograms
 constexpr size_t XF_FIXED = 1024 /*align*/ + 256 /*barriers*/;
@@ -359,21 +359,22 @@ __global__ void __launch_bounds__(XF_NT, 1)
 }
 
 // One CTA per query: the k smallest of the candidates of its 2 G streams.  The
-// streams' counts are scanned into offsets; the candidates (<= XM_SMEM_KEYS of them)
-// are copied into shared memory once and selected there by an 8-bit radix select from
-// the highest differing digit with warp-aggregated histogram increments (beyond that
-// the passes read them from global memory).  The k winners are ranked and written.
+// streams' counts are scanned into offsets; when they fit (cap_keys, sized by the host
+// from the expected count) the candidates are copied into shared memory once, warp by
+// stream; otherwise every pass re-reads them from the (L2-resident) stream buffers.
+// Selection: 8-bit radix select from the highest differing digit, warp-aggregated
+// histogram increments, the bin found by a warp scan.  The k winners are ranked.
 // idx == nullptr: the pilot -- write the k-th smallest key to bound[row0 + r].
-constexpr int XM_NT = 512;
-constexpr int XM_SMEM_KEYS = 20480;       // 160 KB of dynamic shared memory
+constexpr int XM_NT = 512, XM_NW = XM_NT / 32;
 constexpr int XM_MAX_STREAMS = 2 * 160;
+constexpr size_t XM_SMEM_MAX = 200 * 1024;
 
 __global__ void __launch_bounds__(XM_NT) k_exact_merge(XfGeom g, int row0, int32_t *idx, int32_t *dist2,
-                                                       unsigned long long *bound) {
+                                                       unsigned long long *bound, int cap_keys) {
   extern __shared__ unsigned long long skeys[];
   __shared__ uint32_t hist[256];
   __shared__ uint32_t soff[XM_MAX_STREAMS + 1];
-  __shared__ unsigned long long red_o[XM_NT / 32], red_a[XM_NT / 32];
+  __shared__ unsigned long long red_o[XM_NW], red_a[XM_NW];
   __shared__ int sh_bin, sh_before, sh_cb;
   __shared__ unsigned long long sh_kth;
   __shared__ unsigned long long win[XF_MAX_K];
@@ -384,38 +385,62 @@ __global__ void __launch_bounds__(XM_NT) k_exact_merge(XfGeom g, int row0, int32
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   auto stream_base = [&](int l) -> size_t {
     const int seg = l >> 1, half = l & 1;
-    return ((size_t)seg * g.mt + mb) * XF_STREAMS + half * XF_BM + lrow;
+    return (((size_t)seg * g.mt + mb) * XF_STREAMS + half * XF_BM + lrow);
   };
-  if (tid == 0) {
-    uint32_t a = 0;
-    for (int l = 0; l < nl; ++l) {
-      soff[l] = a;
-      a += g.pcnt[stream_base(l)];
+  if (wid == 0) {  // offsets of the streams' candidates: warp scan
+    uint32_t carry = 0;
+    for (int l0 = 0; l0 < nl; l0 += 32) {
+      const int l = l0 + lane;
+      const uint32_t c = l < nl ? g.pcnt[stream_base(l)] : 0u;
+      uint32_t inc = c;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+      }
+      if (l < nl) soff[l] = carry + inc - c;
+      carry += __shfl_sync(0xffffffffu, inc, 31);
     }
-    soff[nl] = a;
+    if (lane == 0) soff[nl] = carry;
   }
   __syncthreads();
   const int M = (int)soff[nl];
-  const bool in_smem = M <= XM_SMEM_KEYS;
-  auto gkey = [&](int c) -> unsigned long long {  // candidate c in global memory
-    int lo = 0, hi = nl;                          // the stream l with soff[l] <= c < soff[l+1]
-    while (hi - lo > 1) {
-      const int mid = (lo + hi) >> 1;
-      if (soff[mid] <= (uint32_t)c) lo = mid; else hi = mid;
-    }
-    return g.buf[stream_base(lo) * XF_BUF + (c - (int)soff[lo])];
-  };
+  const bool in_smem = M <= cap_keys;
   if (in_smem)
-    for (int c = tid; c < M; c += XM_NT) skeys[c] = gkey(c);
+    for (int l = wid; l < nl; l += XM_NW) {
+      const unsigned long long *src = g.buf + stream_base(l) * XF_BUF;
+      const int c = (int)(soff[l + 1] - soff[l]);
+      for (int j = lane; j < c; j += 32) skeys[soff[l] + j] = src[j];
+    }
   __syncthreads();
-  auto key_at = [&](int c) -> unsigned long long { return in_smem ? skeys[c] : gkey(c); };
+  // fn(key, valid) on every candidate, every lane of a warp in lockstep (full-warp match)
+  auto visit = [&](auto &&fn) {
+    if (in_smem) {
+      for (int c0 = 0; c0 < M; c0 += XM_NT) {
+        const int c = c0 + tid;
+        const bool v = c < M;
+        fn(v ? skeys[c] : XF_NONE, v);
+      }
+    } else {
+      for (int l = wid; l < nl; l += XM_NW) {
+        const unsigned long long *src = g.buf + stream_base(l) * XF_BUF;
+        const int c = (int)(soff[l + 1] - soff[l]);
+        for (int j0 = 0; j0 < c; j0 += 32) {
+          const int j = j0 + lane;
+          const bool v = j < c;
+          fn(v ? src[j] : XF_NONE, v);
+        }
+      }
+    }
+  };
   // common high bits of all candidates
   unsigned long long orr = 0, andk = XF_NONE;
-  for (int c = tid; c < M; c += XM_NT) {
-    const unsigned long long v = key_at(c);
-    orr |= v;
-    andk &= v;
-  }
+  visit([&](unsigned long long v, bool ok) {
+    if (ok) {
+      orr |= v;
+      andk &= v;
+    }
+  });
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
     orr |= shfl64(orr, lane ^ o);
@@ -426,18 +451,12 @@ __global__ void __launch_bounds__(XM_NT) k_exact_merge(XfGeom g, int row0, int32
     red_a[wid] = andk;
   }
   __syncthreads();
-  if (tid == 0) {
-    unsigned long long o2 = 0, a2 = XF_NONE;
-    for (int w = 0; w < XM_NT / 32; ++w) {
-      o2 |= red_o[w];
-      a2 &= red_a[w];
-    }
-    red_o[0] = o2;
-    red_a[0] = a2;
+  orr = 0;
+  andk = XF_NONE;
+  for (int w = 0; w < XM_NW; ++w) {
+    orr |= red_o[w];
+    andk &= red_a[w];
   }
-  __syncthreads();
-  orr = red_o[0];
-  andk = red_a[0];
   int shift = radix_top_shift(andk, orr);
   unsigned long long pmask = shift >= 0 ? ~((1ull << (shift + 8)) - 1ull) : XF_NONE;
   unsigned long long prefix = andk & pmask, kth = prefix;
@@ -445,28 +464,40 @@ __global__ void __launch_bounds__(XM_NT) k_exact_merge(XfGeom g, int row0, int32
   for (; shift >= 0; shift -= 8) {
     for (int i = tid; i < 256; i += XM_NT) hist[i] = 0;
     __syncthreads();
-    for (int c0 = 0; c0 < M; c0 += XM_NT) {  // every thread runs every iteration: full-warp match
-      const int c = c0 + tid;
-      const unsigned long long v = c < M ? key_at(c) : XF_NONE;
-      const bool ok = c < M && (v & pmask) == prefix;
+    visit([&](unsigned long long v, bool ok) {
+      ok = ok && (v & pmask) == prefix;
       const uint32_t bin = ok ? (uint32_t)(v >> shift) & 255u : 256u;
       const uint32_t m = __match_any_sync(0xffffffffu, bin);
       if (ok && lane == __ffs(m) - 1) atomicAdd(&hist[bin], (uint32_t)__popc(m));
-    }
+    });
     __syncthreads();
-    if (tid == 0) {
-      uint32_t acc = 0;
-      int bin = 255;
-      for (int i = 0; i < 256; ++i) {
-        if (acc + hist[i] >= (uint32_t)want) {
-          bin = i;
-          break;
-        }
-        acc += hist[i];
+    if (wid == 0) {  // the bin holding the want-th key: warp scan over 8 bins per lane
+      uint32_t h[8], loc = 0;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        h[i] = hist[lane * 8 + i];
+        loc += h[i];
       }
-      sh_bin = bin;
-      sh_before = (int)acc;
-      sh_cb = (int)hist[bin];
+      uint32_t inc = loc;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t t = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += t;
+      }
+      const uint32_t exc = inc - loc;
+      if (exc < (uint32_t)want && (uint32_t)want <= inc) {
+        uint32_t acc = exc;
+        int bin = -1;
+        for (int i = 0; i < 8 && bin < 0; ++i) {
+          if (acc + h[i] >= (uint32_t)want) {
+            bin = lane * 8 + i;
+            sh_bin = bin;
+            sh_before = (int)acc;
+            sh_cb = (int)h[i];
+          }
+          acc += h[i];
+        }
+      }
     }
     __syncthreads();
     prefix |= (unsigned long long)sh_bin << shift;
@@ -474,10 +505,9 @@ __global__ void __launch_bounds__(XM_NT) k_exact_merge(XfGeom g, int row0, int32
     want -= sh_before;
     kth = prefix;
     if (sh_cb == 1) {  // unique: locate it
-      for (int c = tid; c < M; c += XM_NT) {
-        const unsigned long long v = key_at(c);
-        if ((v & pmask) == prefix) sh_kth = v;
-      }
+      visit([&](unsigned long long v, bool ok) {
+        if (ok && (v & pmask) == prefix) sh_kth = v;
+      });
       __syncthreads();
       kth = sh_kth;
       break;
@@ -490,13 +520,12 @@ __global__ void __launch_bounds__(XM_NT) k_exact_merge(XfGeom g, int row0, int32
   }
   if (tid == 0) wcount = 0;
   __syncthreads();
-  for (int c = tid; c < M; c += XM_NT) {
-    const unsigned long long v = key_at(c);
-    if (v <= kth) {
+  visit([&](unsigned long long v, bool ok) {
+    if (ok && v <= kth) {
       const unsigned p = atomicAdd(&wcount, 1u);
       if (p < XF_MAX_K) win[p] = v;
     }
-  }
+  });
   __syncthreads();
   const int m = min((int)wcount, k);
   for (int j = tid; j < m; j += XM_NT) {
@@ -536,21 +565,28 @@ cudaError_t launch_exact_fused(const ExactGeom &e, const int32_t *nq, const int3
     if (err == cudaSuccess)
       err = cudaFuncSetAttribute(k_exact_fused<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn_max);
     if (err == cudaSuccess)
-      err = cudaFuncSetAttribute(k_exact_merge, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 (int)(XM_SMEM_KEYS * sizeof(unsigned long long)));
+      err = cudaFuncSetAttribute(k_exact_merge, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)XM_SMEM_MAX);
     if (err != cudaSuccess) return err;
     attr = true;
   }
-  const bool pilot = e.n >= 4 * XF_PILOT && e.k <= XF_PILOT;
+  // pilot sample: the larger one when n allows (the full pass then appends ~ k n / S
+  // candidates per query instead of ~ k n / 2048)
+  const int S = e.n >= 8 * XF_PILOT_BIG ? XF_PILOT_BIG : XF_PILOT;
+  const bool pilot = e.n >= 4 * S && e.k <= S;
   CUtensorMap tx, txp;
   cudaError_t err = make_map(&tx, e.X, e.n, e.d, e.pitch, XF_BN);
-  if (err == cudaSuccess && pilot) err = make_map(&txp, e.X, XF_PILOT, e.d, e.pitch, XF_BN);
+  if (err == cudaSuccess && pilot) err = make_map(&txp, e.X, S, e.d, e.pitch, XF_BN);
   if (err != cudaSuccess) return err;
   const int mt_all = (e.q + XF_BM - 1) / XF_BM;
   unsigned long long *buf = static_cast<unsigned long long *>(ws);
   uint32_t *pcnt = reinterpret_cast<uint32_t *>(buf + (size_t)num_sms * XF_STREAMS * XF_BUF);
   unsigned long long *bnd = reinterpret_cast<unsigned long long *>(pcnt + (size_t)num_sms * XF_STREAMS);
-  const size_t msmem = XM_SMEM_KEYS * sizeof(unsigned long long);
+  // merge shared memory: 4x the expected candidates per query (capped); a query with
+  // more takes the re-reading path
+  auto merge_smem = [&](size_t expect) {
+    size_t b = std::max<size_t>(16 * 1024, 4 * expect * sizeof(unsigned long long));
+    return std::min(b, XM_SMEM_MAX);
+  };
   for (int mb0 = 0; mb0 < mt_all; mb0 += num_sms) {
     const int mt = std::min(num_sms, mt_all - mb0);
     const int row0 = mb0 * XF_BM, qn = std::min(e.q - row0, mt * XF_BM);
@@ -575,19 +611,23 @@ cudaError_t launch_exact_fused(const ExactGeom &e, const int32_t *nq, const int3
         k_exact_fused<false><<<mt * g.G, XF_NT, smem, s>>>(tq, txm, g);
     };
     if (pilot) {  // the same kernels over the sample, then its k-th key per query
-      g.n = XF_PILOT;
-      g.nt = XF_PILOT / XF_BN;
+      g.n = S;
+      g.nt = S / XF_BN;
       g.G = std::max(1, std::min(g.nt, num_sms / mt));
       g.bound = nullptr;
       run(txp);
-      k_exact_merge<<<qn, XM_NT, msmem, s>>>(g, 0, nullptr, nullptr, bnd);
+      // every sample key is a candidate (no threshold yet): exactly S of them
+      const size_t ms = std::min(XM_SMEM_MAX, std::max<size_t>(16 * 1024, (size_t)S * sizeof(unsigned long long)));
+      k_exact_merge<<<qn, XM_NT, ms, s>>>(g, 0, nullptr, nullptr, bnd, (int)(ms / 8));
     }
     g.n = e.n;
     g.nt = (e.n + XF_BN - 1) / XF_BN;
     g.G = std::max(1, std::min(g.nt, num_sms / mt));
     g.bound = pilot ? bnd : nullptr;
     run(tx);
-    k_exact_merge<<<qn, XM_NT, msmem, s>>>(g, row0, e.idx, e.dist2, nullptr);
+    const size_t ms = merge_smem(pilot ? (size_t)e.k * (size_t)e.n / (size_t)S + (size_t)e.k
+                                       : (size_t)2 * g.G * XF_BUF);
+    k_exact_merge<<<qn, XM_NT, ms, s>>>(g, row0, e.idx, e.dist2, nullptr, (int)(ms / 8));
     err = cudaGetLastError();
     if (err != cudaSuccess) return err;
   }

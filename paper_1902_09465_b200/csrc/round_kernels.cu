@@ -155,7 +155,8 @@ __global__ void __launch_bounds__(128) k_thresholds(Geom g) {
   if (qi >= g.q) return;
   const QState &st = g.qs[qi];
   if (st.done) return;
-  int32_t *t = g.thr + (size_t)qi * THR_STRIDE;
+  const int nlev = g.cmax + 1, hdr = thr_hdr(nlev);
+  int32_t *t = g.thr + (size_t)qi * thr_stride(nlev);
   const unsigned long long kmask = (1ull << g.kbits) - 1ull;
   bool mbit = false, eqk = false, eqkh = false;
   if (c < MAX_LEVELS && c <= g.cmax) {
@@ -190,11 +191,11 @@ __global__ void __launch_bounds__(128) k_thresholds(Geom g) {
   }
   const unsigned m = __ballot_sync(FULL, mbit), mk = __ballot_sync(FULL, eqk), mkh = __ballot_sync(FULL, eqkh);
   if (c == 0) {
-    t[THR_LEVEL_INTS + 0] = (int32_t)m;
-    t[THR_LEVEL_INTS + 1] = (int32_t)mk;
-    t[THR_LEVEL_INTS + 2] = (int32_t)mkh;
-    t[THR_LEVEL_INTS + 3] = (int32_t)(uint32_t)(st.thr_k & kmask);
-    t[THR_LEVEL_INTS + 4] = (int32_t)(uint32_t)(st.thr_kh & kmask);
+    t[hdr + 0] = (int32_t)m;
+    t[hdr + 1] = (int32_t)mk;
+    t[hdr + 2] = (int32_t)mkh;
+    t[hdr + 3] = (int32_t)(uint32_t)(st.thr_k & kmask);
+    t[hdr + 4] = (int32_t)(uint32_t)(st.thr_kh & kmask);
   }
 }
 
@@ -209,9 +210,10 @@ __device__ __forceinline__ uint32_t filter_arms(const Geom &g, const int32_t *th
                                                 uint32_t *draws, uint32_t *leadw) {
   uint32_t actw = 0, dr = 0, lw = 0;
   // thr: the row's table staged in shared memory by k_filter
-  const int4 hdr = *reinterpret_cast<const int4 *>(thr + THR_LEVEL_INTS);
+  const int ho = thr_hdr(g.cmax + 1);
+  const int4 hdr = *reinterpret_cast<const int4 *>(thr + ho);
   const uint32_t mmask = (uint32_t)hdr.x, eqk = (uint32_t)hdr.y, eqkh = (uint32_t)hdr.z;
-  const uint32_t idk = (uint32_t)hdr.w, idkh = (uint32_t)thr[THR_LEVEL_INTS + 4];
+  const uint32_t idk = (uint32_t)hdr.w, idkh = (uint32_t)thr[ho + 4];
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
     const int i = i0 + e;
@@ -279,7 +281,12 @@ struct SlotRun {
 // 2: a lead pass (reading R24).  Separate instantiations keep MODE 0's registers.
 template <int MODE>
 __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
-  extern __shared__ uint32_t tcnt[];  // [FIL_ROWS / R][FIL_NT * 4 / P] (tiles on)
+  // dynamic: [FIL_ROWS][thr stride] blocker thresholds (modes 0, 1), then the tile counts
+  // [FIL_ROWS / R][FIL_NT * 4 / P] (tiles on)
+  extern __shared__ __align__(16) uint32_t fsm[];
+  const int tstride = thr_stride(g.cmax + 1);
+  int32_t *sthr = reinterpret_cast<int32_t *>(fsm);
+  uint32_t *tcnt = fsm + (MODE == 2 ? 0 : FIL_ROWS * tstride);
   __shared__ unsigned scnt[NSLOT];
   __shared__ unsigned lvc[(FIL_NT * 4 / 128) * MAX_LEVELS];
   const int q0 = blockIdx.y * FIL_ROWS;
@@ -294,10 +301,9 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
   __shared__ uint32_t srow_any;  // bit r: row r has an action in this chunk
   if (threadIdx.x == 0) srow_any = 0;
   // the CTA's rows of blocker thresholds (reading R20), staged once
-  __shared__ __align__(16) int32_t sthr[MODE == 2 ? 4 : FIL_ROWS * THR_STRIDE];
   if (MODE != 2)
-    for (int t = threadIdx.x; t < rows * (THR_STRIDE / 4); t += FIL_NT)
-      reinterpret_cast<int4 *>(sthr)[t] = __ldg(reinterpret_cast<const int4 *>(g.thr + (size_t)q0 * THR_STRIDE) + t);
+    for (int t = threadIdx.x; t < rows * (tstride / 4); t += FIL_NT)
+      reinterpret_cast<int4 *>(sthr)[t] = __ldg(reinterpret_cast<const int4 *>(g.thr + (size_t)q0 * tstride) + t);
   __syncthreads();
   const bool arms = i0 < g.n;
   // two rows of loads in flight ahead of the row being decided
@@ -327,7 +333,7 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
     if (MODE == 2) {
       if (arms) actw = lead_arms(g, ca, *reinterpret_cast<const uint32_t *>(g.leadb + (size_t)qi * g.npad + i0), i0, &dr);
     } else {
-      if (arms) actw = filter_arms(g, sthr + r * THR_STRIDE, ca, i0, &dr, &lw);
+      if (arms) actw = filter_arms(g, sthr + r * tstride, ca, i0, &dr, &lw);
       if (MODE == 1 && i0 < g.npad) *reinterpret_cast<uint32_t *>(g.leadb + (size_t)qi * g.npad + i0) = lw;
     }
     if (i0 < g.npad) *reinterpret_cast<uint32_t *>(g.act + (size_t)qi * g.npad + i0) = actw;
@@ -616,9 +622,10 @@ __device__ __forceinline__ uint32_t draw4_pair_wor(const Geom &g, const uint8_t 
 __device__ __forceinline__ uint32_t draw4_pair(const Geom &g, const uint8_t *__restrict__ xr,
                                                const uint8_t *__restrict__ qr, uint32_t gi, uint32_t gq,
                                                uint32_t lv, uint32_t blk0) {
+  const PhiloxPair pc = philox_pair(gi, gq, g.rk0);
   uint4 w[ADV_P];
 #pragma unroll
-  for (int k = 0; k < ADV_P; ++k) w[k] = philox4x32_10_rk(make_uint4(blk0 + k, gi, gq, lv), g.rk0, g.rk1);
+  for (int k = 0; k < ADV_P; ++k) w[k] = philox_from_pair(blk0 + k, lv, pc, g.rk0, g.rk1);
   uint32_t acc = 0;
 #pragma unroll
   for (int k = 0; k < ADV_P; ++k) {
@@ -808,9 +815,10 @@ __global__ void __launch_bounds__(ADV_NT) k_advance(Geom g) {
 // of one random 32-byte sector per draw), then gathers its draws from there.
 __device__ __forceinline__ uint32_t draw4_pair_srow(const Geom &g, const uint8_t *sx, const uint8_t *__restrict__ qr,
                                                     uint32_t gi, uint32_t gq, uint32_t lv, uint32_t blk0) {
+  const PhiloxPair pc = philox_pair(gi, gq, g.rk0);
   uint4 w[ADV_P];
 #pragma unroll
-  for (int k = 0; k < ADV_P; ++k) w[k] = philox4x32_10_rk(make_uint4(blk0 + k, gi, gq, lv), g.rk0, g.rk1);
+  for (int k = 0; k < ADV_P; ++k) w[k] = philox_from_pair(blk0 + k, lv, pc, g.rk0, g.rk1);
   uint32_t acc = 0;
 #pragma unroll
   for (int k = 0; k < ADV_P; ++k) {
@@ -1037,7 +1045,8 @@ cudaError_t launch_select(const Geom &g, int nbits, cudaStream_t s) {
 }
 
 cudaError_t launch_filter(const Geom &g, cudaStream_t s) {
-  const size_t smem = g.tile_on ? sizeof(uint32_t) * (size_t)(FIL_ROWS >> g.tile_lr) * ((FIL_NT * 4) >> g.tile_lp) : 0;
+  const size_t smem = (g.lead_pass ? 0 : sizeof(int32_t) * (size_t)FIL_ROWS * thr_stride(g.cmax + 1)) +
+                      (g.tile_on ? sizeof(uint32_t) * (size_t)(FIL_ROWS >> g.tile_lr) * ((FIL_NT * 4) >> g.tile_lp) : 0);
   const dim3 grid(cdiv(g.npad, FIL_NT * 4), cdiv(g.q, FIL_ROWS));
   auto go = [&](auto kern) {
     if (smem > 48 * 1024) {
