@@ -34,6 +34,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.cuh"
 #include "launch.h"
@@ -67,6 +68,9 @@ struct XfGeom {
   unsigned long long *buf;   // [grid][XF_STREAMS][XF_BUF] candidate keys
   uint32_t *pcnt;            // [grid][XF_STREAMS] candidates per stream
   const unsigned long long *bound;  // [q] initial per-query threshold (the pilot's k-th key), or null
+  unsigned long long *qbound;       // [q] shared per-query bound: the smallest k-th key any stream
+                                    // of the query has compacted to (atomicMin), reset to ~0
+  int first_cap;                    // a stream's first compaction when it holds more keys
 };
 
 __device__ __forceinline__ unsigned long long shfl64(unsigned long long v, int src) {
@@ -301,16 +305,21 @@ __global__ void __launch_bounds__(XF_NT, 1)
     // an invalid row appends nothing; with a pilot bound (the k-th smallest key of a
     // point sample, itself >= the k-th smallest key overall) only keys <= it are kept
     unsigned long long tau = !vrow ? 0ull : (g.bound ? g.bound[row] + 1ull : XF_NONE);
-    int cnt = 0;
+    int cnt = 0, lim = g.first_cap + 32;  // the first compaction comes early (a tight tau soon)
     for (int t = 0; t < ntl; ++t) {
       const uint32_t a = (uint32_t)t & 1u;
+      // every stream's k-th key bounds the query's k-th key: adopt the query's best so far
+      if (vrow && t > 0) {
+        const unsigned long long qb = __ldcg(g.qbound + row);
+        tau = qb < tau ? qb + 1ull : tau;
+      }
       mbar_wait(tfull + a, (uint32_t)(t >> 1) & 1u);
       asm volatile("tcgen05.fence::after_thread_sync;");
       const int cbase = (t_begin + t) * XF_BN + half * (XF_BN / 2);
 #pragma unroll 1
       for (int c0 = 0; c0 < XF_BN / 2; c0 += 32) {
         // room for this chunk: compact the streams of this warp whose buffer is full
-        uint32_t need = __ballot_sync(0xffffffffu, cnt + 32 > XF_BUF);
+        uint32_t need = __ballot_sync(0xffffffffu, cnt + 32 > lim);
         while (need) {
           const int L = __ffs(need) - 1;
           need &= need - 1u;
@@ -319,8 +328,10 @@ __global__ void __launch_bounds__(XF_NT, 1)
           const int cl = __shfl_sync(0xffffffffu, cnt, L);
           const unsigned long long th = warp_compact(bl, cl, g.k, hist, lane);
           if (lane == L) {
-            tau = th;
+            tau = th;  // all kept keys are <= th; keys below it may still enter
             cnt = g.k;
+            lim = XF_BUF;
+            atomicMin(g.qbound + row, th);
           }
         }
         uint32_t v[32];
@@ -543,7 +554,7 @@ size_t exact_fused_ws_bytes(int num_sms, int k) {
   (void)k;
   return (size_t)num_sms * XF_STREAMS * XF_BUF * sizeof(unsigned long long) +  // candidates
          (size_t)num_sms * XF_STREAMS * sizeof(uint32_t) +                     // their counts
-         (size_t)num_sms * XF_BM * sizeof(unsigned long long);                  // pilot bounds
+         2 * (size_t)num_sms * XF_BM * sizeof(unsigned long long);              // pilot + shared bounds
 }
 
 // Queries in chunks of at most num_sms m-blocks; ws >= exact_fused_ws_bytes(num_sms, k).
@@ -572,7 +583,11 @@ cudaError_t launch_exact_fused(const ExactGeom &e, const int32_t *nq, const int3
   // pilot sample: the larger one when n allows (the full pass then appends ~ k n / S
   // candidates per query instead of ~ k n / 2048)
   const int S = e.n >= 8 * XF_PILOT_BIG ? XF_PILOT_BIG : XF_PILOT;
-  const bool pilot = e.n >= 4 * S && e.k <= S;
+  static const int pilot_env = [] {  // AKNN_EXACT_PILOT=0 / 1 forces it off / on (A/B)
+    const char *v = getenv("AKNN_EXACT_PILOT");
+    return v && v[0] ? atoi(v) : -1;
+  }();
+  const bool pilot = (pilot_env < 0 ? e.n >= 4 * S : pilot_env == 1 && e.n >= 2 * S) && e.k <= S;
   CUtensorMap tx, txp;
   cudaError_t err = make_map(&tx, e.X, e.n, e.d, e.pitch, XF_BN);
   if (err == cudaSuccess && pilot) err = make_map(&txp, e.X, S, e.d, e.pitch, XF_BN);
@@ -581,6 +596,7 @@ cudaError_t launch_exact_fused(const ExactGeom &e, const int32_t *nq, const int3
   unsigned long long *buf = static_cast<unsigned long long *>(ws);
   uint32_t *pcnt = reinterpret_cast<uint32_t *>(buf + (size_t)num_sms * XF_STREAMS * XF_BUF);
   unsigned long long *bnd = reinterpret_cast<unsigned long long *>(pcnt + (size_t)num_sms * XF_STREAMS);
+  unsigned long long *qbnd = bnd + (size_t)num_sms * XF_BM;
   // merge shared memory: 4x the expected candidates per query (capped); a query with
   // more takes the re-reading path
   auto merge_smem = [&](size_t expect) {
@@ -604,6 +620,8 @@ cudaError_t launch_exact_fused(const ExactGeom &e, const int32_t *nq, const int3
     g.nx = nx;
     g.buf = buf;
     g.pcnt = pcnt;
+    g.qbound = qbnd;
+    g.first_cap = std::max(128, 2 * e.k);
     auto run = [&](const CUtensorMap &txm) {
       if (qres)
         k_exact_fused<true><<<mt * g.G, XF_NT, smem, s>>>(tq, txm, g);
@@ -615,6 +633,8 @@ cudaError_t launch_exact_fused(const ExactGeom &e, const int32_t *nq, const int3
       g.nt = S / XF_BN;
       g.G = std::max(1, std::min(g.nt, num_sms / mt));
       g.bound = nullptr;
+      err = cudaMemsetAsync(qbnd, 0xFF, sizeof(unsigned long long) * (size_t)qn, s);
+      if (err != cudaSuccess) return err;
       run(txp);
       // every sample key is a candidate (no threshold yet): exactly S of them
       const size_t ms = std::min(XM_SMEM_MAX, std::max<size_t>(16 * 1024, (size_t)S * sizeof(unsigned long long)));
@@ -624,6 +644,8 @@ cudaError_t launch_exact_fused(const ExactGeom &e, const int32_t *nq, const int3
     g.nt = (e.n + XF_BN - 1) / XF_BN;
     g.G = std::max(1, std::min(g.nt, num_sms / mt));
     g.bound = pilot ? bnd : nullptr;
+    err = cudaMemsetAsync(qbnd, 0xFF, sizeof(unsigned long long) * (size_t)qn, s);
+    if (err != cudaSuccess) return err;
     run(tx);
     const size_t ms = merge_smem(pilot ? (size_t)e.k * (size_t)e.n / (size_t)S + (size_t)e.k
                                        : (size_t)2 * g.G * XF_BUF);
