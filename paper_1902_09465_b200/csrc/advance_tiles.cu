@@ -528,6 +528,270 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Geom g) {
   if (threadIdx.x == 0 && s_draws) atomicAdd(&g.ctl->tile_draws, s_draws);
 }
 
+// ---------------------------------------------------------------------------
+// Grouped tiles (one CTA per SM, rows wider than 8 KB: C3).  The CTA walks whole point
+// columns: it stages the column's P point rows ONCE and its NG thread groups then work
+// on different query tiles of that column at the same time -- group j takes query
+// tiles j, j + NG, ... -- each with its own R query-row slots, its own named barrier
+// and mbarrier.  A tile's fixed latency (its action / S / level round trip, the copy
+// of its query rows, the per-level barriers) is hidden by the other groups, as NG
+// CTAs per SM would hide it, while the point rows stay shared (NG CTAs would need NG
+// copies: the shared memory holds NG R + P slots instead of NG (R + P)).  Per-query
+// draws with replacement (MODE 0) only; same arithmetic and result as k_advance_tiles.
+template <int NG>
+__global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
+  constexpr int GT = TILE_NT_WIDE / NG;  // threads per group (whole warps)
+  static_assert(GT % 32 == 0, "groups of whole warps");
+  extern __shared__ __align__(16) unsigned char tsm[];
+  __shared__ unsigned lcnt[NG][MAX_LEVELS], loff[NG][MAX_LEVELS + 1], lfill[NG][MAX_LEVELS];
+  __shared__ __align__(8) uint64_t qbar[NG], pbar;
+  __shared__ unsigned long long s_blocks, s_draws;
+  const int R = 1 << g.tile_lr, P = 1 << g.tile_lp, RP = R * P;
+  const int pitch = (int)g.pitch;
+  const int sl = g.tile_slot_l;
+  const uint32_t slot = 1u << sl;
+  const int tid = threadIdx.x, grp = tid / GT, gtid = tid - grp * GT;
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(tsm);
+  // per group: acc [RP] int32 | lst [RP] u16 | sact [RP] u8 (7 RP bytes, 16-aligned)
+  const uint32_t gsz = ((uint32_t)RP * 7u + 15u) & ~15u;
+  int32_t *acc = reinterpret_cast<int32_t *>(tsm + (size_t)grp * gsz);
+  uint16_t *lst = reinterpret_cast<uint16_t *>(acc + RP);
+  uint8_t *sact = reinterpret_cast<uint8_t *>(lst + RP);
+  const uint32_t rows_s = (base + (uint32_t)NG * gsz + slot - 1) & ~(slot - 1);
+  {
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    if (rows_s + ((uint32_t)(NG * R + P) << sl) > base + dyn) __trap();  // host sizing broken: fail loudly
+  }
+  const uint32_t qs = rows_s + ((uint32_t)(grp * R) << sl);  // this group's query rows
+  const uint32_t xs = rows_s + ((uint32_t)(NG * R) << sl);   // the column's point rows
+  const uint32_t qbar_s = (uint32_t)__cvta_generic_to_shared(&qbar[grp]);
+  const uint32_t pbar_s = (uint32_t)__cvta_generic_to_shared(&pbar);
+  const uint32_t d = (uint32_t)g.d;
+  const int rows = (g.q + R - 1) >> g.tile_lr;
+  const int cols = (g.n + P - 1) >> g.tile_lp;
+  const float dthr = g.tile_min_draws;
+  if (tid == 0) {
+    s_blocks = s_draws = 0;
+    for (int j = 0; j < NG; ++j) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
+                                     (uint32_t)__cvta_generic_to_shared(&qbar[j])));
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(pbar_s));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  uint32_t qphase = 0, pphase = 0;
+  auto gsync = [&] { asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(GT) : "memory"); };
+  auto wait_bar = [](uint32_t bar, uint32_t ph) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "GW_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra GW_%=;\n\t}" ::"r"(bar),
+        "r"(ph)
+        : "memory");
+  };
+  const int c0 = (int)((long long)blockIdx.x * cols / gridDim.x), c1 = (int)((long long)(blockIdx.x + 1) * cols / gridDim.x);
+  for (int tp = c0; tp < c1; ++tp) {
+    // any dense tile in this column?  (all groups are done with the previous column)
+    bool mine = false;
+    for (int tr = tid; tr < rows; tr += TILE_NT_WIDE)
+      mine |= (float)g.tilework[(size_t)tr * g.tile_cols + tp] >= dthr;
+    if (!__syncthreads_or(mine)) continue;
+    const int p0 = tp << g.tile_lp;
+    if (tid == 0) {  // the column's point rows: bulk TMA copies
+      uint32_t bytes = 0;
+      for (int row = 0; row < P; ++row) bytes += p0 + row < g.n ? (uint32_t)pitch : 0u;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(pbar_s), "r"(bytes) : "memory");
+      for (int row = 0; row < P; ++row)
+        if (p0 + row < g.n)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  xs + ((uint32_t)row << sl)),
+              "l"(g.X + (size_t)(p0 + row) * pitch), "r"((uint32_t)pitch), "r"(pbar_s)
+              : "memory");
+    }
+    bool have_x = false;
+    for (int tr = grp; tr < rows; tr += NG) {
+      if ((float)g.tilework[(size_t)tr * g.tile_cols + tp] < dthr) continue;  // uniform in the group
+      const int r0 = tr << g.tile_lr;
+      gsync();  // the group's previous tile is done with its slots and arrays
+      if (gtid < MAX_LEVELS) lcnt[grp][gtid] = 0;
+      if (gtid == 0) {  // the tile's query rows into the group's slots
+        uint32_t bytes = 0;
+        for (int row = 0; row < R; ++row) bytes += r0 + row < g.q ? (uint32_t)pitch : 0u;
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(qbar_s), "r"(bytes) : "memory");
+        for (int row = 0; row < R; ++row)
+          if (r0 + row < g.q)
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    qs + ((uint32_t)row << sl)),
+                "l"(g.Q + (size_t)(r0 + row) * pitch), "r"((uint32_t)pitch), "r"(qbar_s)
+                : "memory");
+      }
+      // thread -> 4 consecutive arms of one query row (RP <= 4 GT): done flag, actions,
+      // S and levels in one round trip
+      const int e4 = gtid * 4;
+      const bool in = e4 < RP;
+      const int rr = in ? e4 >> g.tile_lp : 0, pp = e4 & (P - 1);
+      const bool live = in && r0 + rr < g.q && p0 + pp < g.n;
+      const size_t o4 = (size_t)(r0 + rr) * g.npad + p0 + pp;
+      int4 S4 = make_int4(0, 0, 0, 0);
+      uint32_t A4 = 0, L4 = 0;
+      int dn = 1;
+      if (live) {
+        dn = g.qs[r0 + rr].done;
+        A4 = *reinterpret_cast<const uint32_t *>(g.act + o4);
+        S4 = *reinterpret_cast<const int4 *>(g.S + o4);
+        L4 = *reinterpret_cast<const uint32_t *>(g.lvl + o4);
+      }
+      gsync();  // lcnt cleared
+      uint32_t act4 = 0;  // sampled actions only (exact fallbacks: tensor-core pass)
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        uint8_t a = (uint8_t)(A4 >> (8 * k));
+        if (dn || a > MAX_LEVELS || p0 + pp + k >= g.n) a = 0;
+        act4 |= (uint32_t)a << (8 * k);
+        hist_add(lcnt[grp], a ? a - 1u : NONE);
+      }
+      if (in) *reinterpret_cast<uint32_t *>(sact + e4) = act4;
+      gsync();  // lcnt
+      if (gtid < 32) {
+        const unsigned v = gtid < MAX_LEVELS ? lcnt[grp][gtid] : 0u;
+        unsigned x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+          const unsigned y = __shfl_up_sync(FULL, x, o);
+          if (gtid >= o) x += y;
+        }
+        if (gtid < MAX_LEVELS) {
+          loff[grp][gtid] = x - v;
+          lfill[grp][gtid] = x - v;
+        }
+        if (gtid == MAX_LEVELS - 1) loff[grp][MAX_LEVELS] = x;
+      }
+      gsync();
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint8_t a = (uint8_t)(act4 >> (8 * k));
+        const unsigned key = a ? a - 1u : NONE;
+        const unsigned m = __match_any_sync(FULL, key);
+        const int leader = __ffs(m) - 1;
+        unsigned b0 = 0;
+        if (a && lane_id() == leader) b0 = atomicAdd(&lfill[grp][key], (unsigned)__popc(m));
+        b0 = __shfl_sync(FULL, b0, leader);
+        if (a) lst[b0 + __popc(m & ((1u << lane_id()) - 1u))] = (uint16_t)(e4 + k);
+      }
+      wait_bar(qbar_s, qphase);  // the query rows
+      qphase ^= 1u;
+      if (!have_x) {  // the column's point rows (once per column and group)
+        wait_bar(pbar_s, pphase);
+        have_x = true;
+      }
+      gsync();
+      unsigned lmask = 0;
+      for (int c = 0; c < MAX_LEVELS; ++c) lmask |= (lcnt[grp][c] != 0u) << c;
+      if (gtid == 0) {
+        unsigned long long dr = 0, b = 0;
+        for (int c = 0; c < MAX_LEVELS; ++c) {
+          dr += (unsigned long long)lcnt[grp][c] << c;
+          b += (unsigned long long)lcnt[grp][c] << (c < 2 ? 0 : c - 2);
+        }
+        atomicAdd(&s_draws, dr);
+        atomicAdd(&s_blocks, b);
+      }
+      for (; lmask; lmask &= lmask - 1) {
+        const int c = __ffs(lmask) - 1;
+        const unsigned m = lcnt[grp][c];
+        const int lb = c < 2 ? 0 : c - 2;
+        const unsigned s = 1u << c, nb = 1u << lb;
+        const uint16_t *L = lst + loff[grp][c];
+        const uint32_t lv = (uint32_t)(c + 1);
+        if (nb <= (unsigned)ADV_TP) {
+          const unsigned ppt = ADV_TP / nb;
+          for (unsigned l0 = gtid; l0 < m; l0 += GT * ppt) {
+            uint4 w[ADV_TP];
+            int pr[ADV_TP];
+#pragma unroll
+            for (int k = 0; k < ADV_TP; ++k) {
+              const unsigned li = l0 + (k / nb) * GT;
+              const bool ok = (unsigned)k / nb < ppt && li < m;
+              pr[k] = ok ? (int)L[li] : -1;
+              const int e = ok ? pr[k] : 0;
+              const uint32_t gi = (uint32_t)(p0 + (e & (P - 1))) + g.id_offset;
+              const uint32_t gq = rng_qi(g, (uint32_t)(r0 + (e >> g.tile_lp)));
+              w[k] = philox4x32_10_rk(make_uint4((uint32_t)k & (nb - 1), gi, gq, lv), g.rk0, g.rk1);
+            }
+            uint32_t sum = 0;
+#pragma unroll
+            for (int k = 0; k < ADV_TP; ++k) {
+              if (pr[k] >= 0) {
+                const uint32_t xa = xs + ((uint32_t)(pr[k] & (P - 1)) << sl);
+                const uint32_t qa = qs + ((uint32_t)(pr[k] >> g.tile_lp) << sl);
+                if (s >= 4) {
+                  sum = sq_diff4(xa, qa, w[k], d, sum);
+                } else {
+                  sum += sq_diff(xa, qa, coord_of(w[k].x, d));
+                  if (s == 2) sum += sq_diff(xa, qa, coord_of(w[k].y, d));
+                }
+              }
+              if ((unsigned)(k + 1) % nb == 0) {
+                if (pr[k] >= 0) acc[pr[k]] = (int32_t)sum;
+                sum = 0;
+              }
+            }
+          }
+        } else {
+          for (unsigned l = gtid; l < m; l += GT) acc[L[l]] = 0;
+          gsync();
+          const unsigned lg = (unsigned)(lb - 2);
+          const unsigned total = m << lg;
+          for (unsigned it = gtid; it < total; it += GT) {
+            const unsigned li = it >> lg, b0 = (it & ((1u << lg) - 1u)) * ADV_TP;
+            const int pe = (int)L[li];
+            const uint32_t xa = xs + ((uint32_t)(pe & (P - 1)) << sl);
+            const uint32_t qa = qs + ((uint32_t)(pe >> g.tile_lp) << sl);
+            const uint32_t gi = (uint32_t)(p0 + (pe & (P - 1))) + g.id_offset;
+            const uint32_t gq = rng_qi(g, (uint32_t)(r0 + (pe >> g.tile_lp)));
+            const PhiloxPair pc = philox_pair(gi, gq, g.rk0);
+            uint4 w[ADV_TP];
+#pragma unroll
+            for (int k = 0; k < ADV_TP; ++k) w[k] = philox_from_pair(b0 + k, lv, pc, g.rk0, g.rk1);
+            uint32_t sum = 0;
+#pragma unroll
+            for (int k = 0; k < ADV_TP; ++k) sum = sq_diff4(xa, qa, w[k], d, sum);
+            atomicAdd(reinterpret_cast<uint32_t *>(acc + pe), sum);
+          }
+        }
+      }
+      gsync();
+      if (act4) {  // commit: S += the level's sum, T -> 2T (the thread's own 4 arms)
+        int4 o = S4;
+        uint32_t l4 = L4;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t a = (act4 >> (8 * k)) & 0xFFu;
+          if (!a) continue;
+          const int32_t add = acc[e4 + k];
+          if (k == 0) o.x += add;
+          if (k == 1) o.y += add;
+          if (k == 2) o.z += add;
+          if (k == 3) o.w += add;
+          l4 = (l4 & ~(0xFFu << (8 * k))) | (a << (8 * k));
+        }
+        *reinterpret_cast<int4 *>(g.S + o4) = o;
+        *reinterpret_cast<uint32_t *>(g.lvl + o4) = l4;
+      }
+    }
+    if (!have_x) wait_bar(pbar_s, pphase);  // a group without tiles in this column
+    pphase ^= 1u;
+  }
+  __syncthreads();
+  if (tid == 0 && s_blocks) atomicAdd(&g.ctl->tile_blocks, s_blocks);
+  if (tid == 0 && s_draws) atomicAdd(&g.ctl->tile_draws, s_draws);
+}
+
 int tile_slot_log2(int64_t pitch) {
   int l = 4;
   while ((1ll << l) < pitch) ++l;
@@ -625,7 +889,34 @@ static cudaError_t launch_tiles_k(const Geom &g, int num_sms, cudaStream_t s) {
   return launch_tiles_nt<MODE, TILE_NT>(gt, num_sms, &per_sm, s);
 }
 
+template <int NG>
+static cudaError_t launch_tiles_grp(const Geom &g, int num_sms, cudaStream_t s) {
+  cudaFuncAttributes fa{};
+  int dev = 0, rsv = 0;
+  if (cudaFuncGetAttributes(&fa, k_advance_tiles_grp<NG>) != cudaSuccess) fa.sharedSizeBytes = 4096;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev) != cudaSuccess)
+    rsv = 1024;
+  const size_t base = (size_t)fa.sharedSizeBytes + (size_t)rsv;
+  const size_t R = (size_t)1 << g.tile_lr, P = (size_t)1 << g.tile_lp, slot = (size_t)1 << g.tile_slot_l;
+  const size_t gsz = (R * P * 7 + 15) & ~(size_t)15;
+  const size_t rows0 = (base + NG * gsz + slot - 1) / slot * slot;
+  const size_t smem = rows0 + (NG * R + P) * slot - base;
+  cudaError_t e = cudaFuncSetAttribute(k_advance_tiles_grp<NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_advance_tiles_grp<NG><<<num_sms, TILE_NT_WIDE, smem, s>>>(g);
+  return cudaGetLastError();
+}
+
+size_t tile_grp_smem_bytes(int groups, int lr, int lp, int64_t pitch) {
+  const size_t R = (size_t)1 << lr, P = (size_t)1 << lp, slot = (size_t)1 << tile_slot_log2(pitch);
+  const size_t base = 4096 + 1024, gsz = (R * P * 7 + 15) & ~(size_t)15;
+  return (base + groups * gsz + slot - 1) / slot * slot + (groups * R + P) * slot;
+}
+
 cudaError_t launch_advance_tiles(const Geom &g, int num_sms, cudaStream_t s) {
+  if (g.tile_groups == 4 && !g.shared_draws && !g.wor) return launch_tiles_grp<4>(g, num_sms, s);
+  if (g.tile_groups == 2 && !g.shared_draws && !g.wor) return launch_tiles_grp<2>(g, num_sms, s);
   if (g.shared_draws && g.tile_lr == 5) return launch_tiles_k<1>(g, num_sms, s);
   if (g.wor) return launch_tiles_k<2>(g, num_sms, s);
   return launch_tiles_k<0>(g, num_sms, s);

@@ -408,3 +408,17 @@ def test_shared_draws_level_mma(ak, n, d, q, k, h, kind):
     rows = np.arange(0, q, max(1, q // 6))
     ref = orc.query_br(X, Q[rows], k, h, 43, al, want_sums=True, shared_draws=True)
     _assert_parity(a, ref, rows=rows)
+
+
+@pytest.mark.parametrize("groups", ["0", "2", "4"])
+def test_grouped_tiles_wide_rows(ak, groups, monkeypatch):
+    """Rows wider than 8 KB (C3-like, d = 12,288 and 9,000): the grouped tile kernel
+    (AKNN_TILE_GROUPS = 2 / 4 thread groups sharing the column's point rows) and the
+    classic one (0) agree with the oracle bit for bit, including ragged q and n."""
+    monkeypatch.setenv("AKNN_TILE_GROUPS", groups)
+    monkeypatch.setenv("AKNN_TILE_F", "0.25")  # make most tiles dense at small levels too
+    for (n, d, q, seed) in ((1203, 12288, 7, 41), (700, 9000, 5, 42)):
+        X, Q = synth.small_instance(seed, n, d, q=q)
+        al = orc.alpha_experimental(n, 0.05, d, 0.3)
+        got, ref = _run_both(ak, X, Q, 4, 4, seed, al)
+        _assert_parity(got, ref)
