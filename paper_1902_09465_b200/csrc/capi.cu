@@ -457,6 +457,15 @@ aknn_status key_geom(int64_t n_local, int64_t n_global, int32_t d, KeyGeom *kg, 
   return AKNN_OK;
 }
 
+// Bit c set: an arm advancing out of level c would reach d samples, so it goes exact
+// instead (reading R8).
+uint32_t exnext_mask(int32_t d, int growth) {
+  uint32_t m = 0;
+  for (uint32_t c = 0; c < (uint32_t)MAX_LEVELS; ++c)
+    if (lvl_count(c + 1u, growth) >= (uint32_t)d) m |= 1u << c;
+  return m;
+}
+
 // Build-time domain (include/aknn.h): sizes, and the composite rank key of the
 // whole point set must fit 63 bits, so every later query on the index can rank.
 aknn_status validate_build(int64_t n, int32_t d, int64_t n_global) {
@@ -847,6 +856,7 @@ aknn_status run_query(aknn_index *ix, const uint8_t *queries_dev, int64_t qstrid
   g.Ld = kg.Ld;
   g.L3 = kg.L3;
   g.growth = kg.growth;
+  g.exnext = exnext_mask(d, kg.growth);
   g.ibits = kg.ibits;
   g.kbits = kg.kbits;
   g.world = 1;
@@ -1112,6 +1122,7 @@ aknn_status run_query_sharded(const std::vector<aknn_index *> &shards, bool nccl
     g.Ld = kg[si].Ld;
     g.L3 = kg[si].L3;
     g.growth = kg[si].growth;
+    g.exnext = exnext_mask(d, kg[si].growth);
     g.ibits = kg[si].ibits;
     g.kbits = kg[si].kbits;
     g.cmax = kg[si].cmax;

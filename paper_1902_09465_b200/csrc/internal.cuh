@@ -132,6 +132,7 @@ struct Geom {
   unsigned long long Ld; // L / d
   unsigned long long L3; // L / 3 (growth 2: the counts 3 * 2^j)
   int growth;            // sample-count schedule: 1 doubling (R7), 2 (reading R25)
+  uint32_t exnext;       // bit c: the count after level c reaches d (the P:176 fallback)
   int ibits;             // bits of the local point index in a work-list code
   int kbits;             // bits of the GLOBAL point id in the composite key
   ShardRec *send;        // [q][k+h+1] this shard's summary (sharded query only)

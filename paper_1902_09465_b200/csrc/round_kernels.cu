@@ -229,10 +229,10 @@ __device__ __forceinline__ uint32_t filter_arms(const Geom &g, const int32_t *th
       inM = inM || (((eqkh >> c) & 1u) && S == t.w && gid <= idkh);
     }
     const bool blk = live && (inC ? S >= t.x : (inM ? ((mmask >> c) & 1u) != 0u : S < t.y));
-    // P:176 (reading R8): exact when the next count would reach d
-    const bool ex = lvl_count(c + 1u, g.growth) >= (unsigned)g.d;
+    // P:176 (reading R8): exact when the next count would reach d (bit c of g.exnext)
+    const bool ex = (g.exnext >> c) & 1u;
     const uint32_t act = blk ? (ex ? (uint32_t)ACT_EXACT : c + 1u) : 0u;
-    dr += (blk && !ex) ? lvl_count(c, g.growth) : 0u;  // the advance draws T_{c+1} - T_c = T_c (doubling)
+    dr += (blk && !ex) ? (1u << c) : 0u;  // tiles (doubling only): the advance draws T_c
     actw |= act << (8 * e);
     lw |= (blk && !ex && inM) ? (1u << (8 * e)) : 0u;  // inM: ranks 1..k+h (C or M)
   }
@@ -250,9 +250,9 @@ __device__ __forceinline__ uint32_t lead_arms(const Geom &g, const Arm4 &a, uint
     const uint8_t l = a.l[e];
     const uint32_t c = l & 31u;
     const bool go = i0 + e < g.n && ((lb >> (8 * e)) & 0xFFu) && !lvl_exact(l);
-    const bool ex = lvl_count(c + 1u, g.growth) >= (unsigned)g.d;
+    const bool ex = (g.exnext >> c) & 1u;
     const uint32_t act = go ? (ex ? (uint32_t)ACT_EXACT : c + 1u) : 0u;
-    dr += (go && !ex) ? lvl_count(c, g.growth) : 0u;
+    dr += (go && !ex) ? (1u << c) : 0u;
     actw |= act << (8 * e);
   }
   *draws = dr;
