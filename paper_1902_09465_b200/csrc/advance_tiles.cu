@@ -63,6 +63,21 @@ __device__ __forceinline__ uint32_t sq_diff4_j(uint32_t xa, uint32_t qa, uint32_
   return __dp4a(t, t, acc);
 }
 
+// Tight row slots (stride = pitch, not a power of two): coordinate address = row base + j.
+__device__ __forceinline__ uint32_t sq_diff_t(uint32_t xa, uint32_t qa, uint32_t j) {
+  const int diff = (int)lds_u8(xa + j) - (int)lds_u8(qa + j);
+  return (uint32_t)(diff * diff);
+}
+__device__ __forceinline__ uint32_t sq_diff4_t(uint32_t xa, uint32_t qa, uint4 w, uint32_t d, uint32_t acc) {
+  const uint32_t j0 = coord_of(w.x, d), j1 = coord_of(w.y, d), j2 = coord_of(w.z, d), j3 = coord_of(w.w, d);
+  const uint32_t x01 = __byte_perm(lds_u8(xa + j0), lds_u8(xa + j1), 0x1140);
+  const uint32_t x23 = __byte_perm(lds_u8(xa + j2), lds_u8(xa + j3), 0x4011);
+  const uint32_t q01 = __byte_perm(lds_u8(qa + j0), lds_u8(qa + j1), 0x1140);
+  const uint32_t q23 = __byte_perm(lds_u8(qa + j2), lds_u8(qa + j3), 0x4011);
+  const uint32_t t = __vabsdiffu4(__byte_perm(x01, x23, 0x7610), __byte_perm(q01, q23, 0x7610));
+  return __dp4a(t, t, acc);
+}
+
 __device__ __forceinline__ uint32_t sq_diff4(uint32_t xa, uint32_t qa, uint4 w, uint32_t d, uint32_t acc) {
   return sq_diff4_j(xa, qa, coord_of(w.x, d), coord_of(w.y, d), coord_of(w.z, d), coord_of(w.w, d), acc);
 }
@@ -538,7 +553,7 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Geom g) {
 // CTAs per SM would hide it, while the point rows stay shared (NG CTAs would need NG
 // copies: the shared memory holds NG R + P slots instead of NG (R + P)).  Per-query
 // draws with replacement (MODE 0) only; same arithmetic and result as k_advance_tiles.
-template <int NG>
+template <int NG, bool TIGHT>
 __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
   constexpr int GT = TILE_NT_WIDE / NG;  // threads per group (whole warps)
   static_assert(GT % 32 == 0, "groups of whole warps");
@@ -550,6 +565,8 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
   const int pitch = (int)g.pitch;
   const int sl = g.tile_slot_l;
   const uint32_t slot = 1u << sl;
+  // row stride: a power-of-two slot (coordinate address = row | j) or, TIGHT, the pitch
+  const uint32_t stride = TIGHT ? (uint32_t)pitch : slot;
   const int tid = threadIdx.x, grp = tid / GT, gtid = tid - grp * GT;
   const uint32_t base = (uint32_t)__cvta_generic_to_shared(tsm);
   // per group: acc [RP] int32 | lst [RP] u16 | sact [RP] u8 (7 RP bytes, 16-aligned)
@@ -557,14 +574,14 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
   int32_t *acc = reinterpret_cast<int32_t *>(tsm + (size_t)grp * gsz);
   uint16_t *lst = reinterpret_cast<uint16_t *>(acc + RP);
   uint8_t *sact = reinterpret_cast<uint8_t *>(lst + RP);
-  const uint32_t rows_s = (base + (uint32_t)NG * gsz + slot - 1) & ~(slot - 1);
+  const uint32_t rows_s = TIGHT ? base + (uint32_t)NG * gsz : (base + (uint32_t)NG * gsz + slot - 1) & ~(slot - 1);
   {
     uint32_t dyn;
     asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
-    if (rows_s + ((uint32_t)(NG * R + P) << sl) > base + dyn) __trap();  // host sizing broken: fail loudly
+    if (rows_s + (uint32_t)(NG * R + P) * stride > base + dyn) __trap();  // host sizing broken: fail loudly
   }
-  const uint32_t qs = rows_s + ((uint32_t)(grp * R) << sl);  // this group's query rows
-  const uint32_t xs = rows_s + ((uint32_t)(NG * R) << sl);   // the column's point rows
+  const uint32_t qs = rows_s + (uint32_t)(grp * R) * stride;  // this group's query rows
+  const uint32_t xs = rows_s + (uint32_t)(NG * R) * stride;   // the column's point rows
   const uint32_t qbar_s = (uint32_t)__cvta_generic_to_shared(&qbar[grp]);
   const uint32_t pbar_s = (uint32_t)__cvta_generic_to_shared(&pbar);
   const uint32_t d = (uint32_t)g.d;
@@ -607,7 +624,7 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
         if (p0 + row < g.n)
           asm volatile(
               "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                  xs + ((uint32_t)row << sl)),
+                  xs + (uint32_t)row * stride),
               "l"(g.X + (size_t)(p0 + row) * pitch), "r"((uint32_t)pitch), "r"(pbar_s)
               : "memory");
     }
@@ -626,7 +643,7 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
           if (r0 + row < g.q)
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    qs + ((uint32_t)row << sl)),
+                    qs + (uint32_t)row * stride),
                 "l"(g.Q + (size_t)(r0 + row) * pitch), "r"((uint32_t)pitch), "r"(qbar_s)
                 : "memory");
       }
@@ -727,13 +744,14 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
 #pragma unroll
             for (int k = 0; k < ADV_TP; ++k) {
               if (pr[k] >= 0) {
-                const uint32_t xa = xs + ((uint32_t)(pr[k] & (P - 1)) << sl);
-                const uint32_t qa = qs + ((uint32_t)(pr[k] >> g.tile_lp) << sl);
+                const uint32_t xa = xs + (uint32_t)(pr[k] & (P - 1)) * stride;
+                const uint32_t qa = qs + (uint32_t)(pr[k] >> g.tile_lp) * stride;
                 if (s >= 4) {
-                  sum = sq_diff4(xa, qa, w[k], d, sum);
+                  sum = TIGHT ? sq_diff4_t(xa, qa, w[k], d, sum) : sq_diff4(xa, qa, w[k], d, sum);
                 } else {
-                  sum += sq_diff(xa, qa, coord_of(w[k].x, d));
-                  if (s == 2) sum += sq_diff(xa, qa, coord_of(w[k].y, d));
+                  sum += TIGHT ? sq_diff_t(xa, qa, coord_of(w[k].x, d)) : sq_diff(xa, qa, coord_of(w[k].x, d));
+                  if (s == 2)
+                    sum += TIGHT ? sq_diff_t(xa, qa, coord_of(w[k].y, d)) : sq_diff(xa, qa, coord_of(w[k].y, d));
                 }
               }
               if ((unsigned)(k + 1) % nb == 0) {
@@ -750,8 +768,8 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
           for (unsigned it = gtid; it < total; it += GT) {
             const unsigned li = it >> lg, b0 = (it & ((1u << lg) - 1u)) * ADV_TP;
             const int pe = (int)L[li];
-            const uint32_t xa = xs + ((uint32_t)(pe & (P - 1)) << sl);
-            const uint32_t qa = qs + ((uint32_t)(pe >> g.tile_lp) << sl);
+            const uint32_t xa = xs + (uint32_t)(pe & (P - 1)) * stride;
+            const uint32_t qa = qs + (uint32_t)(pe >> g.tile_lp) * stride;
             const uint32_t gi = (uint32_t)(p0 + (pe & (P - 1))) + g.id_offset;
             const uint32_t gq = rng_qi(g, (uint32_t)(r0 + (pe >> g.tile_lp)));
             const PhiloxPair pc = philox_pair(gi, gq, g.rk0);
@@ -760,7 +778,8 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
             for (int k = 0; k < ADV_TP; ++k) w[k] = philox_from_pair(b0 + k, lv, pc, g.rk0, g.rk1);
             uint32_t sum = 0;
 #pragma unroll
-            for (int k = 0; k < ADV_TP; ++k) sum = sq_diff4(xa, qa, w[k], d, sum);
+            for (int k = 0; k < ADV_TP; ++k)
+              sum = TIGHT ? sq_diff4_t(xa, qa, w[k], d, sum) : sq_diff4(xa, qa, w[k], d, sum);
             atomicAdd(reinterpret_cast<uint32_t *>(acc + pe), sum);
           }
         }
@@ -889,34 +908,38 @@ static cudaError_t launch_tiles_k(const Geom &g, int num_sms, cudaStream_t s) {
   return launch_tiles_nt<MODE, TILE_NT>(gt, num_sms, &per_sm, s);
 }
 
-template <int NG>
+template <int NG, bool TIGHT>
 static cudaError_t launch_tiles_grp(const Geom &g, int num_sms, cudaStream_t s) {
   cudaFuncAttributes fa{};
   int dev = 0, rsv = 0;
-  if (cudaFuncGetAttributes(&fa, k_advance_tiles_grp<NG>) != cudaSuccess) fa.sharedSizeBytes = 4096;
+  if (cudaFuncGetAttributes(&fa, k_advance_tiles_grp<NG, TIGHT>) != cudaSuccess) fa.sharedSizeBytes = 4096;
   if (cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev) != cudaSuccess)
     rsv = 1024;
   const size_t base = (size_t)fa.sharedSizeBytes + (size_t)rsv;
   const size_t R = (size_t)1 << g.tile_lr, P = (size_t)1 << g.tile_lp, slot = (size_t)1 << g.tile_slot_l;
   const size_t gsz = (R * P * 7 + 15) & ~(size_t)15;
-  const size_t rows0 = (base + NG * gsz + slot - 1) / slot * slot;
-  const size_t smem = rows0 + (NG * R + P) * slot - base;
-  cudaError_t e = cudaFuncSetAttribute(k_advance_tiles_grp<NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t rows0 = TIGHT ? base + NG * gsz : (base + NG * gsz + slot - 1) / slot * slot;
+  const size_t smem = rows0 + (NG * R + P) * (TIGHT ? (size_t)g.pitch : slot) - base;
+  cudaError_t e = cudaFuncSetAttribute(k_advance_tiles_grp<NG, TIGHT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_advance_tiles_grp<NG><<<num_sms, TILE_NT_WIDE, smem, s>>>(g);
+  k_advance_tiles_grp<NG, TIGHT><<<num_sms, TILE_NT_WIDE, smem, s>>>(g);
   return cudaGetLastError();
 }
 
-size_t tile_grp_smem_bytes(int groups, int lr, int lp, int64_t pitch) {
+// Shared memory of a grouped shape (the chooser's test): tight = rows at the pitch.
+size_t tile_grp_smem_bytes(int groups, int lr, int lp, int64_t pitch, bool tight) {
   const size_t R = (size_t)1 << lr, P = (size_t)1 << lp, slot = (size_t)1 << tile_slot_log2(pitch);
   const size_t base = 4096 + 1024, gsz = (R * P * 7 + 15) & ~(size_t)15;
+  if (tight) return base + groups * gsz + (groups * R + P) * (size_t)pitch;
   return (base + groups * gsz + slot - 1) / slot * slot + (groups * R + P) * slot;
 }
 
 cudaError_t launch_advance_tiles(const Geom &g, int num_sms, cudaStream_t s) {
-  if (g.tile_groups == 4 && !g.shared_draws && !g.wor) return launch_tiles_grp<4>(g, num_sms, s);
-  if (g.tile_groups == 2 && !g.shared_draws && !g.wor) return launch_tiles_grp<2>(g, num_sms, s);
+  if (g.tile_groups && !g.shared_draws && !g.wor) {
+    if (g.tile_groups == 4) return g.tile_tight ? launch_tiles_grp<4, true>(g, num_sms, s) : launch_tiles_grp<4, false>(g, num_sms, s);
+    if (g.tile_groups == 2) return g.tile_tight ? launch_tiles_grp<2, true>(g, num_sms, s) : launch_tiles_grp<2, false>(g, num_sms, s);
+  }
   if (g.shared_draws && g.tile_lr == 5) return launch_tiles_k<1>(g, num_sms, s);
   if (g.wor) return launch_tiles_k<2>(g, num_sms, s);
   return launch_tiles_k<0>(g, num_sms, s);

@@ -422,3 +422,16 @@ def test_grouped_tiles_wide_rows(ak, groups, monkeypatch):
         al = orc.alpha_experimental(n, 0.05, d, 0.3)
         got, ref = _run_both(ak, X, Q, 4, 4, seed, al)
         _assert_parity(got, ref)
+
+
+def test_grouped_tiles_tight_rows(ak, monkeypatch):
+    """The grouped kernel with rows at the pitch (AKNN_TILE_TIGHT = 1: 2 groups x 1 query
+    row + 16 point rows) against the oracle."""
+    monkeypatch.setenv("AKNN_TILE_GROUPS", "2")
+    monkeypatch.setenv("AKNN_TILE_TIGHT", "1")
+    monkeypatch.setenv("AKNN_TILE_F", "0.25")
+    for (n, d, q, seed) in ((1203, 12288, 7, 43), (777, 9000, 5, 44)):
+        X, Q = synth.small_instance(seed, n, d, q=q)
+        al = orc.alpha_experimental(n, 0.05, d, 0.3)
+        got, ref = _run_both(ak, X, Q, 4, 4, seed, al)
+        _assert_parity(got, ref)
