@@ -561,6 +561,8 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
   __shared__ unsigned lcnt[NG][MAX_LEVELS], loff[NG][MAX_LEVELS + 1], lfill[NG][MAX_LEVELS];
   __shared__ __align__(8) uint64_t qbar[NG], pbar;
   __shared__ unsigned long long s_blocks, s_draws;
+  constexpr int CM_WORDS = 1024;                   // dense-tile bits of the column (rows <= 32768)
+  __shared__ uint32_t colmask[CM_WORDS];
   const int R = 1 << g.tile_lr, P = 1 << g.tile_lp, RP = R * P;
   const int pitch = (int)g.pitch;
   const int sl = g.tile_slot_l;
@@ -609,10 +611,16 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
   };
   const int c0 = (int)((long long)blockIdx.x * cols / gridDim.x), c1 = (int)((long long)(blockIdx.x + 1) * cols / gridDim.x);
   for (int tp = c0; tp < c1; ++tp) {
-    // any dense tile in this column?  (all groups are done with the previous column)
+    // the column's dense query tiles as a bit mask, read once (all groups are done with
+    // the previous column); a column without one is skipped
     bool mine = false;
-    for (int tr = tid; tr < rows; tr += TILE_NT_WIDE)
-      mine |= (float)g.tilework[(size_t)tr * g.tile_cols + tp] >= dthr;
+    for (int w = tid; w < CM_WORDS && w * 32 < rows; w += TILE_NT_WIDE) colmask[w] = 0u;
+    __syncthreads();
+    for (int tr = tid; tr < rows; tr += TILE_NT_WIDE) {
+      const bool dn = (float)g.tilework[(size_t)tr * g.tile_cols + tp] >= dthr;
+      mine |= dn;
+      if (dn && tr < CM_WORDS * 32) atomicOr(&colmask[tr >> 5], 1u << (tr & 31));
+    }
     if (!__syncthreads_or(mine)) continue;
     const int p0 = tp << g.tile_lp;
     if (tid == 0) {  // the column's point rows: bulk TMA copies
@@ -629,8 +637,43 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
               : "memory");
     }
     bool have_x = false;
-    for (int tr = grp; tr < rows; tr += NG) {
-      if ((float)g.tilework[(size_t)tr * g.tile_cols + tp] < dthr) continue;  // uniform in the group
+    auto dense_at = [&](int tr) {
+      return tr < CM_WORDS * 32 ? ((colmask[tr >> 5] >> (tr & 31)) & 1u) != 0u
+                                : (float)g.tilework[(size_t)tr * g.tile_cols + tp] >= dthr;
+    };
+    auto next_dense = [&](int tr) {  // the group's next dense query tile at or after tr
+      while (tr < rows && !dense_at(tr)) tr += NG;
+      return tr;
+    };
+    // thread -> 4 consecutive arms of one query row (RP <= 4 GT): done flag, actions, S
+    // and levels in one round trip, issued one tile AHEAD (the tiles hold disjoint pairs)
+    const int e4 = gtid * 4;
+    const bool in = e4 < RP;
+    const int rr = in ? e4 >> g.tile_lp : 0, pp = e4 & (P - 1);
+    struct TileState {
+      int4 S4;
+      uint32_t A4, L4;
+      int dn;
+    };
+    auto load_state = [&](int tr) {
+      TileState t{make_int4(0, 0, 0, 0), 0u, 0u, 1};
+      const int r0n = tr << g.tile_lr;
+      if (tr < rows && in && r0n + rr < g.q && p0 + pp < g.n) {
+        const size_t o = (size_t)(r0n + rr) * g.npad + p0 + pp;
+        t.dn = g.qs[r0n + rr].done;
+        t.A4 = *reinterpret_cast<const uint32_t *>(g.act + o);
+        t.S4 = *reinterpret_cast<const int4 *>(g.S + o);
+        t.L4 = *reinterpret_cast<const uint32_t *>(g.lvl + o);
+      }
+      return t;
+    };
+    int trn = next_dense(grp);
+    TileState nxt = load_state(trn);
+    while (trn < rows) {
+      const int tr = trn;
+      const TileState cur = nxt;
+      trn = next_dense(tr + NG);
+      nxt = load_state(trn);  // in flight while this tile is processed
       const int r0 = tr << g.tile_lr;
       gsync();  // the group's previous tile is done with its slots and arrays
       if (gtid < MAX_LEVELS) lcnt[grp][gtid] = 0;
@@ -647,22 +690,10 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
                 "l"(g.Q + (size_t)(r0 + row) * pitch), "r"((uint32_t)pitch), "r"(qbar_s)
                 : "memory");
       }
-      // thread -> 4 consecutive arms of one query row (RP <= 4 GT): done flag, actions,
-      // S and levels in one round trip
-      const int e4 = gtid * 4;
-      const bool in = e4 < RP;
-      const int rr = in ? e4 >> g.tile_lp : 0, pp = e4 & (P - 1);
-      const bool live = in && r0 + rr < g.q && p0 + pp < g.n;
       const size_t o4 = (size_t)(r0 + rr) * g.npad + p0 + pp;
-      int4 S4 = make_int4(0, 0, 0, 0);
-      uint32_t A4 = 0, L4 = 0;
-      int dn = 1;
-      if (live) {
-        dn = g.qs[r0 + rr].done;
-        A4 = *reinterpret_cast<const uint32_t *>(g.act + o4);
-        S4 = *reinterpret_cast<const int4 *>(g.S + o4);
-        L4 = *reinterpret_cast<const uint32_t *>(g.lvl + o4);
-      }
+      const int4 S4 = cur.S4;
+      const uint32_t A4 = cur.A4, L4 = cur.L4;
+      const int dn = cur.dn;
       gsync();  // lcnt cleared
       uint32_t act4 = 0;  // sampled actions only (exact fallbacks: tensor-core pass)
 #pragma unroll
