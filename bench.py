@@ -548,6 +548,8 @@ def run_ours(args, dist: Dist):
     adv_draws = max(0, agg["draws"] - args.steps * qpr * n_loc - agg.get("tile_draws", 0))
     x_in_l2 = n_loc * d <= L2_BYTES * 0.8
     kof = KERNEL_OF_SHARED if (args.draws == "shared" and agg.get("level_mma_tiles", 0) > 0) else KERNEL_OF
+    if d > 8192 and kof is KERNEL_OF:  # rows wider than 8 KB: the grouped tile kernel
+        kof = dict(KERNEL_OF, tiles="k_advance_tiles_grp")
     common = {"kernel": kof[dom], "launches": launches[dom],
               "avg_launch_ms": ms_cls[dom] / max(1, launches[dom]),
               "share_of_step": ms_cls[dom] / ms_local_instr,

@@ -614,6 +614,7 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
     // the column's dense query tiles as a bit mask, read once (all groups are done with
     // the previous column); a column without one is skipped
     bool mine = false;
+    __syncthreads();  // every group has left the previous column (its mask reads included)
     for (int w = tid; w < CM_WORDS && w * 32 < rows; w += TILE_NT_WIDE) colmask[w] = 0u;
     __syncthreads();
     for (int tr = tid; tr < rows; tr += TILE_NT_WIDE) {
