@@ -553,13 +553,16 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Geom g) {
 // CTAs per SM would hide it, while the point rows stay shared (NG CTAs would need NG
 // copies: the shared memory holds NG R + P slots instead of NG (R + P)).  Per-query
 // draws with replacement (MODE 0) only; same arithmetic and result as k_advance_tiles.
-template <int NG, bool TIGHT>
+template <int NG, bool TIGHT, bool DB>
 __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
+  // DB: each group double-buffers its query rows -- the next tile's copy runs during this
+  // tile's draws (2 NG R query slots)
+  constexpr int QB = DB ? 2 : 1;
   constexpr int GT = TILE_NT_WIDE / NG;  // threads per group (whole warps)
   static_assert(GT % 32 == 0, "groups of whole warps");
   extern __shared__ __align__(16) unsigned char tsm[];
   __shared__ unsigned lcnt[NG][MAX_LEVELS], loff[NG][MAX_LEVELS + 1], lfill[NG][MAX_LEVELS];
-  __shared__ __align__(8) uint64_t qbar[NG], pbar;
+  __shared__ __align__(8) uint64_t qbar[NG][2], pbar;
   __shared__ unsigned long long s_blocks, s_draws;
   constexpr int CM_WORDS = 1024;                   // dense-tile bits of the column (rows <= 32768)
   __shared__ uint32_t colmask[CM_WORDS];
@@ -580,11 +583,11 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
   {
     uint32_t dyn;
     asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
-    if (rows_s + (uint32_t)(NG * R + P) * stride > base + dyn) __trap();  // host sizing broken: fail loudly
+    if (rows_s + (uint32_t)(QB * NG * R + P) * stride > base + dyn) __trap();  // host sizing broken: fail loudly
   }
-  const uint32_t qs = rows_s + (uint32_t)(grp * R) * stride;  // this group's query rows
-  const uint32_t xs = rows_s + (uint32_t)(NG * R) * stride;   // the column's point rows
-  const uint32_t qbar_s = (uint32_t)__cvta_generic_to_shared(&qbar[grp]);
+  const uint32_t qs0 = rows_s + (uint32_t)(grp * QB * R) * stride;  // this group's query rows (buffer 0)
+  const uint32_t xs = rows_s + (uint32_t)(QB * NG * R) * stride;     // the column's point rows
+  const uint32_t qbar0 = (uint32_t)__cvta_generic_to_shared(&qbar[grp][0]);
   const uint32_t pbar_s = (uint32_t)__cvta_generic_to_shared(&pbar);
   const uint32_t d = (uint32_t)g.d;
   const int rows = (g.q + R - 1) >> g.tile_lr;
@@ -592,13 +595,15 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
   const float dthr = g.tile_min_draws;
   if (tid == 0) {
     s_blocks = s_draws = 0;
-    for (int j = 0; j < NG; ++j) asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(
-                                     (uint32_t)__cvta_generic_to_shared(&qbar[j])));
+    for (int j = 0; j < NG; ++j)
+      for (int b = 0; b < 2; ++b)
+        asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&qbar[j][b])));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(pbar_s));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  uint32_t qphase = 0, pphase = 0;
+  uint32_t qphase = 0u, pphase = 0;  // qphase bit b: the parity of query buffer b's barrier
+  int sel = 0;  // the query buffer of the current tile
   auto gsync = [&] { asm volatile("bar.sync %0, %1;" ::"r"(grp + 1), "r"(GT) : "memory"); };
   auto wait_bar = [](uint32_t bar, uint32_t ph) {
     asm volatile(
@@ -670,6 +675,7 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
     };
     int trn = next_dense(grp);
     TileState nxt = load_state(trn);
+    bool first = true;
     while (trn < rows) {
       const int tr = trn;
       const TileState cur = nxt;
@@ -678,19 +684,29 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
       const int r0 = tr << g.tile_lr;
       gsync();  // the group's previous tile is done with its slots and arrays
       if (gtid < MAX_LEVELS) lcnt[grp][gtid] = 0;
-      if (gtid == 0) {  // the tile's query rows into the group's slots
+      // the query rows: this tile's were copied during the previous tile of the column
+      // (DB) unless it is the group's first; then the next tile's copy is issued into
+      // the other buffer, free since the gsync above
+      auto issue_rows = [&](int trq, int b) {
+        const int rq = trq << g.tile_lr;
+        const uint32_t bar = qbar0 + 8u * (uint32_t)b, dst = qs0 + (uint32_t)(b * R) * stride;
         uint32_t bytes = 0;
-        for (int row = 0; row < R; ++row) bytes += r0 + row < g.q ? (uint32_t)pitch : 0u;
+        for (int row = 0; row < R; ++row) bytes += rq + row < g.q ? (uint32_t)pitch : 0u;
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(qbar_s), "r"(bytes) : "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
         for (int row = 0; row < R; ++row)
-          if (r0 + row < g.q)
+          if (rq + row < g.q)
             asm volatile(
                 "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-                    qs + (uint32_t)row * stride),
-                "l"(g.Q + (size_t)(r0 + row) * pitch), "r"((uint32_t)pitch), "r"(qbar_s)
+                    dst + (uint32_t)row * stride),
+                "l"(g.Q + (size_t)(rq + row) * pitch), "r"((uint32_t)pitch), "r"(bar)
                 : "memory");
+      };
+      if (gtid == 0) {
+        if (!DB || first) issue_rows(tr, sel);
+        if (DB && trn < rows) issue_rows(trn, sel ^ 1);
       }
+      const uint32_t qs = qs0 + (uint32_t)(sel * R) * stride;
       const size_t o4 = (size_t)(r0 + rr) * g.npad + p0 + pp;
       const int4 S4 = cur.S4;
       const uint32_t A4 = cur.A4, L4 = cur.L4;
@@ -732,8 +748,8 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
         b0 = __shfl_sync(FULL, b0, leader);
         if (a) lst[b0 + __popc(m & ((1u << lane_id()) - 1u))] = (uint16_t)(e4 + k);
       }
-      wait_bar(qbar_s, qphase);  // the query rows
-      qphase ^= 1u;
+      wait_bar(qbar0 + 8u * (uint32_t)sel, (qphase >> sel) & 1u);  // the query rows
+      qphase ^= 1u << sel;
       if (!have_x) {  // the column's point rows (once per column and group)
         wait_bar(pbar_s, pphase);
         have_x = true;
@@ -834,6 +850,8 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
         *reinterpret_cast<int4 *>(g.S + o4) = o;
         *reinterpret_cast<uint32_t *>(g.lvl + o4) = l4;
       }
+      first = false;
+      if (DB) sel ^= 1;
     }
     if (!have_x) wait_bar(pbar_s, pphase);  // a group without tiles in this column
     pphase ^= 1u;
@@ -940,11 +958,11 @@ static cudaError_t launch_tiles_k(const Geom &g, int num_sms, cudaStream_t s) {
   return launch_tiles_nt<MODE, TILE_NT>(gt, num_sms, &per_sm, s);
 }
 
-template <int NG, bool TIGHT>
+template <int NG, bool TIGHT, bool DB>
 static cudaError_t launch_tiles_grp(const Geom &g, int num_sms, cudaStream_t s) {
   cudaFuncAttributes fa{};
   int dev = 0, rsv = 0;
-  if (cudaFuncGetAttributes(&fa, k_advance_tiles_grp<NG, TIGHT>) != cudaSuccess) fa.sharedSizeBytes = 4096;
+  if (cudaFuncGetAttributes(&fa, k_advance_tiles_grp<NG, TIGHT, DB>) != cudaSuccess) fa.sharedSizeBytes = 4096;
   if (cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev) != cudaSuccess)
     rsv = 1024;
@@ -952,25 +970,27 @@ static cudaError_t launch_tiles_grp(const Geom &g, int num_sms, cudaStream_t s) 
   const size_t R = (size_t)1 << g.tile_lr, P = (size_t)1 << g.tile_lp, slot = (size_t)1 << g.tile_slot_l;
   const size_t gsz = (R * P * 7 + 15) & ~(size_t)15;
   const size_t rows0 = TIGHT ? base + NG * gsz : (base + NG * gsz + slot - 1) / slot * slot;
-  const size_t smem = rows0 + (NG * R + P) * (TIGHT ? (size_t)g.pitch : slot) - base;
-  cudaError_t e = cudaFuncSetAttribute(k_advance_tiles_grp<NG, TIGHT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = rows0 + ((DB ? 2 : 1) * NG * R + P) * (TIGHT ? (size_t)g.pitch : slot) - base;
+  cudaError_t e = cudaFuncSetAttribute(k_advance_tiles_grp<NG, TIGHT, DB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_advance_tiles_grp<NG, TIGHT><<<num_sms, TILE_NT_WIDE, smem, s>>>(g);
+  k_advance_tiles_grp<NG, TIGHT, DB><<<num_sms, TILE_NT_WIDE, smem, s>>>(g);
   return cudaGetLastError();
 }
 
 // Shared memory of a grouped shape (the chooser's test): tight = rows at the pitch.
-size_t tile_grp_smem_bytes(int groups, int lr, int lp, int64_t pitch, bool tight) {
+size_t tile_grp_smem_bytes(int groups, int lr, int lp, int64_t pitch, bool tight, bool db) {
   const size_t R = (size_t)1 << lr, P = (size_t)1 << lp, slot = (size_t)1 << tile_slot_log2(pitch);
-  const size_t base = 4096 + 1024, gsz = (R * P * 7 + 15) & ~(size_t)15;
-  if (tight) return base + groups * gsz + (groups * R + P) * (size_t)pitch;
-  return (base + groups * gsz + slot - 1) / slot * slot + (groups * R + P) * slot;
+  const size_t base = 4096 + 1024, gsz = (R * P * 7 + 15) & ~(size_t)15, qrows = (db ? 2 : 1) * groups * R;
+  if (tight) return base + groups * gsz + (qrows + P) * (size_t)pitch;
+  return (base + groups * gsz + slot - 1) / slot * slot + (qrows + P) * slot;
 }
 
 cudaError_t launch_advance_tiles(const Geom &g, int num_sms, cudaStream_t s) {
   if (g.tile_groups && !g.shared_draws && !g.wor) {
-    if (g.tile_groups == 4) return g.tile_tight ? launch_tiles_grp<4, true>(g, num_sms, s) : launch_tiles_grp<4, false>(g, num_sms, s);
-    if (g.tile_groups == 2) return g.tile_tight ? launch_tiles_grp<2, true>(g, num_sms, s) : launch_tiles_grp<2, false>(g, num_sms, s);
+    if (g.tile_groups == 4) return launch_tiles_grp<4, false, false>(g, num_sms, s);
+    if (g.tile_groups == 2 && g.tile_tight) return launch_tiles_grp<2, true, false>(g, num_sms, s);
+    if (g.tile_groups == 2 && g.tile_db) return launch_tiles_grp<2, false, true>(g, num_sms, s);
+    if (g.tile_groups == 2) return launch_tiles_grp<2, false, false>(g, num_sms, s);
   }
   if (g.shared_draws && g.tile_lr == 5) return launch_tiles_k<1>(g, num_sms, s);
   if (g.wor) return launch_tiles_k<2>(g, num_sms, s);

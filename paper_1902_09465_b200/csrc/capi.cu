@@ -275,6 +275,7 @@ struct TileShape {
   float row_draws;
   int groups;  // > 0: grouped tiles (one CTA per SM, point rows shared by the groups)
   int tight;   // grouped, rows at the pitch
+  int db;      // grouped, double-buffered query rows
 };
 
 int env_int(const char *name, int dflt) {
@@ -283,7 +284,7 @@ int env_int(const char *name, int dflt) {
 }
 
 TileShape tile_shape(int64_t pitch, int64_t n) {
-  TileShape t{0, 0, 0, 0.f, 0, 0};
+  TileShape t{0, 0, 0, 0.f, 0, 0, 0};
   if (env_int("AKNN_TILE", 1) == 0) return t;
   // the largest tile (R * P) whose shared memory fits 3, 2 or 1 CTAs per SM (228 KB);
   // rows wider than 8 KB: the largest tile at one CTA per SM (C3, d = 12,288: 4 x 8 at
@@ -307,21 +308,28 @@ TileShape tile_shape(int64_t pitch, int64_t n) {
   // R = 4 / NG query rows (AKNN_TILE_GROUPS = 0 / 2 / 4; default 4)
   // AKNN_TILE_TIGHT = 1: rows at the pitch (not in power-of-two slots), so 16 point rows
   // fit with 2 groups of one query row (the query rows restaged per pair halve)
+  // AKNN_TILE_GROUPS = 2 with AKNN_TILE_DB = 1: 2 groups of one query row, each double-
+  // buffering its query rows (the next tile's copy overlaps this tile's draws)
   const int ng = pitch > 8192 ? env_int("AKNN_TILE_GROUPS", 4) : 0;
-  const int tight = env_int("AKNN_TILE_TIGHT", 0);
-  if (ng == 2 && tight && tile_grp_smem_bytes(2, 0, 4, pitch, true) <= (size_t)227 * 1024) {
+  const int tight = env_int("AKNN_TILE_TIGHT", 0), db = env_int("AKNN_TILE_DB", 1);
+  if (ng == 2 && tight && tile_grp_smem_bytes(2, 0, 4, pitch, true, false) <= (size_t)227 * 1024) {
     t.groups = 2;
     t.tight = 1;
     t.lr = 0;
     t.lp = 4;
-  } else if ((ng == 2 || ng == 4) && tile_grp_smem_bytes(ng, ng == 4 ? 0 : 1, 3, pitch, false) <= (size_t)227 * 1024) {
+  } else if (ng == 2 && db && tile_grp_smem_bytes(2, 0, 3, pitch, false, true) <= (size_t)227 * 1024) {
+    t.groups = 2;
+    t.db = 1;
+    t.lr = 0;
+    t.lp = 3;
+  } else if ((ng == 2 || ng == 4) && tile_grp_smem_bytes(ng, ng == 4 ? 0 : 1, 3, pitch, false, false) <= (size_t)227 * 1024) {
     t.groups = ng;
     t.lr = ng == 4 ? 0 : 1;
     t.lp = 3;
   }
   if (t.lr < 0 || t.lr > 5 || t.lp < 2 || t.lp > 5 ||
       (!t.groups && tile_smem_bytes(t.lr, t.lp, pitch) > (size_t)233472))
-    return TileShape{0, 0, 0, 0.f, 0, 0};
+    return TileShape{0, 0, 0, 0.f, 0, 0, 0};
   // X in L2 (C2: 47 MB): a list draw costs one L2 sector, tiles must amortise their
   // staging over >= 4 sectors' worth of draws; X in HBM (C3-C5): a list draw is a
   // random HBM sector (~1/15 the Philox rate): F = 1 measured best on C3 (-2 %) and
@@ -349,6 +357,7 @@ void setup_tiles(Geom &g, const TileShape &t, const aknn_opts &o, int64_t qb, ui
   g.tile_lp = t.lp;
   g.tile_groups = (o.flags & (AKNN_FLAG_SHARED_DRAWS | AKNN_FLAG_WITHOUT_REPLACEMENT)) ? 0 : t.groups;
   g.tile_tight = t.tight;
+  g.tile_db = t.db;
   g.tile_cols = (int)((g.npad + (1ll << t.lp) - 1) >> t.lp);
   g.tilework = reinterpret_cast<uint32_t *>(ws);
   g.tile_slot_l = tile_slot_log2(g.pitch);

@@ -162,6 +162,7 @@ struct Geom {
   int tile_tma;          // 1: rows staged by bulk TMA copies (cp.async.bulk), 0: 16-byte cp.async
   int tile_groups;       // > 0: k_advance_tiles_grp with this many thread groups per CTA
   int tile_tight;        // 1: its row slots are the pitch apart (not a power of two)
+  int tile_db;           // 1: its groups double-buffer their query rows
   unsigned long long *advanced;  // pairs advanced (statistics), device counter
   // the blocker predicate as integer thresholds per (query, level) (k_thresholds)
   int32_t *thr;          // [q][THR_STRIDE]: Su[c], Sl[c] (c < MAX_LEVELS), M-mask

@@ -56,7 +56,7 @@ int stage_level(int64_t pitch);
 // Tile-staged level gathers of dense tiles (advance_tiles.cu).
 cudaError_t launch_advance_tiles(const Geom &g, int num_sms, cudaStream_t s);
 size_t tile_smem_bytes(int lr, int lp, int64_t pitch);
-size_t tile_grp_smem_bytes(int groups, int lr, int lp, int64_t pitch, bool tight);
+size_t tile_grp_smem_bytes(int groups, int lr, int lp, int64_t pitch, bool tight, bool db);
 int tile_slot_log2(int64_t pitch);
 // Per-query counters from the final arm states (before the outputs).
 cudaError_t launch_tally(const Geom &g, cudaStream_t s);

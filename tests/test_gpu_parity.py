@@ -435,3 +435,16 @@ def test_grouped_tiles_tight_rows(ak, monkeypatch):
         al = orc.alpha_experimental(n, 0.05, d, 0.3)
         got, ref = _run_both(ak, X, Q, 4, 4, seed, al)
         _assert_parity(got, ref)
+
+
+@pytest.mark.parametrize("db", ["0", "1"])
+def test_grouped_tiles_two_groups(ak, db, monkeypatch):
+    """Two groups per CTA, with (AKNN_TILE_DB = 1) and without double-buffered query rows,
+    over several point columns per CTA, against the oracle."""
+    monkeypatch.setenv("AKNN_TILE_GROUPS", "2")
+    monkeypatch.setenv("AKNN_TILE_DB", db)
+    monkeypatch.setenv("AKNN_TILE_F", "0.25")
+    X, Q = synth.small_instance(45, 4000, 12288, q=9)
+    al = orc.alpha_experimental(4000, 0.05, 12288, 0.3)
+    got, ref = _run_both(ak, X, Q, 4, 4, 45, al)
+    _assert_parity(got, ref)
