@@ -564,6 +564,7 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
   __shared__ unsigned lcnt[NG][MAX_LEVELS], loff[NG][MAX_LEVELS + 1], lfill[NG][MAX_LEVELS];
   __shared__ __align__(8) uint64_t qbar[NG][2], pbar;
   __shared__ unsigned long long s_blocks, s_draws;
+  __shared__ unsigned lmask_s[NG];
   constexpr int CM_WORDS = 1024;                   // dense-tile bits of the column (rows <= 32768)
   __shared__ uint32_t colmask[CM_WORDS];
   const int R = 1 << g.tile_lr, P = 1 << g.tile_lp, RP = R * P;
@@ -712,17 +713,21 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
       const uint32_t A4 = cur.A4, L4 = cur.L4;
       const int dn = cur.dn;
       gsync();  // lcnt cleared
+      // only the warps holding arms (4 per thread, RP <= 4 GT) list them
+      const bool arm_warp = (gtid & ~31) * 4 < RP;
       uint32_t act4 = 0;  // sampled actions only (exact fallbacks: tensor-core pass)
+      if (arm_warp) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        uint8_t a = (uint8_t)(A4 >> (8 * k));
-        if (dn || a > MAX_LEVELS || p0 + pp + k >= g.n) a = 0;
-        act4 |= (uint32_t)a << (8 * k);
-        hist_add(lcnt[grp], a ? a - 1u : NONE);
+        for (int k = 0; k < 4; ++k) {
+          uint8_t a = (uint8_t)(A4 >> (8 * k));
+          if (dn || a > MAX_LEVELS || p0 + pp + k >= g.n) a = 0;
+          act4 |= (uint32_t)a << (8 * k);
+          hist_add(lcnt[grp], a ? a - 1u : NONE);
+        }
+        if (in) *reinterpret_cast<uint32_t *>(sact + e4) = act4;
       }
-      if (in) *reinterpret_cast<uint32_t *>(sact + e4) = act4;
       gsync();  // lcnt
-      if (gtid < 32) {
+      if (gtid < 32) {  // per-level offsets, the level mask and the statistics: one warp
         const unsigned v = gtid < MAX_LEVELS ? lcnt[grp][gtid] : 0u;
         unsigned x = v;
 #pragma unroll
@@ -735,18 +740,32 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
           lfill[grp][gtid] = x - v;
         }
         if (gtid == MAX_LEVELS - 1) loff[grp][MAX_LEVELS] = x;
+        const unsigned lm = __ballot_sync(FULL, v != 0u);
+        unsigned long long dr = (unsigned long long)v << gtid, bl = (unsigned long long)v << (gtid < 2 ? 0 : gtid - 2);
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          dr += __shfl_xor_sync(FULL, dr, o);
+          bl += __shfl_xor_sync(FULL, bl, o);
+        }
+        if (gtid == 0) {
+          lmask_s[grp] = lm;
+          if (dr) atomicAdd(&s_draws, dr);
+          if (bl) atomicAdd(&s_blocks, bl);
+        }
       }
       gsync();
+      if (arm_warp) {
 #pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        const uint8_t a = (uint8_t)(act4 >> (8 * k));
-        const unsigned key = a ? a - 1u : NONE;
-        const unsigned m = __match_any_sync(FULL, key);
-        const int leader = __ffs(m) - 1;
-        unsigned b0 = 0;
-        if (a && lane_id() == leader) b0 = atomicAdd(&lfill[grp][key], (unsigned)__popc(m));
-        b0 = __shfl_sync(FULL, b0, leader);
-        if (a) lst[b0 + __popc(m & ((1u << lane_id()) - 1u))] = (uint16_t)(e4 + k);
+        for (int k = 0; k < 4; ++k) {
+          const uint8_t a = (uint8_t)(act4 >> (8 * k));
+          const unsigned key = a ? a - 1u : NONE;
+          const unsigned m = __match_any_sync(FULL, key);
+          const int leader = __ffs(m) - 1;
+          unsigned b0 = 0;
+          if (a && lane_id() == leader) b0 = atomicAdd(&lfill[grp][key], (unsigned)__popc(m));
+          b0 = __shfl_sync(FULL, b0, leader);
+          if (a) lst[b0 + __popc(m & ((1u << lane_id()) - 1u))] = (uint16_t)(e4 + k);
+        }
       }
       wait_bar(qbar0 + 8u * (uint32_t)sel, (qphase >> sel) & 1u);  // the query rows
       qphase ^= 1u << sel;
@@ -755,17 +774,7 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
         have_x = true;
       }
       gsync();
-      unsigned lmask = 0;
-      for (int c = 0; c < MAX_LEVELS; ++c) lmask |= (lcnt[grp][c] != 0u) << c;
-      if (gtid == 0) {
-        unsigned long long dr = 0, b = 0;
-        for (int c = 0; c < MAX_LEVELS; ++c) {
-          dr += (unsigned long long)lcnt[grp][c] << c;
-          b += (unsigned long long)lcnt[grp][c] << (c < 2 ? 0 : c - 2);
-        }
-        atomicAdd(&s_draws, dr);
-        atomicAdd(&s_blocks, b);
-      }
+      unsigned lmask = lmask_s[grp];
       for (; lmask; lmask &= lmask - 1) {
         const int c = __ffs(lmask) - 1;
         const unsigned m = lcnt[grp][c];
