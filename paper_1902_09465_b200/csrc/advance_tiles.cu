@@ -553,12 +553,12 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Geom g) {
 // CTAs per SM would hide it, while the point rows stay shared (NG CTAs would need NG
 // copies: the shared memory holds NG R + P slots instead of NG (R + P)).  Per-query
 // draws with replacement (MODE 0) only; same arithmetic and result as k_advance_tiles.
-template <int NG, bool TIGHT, bool DB>
-__global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
+template <int NG, bool TIGHT, bool DB, int NTT>
+__global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
   // DB: each group double-buffers its query rows -- the next tile's copy runs during this
   // tile's draws (2 NG R query slots)
   constexpr int QB = DB ? 2 : 1;
-  constexpr int GT = TILE_NT_WIDE / NG;  // threads per group (whole warps)
+  constexpr int GT = NTT / NG;  // threads per group (whole warps)
   static_assert(GT % 32 == 0, "groups of whole warps");
   extern __shared__ __align__(16) unsigned char tsm[];
   __shared__ unsigned lcnt[NG][MAX_LEVELS], loff[NG][MAX_LEVELS + 1], lfill[NG][MAX_LEVELS];
@@ -621,9 +621,9 @@ __global__ void __launch_bounds__(TILE_NT_WIDE) k_advance_tiles_grp(Geom g) {
     // the previous column); a column without one is skipped
     bool mine = false;
     __syncthreads();  // every group has left the previous column (its mask reads included)
-    for (int w = tid; w < CM_WORDS && w * 32 < rows; w += TILE_NT_WIDE) colmask[w] = 0u;
+    for (int w = tid; w < CM_WORDS && w * 32 < rows; w += NTT) colmask[w] = 0u;
     __syncthreads();
-    for (int tr = tid; tr < rows; tr += TILE_NT_WIDE) {
+    for (int tr = tid; tr < rows; tr += NTT) {
       const bool dn = (float)g.tilework[(size_t)tr * g.tile_cols + tp] >= dthr;
       mine |= dn;
       if (dn && tr < CM_WORDS * 32) atomicOr(&colmask[tr >> 5], 1u << (tr & 31));
@@ -967,11 +967,11 @@ static cudaError_t launch_tiles_k(const Geom &g, int num_sms, cudaStream_t s) {
   return launch_tiles_nt<MODE, TILE_NT>(gt, num_sms, &per_sm, s);
 }
 
-template <int NG, bool TIGHT, bool DB>
+template <int NG, bool TIGHT, bool DB, int NTT = TILE_NT_WIDE>
 static cudaError_t launch_tiles_grp(const Geom &g, int num_sms, cudaStream_t s) {
   cudaFuncAttributes fa{};
   int dev = 0, rsv = 0;
-  if (cudaFuncGetAttributes(&fa, k_advance_tiles_grp<NG, TIGHT, DB>) != cudaSuccess) fa.sharedSizeBytes = 4096;
+  if (cudaFuncGetAttributes(&fa, k_advance_tiles_grp<NG, TIGHT, DB, NTT>) != cudaSuccess) fa.sharedSizeBytes = 4096;
   if (cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev) != cudaSuccess)
     rsv = 1024;
@@ -980,9 +980,9 @@ static cudaError_t launch_tiles_grp(const Geom &g, int num_sms, cudaStream_t s) 
   const size_t gsz = (R * P * 7 + 15) & ~(size_t)15;
   const size_t rows0 = TIGHT ? base + NG * gsz : (base + NG * gsz + slot - 1) / slot * slot;
   const size_t smem = rows0 + ((DB ? 2 : 1) * NG * R + P) * (TIGHT ? (size_t)g.pitch : slot) - base;
-  cudaError_t e = cudaFuncSetAttribute(k_advance_tiles_grp<NG, TIGHT, DB>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(k_advance_tiles_grp<NG, TIGHT, DB, NTT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_advance_tiles_grp<NG, TIGHT, DB><<<num_sms, TILE_NT_WIDE, smem, s>>>(g);
+  k_advance_tiles_grp<NG, TIGHT, DB, NTT><<<num_sms, NTT, smem, s>>>(g);
   return cudaGetLastError();
 }
 
@@ -996,6 +996,7 @@ size_t tile_grp_smem_bytes(int groups, int lr, int lp, int64_t pitch, bool tight
 
 cudaError_t launch_advance_tiles(const Geom &g, int num_sms, cudaStream_t s) {
   if (g.tile_groups && !g.shared_draws && !g.wor) {
+    if (g.tile_groups == 8) return launch_tiles_grp<8, true, false, 512>(g, num_sms, s);
     if (g.tile_groups == 4) return launch_tiles_grp<4, false, false>(g, num_sms, s);
     if (g.tile_groups == 2 && g.tile_tight) return launch_tiles_grp<2, true, false>(g, num_sms, s);
     if (g.tile_groups == 2 && g.tile_db) return launch_tiles_grp<2, false, true>(g, num_sms, s);

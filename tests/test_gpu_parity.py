@@ -448,3 +448,14 @@ def test_grouped_tiles_two_groups(ak, db, monkeypatch):
     al = orc.alpha_experimental(4000, 0.05, 12288, 0.3)
     got, ref = _run_both(ak, X, Q, 4, 4, 45, al)
     _assert_parity(got, ref)
+
+
+def test_grouped_tiles_eight_groups(ak, monkeypatch):
+    """Eight 2-warp groups with rows at the pitch (AKNN_TILE_GROUPS = 8) against the oracle."""
+    monkeypatch.setenv("AKNN_TILE_GROUPS", "8")
+    monkeypatch.setenv("AKNN_TILE_F", "0.25")
+    for (n, d, q, seed) in ((4000, 12288, 9, 46), (777, 9000, 5, 47)):
+        X, Q = synth.small_instance(seed, n, d, q=q)
+        al = orc.alpha_experimental(n, 0.05, d, 0.3)
+        got, ref = _run_both(ak, X, Q, 4, 4, seed, al)
+        _assert_parity(got, ref)
