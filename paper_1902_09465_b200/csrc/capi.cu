@@ -310,10 +310,14 @@ TileShape tile_shape(int64_t pitch, int64_t n) {
   // fit with 2 groups of one query row (the query rows restaged per pair halve)
   // AKNN_TILE_GROUPS = 2 with AKNN_TILE_DB = 1: 2 groups of one query row, each double-
   // buffering its query rows (the next tile's copy overlaps this tile's draws)
-  const int ng = pitch > 8192 ? env_int("AKNN_TILE_GROUPS", 4) : 0;
+  const int ng0 = pitch > 8192 ? env_int("AKNN_TILE_GROUPS", 10) : 0;
+  // the default (10 groups at the pitch) needs 18 rows: narrower CTAs when it does not fit
+  const int ng = (ng0 == 10 && tile_grp_smem_bytes(10, 0, 3, pitch, true, false) > (size_t)227 * 1024)
+                     ? (tile_grp_smem_bytes(8, 0, 3, pitch, true, false) <= (size_t)227 * 1024 ? 8 : 4)
+                     : ng0;
   const int tight = env_int("AKNN_TILE_TIGHT", 0), db = env_int("AKNN_TILE_DB", 1);
-  if (ng == 8 && tile_grp_smem_bytes(8, 0, 3, pitch, true, false) <= (size_t)227 * 1024) {
-    t.groups = 8;  // 8 groups of 2 warps, rows at the pitch (16 rows of 12 KB)
+  if ((ng == 8 || ng == 10 || ng == 24) && tile_grp_smem_bytes(ng == 24 ? 8 : ng, 0, 3, pitch, true, false) <= (size_t)227 * 1024) {
+    t.groups = ng;  // 8 / 10 groups of 2 warps (24: 8 groups of 3 warps), rows at the pitch
     t.tight = 1;
     t.lr = 0;
     t.lp = 3;
@@ -338,10 +342,11 @@ TileShape tile_shape(int64_t pitch, int64_t n) {
   // X in L2 (C2: 47 MB): a list draw costs one L2 sector, tiles must amortise their
   // staging over >= 4 sectors' worth of draws; X in HBM (C3-C5): a list draw is a
   // random HBM sector (~1/15 the Philox rate): F = 1 on C4 (F = 0.25 / 1 / 4: 101.0 /
-  // 100.0 / 100.4 ms), 0.5 with the grouped tiles of rows > 8 KB (C3: -2 %)
+  // 100.0 / 100.4 ms), 0.25 with the grouped tiles of rows > 8 KB (C3, 8 groups: 277.6
+  // / 279.2 / 290.9 ms at F = 0.25 / 0.5 / 1)
   const char *fe = getenv("AKNN_TILE_F");
   const bool x_in_l2 = (double)n * (double)pitch <= 100e6;
-  const double f = fe && fe[0] ? atof(fe) : (x_in_l2 ? 4.0 : (pitch > 8192 ? 0.5 : 1.0));
+  const double f = fe && fe[0] ? atof(fe) : (x_in_l2 ? 4.0 : (pitch > 8192 ? 0.25 : 1.0));
   t.row_draws = (float)(f * (double)pitch / 32.0);
   t.on = 1;
   return t;
