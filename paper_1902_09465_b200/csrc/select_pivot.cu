@@ -215,8 +215,17 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
           const unsigned p = atomicAdd(&cnt, 1u);
           if (p < PIV_CAP) buf[p] = arm_key(S, (uint8_t)l, (uint32_t)i, g);
         } else if (!(__fmaf_rn((float)S, v.invT, v.nae) > boundf)) {  // could be the arg-min
-          const RecBest c{lower_of(S, (uint8_t)l, g.d, g.alpha, g.growth), gid, S, (uint8_t)l};
-          if (better_min(c, bl)) bl = c;
+          // at the level of the thread's best so far, L = fl(fl(S / (65025 T)) - alpha) is
+          // strictly increasing in S (distinct S give estimates many ulps apart, reading R9),
+          // so the integer order (S, id) decides and the fp64 division runs only for an
+          // improvement; in lock-step rounds nearly every candidate is at that level
+          if (bl.gid != 0xffffffffu && (uint8_t)l == bl.lvl) {
+            if (S < bl.S || (S == bl.S && gid < bl.gid))
+              bl = RecBest{lower_of(S, (uint8_t)l, g.d, g.alpha, g.growth), gid, S, (uint8_t)l};
+          } else {
+            const RecBest c{lower_of(S, (uint8_t)l, g.d, g.alpha, g.growth), gid, S, (uint8_t)l};
+            if (better_min(c, bl)) bl = c;
+          }
         }
       }
     }
