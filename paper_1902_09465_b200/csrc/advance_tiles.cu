@@ -995,7 +995,7 @@ size_t tile_grp_smem_bytes(int groups, int lr, int lp, int64_t pitch, bool tight
 }
 
 cudaError_t launch_advance_tiles(const Geom &g, int num_sms, cudaStream_t s) {
-  if (g.tile_groups && !g.shared_draws && !g.wor) {
+  if (g.tile_groups && !g.wor && !(g.shared_draws && g.tile_lr == 5)) {
     if (g.tile_groups == 8) return launch_tiles_grp<8, true, false, 512>(g, num_sms, s);
     if (g.tile_groups == 10) return launch_tiles_grp<10, true, false, 640>(g, num_sms, s);
     if (g.tile_groups == 24) return launch_tiles_grp<8, true, false, 768>(g, num_sms, s);  // 8 groups of 3 warps

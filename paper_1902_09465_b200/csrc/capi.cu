@@ -365,7 +365,8 @@ void setup_tiles(Geom &g, const TileShape &t, const aknn_opts &o, int64_t qb, ui
   if (!g.tile_on) return;
   g.tile_lr = t.lr;
   g.tile_lp = t.lp;
-  g.tile_groups = (o.flags & (AKNN_FLAG_SHARED_DRAWS | AKNN_FLAG_WITHOUT_REPLACEMENT)) ? 0 : t.groups;
+  // (shared draws run per-pair Philox with the shared counter word there: same kernel)
+  g.tile_groups = (o.flags & AKNN_FLAG_WITHOUT_REPLACEMENT) ? 0 : t.groups;
   g.tile_tight = t.tight;
   g.tile_db = t.db;
   g.tile_cols = (int)((g.npad + (1ll << t.lp) - 1) >> t.lp);

@@ -957,16 +957,24 @@ __global__ void __launch_bounds__(256) k_tally(Geom g) {
   __syncthreads();
   unsigned long long dr = 0, ex = 0, bl = 0, xe = 0;
   const uint8_t *lrow = g.lvl + (size_t)qi * g.npad;
-  for (int i = threadIdx.x; i < g.n; i += blockDim.x) {
-    const uint8_t l = lrow[i];
-    const uint32_t c = l & 0x7Fu;
-    dr += lvl_count(c, g.growth);
-    const bool fb = lvl_exact(l) && g.d > 1;
-    ex += fb ? 1u : 0u;
-    // charge of the fallback: d, or without replacement the d - 2^c coordinates the
-    // arm's permutation had not drawn yet (reading R23)
-    xe += fb ? (g.wor ? (unsigned long long)g.d - lvl_count(c, g.growth) : (unsigned long long)g.d) : 0ull;
-    bl += cumbl[c];
+  // 16 level bytes per load (npad is a multiple of 16; bytes past n are skipped)
+  for (int i0 = threadIdx.x * 16; i0 < g.n; i0 += blockDim.x * 16) {
+    const uint4 v = *reinterpret_cast<const uint4 *>(lrow + i0);
+    const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+    for (int e = 0; e < 16; ++e) {
+      if (i0 + e >= g.n) break;
+      const uint8_t l = (uint8_t)(w[e >> 2] >> (8 * (e & 3)));
+      const uint32_t c = l & 0x7Fu;
+      const unsigned long long T = lvl_count(c, g.growth);
+      dr += T;
+      const bool fb = lvl_exact(l) && g.d > 1;
+      ex += fb ? 1u : 0u;
+      // charge of the fallback: d, or without replacement the d - T_c coordinates the
+      // arm's permutation had not drawn yet (reading R23)
+      xe += fb ? (g.wor ? (unsigned long long)g.d - T : (unsigned long long)g.d) : 0ull;
+      bl += cumbl[c];
+    }
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

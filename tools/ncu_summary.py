@@ -37,18 +37,32 @@ def launches(path):
     hdr = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hdr]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    mi = h.index("Metric Name") if "Metric Name" in h else None
     tot, cnt = collections.defaultdict(float), collections.Counter()
+    dram = collections.defaultdict(float)
     for r in rows[hdr + 1:]:
         if len(r) <= vi:
             continue
-        us = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1.0)
         name = r[ki].split("(")[0].replace("void ", "")[:70]
+        metric = r[mi] if mi is not None else "gpu__time_duration.sum"
+        if metric.startswith("dram__bytes"):  # captured alongside: bytes per kernel
+            dram[name] += float(r[vi].replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6,
+                                                           "Gbyte": 1e9}.get(r[ui], 1.0)
+            continue
+        if metric != "gpu__time_duration.sum":
+            continue
+        us = float(r[vi].replace(",", "")) * SCALE.get(r[ui], 1.0)
         tot[name] += us
         cnt[name] += 1
     T = sum(tot.values())
-    out = ["| kernel | launches | total µs | share |", "|---|---:|---:|---:|"]
-    for k, v in sorted(tot.items(), key=lambda x: -x[1]):
-        out.append(f"| `{k}` | {cnt[k]} | {v:,.0f} | {100 * v / T:.1f}% |")
+    if dram:
+        out = ["| kernel | launches | total µs | share | DRAM MB |", "|---|---:|---:|---:|---:|"]
+        for k, v in sorted(tot.items(), key=lambda x: -x[1]):
+            out.append(f"| `{k}` | {cnt[k]} | {v:,.0f} | {100 * v / T:.1f}% | {dram[k] / 1e6:,.0f} |")
+    else:
+        out = ["| kernel | launches | total µs | share |", "|---|---:|---:|---:|"]
+        for k, v in sorted(tot.items(), key=lambda x: -x[1]):
+            out.append(f"| `{k}` | {cnt[k]} | {v:,.0f} | {100 * v / T:.1f}% |")
     return "\n".join(out)
 
 
