@@ -459,3 +459,16 @@ def test_grouped_tiles_eight_groups(ak, monkeypatch):
         al = orc.alpha_experimental(n, 0.05, d, 0.3)
         got, ref = _run_both(ak, X, Q, 4, 4, seed, al)
         _assert_parity(got, ref)
+
+
+def test_grouped_tiles_shared_draws(ak, monkeypatch):
+    """Query-independent draws through the grouped tiles (rows > 8 KB) against the oracle's
+    shared-draw mode."""
+    monkeypatch.setenv("AKNN_TILE_F", "0.25")
+    X, Q = synth.small_instance(48, 2100, 12288, q=6)
+    al = orc.alpha_experimental(2100, 0.05, 12288, 0.3)
+    ix = ak.Index(X)
+    got = ix.query(Q, 4, 4, 0.05, 48, al, counts=True, sums=True, flags=ak.FLAG_SHARED_DRAWS)
+    ix.close()
+    ref = orc.query_br(X, Q, 4, 4, 48, al, want_sums=True, shared_draws=True)
+    _assert_parity(got, ref)
