@@ -176,6 +176,7 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
   }
   __syncthreads();
   const uint32_t idt = (uint32_t)(tau & ((1ull << g.kbits) - 1ull));
+  const uint32_t lvt_s = (uint32_t)__cvta_generic_to_shared(lvt);
   const uint32_t gid0 = g.id_offset;
   const int32_t *Srow = g.S + (size_t)qi * g.npad;
   const uint8_t *Lrow = g.lvl + (size_t)qi * g.npad;
@@ -198,13 +199,18 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
     for (int u = 0; u < U; ++u) {
       const int i0 = b0 + u * PIV_NT * 4;
       const int32_t Sv[4] = {sg[u].x, sg[u].y, sg[u].z, sg[u].w};
+      const int ne = min(4, n - i0);  // arms of this group (<= 0 past the end)
 #pragma unroll
       for (int e = 0; e < 4; ++e) {
         const int i = i0 + e;
-        if (i >= n) break;
+        if (e >= ne) break;
         const uint32_t l = (lg[u] >> (8 * e)) & 0xFFu;
         const int32_t S = Sv[e];
-        const uint4 vv = reinterpret_cast<const uint4 *>(lvt)[(l & LVL_EXACT) ? MAX_LEVELS : l];
+        // the level's 16-byte entry (shared-window address hoisted out of the loop)
+        uint4 vv;
+        asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+            : "=r"(vv.x), "=r"(vv.y), "=r"(vv.z), "=r"(vv.w)
+            : "r"(lvt_s + 16u * ((l & LVL_EXACT) ? (uint32_t)MAX_LEVELS : l)));
         PivLevel v;
         v.lt = (int32_t)vv.x;
         v.eq = (int32_t)vv.y;
