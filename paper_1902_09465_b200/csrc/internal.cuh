@@ -22,6 +22,7 @@ constexpr uint8_t ACT_EXACT = 0xFE;
 // (reading R25); slot MAX_LEVELS = exact list.  Per-level bit masks are 32-bit.
 constexpr int MAX_LEVELS = 32;
 constexpr int NSLOT = MAX_LEVELS + 1;
+static_assert(NSLOT <= 64, "k_plan: one thread per slot, two warps");
 
 // Integer form of the blocker predicate of one query for a round (k_thresholds).
 // Per sampled level c, int4 {Su, Sl, Ck, Ckh}:

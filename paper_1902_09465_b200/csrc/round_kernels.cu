@@ -419,51 +419,78 @@ __host__ __device__ __forceinline__ unsigned pairs_per_chunk(int slot, unsigned 
   return nb <= (unsigned)ADV_P ? 32u * ADV_P / nb : 32u / lanes_per_pair(nb, bpl);
 }
 
+// One thread per slot (NSLOT <= 64): counts and warp-chunks per slot, then the prefix
+// sums across the two warps.
 __global__ void k_plan(RoundCtl *ctl, unsigned bpl, int stage_lo, int level_mma, unsigned level_min, int growth) {
-  if (threadIdx.x != 0) return;
-  if (level_mma) {  // shared draws: the most populated sampled level goes to the tensor cores
+  __shared__ unsigned wsum_c[2];
+  __shared__ unsigned long long wsum_ch[2];
+  const int s = threadIdx.x, lane = s & 31, w = s >> 5;
+  const unsigned c = s < NSLOT ? ctl->cnt[s] : 0u;
+  const unsigned ppc = s < NSLOT ? pairs_per_chunk(s, bpl, stage_lo, growth) : 1u;
+  const unsigned long long chs = (c + ppc - 1) / ppc;
+  unsigned ic = c;
+  unsigned long long ich = chs;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned a = __shfl_up_sync(FULL, ic, o);
+    const unsigned long long b = __shfl_up_sync(FULL, ich, o);
+    if (lane >= o) {
+      ic += a;
+      ich += b;
+    }
+  }
+  if (lane == 31) {
+    wsum_c[w] = ic;
+    wsum_ch[w] = ich;
+  }
+  __syncthreads();
+  const unsigned base_c = w ? wsum_c[0] : 0u;
+  const unsigned long long base_ch = w ? wsum_ch[0] : 0ull;
+  if (s < NSLOT) {
+    ctl->off[s] = base_c + ic - c;
+    ctl->chunk_off[s] = base_ch + ich - chs;
+    ctl->cursor[s] = 0;
+  }
+  if (s == 0) {
+    const unsigned tot = wsum_c[0] + wsum_c[1];
+    ctl->off[NSLOT] = tot;
+    ctl->chunk_off[NSLOT] = wsum_ch[0] + wsum_ch[1];
+    ctl->advanced += tot;
     int best = -1;
     unsigned bc = 0;
-    for (int s = 0; s < MAX_LEVELS; ++s)
-      if (ctl->cnt[s] > bc) {
-        bc = ctl->cnt[s];
-        best = s;
-      }
+    if (level_mma)  // shared draws: the most populated sampled level goes to the tensor cores
+      for (int t = 0; t < MAX_LEVELS; ++t)
+        if (ctl->cnt[t] > bc) {
+          bc = ctl->cnt[t];
+          best = t;
+        }
     ctl->gemm_level = (best >= 0 && bc >= level_min) ? best : -1;
-  } else {
-    ctl->gemm_level = -1;
   }
-  unsigned off = 0;
-  unsigned long long ch = 0, adv = 0;
-  for (int s = 0; s < NSLOT; ++s) {
-    const unsigned c = ctl->cnt[s];
-    ctl->off[s] = off;
-    ctl->chunk_off[s] = ch;
-    ctl->cursor[s] = 0;
-    off += c;
-    adv += c;
-    const unsigned ppc = pairs_per_chunk(s, bpl, stage_lo, growth);
-    ch += (c + ppc - 1) / ppc;
-  }
-  ctl->off[NSLOT] = off;
-  ctl->chunk_off[NSLOT] = ch;
-  ctl->advanced += adv;
 }
 
 // After the scatter: the lists hold only the pairs of sparse tiles (and the exact
 // fallbacks of sparse tensor-core tiles), cursor[s] of them per slot; the advance
 // kernels walk exactly those.
 __global__ void k_plan_lists(RoundCtl *ctl, unsigned bpl, int stage_lo, int growth) {
-  if (threadIdx.x != 0) return;
-  unsigned long long ch = 0;
-  for (int s = 0; s < NSLOT; ++s) {
-    const unsigned c = ctl->cursor[s];
-    ctl->cnt[s] = c;
-    ctl->chunk_off[s] = ch;
-    const unsigned ppc = pairs_per_chunk(s, bpl, stage_lo, growth);
-    ch += (c + ppc - 1) / ppc;
+  __shared__ unsigned long long wsum_ch[2];
+  const int s = threadIdx.x, lane = s & 31, w = s >> 5;
+  const unsigned c = s < NSLOT ? ctl->cursor[s] : 0u;
+  const unsigned ppc = s < NSLOT ? pairs_per_chunk(s, bpl, stage_lo, growth) : 1u;
+  const unsigned long long chs = (c + ppc - 1) / ppc;
+  unsigned long long ich = chs;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const unsigned long long b = __shfl_up_sync(FULL, ich, o);
+    if (lane >= o) ich += b;
   }
-  ctl->chunk_off[NSLOT] = ch;
+  if (lane == 31) wsum_ch[w] = ich;
+  __syncthreads();
+  const unsigned long long base_ch = w ? wsum_ch[0] : 0ull;
+  if (s < NSLOT) {
+    ctl->cnt[s] = c;
+    ctl->chunk_off[s] = base_ch + ich - chs;
+  }
+  if (s == 0) ctl->chunk_off[NSLOT] = wsum_ch[0] + wsum_ch[1];
 }
 
 // a8: compaction of the action bytes into per-slot lists of (qi << ibits | i).
@@ -1070,13 +1097,13 @@ cudaError_t launch_filter(const Geom &g, cudaStream_t s) {
 }
 
 cudaError_t launch_compact(const Geom &g, cudaStream_t s) {
-  k_plan<<<1, 32, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo, g.level_mma, 1u << 16, g.growth);
+  k_plan<<<1, 64, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo, g.level_mma, 1u << 16, g.growth);
   if (g.level_mma) {
     const cudaError_t e = launch_build_w(g, s);
     if (e != cudaSuccess) return e;
   }
   k_scatter<<<dim3(g.q, cdiv(g.npad, FIL_NT * 4)), FIL_NT, 0, s>>>(g);
-  k_plan_lists<<<1, 32, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo, g.growth);  // the lists as written
+  k_plan_lists<<<1, 64, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo, g.growth);  // the lists as written
   return cudaGetLastError();
 }
 
