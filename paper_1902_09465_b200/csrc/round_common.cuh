@@ -10,16 +10,16 @@ namespace aknn {
 // (i0 % 4 == 0, rows padded to npad % 16 == 0, so the loads are aligned).
 struct Arm4 {
   int32_t S[4];
-  uint8_t l[4];
+  uint32_t lw;  // the 4 level bytes, packed: unpacked only where used, so a load issued
+                // ahead (k_filter's prefetch) is not waited on at the load site
+  __device__ __forceinline__ uint8_t l(int e) const { return (uint8_t)(lw >> (8 * e)); }
 };
 
 __device__ __forceinline__ Arm4 load_arm4(const Geom &g, int qi, int i0) {
   Arm4 a;
   const int4 s = *reinterpret_cast<const int4 *>(g.S + (size_t)qi * g.npad + i0);
-  const uint32_t lv = *reinterpret_cast<const uint32_t *>(g.lvl + (size_t)qi * g.npad + i0);
+  a.lw = *reinterpret_cast<const uint32_t *>(g.lvl + (size_t)qi * g.npad + i0);
   a.S[0] = s.x; a.S[1] = s.y; a.S[2] = s.z; a.S[3] = s.w;
-#pragma unroll
-  for (int e = 0; e < 4; ++e) a.l[e] = (uint8_t)(lv >> (8 * e));
   return a;
 }
 
@@ -35,7 +35,7 @@ struct ArmKeys {
     const Arm4 a = load_arm4(*g, qi, i0);
 #pragma unroll
     for (int e = 0; e < 4; ++e)
-      key[e] = (i0 + e < g->n) ? arm_key(a.S[e], a.l[e], (uint32_t)(i0 + e), *g) : KEY_INVALID;
+      key[e] = (i0 + e < g->n) ? arm_key(a.S[e], a.l(e), (uint32_t)(i0 + e), *g) : KEY_INVALID;
   }
 };
 

@@ -86,13 +86,13 @@ __global__ void __launch_bounds__(SEL_NT) k_select(Geom g, int nbits) {
     for (int e = 0; e < 4; ++e) {
       const int i = i0 + e;
       if (i >= g.n) break;
-      const unsigned long long key = arm_key(a.S[e], a.l[e], (uint32_t)i, g);
+      const unsigned long long key = arm_key(a.S[e], a.l(e), (uint32_t)i, g);
       if (key <= thk) {
-        const double U = __dadd_rn(dhat_of(a.S[e], a.l[e], g.d, g.growth), alpha_of(a.l[e], g.alpha, g.growth));
+        const double U = __dadd_rn(dhat_of(a.S[e], a.l(e), g.d, g.growth), alpha_of(a.l(e), g.alpha, g.growth));
         if (U > bu.v || (U == bu.v && i < bu.i)) bu = Best{U, i, 0.0};
       } else if (key > thkh) {
-        const double al = alpha_of(a.l[e], g.alpha, g.growth);
-        const double L = __dsub_rn(dhat_of(a.S[e], a.l[e], g.d, g.growth), al);
+        const double al = alpha_of(a.l(e), g.alpha, g.growth);
+        const double L = __dsub_rn(dhat_of(a.S[e], a.l(e), g.d, g.growth), al);
         if (L < bl.v || (L == bl.v && i < bl.i)) bl = Best{L, i, al};
       }
     }
@@ -144,6 +144,10 @@ __global__ void __launch_bounds__(SEL_NT) k_select(Geom g, int nbits) {
 // with a plain store.
 constexpr int FIL_NT = 256;
 constexpr int FIL_ROWS = 32;
+#ifndef AKNN_FIL_AHEAD
+#define AKNN_FIL_AHEAD 2
+#endif
+constexpr int FIL_AHEAD = AKNN_FIL_AHEAD;
 
 // The round's blocker predicate as integer thresholds (see THR_STRIDE): one warp per
 // undecided query, lane c bisects S in [0, 65025 * 2^c] with the very fp64 operations
@@ -205,7 +209,26 @@ cudaError_t launch_thresholds(const Geom &g, cudaStream_t s) {
 }
 
 // Branch-free decision of 4 arms (R5 with the integer thresholds of reading R20):
-// one 16-byte table load per arm, no 64-bit key arithmetic, no floating point.
+// one 16-byte table load per level (once for the 4 arms when they share it -- the
+// lock-step case), no 64-bit key arithmetic, no floating point.
+__device__ __forceinline__ uint32_t filter_arm(const Geom &g, const int4 &t, uint32_t c, uint8_t l, int32_t S, int i,
+                                               uint32_t mmask, uint32_t eqk, uint32_t eqkh, uint32_t idk,
+                                               uint32_t idkh, uint32_t *dr, uint32_t *lwb) {
+  const bool live = i < g.n && !lvl_exact(l);
+  bool inC = S < t.z, inM = S < t.w;
+  if ((S == t.z) | (S == t.w)) {  // rare: the id decides a tie with the k-th / (k+h)-th key
+    const uint32_t gid = (uint32_t)i + g.id_offset;
+    inC = inC || (((eqk >> c) & 1u) && S == t.z && gid <= idk);
+    inM = inM || (((eqkh >> c) & 1u) && S == t.w && gid <= idkh);
+  }
+  const bool blk = live && (inC ? S >= t.x : (inM ? ((mmask >> c) & 1u) != 0u : S < t.y));
+  // P:176 (reading R8): exact when the next count would reach d (bit c of g.exnext)
+  const bool ex = (g.exnext >> c) & 1u;
+  *dr += (blk && !ex) ? (1u << c) : 0u;  // tiles (doubling only): the advance draws T_c
+  *lwb = (blk && !ex && inM) ? 1u : 0u;  // inM: ranks 1..k+h (C or M)
+  return blk ? (ex ? (uint32_t)ACT_EXACT : c + 1u) : 0u;
+}
+
 __device__ __forceinline__ uint32_t filter_arms(const Geom &g, const int32_t *thr, const Arm4 &a, int i0,
                                                 uint32_t *draws, uint32_t *leadw) {
   uint32_t actw = 0, dr = 0, lw = 0;
@@ -214,27 +237,25 @@ __device__ __forceinline__ uint32_t filter_arms(const Geom &g, const int32_t *th
   const int4 hdr = *reinterpret_cast<const int4 *>(thr + ho);
   const uint32_t mmask = (uint32_t)hdr.x, eqk = (uint32_t)hdr.y, eqkh = (uint32_t)hdr.z;
   const uint32_t idk = (uint32_t)hdr.w, idkh = (uint32_t)thr[ho + 4];
+  const uint32_t c0 = a.l(0) & 31u;
+  if (a.lw == (uint32_t)a.l(0) * 0x01010101u) {  // one level for the 4 arms
+    const int4 t = reinterpret_cast<const int4 *>(thr)[c0];  // Su, Sl, Ck, Ckh
 #pragma unroll
-  for (int e = 0; e < 4; ++e) {
-    const int i = i0 + e;
-    const uint8_t l = a.l[e];
-    const uint32_t c = l & 31u;
-    const bool live = i < g.n && !lvl_exact(l);
-    const int4 t = reinterpret_cast<const int4 *>(thr)[c];  // Su, Sl, Ck, Ckh
-    const int32_t S = a.S[e];
-    bool inC = S < t.z, inM = S < t.w;
-    if ((S == t.z) | (S == t.w)) {  // rare: the id decides a tie with the k-th / (k+h)-th key
-      const uint32_t gid = (uint32_t)i + g.id_offset;
-      inC = inC || (((eqk >> c) & 1u) && S == t.z && gid <= idk);
-      inM = inM || (((eqkh >> c) & 1u) && S == t.w && gid <= idkh);
+    for (int e = 0; e < 4; ++e) {
+      uint32_t lb;
+      actw |= filter_arm(g, t, c0, a.l(0), a.S[e], i0 + e, mmask, eqk, eqkh, idk, idkh, &dr, &lb) << (8 * e);
+      lw |= lb << (8 * e);
     }
-    const bool blk = live && (inC ? S >= t.x : (inM ? ((mmask >> c) & 1u) != 0u : S < t.y));
-    // P:176 (reading R8): exact when the next count would reach d (bit c of g.exnext)
-    const bool ex = (g.exnext >> c) & 1u;
-    const uint32_t act = blk ? (ex ? (uint32_t)ACT_EXACT : c + 1u) : 0u;
-    dr += (blk && !ex) ? (1u << c) : 0u;  // tiles (doubling only): the advance draws T_c
-    actw |= act << (8 * e);
-    lw |= (blk && !ex && inM) ? (1u << (8 * e)) : 0u;  // inM: ranks 1..k+h (C or M)
+  } else {
+#pragma unroll
+    for (int e = 0; e < 4; ++e) {
+      const uint8_t l = a.l(e);
+      const uint32_t c = l & 31u;
+      const int4 t = reinterpret_cast<const int4 *>(thr)[c];
+      uint32_t lb;
+      actw |= filter_arm(g, t, c, l, a.S[e], i0 + e, mmask, eqk, eqkh, idk, idkh, &dr, &lb) << (8 * e);
+      lw |= lb << (8 * e);
+    }
   }
   *draws = dr;
   *leadw = lw;
@@ -247,7 +268,7 @@ __device__ __forceinline__ uint32_t lead_arms(const Geom &g, const Arm4 &a, uint
   uint32_t actw = 0, dr = 0;
 #pragma unroll
   for (int e = 0; e < 4; ++e) {
-    const uint8_t l = a.l[e];
+    const uint8_t l = a.l(e);
     const uint32_t c = l & 31u;
     const bool go = i0 + e < g.n && ((lb >> (8 * e)) & 0xFFu) && !lvl_exact(l);
     const bool ex = (g.exnext >> c) & 1u;
@@ -263,14 +284,14 @@ __device__ __forceinline__ uint32_t lead_arms(const Geom &g, const Arm4 &a, uint
 // only when the slot changes (under lockstep levels: almost never).
 struct SlotRun {
   unsigned slot = NONE, n = 0;
-  __device__ __forceinline__ void add(unsigned s, unsigned *scnt) {
+  __device__ __forceinline__ void add(unsigned s, unsigned *scnt, unsigned k = 1) {
     if (s == slot) {
-      ++n;
+      n += k;
       return;
     }
     if (slot != NONE && n) atomicAdd(&scnt[slot], n);
     slot = s;
-    n = 1;
+    n = k;
   }
   __device__ __forceinline__ void flush(unsigned *scnt) {
     if (slot != NONE && n) atomicAdd(&scnt[slot], n);
@@ -306,12 +327,21 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
       reinterpret_cast<int4 *>(sthr)[t] = __ldg(reinterpret_cast<const int4 *>(g.thr + (size_t)q0 * tstride) + t);
   __syncthreads();
   const bool arms = i0 < g.n;
-  // two rows of loads in flight ahead of the row being decided
-  int st0 = g.qs[q0].done, st1 = rows > 1 ? g.qs[q0 + 1].done : 1;
-  Arm4 a0{}, a1{};
-  if (arms) {
-    a0 = load_arm4(g, q0, i0);
-    if (rows > 1) a1 = load_arm4(g, q0 + 1, i0);
+  // the rows' done flags as one bit mask (read once: a per-row flag load was consumed
+  // at once -- as a uniform register -- and stalled every row on its latency)
+  uint32_t donem;
+  {
+    const int lane_r = lane;
+    const bool dflag = lane_r < rows ? g.qs[q0 + lane_r].done != 0 : true;
+    donem = __ballot_sync(FULL, dflag);
+  }
+  // FIL_AHEAD rows of arm loads in flight ahead of the row being decided (the pass is
+  // load-latency bound: 20 bytes per thread and row)
+  Arm4 aq[FIL_AHEAD];
+#pragma unroll
+  for (int j = 0; j < FIL_AHEAD; ++j) {
+    aq[j] = Arm4{};
+    if (arms && j < rows && !((donem >> j) & 1u)) aq[j] = load_arm4(g, q0 + j, i0);
   }
   SlotRun run, lrun;      // lrun: the thread's pairs per level in its 128 x 128 level tile
   unsigned ex_acc = 0;     // exact fallbacks of this thread (one 128-query tile row: 32 | 128)
@@ -320,15 +350,12 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
   int tr_cur = 0;
   for (int r = 0; r < rows; ++r) {
     const int qi = q0 + r;
-    const int cur = st0;
-    const Arm4 ca = a0;
-    st0 = st1;
-    a0 = a1;
-    if (r + 2 < rows) {  // prefetch the row after next
-      st1 = g.qs[qi + 2].done;
-      if (arms) a1 = load_arm4(g, qi + 2, i0);
-    }
-    if (cur) continue;  // uniform: one query row at a time
+    const Arm4 ca = aq[0];
+#pragma unroll
+    for (int j = 0; j + 1 < FIL_AHEAD; ++j) aq[j] = aq[j + 1];
+    if (r + FIL_AHEAD < rows && arms && !((donem >> (r + FIL_AHEAD)) & 1u))  // prefetch row r + FIL_AHEAD
+      aq[FIL_AHEAD - 1] = load_arm4(g, qi + FIL_AHEAD, i0);
+    if ((donem >> r) & 1u) continue;  // uniform: one query row at a time
     uint32_t dr = 0, actw = 0, lw = 0;
     if (MODE == 2) {
       if (arms) actw = lead_arms(g, ca, *reinterpret_cast<const uint32_t *>(g.leadb + (size_t)qi * g.npad + i0), i0, &dr);
@@ -338,17 +365,26 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
     }
     if (i0 < g.npad) *reinterpret_cast<uint32_t *>(g.act + (size_t)qi * g.npad + i0) = actw;
     rany |= (actw != 0u ? 1u : 0u) << r;
+    if (actw) {
+      const uint32_t a0 = actw & 0xFFu;
+      if (actw == a0 * 0x01010101u) {  // 4 equal actions (lock-step): one count update
+        ex_acc += a0 == ACT_EXACT ? 4u : 0u;
+        run.add(a0 == ACT_EXACT ? (unsigned)MAX_LEVELS : a0 - 1u, scnt, 4u);
+        if (g.level_mma && a0 != ACT_EXACT) lrun.add(a0 - 1u, lvc + ((threadIdx.x * 4) >> 7) * MAX_LEVELS, 4u);
+      } else {
 #pragma unroll
-    for (int e = 0; e < 4; ++e) {
-      const uint32_t act = (actw >> (8 * e)) & 0xFFu;
-      ex_acc += act == ACT_EXACT;
-      if (act) run.add(act == ACT_EXACT ? (unsigned)MAX_LEVELS : act - 1u, scnt);
-    }
-    if (g.level_mma) {
+        for (int e = 0; e < 4; ++e) {
+          const uint32_t act = (actw >> (8 * e)) & 0xFFu;
+          ex_acc += act == ACT_EXACT;
+          if (act) run.add(act == ACT_EXACT ? (unsigned)MAX_LEVELS : act - 1u, scnt);
+        }
+        if (g.level_mma) {
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const uint32_t act = (actw >> (8 * e)) & 0xFFu;
-        if (act && act != ACT_EXACT) lrun.add(act - 1u, lvc + ((threadIdx.x * 4) >> 7) * MAX_LEVELS);
+          for (int e = 0; e < 4; ++e) {
+            const uint32_t act = (actw >> (8 * e)) & 0xFFu;
+            if (act && act != ACT_EXACT) lrun.add(act - 1u, lvc + ((threadIdx.x * 4) >> 7) * MAX_LEVELS);
+          }
+        }
       }
     }
     if (g.tile_on) {
@@ -937,14 +973,14 @@ __global__ void __launch_bounds__(OUT_NT) k_output(Geom g, OutPtrs o) {
     for (int e = 0; e < 4; ++e) {
       const int i = i0 + e;
       if (i >= g.n) break;
-      const unsigned long long kk = arm_key(a.S[e], a.l[e], (uint32_t)i, g);
+      const unsigned long long kk = arm_key(a.S[e], a.l(e), (uint32_t)i, g);
       if (kk <= st.thr_kh) {
         const unsigned p = atomicAdd(&cnt, 1u);
         if (p < (unsigned)kh) {
           key[p] = kk;
           sv[p] = a.S[e];
           iv[p] = i;
-          lv[p] = a.l[e];
+          lv[p] = a.l(e);
         }
       }
     }

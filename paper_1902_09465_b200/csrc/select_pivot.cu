@@ -4,7 +4,7 @@
 // Only the k+h smallest composite keys matter (the split C | M | F).  Per undecided
 // query (one CTA):
 //   1. sample SS keys at fixed strided positions and take the (r_s+1)-th smallest as a
-//      pivot tau (r_s+1 = twice the expected sample rank of k+h, plus 4), found by
+//      pivot tau (r_s+1 = twice the expected sample rank of k+h, plus 10), found by
 //      r_s+1 rounds of block-wide arg-min over the samples held in registers;
 //   2. ONE pass over the n arms: keys <= tau go to a shared-memory buffer, and every
 //      other arm feeds a running arg-min of L = d_hat - alpha (ties: smaller id),
@@ -22,11 +22,19 @@
 #include "round_common.cuh"
 #include "select.cuh"
 
+
+#ifndef AKNN_PIV_WARPSEL
+#define AKNN_PIV_WARPSEL 1
+#endif
+#ifndef AKNN_PIV_B0F32
+#define AKNN_PIV_B0F32 1
+#endif
+
 namespace aknn {
 
-constexpr int PIV_NT = 512;
 constexpr unsigned PIV_CAP = 8192;    // buffer keys (64 KB of dynamic shared memory)
-constexpr unsigned PIV_BRUTE = 1536;  // buffers up to this size are ranked by counting
+constexpr unsigned PIV_BRUTE = 384;  // buffers up to this size are ranked by counting (O(c^2));
+                                     // larger ones by a bitonic sort (O(c log^2 c), a barrier per stage)
 
 __host__ __device__ __forceinline__ unsigned piv_sample_size(int n) {
   unsigned ss = 1024;  // >= n / 16 samples (capped): tau's rank, hence the buffer, stays small
@@ -66,12 +74,42 @@ __device__ void bitonic_keys(unsigned long long *buf, unsigned P) {
 struct PivLevel {
   int32_t lt, eq;  // key <= tau  <=>  S < lt  ||  (S == eq && gid <= id(tau))
   float invT, nae;  // 1 / (65025 T) and -(alpha + eps) in fp32
+  double Tm;        // 65025 T (the fast screen's threshold estimate)
+  double pad;
 };
+
+// The fast screen of the streaming pass for arms at level byte lc: every arm with
+// S > piv_hi(...) is neither a key <= tau (S >= lt and S != eq) nor through the fp32
+// screen (f(S) = fma((float)S, invT, nae) > boundf).  f is non-decreasing in S, so
+// checking f(sthr + 1) > boundf once proves it for every S > sthr; the fp64 estimate
+// of the crossing only has to be close (a bad estimate fails the check and the group
+// takes the per-arm path -- slower, never wrong).
+__device__ __forceinline__ int32_t piv_hi(uint32_t lvt_s, uint32_t lc, float boundf) {
+  const uint32_t a = lvt_s + 32u * ((lc & LVL_EXACT) ? (uint32_t)MAX_LEVELS : lc);
+  uint4 vv;
+  double Tm;
+  asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];" : "=r"(vv.x), "=r"(vv.y), "=r"(vv.z), "=r"(vv.w) : "r"(a));
+  asm("ld.shared.f64 %0, [%1];" : "=d"(Tm) : "r"(a + 16u));
+  const float invT = __uint_as_float(vv.z), nae = __uint_as_float(vv.w);
+  int32_t sthr = 0x7fffffff;
+  if (!(nae > boundf)) {  // else f(0) = nae > boundf: no arm passes (sthr = -1 below)
+    const double est = ((double)boundf - (double)nae) * Tm;
+    if (est < 1.0e9) {
+      const int32_t e = (int32_t)est;
+      const int32_t cand = e + 4 + (e >> 20);
+      if (__fmaf_rn((float)(cand + 1), invT, nae) > boundf) sthr = cand;
+    }
+  } else {
+    sthr = -1;
+  }
+  return max(max((int32_t)vv.x - 1, (int32_t)vv.y), sthr);
+}
 
 // Fills buf[0..cnt) with every key <= tau (unsorted) and rank[t] = the rank of buf[t]
 // among them (0-based; keys are unique), and returns the arg-min of L over the arms
 // with key > tau.  Returns false (and the caller falls back) when fewer than `need`
 // keys are <= tau or the buffer overflows.
+template <int PIV_NT>
 __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long long *buf, unsigned *rank,
                            unsigned *cnt_out, RecBest *outside, RecBest *wsm) {
   __shared__ unsigned cnt;
@@ -79,12 +117,31 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
   __shared__ unsigned long long wmin[PIV_NT / 32];
   __shared__ double wbnd[PIV_NT / 32];
   __shared__ double bound0_s;  // min L over the sampled arms with key > tau (screen start)
-  __shared__ __align__(16) PivLevel lvt[MAX_LEVELS + 1];
+  __shared__ __align__(32) PivLevel lvt[MAX_LEVELS + 1];
+  __shared__ unsigned long long wcand[PIV_NT];  // per-warp sample candidates (32 per warp)
   const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   const int n = g.n;
+  // the per-level table, fp32 screen part first (the sample phase uses it)
+  if (tid <= MAX_LEVELS) {
+    const bool ex = tid == MAX_LEVELS;  // slot MAX_LEVELS: exact arms (T = d, alpha = 0)
+    const bool live = !ex && tid <= g.cmax;
+    const double T = ex ? (double)g.d : (double)lvl_count((uint32_t)tid, g.growth);
+    const float alf = live ? (float)g.alpha[lvl_count((uint32_t)tid, g.growth)] : 0.f;
+    const float eps = (alf + 2.f) * 9.5367431640625e-07f;  // 2^-20
+    PivLevel v;
+    v.lt = 0;
+    v.eq = -1;
+    v.invT = (float)(1.0 / (T * 65025.0));
+    v.nae = -__fadd_ru(alf, eps);
+    v.Tm = T * 65025.0;
+    v.pad = 0.0;
+    lvt[tid] = v;
+  }
+  if (tid == 0) tau_s = KEY_INVALID;
+  __syncthreads();
   if (n > (int)PIV_CAP) {
-    // tau = the (rs+1)-th smallest of ss strided sample keys, rs+1 about twice the
-    // expected sample rank of need, plus 8: found by rs+1 rounds of block arg-min
+    // tau = the rounds-th smallest of ss strided sample keys, rounds about twice the
+    // expected sample rank of need, plus 10
     const unsigned ss = piv_sample_size(n);
     const unsigned per = ss / PIV_NT;  // <= 16 samples per thread
     unsigned long long mine[PIV_CAP / PIV_NT];
@@ -98,27 +155,18 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
         mine[u] = arm_key(g.S[o], g.lvl[o], (uint32_t)i, g);
       }
     }
+    // keys <= tau ~ (n / ss) Gamma(rounds): with rounds = 2 expect + 10 the buffer holds
+    // fewer than `need` keys with probability < 1e-9 at expect = 1 (C4: 0.82 sample ranks;
+    // 2 expect + 4 failed about once per 5,000 query-rounds, and the radix fallback of one
+    // query costs five times a whole pivot pass)
     const unsigned expect = (unsigned)(((unsigned long long)need * ss + n - 1) / n);
-    const unsigned rounds = 2 * expect + 4;
-    unsigned long long t = KEY_INVALID;
+    const unsigned rounds = 2 * expect + 10;
     // the thread's smallest remaining sample; only the owner of a round's minimum
-    // rescans its registers (keys are unique), so a round costs one warp reduction
+    // rescans its registers (keys are unique)
     unsigned long long head = KEY_INVALID;
 #pragma unroll
     for (unsigned u = 0; u < PIV_CAP / PIV_NT; ++u) head = mine[u] < head ? mine[u] : head;
-    for (unsigned r = 0; r < rounds; ++r) {
-      unsigned long long m = head;
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        const unsigned long long y = __shfl_xor_sync(FULL, m, o);
-        m = y < m ? y : m;
-      }
-      if (lane == 0) wmin[warp] = m;
-      __syncthreads();
-      m = wmin[0];
-#pragma unroll
-      for (int w = 1; w < PIV_NT / 32; ++w) m = wmin[w] < m ? wmin[w] : m;
-      t = m;
+    auto pop_min = [&](unsigned long long m) {
       if (head == m) {  // unique keys: exactly one owner
         head = KEY_INVALID;
 #pragma unroll
@@ -127,22 +175,95 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
           head = mine[u] < head ? mine[u] : head;
         }
       }
-      __syncthreads();
-    }
-    if (tid == 0) tau_s = t;
-    // the samples left in `mine` have keys > tau: they are arms outside the buffer, so
-    // their minimum L bounds the outside arg-min from above -- the screen starts there
-    // instead of at +inf (which sent the whole first stretch of arms to fp64)
-    double b = 1.0e300;
+    };
+    auto warp_min = [&](unsigned long long m) {
 #pragma unroll
-    for (unsigned u = 0; u < PIV_CAP / PIV_NT; ++u) {
-      if (u < per && mine[u] != KEY_INVALID) {
-        const unsigned j = tid + u * PIV_NT;
-        const int i = (int)(((unsigned long long)j * (unsigned)n) / ss);
-        const size_t o = (size_t)qi * g.npad + i;
-        b = fmin(b, lower_of(g.S[o], g.lvl[o], g.d, g.alpha, g.growth));
+      for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long y = __shfl_xor_sync(FULL, m, o);
+        m = y < m ? y : m;
+      }
+      return m;
+    };
+    if (AKNN_PIV_WARPSEL && rounds <= 32) {
+      // each warp pops its `rounds` smallest samples (no block barriers); the global
+      // rounds-th smallest is among them, and is the candidate with exactly rounds - 1
+      // smaller candidates
+      for (unsigned r = 0; r < rounds; ++r) {
+        const unsigned long long m = warp_min(head);
+        if (lane == 0) wcand[warp * 32 + r] = m;
+        pop_min(m);
+      }
+      __syncthreads();
+      const unsigned nc = (PIV_NT / 32) * 32;
+      for (unsigned t = tid; t < nc; t += PIV_NT) {
+        if ((t & 31u) >= rounds) continue;
+        const unsigned long long v = wcand[t];
+        if (v == KEY_INVALID) continue;
+        unsigned below = 0;
+        for (unsigned w = 0; w < PIV_NT / 32; ++w)
+          for (unsigned r = 0; r < rounds; ++r) below += wcand[w * 32 + r] < v;
+        if (below == rounds - 1) tau_s = v;
+      }
+    } else {  // rounds of block arg-min
+      unsigned long long t = KEY_INVALID;
+      for (unsigned r = 0; r < rounds; ++r) {
+        unsigned long long m = warp_min(head);
+        if (lane == 0) wmin[warp] = m;
+        __syncthreads();
+        m = wmin[0];
+#pragma unroll
+        for (int w = 1; w < PIV_NT / 32; ++w) m = wmin[w] < m ? wmin[w] : m;
+        t = m;
+        pop_min(m);
+        __syncthreads();
+      }
+      if (tid == 0) tau_s = t;
+    }
+    __syncthreads();
+    // samples with keys > tau are arms outside the buffer, so the L of any of them bounds
+    // the outside arg-min from above -- the screen starts there instead of at +inf
+    // (which sent the whole first stretch of arms to fp64).  The thread's candidate is its
+    // sample with the smallest fp32 screen value; one exact fp64 L per thread.
+    const unsigned long long tau0 = tau_s;
+    float rb = __int_as_float(0x7f800000);
+    int32_t Sb = 0;
+    uint8_t lb = 0;
+    uint32_t left = 0;
+#pragma unroll
+    for (unsigned u = 0; u < PIV_CAP / PIV_NT; ++u)
+      left |= (uint32_t)(u < per && mine[u] != KEY_INVALID && mine[u] > tau0) << u;
+    while (left) {
+      const unsigned u = (unsigned)__ffs(left) - 1;
+      left &= left - 1;
+      const unsigned j = tid + u * PIV_NT;
+      const int i = (int)(((unsigned long long)j * (unsigned)n) / ss);
+      const size_t o = (size_t)qi * g.npad + i;
+      const int32_t S = g.S[o];
+      const uint8_t l = g.lvl[o];
+      const PivLevel &v = lvt[(l & LVL_EXACT) ? MAX_LEVELS : l];
+      const float r = __fmaf_rn((float)S, v.invT, v.nae);
+      if (r < rb) {
+        rb = r;
+        Sb = S;
+        lb = l;
       }
     }
+    double b = rb < __int_as_float(0x7f800000) ? lower_of(Sb, lb, g.d, g.alpha, g.growth) : 1.0e300;
+#if !AKNN_PIV_B0F32
+    b = 1.0e300;
+    left = 0;
+#pragma unroll
+    for (unsigned u = 0; u < PIV_CAP / PIV_NT; ++u)
+      left |= (uint32_t)(u < per && mine[u] != KEY_INVALID && mine[u] > tau0) << u;
+    while (left) {
+      const unsigned u = (unsigned)__ffs(left) - 1;
+      left &= left - 1;
+      const unsigned j = tid + u * PIV_NT;
+      const int i = (int)(((unsigned long long)j * (unsigned)n) / ss);
+      const size_t o = (size_t)qi * g.npad + i;
+      b = fmin(b, lower_of(g.S[o], g.lvl[o], g.d, g.alpha, g.growth));
+    }
+#endif
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) b = fmin(b, __shfl_xor_sync(FULL, b, o));
     if (lane == 0) wbnd[warp] = b;
@@ -158,21 +279,14 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
   if (tid == 0) cnt = 0;
   __syncthreads();
   const unsigned long long tau = tau_s;
-  if (tid <= MAX_LEVELS) {
-    const bool ex = tid == MAX_LEVELS;  // slot MAX_LEVELS: exact arms (T = d, alpha = 0)
+  if (tid <= MAX_LEVELS) {  // the integer key <= tau tests
+    const bool ex = tid == MAX_LEVELS;
     const bool live = !ex && tid <= g.cmax;
-    const double T = ex ? (double)g.d : (double)lvl_count((uint32_t)tid, g.growth);
     const unsigned long long mul = ex ? g.Ld : (live ? lvl_mul((uint32_t)tid, g.L, g.L3, g.growth) : 1ull),
                              Kt = tau >> g.kbits;
     const unsigned long long qt = Kt / mul, rt = Kt % mul, lt = qt + (rt != 0);
-    const float alf = live ? (float)g.alpha[lvl_count((uint32_t)tid, g.growth)] : 0.f;
-    const float eps = (alf + 2.f) * 9.5367431640625e-07f;  // 2^-20
-    PivLevel v;
-    v.lt = lt > 0x7fffffffull ? 0x7fffffff : (int32_t)lt;
-    v.eq = (rt == 0 && qt <= 0x7fffffffull) ? (int32_t)qt : -1;
-    v.invT = (float)(1.0 / (T * 65025.0));
-    v.nae = -__fadd_ru(alf, eps);
-    lvt[tid] = v;
+    lvt[tid].lt = lt > 0x7fffffffull ? 0x7fffffff : (int32_t)lt;
+    lvt[tid].eq = (rt == 0 && qt <= 0x7fffffffull) ? (int32_t)qt : -1;
   }
   __syncthreads();
   const uint32_t idt = (uint32_t)(tau & ((1ull << g.kbits) - 1ull));
@@ -190,55 +304,84 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i0 = b0 + u * PIV_NT * 4;
+      sg[u] = make_int4(0, 0, 0, 0);
+      lg[u] = 0;
       if (i0 < n) {
         sg[u] = *reinterpret_cast<const int4 *>(Srow + i0);
         lg[u] = *reinterpret_cast<const uint32_t *>(Lrow + i0);
       }
     }
+    // fast screen: a full group of 4 arms at the thread's common level whose S all
+    // exceed piv_hi is decided (outside, not the arg-min) by 5 integer compares; in
+    // lock-step rounds that is nearly every group
+    const uint32_t lc = lg[0] & 0xFFu;
+    const int32_t hi = piv_hi(lvt_s, lc, boundf);
+    const uint32_t l4 = lc * 0x01010101u;
+    uint32_t slow = 0;
 #pragma unroll
     for (int u = 0; u < U; ++u) {
       const int i0 = b0 + u * PIV_NT * 4;
-      const int32_t Sv[4] = {sg[u].x, sg[u].y, sg[u].z, sg[u].w};
-      const int ne = min(4, n - i0);  // arms of this group (<= 0 past the end)
+      const bool quiet = i0 + 4 <= n && lg[u] == l4 && min(min(sg[u].x, sg[u].y), min(sg[u].z, sg[u].w)) > hi;
+      slow |= (uint32_t)(!quiet && i0 < n) << u;
+    }
+    if (slow) {
+      // per-arm classification of the other groups: `inb` key <= tau, `cand` outside
+      // and through the fp32 screen (bit u*4+e); their handling (64-bit keys, the fp64
+      // division) runs below from one call site each, re-reading the arm from L1
+      uint32_t inb = 0, cand = 0;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const int i = i0 + e;
-        if (e >= ne) break;
-        const uint32_t l = (lg[u] >> (8 * e)) & 0xFFu;
-        const int32_t S = Sv[e];
-        // the level's 16-byte entry (shared-window address hoisted out of the loop)
-        uint4 vv;
-        asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
-            : "=r"(vv.x), "=r"(vv.y), "=r"(vv.z), "=r"(vv.w)
-            : "r"(lvt_s + 16u * ((l & LVL_EXACT) ? (uint32_t)MAX_LEVELS : l)));
-        PivLevel v;
-        v.lt = (int32_t)vv.x;
-        v.eq = (int32_t)vv.y;
-        v.invT = __uint_as_float(vv.z);
-        v.nae = __uint_as_float(vv.w);
-        const uint32_t gid = (uint32_t)i + gid0;
-        if (S < v.lt || (S == v.eq && gid <= idt)) {  // key <= tau
-          const unsigned p = atomicAdd(&cnt, 1u);
-          if (p < PIV_CAP) buf[p] = arm_key(S, (uint8_t)l, (uint32_t)i, g);
-        } else if (!(__fmaf_rn((float)S, v.invT, v.nae) > boundf)) {  // could be the arg-min
-          // at the level of the thread's best so far, L = fl(fl(S / (65025 T)) - alpha) is
-          // strictly increasing in S (distinct S give estimates many ulps apart, reading R9),
-          // so the integer order (S, id) decides and the fp64 division runs only for an
-          // improvement; in lock-step rounds nearly every candidate is at that level
-          if (bl.gid != 0xffffffffu && (uint8_t)l == bl.lvl) {
-            if (S < bl.S || (S == bl.S && gid < bl.gid))
-              bl = RecBest{lower_of(S, (uint8_t)l, g.d, g.alpha, g.growth), gid, S, (uint8_t)l};
-          } else {
-            const RecBest c{lower_of(S, (uint8_t)l, g.d, g.alpha, g.growth), gid, S, (uint8_t)l};
-            if (better_min(c, bl)) bl = c;
+      for (int u = 0; u < U; ++u) {
+        if (!((slow >> u) & 1u)) continue;
+        const int i0 = b0 + u * PIV_NT * 4;
+        const int32_t Sv[4] = {sg[u].x, sg[u].y, sg[u].z, sg[u].w};
+        const int ne = min(4, n - i0);
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+          if (e < ne) {
+            const uint32_t l = (lg[u] >> (8 * e)) & 0xFFu;
+            const int32_t S = Sv[e];
+            uint4 vv;
+            asm("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                : "=r"(vv.x), "=r"(vv.y), "=r"(vv.z), "=r"(vv.w)
+                : "r"(lvt_s + 32u * ((l & LVL_EXACT) ? (uint32_t)MAX_LEVELS : l)));
+            const uint32_t gid = (uint32_t)(i0 + e) + gid0;
+            const bool in = S < (int32_t)vv.x || (S == (int32_t)vv.y && gid <= idt);  // key <= tau
+            const bool pass = !(__fmaf_rn((float)S, __uint_as_float(vv.z), __uint_as_float(vv.w)) > boundf);
+            inb |= (uint32_t)in << (u * 4 + e);
+            cand |= (uint32_t)(!in && pass) << (u * 4 + e);
           }
         }
       }
+      while (inb) {
+        const int j = __ffs(inb) - 1;
+        inb &= inb - 1;
+        const int i = b0 + (j >> 2) * PIV_NT * 4 + (j & 3);
+        const unsigned p = atomicAdd(&cnt, 1u);
+        if (p < PIV_CAP) buf[p] = arm_key(Srow[i], Lrow[i], (uint32_t)i, g);
+      }
+      while (cand) {  // could be the arg-min of L
+        const int j = __ffs(cand) - 1;
+        cand &= cand - 1;
+        const int i = b0 + (j >> 2) * PIV_NT * 4 + (j & 3);
+        const int32_t S = Srow[i];
+        const uint8_t l = Lrow[i];
+        const uint32_t gid = (uint32_t)i + gid0;
+        // at the level of the thread's best so far, L = fl(fl(S / (65025 T)) - alpha) is
+        // strictly increasing in S (distinct S give estimates many ulps apart, reading R9),
+        // so the integer order (S, id) decides and the fp64 division runs only for an
+        // improvement
+        const bool same = bl.gid != 0xffffffffu && l == bl.lvl;
+        if (same && !(S < bl.S || (S == bl.S && gid < bl.gid))) continue;
+        const RecBest c{lower_of(S, l, g.d, g.alpha, g.growth), gid, S, l};
+        if (same || better_min(c, bl)) bl = c;
+      }
     }
-    double wb = bl.v;  // share the warp's best: an arm above it cannot be the arg-min
+    // share the warp's best: an arm above it cannot be the arg-min (fp32, rounded up:
+    // the minimum of the rounded-up values is the rounded-up minimum)
+    float wb = __double2float_ru(bl.v);
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) wb = fmin(wb, __shfl_xor_sync(FULL, wb, o));
-    boundf = fminf(boundf, __double2float_ru(wb));
+    for (int o = 16; o > 0; o >>= 1) wb = fminf(wb, __shfl_xor_sync(FULL, wb, o));
+    boundf = fminf(boundf, wb);
   }
   __syncthreads();
   const unsigned c = cnt;
@@ -274,7 +417,8 @@ __device__ __forceinline__ RecBest rec_of_key(const Geom &g, int qi, unsigned lo
 }
 
 // Unsharded rank split + bounds + Eq. (5) (same contract as k_select).
-__global__ void __launch_bounds__(PIV_NT, 2) k_select_pivot(Geom g) {
+template <int PIV_NT>
+__global__ void __launch_bounds__(PIV_NT, 1024 / PIV_NT) k_select_pivot(Geom g) {
   extern __shared__ unsigned long long pbuf[];
   unsigned *prank = reinterpret_cast<unsigned *>(pbuf + PIV_CAP);
   __shared__ RecBest wsm[PIV_NT / 32];
@@ -285,7 +429,7 @@ __global__ void __launch_bounds__(PIV_NT, 2) k_select_pivot(Geom g) {
   const unsigned k = (unsigned)g.k, kh = (unsigned)(g.k + g.h);
   unsigned cnt;
   RecBest outside;
-  if (g.force_radix || !pivot_pass(g, qi, kh, pbuf, prank, &cnt, &outside, wsm)) {
+  if (g.force_radix || !pivot_pass<PIV_NT>(g, qi, kh, pbuf, prank, &cnt, &outside, wsm)) {
     if (threadIdx.x == 0) st->fallback = 1;
     return;
   }
@@ -322,7 +466,8 @@ __global__ void __launch_bounds__(PIV_NT, 2) k_select_pivot(Geom g) {
 
 // Sharded local summary (same contract as k_select_local): the local top-(k+h)
 // records and the remainder's minimum-L record.
-__global__ void __launch_bounds__(PIV_NT, 2) k_select_local_pivot(Geom g) {
+template <int PIV_NT>
+__global__ void __launch_bounds__(PIV_NT, 1024 / PIV_NT) k_select_local_pivot(Geom g) {
   extern __shared__ unsigned long long pbuf[];
   unsigned *prank = reinterpret_cast<unsigned *>(pbuf + PIV_CAP);
   __shared__ RecBest wsm[PIV_NT / 32];
@@ -332,7 +477,7 @@ __global__ void __launch_bounds__(PIV_NT, 2) k_select_local_pivot(Geom g) {
   const unsigned kh = (unsigned)(g.k + g.h);
   unsigned cnt;
   RecBest outside;
-  if (g.force_radix || !pivot_pass(g, qi, kh, pbuf, prank, &cnt, &outside, wsm)) {
+  if (g.force_radix || !pivot_pass<PIV_NT>(g, qi, kh, pbuf, prank, &cnt, &outside, wsm)) {
     if (threadIdx.x == 0) st->fallback = 1;
     return;
   }
@@ -369,21 +514,31 @@ __global__ void __launch_bounds__(PIV_NT, 2) k_select_local_pivot(Geom g) {
 
 size_t pivot_smem_bytes() { return (size_t)PIV_CAP * (sizeof(unsigned long long) + sizeof(unsigned)); }
 
-cudaError_t launch_select_pivot(const Geom &g, cudaStream_t s) {
+// One 512-thread CTA per query (two per SM); with at most one query per SM
+// (C4: q = 128) a 1,024-thread CTA instead, so that each SM has twice the arm loads
+// in flight (the pass is load-latency bound there: ncu long-scoreboard stalls).
+template <class K512, class K1024>
+static cudaError_t launch_piv(const Geom &g, cudaStream_t s, K512 k512, K1024 k1024) {
   const size_t smem = pivot_smem_bytes();
-  cudaError_t e = cudaFuncSetAttribute(k_select_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  const bool wide = g.q <= sms;
+  cudaError_t e = wide ? cudaFuncSetAttribute(k1024, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                       : cudaFuncSetAttribute(k512, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_select_pivot<<<g.q, PIV_NT, smem, s>>>(g);
+  if (wide)
+    k1024<<<g.q, 1024, smem, s>>>(g);
+  else
+    k512<<<g.q, 512, smem, s>>>(g);
   return cudaGetLastError();
 }
 
+cudaError_t launch_select_pivot(const Geom &g, cudaStream_t s) {
+  return launch_piv(g, s, k_select_pivot<512>, k_select_pivot<1024>);
+}
+
 cudaError_t launch_select_local_pivot(const Geom &g, cudaStream_t s) {
-  const size_t smem = pivot_smem_bytes();
-  cudaError_t e =
-      cudaFuncSetAttribute(k_select_local_pivot, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  k_select_local_pivot<<<g.q, PIV_NT, smem, s>>>(g);
-  return cudaGetLastError();
+  return launch_piv(g, s, k_select_local_pivot<512>, k_select_local_pivot<1024>);
 }
 
 }  // namespace aknn

@@ -44,18 +44,18 @@ __global__ void __launch_bounds__(SEL_NT) k_select_local(Geom g, int nbits) {
     for (int e = 0; e < 4; ++e) {
       const int i = i0 + e;
       if (i >= g.n) break;
-      const unsigned long long key = arm_key(a.S[e], a.l[e], (uint32_t)i, g);
+      const unsigned long long key = arm_key(a.S[e], a.l(e), (uint32_t)i, g);
       if (key <= th) {
         const unsigned p = atomicAdd(&cnt, 1u);
         ShardRec r;
         r.key = key;
         r.S = a.S[e];
-        r.lvl = a.l[e];
+        r.lvl = a.l(e);
         r.pad[0] = r.pad[1] = r.pad[2] = 0;
         out[p] = r;
       } else {
-        const RecBest c{lower_of(a.S[e], a.l[e], g.d, g.alpha, g.growth), (uint32_t)i + g.id_offset, a.S[e],
-                        a.l[e]};
+        const RecBest c{lower_of(a.S[e], a.l(e), g.d, g.alpha, g.growth), (uint32_t)i + g.id_offset, a.S[e],
+                        a.l(e)};
         if (better_min(c, bl)) bl = c;
       }
     }
