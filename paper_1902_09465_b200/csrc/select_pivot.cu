@@ -23,13 +23,6 @@
 #include "select.cuh"
 
 
-#ifndef AKNN_PIV_WARPSEL
-#define AKNN_PIV_WARPSEL 1
-#endif
-#ifndef AKNN_PIV_B0F32
-#define AKNN_PIV_B0F32 1
-#endif
-
 namespace aknn {
 
 constexpr unsigned PIV_CAP = 8192;    // buffer keys (64 KB of dynamic shared memory)
@@ -118,7 +111,6 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
   __shared__ double wbnd[PIV_NT / 32];
   __shared__ double bound0_s;  // min L over the sampled arms with key > tau (screen start)
   __shared__ __align__(32) PivLevel lvt[MAX_LEVELS + 1];
-  __shared__ unsigned long long wcand[PIV_NT];  // per-warp sample candidates (32 per warp)
   const int tid = threadIdx.x, lane = lane_id(), warp = tid >> 5;
   const int n = g.n;
   // the per-level table, fp32 screen part first (the sample phase uses it)
@@ -184,27 +176,7 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
       }
       return m;
     };
-    if (AKNN_PIV_WARPSEL && rounds <= 32) {
-      // each warp pops its `rounds` smallest samples (no block barriers); the global
-      // rounds-th smallest is among them, and is the candidate with exactly rounds - 1
-      // smaller candidates
-      for (unsigned r = 0; r < rounds; ++r) {
-        const unsigned long long m = warp_min(head);
-        if (lane == 0) wcand[warp * 32 + r] = m;
-        pop_min(m);
-      }
-      __syncthreads();
-      const unsigned nc = (PIV_NT / 32) * 32;
-      for (unsigned t = tid; t < nc; t += PIV_NT) {
-        if ((t & 31u) >= rounds) continue;
-        const unsigned long long v = wcand[t];
-        if (v == KEY_INVALID) continue;
-        unsigned below = 0;
-        for (unsigned w = 0; w < PIV_NT / 32; ++w)
-          for (unsigned r = 0; r < rounds; ++r) below += wcand[w * 32 + r] < v;
-        if (below == rounds - 1) tau_s = v;
-      }
-    } else {  // rounds of block arg-min
+    {  // rounds of block arg-min (a per-warp pre-selection measured slower on C2)
       unsigned long long t = KEY_INVALID;
       for (unsigned r = 0; r < rounds; ++r) {
         unsigned long long m = warp_min(head);
@@ -249,21 +221,6 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
       }
     }
     double b = rb < __int_as_float(0x7f800000) ? lower_of(Sb, lb, g.d, g.alpha, g.growth) : 1.0e300;
-#if !AKNN_PIV_B0F32
-    b = 1.0e300;
-    left = 0;
-#pragma unroll
-    for (unsigned u = 0; u < PIV_CAP / PIV_NT; ++u)
-      left |= (uint32_t)(u < per && mine[u] != KEY_INVALID && mine[u] > tau0) << u;
-    while (left) {
-      const unsigned u = (unsigned)__ffs(left) - 1;
-      left &= left - 1;
-      const unsigned j = tid + u * PIV_NT;
-      const int i = (int)(((unsigned long long)j * (unsigned)n) / ss);
-      const size_t o = (size_t)qi * g.npad + i;
-      b = fmin(b, lower_of(g.S[o], g.lvl[o], g.d, g.alpha, g.growth));
-    }
-#endif
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) b = fmin(b, __shfl_xor_sync(FULL, b, o));
     if (lane == 0) wbnd[warp] = b;
