@@ -194,33 +194,15 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
     __syncthreads();
     // samples with keys > tau are arms outside the buffer, so the L of any of them bounds
     // the outside arg-min from above -- the screen starts there instead of at +inf
-    // (which sent the whole first stretch of arms to fp64).  The thread's candidate is its
-    // sample with the smallest fp32 screen value; one exact fp64 L per thread.
-    const unsigned long long tau0 = tau_s;
-    float rb = __int_as_float(0x7f800000);
-    int32_t Sb = 0;
-    uint8_t lb = 0;
-    uint32_t left = 0;
-#pragma unroll
-    for (unsigned u = 0; u < PIV_CAP / PIV_NT; ++u)
-      left |= (uint32_t)(u < per && mine[u] != KEY_INVALID && mine[u] > tau0) << u;
-    while (left) {
-      const unsigned u = (unsigned)__ffs(left) - 1;
-      left &= left - 1;
-      const unsigned j = tid + u * PIV_NT;
-      const int i = (int)(((unsigned long long)j * (unsigned)n) / ss);
+    // (which sent the whole first stretch of arms to fp64).  The rounds popped exactly
+    // the samples with keys <= tau, so `head` is the thread's smallest outside sample:
+    // one exact fp64 L per thread (at one level, the smallest key is the smallest L).
+    double b = 1.0e300;
+    if (head != KEY_INVALID) {
+      const uint32_t i = (uint32_t)(head & ((1ull << g.kbits) - 1ull)) - g.id_offset;
       const size_t o = (size_t)qi * g.npad + i;
-      const int32_t S = g.S[o];
-      const uint8_t l = g.lvl[o];
-      const PivLevel &v = lvt[(l & LVL_EXACT) ? MAX_LEVELS : l];
-      const float r = __fmaf_rn((float)S, v.invT, v.nae);
-      if (r < rb) {
-        rb = r;
-        Sb = S;
-        lb = l;
-      }
+      b = lower_of(g.S[o], g.lvl[o], g.d, g.alpha, g.growth);
     }
-    double b = rb < __int_as_float(0x7f800000) ? lower_of(Sb, lb, g.d, g.alpha, g.growth) : 1.0e300;
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) b = fmin(b, __shfl_xor_sync(FULL, b, o));
     if (lane == 0) wbnd[warp] = b;
