@@ -22,9 +22,14 @@ namespace aknn {
 
 // ---------------------------------------------------------------------------
 // a2: initialisation -- S_i = (X[i][j] - x[j])^2 for j = Draw(i, 0), T_i = 1.
+// Grid (q, point chunks) when the chunk count fits grid.y: CTAs are issued query-fastest,
+// so the q draws into one chunk's point rows come close together and the rows stay in
+// L2 (one HBM read of X; query-major order streamed X's random sectors once per query:
+// C4: 4 GB of sectors).  PM = false: grid (chunks, q), when the chunks exceed grid.y.
+template <bool PM>
 __global__ void k_init(Geom g) {
-  const int qi = blockIdx.y;
-  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int qi = PM ? blockIdx.x : blockIdx.y;
+  const int i = (PM ? blockIdx.y : blockIdx.x) * blockDim.x + threadIdx.x;
   if (i >= g.npad) return;
   const size_t o = (size_t)qi * g.npad + i;
   if (i >= g.n) {
@@ -535,16 +540,25 @@ __global__ void k_plan_lists(RoundCtl *ctl, unsigned bpl, int stage_lo, int grow
 // (warp-aggregated), the CTA reserves one range per slot with ONE global atomic,
 // and writes its entries there: list order within a slot follows the arm order
 // of each warp, so the advance kernel reads S / level nearly sequentially.
-__global__ void __launch_bounds__(FIL_NT) k_scatter(Geom g) {
+// A CTA walks `cpb` consecutive 1,024-arm chunks of its query row (one CTA per chunk
+// spent most of the pass launching and retiring CTAs that exit at once: in lock-step
+// rounds nearly every chunk lies in dense tiles and lists nothing).  The list order
+// follows the CTA order -- the chunk's queries together -- so the list advance finds a
+// chunk's point rows in L2; cpb stays 1 when cpb chunks of rows would not fit there.
+__global__ void __launch_bounds__(FIL_NT) k_scatter(Geom g, int cpb) {
   const int qi = blockIdx.x;
-  // nothing to list in this row's chunk (k_filter's per-row action mask; finished
-  // queries have no actions): exit before the tile decisions
-  if (!((g.rowany[(size_t)(qi >> 5) * g.rowany_cols + blockIdx.y] >> (qi & 31)) & 1u)) return;
   __shared__ unsigned scnt[NSLOT], sbase[NSLOT];
   __shared__ uint8_t sdense[FIL_NT * 4 / 4];  // the chunk's (R x P) tiles: dense?
   __shared__ uint8_t smma[FIL_NT * 4 / 256];   // its 128 x 256 exact tiles: tensor cores?
   __shared__ int any_listed;
-  const int c0 = blockIdx.y * FIL_NT * 4;
+  __shared__ uint8_t slv[FIL_NT * 4 / 128];  // the chunk's 128 x 128 level tiles: tensor cores?
+  const int nch = (int)((g.npad + FIL_NT * 4 - 1) / (FIL_NT * 4));
+  for (int cy = blockIdx.y * cpb; cy < min(nch, (int)(blockIdx.y + 1) * cpb); ++cy) {
+  // nothing to list in this row's chunk (k_filter's per-row action mask; finished
+  // queries have no actions): skip it before the tile decisions (uniform over the CTA)
+  if (!((g.rowany[(size_t)(qi >> 5) * g.rowany_cols + cy] >> (qi & 31)) & 1u)) continue;
+  __syncthreads();  // the previous chunk's readers of the shared arrays are done
+  const int c0 = cy * FIL_NT * 4;
   const int ntile = g.tile_on ? (FIL_NT * 4) >> g.tile_lp : 0;
   for (int s = threadIdx.x; s < NSLOT; s += FIL_NT) scnt[s] = 0;
   if (threadIdx.x == 0) any_listed = 0;
@@ -560,7 +574,6 @@ __global__ void __launch_bounds__(FIL_NT) k_scatter(Geom g) {
     if (!dense) any_listed = 1;
   }
   if (!g.tile_on && !g.level_mma && threadIdx.x == 0) any_listed = 1;
-  __shared__ uint8_t slv[FIL_NT * 4 / 128];  // the chunk's 128 x 128 level tiles: tensor cores?
   const int glev = g.level_mma ? g.ctl->gemm_level : -1;
   if (g.level_mma && threadIdx.x < (FIL_NT * 4) / 128) {
     // a level tile lists nothing when all its sampled pairs sit at the GEMM level, the
@@ -587,7 +600,7 @@ __global__ void __launch_bounds__(FIL_NT) k_scatter(Geom g) {
     if (!g.exact_mma) any_listed = 1;
   }
   __syncthreads();
-  if (!any_listed) return;
+  if (!any_listed) continue;
   const int base_i = c0 + threadIdx.x;
   const uint8_t *arow = g.act + (size_t)qi * g.npad;
   const int lane = lane_id();
@@ -618,6 +631,7 @@ __global__ void __launch_bounds__(FIL_NT) k_scatter(Geom g) {
   for (int e = 0; e < 4; ++e)
     if (slot[e] != NONE)
       g.list[sbase[slot[e]] + loc[e]] = ((uint32_t)qi << g.ibits) | (uint32_t)(base_i + e * FIL_NT);
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1007,37 +1021,63 @@ __global__ void __launch_bounds__(OUT_NT) k_output(Geom g, OutPtrs o) {
 // an exact arm drew T_c before its fallback, which is charged d (d = 1: exact at
 // initialisation, no fallback).  Philox blocks of the level gathers: the advance out
 // of level l used nblk_of(l) (doubling: max(1, 2^(l-2))).
-__global__ void __launch_bounds__(256) k_tally(Geom g) {
+// Every statistic is a function of the arm's level byte alone, so the pass only counts
+// the arms per byte value (a per-thread run-length count: in lock-step rows a 4-byte
+// word of one level adds 4 at once; a shared histogram takes the runs), and 256 threads
+// then turn the histogram into the sums.  (Per-arm 64-bit sums over 16-byte loads left
+// the pass latency-bound: C4 1.8 ms per query batch.)
+template <int NT>
+__global__ void __launch_bounds__(NT) k_tally(Geom g) {
   const int qi = blockIdx.x;
-  __shared__ unsigned long long cumbl[MAX_LEVELS + 1];  // blocks to reach level c
-  if (threadIdx.x == 0) {
-    unsigned long long a = 0;
-    for (int c = 0; c <= MAX_LEVELS; ++c) {
-      cumbl[c] = a;
-      if (c < MAX_LEVELS) a += nblk_of(c, g.growth);
-    }
-  }
+  __shared__ unsigned hist[256];
+  __shared__ unsigned long long red[4][NT / 32];
+  for (int t = threadIdx.x; t < 256; t += NT) hist[t] = 0;
   __syncthreads();
-  unsigned long long dr = 0, ex = 0, bl = 0, xe = 0;
   const uint8_t *lrow = g.lvl + (size_t)qi * g.npad;
+  uint32_t cur = 0xFFFFFFFFu, run = 0;
+  auto add = [&](uint32_t b, uint32_t k) {
+    if (b == cur) {
+      run += k;
+      return;
+    }
+    if (run) atomicAdd(&hist[cur], run);
+    cur = b;
+    run = k;
+  };
   // 16 level bytes per load (npad is a multiple of 16; bytes past n are skipped)
-  for (int i0 = threadIdx.x * 16; i0 < g.n; i0 += blockDim.x * 16) {
+  for (int i0 = threadIdx.x * 16; i0 < g.n; i0 += NT * 16) {
     const uint4 v = *reinterpret_cast<const uint4 *>(lrow + i0);
     const uint32_t w[4] = {v.x, v.y, v.z, v.w};
 #pragma unroll
-    for (int e = 0; e < 16; ++e) {
-      if (i0 + e >= g.n) break;
-      const uint8_t l = (uint8_t)(w[e >> 2] >> (8 * (e & 3)));
-      const uint32_t c = l & 0x7Fu;
-      const unsigned long long T = lvl_count(c, g.growth);
-      dr += T;
-      const bool fb = lvl_exact(l) && g.d > 1;
-      ex += fb ? 1u : 0u;
-      // charge of the fallback: d, or without replacement the d - T_c coordinates the
-      // arm's permutation had not drawn yet (reading R23)
-      xe += fb ? (g.wor ? (unsigned long long)g.d - T : (unsigned long long)g.d) : 0ull;
-      bl += cumbl[c];
+    for (int q4 = 0; q4 < 4; ++q4) {
+      const int j0 = i0 + 4 * q4;
+      if (j0 + 4 <= g.n && w[q4] == (w[q4] & 0xFFu) * 0x01010101u) {
+        add(w[q4] & 0xFFu, 4u);
+      } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+          if (j0 + e < g.n) add((w[q4] >> (8 * e)) & 0xFFu, 1u);
+      }
     }
+  }
+  if (run) atomicAdd(&hist[cur], run);
+  __syncthreads();
+  unsigned long long dr = 0, ex = 0, bl = 0, xe = 0;
+  for (int b = threadIdx.x; b < 256; b += NT) {
+    const unsigned long long m = hist[b];
+    if (!m) continue;
+    const uint8_t l = (uint8_t)b;
+    const uint32_t c = l & 0x7Fu;
+    const unsigned long long T = lvl_count(c, g.growth);
+    unsigned long long cb = 0;  // Philox blocks drawn to reach level c
+    for (uint32_t c2 = 0; c2 < c && c2 < (uint32_t)MAX_LEVELS; ++c2) cb += nblk_of((int)c2, g.growth);
+    dr += m * T;
+    const bool fb = lvl_exact(l) && g.d > 1;
+    ex += fb ? m : 0ull;
+    // charge of the fallback: d, or without replacement the d - T_c coordinates the
+    // arm's permutation had not drawn yet (reading R23)
+    xe += fb ? m * (g.wor ? (unsigned long long)g.d - T : (unsigned long long)g.d) : 0ull;
+    bl += m * cb;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {
@@ -1046,7 +1086,6 @@ __global__ void __launch_bounds__(256) k_tally(Geom g) {
     bl += __shfl_xor_sync(FULL, bl, o);
     xe += __shfl_xor_sync(FULL, xe, o);
   }
-  __shared__ unsigned long long red[4][8];
   if (lane_id() == 0) {
     red[0][threadIdx.x >> 5] = dr;
     red[1][threadIdx.x >> 5] = ex;
@@ -1055,7 +1094,7 @@ __global__ void __launch_bounds__(256) k_tally(Geom g) {
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    for (int w = 1; w < 8; ++w) {
+    for (int w = 1; w < NT / 32; ++w) {
       dr += red[0][w];
       ex += red[1][w];
       bl += red[2][w];
@@ -1069,7 +1108,12 @@ __global__ void __launch_bounds__(256) k_tally(Geom g) {
 }
 
 cudaError_t launch_tally(const Geom &g, cudaStream_t s) {
-  k_tally<<<g.q, 256, 0, s>>>(g);
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  if (g.q <= sms)
+    k_tally<1024><<<g.q, 1024, 0, s>>>(g);
+  else
+    k_tally<256><<<g.q, 256, 0, s>>>(g);
   return cudaGetLastError();
 }
 
@@ -1089,7 +1133,11 @@ __global__ void k_counts(Geom g, OutPtrs o) {
 static inline unsigned cdiv(long long a, long long b) { return (unsigned)((a + b - 1) / b); }
 
 cudaError_t launch_init(const Geom &g, cudaStream_t s) {
-  k_init<<<dim3(cdiv(g.npad, 256), g.q), 256, 0, s>>>(g);
+  const long long nch = cdiv(g.npad, 256);
+  if (nch <= 65535)
+    k_init<true><<<dim3(g.q, (unsigned)nch), 256, 0, s>>>(g);
+  else
+    k_init<false><<<dim3((unsigned)nch, g.q), 256, 0, s>>>(g);
   k_init_qstate<<<cdiv(g.q, 128), 128, 0, s>>>(g);
   if (g.level_mma) {
     const cudaError_t e = launch_q2_planes(g, s);
@@ -1138,7 +1186,8 @@ cudaError_t launch_compact(const Geom &g, cudaStream_t s) {
     const cudaError_t e = launch_build_w(g, s);
     if (e != cudaSuccess) return e;
   }
-  k_scatter<<<dim3(g.q, cdiv(g.npad, FIL_NT * 4)), FIL_NT, 0, s>>>(g);
+  const int cpb = (long long)4 * FIL_NT * 4 * g.pitch <= (16ll << 20) ? 4 : 1;  // 4 chunks' rows <= 16 MB
+  k_scatter<<<dim3(g.q, cdiv(cdiv(g.npad, FIL_NT * 4), cpb)), FIL_NT, 0, s>>>(g, cpb);
   k_plan_lists<<<1, 64, 0, s>>>(g.ctl, g.adv_bpl, g.stage_lo, g.growth);  // the lists as written
   return cudaGetLastError();
 }
