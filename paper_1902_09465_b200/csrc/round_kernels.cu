@@ -243,13 +243,45 @@ __device__ __forceinline__ uint32_t filter_arms(const Geom &g, const int32_t *th
   const uint32_t mmask = (uint32_t)hdr.x, eqk = (uint32_t)hdr.y, eqkh = (uint32_t)hdr.z;
   const uint32_t idk = (uint32_t)hdr.w, idkh = (uint32_t)thr[ho + 4];
   const uint32_t c0 = a.l(0) & 31u;
-  if (a.lw == (uint32_t)a.l(0) * 0x01010101u) {  // one level for the 4 arms
+  if (a.lw == (uint32_t)a.l(0) * 0x01010101u) {  // one level for the 4 arms (lock-step)
+    // Away from the two rank thresholds the predicate is a union of S intervals:
+    //   S < Ck: C, blocker iff S >= Su;  Ck <= S < Ckh: M, iff mbit;  S >= Ckh: F, iff S < Sl
+    // so blk = S in [Su, Ck) or (mbit and S in [Ck, Ckh)) or S in [Ckh, Sl): three unsigned
+    // range tests per arm.  S equal to Ck or Ckh (the id decides the band) takes filter_arm.
     const int4 t = reinterpret_cast<const int4 *>(thr)[c0];  // Su, Sl, Ck, Ckh
+    const bool mb = (mmask >> c0) & 1u;
+    auto span = [](int32_t lo, int32_t hi) { return hi > lo ? (uint32_t)((int64_t)hi - (int64_t)lo) : 0u; };
+    const uint32_t l1 = span(t.x, t.z), l2 = mb ? span(t.z, t.w) : 0u, l3 = span(t.w, t.y);
+    uint32_t bm = 0, mm = 0, tie = 0;
 #pragma unroll
     for (int e = 0; e < 4; ++e) {
-      uint32_t lb;
-      actw |= filter_arm(g, t, c0, a.l(0), a.S[e], i0 + e, mmask, eqk, eqkh, idk, idkh, &dr, &lb) << (8 * e);
-      lw |= lb << (8 * e);
+      const int32_t S = a.S[e];
+      const bool b = ((uint32_t)S - (uint32_t)t.x < l1) | ((uint32_t)S - (uint32_t)t.z < l2) |
+                     ((uint32_t)S - (uint32_t)t.w < l3);
+      bm |= (uint32_t)b << e;
+      mm |= (uint32_t)(S < t.w) << e;  // ranks 1..k+h (C or M), away from the thresholds
+      tie |= (uint32_t)((S == t.z) | (S == t.w)) << e;
+    }
+    const int nlive = g.n - i0;  // arms past the end are never blockers
+    const uint32_t live = lvl_exact(a.l(0)) ? 0u : (nlive >= 4 ? 0xFu : (nlive > 0 ? (1u << nlive) - 1u : 0u));
+    bm &= live;
+    // P:176 (reading R8): exact when the next count would reach d (bit c of g.exnext)
+    const bool ex = (g.exnext >> c0) & 1u;
+    const uint32_t av = ex ? (uint32_t)ACT_EXACT : c0 + 1u;
+    actw = ((bm * 0x00204081u) & 0x01010101u) * av;  // bit e -> byte e
+    dr = ex ? 0u : (uint32_t)__popc(bm) << c0;       // tiles (doubling only): T_c draws each
+    lw = ex ? 0u : (((mm & bm) * 0x00204081u) & 0x01010101u);
+    if (tie) {  // rare: redo the arms at a threshold with the id rule
+#pragma unroll
+      for (int e = 0; e < 4; ++e) {
+        if (!((tie >> e) & 1u)) continue;
+        uint32_t d1 = 0, lb;
+        const uint32_t act = filter_arm(g, t, c0, a.l(0), a.S[e], i0 + e, mmask, eqk, eqkh, idk, idkh, &d1, &lb);
+        const uint32_t was = (actw >> (8 * e)) & 0xFFu;
+        actw = (actw & ~(0xFFu << (8 * e))) | (act << (8 * e));
+        lw = (lw & ~(0xFFu << (8 * e))) | (lb << (8 * e));
+        dr = dr - ((was && !ex) ? (1u << c0) : 0u) + d1;
+      }
     }
   } else {
 #pragma unroll
