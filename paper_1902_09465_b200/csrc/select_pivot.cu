@@ -25,13 +25,13 @@
 
 namespace aknn {
 
-constexpr unsigned PIV_CAP = 8192;    // buffer keys (64 KB of dynamic shared memory)
+constexpr unsigned PIV_CAP_MAX = 8192;  // buffer keys (64 KB of dynamic shared memory + ranks)
 constexpr unsigned PIV_BRUTE = 384;  // buffers up to this size are ranked by counting (O(c^2));
                                      // larger ones by a bitonic sort (O(c log^2 c), a barrier per stage)
 
-__host__ __device__ __forceinline__ unsigned piv_sample_size(int n) {
+__host__ __device__ __forceinline__ unsigned piv_sample_size(int n, unsigned cap) {
   unsigned ss = 1024;  // >= n / 16 samples (capped): tau's rank, hence the buffer, stays small
-  while (ss < PIV_CAP && (int)(ss * 16u) < n) ss <<= 1;
+  while (ss < cap && (int)(ss * 16u) < n) ss <<= 1;
   return ss;
 }
 
@@ -102,7 +102,7 @@ __device__ __forceinline__ int32_t piv_hi(uint32_t lvt_s, uint32_t lc, float bou
 // among them (0-based; keys are unique), and returns the arg-min of L over the arms
 // with key > tau.  Returns false (and the caller falls back) when fewer than `need`
 // keys are <= tau or the buffer overflows.
-template <int PIV_NT>
+template <int PIV_NT, unsigned PIV_CAP>
 __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long long *buf, unsigned *rank,
                            unsigned *cnt_out, RecBest *outside, RecBest *wsm) {
   __shared__ unsigned cnt;
@@ -134,7 +134,7 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
   if (n > (int)PIV_CAP) {
     // tau = the rounds-th smallest of ss strided sample keys, rounds about twice the
     // expected sample rank of need, plus 10
-    const unsigned ss = piv_sample_size(n);
+    const unsigned ss = piv_sample_size(n, PIV_CAP);
     const unsigned per = ss / PIV_NT;  // <= 16 samples per thread
     unsigned long long mine[PIV_CAP / PIV_NT];
 #pragma unroll
@@ -356,7 +356,7 @@ __device__ __forceinline__ RecBest rec_of_key(const Geom &g, int qi, unsigned lo
 }
 
 // Unsharded rank split + bounds + Eq. (5) (same contract as k_select).
-template <int PIV_NT>
+template <int PIV_NT, unsigned PIV_CAP>
 __global__ void __launch_bounds__(PIV_NT, 1024 / PIV_NT) k_select_pivot(Geom g) {
   extern __shared__ unsigned long long pbuf[];
   unsigned *prank = reinterpret_cast<unsigned *>(pbuf + PIV_CAP);
@@ -368,7 +368,7 @@ __global__ void __launch_bounds__(PIV_NT, 1024 / PIV_NT) k_select_pivot(Geom g) 
   const unsigned k = (unsigned)g.k, kh = (unsigned)(g.k + g.h);
   unsigned cnt;
   RecBest outside;
-  if (g.force_radix || !pivot_pass<PIV_NT>(g, qi, kh, pbuf, prank, &cnt, &outside, wsm)) {
+  if (g.force_radix || !pivot_pass<PIV_NT, PIV_CAP>(g, qi, kh, pbuf, prank, &cnt, &outside, wsm)) {
     if (threadIdx.x == 0) st->fallback = 1;
     return;
   }
@@ -405,7 +405,7 @@ __global__ void __launch_bounds__(PIV_NT, 1024 / PIV_NT) k_select_pivot(Geom g) 
 
 // Sharded local summary (same contract as k_select_local): the local top-(k+h)
 // records and the remainder's minimum-L record.
-template <int PIV_NT>
+template <int PIV_NT, unsigned PIV_CAP>
 __global__ void __launch_bounds__(PIV_NT, 1024 / PIV_NT) k_select_local_pivot(Geom g) {
   extern __shared__ unsigned long long pbuf[];
   unsigned *prank = reinterpret_cast<unsigned *>(pbuf + PIV_CAP);
@@ -416,7 +416,7 @@ __global__ void __launch_bounds__(PIV_NT, 1024 / PIV_NT) k_select_local_pivot(Ge
   const unsigned kh = (unsigned)(g.k + g.h);
   unsigned cnt;
   RecBest outside;
-  if (g.force_radix || !pivot_pass<PIV_NT>(g, qi, kh, pbuf, prank, &cnt, &outside, wsm)) {
+  if (g.force_radix || !pivot_pass<PIV_NT, PIV_CAP>(g, qi, kh, pbuf, prank, &cnt, &outside, wsm)) {
     if (threadIdx.x == 0) st->fallback = 1;
     return;
   }
@@ -451,33 +451,40 @@ __global__ void __launch_bounds__(PIV_NT, 1024 / PIV_NT) k_select_local_pivot(Ge
   }
 }
 
-size_t pivot_smem_bytes() { return (size_t)PIV_CAP * (sizeof(unsigned long long) + sizeof(unsigned)); }
+static size_t pivot_smem_bytes(unsigned cap) { return (size_t)cap * (sizeof(unsigned long long) + sizeof(unsigned)); }
 
-// One 512-thread CTA per query (two per SM); with at most one query per SM
-// (C4: q = 128) a 1,024-thread CTA instead, so that each SM has twice the arm loads
-// in flight (the pass is load-latency bound there: ncu long-scoreboard stalls).
-template <class K512, class K1024>
-static cudaError_t launch_piv(const Geom &g, cudaStream_t s, K512 k512, K1024 k1024) {
-  const size_t smem = pivot_smem_bytes();
+// One CTA per query: 512 threads (two CTAs per SM); with at most one query per SM
+// (C4: q = 128) 1,024 threads, so that each SM has twice the arm loads in flight (the
+// pass is load-latency bound there: ncu long-scoreboard stalls); for short rows (n <=
+// 65,536, C2) 256 threads with a 4,096-key buffer, four CTAs per SM, so the per-query
+// fixed phases (samples, arg-min rounds, ranking) of different queries overlap.
+template <class K256, class K512, class K1024>
+static cudaError_t launch_piv(const Geom &g, cudaStream_t s, K256 k256, K512 k512, K1024 k1024) {
   int dev = 0, sms = 148;
   if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
-  const bool wide = g.q <= sms;
-  cudaError_t e = wide ? cudaFuncSetAttribute(k1024, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
-                       : cudaFuncSetAttribute(k512, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int nt = g.q <= sms ? 1024 : (g.n <= 65536 ? 256 : 512);
+  const size_t smem = pivot_smem_bytes(nt == 256 ? 4096u : PIV_CAP_MAX);
+  cudaError_t e = nt == 1024 ? cudaFuncSetAttribute(k1024, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                  : nt == 512 ? cudaFuncSetAttribute(k512, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem)
+                              : cudaFuncSetAttribute(k256, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  if (wide)
+  if (nt == 1024)
     k1024<<<g.q, 1024, smem, s>>>(g);
-  else
+  else if (nt == 512)
     k512<<<g.q, 512, smem, s>>>(g);
+  else
+    k256<<<g.q, 256, smem, s>>>(g);
   return cudaGetLastError();
 }
 
 cudaError_t launch_select_pivot(const Geom &g, cudaStream_t s) {
-  return launch_piv(g, s, k_select_pivot<512>, k_select_pivot<1024>);
+  return launch_piv(g, s, k_select_pivot<256, 4096>, k_select_pivot<512, PIV_CAP_MAX>,
+                    k_select_pivot<1024, PIV_CAP_MAX>);
 }
 
 cudaError_t launch_select_local_pivot(const Geom &g, cudaStream_t s) {
-  return launch_piv(g, s, k_select_local_pivot<512>, k_select_local_pivot<1024>);
+  return launch_piv(g, s, k_select_local_pivot<256, 4096>, k_select_local_pivot<512, PIV_CAP_MAX>,
+                    k_select_local_pivot<1024, PIV_CAP_MAX>);
 }
 
 }  // namespace aknn
