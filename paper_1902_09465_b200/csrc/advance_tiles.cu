@@ -616,6 +616,7 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
         : "memory");
   };
   const int c0 = (int)((long long)blockIdx.x * cols / gridDim.x), c1 = (int)((long long)(blockIdx.x + 1) * cols / gridDim.x);
+  unsigned long long my_dr = 0, my_bl = 0;  // this group's draws / Philox blocks (gtid 0)
   for (int tp = c0; tp < c1; ++tp) {
     // the column's dense query tiles as a bit mask, read once (all groups are done with
     // the previous column); a column without one is skipped
@@ -712,7 +713,16 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
       const int4 S4 = cur.S4;
       const uint32_t A4 = cur.A4, L4 = cur.L4;
       const int dn = cur.dn;
-      gsync();  // lcnt cleared
+      // RP <= 128: the lcnt clear, the arms (4 per thread) and the scan all sit in warp 0,
+      // so its bookkeeping steps sync that warp only (the other warps meet it below)
+      const bool one_warp = RP <= 128;
+      auto bsync = [&] {
+        if (one_warp)
+          __syncwarp();
+        else
+          gsync();
+      };
+      bsync();  // lcnt cleared
       // only the warps holding arms (4 per thread, RP <= 4 GT) list them
       const bool arm_warp = (gtid & ~31) * 4 < RP;
       uint32_t act4 = 0;  // sampled actions only (exact fallbacks: tensor-core pass)
@@ -726,7 +736,7 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
         }
         if (in) *reinterpret_cast<uint32_t *>(sact + e4) = act4;
       }
-      gsync();  // lcnt
+      bsync();  // lcnt
       if (gtid < 32) {  // per-level offsets, the level mask and the statistics: one warp
         const unsigned v = gtid < MAX_LEVELS ? lcnt[grp][gtid] : 0u;
         unsigned x = v;
@@ -749,11 +759,11 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
         }
         if (gtid == 0) {
           lmask_s[grp] = lm;
-          if (dr) atomicAdd(&s_draws, dr);
-          if (bl) atomicAdd(&s_blocks, bl);
+          my_dr += dr;  // statistics: per group in a register, one shared atomic at the end
+          my_bl += bl;  // (64-bit shared atomics are CAS loops: once per tile cost ~1 %)
         }
       }
-      gsync();
+      bsync();
       if (arm_warp) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
@@ -864,6 +874,10 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
     }
     if (!have_x) wait_bar(pbar_s, pphase);  // a group without tiles in this column
     pphase ^= 1u;
+  }
+  if (gtid == 0) {
+    if (my_bl) atomicAdd(&s_blocks, my_bl);
+    if (my_dr) atomicAdd(&s_draws, my_dr);
   }
   __syncthreads();
   if (tid == 0 && s_blocks) atomicAdd(&g.ctl->tile_blocks, s_blocks);
