@@ -1012,6 +1012,7 @@ cudaError_t launch_advance_tiles(const Geom &g, int num_sms, cudaStream_t s) {
   if (g.tile_groups && !g.wor && !(g.shared_draws && g.tile_lr == 5)) {
     if (g.tile_groups == 8) return launch_tiles_grp<8, true, false, 512>(g, num_sms, s);
     if (g.tile_groups == 10) return launch_tiles_grp<10, true, false, 640>(g, num_sms, s);
+    if (g.tile_groups == 5) return launch_tiles_grp<5, true, false, 640>(g, num_sms, s);  // R = 2
     if (g.tile_groups == 24) return launch_tiles_grp<8, true, false, 768>(g, num_sms, s);  // 8 groups of 3 warps
     if (g.tile_groups == 4) return launch_tiles_grp<4, false, false>(g, num_sms, s);
     if (g.tile_groups == 2 && g.tile_tight) return launch_tiles_grp<2, true, false>(g, num_sms, s);

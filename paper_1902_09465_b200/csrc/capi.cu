@@ -304,8 +304,10 @@ TileShape tile_shape(int64_t pitch, int64_t n) {
   if (lr < 0) return t;
   t.lr = env_int("AKNN_TILE_LR", lr);
   t.lp = env_int("AKNN_TILE_LP", lp);
-  // rows wider than 8 KB: NG thread groups share the column's P = 8 point rows, each with
-  // R = 4 / NG query rows (AKNN_TILE_GROUPS = 0 / 2 / 4; default 4)
+  // rows wider than 8 KB: NG thread groups share the column's P = 8 point rows
+  // (AKNN_TILE_GROUPS: 10 = default, 2-warp groups of one query row at the pitch; 8; 24 =
+  // 8 groups of 3 warps; 5 = 4-warp groups of two query rows; 4 = power-of-two slots;
+  // 2; 0 = the classic kernel)
   // AKNN_TILE_TIGHT = 1: rows at the pitch (not in power-of-two slots), so 16 point rows
   // fit with 2 groups of one query row (the query rows restaged per pair halve)
   // AKNN_TILE_GROUPS = 2 with AKNN_TILE_DB = 1: 2 groups of one query row, each double-
@@ -320,6 +322,11 @@ TileShape tile_shape(int64_t pitch, int64_t n) {
     t.groups = ng;  // 8 / 10 groups of 2 warps (24: 8 groups of 3 warps), rows at the pitch
     t.tight = 1;
     t.lr = 0;
+    t.lp = 3;
+  } else if (ng == 5 && tile_grp_smem_bytes(5, 1, 3, pitch, true, false) <= (size_t)227 * 1024) {
+    t.groups = 5;  // 5 groups of 4 warps, each on two query rows (R = 2) at the pitch
+    t.tight = 1;
+    t.lr = 1;
     t.lp = 3;
   } else if (ng == 2 && tight && tile_grp_smem_bytes(2, 0, 4, pitch, true, false) <= (size_t)227 * 1024) {
     t.groups = 2;

@@ -3,7 +3,7 @@
 //
 // Only the k+h smallest composite keys matter (the split C | M | F).  Per undecided
 // query (one CTA):
-//   1. sample SS keys at fixed strided positions and take the (r_s+1)-th smallest as a
+//   1. sample SS keys (evenly spaced runs of 8 consecutive arms) and take the (r_s+1)-th smallest as a
 //      pivot tau (r_s+1 = twice the expected sample rank of k+h, plus 10), found by
 //      r_s+1 rounds of block-wide arg-min over the samples held in registers;
 //   2. ONE pass over the n arms: keys <= tau go to a shared-memory buffer, and every
@@ -132,19 +132,25 @@ __device__ bool pivot_pass(const Geom &g, int qi, unsigned need, unsigned long l
   if (tid == 0) tau_s = KEY_INVALID;
   __syncthreads();
   if (n > (int)PIV_CAP) {
-    // tau = the rounds-th smallest of ss strided sample keys, rounds about twice the
-    // expected sample rank of need, plus 10
+    // tau = the rounds-th smallest of ss sample keys, rounds about twice the expected
+    // sample rank of need, plus 10.  The samples are ss / 8 evenly spaced runs of 8
+    // consecutive arms (one 32-byte sector of S): single strided arms cost a sector of S
+    // and of the level bytes each, and those sectors did not survive in L2 until the
+    // streaming pass (ncu C2: 604 MB of DRAM reads for 300 MB of arm state)
     const unsigned ss = piv_sample_size(n, PIV_CAP);
     const unsigned per = ss / PIV_NT;  // <= 16 samples per thread
+    const unsigned nruns = ss / 8u;
     unsigned long long mine[PIV_CAP / PIV_NT];
 #pragma unroll
     for (unsigned u = 0; u < PIV_CAP / PIV_NT; ++u) {
       mine[u] = KEY_INVALID;
       if (u < per) {
         const unsigned j = tid + u * PIV_NT;
-        const int i = (int)(((unsigned long long)j * (unsigned)n) / ss);
-        const size_t o = (size_t)qi * g.npad + i;
-        mine[u] = arm_key(g.S[o], g.lvl[o], (uint32_t)i, g);
+        const int i = (int)((((unsigned long long)(j >> 3) * (unsigned)n) / nruns) & ~7ull) + (int)(j & 7u);
+        if (i < n) {
+          const size_t o = (size_t)qi * g.npad + i;
+          mine[u] = arm_key(g.S[o], g.lvl[o], (uint32_t)i, g);
+        }
       }
     }
     // keys <= tau ~ (n / ss) Gamma(rounds): with rounds = 2 expect + 10 the buffer holds

@@ -410,10 +410,11 @@ def test_shared_draws_level_mma(ak, n, d, q, k, h, kind):
     _assert_parity(a, ref, rows=rows)
 
 
-@pytest.mark.parametrize("groups", ["0", "2", "4", "8", "10", "24"])
+@pytest.mark.parametrize("groups", ["0", "2", "4", "5", "8", "10", "24"])
 def test_grouped_tiles_wide_rows(ak, groups, monkeypatch):
     """Rows wider than 8 KB (C3-like, d = 12,288 and 9,000): the grouped tile kernel
-    (AKNN_TILE_GROUPS = 2, 4, 8, 10, 24 thread groups sharing the column's point rows) and the
+    (AKNN_TILE_GROUPS = 2, 4, 5 (two query rows per group), 8, 10, 24 thread groups sharing
+    the column's point rows) and the
     classic one (0) agree with the oracle bit for bit, including ragged q and n."""
     monkeypatch.setenv("AKNN_TILE_GROUPS", groups)
     monkeypatch.setenv("AKNN_TILE_F", "0.25")  # make most tiles dense at small levels too
