@@ -553,6 +553,11 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Geom g) {
 // CTAs per SM would hide it, while the point rows stay shared (NG CTAs would need NG
 // copies: the shared memory holds NG R + P slots instead of NG (R + P)).  Per-query
 // draws with replacement (MODE 0) only; same arithmetic and result as k_advance_tiles.
+// Dense for the grouped kernel: the tiles k_advance_tiles_z takes are left to it.
+__device__ __forceinline__ bool grp_dense(const Geom &g, float tw, float dthr) {
+  return tw >= dthr && !(g.tile_z_draws > 0.f && tw >= g.tile_z_draws);
+}
+
 template <int NG, bool TIGHT, bool DB, int NTT>
 __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
   // DB: each group double-buffers its query rows -- the next tile's copy runs during this
@@ -625,7 +630,7 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
     for (int w = tid; w < CM_WORDS && w * 32 < rows; w += NTT) colmask[w] = 0u;
     __syncthreads();
     for (int tr = tid; tr < rows; tr += NTT) {
-      const bool dn = (float)g.tilework[(size_t)tr * g.tile_cols + tp] >= dthr;
+      const bool dn = grp_dense(g, (float)g.tilework[(size_t)tr * g.tile_cols + tp], dthr);
       mine |= dn;
       if (dn && tr < CM_WORDS * 32) atomicOr(&colmask[tr >> 5], 1u << (tr & 31));
     }
@@ -647,7 +652,7 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
     bool have_x = false;
     auto dense_at = [&](int tr) {
       return tr < CM_WORDS * 32 ? ((colmask[tr >> 5] >> (tr & 31)) & 1u) != 0u
-                                : (float)g.tilework[(size_t)tr * g.tile_cols + tp] >= dthr;
+                                : grp_dense(g, (float)g.tilework[(size_t)tr * g.tile_cols + tp], dthr);
     };
     auto next_dense = [&](int tr) {  // the group's next dense query tile at or after tr
       while (tr < rows && !dense_at(tr)) tr += NG;
@@ -884,6 +889,339 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
   if (tid == 0 && s_draws) atomicAdd(&g.ctl->tile_draws, s_draws);
 }
 
+// ---------------------------------------------------------------------------
+// |x - q| tiles: the largest levels of rows wider than 8 KB (C3's 2,048 and 4,096 draws
+// per pair).  ncu on the grouped kernel at 4,096 draws: shared-memory wavefronts at ~95 %
+// of one per cycle per SM (two random byte gathers per draw, ~4.6 wavefronts per warp
+// load from bank conflicts) -- above the Philox work (fma-heavy 79 %).  Here a tile's
+// pairs first get their row z_p[j] = |x_p[j] - q[j]| (u8, exact) written once, with
+// 16-byte conflict-free loads and stores, and every draw then gathers ONE byte:
+// (x_j - q_j)^2 = z_j^2 summed by IDP.4A, the same integer sum as k_advance_tiles_grp and
+// the oracle.  Materialising z costs ~d bytes per pair, so it pays only where a pair
+// draws a large share of d (tilework >= tile_z_draws, chosen on the host).
+//
+// One CTA per SM walks whole point columns (R = 1 query x P = 8 points per tile, the
+// grouped shape): the column's P raw point rows are staged once by bulk TMA, the query
+// row of each tile by bulk TMA one tile ahead.  Warp-specialised, a job = half a tile
+// (TZ_H pairs) in one of two z buffers with full / empty mbarriers:
+//   4 producer warps   write the job's z rows;
+//   1 bookkeeper warp  loads each job's actions / S / levels one job ahead, publishes the
+//                      actions, and commits a job (S += its sums, level set) once its
+//                      buffer is released -- off the draw path;
+//   16 consumer warps  run the Philox draws: per item (one pair, 4 Philox blocks) a warp
+//                      reduction (REDUX) and one shared atomic into the job's pair sums.
+// A job at 2,048 / 4,096 draws per pair is 512 / 1,024 items: one / two per consumer.
+constexpr int TZ_PW = 4, TZ_BW = 1, TZ_CW = 16;  // producer / bookkeeper / consumer warps
+constexpr int TZ_NT = 32 * (TZ_PW + TZ_BW + TZ_CW);
+constexpr int TZ_H = 4;                             // pairs per job (half a P = 8 tile)
+constexpr int TZ_CM = 256;                          // mask words: rows <= 8192
+
+__device__ __forceinline__ void sts_u128(uint32_t addr, uint4 v) {
+  asm volatile("st.shared.v4.u32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(v.x), "r"(v.y), "r"(v.z), "r"(v.w)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait_parity(uint32_t bar, uint32_t ph) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "ZW_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra ZW_%=;\n\t}" ::"r"(bar),
+      "r"(ph)
+      : "memory");
+}
+__device__ __forceinline__ void mbar_arrive1(uint32_t bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+}
+__device__ __forceinline__ void tma_row(uint32_t dst, const uint8_t *src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(src), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+// Four draws (one Philox block) from a z row: one byte gather each, |x - q|^2 summed.
+__device__ __forceinline__ uint32_t z_sq4(uint32_t za, uint4 w, uint32_t d, uint32_t acc) {
+  const uint32_t b0 = lds_u8(za + coord_of(w.x, d)), b1 = lds_u8(za + coord_of(w.y, d));
+  const uint32_t b2 = lds_u8(za + coord_of(w.z, d)), b3 = lds_u8(za + coord_of(w.w, d));
+  const uint32_t t = __byte_perm(__byte_perm(b0, b1, 0x0040), __byte_perm(b2, b3, 0x0040), 0x5410);
+  return __dp4a(t, t, acc);
+}
+
+// One job's arm state as the bookkeeper holds it until the commit.
+struct ZJob {
+  int4 S4;
+  uint32_t L4, act4;
+  long long o4;  // offset of the job's first arm in S / lvl / act
+};
+
+__global__ void __launch_bounds__(TZ_NT, 1) k_advance_tiles_z(Geom g) {
+  extern __shared__ __align__(16) unsigned char tsm[];
+  __shared__ __align__(8) uint64_t bar_zf[2], bar_ze[2], bar_q[2], bar_x;
+  __shared__ uint32_t colmask[TZ_CM];
+  __shared__ uint32_t zacc[2][TZ_H], zact[2], ztr[2];
+  __shared__ unsigned long long s_blocks, s_draws;
+  constexpr int NJ = 2;  // jobs per tile (P = 2 TZ_H)
+  const int P = 1 << g.tile_lp;
+  const uint32_t pitch = (uint32_t)g.pitch, d = (uint32_t)g.d;
+  const uint32_t base = (uint32_t)__cvta_generic_to_shared(tsm);
+  const uint32_t xs = base;                             // the column's P raw point rows
+  const uint32_t zs = xs + (uint32_t)P * pitch;         // 2 buffers x TZ_H z rows
+  const uint32_t qsm = zs + 2u * TZ_H * pitch;          // 2 query rows
+  {
+    uint32_t dyn;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(dyn));
+    if (P != NJ * TZ_H || qsm + 2u * pitch > base + dyn) __trap();  // host sizing broken: fail loudly
+  }
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int role = warp < TZ_PW ? 0 : (warp < TZ_PW + TZ_BW ? 1 : 2);  // producer / bookkeeper / consumer
+  const int rows = g.q;  // R = 1
+  const int cols = (g.n + P - 1) >> g.tile_lp;
+  const int nw = (rows + 31) >> 5;
+  // only DENSE tiles (k_scatter leaves their pairs out of the lists) are z tiles
+  const float zthr = fmaxf(g.tile_z_draws, g.tile_min_draws);
+  auto sa = [](const void *p) { return (uint32_t)__cvta_generic_to_shared(p); };
+  if (tid == 0) {
+    for (int b = 0; b < 2; ++b) {
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(&bar_zf[b])), "r"(TZ_PW * 32 + 1));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(sa(&bar_ze[b])), "r"(TZ_CW * 32));
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&bar_q[b])));
+      for (int e = 0; e < TZ_H; ++e) zacc[b][e] = 0;
+    }
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(sa(&bar_x)));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_blocks = s_draws = 0;
+  }
+  __syncthreads();
+  auto issue_q = [&](int tr, uint32_t b) {
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&bar_q[b])), "r"(pitch) : "memory");
+    tma_row(qsm + b * pitch, g.Q + (size_t)tr * pitch, pitch, sa(&bar_q[b]));
+  };
+  // bookkeeper: a job's arm state (actions filtered as the grouped kernel filters them)
+  auto load_job = [&](int tr, int pb) {
+    ZJob jb;
+    jb.o4 = (long long)tr * g.npad + pb;
+    const uint32_t a4 = g.qs[tr].done ? 0u : *reinterpret_cast<const uint32_t *>(g.act + jb.o4);
+    jb.S4 = *reinterpret_cast<const int4 *>(g.S + jb.o4);
+    jb.L4 = *reinterpret_cast<const uint32_t *>(g.lvl + jb.o4);
+    jb.act4 = 0;
+#pragma unroll
+    for (int e = 0; e < TZ_H; ++e) {
+      uint32_t a = (a4 >> (8 * e)) & 0xFFu;
+      if (a > (uint32_t)MAX_LEVELS || pb + e >= g.n) a = 0;
+      jb.act4 |= a << (8 * e);
+    }
+    return jb;
+  };
+  unsigned long long my_bl = 0, my_dr = 0;
+  auto commit = [&](const ZJob &jb, uint32_t zb) {  // bookkeeper, after the job's buffer is released
+    if (!jb.act4) return;
+    int4 S4 = jb.S4;
+    uint32_t l4 = jb.L4;
+#pragma unroll
+    for (int e = 0; e < TZ_H; ++e) {
+      const uint32_t a = (jb.act4 >> (8 * e)) & 0xFFu;
+      const int32_t v = (int32_t)zacc[zb][e];
+      zacc[zb][e] = 0u;
+      if (!a) continue;
+      if (e == 0) S4.x += v;
+      if (e == 1) S4.y += v;
+      if (e == 2) S4.z += v;
+      if (e == 3) S4.w += v;
+      l4 = (l4 & ~(0xFFu << (8 * e))) | (a << (8 * e));
+      my_dr += 1ull << (a - 1u);
+      my_bl += a <= 3u ? 1ull : 1ull << (a - 3u);
+    }
+    *reinterpret_cast<int4 *>(g.S + jb.o4) = S4;
+    *reinterpret_cast<uint32_t *>(g.lvl + jb.o4) = l4;
+  };
+  ZJob pend0{}, pend1{};  // bookkeeper: the jobs awaiting their commit, by buffer
+  uint32_t jz = 0, tq = 0, xc = 0;  // jobs / tiles / columns so far (identical in every role)
+  const int c0 = (int)((long long)blockIdx.x * cols / gridDim.x), c1 = (int)((long long)(blockIdx.x + 1) * cols / gridDim.x);
+  for (int tp = c0; tp < c1; ++tp) {
+    __syncthreads();  // every role is done with the previous column
+    for (int w = tid; w < nw; w += TZ_NT) colmask[w] = 0u;
+    __syncthreads();
+    bool any = false;
+    for (int tr = tid; tr < rows; tr += TZ_NT)
+      if ((float)g.tilework[(size_t)tr * g.tile_cols + tp] >= zthr) {
+        any = true;
+        atomicOr(&colmask[tr >> 5], 1u << (tr & 31));
+      }
+    if (!__syncthreads_or(any)) continue;
+    const int p0 = tp << g.tile_lp;
+    auto next_tile = [&](int tr) {  // the first z tile at or after row tr
+      for (int w = tr >> 5; w < nw; ++w) {
+        uint32_t m = colmask[w];
+        if (w == (tr >> 5)) m &= ~0u << (tr & 31);
+        if (m) return w * 32 + __ffs(m) - 1;
+      }
+      return rows;
+    };
+    const int tr0 = next_tile(0);
+    int ntl = 0;
+    for (int w = 0; w < nw; ++w) ntl += __popc(colmask[w]);
+    if (tid == 0) {  // the column's point rows, the first tile's query row
+      uint32_t bytes = 0;
+      for (int row = 0; row < P; ++row) bytes += p0 + row < g.n ? pitch : 0u;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(sa(&bar_x)), "r"(bytes) : "memory");
+      for (int row = 0; row < P; ++row)
+        if (p0 + row < g.n) tma_row(xs + (uint32_t)row * pitch, g.X + (size_t)(p0 + row) * pitch, pitch, sa(&bar_x));
+      issue_q(tr0, tq & 1u);
+    }
+    if (role == 0) {
+      uint32_t t = tq, j = jz;
+      mbar_wait_parity(sa(&bar_x), xc & 1u);
+      const uint32_t n16 = pitch >> 4;
+      for (int tr = tr0; tr < rows;) {
+        const int trn = next_tile(tr + 1);
+        asm volatile("bar.sync 1, %0;" ::"r"(TZ_PW * 32) : "memory");  // the other query buffer is free
+        if (tid == 0 && trn < rows) issue_q(trn, (t + 1u) & 1u);
+        mbar_wait_parity(sa(&bar_q[t & 1u]), (t >> 1) & 1u);
+        const uint32_t qa = qsm + (t & 1u) * pitch;
+#pragma unroll 1
+        for (int h = 0; h < NJ; ++h, ++j) {
+          const uint32_t zb = j & 1u;
+          if (j >= 2) mbar_wait_parity(sa(&bar_ze[zb]), ((j >> 1) + 1u) & 1u);  // job j - 2 consumed
+          const uint32_t zdst = zs + zb * TZ_H * pitch, xsrc = xs + (uint32_t)(h * TZ_H) * pitch;
+          // two 16-byte columns per step: 10 loads in flight before the stores
+          for (uint32_t c = tid; c < n16; c += 2 * TZ_PW * 32) {
+            const uint32_t c2 = c + TZ_PW * 32;
+            const bool two = c2 < n16;
+            const uint4 qv = lds_u128(qa + c * 16u), qw = two ? lds_u128(qa + c2 * 16u) : qv;
+            uint4 xv[TZ_H], xw[TZ_H];
+#pragma unroll
+            for (int e = 0; e < TZ_H; ++e) {
+              xv[e] = lds_u128(xsrc + (uint32_t)e * pitch + c * 16u);
+              xw[e] = two ? lds_u128(xsrc + (uint32_t)e * pitch + c2 * 16u) : xv[e];
+            }
+#pragma unroll
+            for (int e = 0; e < TZ_H; ++e) {
+              sts_u128(zdst + (uint32_t)e * pitch + c * 16u,
+                       make_uint4(__vabsdiffu4(xv[e].x, qv.x), __vabsdiffu4(xv[e].y, qv.y),
+                                  __vabsdiffu4(xv[e].z, qv.z), __vabsdiffu4(xv[e].w, qv.w)));
+              if (two)
+                sts_u128(zdst + (uint32_t)e * pitch + c2 * 16u,
+                         make_uint4(__vabsdiffu4(xw[e].x, qw.x), __vabsdiffu4(xw[e].y, qw.y),
+                                    __vabsdiffu4(xw[e].z, qw.z), __vabsdiffu4(xw[e].w, qw.w)));
+            }
+          }
+          mbar_arrive1(sa(&bar_zf[zb]));
+        }
+        ++t;
+        tr = trn;
+      }
+    } else if (role == 1) {
+      if (lane == 0) {
+        uint32_t j = jz;
+        int tr = tr0, h = 0;
+        ZJob cur = load_job(tr, p0);
+        while (tr < rows) {
+          const int trc = tr;
+          if (++h == NJ) {
+            h = 0;
+            tr = next_tile(tr + 1);
+          }
+          ZJob nxt{};
+          if (tr < rows) nxt = load_job(tr, p0 + h * TZ_H);  // in flight during this job
+          const uint32_t zb = j & 1u;
+          if (j >= 2) mbar_wait_parity(sa(&bar_ze[zb]), ((j >> 1) + 1u) & 1u);  // job j - 2 consumed
+          if (zb == 0) {
+            if (j >= 2) commit(pend0, 0u);
+            pend0 = cur;
+          } else {
+            if (j >= 2) commit(pend1, 1u);
+            pend1 = cur;
+          }
+          zact[zb] = cur.act4;
+          ztr[zb] = (uint32_t)trc;
+          mbar_arrive1(sa(&bar_zf[zb]));
+          cur = nxt;
+          ++j;
+        }
+      }
+      __syncwarp();
+    } else {
+      const uint32_t cw = (uint32_t)(warp - TZ_PW - TZ_BW);
+      uint32_t j = jz;
+      const int njobs = ntl * NJ;
+      for (int jj = 0; jj < njobs; ++jj, ++j) {
+        const uint32_t zb = j & 1u;
+        mbar_wait_parity(sa(&bar_zf[zb]), (j >> 1) & 1u);
+        const uint32_t act4 = zact[zb], trc = ztr[zb];
+        const int pb = p0 + (jj & 1) * TZ_H;
+        // items: (pair e, 4 consecutive Philox blocks of its level)
+        uint32_t ni[TZ_H];
+#pragma unroll
+        for (int e = 0; e < TZ_H; ++e) {
+          const uint32_t a = (act4 >> (8 * e)) & 0xFFu;
+          ni[e] = a == 0u ? 0u : (a <= 5u ? 1u : (1u << (a - 5u)));  // ceil(nb / 4), nb = 2^max(c-2,0)
+        }
+        const uint32_t n0 = ni[0], n01 = n0 + ni[1], n012 = n01 + ni[2], nall = n012 + ni[3];
+        const uint32_t gq = rng_qi(g, trc);
+        const uint32_t zb0 = zs + zb * TZ_H * pitch;
+        for (uint32_t it0 = cw * 32u; it0 < nall; it0 += TZ_CW * 32u) {  // warp-uniform
+          const uint32_t it = it0 + (uint32_t)lane;
+          const bool valid = it < nall;
+          const uint32_t e = it < n01 ? (it < n0 ? 0u : 1u) : (it < n012 ? 2u : 3u);
+          uint32_t sum = 0;
+          if (valid) {
+            const uint32_t k = it - (e == 0u ? 0u : e == 1u ? n0 : e == 2u ? n01 : n012);
+            const uint32_t a = (act4 >> (8 * e)) & 0xFFu, c = a - 1u;
+            const uint32_t gi = (uint32_t)(pb + (int)e) + g.id_offset;
+            const PhiloxPair pc = philox_pair(gi, gq, g.rk0);
+            const uint32_t za = zb0 + e * pitch;
+            if (c >= 4u) {  // 4 whole blocks
+              uint4 w[ADV_TP];
+#pragma unroll
+              for (int kk = 0; kk < ADV_TP; ++kk) w[kk] = philox_from_pair(4u * k + kk, a, pc, g.rk0, g.rk1);
+#pragma unroll
+              for (int kk = 0; kk < ADV_TP; ++kk) sum = z_sq4(za, w[kk], d, sum);
+            } else {  // levels 0-3: 1, 2, 4 or 8 draws (blocks 0 and, at level 3, 1)
+              const uint4 w0 = philox_from_pair(0u, a, pc, g.rk0, g.rk1);
+              if (c >= 2u) {
+                sum = z_sq4(za, w0, d, 0u);
+                if (c == 3u) sum = z_sq4(za, philox_from_pair(1u, a, pc, g.rk0, g.rk1), d, sum);
+              } else {
+                const uint32_t b0 = lds_u8(za + coord_of(w0.x, d));
+                sum = b0 * b0;
+                if (c == 1u) {
+                  const uint32_t b1 = lds_u8(za + coord_of(w0.y, d));
+                  sum += b1 * b1;
+                }
+              }
+            }
+          }
+          // the warp's items usually belong to one pair: one REDUX + one shared atomic
+          const uint32_t e0 = __shfl_sync(FULL, e, 0);
+          if (__all_sync(FULL, !valid || e == e0)) {
+            const uint32_t tot = __reduce_add_sync(FULL, sum);
+            if (lane == 0 && tot) atomicAdd(&zacc[zb][e0], tot);
+          } else if (valid && sum) {
+            atomicAdd(&zacc[zb][e], sum);
+          }
+        }
+        mbar_arrive1(sa(&bar_ze[zb]));
+      }
+    }
+    tq += (uint32_t)ntl;
+    jz += (uint32_t)ntl * NJ;
+    ++xc;
+  }
+  if (role == 1 && lane == 0) {  // the last two jobs: wait for their consumers, commit
+    for (uint32_t j = jz >= 2 ? jz - 2 : 0; j < jz; ++j) {
+      const uint32_t zb = j & 1u;
+      mbar_wait_parity(sa(&bar_ze[zb]), (j >> 1) & 1u);
+      commit(zb == 0 ? pend0 : pend1, zb);
+    }
+    if (my_bl) atomicAdd(&s_blocks, my_bl);
+    if (my_dr) atomicAdd(&s_draws, my_dr);
+  }
+  __syncthreads();
+  if (tid == 0 && s_blocks) atomicAdd(&g.ctl->tile_blocks, s_blocks);
+  if (tid == 0 && s_draws) atomicAdd(&g.ctl->tile_draws, s_draws);
+}
+
 int tile_slot_log2(int64_t pitch) {
   int l = 4;
   while ((1ll << l) < pitch) ++l;
@@ -1008,8 +1346,33 @@ size_t tile_grp_smem_bytes(int groups, int lr, int lp, int64_t pitch, bool tight
   return (base + groups * gsz + slot - 1) / slot * slot + (qrows + P) * slot;
 }
 
+static size_t tiles_z_smem(int lp, int64_t pitch) { return (size_t)((1 << lp) + 2 * TZ_H + 2) * (size_t)pitch; }
+
+bool tile_z_ok(int lr, int lp, int64_t pitch, int64_t q) {
+  if (lr != 0 || (1 << lp) != 2 * TZ_H || pitch % 16 != 0 || q > (int64_t)TZ_CM * 32) return false;
+  cudaFuncAttributes fa{};
+  if (cudaFuncGetAttributes(&fa, k_advance_tiles_z) != cudaSuccess) return false;
+  int dev = 0, optin = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+    return false;
+  return fa.sharedSizeBytes + tiles_z_smem(lp, pitch) <= (size_t)optin;
+}
+
+static cudaError_t launch_tiles_z(const Geom &g, int num_sms, cudaStream_t s) {
+  const size_t smem = tiles_z_smem(g.tile_lp, g.pitch);
+  cudaError_t e = cudaFuncSetAttribute(k_advance_tiles_z, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_advance_tiles_z<<<num_sms, TZ_NT, smem, s>>>(g);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_advance_tiles(const Geom &g, int num_sms, cudaStream_t s) {
   if (g.tile_groups && !g.wor && !(g.shared_draws && g.tile_lr == 5)) {
+    if (g.tile_z_draws > 0.f) {
+      const cudaError_t e = launch_tiles_z(g, num_sms, s);
+      if (e != cudaSuccess) return e;
+    }
     if (g.tile_groups == 8) return launch_tiles_grp<8, true, false, 512>(g, num_sms, s);
     if (g.tile_groups == 10) return launch_tiles_grp<10, true, false, 640>(g, num_sms, s);
     if (g.tile_groups == 5) return launch_tiles_grp<5, true, false, 640>(g, num_sms, s);  // R = 2

@@ -383,6 +383,12 @@ void setup_tiles(Geom &g, const TileShape &t, const aknn_opts &o, int64_t qb, ui
   // consecutive tiles of a point column share the staged point rows: a tile stages
   // about its R query rows (+ one point row's share)
   g.tile_min_draws = t.row_draws * (float)((1 << t.lr) + 1);
+  // AKNN_TILE_ZS = s > 0: the grouped shape's tiles whose pairs draw >= s each take the
+  // |x - q| kernel (k_advance_tiles_z).  Off by default: on C3 it cut the shared-memory
+  // wavefronts of the largest level by 41 % but ran 112.7 / 68.1 ms at 4,096 / 2,048
+  // draws per pair against the grouped kernel's 108.4 / 57.2
+  const int zs = env_int("AKNN_TILE_ZS", 0);
+  g.tile_z_draws = (g.tile_groups && zs > 0 && tile_z_ok(t.lr, t.lp, g.pitch, qb)) ? (float)zs * (float)(1 << t.lp) : 0.f;
 
 }
 

@@ -164,6 +164,8 @@ struct Geom {
   int tile_groups;       // > 0: k_advance_tiles_grp with this many thread groups per CTA
   int tile_tight;        // 1: its row slots are the pitch apart (not a power of two)
   int tile_db;           // 1: its groups double-buffer their query rows
+  float tile_z_draws;    // > 0: dense tiles with tilework >= this run in k_advance_tiles_z
+                         //   (|x - q| rows materialised; the grouped kernel skips them)
   unsigned long long *advanced;  // pairs advanced (statistics), device counter
   // the blocker predicate as integer thresholds per (query, level) (k_thresholds)
   int32_t *thr;          // [q][THR_STRIDE]: Su[c], Sl[c] (c < MAX_LEVELS), M-mask

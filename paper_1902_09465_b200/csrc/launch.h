@@ -58,6 +58,8 @@ cudaError_t launch_advance_tiles(const Geom &g, int num_sms, cudaStream_t s);
 size_t tile_smem_bytes(int lr, int lp, int64_t pitch);
 size_t tile_grp_smem_bytes(int groups, int lr, int lp, int64_t pitch, bool tight, bool db);
 int tile_slot_log2(int64_t pitch);
+// |x - q| tiles (k_advance_tiles_z): usable for this shape (P = 8 points, R = 1, rows fit)
+bool tile_z_ok(int lr, int lp, int64_t pitch, int64_t q);
 // Per-query counters from the final arm states (before the outputs).
 cudaError_t launch_tally(const Geom &g, cudaStream_t s);
 // Device-driven round loop (CUDA graph with a conditional WHILE node).

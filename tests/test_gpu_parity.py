@@ -473,3 +473,31 @@ def test_grouped_tiles_shared_draws(ak, monkeypatch):
     ix.close()
     ref = orc.query_br(X, Q, 4, 4, 48, al, want_sums=True, shared_draws=True)
     _assert_parity(got, ref)
+
+
+@pytest.mark.parametrize("zs", ["4", "64", "1024"])
+def test_z_tiles(ak, zs, monkeypatch):
+    """|x - q| tiles (k_advance_tiles_z: each pair's row |x_p - q| materialised once, one
+    byte gather per draw) for the tiles whose pairs draw >= AKNN_TILE_ZS each, the rest in
+    the grouped kernel: bit-exact against the oracle over mixed levels, ragged n and q,
+    several point columns per CTA, and rows that are not a multiple of 128 bytes (d = 9,000)."""
+    monkeypatch.setenv("AKNN_TILE_ZS", zs)
+    monkeypatch.setenv("AKNN_TILE_F", "0.25")
+    for (n, d, q, seed) in ((1203, 12288, 7, 51), (700, 9000, 5, 52), (4000, 12288, 9, 53)):
+        X, Q = synth.small_instance(seed, n, d, q=q)
+        al = orc.alpha_experimental(n, 0.05, d, 0.3)
+        got, ref = _run_both(ak, X, Q, 4, 4, seed, al)
+        _assert_parity(got, ref)
+
+
+def test_z_tiles_shared_draws(ak, monkeypatch):
+    """Query-independent draws through the |x - q| tiles against the oracle's shared-draw mode."""
+    monkeypatch.setenv("AKNN_TILE_ZS", "4")
+    monkeypatch.setenv("AKNN_TILE_F", "0.25")
+    X, Q = synth.small_instance(54, 2100, 12288, q=6)
+    al = orc.alpha_experimental(2100, 0.05, 12288, 0.3)
+    ix = ak.Index(X)
+    got = ix.query(Q, 4, 4, 0.05, 54, al, counts=True, sums=True, flags=ak.FLAG_SHARED_DRAWS)
+    ix.close()
+    ref = orc.query_br(X, Q, 4, 4, 54, al, want_sums=True, shared_draws=True)
+    _assert_parity(got, ref)
