@@ -553,16 +553,50 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Geom g) {
 // CTAs per SM would hide it, while the point rows stay shared (NG CTAs would need NG
 // copies: the shared memory holds NG R + P slots instead of NG (R + P)).  Per-query
 // draws with replacement (MODE 0) only; same arithmetic and result as k_advance_tiles.
-// Dense for the grouped kernel: the tiles k_advance_tiles_z takes are left to it.
+//
+// QG (the smallest tiled levels): no query-row copies -- a draw's query byte is gathered
+// from global memory (Q is small and L2-resident), its point byte from the staged point
+// rows.  A tile of 8 pairs at s draws each gathers 8 s query sectors instead of copying
+// a whole query row (12 KB on C3): fewer bytes below ~48 draws per pair, and no copy
+// latency in the tile's chain at any s.
+//
+// Dense for this launch: the tiles with tile_lo <= tilework < tile_hi (launch_advance_tiles
+// splits the dense tiles between the QG, plain and |x - q| kernels).
 __device__ __forceinline__ bool grp_dense(const Geom &g, float tw, float dthr) {
-  return tw >= dthr && !(g.tile_z_draws > 0.f && tw >= g.tile_z_draws);
+  return tw >= fmaxf(dthr, g.tile_lo) && tw < g.tile_hi;
 }
 
-template <int NG, bool TIGHT, bool DB, int NTT>
+constexpr int QG_LR = 4;  // QG super tiles: 16 query rows x P = 8 points (RP = 128: one-warp bookkeeping)
+
+__device__ __forceinline__ uint32_t ldg_u8(const uint8_t *p) {
+  uint32_t v;
+  asm volatile("ld.global.nc.u8 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+// QG: point byte from shared memory (x row at xa, coordinate address xa + j or xa | j),
+// query byte from global memory.
+template <bool TIGHT>
+__device__ __forceinline__ uint32_t sq_diff_g(uint32_t xa, const uint8_t *qp, uint32_t j) {
+  const int diff = (int)lds_u8(TIGHT ? xa + j : (xa | j)) - (int)ldg_u8(qp + j);
+  return (uint32_t)(diff * diff);
+}
+template <bool TIGHT>
+__device__ __forceinline__ uint32_t sq_diff4_g(uint32_t xa, const uint8_t *qp, uint4 w, uint32_t d, uint32_t acc) {
+  const uint32_t j0 = coord_of(w.x, d), j1 = coord_of(w.y, d), j2 = coord_of(w.z, d), j3 = coord_of(w.w, d);
+  const uint32_t q0 = ldg_u8(qp + j0), q1 = ldg_u8(qp + j1), q2 = ldg_u8(qp + j2), q3 = ldg_u8(qp + j3);
+  const uint32_t x0 = lds_u8(TIGHT ? xa + j0 : (xa | j0)), x1 = lds_u8(TIGHT ? xa + j1 : (xa | j1));
+  const uint32_t x2 = lds_u8(TIGHT ? xa + j2 : (xa | j2)), x3 = lds_u8(TIGHT ? xa + j3 : (xa | j3));
+  const uint32_t x4 = __byte_perm(__byte_perm(x0, x1, 0x0040), __byte_perm(x2, x3, 0x0040), 0x5410);
+  const uint32_t q4 = __byte_perm(__byte_perm(q0, q1, 0x0040), __byte_perm(q2, q3, 0x0040), 0x5410);
+  const uint32_t t = __vabsdiffu4(x4, q4);
+  return __dp4a(t, t, acc);
+}
+
+template <int NG, bool TIGHT, bool DB, int NTT, bool QG = false>
 __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
   // DB: each group double-buffers its query rows -- the next tile's copy runs during this
-  // tile's draws (2 NG R query slots)
-  constexpr int QB = DB ? 2 : 1;
+  // tile's draws (2 NG R query slots); QG: no query rows in shared memory
+  constexpr int QB = QG ? 0 : (DB ? 2 : 1);
   constexpr int GT = NTT / NG;  // threads per group (whole warps)
   static_assert(GT % 32 == 0, "groups of whole warps");
   extern __shared__ __align__(16) unsigned char tsm[];
@@ -572,7 +606,11 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
   __shared__ unsigned lmask_s[NG];
   constexpr int CM_WORDS = 1024;                   // dense-tile bits of the column (rows <= 32768)
   __shared__ uint32_t colmask[CM_WORDS];
-  const int R = 1 << g.tile_lr, P = 1 << g.tile_lp, RP = R * P;
+  // QG: super tiles of R = 2^QG_LR consecutive query rows (the bookkeeping of a tile --
+  // its level lists, barriers, scan -- amortised over R P pairs instead of P; the tile
+  // rows of tilework stay single query rows, so a row that is not dense is masked out)
+  const int LR = QG ? QG_LR : g.tile_lr;
+  const int R = 1 << LR, P = 1 << g.tile_lp, RP = R * P;
   const int pitch = (int)g.pitch;
   const int sl = g.tile_slot_l;
   const uint32_t slot = 1u << sl;
@@ -596,7 +634,8 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
   const uint32_t qbar0 = (uint32_t)__cvta_generic_to_shared(&qbar[grp][0]);
   const uint32_t pbar_s = (uint32_t)__cvta_generic_to_shared(&pbar);
   const uint32_t d = (uint32_t)g.d;
-  const int rows = (g.q + R - 1) >> g.tile_lr;
+  const int rows = (g.q + R - 1) >> LR;                               // (super) tile rows
+  const int rows1 = (g.q + (1 << g.tile_lr) - 1) >> g.tile_lr;        // tilework rows
   const int cols = (g.n + P - 1) >> g.tile_lp;
   const float dthr = g.tile_min_draws;
   if (tid == 0) {
@@ -627,9 +666,9 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
     // the previous column); a column without one is skipped
     bool mine = false;
     __syncthreads();  // every group has left the previous column (its mask reads included)
-    for (int w = tid; w < CM_WORDS && w * 32 < rows; w += NTT) colmask[w] = 0u;
+    for (int w = tid; w < CM_WORDS && w * 32 < rows1; w += NTT) colmask[w] = 0u;
     __syncthreads();
-    for (int tr = tid; tr < rows; tr += NTT) {
+    for (int tr = tid; tr < rows1; tr += NTT) {
       const bool dn = grp_dense(g, (float)g.tilework[(size_t)tr * g.tile_cols + tp], dthr);
       mine |= dn;
       if (dn && tr < CM_WORDS * 32) atomicOr(&colmask[tr >> 5], 1u << (tr & 31));
@@ -650,9 +689,17 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
               : "memory");
     }
     bool have_x = false;
-    auto dense_at = [&](int tr) {
+    auto row_dense = [&](int tr) {  // tilework row tr
       return tr < CM_WORDS * 32 ? ((colmask[tr >> 5] >> (tr & 31)) & 1u) != 0u
                                 : grp_dense(g, (float)g.tilework[(size_t)tr * g.tile_cols + tp], dthr);
+    };
+    auto dense_at = [&](int tr) {  // (super) tile row tr
+      if (!QG) return row_dense(tr);
+      const int r0 = tr << LR;
+      if (r0 + R <= CM_WORDS * 32) return ((colmask[r0 >> 5] >> (r0 & 31)) & ((1u << R) - 1u)) != 0u;
+      bool any = false;
+      for (int r = r0; r < r0 + R && r < rows1; ++r) any |= row_dense(r);
+      return any;
     };
     auto next_dense = [&](int tr) {  // the group's next dense query tile at or after tr
       while (tr < rows && !dense_at(tr)) tr += NG;
@@ -670,8 +717,8 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
     };
     auto load_state = [&](int tr) {
       TileState t{make_int4(0, 0, 0, 0), 0u, 0u, 1};
-      const int r0n = tr << g.tile_lr;
-      if (tr < rows && in && r0n + rr < g.q && p0 + pp < g.n) {
+      const int r0n = tr << LR;
+      if (tr < rows && in && r0n + rr < g.q && p0 + pp < g.n && (!QG || row_dense(r0n + rr))) {
         const size_t o = (size_t)(r0n + rr) * g.npad + p0 + pp;
         t.dn = g.qs[r0n + rr].done;
         t.A4 = *reinterpret_cast<const uint32_t *>(g.act + o);
@@ -688,14 +735,14 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
       const TileState cur = nxt;
       trn = next_dense(tr + NG);
       nxt = load_state(trn);  // in flight while this tile is processed
-      const int r0 = tr << g.tile_lr;
+      const int r0 = tr << LR;
       gsync();  // the group's previous tile is done with its slots and arrays
       if (gtid < MAX_LEVELS) lcnt[grp][gtid] = 0;
       // the query rows: this tile's were copied during the previous tile of the column
       // (DB) unless it is the group's first; then the next tile's copy is issued into
       // the other buffer, free since the gsync above
       auto issue_rows = [&](int trq, int b) {
-        const int rq = trq << g.tile_lr;
+        const int rq = trq << LR;
         const uint32_t bar = qbar0 + 8u * (uint32_t)b, dst = qs0 + (uint32_t)(b * R) * stride;
         uint32_t bytes = 0;
         for (int row = 0; row < R; ++row) bytes += rq + row < g.q ? (uint32_t)pitch : 0u;
@@ -709,7 +756,7 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
                 "l"(g.Q + (size_t)(rq + row) * pitch), "r"((uint32_t)pitch), "r"(bar)
                 : "memory");
       };
-      if (gtid == 0) {
+      if (!QG && gtid == 0) {
         if (!DB || first) issue_rows(tr, sel);
         if (DB && trn < rows) issue_rows(trn, sel ^ 1);
       }
@@ -782,8 +829,10 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
           if (a) lst[b0 + __popc(m & ((1u << lane_id()) - 1u))] = (uint16_t)(e4 + k);
         }
       }
-      wait_bar(qbar0 + 8u * (uint32_t)sel, (qphase >> sel) & 1u);  // the query rows
-      qphase ^= 1u << sel;
+      if (!QG) {
+        wait_bar(qbar0 + 8u * (uint32_t)sel, (qphase >> sel) & 1u);  // the query rows
+        qphase ^= 1u << sel;
+      }
       if (!have_x) {  // the column's point rows (once per column and group)
         wait_bar(pbar_s, pphase);
         have_x = true;
@@ -815,7 +864,16 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
             uint32_t sum = 0;
 #pragma unroll
             for (int k = 0; k < ADV_TP; ++k) {
-              if (pr[k] >= 0) {
+              if (QG && pr[k] >= 0) {
+                const uint32_t xa = xs + (uint32_t)(pr[k] & (P - 1)) * stride;
+                const uint8_t *qp = g.Q + (size_t)(r0 + (pr[k] >> g.tile_lp)) * pitch;
+                if (s >= 4) {
+                  sum = sq_diff4_g<TIGHT>(xa, qp, w[k], d, sum);
+                } else {
+                  sum += sq_diff_g<TIGHT>(xa, qp, coord_of(w[k].x, d));
+                  if (s == 2) sum += sq_diff_g<TIGHT>(xa, qp, coord_of(w[k].y, d));
+                }
+              } else if (pr[k] >= 0) {
                 const uint32_t xa = xs + (uint32_t)(pr[k] & (P - 1)) * stride;
                 const uint32_t qa = qs + (uint32_t)(pr[k] >> g.tile_lp) * stride;
                 if (s >= 4) {
@@ -849,9 +907,15 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
 #pragma unroll
             for (int k = 0; k < ADV_TP; ++k) w[k] = philox_from_pair(b0 + k, lv, pc, g.rk0, g.rk1);
             uint32_t sum = 0;
+            if (QG) {
+              const uint8_t *qp = g.Q + (size_t)(r0 + (pe >> g.tile_lp)) * pitch;
 #pragma unroll
-            for (int k = 0; k < ADV_TP; ++k)
-              sum = TIGHT ? sq_diff4_t(xa, qa, w[k], d, sum) : sq_diff4(xa, qa, w[k], d, sum);
+              for (int k = 0; k < ADV_TP; ++k) sum = sq_diff4_g<TIGHT>(xa, qp, w[k], d, sum);
+            } else {
+#pragma unroll
+              for (int k = 0; k < ADV_TP; ++k)
+                sum = TIGHT ? sq_diff4_t(xa, qa, w[k], d, sum) : sq_diff4(xa, qa, w[k], d, sum);
+            }
             atomicAdd(reinterpret_cast<uint32_t *>(acc + pe), sum);
           }
         }
@@ -1319,22 +1383,22 @@ static cudaError_t launch_tiles_k(const Geom &g, int num_sms, cudaStream_t s) {
   return launch_tiles_nt<MODE, TILE_NT>(gt, num_sms, &per_sm, s);
 }
 
-template <int NG, bool TIGHT, bool DB, int NTT = TILE_NT_WIDE>
+template <int NG, bool TIGHT, bool DB, int NTT = TILE_NT_WIDE, bool QG = false>
 static cudaError_t launch_tiles_grp(const Geom &g, int num_sms, cudaStream_t s) {
   cudaFuncAttributes fa{};
   int dev = 0, rsv = 0;
-  if (cudaFuncGetAttributes(&fa, k_advance_tiles_grp<NG, TIGHT, DB, NTT>) != cudaSuccess) fa.sharedSizeBytes = 4096;
+  if (cudaFuncGetAttributes(&fa, k_advance_tiles_grp<NG, TIGHT, DB, NTT, QG>) != cudaSuccess) fa.sharedSizeBytes = 4096;
   if (cudaGetDevice(&dev) != cudaSuccess ||
       cudaDeviceGetAttribute(&rsv, cudaDevAttrReservedSharedMemoryPerBlock, dev) != cudaSuccess)
     rsv = 1024;
   const size_t base = (size_t)fa.sharedSizeBytes + (size_t)rsv;
-  const size_t R = (size_t)1 << g.tile_lr, P = (size_t)1 << g.tile_lp, slot = (size_t)1 << g.tile_slot_l;
+  const size_t R = (size_t)1 << (QG ? QG_LR : g.tile_lr), P = (size_t)1 << g.tile_lp, slot = (size_t)1 << g.tile_slot_l;
   const size_t gsz = (R * P * 7 + 15) & ~(size_t)15;
   const size_t rows0 = TIGHT ? base + NG * gsz : (base + NG * gsz + slot - 1) / slot * slot;
-  const size_t smem = rows0 + ((DB ? 2 : 1) * NG * R + P) * (TIGHT ? (size_t)g.pitch : slot) - base;
-  cudaError_t e = cudaFuncSetAttribute(k_advance_tiles_grp<NG, TIGHT, DB, NTT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const size_t smem = rows0 + ((QG ? 0 : DB ? 2 : 1) * NG * R + P) * (TIGHT ? (size_t)g.pitch : slot) - base;
+  cudaError_t e = cudaFuncSetAttribute(k_advance_tiles_grp<NG, TIGHT, DB, NTT, QG>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_advance_tiles_grp<NG, TIGHT, DB, NTT><<<num_sms, NTT, smem, s>>>(g);
+  k_advance_tiles_grp<NG, TIGHT, DB, NTT, QG><<<num_sms, NTT, smem, s>>>(g);
   return cudaGetLastError();
 }
 
@@ -1367,12 +1431,26 @@ static cudaError_t launch_tiles_z(const Geom &g, int num_sms, cudaStream_t s) {
   return cudaGetLastError();
 }
 
-cudaError_t launch_advance_tiles(const Geom &g, int num_sms, cudaStream_t s) {
-  if (g.tile_groups && !g.wor && !(g.shared_draws && g.tile_lr == 5)) {
-    if (g.tile_z_draws > 0.f) {
-      const cudaError_t e = launch_tiles_z(g, num_sms, s);
+cudaError_t launch_advance_tiles(const Geom &g0, int num_sms, cudaStream_t s) {
+  if (g0.tile_groups && !g0.wor && !(g0.shared_draws && g0.tile_lr == 5)) {
+    // the dense tiles by tilework: [0, qg) QG grouped kernel, [qg, z) grouped kernel,
+    // [z, inf) |x - q| kernel (each bound 0 = that kernel off)
+    const float zlo = g0.tile_z_draws > 0.f ? fmaxf(g0.tile_z_draws, g0.tile_min_draws) : INFINITY;
+    const float qhi = fminf(g0.tile_qg_draws, zlo);
+    if (g0.tile_z_draws > 0.f) {
+      const cudaError_t e = launch_tiles_z(g0, num_sms, s);
       if (e != cudaSuccess) return e;
     }
+    if (g0.tile_groups == 10 && qhi > g0.tile_min_draws) {
+      Geom gq = g0;
+      gq.tile_lo = 0.f;
+      gq.tile_hi = qhi;
+      const cudaError_t e = launch_tiles_grp<10, true, false, 640, true>(gq, num_sms, s);
+      if (e != cudaSuccess) return e;
+    }
+    Geom g = g0;
+    g.tile_lo = g0.tile_groups == 10 ? fmaxf(qhi, 0.f) : 0.f;
+    g.tile_hi = zlo;
     if (g.tile_groups == 8) return launch_tiles_grp<8, true, false, 512>(g, num_sms, s);
     if (g.tile_groups == 10) return launch_tiles_grp<10, true, false, 640>(g, num_sms, s);
     if (g.tile_groups == 5) return launch_tiles_grp<5, true, false, 640>(g, num_sms, s);  // R = 2
@@ -1382,9 +1460,9 @@ cudaError_t launch_advance_tiles(const Geom &g, int num_sms, cudaStream_t s) {
     if (g.tile_groups == 2 && g.tile_db) return launch_tiles_grp<2, false, true>(g, num_sms, s);
     if (g.tile_groups == 2) return launch_tiles_grp<2, false, false>(g, num_sms, s);
   }
-  if (g.shared_draws && g.tile_lr == 5) return launch_tiles_k<1>(g, num_sms, s);
-  if (g.wor) return launch_tiles_k<2>(g, num_sms, s);
-  return launch_tiles_k<0>(g, num_sms, s);
+  if (g0.shared_draws && g0.tile_lr == 5) return launch_tiles_k<1>(g0, num_sms, s);
+  if (g0.wor) return launch_tiles_k<2>(g0, num_sms, s);
+  return launch_tiles_k<0>(g0, num_sms, s);
 }
 
 }  // namespace aknn

@@ -388,6 +388,10 @@ void setup_tiles(Geom &g, const TileShape &t, const aknn_opts &o, int64_t qb, ui
   // wavefronts of the largest level by 41 % but ran 112.7 / 68.1 ms at 4,096 / 2,048
   // draws per pair against the grouped kernel's 108.4 / 57.2
   const int zs = env_int("AKNN_TILE_ZS", 0);
+  // AKNN_TILE_QG = s: the 10-group shape's tiles whose pairs draw < s each gather their
+  // query bytes from global memory (no query-row copies; 0 = off)
+  const int qgs = env_int("AKNN_TILE_QG", 128);
+  g.tile_qg_draws = (g.tile_groups == 10 && qgs > 0) ? (float)qgs * (float)(1 << t.lp) : 0.f;
   g.tile_z_draws = (g.tile_groups && zs > 0 && tile_z_ok(t.lr, t.lp, g.pitch, qb)) ? (float)zs * (float)(1 << t.lp) : 0.f;
 
 }

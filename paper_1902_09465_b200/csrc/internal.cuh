@@ -166,6 +166,9 @@ struct Geom {
   int tile_db;           // 1: its groups double-buffer their query rows
   float tile_z_draws;    // > 0: dense tiles with tilework >= this run in k_advance_tiles_z
                          //   (|x - q| rows materialised; the grouped kernel skips them)
+  float tile_qg_draws;   // > 0: dense tiles with tilework < this gather the query bytes from
+                         //   global memory (k_advance_tiles_grp<..., QG>: no query-row copies)
+  float tile_lo, tile_hi;  // this grouped launch takes the dense tiles with lo <= tilework < hi
   unsigned long long *advanced;  // pairs advanced (statistics), device counter
   // the blocker predicate as integer thresholds per (query, level) (k_thresholds)
   int32_t *thr;          // [q][THR_STRIDE]: Su[c], Sl[c] (c < MAX_LEVELS), M-mask

@@ -501,3 +501,19 @@ def test_z_tiles_shared_draws(ak, monkeypatch):
     ix.close()
     ref = orc.query_br(X, Q, 4, 4, 54, al, want_sums=True, shared_draws=True)
     _assert_parity(got, ref)
+
+
+@pytest.mark.parametrize("qg", ["0", "32", "65536"])
+def test_qg_tiles(ak, qg, monkeypatch):
+    """The grouped kernel's QG variant (the query byte of each draw gathered from global
+    memory, no query-row copies, super tiles of several query rows) for the dense tiles
+    whose pairs draw < AKNN_TILE_QG each (65,536: every dense tile; 0: none), the rest in
+    the plain grouped kernel: bit-exact against the oracle over mixed levels, ragged n and
+    q (rows past q, non-dense rows inside a super tile), several columns per CTA."""
+    monkeypatch.setenv("AKNN_TILE_QG", qg)
+    monkeypatch.setenv("AKNN_TILE_F", "0.25")
+    for (n, d, q, seed) in ((1203, 12288, 7, 61), (700, 9000, 21, 62), (4000, 12288, 9, 63)):
+        X, Q = synth.small_instance(seed, n, d, q=q)
+        al = orc.alpha_experimental(n, 0.05, d, 0.3)
+        got, ref = _run_both(ak, X, Q, 4, 4, seed, al)
+        _assert_parity(got, ref)
