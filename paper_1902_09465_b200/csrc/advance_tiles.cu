@@ -778,7 +778,62 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
       // only the warps holding arms (4 per thread, RP <= 4 GT) list them
       const bool arm_warp = (gtid & ~31) * 4 < RP;
       uint32_t act4 = 0;  // sampled actions only (exact fallbacks: tensor-core pass)
-      if (arm_warp) {
+      // Tiles of <= 32 arms (C3's one-query tiles: 8) whose sampled arms all sit at ONE
+      // level (lock-step rounds): warp 0 lists them with a min/max reduction and an
+      // 8-lane prefix sum -- no level histogram, scan or per-level match (the general
+      // path below, ~2x the instructions of this tile's bookkeeping)
+      bool fast = false;
+      if (RP <= 32 && gtid < 32) {
+        if (in) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            uint32_t a = (A4 >> (8 * k)) & 0xFFu;
+            if (dn || a > (uint32_t)MAX_LEVELS || p0 + pp + k >= g.n) a = 0;
+            act4 |= a << (8 * k);
+          }
+          *reinterpret_cast<uint32_t *>(sact + e4) = act4;
+        }
+        uint32_t lo = 255u, hi = 0u, cnt = 0u;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t a = (act4 >> (8 * k)) & 0xFFu;
+          if (a) {
+            lo = min(lo, a);
+            hi = max(hi, a);
+            ++cnt;
+          }
+        }
+        lo = __reduce_min_sync(FULL, lo);
+        hi = __reduce_max_sync(FULL, hi);
+        if (hi == 0u || lo == hi) {
+          fast = true;
+          uint32_t x = cnt;
+#pragma unroll
+          for (int o = 1; o < 8; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(FULL, x, o);
+            if (gtid >= o) x += y;
+          }
+          uint32_t b = x - cnt;
+          const uint32_t tot = __shfl_sync(FULL, x, 7);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)
+            if ((act4 >> (8 * k)) & 0xFFu) lst[b++] = (uint16_t)(e4 + k);
+          if (gtid == 0) {
+            if (hi) {
+              const uint32_t c = hi - 1u;
+              lcnt[grp][c] = tot;
+              loff[grp][c] = 0u;
+              lmask_s[grp] = 1u << c;
+              my_dr += (unsigned long long)tot << c;
+              my_bl += (unsigned long long)tot << (c < 2u ? 0u : c - 2u);
+            } else {
+              lmask_s[grp] = 0u;
+            }
+          }
+        }
+        if (!fast) act4 = 0;
+      }
+      if (!fast && arm_warp) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           uint8_t a = (uint8_t)(A4 >> (8 * k));
@@ -788,8 +843,8 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
         }
         if (in) *reinterpret_cast<uint32_t *>(sact + e4) = act4;
       }
-      bsync();  // lcnt
-      if (gtid < 32) {  // per-level offsets, the level mask and the statistics: one warp
+      if (!fast) bsync();  // lcnt
+      if (!fast && gtid < 32) {  // per-level offsets, the level mask and the statistics: one warp
         const unsigned v = gtid < MAX_LEVELS ? lcnt[grp][gtid] : 0u;
         unsigned x = v;
 #pragma unroll
@@ -815,8 +870,8 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
           my_bl += bl;  // (64-bit shared atomics are CAS loops: once per tile cost ~1 %)
         }
       }
-      bsync();
-      if (arm_warp) {
+      if (!fast) bsync();
+      if (!fast && arm_warp) {
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
           const uint8_t a = (uint8_t)(act4 >> (8 * k));
