@@ -604,6 +604,7 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
   __shared__ __align__(8) uint64_t qbar[NG][2], pbar;
   __shared__ unsigned long long s_blocks, s_draws;
   __shared__ unsigned lmask_s[NG];
+  __shared__ unsigned char accz[NG];  // 1: the tile's acc entries were zeroed by the fast path
   constexpr int CM_WORDS = 1024;                   // dense-tile bits of the column (rows <= 32768)
   __shared__ uint32_t colmask[CM_WORDS];
   // QG: super tiles of R = 2^QG_LR consecutive query rows (the bookkeeping of a tile --
@@ -612,6 +613,7 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
   const int LR = QG ? QG_LR : g.tile_lr;
   const int R = 1 << LR, P = 1 << g.tile_lp, RP = R * P;
   const int pitch = (int)g.pitch;
+  const bool one_warp_tiles = RP <= 128;  // a tile's bookkeeping sits in warp 0
   const int sl = g.tile_slot_l;
   const uint32_t slot = 1u << sl;
   // row stride: a power-of-two slot (coordinate address = row | j) or, TIGHT, the pitch
@@ -736,7 +738,9 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
       trn = next_dense(tr + NG);
       nxt = load_state(trn);  // in flight while this tile is processed
       const int r0 = tr << LR;
-      gsync();  // the group's previous tile is done with its slots and arrays
+      // (no barrier here: the previous tile ended with one after its last read of the
+      // query slot, acc, lst and the level tables, and only warp 0 writes them next)
+      if (!one_warp_tiles) gsync();
       if (gtid < MAX_LEVELS) lcnt[grp][gtid] = 0;
       // the query rows: this tile's were copied during the previous tile of the column
       // (DB) unless it is the group's first; then the next tile's copy is issued into
@@ -818,7 +822,11 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             if ((act4 >> (8 * k)) & 0xFFu) lst[b++] = (uint16_t)(e4 + k);
+#pragma unroll
+          for (int k = 0; k < 4; ++k)  // the level's sums start at 0 (no zeroing pass below)
+            if (in) acc[e4 + k] = 0;
           if (gtid == 0) {
+            accz[grp] = 1;
             if (hi) {
               const uint32_t c = hi - 1u;
               lcnt[grp][c] = tot;
@@ -832,6 +840,7 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
           }
         }
         if (!fast) act4 = 0;
+        if (!fast && gtid == 0) accz[grp] = 0;
       }
       if (!fast && arm_warp) {
 #pragma unroll
@@ -946,8 +955,10 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
             }
           }
         } else {
-          for (unsigned l = gtid; l < m; l += GT) acc[L[l]] = 0;
-          gsync();
+          if (!(RP <= 32 && accz[grp])) {  // (the one-level fast path zeroed them)
+            for (unsigned l = gtid; l < m; l += GT) acc[L[l]] = 0;
+            gsync();
+          }
           const unsigned lg = (unsigned)(lb - 2);
           const unsigned total = m << lg;
           for (unsigned it = gtid; it < total; it += GT) {
