@@ -207,6 +207,7 @@ __device__ __forceinline__ void f1_accumulate(uint32_t qt_s, uint32_t dbuf_s, in
 // 2: per-query draws without replacement (reading R23).
 template <int MODE, int NT>
 __global__ void __launch_bounds__(NT) k_advance_tiles(Geom g) {
+  if ((float)g.ctl->tile_max < g.tile_min_draws) return;  // no dense tile this pass
   static_assert(MODE != 1 || NT == NT, "shared-draw tiles run 8 warps (f1_accumulate)");
   extern __shared__ __align__(16) unsigned char tsm[];
   __shared__ unsigned lcnt[MAX_LEVELS], loff[MAX_LEVELS + 1], lfill[MAX_LEVELS];
@@ -597,6 +598,7 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
   // DB: each group double-buffers its query rows -- the next tile's copy runs during this
   // tile's draws (2 NG R query slots); QG: no query rows in shared memory
   constexpr int QB = QG ? 0 : (DB ? 2 : 1);
+  if ((float)g.ctl->tile_max < fmaxf(g.tile_min_draws, g.tile_lo)) return;  // no tile of this launch's range
   constexpr int GT = NTT / NG;  // threads per group (whole warps)
   static_assert(GT % 32 == 0, "groups of whole warps");
   extern __shared__ __align__(16) unsigned char tsm[];
@@ -1084,6 +1086,7 @@ struct ZJob {
 };
 
 __global__ void __launch_bounds__(TZ_NT, 1) k_advance_tiles_z(Geom g) {
+  if ((float)g.ctl->tile_max < fmaxf(g.tile_z_draws, g.tile_min_draws)) return;  // no z tile this pass
   extern __shared__ __align__(16) unsigned char tsm[];
   __shared__ __align__(8) uint64_t bar_zf[2], bar_ze[2], bar_q[2], bar_x;
   __shared__ uint32_t colmask[TZ_CM];

@@ -76,6 +76,8 @@ struct RoundCtl {
   unsigned int round;                     // rounds evaluated
   unsigned int evaluated;                 // queries the next rank split looks at
   unsigned long long qrounds, brounds;    // sums of evaluated / blocked queries
+  unsigned int tile_max;                  // this pass: the largest tilework (k_filter), so the
+                                          // tile kernels without a tile in their range exit at once
 };
 
 // One arm as exchanged between point shards: its composite key
