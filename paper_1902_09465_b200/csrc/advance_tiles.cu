@@ -762,8 +762,10 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
                 "l"(g.Q + (size_t)(rq + row) * pitch), "r"((uint32_t)pitch), "r"(bar)
                 : "memory");
       };
+      // single-buffered: the tile's query rows were issued right after the previous
+      // tile's last barrier (below) unless this is the group's first tile of the column
       if (!QG && gtid == 0) {
-        if (!DB || first) issue_rows(tr, sel);
+        if (first) issue_rows(tr, sel);
         if (DB && trn < rows) issue_rows(trn, sel ^ 1);
       }
       const uint32_t qs = qs0 + (uint32_t)(sel * R) * stride;
@@ -989,6 +991,9 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
         }
       }
       gsync();
+      // the slot is free (every read of this tile's query rows is behind the barrier):
+      // the next tile's copy starts now, ahead of the commit and the next bookkeeping
+      if (!QG && !DB && gtid == 0 && trn < rows) issue_rows(trn, sel);
       if (act4) {  // commit: S += the level's sum, T -> 2T (the thread's own 4 arms)
         int4 o = S4;
         uint32_t l4 = L4;
