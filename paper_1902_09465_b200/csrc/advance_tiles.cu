@@ -393,12 +393,16 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Geom g) {
     // ADV_TP / nb whole pairs per pass.  nb > ADV_TP: tpp lanes per pair (consecutive
     // lanes), each running ADV_TP independent Philox blocks at a time, then a shuffle
     // reduce inside the lane group; every pair's sum is written by one thread.
-    unsigned lmask = 0;  // levels present in the tile
-    for (int c = 0; c < MAX_LEVELS; ++c) lmask |= (lcnt[c] != 0u) << c;
-    if (tid == 0) {
-      unsigned long long dr = 0;
-      for (int c = 0; c < MAX_LEVELS; ++c) dr += (unsigned long long)lcnt[c] << c;
-      s_draws += dr;
+    // levels present in the tile (one load per lane + a ballot, in every warp) and the
+    // tile's pair draws (warp 0 reduces them; tid 0 adds them up)
+    static_assert(MAX_LEVELS == 32, "one level per lane");
+    const unsigned lv_l = lcnt[lane_id()];
+    unsigned lmask = __ballot_sync(FULL, lv_l != 0u);
+    if (tid < 32) {
+      unsigned long long dr = (unsigned long long)lv_l << lane_id();
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) dr += __shfl_xor_sync(FULL, dr, o);
+      if (tid == 0) s_draws += dr;
     }
     if (f1) {
       // shared draws: per level, the column's draw list (cached across the column's
