@@ -253,6 +253,7 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Geom g) {
   int gen_tp = -1, gen_c = -1;  // shared draws: the column / level whose draw list is in dbuf
   __shared__ unsigned long long s_blocks, s_draws;  // Philox blocks and pair draws (statistics)
   if (tid == 0) s_blocks = s_draws = 0;
+  if (tid < MAX_LEVELS) lcnt[tid] = 0;  // (the chunk loop's first barrier orders it)
   for (long long c0 = t0; c0 < t1; c0 += NT) {
     __syncthreads();  // dlist of the previous chunk is consumed
     {
@@ -281,7 +282,8 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Geom g) {
     constexpr bool f1 = MODE == 1;  // query-independent draws with R = 32 (host-selected instantiation)
     constexpr bool wor = MODE == 2;
     __syncthreads();  // the previous tile's shared memory is no longer in use
-    if (tid < MAX_LEVELS) lcnt[tid] = 0;
+    // (lcnt was cleared after the previous tile's last read of it, before this barrier:
+    // clearing it here would race with the level histogram of the other warps)
 
     // stage the rows.  Bulk TMA copies (one cp.async.bulk per row, issued by thread 0,
     // completion counted in bytes on an mbarrier) unless g.tile_tma == 0; otherwise
@@ -398,11 +400,17 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Geom g) {
     static_assert(MAX_LEVELS == 32, "one level per lane");
     const unsigned lv_l = lcnt[lane_id()];
     unsigned lmask = __ballot_sync(FULL, lv_l != 0u);
+    unsigned long long tile_bl = 0;  // the tile's Philox blocks (tid 0)
     if (tid < 32) {
       unsigned long long dr = (unsigned long long)lv_l << lane_id();
+      unsigned long long bl = (unsigned long long)lv_l << (lane_id() < 2 ? 0 : lane_id() - 2);
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) dr += __shfl_xor_sync(FULL, dr, o);
+      for (int o = 16; o > 0; o >>= 1) {
+        dr += __shfl_xor_sync(FULL, dr, o);
+        bl += __shfl_xor_sync(FULL, bl, o);
+      }
       if (tid == 0) s_draws += dr;
+      tile_bl = bl;
     }
     if (f1) {
       // shared draws: per level, the column's draw list (cached across the column's
@@ -436,9 +444,7 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Geom g) {
       }
       lmask = 0;  // done: skip the per-pair Philox path below
     } else if (tid == 0) {
-      unsigned long long b = 0;
-      for (int c = 0; c < MAX_LEVELS; ++c) b += (unsigned long long)lcnt[c] << (c < 2 ? 0 : c - 2);
-      s_blocks += b;
+      s_blocks += tile_bl;
     }
     for (; lmask; lmask &= lmask - 1) {
       const int c = __ffs(lmask) - 1;
@@ -524,6 +530,7 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Geom g) {
       }
     }
     __syncthreads();
+    if (tid < MAX_LEVELS) lcnt[tid] = 0;  // for the next tile (every read of it is done)
     // commit: S += the level's sum, T -> 2T (the thread's own 4 arms)
     if (act4) {
       int4 o = S4;
