@@ -609,7 +609,8 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
   // DB: each group double-buffers its query rows -- the next tile's copy runs during this
   // tile's draws (2 NG R query slots); QG: no query rows in shared memory
   constexpr int QB = QG ? 0 : (DB ? 2 : 1);
-  if ((float)g.ctl->tile_max < fmaxf(g.tile_min_draws, g.tile_lo)) return;  // no tile of this launch's range
+  // no dense tile of this launch's range [lo, hi) in this pass
+  if ((float)g.ctl->tile_max < fmaxf(g.tile_min_draws, g.tile_lo) || (float)g.ctl->tile_min >= g.tile_hi) return;
   constexpr int GT = NTT / NG;  // threads per group (whole warps)
   static_assert(GT % 32 == 0, "groups of whole warps");
   extern __shared__ __align__(16) unsigned char tsm[];

@@ -408,6 +408,7 @@ cudaError_t launch_round_pass(const Geom &g, int num_sms, cudaStream_t st, Timer
   cudaError_t e = cudaSuccess;
   if (g.level_mma) e = cudaMemsetAsync(g.lvcnt, 0, lvcnt_bytes(g.q, g.npad), st);
   if (e == cudaSuccess && g.tile_on) e = cudaMemsetAsync(&g.ctl->tile_max, 0, sizeof(unsigned int), st);
+  if (e == cudaSuccess && g.tile_on) e = cudaMemsetAsync(&g.ctl->tile_min, 0xFF, sizeof(unsigned int), st);
   if (e == cudaSuccess) e = launch_filter(g, st);
   timer(1);
   if (e == cudaSuccess) e = launch_compact(g, st);

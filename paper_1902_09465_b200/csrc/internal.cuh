@@ -78,6 +78,7 @@ struct RoundCtl {
   unsigned long long qrounds, brounds;    // sums of evaluated / blocked queries
   unsigned int tile_max;                  // this pass: the largest tilework (k_filter), so the
                                           // tile kernels without a tile in their range exit at once
+  unsigned int tile_min;                  // this pass: the smallest tilework of a dense tile
 };
 
 // One arm as exchanged between point shards: its composite key

@@ -456,18 +456,21 @@ __global__ void __launch_bounds__(FIL_NT) k_filter(Geom g) {
         atomicAdd(&g.lvcnt[((size_t)(q0 >> 7) * g.lv_cols + lc) * MAX_LEVELS + t % MAX_LEVELS], lvc[t]);
     }
   // every tile of this CTA, including those of finished queries (count 0)
-  uint32_t tmax = 0;
+  uint32_t tmax = 0, tmin = 0xFFFFFFFFu;
   for (int t = threadIdx.x; t < ntc; t += FIL_NT) {
     const int tr = (q0 >> g.tile_lr) + t / tcols;
     const int tc = ((blockIdx.x * FIL_NT * 4) >> g.tile_lp) + t % tcols;
     if ((tr << g.tile_lr) < g.q && tc < g.tile_cols) {
       g.tilework[(size_t)tr * g.tile_cols + tc] = tcnt[t];
       tmax = max(tmax, tcnt[t]);
+      if ((float)tcnt[t] >= g.tile_min_draws) tmin = min(tmin, tcnt[t]);
     }
   }
   if (g.tile_on) {
     tmax = __reduce_max_sync(FULL, tmax);
+    tmin = __reduce_min_sync(FULL, tmin);
     if (lane == 0 && tmax) atomicMax(&g.ctl->tile_max, tmax);
+    if (lane == 0 && tmin != 0xFFFFFFFFu) atomicMin(&g.ctl->tile_min, tmin);
   }
 }
 
