@@ -677,6 +677,11 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
   };
   const int c0 = (int)((long long)blockIdx.x * cols / gridDim.x), c1 = (int)((long long)(blockIdx.x + 1) * cols / gridDim.x);
   unsigned long long my_dr = 0, my_bl = 0;  // this group's draws / Philox blocks (gtid 0)
+  // rows1 <= NTT (C3: 256): thread tr holds tile row tr's tilework of the NEXT column in a
+  // register, loaded while the current column is processed (the strided reads of a
+  // column's tilework cost an L2 round trip at every column start otherwise)
+  const bool row_per_thread = rows1 <= NTT && rows1 <= CM_WORDS * 32;
+  uint32_t tw_next = (row_per_thread && tid < rows1 && c0 < c1) ? g.tilework[(size_t)tid * g.tile_cols + c0] : 0u;
   for (int tp = c0; tp < c1; ++tp) {
     // the column's dense query tiles as a bit mask, read once (all groups are done with
     // the previous column); a column without one is skipped
@@ -684,13 +689,29 @@ __global__ void __launch_bounds__(NTT) k_advance_tiles_grp(Geom g) {
     __syncthreads();  // every group has left the previous column (its mask reads included)
     for (int w = tid; w < CM_WORDS && w * 32 < rows1; w += NTT) colmask[w] = 0u;
     __syncthreads();
-    for (int tr = tid; tr < rows1; tr += NTT) {
-      const bool dn = grp_dense(g, (float)g.tilework[(size_t)tr * g.tile_cols + tp], dthr);
-      mine |= dn;
-      if (dn && tr < CM_WORDS * 32) atomicOr(&colmask[tr >> 5], 1u << (tr & 31));
+    if (row_per_thread) {
+      const uint32_t tw = tw_next;
+      if (tid < rows1 && tp + 1 < c1) tw_next = g.tilework[(size_t)tid * g.tile_cols + tp + 1];
+      if (tid < rows1 && grp_dense(g, (float)tw, dthr)) {
+        mine = true;
+        atomicOr(&colmask[tid >> 5], 1u << (tid & 31));
+      }
+    } else {
+      for (int tr = tid; tr < rows1; tr += NTT) {
+        const bool dn = grp_dense(g, (float)g.tilework[(size_t)tr * g.tile_cols + tp], dthr);
+        mine |= dn;
+        if (dn && tr < CM_WORDS * 32) atomicOr(&colmask[tr >> 5], 1u << (tr & 31));
+      }
     }
     if (!__syncthreads_or(mine)) continue;
     const int p0 = tp << g.tile_lp;
+    if (tid == 0 && tp + 1 < c1) {  // the next column's point rows: into L2 now (HBM -> L2)
+      for (int row = 0; row < P; ++row)
+        if (p0 + P + row < g.n)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(g.X + (size_t)(p0 + P + row) * pitch),
+                       "r"((uint32_t)pitch)
+                       : "memory");
+    }
     if (tid == 0) {  // the column's point rows: bulk TMA copies
       uint32_t bytes = 0;
       for (int row = 0; row < P; ++row) bytes += p0 + row < g.n ? (uint32_t)pitch : 0u;
