@@ -505,6 +505,35 @@ __global__ void __launch_bounds__(NT) k_advance_tiles(Geom g) {
         __syncthreads();
         const unsigned lg = (unsigned)(lb - 2);  // log2 groups of ADV_TP blocks per pair
         const unsigned total = m << lg;
+        if (!wor) {
+          // a CONTIGUOUS run of items per thread: the pair's constants (row addresses,
+          // Philox round-0/1 products) and its shared atomic once per run of one pair
+          const unsigned per = (total + NT - 1) / NT;
+          const unsigned it1 = min(total, (unsigned)tid * per + per);
+          int pe = -1;
+          uint32_t xa = 0, qa = 0, sum = 0;
+          PhiloxPair pc{};
+          for (unsigned it = (unsigned)tid * per; it < it1; ++it) {
+            const unsigned li = it >> lg, b0 = (it & ((1u << lg) - 1u)) * ADV_TP;
+            if (b0 == 0 || pe < 0) {  // a new pair
+              if (pe >= 0) atomicAdd(reinterpret_cast<uint32_t *>(acc + pe), sum);
+              sum = 0;
+              pe = (int)L[li];
+              xa = xs + ((uint32_t)(pe & (P - 1)) << sl);
+              qa = rows_s + ((uint32_t)(pe >> g.tile_lp) << sl);
+              const uint32_t gi = (uint32_t)(p0 + (pe & (P - 1))) + g.id_offset;
+              const uint32_t gq = rng_qi(g, (uint32_t)(r0 + (pe >> g.tile_lp)));
+              pc = philox_pair(gi, gq, g.rk0);
+            }
+            uint4 w[ADV_TP];
+#pragma unroll
+            for (int k = 0; k < ADV_TP; ++k) w[k] = philox_from_pair(b0 + k, lv, pc, g.rk0, g.rk1);
+#pragma unroll
+            for (int k = 0; k < ADV_TP; ++k) sum = sq_diff4(xa, qa, w[k], d, sum);
+          }
+          if (pe >= 0) atomicAdd(reinterpret_cast<uint32_t *>(acc + pe), sum);
+          continue;  // the next level
+        }
         for (unsigned it = tid; it < total; it += NT) {
           const unsigned li = it >> lg, b0 = (it & ((1u << lg) - 1u)) * ADV_TP;
           const int pe = (int)L[li];
